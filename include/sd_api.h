@@ -1,0 +1,168 @@
+/* sd_api.h — C ABI of the SynerDiff B200 hot path (libsynerdiff.so).
+ *
+ * Paper: "SynerDiff: Synergetic Continuous Batching for Fast and Parallel Diffusion Model
+ * Inference" (arXiv 2605.08835, /root/reference/PAPER.md, cited "P:<line>"). Blueprint:
+ * SURVEY.md §8(b). Readings of the paper the ABI depends on: SURVEY.md §8(c) R1-R32, DESIGN.md.
+ *
+ * Conventions
+ *  - Every call returns sd_status (int32). SD_OK = 0, errors are negative. Nothing throws or
+ *    aborts across the ABI. SD_E_INVAL is returned by argument validation before anything is
+ *    enqueued and leaves all state unchanged. A CUDA error puts the engine into a sticky FAILED
+ *    state: every later call on it returns SD_E_STATE. sd_last_error() gives a per-thread
+ *    message for the last non-OK status.
+ *  - Ownership: the caller owns every buffer it passes; the library never frees caller memory.
+ *    The engine owns its weights, workspaces, caches, decode states and completion images until
+ *    sd_engine_destroy() / sd_release().
+ *  - Device pointers are CUDA global-memory pointers on the engine's device. `stream` arguments
+ *    are cudaStream_t passed as void* (NULL = legacy default stream). Data-plane calls are
+ *    asynchronous on that stream unless stated otherwise.
+ *  - Layouts: latents are fp32 [4][h][w] (NCHW, one request), images fp32 [3][8h][8w],
+ *    text embeddings fp32 [len][dim] row-major.
+ */
+#ifndef SD_API_H
+#define SD_API_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t sd_status;
+enum {
+  SD_OK = 0,
+  SD_E_INVAL = -1,  /* invalid argument (validated before any work is enqueued)            */
+  SD_E_NOMEM = -2,  /* device or host allocation failed                                      */
+  SD_E_CUDA = -3,   /* CUDA runtime error (engine becomes FAILED)                            */
+  SD_E_AGAIN = -4,  /* resource temporarily full (submit queue)                              */
+  SD_E_STATE = -5,  /* call not valid in the current state (FAILED engine, out-of-order)     */
+  SD_E_NOTSUP = -6  /* configuration not supported by this build                            */
+};
+
+enum { SD_MODEL_TINY = 0, SD_MODEL_SD15 = 1 };          /* R1: diffusers SD-1.5 shapes; tiny = CFG#1 */
+enum { SD_PREC_BF16 = 0 };                               /* bf16 storage, fp32 accumulate (R19)       */
+enum { SD_SAMPLER_DDIM = 0, SD_SAMPLER_EULER = 1 };      /* R4 / R5                                  */
+
+typedef struct sd_engine sd_engine;
+typedef struct sd_decode sd_decode;
+typedef struct sd_table sd_table;
+typedef struct sd_controller sd_controller;
+
+/* ---- engine ---------------------------------------------------------------------------------
+ * sd_engine_create: builds the UNet + VAE for `model` on `cuda_device`, allocates workspaces for
+ * up to 2*b_max UNet rows at up to max_latent_hw x max_latent_hw, and initialises every weight
+ * ON THE DEVICE from the counter-based generator keyed by (weight_seed, parameter name) (R20,
+ * synth/__init__.py documents the generator). */
+typedef struct {
+  int32_t model;          /* SD_MODEL_*                                        */
+  int32_t precision;      /* SD_PREC_BF16                                      */
+  int32_t sampler;        /* SD_SAMPLER_*                                      */
+  int32_t max_latent_hw;  /* e.g. 64 for 512x512 images                        */
+  int32_t b_max;          /* max requests per UNet call (paper: BS = 8) */
+  int32_t c_max;          /* max VAE chunks                            */
+  uint64_t weight_seed;
+} sd_engine_config;
+
+sd_status sd_engine_create(const sd_engine_config* cfg, int32_t cuda_device, sd_engine** out);
+sd_status sd_engine_destroy(sd_engine* e);
+const char* sd_last_error(void);
+const char* sd_status_str(sd_status s);
+/* Number of kernels this engine launched since creation (for the bench's gpu_launches claim). */
+sd_status sd_engine_launch_count(sd_engine* e, int64_t* out);
+
+/* Device timing per kernel class, CUDA events on the launching stream around every launch
+ * (used by bench.py for the live roofline). enable != 0 starts recording (and clears old records).
+ * Classes: 0 conv3x3 implicit GEMM, 1 dense GEMM, 2 attention, 3 GroupNorm, 4 LayerNorm.
+ * work_out = algorithmic FLOPs (classes 0-2) or bytes (3-4) of the recorded launches. Reading
+ * synchronises on the recorded events. */
+sd_status sd_engine_profile(sd_engine* e, int32_t enable);
+sd_status sd_engine_profile_read(sd_engine* e, int32_t cls, double* ms_out, int64_t* launches_out, double* work_out);
+
+/* ---- data plane: one step-level batched denoising iteration ---------
+ * sd_ctx_register: cache the cross-attention K/V of one prompt embedding (text_emb_dev: device
+ * fp32 [len][dim], len = 77 / dim = 768 for SD-1.5). Text K/V do not depend on x or t, so they
+ * are computed once at admission. Returns a slot id; slot 0 is the engine-global unconditional
+ * embedding, registered with sd_ctx_set_uncond. */
+sd_status sd_ctx_register(sd_engine* e, const float* text_emb_dev, int32_t len, int32_t dim, int32_t* slot_out,
+                          void* stream);
+sd_status sd_ctx_set_uncond(sd_engine* e, const float* text_emb_dev, int32_t len, int32_t dim, void* stream);
+sd_status sd_ctx_release(sd_engine* e, int32_t slot);
+
+/* One UNet step for n_req requests at one resolution (R22). Rows: one conditional row per
+ * request, plus one unconditional row for requests with has_uncond = 1 (Adaptive Skip-CFG,
+ * P:162; R3), ordered cond rows then uncond rows (R26). Then per request:
+ *   eps~ = has_uncond ? eps_u + g (eps_c - eps_u) : eps_c                  (R2, R3)
+ *   x    = DDIM / Euler update of x at step index step[r] of n_steps[r]     (R4, R5)
+ * latents[r] are updated in place. All host arrays are copied at call time. */
+typedef struct {
+  int32_t n_req, latent_h, latent_w;
+  float* const* latents;      /* [n_req] device ptrs, fp32 [4][h][w]                     */
+  const int32_t* step;        /* [n_req] s_r: steps already done (index of this step)    */
+  const int32_t* n_steps;     /* [n_req] n_r                                             */
+  const uint8_t* has_uncond;  /* [n_req] 1 = CFG row present, 0 = Skip-CFG this step     */
+  const float* guidance;      /* [n_req] g_r                                             */
+  const int32_t* ctx_slot;    /* [n_req] from sd_ctx_register                            */
+} sd_batch;
+sd_status sd_step_batch(sd_engine* e, const sd_batch* b, void* stream);
+
+/* Scheduler coefficients a request needs before its first step: x_T = init_sigma * z. */
+sd_status sd_sampler_init_sigma(sd_engine* e, int32_t n_steps, float* out);
+
+/* ---- chunked VAE decode (R7 "stage-synchronous halo tiles") -----------------------
+ * Chunk j of n_chunks runs the j-th contiguous range of the decode work list. Chunk 0 allocates
+ * *state (must be NULL), the last chunk writes image_dev (fp32 [3][8h][8w]) and frees *state
+ * (set to NULL). Chunks must be issued in order on the same stream, else SD_E_STATE.
+ * n_chunks == 1 is a whole-image decode. Any n_chunks gives the same image (I6). */
+sd_status sd_vae_decode_chunked(sd_engine* e, const float* latent_dev, int32_t h, int32_t w, int32_t n_chunks,
+                                int32_t chunk, sd_decode** state, float* image_dev, void* stream);
+
+/* ---- pure host control plane -------------------------------------------
+ * Latency table: CSV "c,m,n,k,tau_us,delta_us" (integers, µs; R11). */
+sd_status sd_table_load(const char* csv_path, sd_table** out);
+sd_status sd_table_from_arrays(int32_t n, const int32_t* c, const int32_t* m, const int32_t* nn, const int32_t* k,
+                               const int64_t* tau_us, const int64_t* delta_us, sd_table** out);
+sd_status sd_table_free(sd_table* t);
+
+/* Problem P (Eq. 3a-3f) for a window (M, N, K) at chunk granularity c. dp_mode 0 = exact
+ * (Pareto labels, R10), 1 = Alg. 1 verbatim. T_lim = floor((1+a_num/a_den) tau_ref)
+ * (R11, R13). Writes up to max_stages stages (m,n,k) into stages_out (3 ints each), the count
+ * into *n_stages, and the objective cost / total time (µs) into cost_out / time_out. N = 0 gives
+ * the single pure-UNet stage (M,0,0) (R8). */
+sd_status sd_plan(const sd_table* t, int32_t M, int32_t N, int32_t K, int32_t c, int32_t a_num, int32_t a_den,
+                  int32_t dp_mode, int32_t* stages_out, int32_t max_stages, int32_t* n_stages, int64_t* cost_out,
+                  int64_t* time_out);
+
+/* Feedback controller (R15). */
+typedef struct {
+  int32_t c_star, c_max, window, hysteresis;
+  int32_t up_num, up_den;      /* theta_up   = up_num/up_den tasks per second   (default 1/2)  */
+  int32_t down_num, down_den;  /* theta_down = down_num/down_den              (default -1/5) */
+} sd_controller_config;
+typedef struct {
+  int32_t level;     /* 0 = no skip, 1 = s_min 0.7 n, 2 = s_min 0.5 n (R6) */
+  int32_t c;         /* VAE chunk count                                   */
+  int32_t changed;
+} sd_directive;
+sd_status sd_controller_create(const sd_controller_config* cfg, sd_controller** out);
+sd_status sd_controller_decide(sd_controller* c, int64_t now_us, int32_t global_queue, sd_directive* out);
+sd_status sd_controller_free(sd_controller* c);
+
+/* Min-max partition of the ordered VAE work list into c chunks (R7): boundaries[0..c]. */
+sd_status sd_chunk_ranges(const int64_t* costs, int32_t n_items, int32_t c, int32_t* boundaries_out);
+
+/* ---- test-only exports (same library): single kernels on caller-owned device buffers --------- */
+/* D[M][N] = A[M][K] · B[N][K]^T + bias[N] (bf16 in, fp32 accumulate, bf16 or fp32 out). */
+sd_status sd_debug_gemm(const void* A, const void* B, const float* bias, void* D, int32_t M, int32_t N, int32_t K,
+                        int32_t out_f32, int32_t act, void* stream);
+/* 3x3 / stride 1 / pad 1 conv over NHWC bf16 x [nb][h][w][cin] (+ optional second source x2 with
+ * cin2 channels, concatenated after x), weights bf16 [cout][9][cin] (and [cout][9][cin2]),
+ * bias fp32, optional temb fp32 [nb][cout], optional residual bf16 [nb][h][w][cout]. */
+sd_status sd_debug_conv3x3(const void* x, int32_t cin, const void* x2, int32_t cin2, const void* w, const void* w2,
+                           const float* bias, const float* temb, const void* res, void* y, int32_t nb, int32_t h,
+                           int32_t wd, int32_t cout, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SD_API_H */

@@ -1,0 +1,134 @@
+"""Thin ctypes binding of include/sd_api.h (argument marshalling only — every step of the hot path
+runs in libsynerdiff.so's CUDA kernels; there is no Python or CPU fallback).
+
+Function names mirror the C ABI. Pointers are passed as ints (e.g. torch.Tensor.data_ptr()),
+streams as ints (torch.cuda.Stream.cuda_stream) or None.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from .build import LIB
+
+_lib = None
+
+SD_OK, SD_E_INVAL, SD_E_NOMEM, SD_E_CUDA, SD_E_AGAIN, SD_E_STATE, SD_E_NOTSUP = 0, -1, -2, -3, -4, -5, -6
+SD_MODEL_TINY, SD_MODEL_SD15 = 0, 1
+SD_SAMPLER_DDIM, SD_SAMPLER_EULER = 0, 1
+ACT_NONE, ACT_SILU, ACT_GEGLU = 0, 1, 2
+
+
+class SDError(RuntimeError):
+    def __init__(self, fn, status, msg):
+        super().__init__(f"{fn} -> {status_str(status)} ({status}): {msg}")
+        self.status = status
+
+
+class EngineConfig(C.Structure):
+    _fields_ = [("model", C.c_int32), ("precision", C.c_int32), ("sampler", C.c_int32),
+                ("max_latent_hw", C.c_int32), ("b_max", C.c_int32), ("c_max", C.c_int32),
+                ("weight_seed", C.c_uint64)]
+
+
+class Batch(C.Structure):
+    _fields_ = [("n_req", C.c_int32), ("latent_h", C.c_int32), ("latent_w", C.c_int32),
+                ("latents", C.POINTER(C.c_void_p)), ("step", C.POINTER(C.c_int32)),
+                ("n_steps", C.POINTER(C.c_int32)), ("has_uncond", C.POINTER(C.c_uint8)),
+                ("guidance", C.POINTER(C.c_float)), ("ctx_slot", C.POINTER(C.c_int32))]
+
+
+class ControllerConfig(C.Structure):
+    _fields_ = [("c_star", C.c_int32), ("c_max", C.c_int32), ("window", C.c_int32), ("hysteresis", C.c_int32),
+                ("up_num", C.c_int32), ("up_den", C.c_int32), ("down_num", C.c_int32), ("down_den", C.c_int32)]
+
+
+class Directive(C.Structure):
+    _fields_ = [("level", C.c_int32), ("c", C.c_int32), ("changed", C.c_int32)]
+
+
+P = C.c_void_p
+I32 = C.c_int32
+I64 = C.c_int64
+PI32 = C.POINTER(C.c_int32)
+PI64 = C.POINTER(C.c_int64)
+
+# name -> argtypes (restype is sd_status unless listed in _RESTYPE)
+SIGNATURES = {
+    "sd_engine_create": [C.POINTER(EngineConfig), I32, C.POINTER(P)],
+    "sd_engine_destroy": [P],
+    "sd_last_error": [],
+    "sd_status_str": [I32],
+    "sd_engine_launch_count": [P, PI64],
+    "sd_engine_profile": [P, I32],
+    "sd_engine_profile_read": [P, I32, C.POINTER(C.c_double), PI64, C.POINTER(C.c_double)],
+    "sd_ctx_register": [P, P, I32, I32, PI32, P],
+    "sd_ctx_set_uncond": [P, P, I32, I32, P],
+    "sd_ctx_release": [P, I32],
+    "sd_step_batch": [P, C.POINTER(Batch), P],
+    "sd_sampler_init_sigma": [P, I32, C.POINTER(C.c_float)],
+    "sd_vae_decode_chunked": [P, P, I32, I32, I32, I32, C.POINTER(P), P, P],
+    "sd_table_load": [C.c_char_p, C.POINTER(P)],
+    "sd_table_from_arrays": [I32, PI32, PI32, PI32, PI32, PI64, PI64, C.POINTER(P)],
+    "sd_table_free": [P],
+    "sd_plan": [P, I32, I32, I32, I32, I32, I32, I32, PI32, I32, PI32, PI64, PI64],
+    "sd_controller_create": [C.POINTER(ControllerConfig), C.POINTER(P)],
+    "sd_controller_decide": [P, I64, I32, C.POINTER(Directive)],
+    "sd_controller_free": [P],
+    "sd_chunk_ranges": [PI64, I32, I32, PI32],
+    "sd_debug_gemm": [P, P, P, P, I32, I32, I32, I32, I32, P],
+    "sd_debug_conv3x3": [P, I32, P, I32, P, P, P, P, P, P, I32, I32, I32, I32, P],
+}
+_RESTYPE = {"sd_last_error": C.c_char_p, "sd_status_str": C.c_char_p}
+
+
+def lib():
+    """Load libsynerdiff.so. Fails loudly if it is missing (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB):
+            raise ImportError(f"{LIB} not built: run `python -m paper_2605_08835_b200.build` "
+                              "(or __graft_entry__.build()) — there is no CPU fallback")
+        L = C.CDLL(LIB)
+        for name, args in SIGNATURES.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = _RESTYPE.get(name, C.c_int32)
+        _lib = L
+    return _lib
+
+
+def status_str(s):
+    return lib().sd_status_str(s).decode()
+
+
+def last_error():
+    return lib().sd_last_error().decode()
+
+
+def check(fn, status):
+    if status != SD_OK:
+        raise SDError(fn, status, last_error())
+    return status
+
+
+def call(name, *args):
+    return check(name, getattr(lib(), name)(*args))
+
+
+def _p(x):
+    """int pointer / tensor / None → c_void_p."""
+    if x is None:
+        return None
+    if hasattr(x, "data_ptr"):
+        return C.c_void_p(x.data_ptr())
+    return C.c_void_p(int(x))
+
+
+def debug_gemm(A, B, bias, D, M, N, K, out_f32=0, act=ACT_NONE, stream=None):
+    call("sd_debug_gemm", _p(A), _p(B), _p(bias), _p(D), M, N, K, out_f32, act, _p(stream))
+
+
+def debug_conv3x3(x, cin, x2, cin2, w, w2, bias, temb, res, y, nb, h, wd, cout, stream=None):
+    call("sd_debug_conv3x3", _p(x), cin, _p(x2), cin2, _p(w), _p(w2), _p(bias), _p(temb), _p(res), _p(y),
+         nb, h, wd, cout, _p(stream))

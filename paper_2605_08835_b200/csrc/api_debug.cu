@@ -1,0 +1,78 @@
+// Test-only C-ABI exports: single kernels on caller-owned device buffers (sd_api.h, last section).
+#include "api_common.h"
+#include "common.cuh"
+#include "kernels.h"
+
+namespace sd {
+std::atomic<long long> g_launches{0};
+static thread_local std::string g_err;
+void set_error(const std::string& s) { g_err = s; }
+}  // namespace sd
+
+extern "C" const char* sd_last_error(void) { return sd::g_err.c_str(); }
+
+extern "C" const char* sd_status_str(sd_status s) {
+  switch (s) {
+    case SD_OK: return "SD_OK";
+    case SD_E_INVAL: return "SD_E_INVAL";
+    case SD_E_NOMEM: return "SD_E_NOMEM";
+    case SD_E_CUDA: return "SD_E_CUDA";
+    case SD_E_AGAIN: return "SD_E_AGAIN";
+    case SD_E_STATE: return "SD_E_STATE";
+    case SD_E_NOTSUP: return "SD_E_NOTSUP";
+  }
+  return "SD_E_UNKNOWN";
+}
+
+extern "C" sd_status sd_debug_gemm(const void* A, const void* B, const float* bias, void* D, int32_t M, int32_t N,
+                                   int32_t K, int32_t out_f32, int32_t act, void* stream) {
+  SD_REQUIRE(A && B && D && M > 0 && N > 0 && K > 0, "sd_debug_gemm: bad arguments");
+  SD_REQUIRE(K % 8 == 0, "sd_debug_gemm: K must be a multiple of 8");
+  SD_API_BEGIN
+  sd::GemmDesc d;
+  d.mode = sd::GEMM_DENSE;
+  d.A = static_cast<const bf16*>(A);
+  d.M = M;
+  d.K = K;
+  d.lda = K;
+  d.Bw[0] = static_cast<const bf16*>(B);
+  d.N = N;
+  d.ldb = K;
+  d.out = D;
+  d.ldo = act == sd::ACT_GEGLU ? N / 2 : N;
+  d.out_f32 = out_f32;
+  d.bias = bias;
+  d.act = act;
+  sd::gemm(d, static_cast<cudaStream_t>(stream));
+  SD_API_END
+}
+
+extern "C" sd_status sd_debug_conv3x3(const void* x, int32_t cin, const void* x2, int32_t cin2, const void* w,
+                                      const void* w2, const float* bias, const float* temb, const void* res, void* y,
+                                      int32_t nb, int32_t h, int32_t wd, int32_t cout, void* stream) {
+  SD_REQUIRE(x && w && y && cin > 0 && cout > 0 && nb > 0 && h > 0 && wd > 0, "sd_debug_conv3x3: bad arguments");
+  SD_REQUIRE(!x2 || (w2 && cin2 > 0), "sd_debug_conv3x3: second source needs weights");
+  SD_API_BEGIN
+  sd::GemmDesc d;
+  d.mode = sd::GEMM_CONV3;
+  d.nsrc = x2 ? 2 : 1;
+  d.xs[0] = static_cast<const bf16*>(x);
+  d.cs[0] = cin;
+  d.xs[1] = static_cast<const bf16*>(x2);
+  d.cs[1] = cin2;
+  d.Bw[0] = static_cast<const bf16*>(w);
+  d.Bw[1] = static_cast<const bf16*>(w2);
+  d.B = nb;
+  d.H = h;
+  d.W = wd;
+  d.N = cout;
+  d.out = y;
+  d.ldo = cout;
+  d.bias = bias;
+  d.temb = temb;
+  d.ld_temb = cout;
+  d.res = static_cast<const bf16*>(res);
+  d.ldr = cout;
+  sd::gemm(d, static_cast<cudaStream_t>(stream));
+  SD_API_END
+}

@@ -1,0 +1,169 @@
+// C ABI of the engine (include/sd_api.h: engine, data plane, chunked VAE decode).
+#include "api_common.h"
+#include "engine.h"
+
+using namespace sd;
+
+struct sd_engine {
+  Engine e;
+};
+struct sd_decode {};  // opaque; the pointer is really a sd::DecodeState*
+
+namespace sd {
+float init_sigma(int sampler, int n);
+}
+
+#define ENGINE_GUARD(eng)                                               \
+  SD_REQUIRE(eng, "null engine");                                       \
+  if ((eng)->e.failed) {                                                \
+    ::sd::set_error("engine is FAILED after an earlier CUDA error");    \
+    return SD_E_STATE;                                                  \
+  }
+
+// run body; a CUDA error makes the engine FAILED (sticky)
+#define ENGINE_BODY(eng, body)                      \
+  try {                                             \
+    SD_CUDA(cudaSetDevice((eng)->e.device));        \
+    body;                                           \
+  } catch (const ::sd::CudaError& ex) {             \
+    (eng)->e.failed = true;                         \
+    ::sd::set_error(ex.what());                     \
+    return SD_E_CUDA;                               \
+  } catch (const std::bad_alloc&) {                 \
+    ::sd::set_error("out of memory");               \
+    return SD_E_NOMEM;                              \
+  } catch (const std::logic_error& ex) {            \
+    ::sd::set_error(ex.what());                     \
+    return SD_E_STATE;                              \
+  } catch (const std::exception& ex) {              \
+    ::sd::set_error(ex.what());                     \
+    return SD_E_INVAL;                              \
+  }                                                 \
+  return SD_OK;
+
+extern "C" sd_status sd_engine_create(const sd_engine_config* cfg, int32_t dev, sd_engine** out) {
+  SD_REQUIRE(cfg && out, "sd_engine_create: null argument");
+  SD_REQUIRE(cfg->model == SD_MODEL_TINY || cfg->model == SD_MODEL_SD15, "sd_engine_create: unknown model");
+  SD_REQUIRE(cfg->precision == SD_PREC_BF16, "sd_engine_create: only SD_PREC_BF16 is built");
+  SD_REQUIRE(cfg->sampler == SD_SAMPLER_DDIM || cfg->sampler == SD_SAMPLER_EULER, "sd_engine_create: sampler");
+  SD_REQUIRE(cfg->max_latent_hw >= 8 && cfg->max_latent_hw <= 256, "sd_engine_create: max_latent_hw");
+  SD_REQUIRE(cfg->b_max >= 1 && cfg->b_max <= 32, "sd_engine_create: b_max");
+  *out = nullptr;
+  auto* h = new sd_engine();
+  h->e.cfg = *cfg;
+  h->e.device = dev;
+  try {
+    build_engine(&h->e);
+  } catch (const CudaError& ex) {
+    set_error(ex.what());
+    delete h;
+    return SD_E_CUDA;
+  } catch (const std::bad_alloc&) {
+    set_error("out of memory building the engine");
+    delete h;
+    return SD_E_NOMEM;
+  } catch (const std::exception& ex) {
+    set_error(ex.what());
+    delete h;
+    return SD_E_INVAL;
+  }
+  *out = h;
+  return SD_OK;
+}
+
+extern "C" sd_status sd_engine_destroy(sd_engine* e) {
+  if (!e) return SD_OK;
+  cudaSetDevice(e->e.device);
+  cudaDeviceSynchronize();
+  delete e;
+  return SD_OK;
+}
+
+extern "C" sd_status sd_engine_launch_count(sd_engine* e, int64_t* out) {
+  SD_REQUIRE(e && out, "bad args");
+  *out = (int64_t)g_launches.load();
+  return SD_OK;
+}
+
+extern "C" sd_status sd_ctx_register(sd_engine* e, const float* emb, int32_t len, int32_t dim, int32_t* slot_out,
+                                     void* stream) {
+  ENGINE_GUARD(e);
+  SD_REQUIRE(emb && slot_out, "sd_ctx_register: null argument");
+  SD_REQUIRE(len == e->e.uc.ctx_len && dim == e->e.uc.ctx_dim, "sd_ctx_register: embedding shape");
+  ENGINE_BODY(e, { *slot_out = ctx_register(&e->e, emb, len, dim, -1, static_cast<cudaStream_t>(stream)); })
+}
+
+extern "C" sd_status sd_ctx_set_uncond(sd_engine* e, const float* emb, int32_t len, int32_t dim, void* stream) {
+  ENGINE_GUARD(e);
+  SD_REQUIRE(emb, "sd_ctx_set_uncond: null argument");
+  SD_REQUIRE(len == e->e.uc.ctx_len && dim == e->e.uc.ctx_dim, "sd_ctx_set_uncond: embedding shape");
+  ENGINE_BODY(e, { ctx_register(&e->e, emb, len, dim, 0, static_cast<cudaStream_t>(stream)); })
+}
+
+extern "C" sd_status sd_ctx_release(sd_engine* e, int32_t slot) {
+  ENGINE_GUARD(e);
+  SD_REQUIRE(slot >= 1 && slot < e->e.max_slots && e->e.slot_used[slot], "sd_ctx_release: bad slot");
+  std::lock_guard<std::mutex> g(e->e.mu);
+  e->e.slot_used[slot] = 0;
+  return SD_OK;
+}
+
+extern "C" sd_status sd_step_batch(sd_engine* e, const sd_batch* b, void* stream) {
+  ENGINE_GUARD(e);
+  SD_REQUIRE(b && b->n_req >= 1 && b->n_req <= e->e.cfg.b_max, "sd_step_batch: n_req out of range [1, b_max]");
+  SD_REQUIRE(b->latent_h >= 1 && b->latent_w >= 1 && b->latent_h <= e->e.cfg.max_latent_hw &&
+                 b->latent_w <= e->e.cfg.max_latent_hw,
+             "sd_step_batch: latent size");
+  const int L = (int)e->e.uc.block_out.size();
+  SD_REQUIRE(b->latent_h % (1 << (L - 1)) == 0 && b->latent_w % (1 << (L - 1)) == 0,
+             "sd_step_batch: latent size must be divisible by 2^(levels-1)");
+  SD_REQUIRE(b->latents && b->step && b->n_steps && b->has_uncond && b->guidance && b->ctx_slot,
+             "sd_step_batch: null array");
+  for (int r = 0; r < b->n_req; ++r) {
+    SD_REQUIRE(b->latents[r], "sd_step_batch: null latent");
+    SD_REQUIRE(b->n_steps[r] >= 1 && b->n_steps[r] <= 1000, "sd_step_batch: n_steps");
+    SD_REQUIRE(b->step[r] >= 0 && b->step[r] < b->n_steps[r], "sd_step_batch: step index");
+    SD_REQUIRE(b->ctx_slot[r] >= 0 && b->ctx_slot[r] < e->e.max_slots && e->e.slot_used[b->ctx_slot[r]],
+               "sd_step_batch: ctx slot not registered");
+  }
+  ENGINE_BODY(e, { step_batch(&e->e, b, static_cast<cudaStream_t>(stream)); })
+}
+
+extern "C" sd_status sd_sampler_init_sigma(sd_engine* e, int32_t n_steps, float* out) {
+  SD_REQUIRE(e && out && n_steps >= 1 && n_steps <= 1000, "sd_sampler_init_sigma: bad args");
+  *out = init_sigma(e->e.cfg.sampler, n_steps);
+  return SD_OK;
+}
+
+extern "C" sd_status sd_vae_decode_chunked(sd_engine* e, const float* z, int32_t h, int32_t w, int32_t n_chunks,
+                                           int32_t chunk, sd_decode** state, float* image, void* stream) {
+  ENGINE_GUARD(e);
+  SD_REQUIRE(z && state && image, "sd_vae_decode_chunked: null argument");
+  SD_REQUIRE(h >= 1 && w >= 1 && h <= e->e.cfg.max_latent_hw && w <= e->e.cfg.max_latent_hw,
+             "sd_vae_decode_chunked: latent size");
+  SD_REQUIRE(n_chunks >= 1 && n_chunks <= std::max(1, e->e.cfg.c_max) && chunk >= 0 && chunk < n_chunks,
+             "sd_vae_decode_chunked: chunk index");
+  ENGINE_BODY(e, {
+    DecodeState* s = reinterpret_cast<DecodeState*>(*state);
+    vae_decode_chunk(&e->e, z, h, w, n_chunks, chunk, &s, image, static_cast<cudaStream_t>(stream));
+    *state = reinterpret_cast<sd_decode*>(s);
+  })
+}
+
+extern "C" sd_status sd_engine_profile(sd_engine* e, int32_t enable) {
+  ENGINE_GUARD(e);
+  ENGINE_BODY(e, {
+    e->e.prof.reset();
+    e->e.prof.on = enable != 0;
+  })
+}
+
+extern "C" sd_status sd_engine_profile_read(sd_engine* e, int32_t cls, double* ms, int64_t* n, double* work) {
+  ENGINE_GUARD(e);
+  SD_REQUIRE(cls >= 0 && cls < PC_N && ms && n && work, "sd_engine_profile_read: bad args");
+  ENGINE_BODY(e, {
+    long long c = 0;
+    e->e.prof.read(cls, ms, &c, work);
+    *n = c;
+  })
+}

@@ -1,0 +1,814 @@
+// Engine: model definitions (diffusers SD-1.5 / tiny shapes, R1, App. C), on-device weight init,
+// text K/V cache, and the step-level batched UNet iteration behind sd_step_batch (SURVEY §8(a)
+// rows a4-a9). Every op is one of our sm_100a kernels; there is no library or CPU fallback.
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+
+#include "engine.h"
+
+namespace sd {
+
+// ---------------------------------------------------------------------------------------------
+// configs (must match oracle/configs.py by construction; checked end to end by the parity tests)
+// ---------------------------------------------------------------------------------------------
+UNetCfg unet_cfg(int model) {
+  UNetCfg c;
+  if (model == SD_MODEL_TINY) {
+    c.block_out = {32, 64};
+    c.attn = {1, 1};
+    c.layers = 1;
+    c.groups = 8;
+    c.heads = 2;
+    c.ctx_dim = 32;
+    c.ctx_len = 8;
+  } else {
+    c.block_out = {320, 640, 1280, 1280};
+    c.attn = {1, 1, 1, 0};
+    c.layers = 2;
+    c.groups = 32;
+    c.heads = 8;
+    c.ctx_dim = 768;
+    c.ctx_len = 77;
+  }
+  return c;
+}
+
+VAECfg vae_cfg(int model) {
+  VAECfg c;
+  if (model == SD_MODEL_TINY) {
+    c.block_out = {32, 64};
+    c.layers = 1;
+    c.groups = 8;
+  } else {
+    c.block_out = {128, 256, 512, 512};
+    c.layers = 2;
+    c.groups = 32;
+  }
+  c.sf = 0.18215f;
+  return c;
+}
+
+void Arena::init(size_t bytes) {
+  SD_CUDA(cudaMalloc(&base, bytes));
+  cap = bytes;
+  used = 0;
+}
+void Arena::release() {
+  if (base) cudaFree(base);
+  base = nullptr;
+  cap = used = 0;
+}
+void* Arena::alloc(size_t bytes) {
+  size_t off = (used + 255) & ~size_t(255);
+  if (off + bytes > cap) throw std::bad_alloc();
+  used = off + bytes;
+  return base + off;
+}
+
+// ---------------------------------------------------------------------------------------------
+// generator seeds (synth/__init__.py): tensor_seed = mix64(fnv1a64(name) ^ mix64(global_seed))
+// ---------------------------------------------------------------------------------------------
+static uint64_t mix64h(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+static uint64_t fnv1a64(const std::string& s) {
+  uint64_t h = 0xCBF29CE484222325ull;
+  for (unsigned char ch : s) {
+    h ^= ch;
+    h *= 0x100000001B3ull;
+  }
+  return h;
+}
+
+struct Builder {
+  Engine* e;
+  cudaStream_t st;
+  long n_params = 0;
+  template <class T>
+  T* alloc(long n) {
+    T* p = e->warena.get<T>((size_t)n);
+    return p;
+  }
+  // canonical tensor `name` of n elements → generated into dst (layout given)
+  void gen(const std::string& name, long n, int kind, long fan_in, int layout, void* d0, void* d1, bool bf,
+           int O = 0, int I = 0, int I1 = 0, int Ipad = 0, int F = 0) {
+    WeightInit w{};
+    w.tseed = mix64h(fnv1a64(name) ^ mix64h(e->cfg.weight_seed));
+    w.kind = kind;
+    w.bound = (float)(1.0 / sqrt((double)fan_in));
+    w.layout = layout;
+    w.n = n;
+    w.O = O;
+    w.I = I;
+    w.I1 = I1;
+    w.Ipad = Ipad;
+    w.F = F;
+    w.dst0 = d0;
+    w.dst1 = d1;
+    w.out_bf16 = bf ? 1 : 0;
+    init_weight(w, st);
+    n_params += n;
+  }
+  float* bias(const std::string& name, int n, long fan_in, float* dst = nullptr) {
+    if (!dst) dst = alloc<float>(n);
+    gen(name, n, WK_UNIFORM, fan_in, WL_PLAIN, dst, nullptr, false);
+    return dst;
+  }
+  void norm(const std::string& p, int c, float** g, float** b) {
+    *g = alloc<float>(c);
+    *b = alloc<float>(c);
+    gen(p + ".weight", c, WK_GAMMA, 1, WL_PLAIN, *g, nullptr, false);
+    gen(p + ".bias", c, WK_BETA, 1, WL_PLAIN, *b, nullptr, false);
+  }
+  // conv3x3 [O][I][3][3] → [O][9][Ipad] bf16
+  bf16* conv3(const std::string& p, int O, int I, int Ipad, float** b) {
+    bf16* w = alloc<bf16>((long)O * 9 * Ipad);
+    if (Ipad != I) SD_CUDA(cudaMemsetAsync(w, 0, (size_t)O * 9 * Ipad * 2, st));
+    gen(p + ".weight", (long)O * I * 9, WK_UNIFORM, (long)I * 9, WL_CONV3, w, nullptr, true, O, I, I, Ipad);
+    if (b) *b = bias(p + ".bias", O, (long)I * 9);
+    return w;
+  }
+  // linear / 1x1 conv [O][I] → bf16 (optionally into dst rows)
+  bf16* lin(const std::string& p, int O, int I, float** b, bf16* dst = nullptr, float* bdst = nullptr) {
+    bf16* w = dst ? dst : alloc<bf16>((long)O * I);
+    gen(p + ".weight", (long)O * I, WK_UNIFORM, I, WL_PLAIN, w, nullptr, true);
+    if (b) *b = bias(p + ".bias", O, I, bdst);
+    return w;
+  }
+};
+
+static void build_res(Builder& B, const std::string& p, int cin, int cout, int* temb_cursor, ResW* r, bool temb) {
+  r->cin = cin;
+  r->cout = cout;
+  B.norm(p + ".norm1", cin, &r->n1g, &r->n1b);
+  r->w1 = B.conv3(p + ".conv1", cout, cin, cin, &r->b1);
+  if (temb) {
+    const int T = B.e->uc.temb_dim();
+    r->temb_off = *temb_cursor;
+    B.lin(p + ".time_emb_proj", cout, T, nullptr, B.e->U.temb_all_w + (long)r->temb_off * T, nullptr);
+    B.bias(p + ".time_emb_proj.bias", cout, T, B.e->U.temb_all_b + r->temb_off);
+    *temb_cursor += cout;
+  }
+  B.norm(p + ".norm2", cout, &r->n2g, &r->n2b);
+  r->w2 = B.conv3(p + ".conv2", cout, cout, cout, &r->b2);
+  if (cin != cout) r->wsc = B.lin(p + ".conv_shortcut", cout, cin, &r->bsc);
+}
+
+static void build_tf(Builder& B, const std::string& p, int C, int* kv_cursor, TfW* t) {
+  Engine* e = B.e;
+  const int D = e->uc.ctx_dim;
+  t->C = C;
+  B.norm(p + ".norm", C, &t->gng, &t->gnb);
+  t->wpin = B.lin(p + ".proj_in", C, C, &t->bpin);
+  const std::string b = p + ".transformer_blocks.0";
+  B.norm(b + ".norm1", C, &t->l1g, &t->l1b);
+  t->wqkv = B.alloc<bf16>(3L * C * C);
+  B.lin(b + ".attn1.to_q", C, C, nullptr, t->wqkv);
+  B.lin(b + ".attn1.to_k", C, C, nullptr, t->wqkv + (long)C * C);
+  B.lin(b + ".attn1.to_v", C, C, nullptr, t->wqkv + 2L * C * C);
+  t->wo = B.lin(b + ".attn1.to_out.0", C, C, &t->bo);
+  B.norm(b + ".norm2", C, &t->l2g, &t->l2b);
+  t->wq2 = B.lin(b + ".attn2.to_q", C, C, nullptr);
+  t->koff = *kv_cursor;
+  B.lin(b + ".attn2.to_k", C, D, nullptr, e->U.kv_all_w + (long)t->koff * D);
+  t->voff = *kv_cursor + C;
+  B.lin(b + ".attn2.to_v", C, D, nullptr, e->U.kv_all_w + (long)t->voff * D);
+  *kv_cursor += 2 * C;
+  t->wo2 = B.lin(b + ".attn2.to_out.0", C, C, &t->bo2);
+  B.norm(b + ".norm3", C, &t->l3g, &t->l3b);
+  // GEGLU proj [8C][C] with rows interleaved per 64 (value | gate) for the fused epilogue
+  t->wff1 = B.alloc<bf16>(8L * C * C);
+  B.gen(b + ".ff.net.0.proj.weight", 8L * C * C, WK_UNIFORM, C, WL_GEGLU, t->wff1, nullptr, true, 0, 0, 0, 0, 4 * C);
+  t->bff1 = B.alloc<float>(8L * C);
+  B.gen(b + ".ff.net.0.proj.bias", 8L * C, WK_UNIFORM, C, WL_GEGLU, t->bff1, nullptr, false, 0, 0, 0, 0, 4 * C);
+  t->wff2 = B.lin(b + ".ff.net.2", C, 4 * C, &t->bff2);
+  t->wpout = B.lin(p + ".proj_out", C, C, &t->bpout);
+}
+
+static void build_unet(Engine* e, cudaStream_t st) {
+  Builder B{e, st};
+  const UNetCfg& c = e->uc;
+  const int L = (int)c.block_out.size();
+  const int T = c.temb_dim();
+  // sizes of the fused temb-projection and text-K/V weights
+  int temb_total = 0, kv_total = 0;
+  {
+    int out = c.block_out[0];
+    for (int i = 0; i < L; ++i) {
+      out = c.block_out[i];
+      temb_total += c.layers * out;
+      if (c.attn[i]) kv_total += c.layers * 2 * out;
+    }
+    temb_total += 2 * c.block_out[L - 1];
+    kv_total += 2 * c.block_out[L - 1];
+    for (int i = 0; i < L; ++i) {
+      const int o = c.block_out[L - 1 - i];
+      temb_total += (c.layers + 1) * o;
+      if (c.attn[L - 1 - i]) kv_total += (c.layers + 1) * 2 * o;
+    }
+  }
+  UNetW& U = e->U;
+  U.temb_all_n = temb_total;
+  U.temb_all_w = B.alloc<bf16>((long)temb_total * T);
+  U.temb_all_b = B.alloc<float>(temb_total);
+  U.kv_width = kv_total;
+  U.kv_all_w = B.alloc<bf16>((long)kv_total * c.ctx_dim);
+  int tcur = 0, kcur = 0;
+
+  // conv_in: input padded to 64 channels (zeros) so every TMA box is 128-byte aligned
+  U.conv_in_w = B.conv3("conv_in", c.block_out[0], c.in_ch, 64, &U.conv_in_b);
+  U.lin1_w = B.lin("time_embedding.linear_1", T, c.block_out[0], &U.lin1_b);
+  U.lin2_w = B.lin("time_embedding.linear_2", T, T, &U.lin2_b);
+  int out = c.block_out[0];
+  for (int i = 0; i < L; ++i) {
+    const int in = out;
+    out = c.block_out[i];
+    DownW d;
+    d.ch = out;
+    d.down = i != L - 1;
+    for (int j = 0; j < c.layers; ++j) {
+      ResW r;
+      build_res(B, "down_blocks." + std::to_string(i) + ".resnets." + std::to_string(j), j == 0 ? in : out, out, &tcur,
+                &r, true);
+      d.res.push_back(r);
+      if (c.attn[i]) {
+        TfW t;
+        build_tf(B, "down_blocks." + std::to_string(i) + ".attentions." + std::to_string(j), out, &kcur, &t);
+        d.tf.push_back(t);
+      }
+    }
+    if (d.down) d.wdown = B.conv3("down_blocks." + std::to_string(i) + ".downsamplers.0.conv", out, out, out, &d.bdown);
+    U.down.push_back(d);
+  }
+  const int cm = c.block_out[L - 1];
+  build_res(B, "mid_block.resnets.0", cm, cm, &tcur, &U.mid0, true);
+  build_tf(B, "mid_block.attentions.0", cm, &kcur, &U.midtf);
+  build_res(B, "mid_block.resnets.1", cm, cm, &tcur, &U.mid1, true);
+  out = c.block_out[L - 1];
+  for (int i = 0; i < L; ++i) {
+    const int prev = out;
+    out = c.block_out[L - 1 - i];
+    const int in = c.block_out[std::max(L - 2 - i, 0)];
+    UpW u;
+    u.ch = out;
+    u.up = i != L - 1;
+    const int nl = c.layers + 1;
+    for (int j = 0; j < nl; ++j) {
+      const int skip = j == nl - 1 ? in : out;
+      const int rin = j == 0 ? prev : out;
+      ResW r;
+      build_res(B, "up_blocks." + std::to_string(i) + ".resnets." + std::to_string(j), rin + skip, out, &tcur, &r,
+                true);
+      u.res.push_back(r);
+      if (c.attn[L - 1 - i]) {
+        TfW t;
+        build_tf(B, "up_blocks." + std::to_string(i) + ".attentions." + std::to_string(j), out, &kcur, &t);
+        u.tf.push_back(t);
+      }
+    }
+    if (u.up) u.wup = B.conv3("up_blocks." + std::to_string(i) + ".upsamplers.0.conv", out, out, out, &u.bup);
+    U.up.push_back(u);
+  }
+  B.norm("conv_norm_out", c.block_out[0], &U.nout_g, &U.nout_b);
+  U.conv_out_w = B.conv3("conv_out", 4, c.block_out[0], c.block_out[0], &U.conv_out_b);
+  if (tcur != temb_total || kcur != kv_total) throw CudaError("internal: temb/kv width mismatch");
+}
+
+static void build_vae(Engine* e, cudaStream_t st) {
+  Builder B{e, st};
+  const VAECfg& c = e->vc;
+  VAEW& V = e->V;
+  const int cm = c.block_out.back();
+  V.pq_w = B.lin("post_quant_conv", 4, 4, &V.pq_b);
+  // pq is applied by a tiny dense GEMM on 64-channel-padded input: store [4][64]
+  {
+    bf16* w64 = B.alloc<bf16>(16 * 64);  // N padded to 16 rows
+    SD_CUDA(cudaMemsetAsync(w64, 0, 16 * 64 * 2, st));
+    SD_CUDA(cudaMemcpy2DAsync(w64, 64 * 2, V.pq_w, 4 * 2, 4 * 2, 4, cudaMemcpyDeviceToDevice, st));
+    V.pq_w = w64;
+  }
+  V.cin_w = B.conv3("decoder.conv_in", cm, 4, 64, &V.cin_b);
+  int dummy = 0;
+  build_res(B, "decoder.mid_block.resnets.0", cm, cm, &dummy, &V.mid0, false);
+  const std::string a = "decoder.mid_block.attentions.0";
+  B.norm(a + ".group_norm", cm, &V.ag, &V.ab);
+  V.wq = B.lin(a + ".to_q", cm, cm, &V.bq);
+  V.wk = B.lin(a + ".to_k", cm, cm, &V.bk);
+  V.wv = B.lin(a + ".to_v", cm, cm, &V.bv);
+  V.wo = B.lin(a + ".to_out.0", cm, cm, &V.bo);
+  build_res(B, "decoder.mid_block.resnets.1", cm, cm, &dummy, &V.mid1, false);
+  const int L = (int)c.block_out.size();
+  int out = c.block_out[L - 1];
+  for (int i = 0; i < L; ++i) {
+    const int prev = out;
+    out = c.block_out[L - 1 - i];
+    UpW u;
+    u.ch = out;
+    u.up = i != L - 1;
+    for (int j = 0; j < c.layers + 1; ++j) {
+      ResW r;
+      build_res(B, "decoder.up_blocks." + std::to_string(i) + ".resnets." + std::to_string(j), j == 0 ? prev : out,
+                out, &dummy, &r, false);
+      u.res.push_back(r);
+    }
+    if (u.up)
+      u.wup = B.conv3("decoder.up_blocks." + std::to_string(i) + ".upsamplers.0.conv", out, out, out, &u.bup);
+    V.up.push_back(u);
+  }
+  B.norm("decoder.conv_norm_out", c.block_out[0], &V.nout_g, &V.nout_b);
+  V.cout_w = B.conv3("decoder.conv_out", 3, c.block_out[0], c.block_out[0], &V.cout_b);
+}
+
+Engine::~Engine() {
+  for (auto* d : free_decodes) destroy_decode(this, d);
+  warena.release();
+  ws.release();
+  if (kv_cache) cudaFree(kv_cache);
+  if (meta_dev) cudaFree(meta_dev);
+}
+
+static size_t unet_ws_bytes(const Engine* e) {
+  // generous bound: every intermediate of one forward at max rows / max resolution
+  const long P = (long)e->cfg.max_latent_hw * e->cfg.max_latent_hw;
+  const long R = e->max_rows;
+  const int c0 = e->uc.block_out[0];
+  // ≈ 60 tensors of R·P·c0 at the top level dominate (level k has P/4^k pixels, ≤ 4·c0 channels)
+  const double top = (double)R * P * c0 * 2;
+  return (size_t)(top * 140) + ((size_t)512 << 20);
+}
+
+void build_engine(Engine* e) {
+  SD_CUDA(cudaSetDevice(e->device));
+  e->uc = unet_cfg(e->cfg.model);
+  e->vc = vae_cfg(e->cfg.model);
+  e->max_rows = 2 * e->cfg.b_max;
+  const size_t wbytes = e->cfg.model == SD_MODEL_SD15 ? ((size_t)2200 << 20) : ((size_t)64 << 20);
+  e->warena.init(wbytes);
+  cudaStream_t st;
+  SD_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  build_unet(e, st);
+  build_vae(e, st);
+  SD_CUDA(cudaStreamSynchronize(st));
+  SD_CUDA(cudaStreamDestroy(st));
+  e->ws.init(unet_ws_bytes(e));
+  // text K/V cache slots (slot 0 = unconditional)
+  e->max_slots = 4 * e->cfg.b_max + 8;
+  e->slot_elems = (long)e->uc.ctx_len * e->U.kv_width;
+  SD_CUDA(cudaMalloc(&e->kv_cache, (size_t)e->max_slots * e->slot_elems * 2));
+  SD_CUDA(cudaMemset(e->kv_cache, 0, (size_t)e->max_slots * e->slot_elems * 2));
+  e->slot_used.assign(e->max_slots, 0);
+  e->slot_used[0] = 1;
+  e->meta_bytes = 64 << 10;
+  SD_CUDA(cudaMalloc(&e->meta_dev, e->meta_bytes));
+  e->meta_host.resize(e->meta_bytes);
+}
+
+// ---------------------------------------------------------------------------------------------
+// text K/V cache (computed once per prompt at admission; K/V do not depend on x or t)
+// ---------------------------------------------------------------------------------------------
+int ctx_register(Engine* e, const float* emb, int len, int dim, int slot, cudaStream_t st) {
+  if (len != e->uc.ctx_len || dim != e->uc.ctx_dim) throw std::invalid_argument("ctx shape mismatch");
+  if (slot < 0) {
+    std::lock_guard<std::mutex> g(e->mu);
+    for (int s = 1; s < e->max_slots; ++s)
+      if (!e->slot_used[s]) {
+        slot = s;
+        break;
+      }
+    if (slot < 0) throw std::runtime_error("no free ctx slot");
+    e->slot_used[slot] = 1;
+  }
+  bf16* tmp;
+  SD_CUDA(cudaMallocAsync(&tmp, (size_t)len * dim * 2, st));
+  f32_to_bf16(emb, tmp, (long)len * dim, st);
+  GemmDesc d;
+  d.A = tmp;
+  d.M = len;
+  d.K = dim;
+  d.lda = dim;
+  d.Bw[0] = e->U.kv_all_w;
+  d.N = e->U.kv_width;
+  d.ldb = dim;
+  d.out = e->kv_cache + (long)slot * e->slot_elems;
+  d.ldo = e->U.kv_width;
+  gemm(d, st);
+  SD_CUDA(cudaFreeAsync(tmp, st));
+  return slot;
+}
+
+// ---------------------------------------------------------------------------------------------
+// UNet forward over `rows` rows at h×w (activations NHWC bf16)
+// ---------------------------------------------------------------------------------------------
+struct Fwd {
+  Engine* e;
+  cudaStream_t st;
+  int R;
+  const float* temb_all;  // [R][temb_all_n] fp32
+  const int* kv_index;    // [R] ctx slot per row
+  void* gn_ws;
+
+  bf16* buf(long elems) { return e->ws.get<bf16>((size_t)elems); }
+
+  void gn(const bf16* x, bf16* y, int P, int C, const float* g, const float* b, float eps, bool silu) {
+    const int pi = e->prof.begin(PC_GN, st, 3.0 * R * P * C * 2);
+    group_norm(x, y, R, P, C, e->uc.groups, g, b, eps, silu, gn_ws, st);
+    e->prof.end(pi, st);
+  }
+  void ln(const bf16* x, bf16* y, long T, int C, const float* g, const float* b) {
+    const int pi = e->prof.begin(PC_LN, st, 2.0 * T * C * 2);
+    layer_norm(x, y, (int)T, C, g, b, e->uc.eps_ln, st);
+    e->prof.end(pi, st);
+  }
+  void attn(const AttnDesc& a) {
+    const int pi = e->prof.begin(PC_ATTN, st, 4.0 * a.rows * a.heads * (double)a.Lq * a.Lk * a.d);
+    attention(a, st);
+    e->prof.end(pi, st);
+  }
+  void linear(const bf16* A, long M, int K, const bf16* W, int N, const float* bias, void* out, int ldo,
+              const bf16* res = nullptr, int act = ACT_NONE, int out_f32 = 0) {
+    GemmDesc d;
+    d.A = A;
+    d.M = (int)M;
+    d.K = K;
+    d.lda = K;
+    d.Bw[0] = W;
+    d.N = N;
+    d.ldb = K;
+    d.out = out;
+    d.ldo = ldo;
+    d.bias = bias;
+    d.res = res;
+    d.ldr = ldo;
+    d.act = act;
+    d.out_f32 = out_f32;
+    const int pi = e->prof.begin(PC_GEMM, st, 2.0 * M * N * K);
+    gemm(d, st);
+    e->prof.end(pi, st);
+  }
+  void conv(const bf16* x, int H, int W, int C, const bf16* w, int N, const float* bias, void* out,
+            const float* temb = nullptr, const bf16* res = nullptr, int out_f32 = 0, int ldo = 0, int c_real = 0) {
+    GemmDesc d;
+    d.mode = GEMM_CONV3;
+    d.xs[0] = x;
+    d.cs[0] = C;
+    d.B = R;
+    d.H = H;
+    d.W = W;
+    d.Bw[0] = w;
+    d.N = N;
+    d.out = out;
+    d.ldo = ldo ? ldo : N;
+    d.bias = bias;
+    d.temb = temb;
+    d.ld_temb = e->U.temb_all_n;
+    d.res = res;
+    d.ldr = N;
+    d.out_f32 = out_f32;
+    const int pi = e->prof.begin(PC_CONV, st, 2.0 * R * H * W * N * 9.0 * (c_real ? c_real : C));
+    gemm(d, st);
+    e->prof.end(pi, st);
+  }
+
+  bf16* resblock(const ResW& r, const bf16* x, int H, int W) {
+    const int P = H * W;
+    const size_t mk = e->ws.mark();
+    bf16* out = buf((long)R * P * r.cout);  // allocated below the scratch mark
+    const size_t mk2 = e->ws.mark();
+    (void)mk;
+    bf16* a = buf((long)R * P * r.cin);
+    gn(x, a, P, r.cin, r.n1g, r.n1b, e->uc.eps_res, true);
+    bf16* h1 = buf((long)R * P * r.cout);
+    conv(a, H, W, r.cin, r.w1, r.cout, r.b1, h1, temb_all + r.temb_off);
+    bf16* a2 = buf((long)R * P * r.cout);
+    gn(h1, a2, P, r.cout, r.n2g, r.n2b, e->uc.eps_res, true);
+    const bf16* sc = x;
+    if (r.wsc) {
+      bf16* s = buf((long)R * P * r.cout);
+      linear(x, (long)R * P, r.cin, r.wsc, r.cout, r.bsc, s, r.cout);
+      sc = s;
+    }
+    conv(a2, H, W, r.cout, r.w2, r.cout, r.b2, out, nullptr, sc);
+    e->ws.reset(mk2);
+    return out;
+  }
+
+  bf16* transformer(const TfW& t, const bf16* x, int H, int W) {
+    const int C = t.C, P = H * W;
+    const long T = (long)R * P;
+    const int heads = e->uc.heads, dh = C / heads;
+    bf16* out = buf(T * C);
+    const size_t mk = e->ws.mark();
+    bf16* a = buf(T * C);
+    gn(x, a, P, C, t.gng, t.gnb, e->uc.eps_tf, false);
+    bf16* h = buf(T * C);
+    linear(a, T, C, t.wpin, C, t.bpin, h, C);
+    bf16* n = buf(T * C);
+    ln(h, n, T, C, t.l1g, t.l1b);
+    bf16* qkv = buf(T * 3 * C);
+    linear(n, T, C, t.wqkv, 3 * C, nullptr, qkv, 3 * C);
+    bf16* o = buf(T * C);
+    AttnDesc ad{};
+    ad.Q = qkv;
+    ad.ldq = 3 * C;
+    ad.q_bstride = (long)P * 3 * C;
+    ad.K = qkv + C;
+    ad.V = qkv + 2 * C;
+    ad.ldk = 3 * C;
+    ad.kv_bstride = (long)P * 3 * C;
+    ad.kv_index = nullptr;
+    ad.O = o;
+    ad.ldo = C;
+    ad.o_bstride = (long)P * C;
+    ad.rows = R;
+    ad.heads = heads;
+    ad.d = dh;
+    ad.Lq = P;
+    ad.Lk = P;
+    attn(ad);
+    bf16* h2 = buf(T * C);
+    linear(o, T, C, t.wo, C, t.bo, h2, C, h);
+    ln(h2, n, T, C, t.l2g, t.l2b);
+    bf16* q2 = buf(T * C);
+    linear(n, T, C, t.wq2, C, nullptr, q2, C);
+    AttnDesc cd{};
+    cd.Q = q2;
+    cd.ldq = C;
+    cd.q_bstride = (long)P * C;
+    cd.K = e->kv_cache + t.koff;
+    cd.V = e->kv_cache + t.voff;
+    cd.ldk = e->U.kv_width;
+    cd.kv_bstride = e->slot_elems;
+    cd.kv_index = kv_index;
+    cd.O = o;
+    cd.ldo = C;
+    cd.o_bstride = (long)P * C;
+    cd.rows = R;
+    cd.heads = heads;
+    cd.d = dh;
+    cd.Lq = P;
+    cd.Lk = e->uc.ctx_len;
+    attn(cd);
+    bf16* h3 = buf(T * C);
+    linear(o, T, C, t.wo2, C, t.bo2, h3, C, h2);
+    ln(h3, n, T, C, t.l3g, t.l3b);
+    bf16* gg = buf(T * 4 * C);
+    linear(n, T, C, t.wff1, 8 * C, t.bff1, gg, 4 * C, nullptr, ACT_GEGLU);
+    bf16* h4 = buf(T * C);
+    linear(gg, T, 4 * C, t.wff2, C, t.bff2, h4, C, h3);
+    linear(h4, T, C, t.wpout, C, t.bpout, out, C, x);  // 3 LN + 2 attention
+    e->ws.reset(mk);
+    return out;
+  }
+};
+
+static void unet_forward(Engine* e, cudaStream_t st, int R, int H, int W, const bf16* x_in, const float* t_row,
+                         const int* kv_index, float* eps_out) {
+  const UNetCfg& c = e->uc;
+  UNetW& U = e->U;
+  Fwd f{e, st, R, nullptr, kv_index, nullptr};
+  f.gn_ws = e->ws.alloc(gn_workspace_bytes(R, H * W * 4, 64) + (1 << 20));
+  const int T = c.temb_dim(), C0 = c.block_out[0];
+  // time embedding: sinusoid → linear_1 → SiLU → linear_2 → SiLU (the ResBlocks consume SiLU(temb))
+  bf16* sinus = f.buf((long)R * C0);
+  timestep_sinusoid(t_row, R, C0, sinus, st);
+  bf16* t1 = f.buf((long)R * T);
+  f.linear(sinus, R, C0, U.lin1_w, T, U.lin1_b, t1, T, nullptr, ACT_SILU);
+  bf16* t2 = f.buf((long)R * T);
+  f.linear(t1, R, T, U.lin2_w, T, U.lin2_b, t2, T, nullptr, ACT_SILU);
+  float* temb_all = e->ws.get<float>((size_t)R * U.temb_all_n);
+  f.linear(t2, R, T, U.temb_all_w, U.temb_all_n, U.temb_all_b, temb_all, U.temb_all_n, nullptr, ACT_NONE, 1);
+  f.temb_all = temb_all;
+
+  int h = H, w = W;
+  bf16* x = f.buf((long)R * h * w * C0);
+  f.conv(x_in, h, w, 64, U.conv_in_w, C0, U.conv_in_b, x, nullptr, nullptr, 0, 0, c.in_ch);
+  struct Skip {
+    bf16* p;
+    int C;
+  };
+  std::vector<Skip> skips;
+  skips.push_back({x, C0});
+  int C = C0;
+  for (auto& d : U.down) {
+    for (size_t j = 0; j < d.res.size(); ++j) {
+      x = f.resblock(d.res[j], x, h, w);
+      C = d.res[j].cout;
+      if (!d.tf.empty()) x = f.transformer(d.tf[j], x, h, w);
+      skips.push_back({x, C});
+    }
+    if (d.down) {
+      const int ho = (h + 1) / 2, wo = (w + 1) / 2;
+      const size_t mk = e->ws.mark();
+      bf16* out = f.buf((long)R * ho * wo * C);
+      const size_t mk2 = e->ws.mark();
+      bf16* cols = f.buf((long)R * ho * wo * 9 * C);
+      im2col_s2(x, cols, R, h, w, C, st);
+      f.linear(cols, (long)R * ho * wo, 9 * C, d.wdown, C, d.bdown, out, C);
+      e->ws.reset(mk2);
+      (void)mk;
+      x = out;
+      h = ho;
+      w = wo;
+      skips.push_back({x, C});
+    }
+  }
+  x = f.resblock(U.mid0, x, h, w);
+  x = f.transformer(U.midtf, x, h, w);
+  x = f.resblock(U.mid1, x, h, w);
+  for (auto& u : U.up) {
+    for (size_t j = 0; j < u.res.size(); ++j) {
+      Skip s = skips.back();
+      skips.pop_back();
+      const int Ccat = C + s.C;
+      bf16* cat = f.buf((long)R * h * w * Ccat);
+      concat_channels(x, C, s.p, s.C, cat, (long)R * h * w, st);
+      x = f.resblock(u.res[j], cat, h, w);
+      C = u.res[j].cout;
+      if (!u.tf.empty()) x = f.transformer(u.tf[j], x, h, w);
+    }
+    if (u.up) {
+      bf16* upx = f.buf((long)R * 4 * h * w * C);
+      upsample2x(x, upx, R, h, w, C, st);
+      h *= 2;
+      w *= 2;
+      bf16* out = f.buf((long)R * h * w * C);
+      f.conv(upx, h, w, C, u.wup, C, u.bup, out);
+      x = out;
+    }
+  }
+  bf16* a = f.buf((long)R * h * w * C);
+  f.gn(x, a, h * w, C, U.nout_g, U.nout_b, c.eps_res, true);
+  f.conv(a, h, w, C, U.conv_out_w, 4, U.conv_out_b, eps_out, nullptr, nullptr, 1, 4);
+}
+
+// ---------------------------------------------------------------------------------------------
+// sampler coefficients (R4 / R5), fp64 on the host, passed as fp32
+// ---------------------------------------------------------------------------------------------
+struct Sched {
+  double ac[1000];
+  Sched() {
+    const double a = sqrt(0.00085), b = sqrt(0.012);
+    double prod = 1.0;
+    for (int i = 0; i < 1000; ++i) {
+      const double s = a + (b - a) * i / 999.0;
+      prod *= 1.0 - s * s;
+      ac[i] = prod;
+    }
+  }
+};
+static const Sched& sched() {
+  static Sched s;
+  return s;
+}
+static int t_of(int n, int i) { return (n - 1 - i) * (1000 / n) + 1; }
+static double euler_sigma(int n, int i) {
+  if (i >= n) return 0.0;
+  const double a = sched().ac[t_of(n, i)];
+  return sqrt((1.0 - a) / a);
+}
+
+void sampler_coefs(int sampler, int n, int i, float* t_out, float* c_in, float* A, float* Bc) {
+  const Sched& s = sched();
+  const int t = t_of(n, i);
+  *t_out = (float)t;
+  if (sampler == SD_SAMPLER_DDIM) {
+    const int tp = t - 1000 / n;
+    const double at = s.ac[t], ap = tp >= 0 ? s.ac[tp] : s.ac[0];
+    *c_in = 1.f;
+    *A = (float)sqrt(ap / at);
+    *Bc = (float)(sqrt(1.0 - ap) - sqrt(ap) * sqrt(1.0 - at) / sqrt(at));
+  } else {
+    const double si = euler_sigma(n, i), sn = euler_sigma(n, i + 1);
+    *c_in = (float)(1.0 / sqrt(si * si + 1.0));
+    *A = 1.f;
+    *Bc = (float)(sn - si);
+  }
+}
+
+float init_sigma(int sampler, int n) {
+  if (sampler == SD_SAMPLER_DDIM) return 1.f;
+  const double s0 = euler_sigma(n, 0);
+  return (float)sqrt(s0 * s0 + 1.0);
+}
+
+// ---------------------------------------------------------------------------------------------
+// sd_step_batch
+// ---------------------------------------------------------------------------------------------
+void step_batch(Engine* e, const sd_batch* b, cudaStream_t st) {
+  const int n = b->n_req, h = b->latent_h, w = b->latent_w, hw = h * w;
+  std::vector<int> row_req, unc_row(n, -1);
+  for (int r = 0; r < n; ++r) row_req.push_back(r);
+  for (int r = 0; r < n; ++r)
+    if (b->has_uncond[r]) {
+      unc_row[r] = (int)row_req.size();
+      row_req.push_back(r);
+    }
+  const int R = (int)row_req.size();
+  // host metadata block → one H2D copy
+  char* hb = e->meta_host.data();
+  size_t off = 0;
+  auto put = [&](const void* src, size_t bytes) {
+    off = (off + 15) & ~size_t(15);
+    const size_t o = off;
+    memcpy(hb + o, src, bytes);
+    off += bytes;
+    return o;
+  };
+  std::vector<float> c_in(n), ga(n), A(n), Bc(n), t_row(R);
+  std::vector<int> kv(R);
+  std::vector<const float*> lat(n);
+  for (int r = 0; r < n; ++r) {
+    float t;
+    sampler_coefs(e->cfg.sampler, b->n_steps[r], b->step[r], &t, &c_in[r], &A[r], &Bc[r]);
+    ga[r] = b->guidance[r];
+    lat[r] = b->latents[r];
+    t_row[r] = t;
+  }
+  for (int k = 0; k < R; ++k) {
+    const int r = row_req[k];
+    t_row[k] = t_row[r];
+    kv[k] = k < n ? b->ctx_slot[r] : 0;
+  }
+  const size_t o_lat = put(lat.data(), n * sizeof(float*));
+  const size_t o_cin = put(c_in.data(), n * 4);
+  const size_t o_t = put(t_row.data(), R * 4);
+  const size_t o_rr = put(row_req.data(), R * 4);
+  const size_t o_ur = put(unc_row.data(), n * 4);
+  const size_t o_g = put(ga.data(), n * 4);
+  const size_t o_a = put(A.data(), n * 4);
+  const size_t o_b = put(Bc.data(), n * 4);
+  const size_t o_kv = put(kv.data(), R * 4);
+  SD_CUDA(cudaMemcpyAsync(e->meta_dev, hb, off, cudaMemcpyHostToDevice, st));
+  char* db = e->meta_dev;
+  RowMap m;
+  m.latents = reinterpret_cast<const float* const*>(db + o_lat);
+  m.c_in = reinterpret_cast<const float*>(db + o_cin);
+  m.t_row = reinterpret_cast<const float*>(db + o_t);
+  m.row_req = reinterpret_cast<const int*>(db + o_rr);
+  m.unc_row = reinterpret_cast<const int*>(db + o_ur);
+  m.guidance = reinterpret_cast<const float*>(db + o_g);
+  m.coef_a = reinterpret_cast<const float*>(db + o_a);
+  m.coef_b = reinterpret_cast<const float*>(db + o_b);
+  const int* kv_dev = reinterpret_cast<const int*>(db + o_kv);
+
+  e->ws.reset(0);
+  bf16* x_in = e->ws.get<bf16>((size_t)R * hw * 64);
+  gather_rows(m, R, hw, 64, x_in, st);
+  float* eps = e->ws.get<float>((size_t)R * hw * 4);
+  unet_forward(e, st, R, h, w, x_in, m.t_row, kv_dev, eps);
+  combine_update(m, n, hw, eps, 4, reinterpret_cast<float* const*>(db + o_lat), st);
+}
+
+}  // namespace sd
+
+namespace sd {
+cudaEvent_t Prof::ev() {
+  if (!pool.empty()) {
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  SD_CUDA(cudaEventCreate(&e));
+  return e;
+}
+int Prof::begin(int cls, cudaStream_t st, double work) {
+  if (!on) return -1;
+  Rec r{cls, ev(), ev(), work};
+  SD_CUDA(cudaEventRecord(r.a, st));
+  recs.push_back(r);
+  return (int)recs.size() - 1;
+}
+void Prof::end(int idx, cudaStream_t st) {
+  if (idx >= 0) SD_CUDA(cudaEventRecord(recs[idx].b, st));
+}
+void Prof::read(int cls, double* ms, long long* n, double* work) {
+  *ms = 0;
+  *n = 0;
+  *work = 0;
+  for (auto& r : recs)
+    if (r.cls == cls) {
+      SD_CUDA(cudaEventSynchronize(r.b));
+      float t = 0;
+      SD_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+      *ms += t;
+      *n += 1;
+      *work += r.work;
+    }
+}
+void Prof::reset() {
+  for (auto& r : recs) {
+    pool.push_back(r.a);
+    pool.push_back(r.b);
+  }
+  recs.clear();
+}
+Prof::~Prof() {
+  reset();
+  for (auto e : pool) cudaEventDestroy(e);
+}
+}  // namespace sd

@@ -1,0 +1,168 @@
+// Engine internals: model definitions, device weights, workspaces, UNet / VAE forward.
+#pragma once
+#include <atomic>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "kernels_ew.h"
+#include "sd_api.h"
+
+namespace sd {
+
+struct UNetCfg {
+  std::vector<int> block_out;
+  std::vector<int> attn;
+  int layers, groups, heads, ctx_dim, ctx_len;
+  float eps_res = 1e-5f, eps_tf = 1e-6f, eps_ln = 1e-5f;
+  int in_ch = 4;
+  int temb_dim() const { return 4 * block_out[0]; }
+};
+struct VAECfg {
+  std::vector<int> block_out;
+  int layers, groups;
+  float sf;
+  float eps = 1e-6f;
+};
+UNetCfg unet_cfg(int model);
+VAECfg vae_cfg(int model);
+
+// bump allocator over one cudaMalloc'd block
+struct Arena {
+  char* base = nullptr;
+  size_t cap = 0, used = 0;
+  void init(size_t bytes);
+  void release();
+  void* alloc(size_t bytes);
+  template <class T>
+  T* get(size_t n) { return reinterpret_cast<T*>(alloc(n * sizeof(T))); }
+  size_t mark() const { return used; }
+  void reset(size_t m) { used = m; }
+};
+
+struct ResW {
+  int cin, cout, temb_off;
+  float *n1g, *n1b, *b1, *n2g, *n2b, *b2, *bsc = nullptr;
+  bf16 *w1, *w2, *wsc = nullptr;
+};
+struct TfW {
+  int C;
+  float *gng, *gnb, *bpin, *l1g, *l1b, *bo, *l2g, *l2b, *bo2, *l3g, *l3b, *bff1, *bff2, *bpout;
+  bf16 *wpin, *wqkv, *wo, *wq2, *wo2, *wff1, *wff2, *wpout;
+  int koff, voff;  // column offsets of this block's K / V in the text K/V cache rows
+};
+struct DownW {
+  std::vector<ResW> res;
+  std::vector<TfW> tf;
+  bool down;
+  bf16* wdown = nullptr;
+  float* bdown = nullptr;
+  int ch;
+};
+struct UpW {
+  std::vector<ResW> res;
+  std::vector<TfW> tf;
+  bool up;
+  bf16* wup = nullptr;
+  float* bup = nullptr;
+  int ch;
+};
+struct UNetW {
+  bf16* conv_in_w;
+  float* conv_in_b;
+  bf16 *lin1_w, *lin2_w, *temb_all_w;
+  float *lin1_b, *lin2_b, *temb_all_b;
+  int temb_all_n = 0;
+  std::vector<DownW> down;
+  ResW mid0, mid1;
+  TfW midtf;
+  std::vector<UpW> up;
+  float *nout_g, *nout_b, *conv_out_b;
+  bf16* conv_out_w;
+  bf16* kv_all_w;   // [kv_width][ctx_dim]: for each transformer (forward order) K_j then V_j
+  int kv_width = 0;
+};
+struct VAEW {
+  float *pq_b, *cin_b;
+  bf16 *pq_w, *cin_w;
+  ResW mid0, mid1;
+  float *ag, *ab, *bq, *bk, *bv, *bo;
+  bf16 *wq, *wk, *wv, *wo;
+  std::vector<UpW> up;
+  float *nout_g, *nout_b, *cout_b;
+  bf16* cout_w;
+};
+
+// one VAE work item: op over a band of output rows [y0, y1) (R7 V1)
+struct VItem {
+  int op;          // VOP_*
+  int a, b, c;     // buffer ids (src, dst, extra)
+  const void* p0;  // layer parameters
+  int C, C2, H, W; // channels in/out, spatial size of the OUTPUT
+  int y0, y1;
+  int gn;          // GN layer index (partials slot)
+  int silu;
+  const void* p1 = nullptr;
+};
+
+struct DecodeState;
+
+// Per-kernel-class device timing with CUDA events on the launching stream (bench roofline).
+enum { PC_CONV = 0, PC_GEMM = 1, PC_ATTN = 2, PC_GN = 3, PC_LN = 4, PC_OTHER = 5, PC_VAE = 6, PC_N = 7 };
+struct Prof {
+  bool on = false;
+  struct Rec {
+    int cls;
+    cudaEvent_t a, b;
+    double work;
+  };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t ev();
+  int begin(int cls, cudaStream_t st, double work);
+  void end(int idx, cudaStream_t st);
+  void read(int cls, double* ms, long long* n, double* work);
+  void reset();
+  ~Prof();
+};
+
+struct Engine {
+  Prof prof;
+  sd_engine_config cfg{};
+  int device = 0;
+  UNetCfg uc;
+  VAECfg vc;
+  Arena warena;          // weights
+  Arena ws;              // UNet workspace (reset every step)
+  UNetW U{};
+  VAEW V{};
+  // text K/V cache
+  bf16* kv_cache = nullptr;
+  int max_slots = 0;
+  long slot_elems = 0;
+  std::vector<int> slot_used;
+  // per-step metadata (device)
+  char* meta_dev = nullptr;
+  size_t meta_bytes = 0;
+  std::vector<char> meta_host;
+  int max_rows = 0;
+  std::atomic<int64_t> launches{0};
+  bool failed = false;
+  std::mutex mu;
+  // VAE decode slots
+  std::vector<DecodeState*> free_decodes;
+  std::mutex dmu;
+  ~Engine();
+};
+
+void build_engine(Engine* e);
+void step_batch(Engine* e, const sd_batch* b, cudaStream_t st);
+int ctx_register(Engine* e, const float* emb, int len, int dim, int slot, cudaStream_t st);
+void vae_decode_chunk(Engine* e, const float* z, int h, int w, int n_chunks, int chunk, DecodeState** state,
+                      float* image, cudaStream_t st);
+void destroy_decode(Engine* e, DecodeState* d);
+
+}  // namespace sd

@@ -1,0 +1,54 @@
+// Internal (C++) interface of the sm_100a kernels. Not part of the C ABI (include/sd_api.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+typedef __nv_bfloat16 bf16;
+
+namespace sd {
+
+enum { ACT_NONE = 0, ACT_SILU = 1, ACT_GEGLU = 2 };
+enum { GEMM_DENSE = 0, GEMM_CONV3 = 1 };
+
+// One tcgen05 GEMM launch: D[M][N] = A[M][K] · B[N][K]ᵀ, fp32 accumulate in TMEM, fused epilogue.
+//  mode GEMM_DENSE : A row-major [M][K] (row stride lda elements), B [N][K] (ldb = K).
+//  mode GEMM_CONV3 : implicit 3x3 / stride 1 / pad 1 convolution over NHWC bf16 inputs.
+//                    A = im2col(concat(xs[0], xs[1])) is never materialised: every K block is one
+//                    TMA box of 128 output pixels × 64 input channels shifted by the tap (dy,dx);
+//                    out-of-image rows/cols are zero-filled by TMA (= the conv padding).
+//                    B = weights [N][9][cs[s]] per source (tap-major, channel-minor).
+// Epilogue: v = alpha·acc + bias[n] (or bias[m] if bias_per_row) + temb[img][n];
+//           act (SiLU, or GEGLU over column pairs (c, c+64) of every 128-column group);
+//           + res[m][n]; stored bf16 or fp32 at out[m·ldo + col_off + n].
+struct GemmDesc {
+  int mode = GEMM_DENSE;
+  const bf16* A = nullptr;
+  int M = 0, K = 0, lda = 0;
+  int nsrc = 1;
+  const bf16* xs[2] = {nullptr, nullptr};
+  int cs[2] = {0, 0};
+  int B = 0, H = 0, W = 0;
+  const bf16* Bw[2] = {nullptr, nullptr};
+  int N = 0, ldb = 0;
+  void* out = nullptr;
+  int ldo = 0, col_off = 0, out_f32 = 0;
+  const float* bias = nullptr;
+  int bias_per_row = 0;
+  float alpha = 1.f;
+  const float* temb = nullptr;
+  int ld_temb = 0;
+  int rows_per_img = 1;       // dense mode: image index = m / rows_per_img (for temb)
+  const bf16* res = nullptr;
+  int ldr = 0;
+  int act = ACT_NONE;
+  int m_tile_begin = 0, m_tile_count = -1;  // restrict to a contiguous range of M tiles (bands)
+  int bn = 0;                 // N tile (64/128/160/256), 0 = auto
+};
+
+void gemm(const GemmDesc& d, cudaStream_t st);
+// M tiles of a conv3 launch whose output rows lie in [y0, y1) of image 0 (used for bands).
+void conv3_tile_geometry(int B, int H, int W, int* wt, int* ht, int* bt);
+int num_sms();
+
+}  // namespace sd

@@ -1,0 +1,86 @@
+// Internal interface of the non-GEMM kernels (norms, attention, elementwise, weight init).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stddef.h>
+#include <stdint.h>
+
+typedef __nv_bfloat16 bf16;
+
+namespace sd {
+
+// ---- norms (norm.cu) ----
+size_t gn_workspace_bytes(int B, int P, int G);
+// x, y: [B][P][C] bf16 (may alias? no: y != x required only if silu chain needs x later)
+void group_norm(const bf16* x, bf16* y, int B, int P, int C, int G, const float* gamma, const float* beta, float eps,
+                bool silu, void* ws, cudaStream_t st);
+int gn_chunks(int P);  // 128-pixel chunks of one image
+void gn_stats_range(const bf16* x, int P, int C, int G, int c0, int c1, void* ws, cudaStream_t st);
+void gn_apply_range(const bf16* x, bf16* y, int P, int C, int G, int c0, int c1, const float* gamma, const float* beta,
+                    float eps, bool silu, void* ws, cudaStream_t st);
+void layer_norm(const bf16* x, bf16* y, int T, int C, const float* gamma, const float* beta, float eps,
+                cudaStream_t st);
+
+// ---- attention (attention.cu): O = softmax(Q Kᵀ/√d) V per (batch row, head) ----
+struct AttnDesc {
+  const bf16* Q;
+  int ldq;           // elements between consecutive tokens
+  long q_bstride;    // elements between batch rows
+  const bf16* K;
+  const bf16* V;
+  int ldk;
+  long kv_bstride;
+  const int* kv_index;  // optional per-row batch index for K/V (cross-attention ctx slots)
+  bf16* O;
+  int ldo;
+  long o_bstride;
+  int rows, heads, d, Lq, Lk;
+};
+void attention(const AttnDesc& a, cudaStream_t st);
+
+// row softmax for the VAE attention path: P[r][:] = softmax(S[r][:]) (S fp32, P bf16)
+void softmax_rows(const float* S, bf16* P, int rows, int cols, cudaStream_t st);
+
+// ---- elementwise (elementwise.cu) ----
+struct RowMap {                 // device-side per-step metadata (uploaded once per call)
+  const float* const* latents;  // [n_req] fp32 [4][h][w]
+  const float* c_in;            // [n_req]
+  const float* t_row;           // [rows]
+  const int* row_req;           // [rows] request index of each UNet row
+  const int* unc_row;           // [n_req] row index of the uncond row or -1
+  const float* guidance;        // [n_req]
+  const float* coef_a;          // [n_req] x ← a·x + b·ε̃
+  const float* coef_b;          // [n_req]
+};
+void gather_rows(const RowMap& m, int rows, int hw, int cpad, bf16* out, cudaStream_t st);
+void combine_update(const RowMap& m, int n_req, int hw, const float* eps, int ld_eps, float* const* latents_dev,
+                    cudaStream_t st);
+void timestep_sinusoid(const float* t_row, int rows, int dim, bf16* out, cudaStream_t st);
+void upsample2x(const bf16* x, bf16* y, int B, int H, int W, int C, cudaStream_t st);
+void im2col_s2(const bf16* x, bf16* y, int B, int H, int W, int C, cudaStream_t st);  // 3x3 stride 2 pad 1
+void concat_channels(const bf16* a, int ca, const bf16* b, int cb, bf16* y, long P, cudaStream_t st);
+void f32_to_bf16(const float* x, bf16* y, long n, cudaStream_t st);
+// VAE head input: z fp32 [4][h][w] → bf16 NHWC [h][w][cpad] of z·scale (zeros in channels ≥ 4)
+void latent_to_nhwc(const float* z, int hw, float scale, int cpad, bf16* out, cudaStream_t st);
+// image NHWC fp32 [P][ld] (first 3 channels) → NCHW fp32 [3][P]
+void nhwc_to_nchw3(const float* x, int ld, long P, float* y, cudaStream_t st);
+
+// ---- weight init (weights.cu) — counter-based generator shared in spec with synth/ ----
+enum { WL_PLAIN = 0, WL_CONV3 = 1, WL_GEGLU = 2, WL_CONV1 = 3 };
+enum { WK_UNIFORM = 0, WK_GAMMA = 1, WK_BETA = 2 };
+struct WeightInit {
+  uint64_t tseed;      // tensor_seed(global_seed, name)
+  int kind;            // WK_*
+  float bound;         // fl32(1/sqrt(fan_in)) (uniform kind)
+  int layout;          // WL_*
+  long n;              // canonical element count
+  int O, I, I1;        // conv3: O out channels, I in channels, I1 split (first source channels)
+  int Ipad;            // conv3 destination channels of source 0 (≥ I1) when no split
+  int F;               // GEGLU: half width (rows are [value F | gate F])
+  void* dst0;
+  void* dst1;
+  int out_bf16;
+};
+void init_weight(const WeightInit& w, cudaStream_t st);
+
+}  // namespace sd

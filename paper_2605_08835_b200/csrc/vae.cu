@@ -1,0 +1,438 @@
+// Chunked VAE decode (SURVEY §8(a) a11; PAPER.md:162, :230 VAE Chunking; reading R7 V1
+// "stage-synchronous halo tiles"). The decode is an ordered list of work items:
+//   HEAD                 post_quant_conv, conv_in, mid block (res, d=512 attention, res) on the whole latent
+//   GN_STATS / GN_APPLY  per row band: 128-pixel-chunk partials, merged in fixed order over ALL chunks
+//   CONV / SHORTCUT      per row band of the output; the 1-row halo is read from the full input tensor
+//                        by the TMA box (zero outside the image = the conv padding)
+//   UPSAMPLE             per row band of the 2x output
+// `c` chunks are `c` contiguous ranges of the list (min-max partition of the predicted item cost).
+// Every item computes exactly what the whole-layer kernel computes for those rows, so any chunking
+// is bitwise equal to the whole decode (I6).
+#include <algorithm>
+#include <cmath>
+
+#include "engine.h"
+
+namespace sd {
+
+enum { VOP_HEAD = 0, VOP_GN_STATS, VOP_GN_APPLY, VOP_CONV, VOP_SHORTCUT, VOP_UPSAMPLE, VOP_FINAL };
+enum { NBUF = 6 };
+
+struct DecodeState {
+  int h = 0, w = 0, n_chunks = 0, next_chunk = 0;
+  Arena ar;
+  size_t buf_elems = 0;
+  bf16* buf[NBUF];
+  float* img_nhwc = nullptr;
+  void* gn_ws = nullptr;
+  std::vector<VItem> items;
+  std::vector<int64_t> cost;
+  std::vector<int> bounds;
+};
+
+static int band_rows(int H) { return H >= 64 ? 32 : std::max(8, H / 2); }
+
+static void conv_desc(GemmDesc& d, const bf16* x, int H, int W, int C, const bf16* w, int N, const float* b, void* out,
+                      const bf16* res) {
+  d.mode = GEMM_CONV3;
+  d.xs[0] = x;
+  d.cs[0] = C;
+  d.B = 1;
+  d.H = H;
+  d.W = W;
+  d.Bw[0] = w;
+  d.N = N;
+  d.out = out;
+  d.ldo = N;
+  d.bias = b;
+  d.res = res;
+  d.ldr = N;
+}
+
+static void run_conv_band(Engine* e, const bf16* x, int H, int W, int C, const bf16* w, int N, const float* b, void* out,
+                          const bf16* res, int y0, int y1, int out_f32, cudaStream_t st) {
+  GemmDesc d;
+  conv_desc(d, x, H, W, C, w, N, b, out, res);
+  d.out_f32 = out_f32;
+  int wt, ht, bt;
+  conv3_tile_geometry(1, H, W, &wt, &ht, &bt);
+  const int tx = cdiv(W, wt);
+  if (y0 % ht || (y1 % ht && y1 != H)) throw CudaError("vae band not aligned to conv tile height");
+  d.m_tile_begin = (y0 / ht) * tx;
+  d.m_tile_count = cdiv(y1 - y0, ht) * tx;
+  gemm(d, st);
+}
+
+// whole-tensor resblock at the latent resolution (head)
+static void head_res(Engine* e, DecodeState* s, const ResW& r, bf16* x, bf16* out, bf16* t1, bf16* t2, int H, int W,
+                     cudaStream_t st) {
+  const int P = H * W, G = e->vc.groups;
+  group_norm(x, t1, 1, P, r.cin, G, r.n1g, r.n1b, e->vc.eps, true, s->gn_ws, st);
+  run_conv_band(e, t1, H, W, r.cin, r.w1, r.cout, r.b1, t2, nullptr, 0, H, 0, st);
+  group_norm(t2, t1, 1, P, r.cout, G, r.n2g, r.n2b, e->vc.eps, true, s->gn_ws, st);
+  run_conv_band(e, t1, H, W, r.cout, r.w2, r.cout, r.b2, out, x, 0, H, 0, st);
+}
+
+static void run_head(Engine* e, DecodeState* s, const float* z, cudaStream_t st) {
+  const int H = s->h, W = s->w, P = H * W;
+  const int cm = e->vc.block_out.back();
+  VAEW& V = e->V;
+  size_t mk = s->ar.mark();
+  bf16* zin = s->ar.get<bf16>((size_t)P * 64);
+  latent_to_nhwc(z, P, 1.f / e->vc.sf, 64, zin, st);
+  bf16* hq = s->ar.get<bf16>((size_t)P * 64);
+  SD_CUDA(cudaMemsetAsync(hq, 0, (size_t)P * 64 * 2, st));
+  GemmDesc d;
+  d.A = zin;
+  d.M = P;
+  d.K = 64;
+  d.lda = 64;
+  d.Bw[0] = V.pq_w;
+  d.N = 4;
+  d.ldb = 64;
+  d.out = hq;
+  d.ldo = 64;
+  d.bias = V.pq_b;
+  gemm(d, st);
+  bf16* x0 = s->buf[1];
+  run_conv_band(e, hq, H, W, 64, V.cin_w, cm, V.cin_b, x0, nullptr, 0, H, 0, st);
+  bf16* x1 = s->buf[2];
+  head_res(e, s, V.mid0, x0, x1, s->buf[3], s->buf[4], H, W, st);
+  // single-head attention, d = cm, via GEMMs: S = QKᵀ/√d (fp32), P = softmax(S), O = P·V
+  bf16* a = s->buf[3];
+  group_norm(x1, a, 1, P, cm, e->vc.groups, V.ag, V.ab, e->vc.eps, false, s->gn_ws, st);
+  bf16* q = s->ar.get<bf16>((size_t)P * cm);
+  bf16* k = s->ar.get<bf16>((size_t)P * cm);
+  bf16* vt = s->ar.get<bf16>((size_t)P * cm);
+  float* S = s->ar.get<float>((size_t)P * P);
+  bf16* Pm = s->ar.get<bf16>((size_t)P * P);
+  auto lin = [&](const bf16* A, int M, int K, const bf16* Wt, int N, const float* b, void* out, int ldo,
+                 const bf16* res, int bias_row, float alpha, int f32) {
+    GemmDesc g;
+    g.A = A;
+    g.M = M;
+    g.K = K;
+    g.lda = K;
+    g.Bw[0] = Wt;
+    g.N = N;
+    g.ldb = K;
+    g.out = out;
+    g.ldo = ldo;
+    g.bias = b;
+    g.bias_per_row = bias_row;
+    g.res = res;
+    g.ldr = ldo;
+    g.alpha = alpha;
+    g.out_f32 = f32;
+    gemm(g, st);
+  };
+  lin(a, P, cm, V.wq, cm, V.bq, q, cm, nullptr, 0, 1.f, 0);
+  lin(a, P, cm, V.wk, cm, V.bk, k, cm, nullptr, 0, 1.f, 0);
+  lin(V.wv, cm, cm, a, P, V.bv, vt, P, nullptr, 1, 1.f, 0);            // Vᵀ = Wv·aᵀ (+bv per row)
+  lin(q, P, cm, k, P, nullptr, S, P, nullptr, 0, 1.f / sqrtf((float)cm), 1);
+  softmax_rows(S, Pm, P, P, st);
+  bf16* o = s->buf[4];
+  lin(Pm, P, P, vt, cm, nullptr, o, cm, nullptr, 0, 1.f, 0);
+  bf16* x2 = s->buf[1];
+  lin(o, P, cm, V.wo, cm, V.bo, x2, cm, x1, 0, 1.f, 0);
+  head_res(e, s, V.mid1, x2, s->buf[0], s->buf[3], s->buf[4], H, W, st);
+  s->ar.reset(mk);
+}
+
+static int64_t conv_cost(long P, int C, int N) { return std::max<int64_t>(1, (int64_t)2 * P * C * 9 * N / 1000000); }
+
+static void build_items(Engine* e, DecodeState* s) {
+  const VAECfg& c = e->vc;
+  auto& it = s->items;
+  auto& cost = s->cost;
+  it.clear();
+  cost.clear();
+  int H = s->h, W = s->w;
+  it.push_back(VItem{VOP_HEAD});
+  const int cm = c.block_out.back();
+  cost.push_back(conv_cost((long)H * W, cm, cm) * 5 + (int64_t)H * W * H * W * cm * 4 / 1000000);
+  int cur = 0;
+  auto other = [&](std::initializer_list<int> used) {
+    for (int b = 0; b < 5; ++b)
+      if (std::find(used.begin(), used.end(), b) == used.end()) return b;
+    return -1;
+  };
+  int gn_id = 0;
+  for (auto& u : e->V.up) {
+    for (auto& r : u.res) {
+      const int t1 = other({cur});
+      const int t2 = other({cur, t1});
+      const int t3 = other({cur, t1, t2});
+      const int y = other({cur, t1, t2, t3});
+      const int br = band_rows(H);
+      auto push_gn = [&](int src, int dst, const float* gam, const float* bet, int C) {
+        for (int yy = 0; yy < H; yy += br) {
+          VItem v{VOP_GN_STATS, src, dst, 0, gam, C, 0, H, W, yy, std::min(H, yy + br), gn_id, 1};
+          it.push_back(v);
+          cost.push_back(std::max<int64_t>(1, (int64_t)(v.y1 - v.y0) * W * C * 2 / 6000));
+        }
+        for (int yy = 0; yy < H; yy += br) {
+          VItem v{VOP_GN_APPLY, src, dst, 0, gam, C, 0, H, W, yy, std::min(H, yy + br), gn_id, 1};
+          v.p1 = bet;
+          it.push_back(v);
+          cost.push_back(std::max<int64_t>(1, (int64_t)(v.y1 - v.y0) * W * C * 4 / 6000));
+        }
+        ++gn_id;
+      };
+      push_gn(cur, t1, r.n1g, r.n1b, r.cin);
+      for (int yy = 0; yy < H; yy += br) {
+        VItem v{VOP_CONV, t1, t2, -1, &r, r.cin, r.cout, H, W, yy, std::min(H, yy + br), 1, 0};
+        it.push_back(v);
+        cost.push_back(conv_cost((long)(v.y1 - v.y0) * W, r.cin, r.cout));
+      }
+      push_gn(t2, t1, r.n2g, r.n2b, r.cout);
+      int resb = cur;
+      if (r.wsc) {
+        for (int yy = 0; yy < H; yy += br) {
+          VItem v{VOP_SHORTCUT, cur, t3, -1, &r, r.cin, r.cout, H, W, yy, std::min(H, yy + br), 0, 0};
+          it.push_back(v);
+          cost.push_back(std::max<int64_t>(1, conv_cost((long)(v.y1 - v.y0) * W, r.cin, r.cout) / 9));
+        }
+        resb = t3;
+      }
+      for (int yy = 0; yy < H; yy += br) {
+        VItem v{VOP_CONV, t1, y, resb, &r, r.cout, r.cout, H, W, yy, std::min(H, yy + br), 2, 0};
+        it.push_back(v);
+        cost.push_back(conv_cost((long)(v.y1 - v.y0) * W, r.cout, r.cout));
+      }
+      cur = y;
+    }
+    if (u.up) {
+      const int C = u.ch;
+      H *= 2;
+      W *= 2;
+      const int br = band_rows(H);
+      for (int yy = 0; yy < H; yy += br) {
+        VItem v{VOP_UPSAMPLE, cur, 5, -1, nullptr, C, C, H, W, yy, std::min(H, yy + br), 0, 0};
+        it.push_back(v);
+        cost.push_back(std::max<int64_t>(1, (int64_t)(v.y1 - v.y0) * W * C * 3 / 6000));
+      }
+      const int y = other({cur});
+      for (int yy = 0; yy < H; yy += br) {
+        VItem v{VOP_CONV, 5, y, -1, &u, C, C, H, W, yy, std::min(H, yy + br), 3, 0};
+        it.push_back(v);
+        cost.push_back(conv_cost((long)(v.y1 - v.y0) * W, C, C));
+      }
+      cur = y;
+    }
+  }
+  const int C0 = c.block_out[0];
+  const int t1 = other({cur});
+  {
+    const int br = band_rows(H);
+    for (int yy = 0; yy < H; yy += br) {
+      VItem v{VOP_GN_STATS, cur, t1, 0, e->V.nout_g, C0, 0, H, W, yy, std::min(H, yy + br), gn_id, 1};
+      it.push_back(v);
+      cost.push_back(std::max<int64_t>(1, (int64_t)(v.y1 - v.y0) * W * C0 * 2 / 6000));
+    }
+    for (int yy = 0; yy < H; yy += br) {
+      VItem v{VOP_GN_APPLY, cur, t1, 0, e->V.nout_g, C0, 0, H, W, yy, std::min(H, yy + br), gn_id, 1};
+      v.p1 = e->V.nout_b;
+      it.push_back(v);
+      cost.push_back(std::max<int64_t>(1, (int64_t)(v.y1 - v.y0) * W * C0 * 4 / 6000));
+    }
+    ++gn_id;
+    for (int yy = 0; yy < H; yy += br) {
+      VItem v{VOP_CONV, t1, -2, -1, nullptr, C0, 3, H, W, yy, std::min(H, yy + br), 4, 0};
+      it.push_back(v);
+      cost.push_back(conv_cost((long)(v.y1 - v.y0) * W, C0, 16));
+    }
+  }
+  it.push_back(VItem{VOP_FINAL, 0, 0, 0, nullptr, 0, 0, H, W, 0, H, 0, 0});
+  cost.push_back(1);
+}
+
+static void run_item(Engine* e, DecodeState* s, const VItem& v, const float* z, float* image, cudaStream_t st) {
+  const int G = e->vc.groups;
+  switch (v.op) {
+    case VOP_HEAD: run_head(e, s, z, st); break;
+    case VOP_GN_STATS: {
+      const int P = v.H * v.W;
+      gn_stats_range(s->buf[v.a], P, v.C, G, v.y0 * v.W / 128, cdiv((long)v.y1 * v.W, 128), s->gn_ws, st);
+      break;
+    }
+    case VOP_GN_APPLY: {
+      const int P = v.H * v.W;
+      const float* gam = static_cast<const float*>(v.p0);
+      gn_apply_range(s->buf[v.a], s->buf[v.b], P, v.C, G, v.y0 * v.W / 128, cdiv((long)v.y1 * v.W, 128), gam,
+                     static_cast<const float*>(v.p1), e->vc.eps, v.silu != 0, s->gn_ws, st);
+      break;
+    }
+    case VOP_CONV: {
+      const bf16* res = v.c >= 0 ? s->buf[v.c] : nullptr;
+      if (v.gn == 1) {
+        const ResW* r = static_cast<const ResW*>(v.p0);
+        run_conv_band(e, s->buf[v.a], v.H, v.W, v.C, r->w1, v.C2, r->b1, s->buf[v.b], res, v.y0, v.y1, 0, st);
+      } else if (v.gn == 2) {
+        const ResW* r = static_cast<const ResW*>(v.p0);
+        run_conv_band(e, s->buf[v.a], v.H, v.W, v.C, r->w2, v.C2, r->b2, s->buf[v.b], res, v.y0, v.y1, 0, st);
+      } else if (v.gn == 3) {
+        const UpW* u = static_cast<const UpW*>(v.p0);
+        run_conv_band(e, s->buf[v.a], v.H, v.W, v.C, u->wup, v.C2, u->bup, s->buf[v.b], res, v.y0, v.y1, 0, st);
+      } else {
+        GemmDesc d;
+        conv_desc(d, s->buf[v.a], v.H, v.W, v.C, e->V.cout_w, 3, e->V.cout_b, s->img_nhwc, nullptr);
+        d.out_f32 = 1;
+        d.ldo = 3;
+        int wt, ht, bt;
+        conv3_tile_geometry(1, v.H, v.W, &wt, &ht, &bt);
+        const int tx = cdiv(v.W, wt);
+        d.m_tile_begin = (v.y0 / ht) * tx;
+        d.m_tile_count = cdiv(v.y1 - v.y0, ht) * tx;
+        gemm(d, st);
+      }
+      break;
+    }
+    case VOP_SHORTCUT: {
+      const ResW* r = static_cast<const ResW*>(v.p0);
+      GemmDesc d;
+      d.A = s->buf[v.a] + (long)v.y0 * v.W * v.C;
+      d.M = (v.y1 - v.y0) * v.W;
+      d.K = v.C;
+      d.lda = v.C;
+      d.Bw[0] = r->wsc;
+      d.N = v.C2;
+      d.ldb = v.C;
+      d.out = s->buf[v.b] + (long)v.y0 * v.W * v.C2;
+      d.ldo = v.C2;
+      d.bias = r->bsc;
+      gemm(d, st);
+      break;
+    }
+    case VOP_UPSAMPLE: {
+      const int Wi = v.W / 2;
+      upsample2x(s->buf[v.a] + (long)(v.y0 / 2) * Wi * v.C, s->buf[v.b] + (long)v.y0 * v.W * v.C, 1, (v.y1 - v.y0) / 2,
+                 Wi, v.C, st);
+      break;
+    }
+    case VOP_FINAL:
+      nhwc_to_nchw3(s->img_nhwc, 3, (long)v.H * v.W, image, st);
+      break;
+  }
+}
+
+static std::vector<int> chunk_bounds(const std::vector<int64_t>& costs, int c);
+
+static size_t decode_buf_elems(Engine* e, int h, int w) {
+  // max P·C over the tail (incl. the 2x-upsampled tensors) and the head
+  size_t m = (size_t)h * w * 64;
+  int H = h, W = w;
+  const int cm = e->vc.block_out.back();
+  m = std::max(m, (size_t)H * W * cm);
+  for (auto& u : e->V.up) {
+    for (auto& r : u.res) m = std::max(m, (size_t)H * W * std::max(r.cin, r.cout));
+    if (u.up) {
+      H *= 2;
+      W *= 2;
+      m = std::max(m, (size_t)H * W * u.ch);
+    }
+  }
+  return m;
+}
+
+static DecodeState* new_decode(Engine* e, int h, int w) {
+  auto* s = new DecodeState();
+  s->h = h;
+  s->w = w;
+  s->buf_elems = decode_buf_elems(e, h, w);
+  const size_t P = (size_t)h * w;
+  const int cm = e->vc.block_out.back();
+  const size_t head = P * 64 * 2 * 2 + P * cm * 2 * 3 + P * P * 6 + ((size_t)8 << 20);
+  const size_t img = (size_t)64 * P * 3 * 4;
+  const size_t gnb = gn_workspace_bytes(1, (int)(64 * P), 64);
+  s->ar.init(NBUF * (s->buf_elems * 2 + 4096) + head + img + gnb + ((size_t)16 << 20));
+  for (int i = 0; i < NBUF; ++i) s->buf[i] = s->ar.get<bf16>(s->buf_elems);
+  s->img_nhwc = s->ar.get<float>(64 * P * 3);
+  s->gn_ws = s->ar.alloc(gnb);
+  build_items(e, s);
+  return s;
+}
+
+void destroy_decode(Engine* e, DecodeState* d) {
+  (void)e;
+  d->ar.release();
+  delete d;
+}
+
+void vae_decode_chunk(Engine* e, const float* z, int h, int w, int n_chunks, int chunk, DecodeState** state,
+                      float* image, cudaStream_t st) {
+  DecodeState* s = *state;
+  if (chunk == 0) {
+    if (s) throw std::logic_error("chunk 0 needs *state == NULL");
+    {
+      std::lock_guard<std::mutex> g(e->dmu);
+      for (size_t i = 0; i < e->free_decodes.size(); ++i)
+        if (e->free_decodes[i]->h == h && e->free_decodes[i]->w == w) {
+          s = e->free_decodes[i];
+          e->free_decodes.erase(e->free_decodes.begin() + i);
+          break;
+        }
+    }
+    if (!s) s = new_decode(e, h, w);
+    s->n_chunks = n_chunks;
+    s->next_chunk = 0;
+    s->bounds = chunk_bounds(s->cost, n_chunks);
+    *state = s;
+  }
+  if (!s || chunk != s->next_chunk || n_chunks != s->n_chunks || h != s->h || w != s->w)
+    throw std::logic_error("VAE chunk out of order");
+  const int nb = (int)s->bounds.size() - 1;
+  if (chunk < nb)
+    for (int i = s->bounds[chunk]; i < s->bounds[chunk + 1]; ++i) run_item(e, s, s->items[i], z, image, st);
+  s->next_chunk++;
+  if (s->next_chunk == n_chunks) {
+    std::lock_guard<std::mutex> g(e->dmu);
+    e->free_decodes.push_back(s);
+    *state = nullptr;
+  }
+}
+
+// min-max contiguous partition, boundaries placed as early as possible (oracle/vae.py chunk_ranges
+// is the independent reference; the C-ABI sd_chunk_ranges exposes this function for the tests)
+static int need(const std::vector<int64_t>& pre, int s, int n, int64_t cap) {
+  if (s >= n) return 0;
+  int cnt = 1, start = s;
+  for (int k = s + 1; k <= n; ++k)
+    if (pre[k] - pre[start] > cap) {
+      start = k - 1;
+      ++cnt;
+    }
+  return cnt;
+}
+
+static std::vector<int> chunk_bounds(const std::vector<int64_t>& costs, int c) {
+  const int n = (int)costs.size();
+  c = std::max(1, std::min(c, n));
+  std::vector<int64_t> pre(n + 1, 0);
+  int64_t mx = 0;
+  for (int i = 0; i < n; ++i) {
+    pre[i + 1] = pre[i] + costs[i];
+    mx = std::max(mx, costs[i]);
+  }
+  int64_t lo = mx, hi = pre[n];
+  while (lo < hi) {
+    const int64_t mid = lo + (hi - lo) / 2;
+    if (need(pre, 0, n, mid) <= c)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  std::vector<int> b{0};
+  for (int j = 1; j < c; ++j) {
+    const int s = b.back();
+    int e = s + 1;
+    while (!(pre[e] - pre[s] <= lo && need(pre, e, n, lo) <= c - j && n - e >= c - j)) ++e;
+    b.push_back(e);
+  }
+  b.push_back(n);
+  return b;
+}
+
+std::vector<int> chunk_ranges_api(const std::vector<int64_t>& costs, int c) { return chunk_bounds(costs, c); }
+
+}  // namespace sd

@@ -1,0 +1,104 @@
+"""Python wrapper around the C-ABI engine for torch-allocated buffers (marshalling only).
+
+torch provides device memory and streams; every computation happens in libsynerdiff.so.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import binding as B
+
+
+def _stream(s):
+    if s is None:
+        s = torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+class Engine:
+    def __init__(self, model="tiny", sampler="ddim", max_latent_hw=None, b_max=8, c_max=16, weight_seed=0,
+                 device=0):
+        m = {"tiny": B.SD_MODEL_TINY, "sd15": B.SD_MODEL_SD15}[model]
+        sm = {"ddim": B.SD_SAMPLER_DDIM, "euler": B.SD_SAMPLER_EULER}[sampler]
+        if max_latent_hw is None:
+            max_latent_hw = 8 if model == "tiny" else 64
+        cfg = B.EngineConfig(m, 0, sm, max_latent_hw, b_max, c_max, weight_seed)
+        h = C.c_void_p()
+        B.call("sd_engine_create", C.byref(cfg), device, C.byref(h))
+        self.h = h
+        self.model = model
+        self.sampler = sampler
+        self.device = device
+        self.ctx_len, self.ctx_dim = (8, 32) if model == "tiny" else (77, 768)
+
+    def close(self):
+        if self.h:
+            B.lib().sd_engine_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def launch_count(self):
+        v = C.c_int64()
+        B.call("sd_engine_launch_count", self.h, C.byref(v))
+        return v.value
+
+    def profile(self, enable: bool):
+        B.call("sd_engine_profile", self.h, 1 if enable else 0)
+
+    def profile_read(self, cls: int):
+        """(ms, launches, work) for kernel class cls (0 conv, 1 gemm, 2 attention, 3 GN, 4 LN)."""
+        ms, n, w = C.c_double(), C.c_int64(), C.c_double()
+        B.call("sd_engine_profile_read", self.h, cls, C.byref(ms), C.byref(n), C.byref(w))
+        return ms.value, n.value, w.value
+
+    def set_uncond(self, emb: torch.Tensor, stream=None):
+        emb = emb.to(device=f"cuda:{self.device}", dtype=torch.float32).contiguous()
+        B.call("sd_ctx_set_uncond", self.h, B._p(emb), emb.shape[0], emb.shape[1], _stream(stream))
+        torch.cuda.current_stream().synchronize() if stream is None else stream.synchronize()
+
+    def register(self, emb: torch.Tensor, stream=None) -> int:
+        emb = emb.to(device=f"cuda:{self.device}", dtype=torch.float32).contiguous()
+        slot = C.c_int32()
+        B.call("sd_ctx_register", self.h, B._p(emb), emb.shape[0], emb.shape[1], C.byref(slot), _stream(stream))
+        (torch.cuda.current_stream() if stream is None else stream).synchronize()
+        return slot.value
+
+    def release(self, slot: int):
+        B.call("sd_ctx_release", self.h, slot)
+
+    def init_sigma(self, n_steps: int) -> float:
+        v = C.c_float()
+        B.call("sd_sampler_init_sigma", self.h, n_steps, C.byref(v))
+        return v.value
+
+    def step(self, latents, steps, n_steps, has_uncond, guidance, slots, stream=None):
+        """One sd_step_batch call. latents: list of cuda fp32 [4,h,w] tensors (updated in place)."""
+        n = len(latents)
+        h, w = latents[0].shape[-2:]
+        ptrs = (C.c_void_p * n)(*[t.data_ptr() for t in latents])
+        b = B.Batch(n, h, w, C.cast(ptrs, C.POINTER(C.c_void_p)),
+                    (C.c_int32 * n)(*steps), (C.c_int32 * n)(*n_steps), (C.c_uint8 * n)(*[int(x) for x in has_uncond]),
+                    (C.c_float * n)(*guidance), (C.c_int32 * n)(*slots))
+        B.call("sd_step_batch", self.h, C.byref(b), _stream(stream))
+
+    def decode(self, latent: torch.Tensor, n_chunks=1, image=None, stream=None):
+        """Whole or chunked VAE decode of one fp32 [4,h,w] latent → fp32 [3,8h,8w]."""
+        h, w = latent.shape[-2:]
+        if image is None:
+            image = torch.empty(3, 8 * h, 8 * w, device=latent.device, dtype=torch.float32)
+        st = C.c_void_p()
+        for j in range(n_chunks):
+            self.decode_chunk(latent, n_chunks, j, st, image, stream)
+        return image
+
+    def decode_chunk(self, latent, n_chunks, chunk, state: C.c_void_p, image, stream=None):
+        h, w = latent.shape[-2:]
+        B.call("sd_vae_decode_chunked", self.h, B._p(latent), h, w, n_chunks, chunk, C.byref(state), B._p(image),
+               _stream(stream))

@@ -1,0 +1,97 @@
+"""Kernel-level numerics on the B200: each sm_100a kernel vs a plain PyTorch fp64 CPU reference of the
+same op on the same bf16-rounded inputs (op-level checks; end-to-end parity vs the oracle is in
+test_gpu_parity.py)."""
+import pytest
+import torch
+import torch.nn.functional as F
+
+pytestmark = pytest.mark.gpu
+
+from paper_2605_08835_b200 import binding as B  # noqa: E402
+
+
+def rel(a, b):
+    return float((a.double() - b.double()).norm() / b.double().norm().clamp_min(1e-30))
+
+
+def bf(x):
+    return x.to(torch.bfloat16)
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 64, 64), (300, 320, 320), (1000, 1280, 640), (77, 256, 768),
+                                   (4096, 160, 2880), (200, 128, 32), (129, 16, 64), (513, 4, 128)])
+@pytest.mark.parametrize("out_f32", [0, 1])
+def test_gemm_dense(M, N, K, out_f32):
+    g = torch.Generator().manual_seed(M * 7 + N + K)
+    A = torch.randn(M, K, generator=g)
+    Wt = torch.randn(N, K, generator=g) / K ** 0.5
+    bias = torch.randn(N, generator=g)
+    ref = bf(A).double() @ bf(Wt).double().T + bias.double()
+    Ad, Wd = bf(A).cuda(), bf(Wt).cuda()
+    D = torch.empty(M, N, device="cuda", dtype=torch.float32 if out_f32 else torch.bfloat16)
+    B.debug_gemm(Ad, Wd, bias.cuda(), D, M, N, K, out_f32=out_f32)
+    torch.cuda.synchronize()
+    assert rel(D.cpu(), ref) < (1e-5 if out_f32 else 6e-3)
+
+
+def test_gemm_geglu_and_silu():
+    M, N, K = 260, 512, 128
+    g = torch.Generator().manual_seed(5)
+    A, Wt, bias = torch.randn(M, K, generator=g), torch.randn(N, K, generator=g) / 11, torch.randn(N, generator=g)
+    full = bf(A).double() @ bf(Wt).double().T + bias.double()
+    # GEGLU: per 128-column group, columns [0,64) value and [64,128) gate
+    v = torch.cat([full[:, 128 * j:128 * j + 64] for j in range(N // 128)], 1)
+    gt = torch.cat([full[:, 128 * j + 64:128 * j + 128] for j in range(N // 128)], 1)
+    ref = v * F.gelu(gt)
+    D = torch.empty(M, N // 2, device="cuda", dtype=torch.bfloat16)
+    B.debug_gemm(bf(A).cuda(), bf(Wt).cuda(), bias.cuda(), D, M, N, K, act=B.ACT_GEGLU)
+    S = torch.empty(M, N, device="cuda", dtype=torch.float32)
+    B.debug_gemm(bf(A).cuda(), bf(Wt).cuda(), bias.cuda(), S, M, N, K, out_f32=1, act=B.ACT_SILU)
+    torch.cuda.synchronize()
+    assert rel(D.cpu(), ref) < 6e-3
+    assert rel(S.cpu(), F.silu(full)) < 1e-5
+
+
+def _conv_ref(x, w, b, temb, res):
+    y = F.conv2d(x.permute(0, 3, 1, 2).double(), w.double(), b.double(), padding=1)
+    if temb is not None:
+        y = y + temb.double()[:, :, None, None]
+    y = y.permute(0, 2, 3, 1)
+    if res is not None:
+        y = y + res.double()
+    return y
+
+
+def _to_dev_w(w):            # [O][I][3][3] → [O][9][I] bf16
+    return bf(w).permute(0, 2, 3, 1).reshape(w.shape[0], 9, w.shape[1]).contiguous().cuda()
+
+
+@pytest.mark.parametrize("nb,h,w,cin,cout", [(2, 16, 16, 64, 320), (3, 8, 8, 320, 640), (16, 8, 8, 1280, 1280),
+                                             (1, 64, 64, 128, 128), (2, 12, 12, 32, 64), (4, 4, 4, 64, 128),
+                                             (2, 24, 40, 64, 256), (1, 9, 20, 8, 64)])
+def test_conv3x3(nb, h, w, cin, cout):
+    g = torch.Generator().manual_seed(nb * 1000 + h * 10 + cin)
+    x = bf(torch.randn(nb, h, w, cin, generator=g))
+    wt = bf(torch.randn(cout, cin, 3, 3, generator=g) / (9 * cin) ** 0.5)
+    b = torch.randn(cout, generator=g)
+    temb = torch.randn(nb, cout, generator=g)
+    res = bf(torch.randn(nb, h, w, cout, generator=g))
+    ref = _conv_ref(x.float(), wt.float(), b, temb, res.float())
+    y = torch.empty(nb, h, w, cout, device="cuda", dtype=torch.bfloat16)
+    B.debug_conv3x3(x.cuda(), cin, None, 0, _to_dev_w(wt), None, b.cuda(), temb.cuda(), res.cuda(), y, nb, h, w, cout)
+    torch.cuda.synchronize()
+    assert rel(y.cpu(), ref) < 6e-3
+
+
+def test_conv3x3_concat():
+    nb, h, w, c1, c2, cout = 2, 16, 16, 320, 640, 320
+    g = torch.Generator().manual_seed(9)
+    x1, x2 = bf(torch.randn(nb, h, w, c1, generator=g)), bf(torch.randn(nb, h, w, c2, generator=g))
+    wt = bf(torch.randn(cout, c1 + c2, 3, 3, generator=g) / (9 * (c1 + c2)) ** 0.5)
+    b = torch.randn(cout, generator=g)
+    ref = _conv_ref(torch.cat([x1, x2], -1).float(), wt.float(), b, None, None)
+    y = torch.empty(nb, h, w, cout, device="cuda", dtype=torch.bfloat16)
+    B.debug_conv3x3(x1.cuda(), c1, x2.cuda(), c2, _to_dev_w(wt[:, :c1]), _to_dev_w(wt[:, c1:]), b.cuda(), None, None,
+                    y, nb, h, w, cout)
+    torch.cuda.synchronize()
+    assert rel(y.cpu(), ref) < 6e-3

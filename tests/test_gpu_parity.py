@@ -1,0 +1,192 @@
+"""End-to-end parity of the CUDA path (through the C ABI) against the NumPy oracle on the same seeded
+inputs (north star tolerances: bf16 rel-L2 ≤ 2e-2 on latents and images).
+
+The oracle uses the bf16-rounded weights the GPU stores (R20) and the bf16-rounded text embedding
+(the GPU computes the text K/V from a bf16 copy); everything else in the oracle is fp32."""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import configs, pipeline, sampling, unet, vae
+
+pytestmark = pytest.mark.gpu
+
+from paper_2605_08835_b200.engine import Engine  # noqa: E402
+
+TOL = 2e-2
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    eng = Engine("tiny", max_latent_hw=16, b_max=4)
+    ctx_u = synth.uncond_embedding(0, 8, 32)
+    eng.set_uncond(torch.from_numpy(ctx_u))
+    P = configs.unet_params(configs.TINY_UNET, 0, np.float32, bf16_weights=True)
+    V = configs.vae_params(configs.TINY_VAE, 0, np.float32, bf16_weights=True)
+    yield eng, P, V, synth.bf16_round(ctx_u)
+    eng.close()
+
+
+def _cfg_gain(P, x, t, ctx, ctx_u, g):
+    """Error-propagation factor of the CFG combine for one request: ε̃ = (1−g)ε_u + g ε_c, so a
+    relative kernel error δ on ε_c and ε_u becomes ≤ κ·δ on ε̃ with
+    κ = (|1−g|·‖ε_u‖ + g·‖ε_c‖) / ‖ε̃‖ (tolerance derivation)."""
+    e = unet.forward(P, configs.TINY_UNET, np.stack([x, x]), np.array([t, t]), np.stack([ctx, ctx_u]))
+    ec, eu = e[0], e[1]
+    et = eu + np.float32(g) * (ec - eu)
+    return (abs(1 - g) * np.linalg.norm(eu) + g * np.linalg.norm(ec)) / np.linalg.norm(et)
+
+
+def _run_tiny(eng, P, ctx_u, sampler, schedule, g=(7.5, 5.0)):
+    """schedule[s] = per-request has_uncond at step s; both requests 4 steps. Returns the final
+    rel-L2 vs the free-running oracle and, per step, the teacher-forced ε-part error divided by
+    its allowed bound (TOL for cond-only steps, TOL·κ for CFG steps)."""
+    n = len(g)
+    ctx = [synth.text_embedding(1, i, 8, 32) for i in range(n)]
+    slots = [eng.register(torch.from_numpy(c)) for c in ctx]
+    sig = sampling.init_sigma(sampler, 4)
+    assert abs(eng.init_sigma(4) - sig) < 1e-6
+    x0 = [synth.initial_noise(1, i, 8, 8) * np.float32(sig) for i in range(n)]
+    lat = [torch.from_numpy(x).cuda() for x in x0]
+    xo = [x.copy() for x in x0]
+    worst = 0.0
+    for s in range(4):
+        hu = schedule[s]
+        xg = [t.cpu().numpy() for t in lat]
+        eng.step(lat, [s] * n, [4] * n, hu, list(g), slots)
+        torch.cuda.synchronize()
+        cb = [synth.bf16_round(c) for c in ctx]
+        reqs_tf = [dict(x=xg[i], ctx=cb[i], step=s, n_steps=4, has_uncond=bool(hu[i]), g=g[i]) for i in range(n)]
+        tf = pipeline.step_batch(P, configs.TINY_UNET, reqs_tf, ctx_u, sampler)
+        a, ap = sampling.ddim_alphas(4, s)
+        A = np.sqrt(ap / a) if sampler == "ddim" else 1.0
+        t = int(sampling.timesteps(4)[s])
+        for i in range(n):
+            got = lat[i].cpu().numpy()
+            r_eps = rel(got - A * xg[i], tf[i] - A * xg[i])        # ε-part of the update (R21)
+            kappa = _cfg_gain(P, xg[i] * np.float32(sampling.c_in(sampler, 4, s)), t, cb[i], ctx_u, g[i]) \
+                if hu[i] else 1.0
+            print(f"  step {s} req {i} cfg={hu[i]} eps-part rel {r_eps:.3e} (kappa {kappa:.2f}) x rel "
+                  f"{rel(got, tf[i]):.3e}")
+            worst = max(worst, r_eps / (TOL * kappa), rel(got, tf[i]) / TOL)
+        reqs = [dict(x=xo[i], ctx=cb[i], step=s, n_steps=4, has_uncond=bool(hu[i]), g=g[i]) for i in range(n)]
+        xo = pipeline.step_batch(P, configs.TINY_UNET, reqs, ctx_u, sampler)
+    final = max(rel(lat[i].cpu().numpy(), xo[i]) for i in range(n))
+    for sl in slots:
+        eng.release(sl)
+    return final, worst, lat, xo
+
+
+@pytest.mark.parametrize("sampler", ["ddim"])
+def test_tiny_unet_cfg_on_off(tiny, sampler):
+    eng, P, V, ctx_u = tiny
+    sched = [[1, 1], [1, 0], [0, 1], [0, 0]]     # CFG on / Skip-CFG mixes (CFG#1)
+    final, worst, lat, xo = _run_tiny(eng, P, ctx_u, sampler, sched)
+    print(f"tiny final rel-L2 {final:.3e}, worst per-step error / bound {worst:.3f}")
+    assert final <= TOL and worst <= 1.0
+
+
+def test_tiny_batch_invariance(tiny):
+    """I5 on the GPU: a request's update in a batch equals its update alone (bitwise)."""
+    eng, P, V, ctx_u = tiny
+    ctx = [synth.text_embedding(4, i, 8, 32) for i in range(3)]
+    slots = [eng.register(torch.from_numpy(c)) for c in ctx]
+    x0 = [synth.initial_noise(4, i, 8, 8) for i in range(3)]
+    lat = [torch.from_numpy(x).cuda() for x in x0]
+    eng.step(lat, [0, 1, 2], [4, 4, 4], [1, 0, 1], [7.5, 7.5, 3.0], slots)
+    alone = []
+    for i in range(3):
+        t = [torch.from_numpy(x0[i]).cuda()]
+        eng.step(t, [[0, 1, 2][i]], [4], [[1, 0, 1][i]], [[7.5, 7.5, 3.0][i]], [slots[i]])
+        alone.append(t[0])
+    torch.cuda.synchronize()
+    for i in range(3):
+        assert torch.equal(lat[i], alone[i]), i
+    for s in slots:
+        eng.release(s)
+
+
+def test_tiny_vae_whole_and_chunked(tiny):
+    eng, P, V, ctx_u = tiny
+    z = synth.initial_noise(2, 0, 8, 8)
+    ref = vae.decode(V, configs.TINY_VAE, z[None].astype(np.float32))[0]
+    zt = torch.from_numpy(z).cuda()
+    whole = eng.decode(zt, 1)
+    torch.cuda.synchronize()
+    r = rel(whole.cpu().numpy(), ref)
+    print(f"tiny VAE rel-L2 {r:.3e}")
+    assert r <= TOL
+    for c in (2, 3, 5):
+        ch = eng.decode(zt, c)
+        torch.cuda.synchronize()
+        assert torch.equal(ch, whole), c                 # I6 on the GPU: bitwise
+
+
+def test_vae_chunk_order_enforced(tiny):
+    eng, *_ = tiny
+    from paper_2605_08835_b200 import binding as B
+    z = torch.zeros(4, 8, 8, device="cuda")
+    img = torch.empty(3, 64, 64, device="cuda")
+    st = C.c_void_p()
+    with pytest.raises(B.SDError) as ei:
+        eng.decode_chunk(z, 3, 1, st, img)
+    assert ei.value.status in (B.SD_E_STATE, B.SD_E_INVAL)
+
+
+@pytest.fixture(scope="module")
+def sd15():
+    eng = Engine("sd15", max_latent_hw=64, b_max=8)
+    ctx_u = synth.uncond_embedding(0, 77, 768)
+    eng.set_uncond(torch.from_numpy(ctx_u))
+    yield eng, synth.bf16_round(ctx_u)
+    eng.close()
+
+
+def test_sd15_step_parity(sd15):
+    """One ragged SD-1.5 512² step (3 requests, 5 rows: two CFG rows + one Skip-CFG) vs the oracle."""
+    eng, ctx_u = sd15
+    P = configs.unet_params(configs.SD15_UNET, 0, np.float32, bf16_weights=True)
+    ctx = [synth.text_embedding(1, i, 77, 768) for i in range(3)]
+    slots = [eng.register(torch.from_numpy(c)) for c in ctx]
+    steps, hu, g = [0, 20, 45], [1, 0, 1], [7.5, 7.5, 4.0]
+    x0 = [synth.initial_noise(1, i, 64, 64) for i in range(3)]
+    lat = [torch.from_numpy(x).cuda() for x in x0]
+    eng.step(lat, steps, [50] * 3, hu, g, slots)
+    torch.cuda.synchronize()
+    reqs = [dict(x=x0[i], ctx=synth.bf16_round(ctx[i]), step=steps[i], n_steps=50, has_uncond=bool(hu[i]), g=g[i])
+            for i in range(3)]
+    ref = pipeline.step_batch(P, configs.SD15_UNET, reqs, ctx_u, "ddim")
+    for i in range(3):
+        a, ap = sampling.ddim_alphas(50, steps[i])
+        A = np.sqrt(ap / a)
+        got, exp = lat[i].cpu().numpy(), ref[i]
+        r_x = rel(got, exp)
+        r_eps = rel(got - A * x0[i], exp - A * x0[i])      # ε-part (R21)
+        print(f"sd15 req {i}: x rel-L2 {r_x:.3e}, eps-part rel-L2 {r_eps:.3e}")
+        assert r_x <= TOL and r_eps <= TOL
+    for s in slots:
+        eng.release(s)
+
+
+def test_sd15_vae_parity(sd15):
+    eng, _ = sd15
+    V = configs.vae_params(configs.SD_VAE, 0, np.float32, bf16_weights=True)
+    z = synth.initial_noise(3, 0, 64, 64)
+    ref = vae.decode(V, configs.SD_VAE, z[None])[0]
+    zt = torch.from_numpy(z).cuda()
+    whole = eng.decode(zt, 1)
+    ch = eng.decode(zt, 4)
+    torch.cuda.synchronize()
+    r = rel(whole.cpu().numpy(), ref)
+    print(f"sd VAE 512² rel-L2 {r:.3e}")
+    assert r <= TOL
+    assert torch.equal(ch, whole)
