@@ -151,6 +151,52 @@ sd_status sd_controller_free(sd_controller* c);
 /* Min-max partition of the ordered VAE work list into c chunks (R7): boundaries[0..c]. */
 sd_status sd_chunk_ranges(const int64_t* costs, int32_t n_items, int32_t c, int32_t* boundaries_out);
 
+/* ---- serving: the paper's problem statement (P:289 Problem P, P:297 E2E = V_i - A_i) ----------
+ * Continuous batching with step-level refill, the threshold-aware plan per window
+ * (Eq. 3, Alg. 1 / exact DP), Skip-CFG and VAE chunking as planned, and the feedback
+ * controller. Semantics: SURVEY §8(c) steps 1-5, DESIGN.md §2 (R6-R17). */
+typedef struct {
+  int32_t b_max;                /* max UNet batch (8)                                     */
+  int32_t a_num, a_den;         /* throughput slack alpha (1/10)                          */
+  int32_t dp_mode;              /* 0 exact, 1 Alg. 1 verbatim                                    */
+  int32_t c_star;               /* offline chunk granularity c* (Eq. 1)                          */
+  sd_controller_config ctl;     /* controller (R15); ctl.c_max = C_max                           */
+  const sd_table* table;        /* tau/delta table for c = 1..C_max (owned by the caller)        */
+  int32_t latent_hw;            /* GPU mode: one resolution per server (R22)                     */
+  uint64_t trace_seed;          /* GPU mode: initial noise z ~ N(0,1) keyed by (trace_seed, id)  */
+} sd_serve_config;
+typedef struct {
+  uint64_t id;
+  int64_t arrival_us;           /* A_i, µs since sd_serve_start; not admitted before it          */
+  int32_t n_steps;              /* n_i                                                           */
+  float guidance;               /* g_i                                                           */
+  const float* text_emb_host;   /* fp32 [emb_len][emb_dim], copied at submit                     */
+  int32_t emb_len, emb_dim;
+} sd_request;
+typedef struct {
+  uint64_t id;
+  int64_t arrival_us, denoise_done_us, decode_done_us;  /* A_i, U_i, V_i (µs)                     */
+  int32_t n_skipped, h, w;      /* Skip-CFG steps taken; image is [3][h][w]                      */
+  const float* image_host;      /* engine-owned pinned buffer, valid until sd_release(id)       */
+} sd_completion;
+/* GPU server: a thread per engine runs the loop; UNet rounds on a high-priority stream, VAE
+ * chunks on a low-priority stream. */
+sd_status sd_serve_start(sd_engine* e, const sd_serve_config* cfg);
+sd_status sd_submit(sd_engine* e, const sd_request* r);    /* thread-safe; copies the embedding */
+sd_status sd_poll(sd_engine* e, sd_completion* out, int32_t max, int32_t* n_out, int32_t timeout_ms);
+sd_status sd_release(sd_engine* e, uint64_t id);           /* frees the completion's image        */
+sd_status sd_serve_stop(sd_engine* e);                     /* drains nothing; stops the thread    */
+/* loads = int32 [P][4] {waiting, decode-pending, active, completed} all-gathered over ranks (C1);
+ * the controller then sums `waiting` over ranks. sd_get_load returns this rank's 4 counters. */
+sd_status sd_set_global_load(sd_engine* e, const int32_t* loads, int32_t P, uint64_t epoch);
+sd_status sd_get_load(sd_engine* e, int32_t* out4);
+/* Virtual-clock twin of the loop (no GPU): round durations from the table. Fills U_i, V_i and
+ * the number of Skip-CFG steps per request, and the number of windows. Bit-exact with
+ * oracle/serving.py. */
+sd_status sd_serve_simulate(const sd_serve_config* cfg, const sd_table* t, int32_t n, const uint64_t* ids,
+                            const int64_t* arrival_us, const int32_t* n_steps, int64_t* U_out, int64_t* V_out,
+                            int32_t* n_skips_out, int32_t* windows_out);
+
 /* ---- test-only exports (same library): single kernels on caller-owned device buffers --------- */
 /* D[M][N] = A[M][K] · B[N][K]^T + bias[N] (bf16 in, fp32 accumulate, bf16 or fp32 out). */
 sd_status sd_debug_gemm(const void* A, const void* B, const float* bias, void* D, int32_t M, int32_t N, int32_t K,

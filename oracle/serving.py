@@ -1,0 +1,106 @@
+"""Continuous-batching serving semantics on a virtual clock (ORACLE — test infrastructure only).
+
+The plain algorithm of SURVEY.md §8(c) steps 1-5 (PAPER.md:66 step-level scheduling and refill;
+:289-307 Problem P, threshold-aware plan, controller; :262 Eq. 2 final-round early release),
+with round durations taken from the τ/δ table instead of a GPU (SPEC.md's simulator idea).
+The C++ serving loop in virtual-clock mode must reproduce every decision and timestamp bit-exactly.
+
+Per window:
+  1. admit arrived requests (A_i ≤ now) FCFS by (A_i, id) until the batch holds B_max (R16);
+  2. M = |batch|, decode-pending D sorted by (A_i, id), N = min(|D|, B_max); with the controller's
+     level f: s_min_r = ⌈f·n_r⌉, K = #{r : s_r ≥ s_min_r} (R6);
+  3. N = 0 → one round (M, 0, 0) from the c = 1 table (R8); else plan (S, E) at the current c
+     (R10, R11, R13, R14) and run every stage as c rounds (R9);
+  4. a stage (m, n, k) lasts τ^c(m,n,k) split into c rounds (⌊τ/c⌋ each, the remainder in the last);
+     each of its UNet tasks takes one step per round (its k skip tasks without the uncond row);
+     a task reaching n_r stamps U_r at that round's end and becomes decode-pending; each of the
+     stage's decodes completes at stage start + δ^c(m,n,k) (Eq. 2) and stamps V_r;
+  5. the controller observes (now, waiting queue) after the window (R15).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+from . import controller as ctl
+from . import sched
+
+
+@dataclass
+class Task:
+    id: int
+    A: int
+    n: int
+    g: float = 7.5
+    s: int = 0
+    U: int | None = None
+    V: int | None = None
+    skips: list = field(default_factory=list)
+
+
+def simulate(trace, tables, b_max=8, a_num=1, a_den=10, mode="exact", c_star=1, c_max=4, ctl_kw=None,
+             log=None):
+    """trace: [(id, arrival_us, n_steps)], tables: {c: {(m,n,k): (tau_us, delta_us)}}.
+    Returns {id: Task}. `log` (list) receives one dict per window."""
+    pending = sorted((Task(i, a, n) for i, a, n in trace), key=lambda t: (t.A, t.id))
+    pi = 0
+    batch, dec, done = [], [], {}
+    now = 0
+    C = ctl.Controller(c_star=c_star, c_max=c_max, **(ctl_kw or {}))
+    while pi < len(pending) or batch or dec:
+        while pi < len(pending) and pending[pi].A <= now and len(batch) < b_max:
+            batch.append(pending[pi])
+            pi += 1
+        if not batch and not dec:
+            now = pending[pi].A
+            continue
+        level, c = C.level, C.c
+        f = ctl.LEVELS[level]
+        M = len(batch)
+        dq = sorted(dec, key=lambda t: (t.A, t.id))[:b_max]
+        N = len(dq)
+        elig = [t.s >= ctl.s_min(f, t.n) for t in batch]
+        K = sum(elig)
+        if N == 0:
+            stages, tc, rounds = ((M, 0, 0),), 1, 1
+        else:
+            stages = sched.plan_window(tables[c], M, N, K, a_num, a_den, mode)
+            tc, rounds = c, c
+        tab = tables[tc]
+        mapping = sched.map_tasks(stages, [(t.id, t.s, t.n, e) for t, e in zip(batch, elig)],
+                                  [(t.id, t.A) for t in dq])
+        by_id = {t.id: t for t in batch + dq}
+        if log is not None:
+            log.append(dict(now=now, M=M, N=N, K=K, level=level, c=c, stages=tuple(stages)))
+        for (m, n, k), (u_ids, skip_ids, d_ids) in zip(stages, mapping):
+            tau, delta = tab[(m, n, k)]
+            t0 = now
+            per, rem = divmod(tau, rounds)
+            for rho in range(rounds):
+                now += per + (rem if rho == rounds - 1 else 0)
+                for uid in u_ids:
+                    t = by_id[uid]
+                    if t.s >= t.n:
+                        continue
+                    if uid in skip_ids:
+                        t.skips.append(t.s)
+                    t.s += 1
+                    if t.s == t.n:
+                        t.U = now
+                        batch.remove(t)
+                        dec.append(t)
+            for did in d_ids:
+                t = by_id[did]
+                t.V = t0 + delta
+                dec.remove(t)
+                done[t.id] = t
+        waiting = sum(1 for t in pending[pi:] if t.A <= now)
+        C.decide(now, waiting)
+    return done
+
+
+def metrics(done):
+    """R18: throughput = completed / (last V − first A); mean E2E; P99 by ceil rank."""
+    e2e = [t.V - t.A for t in done.values()]
+    span = max(t.V for t in done.values()) - min(t.A for t in done.values())
+    return dict(n=len(e2e), throughput_per_s=len(e2e) / (span / 1e6) if span > 0 else 0.0,
+                mean_e2e_us=sum(e2e) / len(e2e), p99_e2e_us=sched.p99(e2e))

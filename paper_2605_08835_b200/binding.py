@@ -43,6 +43,23 @@ class ControllerConfig(C.Structure):
                 ("up_num", C.c_int32), ("up_den", C.c_int32), ("down_num", C.c_int32), ("down_den", C.c_int32)]
 
 
+class ServeConfig(C.Structure):
+    _fields_ = [("b_max", C.c_int32), ("a_num", C.c_int32), ("a_den", C.c_int32), ("dp_mode", C.c_int32),
+                ("c_star", C.c_int32), ("ctl", ControllerConfig), ("table", C.c_void_p), ("latent_hw", C.c_int32),
+                ("trace_seed", C.c_uint64)]
+
+
+class Request(C.Structure):
+    _fields_ = [("id", C.c_uint64), ("arrival_us", C.c_int64), ("n_steps", C.c_int32), ("guidance", C.c_float),
+                ("text_emb_host", C.c_void_p), ("emb_len", C.c_int32), ("emb_dim", C.c_int32)]
+
+
+class Completion(C.Structure):
+    _fields_ = [("id", C.c_uint64), ("arrival_us", C.c_int64), ("denoise_done_us", C.c_int64),
+                ("decode_done_us", C.c_int64), ("n_skipped", C.c_int32), ("h", C.c_int32), ("w", C.c_int32),
+                ("image_host", C.c_void_p)]
+
+
 class Directive(C.Structure):
     _fields_ = [("level", C.c_int32), ("c", C.c_int32), ("changed", C.c_int32)]
 
@@ -76,6 +93,14 @@ SIGNATURES = {
     "sd_controller_decide": [P, I64, I32, C.POINTER(Directive)],
     "sd_controller_free": [P],
     "sd_chunk_ranges": [PI64, I32, I32, PI32],
+    "sd_serve_start": [P, C.POINTER(ServeConfig)],
+    "sd_submit": [P, C.POINTER(Request)],
+    "sd_poll": [P, C.POINTER(Completion), I32, PI32, I32],
+    "sd_release": [P, C.c_uint64],
+    "sd_serve_stop": [P],
+    "sd_set_global_load": [P, PI32, I32, C.c_uint64],
+    "sd_get_load": [P, PI32],
+    "sd_serve_simulate": [C.POINTER(ServeConfig), P, I32, C.POINTER(C.c_uint64), PI64, PI32, PI64, PI64, PI32, PI32],
     "sd_debug_gemm": [P, P, P, P, I32, I32, I32, I32, I32, P],
     "sd_debug_conv3x3": [P, I32, P, I32, P, P, P, P, P, P, I32, I32, I32, I32, P],
 }

@@ -4,9 +4,6 @@
 
 using namespace sd;
 
-struct sd_engine {
-  Engine e;
-};
 struct sd_decode {};  // opaque; the pointer is really a sd::DecodeState*
 
 namespace sd {
@@ -73,6 +70,7 @@ extern "C" sd_status sd_engine_create(const sd_engine_config* cfg, int32_t dev, 
 
 extern "C" sd_status sd_engine_destroy(sd_engine* e) {
   if (!e) return SD_OK;
+  if (e->e.server) sd_serve_stop(e);
   cudaSetDevice(e->e.device);
   cudaDeviceSynchronize();
   delete e;

@@ -273,9 +273,6 @@ sd_directive Controller::decide(int64_t now, int32_t q) {
 // =============================== C ABI =========================================================
 using namespace sd;
 
-struct sd_table {
-  Table t;
-};
 struct sd_controller {
   Controller c;
 };

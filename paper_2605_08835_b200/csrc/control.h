@@ -38,3 +38,7 @@ struct Controller {
 };
 
 }  // namespace sd
+
+struct sd_table {
+  sd::Table t;
+};

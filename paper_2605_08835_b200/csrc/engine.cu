@@ -5,6 +5,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <stdlib.h>
 
 #include "engine.h"
 
@@ -329,6 +330,13 @@ Engine::~Engine() {
   ws.release();
   if (kv_cache) cudaFree(kv_cache);
   if (meta_dev) cudaFree(meta_dev);
+  for (auto& kv : graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  for (int i = 0; i < 2; ++i) {
+    if (meta_pinned[i]) cudaFreeHost(meta_pinned[i]);
+    if (meta_ev[i]) cudaEventDestroy(meta_ev[i]);
+  }
+  if (cap_stream) cudaStreamDestroy(cap_stream);
 }
 
 static size_t unet_ws_bytes(const Engine* e) {
@@ -365,6 +373,13 @@ void build_engine(Engine* e) {
   e->meta_bytes = 64 << 10;
   SD_CUDA(cudaMalloc(&e->meta_dev, e->meta_bytes));
   e->meta_host.resize(e->meta_bytes);
+  for (int i = 0; i < 2; ++i) {
+    SD_CUDA(cudaMallocHost(&e->meta_pinned[i], e->meta_bytes));
+    SD_CUDA(cudaEventCreateWithFlags(&e->meta_ev[i], cudaEventDisableTiming));
+  }
+  SD_CUDA(cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking));
+  const char* ng = getenv("SD_NO_GRAPH");
+  e->use_graphs = !(ng && ng[0] == '1');
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -742,7 +757,11 @@ void step_batch(Engine* e, const sd_batch* b, cudaStream_t st) {
   const size_t o_a = put(A.data(), n * 4);
   const size_t o_b = put(Bc.data(), n * 4);
   const size_t o_kv = put(kv.data(), R * 4);
-  SD_CUDA(cudaMemcpyAsync(e->meta_dev, hb, off, cudaMemcpyHostToDevice, st));
+  // the pinned staging buffer is reused: wait until the previous step's H2D copy consumed it
+  const int par = e->meta_parity;
+  e->meta_parity ^= 1;
+  if (e->meta_ev_valid[par]) SD_CUDA(cudaEventSynchronize(e->meta_ev[par]));
+  memcpy(e->meta_pinned[par], hb, off);
   char* db = e->meta_dev;
   RowMap m;
   m.latents = reinterpret_cast<const float* const*>(db + o_lat);
@@ -755,12 +774,59 @@ void step_batch(Engine* e, const sd_batch* b, cudaStream_t st) {
   m.coef_b = reinterpret_cast<const float*>(db + o_b);
   const int* kv_dev = reinterpret_cast<const int*>(db + o_kv);
 
-  e->ws.reset(0);
-  bf16* x_in = e->ws.get<bf16>((size_t)R * hw * 64);
-  gather_rows(m, R, hw, 64, x_in, st);
-  float* eps = e->ws.get<float>((size_t)R * hw * 4);
-  unet_forward(e, st, R, h, w, x_in, m.t_row, kv_dev, eps);
-  combine_update(m, n, hw, eps, 4, reinterpret_cast<float* const*>(db + o_lat), st);
+  // the whole step: metadata H2D → K11 gather → UNet → K12 combine + sampler. Deterministic arena
+  // addresses for a given (n_req, rows, h, w), so it is captured once as a CUDA graph and replayed.
+  auto run = [&](cudaStream_t s) {
+    SD_CUDA(cudaMemcpyAsync(e->meta_dev, e->meta_pinned[par], off, cudaMemcpyHostToDevice, s));
+    e->ws.reset(0);
+    bf16* x_in = e->ws.get<bf16>((size_t)R * hw * 64);
+    gather_rows(m, R, hw, 64, x_in, s);
+    float* eps = e->ws.get<float>((size_t)R * hw * 4);
+    unet_forward(e, s, R, h, w, x_in, m.t_row, kv_dev, eps);
+    combine_update(m, n, hw, eps, 4, reinterpret_cast<float* const*>(db + o_lat), s);
+  };
+  const bool use_graph = e->use_graphs && !e->prof.on;
+  if (!use_graph) {
+    run(st);
+  } else {
+    auto& g = e->graphs[std::make_tuple(n, R, h, w, par)];
+    if (!g.seen) {
+      run(st);  // first call runs eagerly (sets kernel attributes, validates), capture next time
+      g.seen = true;
+    } else {
+      if (!g.exec) {
+        cudaGraph_t graph;
+        SD_CUDA(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal));
+        try {
+          run(e->cap_stream);
+        } catch (...) {
+          cudaStreamEndCapture(e->cap_stream, &graph);
+          throw;
+        }
+        SD_CUDA(cudaStreamEndCapture(e->cap_stream, &graph));
+        size_t nn = 0;
+        SD_CUDA(cudaGraphGetNodes(graph, nullptr, &nn));
+        std::vector<cudaGraphNode_t> nodes(nn);
+        SD_CUDA(cudaGraphGetNodes(graph, nodes.data(), &nn));
+        long kern = 0;
+        for (auto nd : nodes) {
+          cudaGraphNodeType ty;
+          SD_CUDA(cudaGraphNodeGetType(nd, &ty));
+          kern += ty == cudaGraphNodeTypeKernel;
+        }
+        ::sd::g_launches.fetch_sub(kern, std::memory_order_relaxed);  // capture executes nothing
+        g.kernels = kern;
+        SD_CUDA(cudaGraphInstantiate(&g.exec, graph, 0));
+        SD_CUDA(cudaGraphDestroy(graph));
+        ++e->graphs_built;
+      }
+      SD_CUDA(cudaGraphLaunch(g.exec, st));
+      ::sd::g_launches.fetch_add(g.kernels ? g.kernels : 0, std::memory_order_relaxed);
+    }
+  }
+  // the staging buffer `par` may be rewritten once this step's copy has run
+  SD_CUDA(cudaEventRecord(e->meta_ev[par], st));
+  e->meta_ev_valid[par] = true;
 }
 
 }  // namespace sd

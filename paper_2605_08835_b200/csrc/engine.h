@@ -4,6 +4,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "common.cuh"
@@ -148,6 +149,20 @@ struct Engine {
   char* meta_dev = nullptr;
   size_t meta_bytes = 0;
   std::vector<char> meta_host;
+  char* meta_pinned[2] = {nullptr, nullptr};  // double-buffered pinned staging (graph H2D source)
+  cudaEvent_t meta_ev[2] = {nullptr, nullptr};  // recorded after the step that read staging [i]
+  bool meta_ev_valid[2] = {false, false};
+  int meta_parity = 0;
+  // CUDA graphs of the whole step keyed by (n_req, rows, h, w)
+  struct GraphEntry {
+    bool seen = false;
+    cudaGraphExec_t exec = nullptr;
+    long kernels = 0;
+  };
+  std::map<std::tuple<int, int, int, int, int>, GraphEntry> graphs;
+  bool use_graphs = true;
+  int graphs_built = 0;
+  cudaStream_t cap_stream = nullptr;
   int max_rows = 0;
   std::atomic<int64_t> launches{0};
   bool failed = false;
@@ -155,6 +170,8 @@ struct Engine {
   // VAE decode slots
   std::vector<DecodeState*> free_decodes;
   std::mutex dmu;
+  void* server = nullptr;  // serve_gpu.cu Server while serving
+  int upscale() const { return 1 << ((int)vc.block_out.size() - 1); }
   ~Engine();
 };
 
@@ -166,3 +183,7 @@ void vae_decode_chunk(Engine* e, const float* z, int h, int w, int n_chunks, int
 void destroy_decode(Engine* e, DecodeState* d);
 
 }  // namespace sd
+
+struct sd_engine {
+  sd::Engine e;
+};

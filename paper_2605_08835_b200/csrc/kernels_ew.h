@@ -14,9 +14,10 @@ size_t gn_workspace_bytes(int B, int P, int G);
 // x, y: [B][P][C] bf16 (may alias? no: y != x required only if silu chain needs x later)
 void group_norm(const bf16* x, bf16* y, int B, int P, int C, int G, const float* gamma, const float* beta, float eps,
                 bool silu, void* ws, cudaStream_t st);
-int gn_chunks(int P);  // 128-pixel chunks of one image
-void gn_stats_range(const bf16* x, int P, int C, int G, int c0, int c1, void* ws, cudaStream_t st);
-void gn_apply_range(const bf16* x, bf16* y, int P, int C, int G, int c0, int c1, const float* gamma, const float* beta,
+int gn_chunk_px(int C);  // pixels per statistics chunk (divides 128)
+// pixel ranges [p0, p1) must be multiples of 128 (or end at P)
+void gn_stats_range(const bf16* x, int P, int C, int G, int p0, int p1, void* ws, cudaStream_t st);
+void gn_apply_range(const bf16* x, bf16* y, int P, int C, int G, int p0, int p1, const float* gamma, const float* beta,
                     float eps, bool silu, void* ws, cudaStream_t st);
 void layer_norm(const bf16* x, bf16* y, int T, int C, const float* gamma, const float* beta, float eps,
                 cudaStream_t st);

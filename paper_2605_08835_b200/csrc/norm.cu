@@ -1,10 +1,11 @@
 // GroupNorm (+SiLU) and LayerNorm on NHWC / token-major bf16 activations.
 //
 // GroupNorm is two launches: `gn_stats` writes deterministic per-(image, pixel-chunk, group)
-// partials (count, mean, M2) computed from fp32 register sums; `gn_apply` merges the partials of
-// its image in fixed chunk order (Chan et al.), then normalises, applies γ/β (+SiLU) and writes
-// bf16 with 16-byte vector accesses. Reduction order never depends on the batch size, so a row's
-// result is independent of the other rows in the batch (batch invariance, I5).
+// partials (mean, M2) from fp32 register sums; `gn_apply` merges the partials of its image in fixed
+// chunk order (Chan et al.), then normalises, applies γ/β (+SiLU) and writes bf16 with 16-byte
+// vector accesses. Thread (v, r) of a block always owns channel vector v, so the reduction order
+// is fixed and never depends on the batch (batch invariance, I5) or on banding (I6).
+// Chunk size adapts to C (≈ 32 K elements per chunk) so every block has enough loads in flight.
 #include "common.cuh"
 #include "kernels_ew.h"
 
@@ -14,10 +15,19 @@ struct GNPart {
   float mean, m2;
 };
 
-// block (V, R): V = C/8 vector lanes (≤ 256), R pixel rows; grid (chunks, B)
+int gn_chunk_px(int C) { return C <= 256 ? 128 : C <= 512 ? 64 : C <= 1024 ? 32 : 16; }
+
+static dim3 gn_block(int C) {
+  const int V = C / 8;
+  int R = 512 / V;
+  if (R < 1) R = 1;
+  return dim3(V, R);
+}
+
+// block (V, R): V = C/8 vector lanes, R pixel rows; grid (chunks in range, B)
 __global__ void gn_stats_kernel(const bf16* __restrict__ x, int P, int C, int G, int chunk_px, int c_base,
                                 int nch_total, GNPart* __restrict__ part) {
-  extern __shared__ float sh[];  // [R][V][8] sums and sumsq
+  extern __shared__ float sh[];  // [R][V][8] sums, then sumsq
   const int V = blockDim.x, R = blockDim.y;
   const int v = threadIdx.x, ry = threadIdx.y;
   const int b = blockIdx.y, ch = blockIdx.x + c_base;
@@ -26,12 +36,28 @@ __global__ void gn_stats_kernel(const bf16* __restrict__ x, int P, int C, int G,
 #pragma unroll
   for (int i = 0; i < 8; ++i) s[i] = q[i] = 0.f;
   const bf16* xb = x + (long)b * P * C + v * 8;
-  for (int p = p0 + ry; p < p1; p += R) {
-    uint4 u = *reinterpret_cast<const uint4*>(xb + (long)p * C);
+  int p = p0 + ry;
+  for (; p + 3 * R < p1; p += 4 * R) {  // 4 independent 16-byte loads in flight
+    uint4 u[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) u[k] = *reinterpret_cast<const uint4*>(xb + (long)(p + k * R) * C);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const bf16* e = reinterpret_cast<const bf16*>(&u[k]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float f = __bfloat162float(e[i]);
+        s[i] += f;
+        q[i] += f * f;
+      }
+    }
+  }
+  for (; p < p1; p += R) {
+    const uint4 u = *reinterpret_cast<const uint4*>(xb + (long)p * C);
     const bf16* e = reinterpret_cast<const bf16*>(&u);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      float f = __bfloat162float(e[i]);
+      const float f = __bfloat162float(e[i]);
       s[i] += f;
       q[i] += f * f;
     }
@@ -63,8 +89,8 @@ __global__ void gn_stats_kernel(const bf16* __restrict__ x, int P, int C, int G,
   }
 }
 
-__global__ void gn_apply_kernel(const bf16* __restrict__ x, int P, int C, int G, int chunk_px, int c_base, int nchunks,
-                                const GNPart* __restrict__ part, const float* __restrict__ gamma,
+__global__ void gn_apply_kernel(const bf16* __restrict__ x, int P, int C, int G, int chunk_px, int c_base,
+                                int nchunks, const GNPart* __restrict__ part, const float* __restrict__ gamma,
                                 const float* __restrict__ beta, float eps, int silu, bf16* __restrict__ y) {
   __shared__ float s_mean[64], s_rstd[64];
   const int V = blockDim.x, R = blockDim.y;
@@ -88,23 +114,40 @@ __global__ void gn_apply_kernel(const bf16* __restrict__ x, int P, int C, int G,
   }
   __syncthreads();
   const int p0 = ch * chunk_px, p1 = min(P, p0 + chunk_px);
-  float ga[8], be[8], mu[8], rs[8];
+  float ga[8], be[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int c = v * 8 + i;
-    ga[i] = gamma[c];
-    be[i] = beta[c];
-    mu[i] = s_mean[c / cg];
-    rs[i] = s_rstd[c / cg];
+    const float rs = s_rstd[c / cg];
+    ga[i] = gamma[c] * rs;                      // y = x·(γ·rstd) + (β − mean·γ·rstd)
+    be[i] = beta[c] - s_mean[c / cg] * ga[i];
   }
   const long base = (long)b * P * C + v * 8;
-  for (int p = p0 + ry; p < p1; p += R) {
-    uint4 u = *reinterpret_cast<const uint4*>(x + base + (long)p * C);
+  int p = p0 + ry;
+  for (; p + R < p1; p += 2 * R) {
+    uint4 u[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) u[k] = *reinterpret_cast<const uint4*>(x + base + (long)(p + k * R) * C);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const bf16* e = reinterpret_cast<const bf16*>(&u[k]);
+      float o[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float f = __bfloat162float(e[i]) * ga[i] + be[i];
+        o[i] = silu ? silu_f(f) : f;
+      }
+      *reinterpret_cast<uint4*>(y + base + (long)(p + k * R) * C) =
+          make_uint4(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]), pack_bf16(o[4], o[5]), pack_bf16(o[6], o[7]));
+    }
+  }
+  for (; p < p1; p += R) {
+    const uint4 u = *reinterpret_cast<const uint4*>(x + base + (long)p * C);
     const bf16* e = reinterpret_cast<const bf16*>(&u);
     float o[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      float f = (__bfloat162float(e[i]) - mu[i]) * rs[i] * ga[i] + be[i];
+      const float f = __bfloat162float(e[i]) * ga[i] + be[i];
       o[i] = silu ? silu_f(f) : f;
     }
     *reinterpret_cast<uint4*>(y + base + (long)p * C) =
@@ -112,51 +155,46 @@ __global__ void gn_apply_kernel(const bf16* __restrict__ x, int P, int C, int G,
   }
 }
 
-static void gn_block(int C, dim3* blk) {
-  const int V = C / 8;
-  int R = 256 / V;
-  if (R < 1) R = 1;
-  *blk = dim3(V, R);
+size_t gn_workspace_bytes(int B, int P, int G) { return (size_t)B * cdiv(P, 16) * G * sizeof(GNPart) + 256; }
+
+static void check_gn(int C, int G) {
+  if (C % 8 || C / 8 > 1024 || G > 64 || C % G) throw CudaError("group_norm: unsupported C/G");
 }
 
-size_t gn_workspace_bytes(int B, int P, int G) {
-  const int chunk = 128;
-  return (size_t)B * cdiv(P, chunk) * G * sizeof(GNPart) + 256;
-}
-
-int gn_chunks(int P) { return cdiv(P, 128); }
-
-// band-restricted halves of group_norm (B = 1): statistics of chunks [c0, c1) / normalisation of
-// chunks [c0, c1) with ALL chunk partials merged in fixed order — so a banded GN is bitwise equal
-// to the whole-tensor GN (R7 V1).
-void gn_stats_range(const bf16* x, int P, int C, int G, int c0, int c1, void* ws, cudaStream_t st) {
-  dim3 blk(C / 8, 256 / (C / 8) > 0 ? 256 / (C / 8) : 1);
+// band-restricted halves of group_norm (B = 1) over pixels [p0, p1) (multiples of 128): stats of the
+// chunks in the range; normalisation of the chunks in the range with ALL chunk partials merged in
+// fixed order — a banded GN is bitwise equal to the whole-tensor GN (R7 V1).
+void gn_stats_range(const bf16* x, int P, int C, int G, int p0, int p1, void* ws, cudaStream_t st) {
+  check_gn(C, G);
+  const int cp = gn_chunk_px(C);
+  const dim3 blk = gn_block(C);
   const size_t sh = (size_t)blk.x * blk.y * 8 * 2 * sizeof(float);
-  gn_stats_kernel<<<dim3(c1 - c0, 1), blk, sh, st>>>(x, P, C, G, 128, c0, gn_chunks(P),
-                                                       reinterpret_cast<GNPart*>(ws));
+  gn_stats_kernel<<<dim3(cdiv(p1, cp) - p0 / cp, 1), blk, sh, st>>>(x, P, C, G, cp, p0 / cp, cdiv(P, cp),
+                                                                     reinterpret_cast<GNPart*>(ws));
   SD_CHECK_LAUNCH();
 }
-void gn_apply_range(const bf16* x, bf16* y, int P, int C, int G, int c0, int c1, const float* gamma, const float* beta,
+void gn_apply_range(const bf16* x, bf16* y, int P, int C, int G, int p0, int p1, const float* gamma, const float* beta,
                     float eps, bool silu, void* ws, cudaStream_t st) {
-  dim3 blk(C / 8, 256 / (C / 8) > 0 ? 256 / (C / 8) : 1);
-  gn_apply_kernel<<<dim3(c1 - c0, 1), blk, 0, st>>>(x, P, C, G, 128, c0, gn_chunks(P),
-                                                          reinterpret_cast<const GNPart*>(ws), gamma, beta, eps,
-                                                          silu ? 1 : 0, y);
+  check_gn(C, G);
+  const int cp = gn_chunk_px(C);
+  const dim3 blk = gn_block(C);
+  gn_apply_kernel<<<dim3(cdiv(p1, cp) - p0 / cp, 1), blk, 0, st>>>(x, P, C, G, cp, p0 / cp, cdiv(P, cp),
+                                                                    reinterpret_cast<const GNPart*>(ws), gamma, beta,
+                                                                    eps, silu ? 1 : 0, y);
   SD_CHECK_LAUNCH();
 }
 
 void group_norm(const bf16* x, bf16* y, int B, int P, int C, int G, const float* gamma, const float* beta, float eps,
                 bool silu, void* ws, cudaStream_t st) {
-  if (C % 8 || C / 8 > 1024 || G > 64 || C % G) throw CudaError("group_norm: unsupported C/G");
-  dim3 blk;
-  gn_block(C, &blk);
-  const int chunk = 128;
-  const int nch = cdiv(P, chunk);
+  check_gn(C, G);
+  const dim3 blk = gn_block(C);
+  const int cp = gn_chunk_px(C);
+  const int nch = cdiv(P, cp);
   GNPart* part = reinterpret_cast<GNPart*>(ws);
   const size_t sh = (size_t)blk.x * blk.y * 8 * 2 * sizeof(float);
-  gn_stats_kernel<<<dim3(nch, B), blk, sh, st>>>(x, P, C, G, chunk, 0, nch, part);
+  gn_stats_kernel<<<dim3(nch, B), blk, sh, st>>>(x, P, C, G, cp, 0, nch, part);
   SD_CHECK_LAUNCH();
-  gn_apply_kernel<<<dim3(nch, B), blk, 0, st>>>(x, P, C, G, chunk, 0, nch, part, gamma, beta, eps, silu ? 1 : 0, y);
+  gn_apply_kernel<<<dim3(nch, B), blk, 0, st>>>(x, P, C, G, cp, 0, nch, part, gamma, beta, eps, silu ? 1 : 0, y);
   SD_CHECK_LAUNCH();
 }
 

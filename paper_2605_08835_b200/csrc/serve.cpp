@@ -1,0 +1,193 @@
+// Serving loop shared by the GPU server and the virtual-clock simulator (see serve.h).
+// Semantics: SURVEY.md §8(c) steps 1-5 with readings R6, R8, R9, R13, R14, R16, R17;
+// the independent reference is oracle/serving.py.
+#include "serve.h"
+
+#include <algorithm>
+#include <stdexcept>
+
+#include "api_common.h"
+#include "common.cuh"
+
+namespace sd {
+
+void insert_pending(std::vector<STask*>& p, STask* t) {
+  auto it = std::upper_bound(p.begin(), p.end(), t, [](const STask* a, const STask* b) {
+    return a->A != b->A ? a->A < b->A : a->id < b->id;
+  });
+  p.insert(it, t);
+}
+
+static int s_min(int level, int n) {
+  if (level <= 0) return n + 1;            // f = ∞: no step is eligible
+  if (level == 1) return (7 * n + 9) / 10;  // ⌈0.7 n⌉
+  return (n + 1) / 2;                       // ⌈0.5 n⌉
+}
+
+bool Loop::window(Exec& ex) {
+  int64_t now = ex.now();
+  size_t taken = 0;
+  while (taken < pending.size() && pending[taken]->A <= now && (int)batch.size() < cfg.b_max) {
+    batch.push_back(pending[taken]);
+    ex.admit(pending[taken]);
+    ++taken;
+  }
+  pending.erase(pending.begin(), pending.begin() + taken);
+  if (batch.empty() && dec.empty()) return false;
+  const int level = ctl.level, c = ctl.c;
+  const int M = (int)batch.size();
+  std::vector<STask*> dq = dec;
+  std::sort(dq.begin(), dq.end(), [](const STask* a, const STask* b) { return a->A != b->A ? a->A < b->A : a->id < b->id; });
+  if ((int)dq.size() > cfg.b_max) dq.resize(cfg.b_max);
+  const int N = (int)dq.size();
+  std::vector<uint8_t> elig(M);
+  int K = 0;
+  for (int i = 0; i < M; ++i) {
+    elig[i] = batch[i]->s >= s_min(level, batch[i]->n);
+    K += elig[i];
+  }
+  PlanOut plan;
+  int tc = 1, rounds = 1;
+  if (N == 0) {
+    plan.stages.push_back({M, 0, 0});
+  } else {
+    plan_window(*table, M, N, K, c, cfg.a_num, cfg.a_den, cfg.dp_mode, &plan);
+    tc = c;
+    rounds = c;
+  }
+  if (log) log->push_back(WindowLog{now, M, N, K, level, c, plan.stages});
+  // task mapping E (R14)
+  std::vector<STask*> el;
+  for (int i = 0; i < M; ++i)
+    if (elig[i]) el.push_back(batch[i]);
+  std::stable_sort(el.begin(), el.end(), [](const STask* a, const STask* b) {
+    const int64_t l = (int64_t)a->s * b->n, r = (int64_t)b->s * a->n;  // a.s/a.n vs b.s/b.n
+    return l != r ? l > r : a->id < b->id;
+  });
+  int nskip = 0;
+  for (auto& st : plan.stages) nskip += st[2];
+  std::vector<STask*> skippers(el.begin(), el.begin() + std::min<size_t>(nskip, el.size()));
+  std::vector<STask*> rest;
+  for (auto* t : batch)
+    if (std::find(skippers.begin(), skippers.end(), t) == skippers.end()) rest.push_back(t);
+  size_t si = 0, ri = 0, di = 0;
+  for (auto& st : plan.stages) {
+    const int m = st[0], n = st[1], k = st[2];
+    std::vector<STask*> u_ids, d_ids;
+    std::vector<uint8_t> is_skip;
+    for (int q = 0; q < k; ++q) {
+      u_ids.push_back(skippers[si++]);
+      is_skip.push_back(1);
+    }
+    for (int q = 0; q < m - k; ++q) {
+      u_ids.push_back(rest[ri++]);
+      is_skip.push_back(0);
+    }
+    for (int q = 0; q < n; ++q) d_ids.push_back(dq[di++]);
+    int64_t tau, delta;
+    if (!table->get(tc, m, n, k, &tau, &delta))
+      throw std::invalid_argument("latency table miss (c,m,n,k)=(" + std::to_string(tc) + "," + std::to_string(m) + "," +
+                                  std::to_string(n) + "," + std::to_string(k) + ")");
+    const int64_t t0 = ex.now();
+    for (int rho = 0; rho < rounds; ++rho) {
+      std::vector<STask*> step;
+      std::vector<uint8_t> skip;
+      for (size_t q = 0; q < u_ids.size(); ++q)
+        if (u_ids[q]->s < u_ids[q]->n) {
+          step.push_back(u_ids[q]);
+          skip.push_back(is_skip[q]);
+        }
+      std::vector<int64_t> dd(d_ids.size(), -1);
+      const int64_t end = ex.round(step, skip, d_ids, rho, rounds, t0, tau, delta, &dd);
+      for (size_t q = 0; q < step.size(); ++q) {
+        STask* t = step[q];
+        if (skip[q]) t->skips.push_back(t->s);
+        t->s += 1;
+        if (t->s == t->n) {
+          t->U = end;
+          batch.erase(std::find(batch.begin(), batch.end(), t));
+          dec.push_back(t);
+        }
+      }
+      if (rho == rounds - 1) {
+        for (size_t q = 0; q < d_ids.size(); ++q) {
+          STask* t = d_ids[q];
+          t->V = dd[q];
+          dec.erase(std::find(dec.begin(), dec.end(), t));
+          ex.complete(t);
+        }
+      }
+    }
+  }
+  now = ex.now();
+  int64_t waiting = 0;
+  for (auto* t : pending)
+    if (t->A <= now) ++waiting;
+  ctl.decide(now, (int32_t)ex.global_waiting(waiting));
+  return true;
+}
+
+// ---- virtual clock ----------------------------------------------------------------------------
+struct VirtualExec : Exec {
+  int64_t t = 0;
+  std::vector<STask*> done;
+  int64_t now() override { return t; }
+  void admit(STask*) override {}
+  int64_t round(const std::vector<STask*>&, const std::vector<uint8_t>&, const std::vector<STask*>& decs, int rho,
+                int rounds, int64_t t0, int64_t tau, int64_t delta, std::vector<int64_t>* dd) override {
+    const int64_t per = tau / rounds, rem = tau % rounds;
+    t += per + (rho == rounds - 1 ? rem : 0);
+    for (size_t i = 0; i < decs.size(); ++i) (*dd)[i] = t0 + delta;
+    return t;
+  }
+  void complete(STask* x) override { done.push_back(x); }
+};
+
+}  // namespace sd
+
+using namespace sd;
+
+
+extern "C" sd_status sd_serve_simulate(const sd_serve_config* cfg, const sd_table* table, int32_t n,
+                                       const uint64_t* ids, const int64_t* arrival_us, const int32_t* n_steps,
+                                       int64_t* U_out, int64_t* V_out, int32_t* n_skips_out, int32_t* windows_out) {
+  SD_REQUIRE(cfg && table && n >= 0 && (n == 0 || (ids && arrival_us && n_steps && U_out && V_out)),
+             "sd_serve_simulate: bad args");
+  SD_REQUIRE(cfg->b_max >= 1 && cfg->a_den > 0 && cfg->c_star >= 1 && cfg->ctl.c_max >= cfg->c_star,
+             "sd_serve_simulate: bad config");
+  for (int i = 0; i < n; ++i) SD_REQUIRE(n_steps[i] >= 1 && arrival_us[i] >= 0, "sd_serve_simulate: bad request");
+  SD_API_BEGIN
+  std::vector<STask> tasks(n);
+  Loop L;
+  L.cfg.b_max = cfg->b_max;
+  L.cfg.a_num = cfg->a_num;
+  L.cfg.a_den = cfg->a_den;
+  L.cfg.dp_mode = cfg->dp_mode;
+  L.cfg.c_star = cfg->c_star;
+  L.table = &table->t;
+  L.ctl.cfg = cfg->ctl;
+  L.ctl.cfg.c_star = cfg->c_star;
+  L.ctl.c = cfg->c_star;
+  for (int i = 0; i < n; ++i) {
+    tasks[i].id = ids[i];
+    tasks[i].A = arrival_us[i];
+    tasks[i].n = n_steps[i];
+    insert_pending(L.pending, &tasks[i]);
+  }
+  VirtualExec ex;
+  int windows = 0;
+  while (!L.pending.empty() || !L.batch.empty() || !L.dec.empty()) {
+    if (!L.window(ex)) {
+      ex.t = L.next_arrival();
+      continue;
+    }
+    ++windows;
+  }
+  for (int i = 0; i < n; ++i) {
+    U_out[i] = tasks[i].U;
+    V_out[i] = tasks[i].V;
+    if (n_skips_out) n_skips_out[i] = (int32_t)tasks[i].skips.size();
+  }
+  if (windows_out) *windows_out = windows;
+  SD_API_END
+}

@@ -1,0 +1,77 @@
+// Continuous-batching serving loop (§8(c) steps 1-5): one loop,
+// two executors — the GPU executor (real clock, sd_step_batch + chunked decodes on two streams) and
+// the virtual-clock executor (round durations from the τ/δ table; bit-exact with oracle/serving.py).
+#pragma once
+#include <stdint.h>
+
+#include <functional>
+#include <vector>
+
+#include "control.h"
+#include "sd_api.h"
+
+namespace sd {
+
+struct STask {
+  uint64_t id = 0;
+  int64_t A = 0;
+  int h = 0, w = 0, n = 0;
+  float g = 7.5f;
+  uint64_t noise_seed = 0;
+  std::vector<float> emb;
+  int emb_len = 0, emb_dim = 0;
+  int s = 0;
+  int64_t U = -1, V = -1;
+  std::vector<int> skips;
+  // GPU executor state
+  float* lat = nullptr;
+  int slot = -1;
+  void* decode = nullptr;
+  float* img_dev = nullptr;
+  float* img_host = nullptr;
+};
+
+struct LoopCfg {
+  int b_max = 8;
+  int a_num = 1, a_den = 10;
+  int dp_mode = 0;
+  int c_star = 1;
+  sd_controller_config ctl{};
+};
+
+struct WindowLog {
+  int64_t now;
+  int M, N, K, level, c;
+  std::vector<std::array<int, 3>> stages;
+};
+
+// Executor interface: the loop is identical for the GPU and the virtual clock.
+struct Exec {
+  virtual ~Exec() {}
+  virtual int64_t now() = 0;
+  virtual void admit(STask* t) = 0;
+  // one round of a stage; step = tasks stepping this round, skip[i] = Skip-CFG for step[i];
+  // decodes run chunk `rho` of `rounds`. Returns the round end time; fills dec_done (per decode,
+  // completion time when rho == rounds-1).
+  virtual int64_t round(const std::vector<STask*>& step, const std::vector<uint8_t>& skip,
+                        const std::vector<STask*>& decs, int rho, int rounds, int64_t stage_t0, int64_t tau,
+                        int64_t delta, std::vector<int64_t>* dec_done) = 0;
+  virtual void complete(STask* t) = 0;
+  virtual int64_t global_waiting(int64_t local) { return local; }
+};
+
+struct Loop {
+  LoopCfg cfg;
+  const Table* table = nullptr;
+  Controller ctl;
+  std::vector<STask*> pending;  // sorted by (A, id)
+  std::vector<STask*> batch, dec;
+  std::vector<WindowLog>* log = nullptr;
+  // one window; returns false if there was nothing to do (caller waits for arrivals)
+  bool window(Exec& ex);
+  int64_t next_arrival() const { return pending.empty() ? -1 : pending.front()->A; }
+};
+
+void insert_pending(std::vector<STask*>& pending, STask* t);
+
+}  // namespace sd

@@ -1,0 +1,364 @@
+// GPU server behind sd_serve_start / sd_submit / sd_poll (SURVEY §3 call stack 1-2): a thread per
+// engine runs serve.h's Loop with the GPU executor. UNet rounds (sd_step_batch internals) run on a
+// high-priority stream, VAE decode chunks on a low-priority stream ("tasks switching
+// from UNet denoising to VAE decoding ... overlap with ongoing UNet batch iterations").
+#include <math.h>
+#include <string.h>
+
+#include <chrono>
+#include <condition_variable>
+#include <deque>
+#include <thread>
+
+#include "api_common.h"
+#include "engine.h"
+#include "serve.h"
+
+namespace sd {
+float init_sigma(int sampler, int n);
+
+static uint64_t mix64s(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+static uint64_t fnv(const std::string& s) {
+  uint64_t h = 0xCBF29CE484222325ull;
+  for (unsigned char c : s) {
+    h ^= c;
+    h *= 0x100000001B3ull;
+  }
+  return h;
+}
+// synth.initial_noise(trace_seed, id, h, w): Box-Muller over counters (2i, 2i+1), fp64 → fp32
+static void initial_noise(uint64_t trace_seed, uint64_t id, int n, float* out) {
+  const uint64_t seed = mix64s(fnv("noise/" + std::to_string(id)) ^ mix64s(trace_seed));
+  for (int i = 0; i < n; ++i) {
+    const uint64_t b1 = mix64s(seed + (uint64_t)(2 * i + 1) * 0x9E3779B97F4A7C15ull);
+    const uint64_t b2 = mix64s(seed + (uint64_t)(2 * i + 2) * 0x9E3779B97F4A7C15ull);
+    const double u1 = 1.0 - (double)(b1 >> 11) * 0x1.0p-53;
+    const double u2 = (double)(b2 >> 11) * 0x1.0p-53;
+    out[i] = (float)(sqrt(-2.0 * log(u1)) * cos(2.0 * M_PI * u2));
+  }
+}
+
+struct Server;
+
+struct GpuExec : Exec {
+  Server* S;
+  explicit GpuExec(Server* s) : S(s) {}
+  int64_t now() override;
+  void admit(STask* t) override;
+  int64_t round(const std::vector<STask*>& step, const std::vector<uint8_t>& skip, const std::vector<STask*>& decs,
+                int rho, int rounds, int64_t t0, int64_t tau, int64_t delta, std::vector<int64_t>* dd) override;
+  void complete(STask* t) override;
+  int64_t global_waiting(int64_t local) override;
+};
+
+struct Server {
+  Engine* e;
+  sd_serve_config cfg;
+  Loop loop;
+  GpuExec ex{this};
+  std::thread th;
+  std::mutex mu;
+  std::condition_variable cv_sub, cv_done;
+  bool stop = false;
+  std::string error;
+  std::vector<STask*> inbox;
+  std::deque<STask*> completed;
+  std::map<uint64_t, STask*> owned;
+  std::chrono::steady_clock::time_point t0;
+  cudaStream_t hi = nullptr, lo = nullptr;
+  cudaEvent_t ev_hi = nullptr, ev_lo = nullptr;
+  int32_t counters[4] = {0, 0, 0, 0};  // waiting, decode-pending, active, completed
+  std::vector<int32_t> global;
+  int P = 0;
+  float* pinned_noise = nullptr;
+  float* pinned_emb = nullptr;
+
+  void run();
+};
+
+int64_t GpuExec::now() {
+  return std::chrono::duration_cast<std::chrono::microseconds>(std::chrono::steady_clock::now() - S->t0).count();
+}
+
+void GpuExec::admit(STask* t) {
+  Engine* e = S->e;
+  const int hw = t->h * t->w;
+  SD_CUDA(cudaMalloc(&t->lat, (size_t)4 * hw * 4));
+  SD_CUDA(cudaMalloc(&t->img_dev, (size_t)3 * 64 * hw * 4));
+  SD_CUDA(cudaMallocHost(&t->img_host, (size_t)3 * 64 * hw * 4));
+  initial_noise(S->cfg.trace_seed, t->id, 4 * hw, S->pinned_noise);
+  const float sig = init_sigma(e->cfg.sampler, t->n);
+  for (int i = 0; i < 4 * hw; ++i) S->pinned_noise[i] *= sig;
+  SD_CUDA(cudaMemcpyAsync(t->lat, S->pinned_noise, (size_t)4 * hw * 4, cudaMemcpyHostToDevice, S->hi));
+  memcpy(S->pinned_emb, t->emb.data(), t->emb.size() * 4);
+  float* emb_dev;
+  SD_CUDA(cudaMallocAsync(&emb_dev, t->emb.size() * 4, S->hi));
+  SD_CUDA(cudaMemcpyAsync(emb_dev, S->pinned_emb, t->emb.size() * 4, cudaMemcpyHostToDevice, S->hi));
+  t->slot = ctx_register(e, emb_dev, t->emb_len, t->emb_dim, -1, S->hi);
+  SD_CUDA(cudaFreeAsync(emb_dev, S->hi));
+  SD_CUDA(cudaStreamSynchronize(S->hi));  // pinned staging is reused by the next admission
+}
+
+int64_t GpuExec::round(const std::vector<STask*>& step, const std::vector<uint8_t>& skip,
+                       const std::vector<STask*>& decs, int rho, int rounds, int64_t, int64_t, int64_t,
+                       std::vector<int64_t>* dd) {
+  Engine* e = S->e;
+  if (!step.empty()) {
+    const int n = (int)step.size();
+    std::vector<float*> lat(n);
+    std::vector<int32_t> s(n), ns(n), slot(n);
+    std::vector<uint8_t> hu(n);
+    std::vector<float> g(n);
+    for (int i = 0; i < n; ++i) {
+      lat[i] = step[i]->lat;
+      s[i] = step[i]->s;
+      ns[i] = step[i]->n;
+      hu[i] = skip[i] ? 0 : 1;
+      g[i] = step[i]->g;
+      slot[i] = step[i]->slot;
+    }
+    sd_batch b{n, step[0]->h, step[0]->w, lat.data(), s.data(), ns.data(), hu.data(), g.data(), slot.data()};
+    step_batch(e, &b, S->hi);
+  }
+  for (STask* t : decs) {
+    DecodeState* ds = reinterpret_cast<DecodeState*>(t->decode);
+    vae_decode_chunk(e, t->lat, t->h, t->w, rounds, rho, &ds, t->img_dev, S->lo);
+    t->decode = ds;
+  }
+  SD_CUDA(cudaEventRecord(S->ev_lo, S->lo));
+  SD_CUDA(cudaEventRecord(S->ev_hi, S->hi));
+  if (!decs.empty() && rho == rounds - 1) {
+    SD_CUDA(cudaEventSynchronize(S->ev_lo));  // Eq. 2: the decode does not wait for the UNet
+    const int64_t td = now();
+    for (size_t i = 0; i < decs.size(); ++i) (*dd)[i] = td;
+  }
+  SD_CUDA(cudaEventSynchronize(S->ev_hi));
+  SD_CUDA(cudaEventSynchronize(S->ev_lo));
+  return now();
+}
+
+void GpuExec::complete(STask* t) {
+  const size_t bytes = (size_t)3 * 64 * t->h * t->w * 4;
+  SD_CUDA(cudaMemcpyAsync(t->img_host, t->img_dev, bytes, cudaMemcpyDeviceToHost, S->lo));
+  SD_CUDA(cudaStreamSynchronize(S->lo));
+  {
+    std::lock_guard<std::mutex> g(S->e->mu);
+    if (t->slot > 0) S->e->slot_used[t->slot] = 0;
+  }
+  cudaFree(t->lat);
+  cudaFree(t->img_dev);
+  t->lat = t->img_dev = nullptr;
+  std::lock_guard<std::mutex> g(S->mu);
+  S->completed.push_back(t);
+  S->counters[3]++;
+  S->cv_done.notify_all();
+}
+
+int64_t GpuExec::global_waiting(int64_t local) {
+  std::lock_guard<std::mutex> g(S->mu);
+  S->counters[0] = (int32_t)local;
+  S->counters[1] = (int32_t)S->loop.dec.size();
+  S->counters[2] = (int32_t)S->loop.batch.size();
+  if (S->P <= 1) return local;
+  int64_t sum = 0;
+  for (int r = 0; r < S->P; ++r) sum += S->global[4 * r];
+  return sum;
+}
+
+void Server::run() {
+  try {
+    SD_CUDA(cudaSetDevice(e->device));
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> g(mu);
+        for (STask* t : inbox) insert_pending(loop.pending, t);
+        inbox.clear();
+        if (stop) break;
+      }
+      if (!loop.window(ex)) {
+        std::unique_lock<std::mutex> g(mu);
+        const int64_t na = loop.next_arrival();
+        const int64_t wait_us = na < 0 ? 2000 : std::max<int64_t>(0, na - ex.now());
+        cv_sub.wait_for(g, std::chrono::microseconds(std::min<int64_t>(wait_us, 2000)),
+                        [&] { return stop || !inbox.empty(); });
+      }
+    }
+  } catch (const std::exception& ex_) {
+    std::lock_guard<std::mutex> g(mu);
+    error = ex_.what();
+    e->failed = true;
+    cv_done.notify_all();
+  }
+}
+
+}  // namespace sd
+
+using namespace sd;
+
+static Server* server_of(sd_engine* e) { return reinterpret_cast<Server*>(e->e.server); }
+
+extern "C" sd_status sd_serve_start(sd_engine* e, const sd_serve_config* cfg) {
+  SD_REQUIRE(e && cfg && cfg->table, "sd_serve_start: bad args");
+  SD_REQUIRE(!e->e.server, "sd_serve_start: already serving");
+  SD_REQUIRE(cfg->b_max >= 1 && cfg->b_max <= e->e.cfg.b_max, "sd_serve_start: b_max exceeds the engine's");
+  SD_REQUIRE(cfg->latent_hw >= 8 && cfg->latent_hw <= e->e.cfg.max_latent_hw, "sd_serve_start: latent_hw");
+  SD_REQUIRE(cfg->c_star >= 1 && cfg->ctl.c_max >= cfg->c_star && cfg->ctl.c_max <= e->e.cfg.c_max,
+             "sd_serve_start: chunk bounds");
+  SD_API_BEGIN
+  auto* S = new Server();
+  S->e = &e->e;
+  S->cfg = *cfg;
+  S->loop.cfg.b_max = cfg->b_max;
+  S->loop.cfg.a_num = cfg->a_num;
+  S->loop.cfg.a_den = cfg->a_den;
+  S->loop.cfg.dp_mode = cfg->dp_mode;
+  S->loop.cfg.c_star = cfg->c_star;
+  S->loop.table = &cfg->table->t;
+  S->loop.ctl.cfg = cfg->ctl;
+  S->loop.ctl.cfg.c_star = cfg->c_star;
+  S->loop.ctl.c = cfg->c_star;
+  SD_CUDA(cudaSetDevice(e->e.device));
+  int lo_p, hi_p;
+  SD_CUDA(cudaDeviceGetStreamPriorityRange(&lo_p, &hi_p));
+  SD_CUDA(cudaStreamCreateWithPriority(&S->hi, cudaStreamNonBlocking, hi_p));
+  SD_CUDA(cudaStreamCreateWithPriority(&S->lo, cudaStreamNonBlocking, lo_p));
+  SD_CUDA(cudaEventCreateWithFlags(&S->ev_hi, cudaEventDisableTiming));
+  SD_CUDA(cudaEventCreateWithFlags(&S->ev_lo, cudaEventDisableTiming));
+  const size_t hw = (size_t)cfg->latent_hw * cfg->latent_hw;
+  SD_CUDA(cudaMallocHost(&S->pinned_noise, 4 * hw * 4));
+  SD_CUDA(cudaMallocHost(&S->pinned_emb, (size_t)e->e.uc.ctx_len * e->e.uc.ctx_dim * 4));
+  S->t0 = std::chrono::steady_clock::now();
+  e->e.server = S;
+  S->th = std::thread([S] { S->run(); });
+  SD_API_END
+}
+
+extern "C" sd_status sd_submit(sd_engine* e, const sd_request* r) {
+  SD_REQUIRE(e && r && server_of(e), "sd_submit: not serving");
+  SD_REQUIRE(r->n_steps >= 1 && r->n_steps <= 1000 && r->arrival_us >= 0, "sd_submit: bad request");
+  SD_REQUIRE(r->text_emb_host && r->emb_len == e->e.uc.ctx_len && r->emb_dim == e->e.uc.ctx_dim,
+             "sd_submit: embedding shape");
+  Server* S = server_of(e);
+  if (e->e.failed) {
+    set_error("engine FAILED: " + S->error);
+    return SD_E_STATE;
+  }
+  auto* t = new STask();
+  t->id = r->id;
+  t->A = r->arrival_us;
+  t->n = r->n_steps;
+  t->g = r->guidance;
+  t->h = t->w = S->cfg.latent_hw;
+  t->emb.assign(r->text_emb_host, r->text_emb_host + (size_t)r->emb_len * r->emb_dim);
+  t->emb_len = r->emb_len;
+  t->emb_dim = r->emb_dim;
+  std::lock_guard<std::mutex> g(S->mu);
+  if (S->owned.count(r->id)) {
+    delete t;
+    set_error("sd_submit: duplicate id");
+    return SD_E_INVAL;
+  }
+  S->owned[r->id] = t;
+  S->inbox.push_back(t);
+  S->cv_sub.notify_all();
+  return SD_OK;
+}
+
+extern "C" sd_status sd_poll(sd_engine* e, sd_completion* out, int32_t max, int32_t* n_out, int32_t timeout_ms) {
+  SD_REQUIRE(e && out && n_out && max >= 0 && server_of(e), "sd_poll: bad args");
+  Server* S = server_of(e);
+  std::unique_lock<std::mutex> g(S->mu);
+  S->cv_done.wait_for(g, std::chrono::milliseconds(std::max(0, timeout_ms)),
+                      [&] { return !S->completed.empty() || !S->error.empty(); });
+  if (!S->error.empty()) {
+    set_error("serving loop failed: " + S->error);
+    return SD_E_CUDA;
+  }
+  int n = 0;
+  while (n < max && !S->completed.empty()) {
+    STask* t = S->completed.front();
+    S->completed.pop_front();
+    out[n].id = t->id;
+    out[n].arrival_us = t->A;
+    out[n].denoise_done_us = t->U;
+    out[n].decode_done_us = t->V;
+    out[n].n_skipped = (int32_t)t->skips.size();
+    out[n].h = S->e->upscale() * t->h;
+    out[n].w = S->e->upscale() * t->w;
+    out[n].image_host = t->img_host;
+    ++n;
+  }
+  *n_out = n;
+  return SD_OK;
+}
+
+extern "C" sd_status sd_release(sd_engine* e, uint64_t id) {
+  SD_REQUIRE(e && server_of(e), "sd_release: not serving");
+  Server* S = server_of(e);
+  std::lock_guard<std::mutex> g(S->mu);
+  auto it = S->owned.find(id);
+  SD_REQUIRE(it != S->owned.end() && it->second->V >= 0, "sd_release: unknown or unfinished id");
+  if (it->second->img_host) cudaFreeHost(it->second->img_host);
+  delete it->second;
+  S->owned.erase(it);
+  return SD_OK;
+}
+
+extern "C" sd_status sd_serve_stop(sd_engine* e) {
+  SD_REQUIRE(e && server_of(e), "sd_serve_stop: not serving");
+  Server* S = server_of(e);
+  {
+    std::lock_guard<std::mutex> g(S->mu);
+    S->stop = true;
+    S->cv_sub.notify_all();
+  }
+  if (S->th.joinable()) S->th.join();
+  cudaSetDevice(e->e.device);
+  cudaDeviceSynchronize();
+  for (auto& kv : S->owned) {
+    STask* t = kv.second;
+    if (t->lat) cudaFree(t->lat);
+    if (t->img_dev) cudaFree(t->img_dev);
+    if (t->img_host) cudaFreeHost(t->img_host);
+    if (t->decode) destroy_decode(&e->e, reinterpret_cast<DecodeState*>(t->decode));
+    delete t;
+  }
+  cudaFreeHost(S->pinned_noise);
+  cudaFreeHost(S->pinned_emb);
+  cudaEventDestroy(S->ev_hi);
+  cudaEventDestroy(S->ev_lo);
+  cudaStreamDestroy(S->hi);
+  cudaStreamDestroy(S->lo);
+  const std::string err = S->error;
+  delete S;
+  e->e.server = nullptr;
+  if (!err.empty()) {
+    set_error(err);
+    return SD_E_CUDA;
+  }
+  return SD_OK;
+}
+
+extern "C" sd_status sd_set_global_load(sd_engine* e, const int32_t* loads, int32_t P, uint64_t) {
+  SD_REQUIRE(e && loads && P >= 1 && server_of(e), "sd_set_global_load: bad args");
+  Server* S = server_of(e);
+  std::lock_guard<std::mutex> g(S->mu);
+  S->global.assign(loads, loads + 4 * P);
+  S->P = P;
+  return SD_OK;
+}
+
+extern "C" sd_status sd_get_load(sd_engine* e, int32_t* out4) {
+  SD_REQUIRE(e && out4 && server_of(e), "sd_get_load: bad args");
+  Server* S = server_of(e);
+  std::lock_guard<std::mutex> g(S->mu);
+  int32_t waiting = 0;
+  for (auto* t : S->inbox) waiting += 1;
+  for (int i = 0; i < 4; ++i) out4[i] = S->counters[i];
+  out4[0] = std::max(out4[0], waiting);
+  return SD_OK;
+}

@@ -253,13 +253,13 @@ static void run_item(Engine* e, DecodeState* s, const VItem& v, const float* z, 
     case VOP_HEAD: run_head(e, s, z, st); break;
     case VOP_GN_STATS: {
       const int P = v.H * v.W;
-      gn_stats_range(s->buf[v.a], P, v.C, G, v.y0 * v.W / 128, cdiv((long)v.y1 * v.W, 128), s->gn_ws, st);
+      gn_stats_range(s->buf[v.a], P, v.C, G, v.y0 * v.W, v.y1 * v.W, s->gn_ws, st);
       break;
     }
     case VOP_GN_APPLY: {
       const int P = v.H * v.W;
       const float* gam = static_cast<const float*>(v.p0);
-      gn_apply_range(s->buf[v.a], s->buf[v.b], P, v.C, G, v.y0 * v.W / 128, cdiv((long)v.y1 * v.W, 128), gam,
+      gn_apply_range(s->buf[v.a], s->buf[v.b], P, v.C, G, v.y0 * v.W, v.y1 * v.W, gam,
                      static_cast<const float*>(v.p1), e->vc.eps, v.silu != 0, s->gn_ws, st);
       break;
     }

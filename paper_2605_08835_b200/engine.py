@@ -32,6 +32,7 @@ class Engine:
         self.sampler = sampler
         self.device = device
         self.ctx_len, self.ctx_dim = (8, 32) if model == "tiny" else (77, 768)
+        self.upscale = 2 if model == "tiny" else 8      # VAE decoder: 2^(levels-1)
 
     def close(self):
         if self.h:
@@ -92,7 +93,8 @@ class Engine:
         """Whole or chunked VAE decode of one fp32 [4,h,w] latent → fp32 [3,8h,8w]."""
         h, w = latent.shape[-2:]
         if image is None:
-            image = torch.empty(3, 8 * h, 8 * w, device=latent.device, dtype=torch.float32)
+            f = self.upscale
+            image = torch.empty(3, f * h, f * w, device=latent.device, dtype=torch.float32)
         st = C.c_void_p()
         for j in range(n_chunks):
             self.decode_chunk(latent, n_chunks, j, st, image, stream)

@@ -156,3 +156,74 @@ def test_chunk_ranges_bitexact_vs_oracle():
         B.call("sd_chunk_ranges", (C.c_int64 * n)(*costs), n, c, out)
         exp = vae.chunk_ranges(costs, c)
         assert list(out[:len(exp)]) == exp
+
+
+# ---- serving loop, virtual clock (T5/T6: decisions and timestamps bit-exact with oracle/serving.py) ----
+
+def serve_table(rng, B_=8, cmax=4):
+    """τ^c/δ^c per (c, m, n, k): Eq. 2 composition of a synthetic per-round model (µs)."""
+    tabs = {}
+    for c in range(1, cmax + 1):
+        t = {}
+        for m in range(0, B_ + 1):
+            for n in range(0, B_ + 1):
+                for k in range(0, m + 1):
+                    if m == 0 and n == 0:
+                        continue
+                    if m >= 1 and n > m:
+                        continue
+                    if m == 0 and k:
+                        continue
+                    tu = int(8000 + 2500 * (2 * m - k)) if m else 0
+                    tv = (int(60000 * n / c) + 3000) if n else 0
+                    rounds_u = [tu] * c
+                    rounds_v = [tv] * c
+                    Tu, Tv = sched.cumulative_latencies(rounds_u, rounds_v) if n else (sum(rounds_u), 0)
+                    t[(m, n, k)] = (Tu, Tv if n else 0)
+        tabs[c] = t
+    return tabs
+
+
+def make_multi_table(tabs):
+    keys = [(c, *k) for c in sorted(tabs) for k in sorted(tabs[c])]
+    n = len(keys)
+    h = C.c_void_p()
+    col = lambda i, t: (t * n)(*[k[i] for k in keys])
+    B.call("sd_table_from_arrays", n, col(0, C.c_int32), col(1, C.c_int32), col(2, C.c_int32), col(3, C.c_int32),
+           (C.c_int64 * n)(*[tabs[k[0]][k[1:]][0] for k in keys]),
+           (C.c_int64 * n)(*[tabs[k[0]][k[1:]][1] for k in keys]), C.byref(h))
+    return h
+
+
+@pytest.mark.parametrize("rate,mode,cstar", [(2.0, 0, 1), (6.0, 0, 1), (6.0, 1, 2), (12.0, 0, 1)])
+def test_serving_simulation_bitexact(rate, mode, cstar):
+    from oracle import serving
+    rng = np.random.default_rng(int(rate * 10) + mode)
+    tabs = serve_table(rng)
+    h = make_multi_table(tabs)
+    n = 120
+    gaps = rng.exponential(1e6 / rate, n)
+    arr = np.cumsum(gaps).astype(np.int64)
+    steps = rng.integers(20, 51, n)
+    trace = [(i, int(arr[i]), int(steps[i])) for i in range(n)]
+    ctl_cfg = B.ControllerConfig(cstar, 4, 10, 3, 1, 2, -1, 5)
+    cfg = B.ServeConfig(8, 1, 10, mode, cstar, ctl_cfg, h, 64, 1)
+    U, V = (C.c_int64 * n)(), (C.c_int64 * n)()
+    ns, win = (C.c_int32 * n)(), C.c_int32()
+    B.call("sd_serve_simulate", C.byref(cfg), h, n, (C.c_uint64 * n)(*range(n)), (C.c_int64 * n)(*arr.tolist()),
+           (C.c_int32 * n)(*steps.tolist()), U, V, ns, C.byref(win))
+    log = []
+    done = serving.simulate(trace, tabs, b_max=8, mode="exact" if mode == 0 else "alg1", c_star=cstar, c_max=4,
+                            log=log)
+    assert len(done) == n and win.value == len(log)
+    for i in range(n):
+        t = done[i]
+        assert (U[i], V[i], ns[i]) == (t.U, t.V, len(t.skips)), i
+        assert t.A <= t.U <= t.V
+        # skip audit: every skipped step index respects the most permissive s_min (⌈0.5 n⌉)
+        assert all(s >= (t.n + 1) // 2 for s in t.skips)
+    m = serving.metrics(done)
+    assert m["p99_e2e_us"] >= m["mean_e2e_us"] * 0.5
+    if rate >= 12:
+        assert any(w["level"] > 0 for w in log) and sum(ns) > 0     # the controller engaged Skip-CFG
+    B.lib().sd_table_free(h)

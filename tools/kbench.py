@@ -1,0 +1,81 @@
+"""Kernel micro-benchmarks on the B200 (CUDA events, warm L2 unless --flush): the SD-1.5 512² conv3x3
+shapes at 16 rows and the big dense GEMMs, through the test-only C-ABI exports. Prints TFLOP/s per
+shape and the fraction of the measured sustained bf16 peak.
+
+  python tools/kbench.py [--reps 20] [--only conv|gemm]
+"""
+import argparse
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2605_08835_b200 import binding as B  # noqa: E402
+
+CONV = [  # (rows, H, W, Cin, Cout, count per UNet step)
+    (16, 64, 64, 320, 320, 7), (16, 32, 32, 640, 640, 6), (16, 16, 16, 1280, 1280, 6), (16, 8, 8, 1280, 1280, 11),
+    (16, 64, 64, 640, 320, 2), (16, 32, 32, 1280, 640, 1), (16, 16, 16, 2560, 1280, 2), (16, 8, 8, 2560, 1280, 3),
+    (16, 64, 64, 640, 640, 1), (16, 32, 32, 1280, 1280, 1), (16, 64, 64, 960, 320, 2), (16, 32, 32, 1920, 640, 1),
+]
+GEMM = [  # (M, N, K, act)
+    (65536, 2560, 320, 2), (65536, 320, 1280, 0), (65536, 960, 320, 0), (65536, 320, 320, 0),
+    (16384, 5120, 640, 2), (16384, 640, 2560, 0), (4096, 10240, 1280, 2), (4096, 1280, 5120, 0),
+]
+
+
+def timeit(fn, reps):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--only", default="")
+    args = ap.parse_args()
+    peak = 1417.2
+    p = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        peak = json.load(open(p)).get("bf16_tflops_sustained", peak)
+    out = []
+    tot_t = tot_f = 0.0
+    if args.only in ("", "conv"):
+        for (R, H, W, ci, co, cnt) in CONV:
+            x = torch.randn(R, H, W, ci, device="cuda").to(torch.bfloat16)
+            w = (torch.randn(co, 9, ci, device="cuda") / (9 * ci) ** 0.5).to(torch.bfloat16)
+            b = torch.zeros(co, device="cuda")
+            y = torch.empty(R, H, W, co, device="cuda", dtype=torch.bfloat16)
+            ms = timeit(lambda: B.debug_conv3x3(x, ci, None, 0, w, None, b, None, None, y, R, H, W, co), args.reps)
+            fl = 2.0 * R * H * W * co * 9 * ci
+            tot_t += ms * cnt
+            tot_f += fl * cnt
+            r = dict(kind="conv", shape=[R, H, W, ci, co], ms=ms, tflops=fl / ms / 1e9, frac=fl / ms / 1e9 / peak)
+            out.append(r)
+            print(json.dumps(r), flush=True)
+        print(json.dumps({"conv_weighted_tflops": tot_f / tot_t / 1e9, "frac": tot_f / tot_t / 1e9 / peak,
+                          "conv_ms_per_step": tot_t}), flush=True)
+    if args.only in ("", "gemm"):
+        for (M, N, K, act) in GEMM:
+            A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+            Wt = (torch.randn(N, K, device="cuda") / K ** 0.5).to(torch.bfloat16)
+            b = torch.zeros(N, device="cuda")
+            D = torch.empty(M, N // 2 if act == 2 else N, device="cuda", dtype=torch.bfloat16)
+            ms = timeit(lambda: B.debug_gemm(A, Wt, b, D, M, N, K, 0, act), args.reps)
+            fl = 2.0 * M * N * K
+            r = dict(kind="gemm", shape=[M, N, K, act], ms=ms, tflops=fl / ms / 1e9, frac=fl / ms / 1e9 / peak)
+            out.append(r)
+            print(json.dumps(r), flush=True)
+
+
+if __name__ == "__main__":
+    main()
