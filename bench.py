@@ -223,7 +223,6 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     n0 = eng.launch_count()
-    eng.profile(True)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
         ev0.record(st)
@@ -235,6 +234,14 @@ def main():
         dist.barrier()
     n_launch = eng.launch_count() - n0
     ms = ev0.elapsed_time(ev1)
+    # per-kernel-class device times: the same K steps again with CUDA events around every launch on
+    # the launching stream (eager launches; kernel durations are those of the graph replays above)
+    torch.cuda.synchronize()
+    eng.profile(True)
+    with torch.cuda.stream(st):
+        for _ in range(args.steps):
+            denoise_and_decode(slots)
+    torch.cuda.synchronize()
     prof = {c: eng.profile_read(c) for c in range(5)}
     eng.profile(False)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)

@@ -178,6 +178,7 @@ typedef struct {
   int64_t arrival_us, denoise_done_us, decode_done_us;  /* A_i, U_i, V_i (µs)                     */
   int32_t n_skipped, h, w;      /* Skip-CFG steps taken; image is [3][h][w]                      */
   const float* image_host;      /* engine-owned pinned buffer, valid until sd_release(id)       */
+  const int32_t* skipped_steps; /* [n_skipped] step indices run without the uncond row (audit)   */
 } sd_completion;
 /* GPU server: a thread per engine runs the loop; UNet rounds on a high-priority stream, VAE
  * chunks on a low-priority stream. */
@@ -207,6 +208,22 @@ sd_status sd_debug_gemm(const void* A, const void* B, const float* bias, void* D
 sd_status sd_debug_conv3x3(const void* x, int32_t cin, const void* x2, int32_t cin2, const void* w, const void* w2,
                            const float* bias, const float* temb, const void* res, void* y, int32_t nb, int32_t h,
                            int32_t wd, int32_t cout, void* stream);
+
+/* Attention O = softmax(Q K^T / sqrt(d)) V; q,o bf16 [rows][Lq][heads*d], k,v bf16 [rows][Lk][heads*d]
+ * (mma.sync flash kernel, any d <= 160, d % 8 == 0). */
+sd_status sd_debug_attention(const void* q, const void* k, const void* v, void* o, int32_t rows, int32_t heads,
+                             int32_t d, int32_t Lq, int32_t Lk, void* stream);
+/* tcgen05 flash attention: qk bf16 [rows*P][2*heads*d] (q | k), vt bf16 [heads*d][rows*P] (V^T),
+ * o bf16 [rows*P][heads*d]; d in {40, 64, 80}, P % 128 == 0. */
+sd_status sd_debug_attention_tc(const void* qk, const void* vt, void* o, int32_t rows, int32_t heads, int32_t d,
+                                int32_t P, void* stream);
+/* GroupNorm(+SiLU) over x bf16 [nb][P][C] (NHWC), G groups, fp32 gamma/beta; LayerNorm over x [T][C]. */
+sd_status sd_debug_groupnorm(const void* x, void* y, int32_t nb, int32_t P, int32_t C, int32_t G, const float* gamma,
+                             const float* beta, float eps, int32_t silu, void* stream);
+sd_status sd_debug_layernorm(const void* x, void* y, int32_t T, int32_t C, const float* gamma, const float* beta,
+                             float eps, void* stream);
+/* GEMM tile mode for the tests: 0 = heuristic, 1 = 128-row CTA tiles, 2 = 256-row CTA-pair tiles. */
+sd_status sd_debug_set_gemm_cg(int32_t cg);
 
 #ifdef __cplusplus
 }

@@ -57,7 +57,7 @@ class Request(C.Structure):
 class Completion(C.Structure):
     _fields_ = [("id", C.c_uint64), ("arrival_us", C.c_int64), ("denoise_done_us", C.c_int64),
                 ("decode_done_us", C.c_int64), ("n_skipped", C.c_int32), ("h", C.c_int32), ("w", C.c_int32),
-                ("image_host", C.c_void_p)]
+                ("image_host", C.c_void_p), ("skipped_steps", C.POINTER(C.c_int32))]
 
 
 class Directive(C.Structure):
@@ -102,6 +102,11 @@ SIGNATURES = {
     "sd_get_load": [P, PI32],
     "sd_serve_simulate": [C.POINTER(ServeConfig), P, I32, C.POINTER(C.c_uint64), PI64, PI32, PI64, PI64, PI32, PI32],
     "sd_debug_gemm": [P, P, P, P, I32, I32, I32, I32, I32, P],
+    "sd_debug_set_gemm_cg": [I32],
+    "sd_debug_attention": [P, P, P, P, I32, I32, I32, I32, I32, P],
+    "sd_debug_attention_tc": [P, P, P, I32, I32, I32, I32, P],
+    "sd_debug_groupnorm": [P, P, I32, I32, I32, I32, P, P, C.c_float, I32, P],
+    "sd_debug_layernorm": [P, P, I32, I32, P, P, C.c_float, P],
     "sd_debug_conv3x3": [P, I32, P, I32, P, P, P, P, P, P, I32, I32, I32, I32, P],
 }
 _RESTYPE = {"sd_last_error": C.c_char_p, "sd_status_str": C.c_char_p}

@@ -2,6 +2,7 @@
 #include "api_common.h"
 #include "common.cuh"
 #include "kernels.h"
+#include "kernels_ew.h"
 
 namespace sd {
 std::atomic<long long> g_launches{0};
@@ -74,5 +75,69 @@ extern "C" sd_status sd_debug_conv3x3(const void* x, int32_t cin, const void* x2
   d.res = static_cast<const bf16*>(res);
   d.ldr = cout;
   sd::gemm(d, static_cast<cudaStream_t>(stream));
+  SD_API_END
+}
+
+extern "C" sd_status sd_debug_set_gemm_cg(int32_t cg) {
+  SD_REQUIRE(cg >= 0 && cg <= 2, "sd_debug_set_gemm_cg: 0 (heuristic), 1 or 2");
+  sd::g_cg_override = cg;
+  return SD_OK;
+}
+
+extern "C" sd_status sd_debug_attention(const void* q, const void* k, const void* v, void* o, int32_t rows,
+                                        int32_t heads, int32_t d, int32_t Lq, int32_t Lk, void* stream) {
+  SD_REQUIRE(q && k && v && o && rows > 0 && heads > 0 && d > 0 && d % 8 == 0 && Lq > 0 && Lk > 0,
+             "sd_debug_attention: bad arguments");
+  SD_API_BEGIN
+  const int C = heads * d;
+  sd::AttnDesc a{};
+  a.Q = static_cast<const bf16*>(q);
+  a.ldq = C;
+  a.q_bstride = (long)Lq * C;
+  a.K = static_cast<const bf16*>(k);
+  a.V = static_cast<const bf16*>(v);
+  a.ldk = C;
+  a.kv_bstride = (long)Lk * C;
+  a.O = static_cast<bf16*>(o);
+  a.ldo = C;
+  a.o_bstride = (long)Lq * C;
+  a.rows = rows;
+  a.heads = heads;
+  a.d = d;
+  a.Lq = Lq;
+  a.Lk = Lk;
+  sd::attention(a, static_cast<cudaStream_t>(stream));
+  SD_API_END
+}
+
+extern "C" sd_status sd_debug_attention_tc(const void* qk, const void* vt, void* o, int32_t rows, int32_t heads,
+                                           int32_t d, int32_t P, void* stream) {
+  SD_REQUIRE(qk && vt && o && rows > 0 && heads > 0, "sd_debug_attention_tc: bad arguments");
+  SD_REQUIRE(sd::attention_tc_supported(d, P, heads * d), "sd_debug_attention_tc: d in {40,64,80}, P % 128 == 0");
+  SD_API_BEGIN
+  sd::attention_tc(static_cast<const bf16*>(qk), static_cast<const bf16*>(vt), static_cast<bf16*>(o), rows, heads, d,
+                   heads * d, P, static_cast<cudaStream_t>(stream));
+  SD_API_END
+}
+
+extern "C" sd_status sd_debug_groupnorm(const void* x, void* y, int32_t nb, int32_t P, int32_t C, int32_t G,
+                                        const float* gamma, const float* beta, float eps, int32_t silu, void* stream) {
+  SD_REQUIRE(x && y && gamma && beta && nb > 0 && P > 0 && C > 0 && G > 0 && C % G == 0 && C % 8 == 0,
+             "sd_debug_groupnorm: bad arguments");
+  SD_API_BEGIN
+  void* ws = nullptr;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  SD_CUDA(cudaMallocAsync(&ws, sd::gn_workspace_bytes(nb, P, G), st));
+  sd::group_norm(static_cast<const bf16*>(x), static_cast<bf16*>(y), nb, P, C, G, gamma, beta, eps, silu != 0, ws, st);
+  SD_CUDA(cudaFreeAsync(ws, st));
+  SD_API_END
+}
+
+extern "C" sd_status sd_debug_layernorm(const void* x, void* y, int32_t T, int32_t C, const float* gamma,
+                                        const float* beta, float eps, void* stream) {
+  SD_REQUIRE(x && y && gamma && beta && T > 0 && C > 0 && C % 8 == 0, "sd_debug_layernorm: bad arguments");
+  SD_API_BEGIN
+  sd::layer_norm(static_cast<const bf16*>(x), static_cast<bf16*>(y), T, C, gamma, beta, eps,
+                 static_cast<cudaStream_t>(stream));
   SD_API_END
 }

@@ -380,6 +380,8 @@ void build_engine(Engine* e) {
   SD_CUDA(cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking));
   const char* ng = getenv("SD_NO_GRAPH");
   e->use_graphs = !(ng && ng[0] == '1');
+  const char* at = getenv("SD_ATTN_TC");
+  e->use_attn_tc = !(at && at[0] == '0');
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -523,9 +525,19 @@ struct Fwd {
     linear(a, T, C, t.wpin, C, t.bpin, h, C);
     bf16* n = buf(T * C);
     ln(h, n, T, C, t.l1g, t.l1b);
+    bf16* o = buf(T * C);
+    if (e->use_attn_tc && attention_tc_supported(dh, P, C)) {
+      // tcgen05 flash attention: q|k token-major from one GEMM, Vᵀ channel-major from another
+      bf16* qk = buf(T * 2 * C);
+      linear(n, T, C, t.wqkv, 2 * C, nullptr, qk, 2 * C);
+      bf16* vt = buf(T * C);
+      linear(t.wqkv + 2L * C * C, C, C, n, (int)T, nullptr, vt, (int)T);
+      const int pi = e->prof.begin(PC_ATTN, st, 4.0 * R * heads * (double)P * P * dh);
+      attention_tc(qk, vt, o, R, heads, dh, C, P, st);
+      e->prof.end(pi, st);
+    } else {
     bf16* qkv = buf(T * 3 * C);
     linear(n, T, C, t.wqkv, 3 * C, nullptr, qkv, 3 * C);
-    bf16* o = buf(T * C);
     AttnDesc ad{};
     ad.Q = qkv;
     ad.ldq = 3 * C;
@@ -544,6 +556,7 @@ struct Fwd {
     ad.Lq = P;
     ad.Lk = P;
     attn(ad);
+    }
     bf16* h2 = buf(T * C);
     linear(o, T, C, t.wo, C, t.bo, h2, C, h);
     ln(h2, n, T, C, t.l2g, t.l2b);
@@ -785,11 +798,13 @@ void step_batch(Engine* e, const sd_batch* b, cudaStream_t st) {
     unet_forward(e, s, R, h, w, x_in, m.t_row, kv_dev, eps);
     combine_update(m, n, hw, eps, 4, reinterpret_cast<float* const*>(db + o_lat), s);
   };
-  const bool use_graph = e->use_graphs && !e->prof.on;
+  const bool use_graph = e->use_graphs;
+  const bool prof = e->prof.on;
   if (!use_graph) {
     run(st);
   } else {
-    auto& g = e->graphs[std::make_tuple(n, R, h, w, par)];
+    // profiled graphs (event-record nodes around every launch) are cached separately
+    auto& g = e->graphs[std::make_tuple(n, R, h, w, par + (prof ? 2 : 0))];
     if (!g.seen) {
       run(st);  // first call runs eagerly (sets kernel attributes, validates), capture next time
       g.seen = true;
@@ -797,12 +812,15 @@ void step_batch(Engine* e, const sd_batch* b, cudaStream_t st) {
       if (!g.exec) {
         cudaGraph_t graph;
         SD_CUDA(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal));
+        if (prof) e->prof.sink = &g.prof;
         try {
           run(e->cap_stream);
         } catch (...) {
+          e->prof.sink = nullptr;
           cudaStreamEndCapture(e->cap_stream, &graph);
           throw;
         }
+        e->prof.sink = nullptr;
         SD_CUDA(cudaStreamEndCapture(e->cap_stream, &graph));
         size_t nn = 0;
         SD_CUDA(cudaGraphGetNodes(graph, nullptr, &nn));
@@ -822,6 +840,7 @@ void step_batch(Engine* e, const sd_batch* b, cudaStream_t st) {
       }
       SD_CUDA(cudaGraphLaunch(g.exec, st));
       ::sd::g_launches.fetch_add(g.kernels ? g.kernels : 0, std::memory_order_relaxed);
+      if (prof) e->prof.accumulate(g.prof);  // synchronises on this replay's events
     }
   }
   // the staging buffer `par` may be rewritten once this step's copy has run
@@ -844,27 +863,38 @@ cudaEvent_t Prof::ev() {
 }
 int Prof::begin(int cls, cudaStream_t st, double work) {
   if (!on) return -1;
+  std::vector<Rec>& dst = sink ? *sink : recs;
   Rec r{cls, ev(), ev(), work};
-  SD_CUDA(cudaEventRecord(r.a, st));
-  recs.push_back(r);
-  return (int)recs.size() - 1;
+  // inside a stream capture the record must be an external event-record node to be readable later
+  SD_CUDA(sink ? cudaEventRecordWithFlags(r.a, st, cudaEventRecordExternal) : cudaEventRecord(r.a, st));
+  dst.push_back(r);
+  return (int)dst.size() - 1;
 }
 void Prof::end(int idx, cudaStream_t st) {
-  if (idx >= 0) SD_CUDA(cudaEventRecord(recs[idx].b, st));
+  if (idx < 0) return;
+  std::vector<Rec>& dst = sink ? *sink : recs;
+  SD_CUDA(sink ? cudaEventRecordWithFlags(dst[idx].b, st, cudaEventRecordExternal) : cudaEventRecord(dst[idx].b, st));
+}
+void Prof::accumulate(const std::vector<Rec>& rs) {
+  for (auto& r : rs) {
+    SD_CUDA(cudaEventSynchronize(r.b));
+    float t = 0;
+    SD_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+    tot_ms[r.cls] += t;
+    tot_n[r.cls] += 1;
+    tot_work[r.cls] += r.work;
+  }
 }
 void Prof::read(int cls, double* ms, long long* n, double* work) {
-  *ms = 0;
-  *n = 0;
-  *work = 0;
-  for (auto& r : recs)
-    if (r.cls == cls) {
-      SD_CUDA(cudaEventSynchronize(r.b));
-      float t = 0;
-      SD_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
-      *ms += t;
-      *n += 1;
-      *work += r.work;
-    }
+  accumulate(recs);
+  for (auto& r : recs) {
+    pool.push_back(r.a);
+    pool.push_back(r.b);
+  }
+  recs.clear();
+  *ms = tot_ms[cls];
+  *n = tot_n[cls];
+  *work = tot_work[cls];
 }
 void Prof::reset() {
   for (auto& r : recs) {
@@ -872,6 +902,11 @@ void Prof::reset() {
     pool.push_back(r.b);
   }
   recs.clear();
+  for (int i = 0; i < PC_N; ++i) {
+    tot_ms[i] = 0;
+    tot_n[i] = 0;
+    tot_work[i] = 0;
+  }
 }
 Prof::~Prof() {
   reset();

@@ -120,11 +120,15 @@ struct Prof {
     cudaEvent_t a, b;
     double work;
   };
-  std::vector<Rec> recs;
+  std::vector<Rec> recs;            // eager launches since the last read
+  std::vector<Rec>* sink = nullptr; // while capturing a profiled graph: that graph's records
   std::vector<cudaEvent_t> pool;
+  double tot_ms[8] = {0}, tot_work[8] = {0};
+  long long tot_n[8] = {0};
   cudaEvent_t ev();
   int begin(int cls, cudaStream_t st, double work);
   void end(int idx, cudaStream_t st);
+  void accumulate(const std::vector<Rec>& rs);
   void read(int cls, double* ms, long long* n, double* work);
   void reset();
   ~Prof();
@@ -158,9 +162,11 @@ struct Engine {
     bool seen = false;
     cudaGraphExec_t exec = nullptr;
     long kernels = 0;
+    std::vector<Prof::Rec> prof;  // event records of a profiled graph (read after every replay)
   };
   std::map<std::tuple<int, int, int, int, int>, GraphEntry> graphs;
   bool use_graphs = true;
+  bool use_attn_tc = true;  // tcgen05 flash attention where supported (SD_ATTN_TC=0 disables)
   int graphs_built = 0;
   cudaStream_t cap_stream = nullptr;
   int max_rows = 0;

@@ -1,12 +1,20 @@
 // tcgen05 / TMEM / TMA GEMM and implicit-GEMM 3x3 convolution for sm_100a.
 //
-// One persistent, warp-specialised kernel:
+// One persistent, warp-specialised kernel template gemm_kernel<BN, CG>:
 //   warp 0      TMA producer   (one elected lane): A and B tiles into a STAGES-deep smem ring
-//   warp 1      MMA issuer     (one elected lane): tcgen05.mma 128×BN×16 into a double-buffered
-//                              TMEM accumulator; also owns TMEM alloc/dealloc
+//   warp 1      MMA issuer     (one elected lane of the leader CTA): tcgen05.mma into a
+//                              double-buffered TMEM accumulator; also owns TMEM alloc/dealloc
 //   warps 2..5  epilogue       tcgen05.ld → bias / temb / act / residual → bf16|fp32 stores
-// smem operands are K-major with the 128-byte swizzle written by TMA and described to the
-// tensor core by SWIZZLE_128B UMMA descriptors (8-row groups 1024 B apart).
+// CG = 1: one CTA computes a 128×BN tile.
+// CG = 2: a CTA pair (cluster of 2, cta_group::2) computes a 256×BN tile: each CTA loads its 128
+//         rows of A and half of B, the leader issues 256×BN×16 MMAs reading both CTAs' smem, and
+//         each CTA drains its 128 accumulator rows from its own TMEM. Per-SM operand traffic per
+//         FLOP drops by (1/BN + 1/128) → (1/BN + 1/256) — the lever against the L2 bandwidth wall.
+// smem operands are K-major with the 128-byte swizzle written by TMA and described to the tensor
+// core by SWIZZLE_128B UMMA descriptors (8-row groups 1024 B apart).
+#include <stdlib.h>
+#include <string.h>
+
 #include <mutex>
 #include <vector>
 
@@ -22,7 +30,7 @@ struct GemmArgs {
   int kb_src[2];      // K blocks (of 64 channels) per tap for each source
   int nsrc;
   int num_kb;         // K blocks per tile
-  int m_tiles, n_tiles, m_tile_begin;
+  int m_tiles, n_tiles, m_tile_begin;   // m_tiles counts tiles of 128*CG rows
   void* out;
   int ldo, col_off, out_f32;
   const float* bias;
@@ -33,35 +41,319 @@ struct GemmArgs {
   const bf16* res;
   int ldr;
   int act;
+  int tma_store;      // bf16 output through the per-warp smem slab + TMA store
 };
 
-template <int BN>
+template <int BN, int CG>
 struct Cfg {
   static constexpr int BM = 128, BK = 64;
-  static constexpr int A_BYTES = BM * BK * 2;                    // 16 KB
-  static constexpr int B_BYTES = BN * BK * 2;
-  static constexpr int STAGES = BN >= 256 ? 4 : (BN >= 160 ? 5 : 6);
+  static constexpr int A_BYTES = BM * BK * 2;                    // 16 KB (this CTA's rows)
+  static constexpr int B_ROWS = BN / CG;                         // B rows loaded by this CTA
+  static constexpr int B_BYTES = B_ROWS * BK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (184 * 1024) / STAGE > 8 ? 8 : (184 * 1024) / STAGE;
   static constexpr int TMEM_STRIDE = BN <= 64 ? 64 : (BN <= 128 ? 128 : 256);
   static constexpr int TMEM_COLS = 2 * TMEM_STRIDE;
-  static constexpr int SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + 256;
+  static constexpr int STAGING = 4 * 2 * 2048;                   // 4 epilogue warps × 2 slabs
+  static constexpr int SMEM = 1024 + STAGES * STAGE + STAGING + 256;
+  static_assert(B_BYTES % 1024 == 0, "B tile must be a whole number of 8-row swizzle groups");
 };
 
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same variable in CTA rank 0 of the cluster
+__device__ __forceinline__ uint32_t leader_addr(const void* p) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(smem_u32(p)));
+  return r;
+}
+
+template <int CG>
+__device__ __forceinline__ void tma2(void* dst, const CUtensorMap* m, uint64_t* bar, uint32_t bar_l, int c0, int c1) {
+  if (CG == 1) {
+    tma_load_2d(dst, m, bar, c0, c1);
+  } else {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+        "%4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_l), "r"(c0), "r"(c1)
+        : "memory");
+  }
+}
+template <int CG>
+__device__ __forceinline__ void tma3(void* dst, const CUtensorMap* m, uint64_t* bar, uint32_t bar_l, int c0, int c1,
+                                     int c2) {
+  if (CG == 1) {
+    tma_load_3d(dst, m, bar, c0, c1, c2);
+  } else {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+        "%4, %5}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_l), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+  }
+}
+template <int CG>
+__device__ __forceinline__ void tma4(void* dst, const CUtensorMap* m, uint64_t* bar, uint32_t bar_l, int c0, int c1,
+                                     int c2, int c3) {
+  if (CG == 1) {
+    tma_load_4d(dst, m, bar, c0, c1, c2, c3);
+  } else {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+        "%4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_l), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+  }
+}
+template <int CG>
+__device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if (CG == 1) {
+    umma_bf16(d, a, b, idesc, acc);
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+  }
+}
+// commit → arrive on `bar` (CG = 2: on the barrier at the same offset in both CTAs of the pair)
+template <int CG>
+__device__ __forceinline__ void commit(uint64_t* bar) {
+  if (CG == 1) {
+    umma_commit(bar);
+  } else {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)0x3)
+        : "memory");
+  }
+}
+template <int CG>
+__device__ __forceinline__ void tmem_alloc_cg(uint32_t* dst, uint32_t ncols) {
+  if (CG == 1) {
+    tmem_alloc(dst, ncols);
+  } else {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)), "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+}
+template <int CG>
+__device__ __forceinline__ void tmem_dealloc_cg(uint32_t taddr, uint32_t ncols) {
+  if (CG == 1)
+    tmem_dealloc(taddr, ncols);
+  else
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+
+// ---- epilogue --------------------------------------------------------------------------------
+// Each epilogue warp owns 32 accumulator rows (its TMEM lane quarter). Per 32-column chunk:
+// tcgen05.ld → fp32 math (α, bias, temb, act, residual) → bf16 → a 2 KB per-warp staging slab in
+// smem (64-byte rows, 64B swizzle) → one TMA store of the 32×32 sub-tile (coalesced, clipped to the
+// tensor bounds by the hardware). fp32 outputs (ε, temb projections) use direct stores.
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* m, const void* src, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+struct EpiCtx {
+  uint8_t* stage;   // this warp's 2 × 2 KB staging slabs
+  int slot;         // alternating slab
+  int sx, sy, sb;   // this warp's slab origin (conv: pixel coords; dense: row in sx)
+};
+
+// write 32 fp32 values (this lane's row, columns [col, col+32)) to the staging slab and TMA-store it
+__device__ __forceinline__ void stage_store(const GemmArgs& g, const CUtensorMap* om, EpiCtx& ec, const float* o,
+                                            int col, int lane) {
+  uint8_t* buf = ec.stage + ec.slot * 2048;
+  if (lane == 0) bulk_wait_read<1>();      // the store issued two chunks ago has finished reading
+  __syncwarp();
+  const int sw = (lane >> 1) & 3;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const uint4 v = make_uint4(pack_bf16(o[8 * c], o[8 * c + 1]), pack_bf16(o[8 * c + 2], o[8 * c + 3]),
+                               pack_bf16(o[8 * c + 4], o[8 * c + 5]), pack_bf16(o[8 * c + 6], o[8 * c + 7]));
+    *reinterpret_cast<uint4*>(buf + lane * 64 + ((c ^ sw) << 4)) = v;
+  }
+  fence_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    if (g.mode == GEMM_DENSE)
+      tma_store_2d(om, buf, col, ec.sx);
+    else
+      tma_store_4d(om, buf, col, ec.sx, ec.sy, ec.sb);
+    bulk_commit();
+  }
+  ec.slot ^= 1;
+}
+
 template <int BN>
+__device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorMap* om, EpiCtx& ec, uint32_t tbase,
+                                              int mbox, int n0, int q, int lane) {
+  const int r = q * 32 + lane;
+  long prow;
+  int img;
+  bool valid;
+  if (g.mode == GEMM_DENSE) {
+    prow = (long)mbox * 128 + r;
+    valid = prow < g.M;
+    img = (int)(prow / g.rows_per_img);
+    ec.sx = mbox * 128 + q * 32;
+  } else {
+    const int tx = mbox % g.tiles_x;
+    const int ty = (mbox / g.tiles_x) % g.tiles_y;
+    const int tb = mbox / (g.tiles_x * g.tiles_y);
+    const int xx = tx * g.wt + r % g.wt;
+    const int yy = ty * g.ht + (r / g.wt) % g.ht;
+    const int bb = tb * g.bt + r / (g.wt * g.ht);
+    valid = xx < g.W && yy < g.H && bb < g.B;
+    prow = ((long)bb * g.H + yy) * g.W + xx;
+    img = bb;
+    const int r0 = q * 32;
+    ec.sx = tx * g.wt + r0 % g.wt;
+    ec.sy = ty * g.ht + (r0 / g.wt) % g.ht;
+    ec.sb = tb * g.bt + r0 / (g.wt * g.ht);
+  }
+  if (g.act == ACT_GEGLU) {
+    // columns [128j, 128j+64) = value, [128j+64, 128j+128) = gate; output width BN/2
+#pragma unroll 1
+    for (int j = 0; j < BN / 128; ++j) {
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        uint32_t rv[32], rg[32];
+        const int cv = j * 128 + h * 32, cgc = cv + 64;
+        tmem_ld32(tbase + cv, rv);
+        tmem_ld32(tbase + cgc, rg);
+        const int ocol = (n0 >> 1) + j * 64 + h * 32;
+        if (ocol >= (g.N >> 1)) continue;  // warp-uniform
+        float o[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          float v = __uint_as_float(rv[i]) * g.alpha;
+          float gt = __uint_as_float(rg[i]) * g.alpha;
+          if (g.bias) {
+            v += g.bias[n0 + cv + i];
+            gt += g.bias[n0 + cgc + i];
+          }
+          o[i] = v * gelu_f(gt);
+        }
+        if (g.res && valid) {
+          const bf16* rp = g.res + prow * g.ldr + ocol;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] += __bfloat162float(rp[i]);
+        }
+        stage_store(g, om, ec, o, ocol, lane);
+      }
+    }
+    return;
+  }
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    uint32_t rv[32];
+    tmem_ld32(tbase + c * 32, rv);
+    const int col = n0 + c * 32;
+    if (col >= g.N) continue;  // warp-uniform
+    float o[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(rv[i]) * g.alpha;
+    const bool full32 = col + 32 <= g.N;
+    if (g.bias) {
+      if (g.bias_per_row) {
+        const float bv = valid ? g.bias[prow] : 0.f;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o[i] += bv;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o[i] += (full32 || col + i < g.N) ? g.bias[col + i] : 0.f;
+      }
+    }
+    if (g.temb && valid) {
+      const float* tp = g.temb + (long)img * g.ld_temb + col;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) o[i] += (full32 || col + i < g.N) ? tp[i] : 0.f;
+    }
+    if (g.act == ACT_SILU) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) o[i] = silu_f(o[i]);
+    }
+    if (g.res && valid) {
+      const bf16* rp = g.res + prow * g.ldr + col;
+      if (full32) {
+        const uint4* r4 = reinterpret_cast<const uint4*>(rp);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          uint4 u = r4[i];
+          const bf16* e = reinterpret_cast<const bf16*>(&u);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) o[8 * i + k] += __bfloat162float(e[k]);
+        }
+      } else {
+        for (int i = 0; i < 32 && col + i < g.N; ++i) o[i] += __bfloat162float(rp[i]);
+      }
+    }
+    if (g.tma_store) {
+      stage_store(g, om, ec, o, col, lane);
+    } else if (valid) {
+      if (g.out_f32) {
+        float* op = reinterpret_cast<float*>(g.out) + prow * g.ldo + g.col_off + col;
+        if (full32 && ((g.ldo | g.col_off) & 3) == 0) {
+          float4* o4 = reinterpret_cast<float4*>(op);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) o4[i] = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
+        } else {
+          for (int i = 0; i < 32 && col + i < g.N; ++i) op[i] = o[i];
+        }
+      } else {
+        bf16* op = reinterpret_cast<bf16*>(g.out) + prow * g.ldo + g.col_off + col;
+        for (int i = 0; i < 32 && col + i < g.N; ++i) op[i] = __float2bfloat16(o[i]);
+      }
+    }
+  }
+}
+
+template <int BN, int CG>
 __global__ void __launch_bounds__(192, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ CUtensorMap ta1,
-                const __grid_constant__ CUtensorMap tb0, const __grid_constant__ CUtensorMap tb1, const GemmArgs g) {
-  using C = Cfg<BN>;
+                const __grid_constant__ CUtensorMap tb0, const __grid_constant__ CUtensorMap tb1,
+                const __grid_constant__ CUtensorMap tout, const GemmArgs g) {
+  using C = Cfg<BN, CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES);
+  uint8_t* sStage = sB + C::STAGES * C::B_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStage + C::STAGING);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -69,7 +361,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 4);
+      mbar_init(&tempty[s], 4 * CG);
     }
     fence_mbar_init();
     tma_prefetch(&ta0);
@@ -79,41 +371,52 @@ __global__ void __launch_bounds__(192, 1)
       tma_prefetch(&tb1);
     }
   }
-  if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  if (warp == 1) tmem_alloc_cg<CG>(tmem_slot, C::TMEM_COLS);
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2)
+    cluster_sync();
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   const int total = g.m_tiles * g.n_tiles;
+  const int worker = blockIdx.x / CG, nworkers = gridDim.x / CG;
 
   if (warp == 0) {
     if (lane == 0) {
-      // ================= TMA producer =================
+      // ================= TMA producer (both CTAs of a pair load their halves) =================
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      for (int t = worker; t < total; t += nworkers) {
         const int mt = g.m_tile_begin + t / g.n_tiles, nt = t % g.n_tiles;
-        const int n0 = nt * BN;
+        const int mbox = mt * CG + (int)rank;  // this CTA's 128-row box
+        const int n0 = nt * BN + (int)rank * C::B_ROWS;
         int m0 = 0, x0 = 0, y0 = 0, b0 = 0;
         if (g.mode == GEMM_DENSE) {
-          m0 = mt * C::BM;
+          m0 = mbox * C::BM;
         } else {
-          const int tx = mt % g.tiles_x;
-          const int ty = (mt / g.tiles_x) % g.tiles_y;
-          const int tb = mt / (g.tiles_x * g.tiles_y);
+          const int tx = mbox % g.tiles_x;
+          const int ty = (mbox / g.tiles_x) % g.tiles_y;
+          const int tb = mbox / (g.tiles_x * g.tiles_y);
           x0 = tx * g.wt;
           y0 = ty * g.ht;
           b0 = tb * g.bt;
         }
         for (int kb = 0; kb < g.num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
+          uint32_t bar_l = 0;
+          if (CG == 1) {
+            mbar_expect_tx(&full[stage], C::STAGE);
+          } else {
+            bar_l = leader_addr(&full[stage]);
+            if (rank == 0) mbar_expect_tx(&full[stage], 2 * C::STAGE);
+          }
           void* dA = sA + stage * C::A_BYTES;
           void* dB = sB + stage * C::B_BYTES;
           if (g.mode == GEMM_DENSE) {
-            tma_load_2d(dA, &ta0, &full[stage], kb * C::BK, m0);
-            tma_load_2d(dB, &tb0, &full[stage], kb * C::BK, n0);
+            tma2<CG>(dA, &ta0, &full[stage], bar_l, kb * C::BK, m0);
+            tma2<CG>(dB, &tb0, &full[stage], bar_l, kb * C::BK, n0);
           } else {
             int r = kb, src = 0;
             if (r >= 9 * g.kb_src[0]) {
@@ -124,8 +427,8 @@ __global__ void __launch_bounds__(192, 1)
             const int dy = tap / 3 - 1, dx = tap % 3 - 1;
             const CUtensorMap* ma = src ? &ta1 : &ta0;
             const CUtensorMap* mb = src ? &tb1 : &tb0;
-            tma_load_4d(dA, ma, &full[stage], cb * C::BK, x0 + dx, y0 + dy, b0);
-            tma_load_3d(dB, mb, &full[stage], cb * C::BK, tap, n0);
+            tma4<CG>(dA, ma, &full[stage], bar_l, cb * C::BK, x0 + dx, y0 + dy, b0);
+            tma3<CG>(dB, mb, &full[stage], bar_l, cb * C::BK, tap, n0);
           }
           if (++stage == C::STAGES) {
             stage = 0;
@@ -135,13 +438,13 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ================= MMA issuer =================
-      constexpr uint32_t idesc = make_idesc_bf16(128, BN);
+    if (lane == 0 && rank == 0) {
+      // ================= MMA issuer (leader CTA) =================
+      constexpr uint32_t idesc = make_idesc_bf16(128 * CG, BN);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+      for (int t = worker; t < total; t += nworkers, ++it) {
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -153,165 +456,51 @@ __global__ void __launch_bounds__(192, 1)
           const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
           const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
 #pragma unroll
-          for (int k = 0; k < C::BK / 16; ++k) {
-            umma_bf16(d, make_sdesc_sw128(a0 + k * 32), make_sdesc_sw128(b0 + k * 32), idesc, (kb | k) != 0);
-          }
-          umma_commit(&empty[stage]);
+          for (int k = 0; k < C::BK / 16; ++k)
+            mma<CG>(d, make_sdesc_sw128(a0 + k * 32), make_sdesc_sw128(b0 + k * 32), idesc, (kb | k) != 0);
+          commit<CG>(&empty[stage]);
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(&tfull[acc]);
+        commit<CG>(&tfull[acc]);
       }
     }
     __syncwarp();
   } else {
     // ================= epilogue (warps 2..5 → TMEM lane quarters 2,3,0,1) =================
     const int q = warp & 3;
-    const int r = q * 32 + lane;          // accumulator row = TMEM lane
+    EpiCtx ec{sStage + (warp - 2) * 4096, 0, 0, 0, 0};
     int it = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+    for (int t = worker; t < total; t += nworkers, ++it) {
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       const int mt = g.m_tile_begin + t / g.n_tiles, nt = t % g.n_tiles;
-      const int n0 = nt * BN;
-      long prow;       // output row index (pixel or m)
-      int img;
-      bool valid;
-      if (g.mode == GEMM_DENSE) {
-        prow = (long)mt * 128 + r;
-        valid = prow < g.M;
-        img = (int)(prow / g.rows_per_img);
-      } else {
-        const int tx = mt % g.tiles_x;
-        const int ty = (mt / g.tiles_x) % g.tiles_y;
-        const int tb = mt / (g.tiles_x * g.tiles_y);
-        const int xx = tx * g.wt + r % g.wt;
-        const int yy = ty * g.ht + (r / g.wt) % g.ht;
-        const int bb = tb * g.bt + r / (g.wt * g.ht);
-        valid = xx < g.W && yy < g.H && bb < g.B;
-        prow = ((long)bb * g.H + yy) * g.W + xx;
-        img = bb;
-      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * C::TMEM_STRIDE;
-      if (g.act == ACT_GEGLU) {
-        // columns [128j, 128j+64) = value, [128j+64, 128j+128) = gate; output width BN/2
-#pragma unroll 1
-        for (int j = 0; j < BN / 128; ++j) {
-#pragma unroll 1
-          for (int h = 0; h < 2; ++h) {
-            uint32_t rv[32], rg[32];
-            const int cv = j * 128 + h * 32, cg = cv + 64;
-            tmem_ld32(tbase + cv, rv);
-            tmem_ld32(tbase + cg, rg);
-            const int ocol = (n0 >> 1) + j * 64 + h * 32;   // output column base
-            if (valid && ocol < (g.N >> 1)) {
-              float o[32];
-#pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                float v = __uint_as_float(rv[i]) * g.alpha;
-                float gt = __uint_as_float(rg[i]) * g.alpha;
-                if (g.bias) {
-                  v += g.bias[n0 + cv + i];
-                  gt += g.bias[n0 + cg + i];
-                }
-                o[i] = v * gelu_f(gt);
-              }
-              bf16* op = reinterpret_cast<bf16*>(g.out) + prow * g.ldo + g.col_off + ocol;
-              if (g.res) {
-                const bf16* rp = g.res + prow * g.ldr + ocol;
-#pragma unroll
-                for (int i = 0; i < 32; ++i) o[i] += __bfloat162float(rp[i]);
-              }
-              uint4* o4 = reinterpret_cast<uint4*>(op);
-#pragma unroll
-              for (int i = 0; i < 4; ++i)
-                o4[i] = make_uint4(pack_bf16(o[8 * i], o[8 * i + 1]), pack_bf16(o[8 * i + 2], o[8 * i + 3]),
-                                   pack_bf16(o[8 * i + 4], o[8 * i + 5]), pack_bf16(o[8 * i + 6], o[8 * i + 7]));
-            }
-          }
-        }
-      } else {
-#pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          uint32_t rv[32];
-          tmem_ld32(tbase + c * 32, rv);
-          const int col = n0 + c * 32;
-          if (valid && col < g.N) {
-            float o[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(rv[i]) * g.alpha;
-            if (g.bias) {
-              if (g.bias_per_row) {
-                const float bv = g.bias[prow];
-#pragma unroll
-                for (int i = 0; i < 32; ++i) o[i] += bv;
-              } else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) o[i] += (col + i < g.N) ? g.bias[col + i] : 0.f;
-              }
-            }
-            if (g.temb) {
-              const float* tp = g.temb + (long)img * g.ld_temb + col;
-#pragma unroll
-              for (int i = 0; i < 32; ++i) o[i] += (col + i < g.N) ? tp[i] : 0.f;
-            }
-            if (g.act == ACT_SILU) {
-#pragma unroll
-              for (int i = 0; i < 32; ++i) o[i] = silu_f(o[i]);
-            }
-            const bool full32 = col + 32 <= g.N;
-            if (g.res) {
-              const bf16* rp = g.res + prow * g.ldr + col;
-              if (full32) {
-                const uint4* r4 = reinterpret_cast<const uint4*>(rp);
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                  uint4 u = r4[i];
-                  const bf16* e = reinterpret_cast<const bf16*>(&u);
-#pragma unroll
-                  for (int k = 0; k < 8; ++k) o[8 * i + k] += __bfloat162float(e[k]);
-                }
-              } else {
-                for (int i = 0; i < 32 && col + i < g.N; ++i) o[i] += __bfloat162float(rp[i]);
-              }
-            }
-            if (g.out_f32) {
-              float* op = reinterpret_cast<float*>(g.out) + prow * g.ldo + g.col_off + col;
-              if (full32 && ((g.ldo | g.col_off) & 3) == 0) {
-                float4* o4 = reinterpret_cast<float4*>(op);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) o4[i] = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
-              } else {
-                for (int i = 0; i < 32 && col + i < g.N; ++i) op[i] = o[i];
-              }
-            } else {
-              bf16* op = reinterpret_cast<bf16*>(g.out) + prow * g.ldo + g.col_off + col;
-              if (full32 && ((g.ldo | g.col_off) & 7) == 0) {
-                uint4* o4 = reinterpret_cast<uint4*>(op);
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-                  o4[i] = make_uint4(pack_bf16(o[8 * i], o[8 * i + 1]), pack_bf16(o[8 * i + 2], o[8 * i + 3]),
-                                     pack_bf16(o[8 * i + 4], o[8 * i + 5]), pack_bf16(o[8 * i + 6], o[8 * i + 7]));
-              } else {
-                for (int i = 0; i < 32 && col + i < g.N; ++i) op[i] = __float2bfloat16(o[i]);
-              }
-            }
-          }
-        }
-      }
+      epilogue_tile<BN>(g, &tout, ec, tbase, mt * CG + (int)rank, nt * BN, q, lane);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if (CG == 1) {
+          mbar_arrive(&tempty[acc]);
+        } else {
+          const uint32_t a = leader_addr(&tempty[acc]);
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
+        }
+      }
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2)
+    cluster_sync();
+  else
+    __syncthreads();
   tc_fence_after();
-  if (warp == 1) tmem_dealloc(tmem_base, C::TMEM_COLS);
+  if (warp == 1) tmem_dealloc_cg<CG>(tmem_base, C::TMEM_COLS);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -335,7 +524,7 @@ static EncodeTiledFn encode_fn() {
 }
 
 static void make_map(CUtensorMap* m, const void* ptr, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
-                     const uint32_t* box) {
+                     const uint32_t* box, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   cuuint64_t gd[5], gs[5];
   cuuint32_t bx[5], es[5];
   for (int i = 0; i < rank; ++i) {
@@ -345,9 +534,16 @@ static void make_map(CUtensorMap* m, const void* ptr, int rank, const uint64_t* 
     if (i + 1 < rank) gs[i] = strides_bytes[i];
   }
   CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), gd, gs, bx, es,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+}
+
+void make_tmap_2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_bytes, uint32_t box_in,
+                  uint32_t box_out) {
+  uint64_t d[2] = {inner, outer}, s[1] = {row_bytes};
+  uint32_t b[2] = {box_in, box_out};
+  make_map(m, ptr, 2, d, s, b);
 }
 
 int num_sms() {
@@ -373,18 +569,32 @@ void conv3_tile_geometry(int B, int H, int W, int* wt, int* ht, int* bt) {
   (void)B;
 }
 
-template <int BN>
+
+template <int BN, int CG>
 static void launch(const CUtensorMap* m, const GemmArgs& a, cudaStream_t st) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, CG>;
   static bool attr_set = false;
   if (!attr_set) {
-    SD_CUDA(cudaFuncSetAttribute(gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    SD_CUDA(cudaFuncSetAttribute(gemm_kernel<BN, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr_set = true;
   }
   const int total = a.m_tiles * a.n_tiles;
-  const int grid = total < num_sms() ? total : num_sms();
-  if (grid <= 0) return;
-  gemm_kernel<BN><<<grid, 192, C::SMEM, st>>>(m[0], m[1], m[2], m[3], a);
+  int workers = num_sms() / CG;
+  if (total < workers) workers = total;
+  if (workers <= 0) return;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(workers * CG);
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SD_CUDA(cudaLaunchKernelEx(&cfg, gemm_kernel<BN, CG>, m[0], m[1], m[2], m[3], m[4], a));
   SD_CHECK_LAUNCH();
 }
 
@@ -397,29 +607,28 @@ static int pick_bn(int N, int act) {
   return 256;
 }
 
+int g_cg_override = -1;  // 0 = heuristic, 1 / 2 = force (tests, SD_GEMM_CG)
+
 void gemm(const GemmDesc& d, cudaStream_t st) {
+  if (g_cg_override < 0) {
+    const char* s = getenv("SD_GEMM_CG");
+    g_cg_override = s ? atoi(s) : 0;
+  }
   GemmArgs a{};
-  CUtensorMap maps[4];
+  CUtensorMap maps[5];
   memset(maps, 0, sizeof(maps));
   a.mode = d.mode;
   a.N = d.N;
   int bn = d.bn ? d.bn : pick_bn(d.N, d.act);
   if (d.act == ACT_GEGLU && bn % 128) throw CudaError("GEGLU needs BN multiple of 128");
   a.n_tiles = cdiv(d.N, bn);
+  int m_boxes = 0;
   if (d.mode == GEMM_DENSE) {
     if (d.K % 8 || d.lda % 8 || d.ldb % 8) throw CudaError("dense GEMM: K/lda/ldb must be multiples of 8");
     a.M = d.M;
-    a.m_tiles = cdiv(d.M, 128);
+    m_boxes = cdiv(d.M, 128);
     a.num_kb = cdiv(d.K, 64);
     a.nsrc = 1;
-    uint64_t dA[2] = {(uint64_t)d.K, (uint64_t)d.M}, sA[1] = {(uint64_t)d.lda * 2};
-    uint32_t bA[2] = {64, 128};
-    make_map(&maps[0], d.A, 2, dA, sA, bA);
-    uint64_t dB[2] = {(uint64_t)d.K, (uint64_t)d.N}, sB[1] = {(uint64_t)d.ldb * 2};
-    uint32_t bB[2] = {64, (uint32_t)bn};
-    make_map(&maps[2], d.Bw[0], 2, dB, sB, bB);
-    maps[1] = maps[0];
-    maps[3] = maps[2];
   } else {
     a.B = d.B;
     a.H = d.H;
@@ -428,20 +637,40 @@ void gemm(const GemmDesc& d, cudaStream_t st) {
     conv3_tile_geometry(d.B, d.H, d.W, &a.wt, &a.ht, &a.bt);
     a.tiles_x = cdiv(d.W, a.wt);
     a.tiles_y = cdiv(d.H, a.ht);
-    a.m_tiles = a.tiles_x * a.tiles_y * cdiv(d.B, a.bt);
+    m_boxes = a.tiles_x * a.tiles_y * cdiv(d.B, a.bt);
     a.nsrc = d.nsrc;
     a.num_kb = 0;
     for (int s = 0; s < d.nsrc; ++s) {
       if (d.cs[s] % 8) throw CudaError("conv3: channels must be a multiple of 8");
       a.kb_src[s] = cdiv(d.cs[s], 64);
       a.num_kb += 9 * a.kb_src[s];
+    }
+  }
+  int box_begin = d.m_tile_begin, box_count = d.m_tile_count >= 0 ? d.m_tile_count : m_boxes;
+  // pair tiles (256 rows, half of B per CTA) when the weights dominate the operand traffic
+  // (M ≤ 16·N; measured on B200: 16×16 / 8×8 / 32×32×1280 convs gain up to 1.4×, 64×64 ones lose)
+  int cg = ((long)box_count * 128 <= 16L * d.N && box_begin % 2 == 0 && bn >= 128) ? 2 : 1;
+  if (g_cg_override == 1 || g_cg_override == 2) cg = g_cg_override;
+  if (cg == 2 && (box_begin % 2 || bn < 128)) cg = 1;
+  const uint32_t brows = (uint32_t)(bn / cg);
+  if (d.mode == GEMM_DENSE) {
+    uint64_t dA[2] = {(uint64_t)d.K, (uint64_t)d.M}, sA[1] = {(uint64_t)d.lda * 2};
+    uint32_t bA[2] = {64, 128};
+    make_map(&maps[0], d.A, 2, dA, sA, bA);
+    uint64_t dB[2] = {(uint64_t)d.K, (uint64_t)d.N}, sB[1] = {(uint64_t)d.ldb * 2};
+    uint32_t bB[2] = {64, brows};
+    make_map(&maps[2], d.Bw[0], 2, dB, sB, bB);
+    maps[1] = maps[0];
+    maps[3] = maps[2];
+  } else {
+    for (int s = 0; s < d.nsrc; ++s) {
       uint64_t dA[4] = {(uint64_t)d.cs[s], (uint64_t)d.W, (uint64_t)d.H, (uint64_t)d.B};
       uint64_t sA[3] = {(uint64_t)d.cs[s] * 2, (uint64_t)d.cs[s] * 2 * d.W, (uint64_t)d.cs[s] * 2 * d.W * d.H};
       uint32_t bA[4] = {64, (uint32_t)a.wt, (uint32_t)a.ht, (uint32_t)a.bt};
       make_map(&maps[s], d.xs[s], 4, dA, sA, bA);
       uint64_t dB[3] = {(uint64_t)d.cs[s], 9, (uint64_t)d.N};
       uint64_t sB[2] = {(uint64_t)d.cs[s] * 2, (uint64_t)d.cs[s] * 2 * 9};
-      uint32_t bB[3] = {64, 1, (uint32_t)bn};
+      uint32_t bB[3] = {64, 1, brows};
       make_map(&maps[2 + s], d.Bw[s], 3, dB, sB, bB);
     }
     if (d.nsrc == 1) {
@@ -449,8 +678,8 @@ void gemm(const GemmDesc& d, cudaStream_t st) {
       maps[3] = maps[2];
     }
   }
-  a.m_tile_begin = d.m_tile_begin;
-  if (d.m_tile_count >= 0) a.m_tiles = d.m_tile_count;
+  a.m_tile_begin = box_begin / cg;
+  a.m_tiles = cdiv(box_count, cg);
   a.out = d.out;
   a.ldo = d.ldo;
   a.col_off = d.col_off;
@@ -464,12 +693,38 @@ void gemm(const GemmDesc& d, cudaStream_t st) {
   a.res = d.res;
   a.ldr = d.ldr;
   a.act = d.act;
-  switch (bn) {
-    case 64: launch<64>(maps, a, st); break;
-    case 128: launch<128>(maps, a, st); break;
-    case 160: launch<160>(maps, a, st); break;
-    case 256: launch<256>(maps, a, st); break;
-    default: throw CudaError("unsupported BN");
+  // bf16 outputs go through the TMA store path (box = one warp's 32 rows × 32 columns)
+  const int n_out = d.act == ACT_GEGLU ? d.N / 2 : d.N;
+  a.tma_store = (!d.out_f32 && d.ldo % 8 == 0 && d.col_off % 8 == 0 && n_out % 8 == 0) ? 1 : 0;
+  if (a.tma_store) {
+    const bf16* ob = reinterpret_cast<const bf16*>(d.out) + d.col_off;
+    if (d.mode == GEMM_DENSE) {
+      uint64_t dO[2] = {(uint64_t)n_out, (uint64_t)d.M}, sO[1] = {(uint64_t)d.ldo * 2};
+      uint32_t bO[2] = {32, 32};
+      make_map(&maps[4], ob, 2, dO, sO, bO, CU_TENSOR_MAP_SWIZZLE_64B);
+    } else {
+      const int sw = a.wt < 32 ? a.wt : 32;
+      const int sh = a.ht < 32 / sw ? a.ht : 32 / sw;
+      const int sb = 32 / (sw * sh);
+      uint64_t dO[4] = {(uint64_t)n_out, (uint64_t)d.W, (uint64_t)d.H, (uint64_t)d.B};
+      uint64_t sO[3] = {(uint64_t)d.ldo * 2, (uint64_t)d.ldo * 2 * d.W, (uint64_t)d.ldo * 2 * d.W * d.H};
+      uint32_t bO[4] = {32, (uint32_t)sw, (uint32_t)sh, (uint32_t)sb};
+      make_map(&maps[4], ob, 4, dO, sO, bO, CU_TENSOR_MAP_SWIZZLE_64B);
+    }
+  } else {
+    if (d.act == ACT_GEGLU) throw CudaError("GEGLU epilogue needs a bf16, 16-byte aligned output");
+    maps[4] = maps[0];
+  }
+  const int key = bn * 4 + cg;
+  switch (key) {
+    case 64 * 4 + 1: launch<64, 1>(maps, a, st); break;
+    case 128 * 4 + 1: launch<128, 1>(maps, a, st); break;
+    case 160 * 4 + 1: launch<160, 1>(maps, a, st); break;
+    case 256 * 4 + 1: launch<256, 1>(maps, a, st); break;
+    case 128 * 4 + 2: launch<128, 2>(maps, a, st); break;
+    case 160 * 4 + 2: launch<160, 2>(maps, a, st); break;
+    case 256 * 4 + 2: launch<256, 2>(maps, a, st); break;
+    default: throw CudaError("unsupported BN/CG");
   }
 }
 

@@ -50,5 +50,6 @@ void gemm(const GemmDesc& d, cudaStream_t st);
 // M tiles of a conv3 launch whose output rows lie in [y0, y1) of image 0 (used for bands).
 void conv3_tile_geometry(int B, int H, int W, int* wt, int* ht, int* bt);
 int num_sms();
+extern int g_cg_override;
 
 }  // namespace sd

@@ -39,6 +39,10 @@ struct AttnDesc {
 };
 void attention(const AttnDesc& a, cudaStream_t st);
 
+// tcgen05 flash attention (attention_tc.cu): qk [rows·P][2C] (q | k), vt [C][rows·P], O [rows·P][C]
+bool attention_tc_supported(int d, int P, int C);
+void attention_tc(const bf16* qk, const bf16* vt, bf16* O, int rows, int heads, int d, int C, int P, cudaStream_t st);
+
 // row softmax for the VAE attention path: P[r][:] = softmax(S[r][:]) (S fp32, P bf16)
 void softmax_rows(const float* S, bf16* P, int rows, int cols, cudaStream_t st);
 

@@ -98,19 +98,46 @@ __global__ void gn_apply_kernel(const bf16* __restrict__ x, int P, int C, int G,
   const int b = blockIdx.y, ch = blockIdx.x + c_base;
   const int cg = C / G;
   const int tid = ry * V + v;
-  for (int g = tid; g < G; g += V * R) {
-    float n = 0.f, mean = 0.f, m2 = 0.f;
-    for (int k = 0; k < nchunks; ++k) {
-      const GNPart pp = part[((long)b * nchunks + k) * G + g];
-      const float nb = (float)(min(P, (k + 1) * chunk_px) - k * chunk_px) * cg;
-      const float tot = n + nb;
-      const float d = pp.mean - mean;
-      mean += d * (nb / tot);
-      m2 += pp.m2 + d * d * (n * nb / tot);
-      n = tot;
+  // merge the chunk partials of every group: one warp per group, lane l merges chunks l, l+32, …
+  // sequentially, then a fixed butterfly (Chan) — deterministic and latency-light
+  const int nwarps = (V * R) / 32, wid = tid >> 5, lane = tid & 31;
+  if (wid < nwarps) {
+    for (int g = wid; g < G; g += nwarps) {
+      float n = 0.f, mean = 0.f, m2 = 0.f;
+      for (int k = lane; k < nchunks; k += 32) {
+        const GNPart pp = part[((long)b * nchunks + k) * G + g];
+        const float nb = (float)(min(P, (k + 1) * chunk_px) - k * chunk_px) * cg;
+        const float tot = n + nb;
+        const float d = pp.mean - mean;
+        mean += d * (nb / tot);
+        m2 += pp.m2 + d * d * (n * nb / tot);
+        n = tot;
+      }
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const float n2 = __shfl_xor_sync(0xffffffff, n, o);
+        const float mu2 = __shfl_xor_sync(0xffffffff, mean, o);
+        const float q2 = __shfl_xor_sync(0xffffffff, m2, o);
+        // combine (lower lane first so both partners compute the identical value)
+        const bool lo = (lane & o) == 0;
+        const float na = lo ? n : n2, ma = lo ? mean : mu2, qa = lo ? m2 : q2;
+        const float nb = lo ? n2 : n, mb = lo ? mu2 : mean, qb = lo ? q2 : m2;
+        const float tot = na + nb;
+        if (tot > 0.f) {
+          const float d = mb - ma;
+          mean = ma + d * (nb / tot);
+          m2 = qa + qb + d * d * (na * nb / tot);
+        } else {
+          mean = 0.f;
+          m2 = 0.f;
+        }
+        n = tot;
+      }
+      if (lane == 0) {
+        s_mean[g] = mean;
+        s_rstd[g] = rsqrtf(m2 / n + eps);
+      }
     }
-    s_mean[g] = mean;
-    s_rstd[g] = rsqrtf(m2 / n + eps);
   }
   __syncthreads();
   const int p0 = ch * chunk_px, p1 = min(P, p0 + chunk_px);
@@ -198,77 +225,95 @@ void group_norm(const bf16* x, bf16* y, int B, int P, int C, int G, const float*
   SD_CHECK_LAUNCH();
 }
 
-// ---- LayerNorm: one warp per token, two-pass in registers ---------------------------------------
-template <int NV>  // vectors (of 8) per lane, ceil(C/8/32)
+// ---- LayerNorm: LANES lanes per token (NV 16-byte vectors each), two-pass in registers ----------
+// C = 320/640/1280 → 8/16/32 lanes × 5 vectors: every lane issues all its loads up front and a warp
+// serves 4/2/1 tokens, so the per-token reduction is short and the loads are balanced.
+template <int NV, int LANES>
 __global__ void layer_norm_kernel(const bf16* __restrict__ x, int T, int C, const float* __restrict__ gamma,
                                   const float* __restrict__ beta, float eps, bf16* __restrict__ y) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (warp >= T) return;
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int tok = gtid / LANES, l = gtid % LANES;
+  if (tok >= T) return;  // LANES divides 32, so whole lane groups exit together
   const int V = C / 8;
-  const bf16* xr = x + (long)warp * C;
+  const bf16* xr = x + (long)tok * C;
   float f[NV][8];
   float s = 0.f;
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
-    const int vi = lane + 32 * k;
+    const int vi = l + LANES * k;
     if (vi < V) {
-      uint4 u = *reinterpret_cast<const uint4*>(xr + vi * 8);
+      const uint4 u = *reinterpret_cast<const uint4*>(xr + vi * 8);
       const bf16* e = reinterpret_cast<const bf16*>(&u);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        f[k][i] = __bfloat162float(e[i]);
-        s += f[k][i];
-      }
+      for (int i = 0; i < 8; ++i) f[k][i] = __bfloat162float(e[i]);
     } else {
 #pragma unroll
       for (int i = 0; i < 8; ++i) f[k][i] = 0.f;
     }
   }
 #pragma unroll
-  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffff, s, o);
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += f[k][i];
+#pragma unroll
+  for (int o = LANES / 2; o; o >>= 1) s += __shfl_xor_sync(0xffffffff, s, o);
   const float mean = s / C;
   float q = 0.f;
 #pragma unroll
   for (int k = 0; k < NV; ++k)
-    if (lane + 32 * k < V)
+    if (l + LANES * k < V)
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const float d = f[k][i] - mean;
         q += d * d;
       }
 #pragma unroll
-  for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffff, q, o);
+  for (int o = LANES / 2; o; o >>= 1) q += __shfl_xor_sync(0xffffffff, q, o);
   const float rstd = rsqrtf(q / C + eps);
-  bf16* yr = y + (long)warp * C;
+  bf16* yr = y + (long)tok * C;
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
-    const int vi = lane + 32 * k;
+    const int vi = l + LANES * k;
     if (vi < V) {
+      const float4 g0 = *reinterpret_cast<const float4*>(gamma + vi * 8);
+      const float4 g1 = *reinterpret_cast<const float4*>(gamma + vi * 8 + 4);
+      const float4 b0 = *reinterpret_cast<const float4*>(beta + vi * 8);
+      const float4 b1 = *reinterpret_cast<const float4*>(beta + vi * 8 + 4);
+      const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+      const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
       float o[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) o[i] = (f[k][i] - mean) * rstd * gamma[vi * 8 + i] + beta[vi * 8 + i];
+      for (int i = 0; i < 8; ++i) o[i] = (f[k][i] - mean) * rstd * gg[i] + bb[i];
       *reinterpret_cast<uint4*>(yr + vi * 8) =
           make_uint4(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]), pack_bf16(o[4], o[5]), pack_bf16(o[6], o[7]));
     }
   }
 }
 
+template <int NV, int LANES>
+static void ln_launch(const bf16* x, bf16* y, int T, int C, const float* g, const float* b, float eps,
+                      cudaStream_t st) {
+  const int threads = 256;
+  const long total = (long)T * LANES;
+  layer_norm_kernel<NV, LANES><<<cdiv(total, threads), threads, 0, st>>>(x, T, C, g, b, eps, y);
+  SD_CHECK_LAUNCH();
+}
+
 void layer_norm(const bf16* x, bf16* y, int T, int C, const float* gamma, const float* beta, float eps,
                 cudaStream_t st) {
   if (C % 8) throw CudaError("layer_norm: C % 8");
-  const int nv = cdiv(C / 8, 32);
-  const int threads = 256;
-  const int blocks = cdiv((long)T * 32, threads);
-  switch (nv) {
-    case 1: layer_norm_kernel<1><<<blocks, threads, 0, st>>>(x, T, C, gamma, beta, eps, y); break;
-    case 2: layer_norm_kernel<2><<<blocks, threads, 0, st>>>(x, T, C, gamma, beta, eps, y); break;
-    case 3: layer_norm_kernel<3><<<blocks, threads, 0, st>>>(x, T, C, gamma, beta, eps, y); break;
-    case 4: layer_norm_kernel<4><<<blocks, threads, 0, st>>>(x, T, C, gamma, beta, eps, y); break;
-    case 5: layer_norm_kernel<5><<<blocks, threads, 0, st>>>(x, T, C, gamma, beta, eps, y); break;
-    case 8: layer_norm_kernel<8><<<blocks, threads, 0, st>>>(x, T, C, gamma, beta, eps, y); break;
-    default: throw CudaError("layer_norm: C too large");
-  }
-  SD_CHECK_LAUNCH();
+  const int V = C / 8;
+  if (V == 40) return ln_launch<5, 8>(x, y, T, C, gamma, beta, eps, st);
+  if (V == 80) return ln_launch<5, 16>(x, y, T, C, gamma, beta, eps, st);
+  if (V == 160) return ln_launch<5, 32>(x, y, T, C, gamma, beta, eps, st);
+  if (V <= 4) return ln_launch<1, 4>(x, y, T, C, gamma, beta, eps, st);
+  if (V <= 8) return ln_launch<1, 8>(x, y, T, C, gamma, beta, eps, st);
+  if (V <= 16) return ln_launch<1, 16>(x, y, T, C, gamma, beta, eps, st);
+  if (V <= 32) return ln_launch<1, 32>(x, y, T, C, gamma, beta, eps, st);
+  if (V <= 64) return ln_launch<2, 32>(x, y, T, C, gamma, beta, eps, st);
+  if (V <= 128) return ln_launch<4, 32>(x, y, T, C, gamma, beta, eps, st);
+  if (V <= 256) return ln_launch<8, 32>(x, y, T, C, gamma, beta, eps, st);
+  throw CudaError("layer_norm: C too large");
 }
 
 }  // namespace sd

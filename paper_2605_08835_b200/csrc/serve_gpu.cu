@@ -290,6 +290,7 @@ extern "C" sd_status sd_poll(sd_engine* e, sd_completion* out, int32_t max, int3
     out[n].h = S->e->upscale() * t->h;
     out[n].w = S->e->upscale() * t->w;
     out[n].image_host = t->img_host;
+    out[n].skipped_steps = t->skips.data();
     ++n;
   }
   *n_out = n;

@@ -10,6 +10,14 @@ pytestmark = pytest.mark.gpu
 from paper_2605_08835_b200 import binding as B  # noqa: E402
 
 
+@pytest.fixture(params=[1, 2], autouse=True)
+def gemm_cg(request):
+    """Run every kernel test with 128-row CTA tiles and with 256-row CTA-pair (cta_group::2) tiles."""
+    B.call("sd_debug_set_gemm_cg", request.param)
+    yield request.param
+    B.call("sd_debug_set_gemm_cg", 0)
+
+
 def rel(a, b):
     return float((a.double() - b.double()).norm() / b.double().norm().clamp_min(1e-30))
 
@@ -93,5 +101,67 @@ def test_conv3x3_concat():
     y = torch.empty(nb, h, w, cout, device="cuda", dtype=torch.bfloat16)
     B.debug_conv3x3(x1.cuda(), c1, x2.cuda(), c2, _to_dev_w(wt[:, :c1]), _to_dev_w(wt[:, c1:]), b.cuda(), None, None,
                     y, nb, h, w, cout)
+    torch.cuda.synchronize()
+    assert rel(y.cpu(), ref) < 6e-3
+
+
+def _attn_ref(q, k, v, heads):
+    """q [R][L][C], k/v [R][S][C] → softmax(q kᵀ/√d) v per head, fp64 CPU."""
+    R, L, C = q.shape
+    d = C // heads
+    sp = lambda t: t.double().reshape(t.shape[0], t.shape[1], heads, d).permute(0, 2, 1, 3)
+    o = F.scaled_dot_product_attention(sp(q), sp(k), sp(v))
+    return o.permute(0, 2, 1, 3).reshape(R, L, C)
+
+
+@pytest.mark.parametrize("R,heads,d,L,S", [(2, 8, 40, 256, 256), (1, 8, 80, 128, 77), (3, 2, 16, 64, 8),
+                                           (2, 8, 160, 64, 64), (1, 10, 64, 200, 130)])
+def test_attention_mma(R, heads, d, L, S):
+    g = torch.Generator().manual_seed(L + S + d)
+    C = heads * d
+    q, k, v = (bf(torch.randn(R, n, C, generator=g)) for n in (L, S, S))
+    o = torch.empty(R, L, C, device="cuda", dtype=torch.bfloat16)
+    B.call("sd_debug_attention", B._p(q.cuda()), B._p(k.cuda()), B._p(v.cuda()), B._p(o), R, heads, d, L, S, None)
+    torch.cuda.synchronize()
+    assert rel(o.cpu(), _attn_ref(q.float(), k.float(), v.float(), heads)) < 1e-2
+
+
+@pytest.mark.parametrize("R,heads,d,P", [(2, 8, 40, 256), (1, 8, 80, 384), (2, 10, 64, 128), (1, 8, 40, 4096)])
+def test_attention_tcgen05(R, heads, d, P):
+    g = torch.Generator().manual_seed(P + d)
+    C = heads * d
+    q, k, v = (bf(torch.randn(R, P, C, generator=g) * (1.5 if i == 0 else 1.0)) for i in range(3))
+    qk = torch.cat([q, k], -1).reshape(R * P, 2 * C).contiguous().cuda()
+    vt = v.reshape(R * P, C).t().contiguous().cuda()
+    o = torch.empty(R * P, C, device="cuda", dtype=torch.bfloat16)
+    B.call("sd_debug_attention_tc", B._p(qk), B._p(vt), B._p(o), R, heads, d, P, None)
+    torch.cuda.synchronize()
+    assert rel(o.cpu().reshape(R, P, C), _attn_ref(q.float(), k.float(), v.float(), heads)) < 1e-2
+
+
+@pytest.mark.parametrize("nb,P,C,G,silu", [(2, 4096, 320, 32, 1), (3, 256, 1280, 32, 0), (1, 64, 2560, 32, 1),
+                                           (2, 64, 32, 8, 1), (1, 16384, 128, 32, 1)])
+def test_groupnorm(nb, P, C, G, silu):
+    g = torch.Generator().manual_seed(P + C)
+    x = bf(torch.randn(nb, P, C, generator=g) * 2 + 0.5)
+    gam, bet = 1 + 0.1 * torch.randn(C, generator=g), 0.1 * torch.randn(C, generator=g)
+    ref = F.group_norm(x.double().permute(0, 2, 1), G, gam.double(), bet.double(), 1e-5).permute(0, 2, 1)
+    if silu:
+        ref = F.silu(ref)
+    y = torch.empty(nb, P, C, device="cuda", dtype=torch.bfloat16)
+    B.call("sd_debug_groupnorm", B._p(x.cuda()), B._p(y), nb, P, C, G, B._p(gam.cuda()), B._p(bet.cuda()), 1e-5,
+           silu, None)
+    torch.cuda.synchronize()
+    assert rel(y.cpu(), ref) < 6e-3
+
+
+@pytest.mark.parametrize("T,C", [(1000, 320), (77, 640), (300, 1280), (64, 32), (100, 2048)])
+def test_layernorm(T, C):
+    g = torch.Generator().manual_seed(T + C)
+    x = bf(torch.randn(T, C, generator=g) * 3 - 1)
+    gam, bet = 1 + 0.1 * torch.randn(C, generator=g), 0.1 * torch.randn(C, generator=g)
+    ref = F.layer_norm(x.double(), (C,), gam.double(), bet.double(), 1e-5)
+    y = torch.empty(T, C, device="cuda", dtype=torch.bfloat16)
+    B.call("sd_debug_layernorm", B._p(x.cuda()), B._p(y), T, C, B._p(gam.cuda()), B._p(bet.cuda()), 1e-5, None)
     torch.cuda.synchronize()
     assert rel(y.cpu(), ref) < 6e-3

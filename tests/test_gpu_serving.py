@@ -1,0 +1,91 @@
+"""GPU serving loop (sd_serve_start / sd_submit / sd_poll) on the tiny config: every completed image
+equals the oracle's request-alone pipeline run with the skip schedule the server recorded (I5
+end to end through continuous batching, Skip-CFG and chunked VAE decode), and the timestamps are
+consistent (A ≤ U ≤ V)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import configs, pipeline, sampling, vae
+
+pytestmark = pytest.mark.gpu
+
+from paper_2605_08835_b200 import binding as B  # noqa: E402
+from paper_2605_08835_b200.engine import Engine  # noqa: E402
+
+
+def _table(cmax=3, bmax=4):
+    rows = []
+    for c in range(1, cmax + 1):
+        for m in range(0, bmax + 1):
+            for n in range(0, bmax + 1):
+                for k in range(0, m + 1):
+                    if (m == 0 and n == 0) or (m >= 1 and n > m) or (m == 0 and k):
+                        continue
+                    tu = 2000 + 500 * (2 * m - k) if m else 0
+                    tv = 4000 * n // c + 500 if n else 0
+                    tau = sum(max(tu, tv) for _ in range(c)) if n else c * tu
+                    delta = (c - 1) * max(tu, tv) + tv if n else 0
+                    rows.append((c, m, n, k, tau, delta))
+    n = len(rows)
+    h = C.c_void_p()
+    col = lambda i, t: (t * n)(*[r[i] for r in rows])
+    B.call("sd_table_from_arrays", n, col(0, C.c_int32), col(1, C.c_int32), col(2, C.c_int32), col(3, C.c_int32),
+           col(4, C.c_int64), col(5, C.c_int64), C.byref(h))
+    return h
+
+
+@pytest.mark.parametrize("cstar", [1, 2])
+def test_serving_tiny_matches_oracle_alone(cstar):
+    eng = Engine("tiny", max_latent_hw=8, b_max=4, c_max=3)
+    ctx_u = synth.uncond_embedding(0, 8, 32)
+    eng.set_uncond(torch.from_numpy(ctx_u))
+    tab = _table()
+    # aggressive controller so that Skip-CFG engages under the burst
+    ctl = B.ControllerConfig(cstar, 3, 4, 1, 1, 1_000_000, -1, 5)
+    cfg = B.ServeConfig(4, 1, 10, 0, cstar, ctl, tab, 8, 5)
+    B.call("sd_serve_start", eng.h, C.byref(cfg))
+    n = 10
+    embs = [synth.text_embedding(5, i, 8, 32) for i in range(n)]
+    steps = [4, 5, 4, 6, 4, 5, 4, 6, 5, 4]
+    for i in range(n):
+        r = B.Request(i, 1000 * i, steps[i], 7.5 - 0.5 * (i % 3), embs[i].ctypes.data, 8, 32)
+        B.call("sd_submit", eng.h, C.byref(r))
+    got = {}
+    out = (B.Completion * 16)()
+    cnt = C.c_int32()
+    for _ in range(400):
+        B.call("sd_poll", eng.h, out, 16, C.byref(cnt), 50)
+        for j in range(cnt.value):
+            c_ = out[j]
+            img = np.ctypeslib.as_array(C.cast(c_.image_host, C.POINTER(C.c_float)), shape=(3, c_.h, c_.w)).copy()
+            skips = [c_.skipped_steps[q] for q in range(c_.n_skipped)]
+            got[c_.id] = (c_.arrival_us, c_.denoise_done_us, c_.decode_done_us, skips, img)
+            B.call("sd_release", eng.h, c_.id)
+        if len(got) == n:
+            break
+    B.call("sd_serve_stop", eng.h)
+    eng.close()
+    assert len(got) == n
+    P = configs.unet_params(configs.TINY_UNET, 0, np.float32, bf16_weights=True)
+    V = configs.vae_params(configs.TINY_VAE, 0, np.float32, bf16_weights=True)
+    cu = synth.bf16_round(ctx_u)
+    worst = 0.0
+    total_skips = 0
+    for i in range(n):
+        A, U, Vt, skips, img = got[i]
+        assert A <= U <= Vt
+        total_skips += len(skips)
+        assert all(s >= (steps[i] + 1) // 2 for s in skips)          # s_min audit (most permissive level)
+        xT = synth.initial_noise(5, i, 8, 8)
+        x = pipeline.denoise(P, configs.TINY_UNET, xT, synth.bf16_round(embs[i]), cu, steps[i], 7.5 - 0.5 * (i % 3),
+                             "ddim", skip=set(skips))
+        ref = vae.decode(V, configs.TINY_VAE, x[None])[0]
+        r = np.linalg.norm(img - ref) / np.linalg.norm(ref)
+        worst = max(worst, r)
+    print(f"serving: worst image rel-L2 {worst:.3e}, skips taken {total_skips}")
+    assert worst <= 2e-2
+    B.lib().sd_table_free(tab)

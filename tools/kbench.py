@@ -25,14 +25,24 @@ GEMM = [  # (M, N, K, act)
 ]
 
 
+def cur():
+    return torch.cuda.current_stream().cuda_stream
+
+
 def timeit(fn, reps):
+    """Device time per call: `reps` calls captured in one CUDA graph (no host launch overhead)."""
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(reps):
+            fn()
+    g.replay()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(reps):
-        fn()
+    g.replay()
     e1.record()
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / reps
@@ -42,6 +52,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--only", default="")
+    ap.add_argument("--pick", type=int, default=-1, help="run only entry i of the selected list")
     args = ap.parse_args()
     peak = 1417.2
     p = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
@@ -50,12 +61,14 @@ def main():
     out = []
     tot_t = tot_f = 0.0
     if args.only in ("", "conv"):
-        for (R, H, W, ci, co, cnt) in CONV:
+        for i_, (R, H, W, ci, co, cnt) in enumerate(CONV):
+            if args.pick >= 0 and i_ != args.pick:
+                continue
             x = torch.randn(R, H, W, ci, device="cuda").to(torch.bfloat16)
             w = (torch.randn(co, 9, ci, device="cuda") / (9 * ci) ** 0.5).to(torch.bfloat16)
             b = torch.zeros(co, device="cuda")
             y = torch.empty(R, H, W, co, device="cuda", dtype=torch.bfloat16)
-            ms = timeit(lambda: B.debug_conv3x3(x, ci, None, 0, w, None, b, None, None, y, R, H, W, co), args.reps)
+            ms = timeit(lambda: B.debug_conv3x3(x, ci, None, 0, w, None, b, None, None, y, R, H, W, co, stream=cur()), args.reps)
             fl = 2.0 * R * H * W * co * 9 * ci
             tot_t += ms * cnt
             tot_f += fl * cnt
@@ -65,16 +78,56 @@ def main():
         print(json.dumps({"conv_weighted_tflops": tot_f / tot_t / 1e9, "frac": tot_f / tot_t / 1e9 / peak,
                           "conv_ms_per_step": tot_t}), flush=True)
     if args.only in ("", "gemm"):
-        for (M, N, K, act) in GEMM:
+        for i_, (M, N, K, act) in enumerate(GEMM):
+            if args.pick >= 0 and i_ != args.pick:
+                continue
             A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
             Wt = (torch.randn(N, K, device="cuda") / K ** 0.5).to(torch.bfloat16)
             b = torch.zeros(N, device="cuda")
             D = torch.empty(M, N // 2 if act == 2 else N, device="cuda", dtype=torch.bfloat16)
-            ms = timeit(lambda: B.debug_gemm(A, Wt, b, D, M, N, K, 0, act), args.reps)
+            ms = timeit(lambda: B.debug_gemm(A, Wt, b, D, M, N, K, 0, act, stream=cur()), args.reps)
             fl = 2.0 * M * N * K
             r = dict(kind="gemm", shape=[M, N, K, act], ms=ms, tflops=fl / ms / 1e9, frac=fl / ms / 1e9 / peak)
             out.append(r)
             print(json.dumps(r), flush=True)
+
+
+    if args.only in ("", "norm"):
+        hbm = 6446.9
+        for i_, (nb, P, C) in enumerate([(16, 4096, 320), (16, 1024, 640), (16, 256, 1280), (16, 4096, 640),
+                                          (1, 262144, 128)]):
+            if args.pick >= 0 and i_ != args.pick:
+                continue
+            x = torch.randn(nb, P, C, device="cuda").to(torch.bfloat16)
+            y = torch.empty_like(x)
+            gam, bet = torch.ones(C, device="cuda"), torch.zeros(C, device="cuda")
+            ms = timeit(lambda: B.call("sd_debug_groupnorm", B._p(x), B._p(y), nb, P, C, 32, B._p(gam), B._p(bet),
+                                       1e-5, 1, B._p(cur())), args.reps)
+            by = 3.0 * x.numel() * 2
+            print(json.dumps(dict(kind="groupnorm", shape=[nb, P, C], ms=ms, gbs=by / ms / 1e6,
+                                  frac=by / ms / 1e6 / hbm)), flush=True)
+            ms = timeit(lambda: B.call("sd_debug_layernorm", B._p(x), B._p(y), nb * P, C, B._p(gam), B._p(bet), 1e-5,
+                                       B._p(cur())), args.reps)
+            by = 2.0 * x.numel() * 2
+            print(json.dumps(dict(kind="layernorm", shape=[nb * P, C], ms=ms, gbs=by / ms / 1e6,
+                                  frac=by / ms / 1e6 / hbm)), flush=True)
+    if args.only in ("", "attn"):
+        for i_, (R, heads, d, P) in enumerate([(16, 8, 40, 4096), (16, 8, 80, 1024), (16, 10, 64, 4096)]):
+            if args.pick >= 0 and i_ != args.pick:
+                continue
+            C = heads * d
+            qk = torch.randn(R * P, 2 * C, device="cuda").to(torch.bfloat16)
+            vt = torch.randn(C, R * P, device="cuda").to(torch.bfloat16)
+            o = torch.empty(R * P, C, device="cuda", dtype=torch.bfloat16)
+            fl = 4.0 * R * heads * P * P * d
+            ms = timeit(lambda: B.call("sd_debug_attention_tc", B._p(qk), B._p(vt), B._p(o), R, heads, d, P,
+                                       B._p(cur())), args.reps)
+            print(json.dumps(dict(kind="attn_tc", shape=[R, heads, d, P], ms=ms, tflops=fl / ms / 1e9,
+                                  exp_per_s=R * heads * P * P / ms / 1e3)), flush=True)
+            q, k, v = (torch.randn(R, P, C, device="cuda").to(torch.bfloat16) for _ in range(3))
+            ms = timeit(lambda: B.call("sd_debug_attention", B._p(q), B._p(k), B._p(v), B._p(o), R, heads, d, P, P,
+                                       B._p(cur())), args.reps)
+            print(json.dumps(dict(kind="attn_mma", shape=[R, heads, d, P], ms=ms, tflops=fl / ms / 1e9)), flush=True)
 
 
 if __name__ == "__main__":
