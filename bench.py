@@ -152,6 +152,78 @@ def config(n):
             "l2": "inputs larger than L2: 1.7 GB of UNet weights and >40 MB per activation stream through HBM"}
 
 
+def serving_bench(eng, world, rank, args):
+    """CFG#3-shaped serving on this GPU (and, for N > 1, every rank serves its shard id mod P with
+    the per-rank loads all-gathered over NCCL for the controller — weak scaling):
+      1. offline profiler: τ/δ table for c ∈ {1, 2}, m ≤ 8, n ≤ 3 on two streams (§III-C)
+      2. C₁ = saturation throughput (16 requests arriving at t = 0)
+      3. a Poisson trace at λ = ρ·C₁ per GPU, steps U{20..50}, g = 7.5 → images/s, mean / P99 E2E."""
+    import threading
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_08835_b200 import binding as Bd
+    from paper_2605_08835_b200 import profiler, serving
+    t0 = time.perf_counter()
+    prof = profiler.Profiler(eng, LAT, LAT, N_REQ, reps=1)
+    tab = prof.measure([1, 2], b_max=N_REQ, n_max=3)
+    prof.close()
+    h = profiler.to_table_handle(tab)
+    c_max, c_star, _ = profiler.chunk_choice(tab, [1, 2], m=N_REQ, n=1)
+    c_max = max(c_max, c_star)
+    t_prof = time.perf_counter() - t0
+    stop = threading.Event()
+    if world > 1:
+        import ctypes as C
+
+        def control():  # C1: all-gather of per-rank loads, then sd_set_global_load
+            mine = (C.c_int32 * 4)()
+            loads = torch.zeros(4, dtype=torch.int32, device=f"cuda:{rank}")
+            allv = torch.zeros(4 * world, dtype=torch.int32, device=f"cuda:{rank}")
+            epoch = 0
+            while not stop.is_set():
+                try:
+                    Bd.lib().sd_get_load(eng.h, mine)
+                    loads.copy_(torch.tensor(list(mine), dtype=torch.int32))
+                    dist.all_gather_into_tensor(allv, loads)
+                    arr = (C.c_int32 * (4 * world))(*allv.cpu().tolist())
+                    Bd.lib().sd_set_global_load(eng.h, arr, world, epoch)
+                except Exception:
+                    pass
+                epoch += 1
+                time.sleep(0.05)
+    cal_trace = [(i, 0, n) for (i, _, n) in serving.poisson_trace(16, 0.0, seed=11)]
+    _, cal = serving.run_trace(eng, h, cal_trace, LAT, N_REQ, c_star, c_max, n_max=3)
+    c1 = cal["images_per_s"]
+    full = serving.poisson_trace(args.serving_requests * world, args.rho * c1 * world, seed=7)
+    mine_tr = [(i, a, n) for (i, a, n) in full if i % world == rank]
+    th = None
+    if world > 1:
+        th = threading.Thread(target=control, daemon=True)
+        th.start()
+    _, m = serving.run_trace(eng, h, mine_tr, LAT, N_REQ, c_star, c_max, n_max=3)
+    stop.set()
+    if th:
+        th.join(timeout=5)
+    Bd.lib().sd_table_free(h)
+    out = {"workload": f"CFG#3-shaped: SD-1.5 512², Poisson λ = {args.rho}·C₁ per GPU, steps U{{20..50}}, g 7.5, "
+                       f"controller on, c* = {c_star}, C_max = {c_max}, B_max = 8",
+           "c1_images_per_s": c1, "rho": args.rho, "table_entries": len(tab), "profile_s": t_prof,
+           "per_rank": m}
+    if world > 1:
+        vec = torch.tensor([m["images_per_s"], m["mean_e2e_ms"], m["p99_e2e_ms"]], dtype=torch.float64,
+                           device=f"cuda:{rank}")
+        g = [torch.zeros_like(vec) for _ in range(world)]
+        dist.all_gather(g, vec)
+        out["images_per_s"] = float(sum(x[0].item() for x in g))
+        out["mean_e2e_ms"] = float(max(x[1].item() for x in g))
+        out["p99_e2e_ms"] = float(max(x[2].item() for x in g))
+    else:
+        out.update(images_per_s=m["images_per_s"], mean_e2e_ms=m["mean_e2e_ms"], p99_e2e_ms=m["p99_e2e_ms"])
+    return out
+
+
 # ------------------------------------------------------------------------------------------------
 # our arm
 # ------------------------------------------------------------------------------------------------
@@ -164,6 +236,9 @@ def main():
     ap.add_argument("--denoise-steps", type=int, default=N_STEPS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-serving", action="store_true")
+    ap.add_argument("--serving-requests", type=int, default=48)
+    ap.add_argument("--rho", type=float, default=0.8)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -281,6 +356,14 @@ def main():
                "note": "per step: H2D of 8 prompt embeddings + 8 noise latents (pinned), text K/V admission, "
                        "50 steps, 8 decodes, D2H of 8 images"}
 
+    # ---- continuous-batching serving (CFG#3 shape): offline profile → trace → mean / P99 E2E ----
+    serving_out = None
+    if not args.no_serving:
+        try:
+            serving_out = serving_bench(eng, world, rank, args)
+        except Exception as ex:  # the serving leg must never sink the bench line
+            serving_out = {"error": repr(ex)}
+
     if rank == 0:
         sus, burst, hbm, src = peaks()
         conv_ms, conv_n, conv_flops = prof[0]
@@ -311,6 +394,7 @@ def main():
             "clocks": clk.summary(),
             "latency_ms": {"mean_e2e": ms_max / args.steps, "p99_e2e": ms_max / args.steps,
                            "note": "lockstep batch: all 8 images of a step complete together"},
+            "serving": serving_out,
         }
         if not args.no_cpu_baseline:
             try:

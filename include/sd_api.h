@@ -164,6 +164,7 @@ typedef struct {
   const sd_table* table;        /* tau/delta table for c = 1..C_max (owned by the caller)        */
   int32_t latent_hw;            /* GPU mode: one resolution per server (R22)                     */
   uint64_t trace_seed;          /* GPU mode: initial noise z ~ N(0,1) keyed by (trace_seed, id)  */
+  int32_t n_max;                /* max decodes planned per window (0 = b_max); the table needs n ≤ n_max */
 } sd_serve_config;
 typedef struct {
   uint64_t id;

@@ -46,7 +46,7 @@ class ControllerConfig(C.Structure):
 class ServeConfig(C.Structure):
     _fields_ = [("b_max", C.c_int32), ("a_num", C.c_int32), ("a_den", C.c_int32), ("dp_mode", C.c_int32),
                 ("c_star", C.c_int32), ("ctl", ControllerConfig), ("table", C.c_void_p), ("latent_hw", C.c_int32),
-                ("trace_seed", C.c_uint64)]
+                ("trace_seed", C.c_uint64), ("n_max", C.c_int32)]
 
 
 class Request(C.Structure):

@@ -17,7 +17,10 @@
 
 namespace sd {
 
-template <int D>
+// NB = number of S (TMEM) / P (smem) buffers. NB = 2: one CTA per SM, S_{j+1} computed while the
+// softmax works on S_j. NB = 1: 256 TMEM columns and ~105 KB smem so two CTAs share an SM and
+// interleave their MMA / softmax phases (the MMA of S_{j+1} still overlaps the tail of softmax_j).
+template <int D, int NB>
 struct TcAttn {
   static constexpr int BQ = 128, BK = 128;
   static constexpr int KQ = (D + 63) / 64;       // 64-column blocks of the head dim (Q/K tiles)
@@ -27,10 +30,13 @@ struct TcAttn {
   static constexpr int K_BYTES = KQ * BK * 128;
   static constexpr int V_BYTES = 2 * NPV * 128;  // two 64-key blocks of Vᵀ rows
   static constexpr int STAGE = K_BYTES + V_BYTES;
-  static constexpr int STAGES = D <= 64 ? 3 : 2;
+  static constexpr int STAGES = (NB == 2 && D <= 64) ? 3 : 2;
   static constexpr int P_BYTES = 2 * BQ * 128;   // one P tile: 128 rows × 128 keys bf16
-  static constexpr int SMEM = 1024 + Q_BYTES + STAGES * STAGE + 2 * P_BYTES + 256;
+  static constexpr int SMEM = 1024 + Q_BYTES + STAGES * STAGE + NB * P_BYTES + 256;
+  static constexpr int TMEM_COLS = NB == 2 ? 512 : 256;
+  static constexpr int O_COL = NB * 128;         // O accumulator after the S buffers
   static_assert(V_BYTES % 1024 == 0, "Vᵀ tile rows must be a multiple of 8");
+  static_assert(NPV <= 128, "O must fit beside the S buffers");
 };
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
@@ -56,17 +62,17 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-template <int D>
-__global__ void __launch_bounds__(192, 1)
+template <int D, int NB>
+__global__ void __launch_bounds__(192, 3 - NB)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tqk, const __grid_constant__ CUtensorMap tvt, bf16* __restrict__ O,
                    int ldo, int C, int P, int Lk, float scale_log2) {
-  using A = TcAttn<D>;
+  using A = TcAttn<D, NB>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
   uint8_t* sKV = sQ + A::Q_BYTES;
   uint8_t* sP = sKV + A::STAGES * A::STAGE;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + 2 * A::P_BYTES);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + NB * A::P_BYTES);
   uint64_t* q_full = bar;
   uint64_t* kv_full = bar + 1;
   uint64_t* kv_empty = kv_full + A::STAGES;
@@ -99,7 +105,7 @@ __global__ void __launch_bounds__(192, 1)
     tma_prefetch(&tqk);
     tma_prefetch(&tvt);
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (warp == 1) tmem_alloc(tmem_slot, A::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -132,9 +138,9 @@ __global__ void __launch_bounds__(192, 1)
       const uint32_t aq = smem_u32(sQ);
       for (int j = 0; j <= nb; ++j) {
         if (j < nb) {
-          const int s = j % A::STAGES, sb = j & 1;
+          const int s = j % A::STAGES, sb = j % NB;
           mbar_wait(&kv_full[s], (j / A::STAGES) & 1);
-          if (j >= 2) mbar_wait(&s_empty[sb], ((j >> 1) - 1) & 1);
+          if (j >= NB) mbar_wait(&s_empty[sb], (j / NB - 1) & 1);
           tc_fence_after();
           const uint32_t ak = smem_u32(sKV + s * A::STAGE);
 #pragma unroll
@@ -145,8 +151,8 @@ __global__ void __launch_bounds__(192, 1)
           umma_commit(&s_full[sb]);
         }
         if (j >= 1) {
-          const int jp = j - 1, pb = jp & 1, sp = jp % A::STAGES;
-          mbar_wait(&p_full[pb], (jp >> 1) & 1);
+          const int jp = j - 1, pb = jp % NB, sp = jp % A::STAGES;
+          mbar_wait(&p_full[pb], (jp / NB) & 1);
           tc_fence_after();
           const uint32_t ap = smem_u32(sP + pb * A::P_BYTES);
           const uint32_t av = smem_u32(sKV + sp * A::STAGE + A::K_BYTES);
@@ -154,7 +160,7 @@ __global__ void __launch_bounds__(192, 1)
           for (int k = 0; k < 8; ++k) {
             const uint32_t offp = (k >> 2) * (A::BQ * 128) + (k & 3) * 32;
             const uint32_t offv = (k >> 2) * (A::NPV * 128) + (k & 3) * 32;
-            umma_bf16(tmem + 256, make_sdesc_sw128(ap + offp), make_sdesc_sw128(av + offv), id_pv, (jp | k) != 0);
+            umma_bf16(tmem + A::O_COL, make_sdesc_sw128(ap + offp), make_sdesc_sw128(av + offv), id_pv, (jp | k) != 0);
           }
           umma_commit(&kv_empty[sp]);
           umma_commit(pv_done);
@@ -181,42 +187,46 @@ __global__ void __launch_bounds__(192, 1)
     __syncwarp();
     if (lane == 0) mbar_arrive(q_ready);
     for (int j = 0; j < nb; ++j) {
-      const int sb = j & 1;
-      mbar_wait(&s_full[sb], (j >> 1) & 1);
+      const int sb = j % NB;
+      mbar_wait(&s_full[sb], (j / NB) & 1);
       tc_fence_after();
-      uint32_t v[128];
+      // pass 1: row max over the 128 scores (TMEM is re-read in pass 2 instead of holding 128
+      // registers; keys beyond Lk are masked)
+      const bool ragged = (j + 1) * A::BK > Lk;
+      float mx = m;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t t[32];
         tmem_ld32(tmem + lane_base + sb * 128 + c * 32, t);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[c * 32 + i] = t[i];
+        for (int i = 0; i < 32; ++i)
+          if (!ragged || j * A::BK + c * 32 + i < Lk) mx = fmaxf(mx, __uint_as_float(t[i]));
+      }
+      const float ms = mx * scale_log2;
+      const float alpha = ex2((m - mx) * scale_log2);
+      // pass 2: P = exp2(s·scale − m) packed to bf16
+      float sum = 0.f;
+      uint32_t pk[64];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t t[32];
+        tmem_ld32(tmem + lane_base + sb * 128 + c * 32, t);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          float s0 = __uint_as_float(t[2 * i]), s1 = __uint_as_float(t[2 * i + 1]);
+          if (ragged) {
+            if (j * A::BK + c * 32 + 2 * i >= Lk) s0 = -FLT_MAX;
+            if (j * A::BK + c * 32 + 2 * i + 1 >= Lk) s1 = -FLT_MAX;
+          }
+          const float p0 = ex2(fmaf(s0, scale_log2, -ms));
+          const float p1 = ex2(fmaf(s1, scale_log2, -ms));
+          sum += p0 + p1;
+          pk[c * 16 + i] = pack_bf16(p0, p1);
+        }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_empty[sb]);
-      float s[128];
-#pragma unroll
-      for (int i = 0; i < 128; ++i) s[i] = __uint_as_float(v[i]);
-      if ((j + 1) * A::BK > Lk) {
-#pragma unroll
-        for (int i = 0; i < 128; ++i)
-          if (j * A::BK + i >= Lk) s[i] = -FLT_MAX;
-      }
-      float mx = m;
-#pragma unroll
-      for (int i = 0; i < 128; ++i) mx = fmaxf(mx, s[i]);
-      const float ms = mx * scale_log2;
-      const float alpha = ex2((m - mx) * scale_log2);
-      float sum = 0.f;
-      uint32_t pk[64];
-#pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        const float p0 = ex2(fmaf(s[2 * i], scale_log2, -ms));
-        const float p1 = ex2(fmaf(s[2 * i + 1], scale_log2, -ms));
-        sum += p0 + p1;
-        pk[i] = pack_bf16(p0, p1);
-      }
       l = l * alpha + sum;
       m = mx;
       if (j >= 1) {
@@ -226,11 +236,11 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
           for (int c = 0; c < A::NPV / 16; ++c) {
             uint32_t o[16];
-            tmem_ld16(tmem + lane_base + 256 + c * 16, o);
+            tmem_ld16(tmem + lane_base + A::O_COL + c * 16, o);
             tmem_wait_ld();
 #pragma unroll
             for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tmem_st16(tmem + lane_base + 256 + c * 16, o);
+            tmem_st16(tmem + lane_base + A::O_COL + c * 16, o);
           }
           tmem_wait_st();
         }
@@ -259,7 +269,7 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
     for (int c = 0; c < A::NPV / 16; ++c) {
       uint32_t o[16];
-      tmem_ld16(tmem + lane_base + 256 + c * 16, o);
+      tmem_ld16(tmem + lane_base + A::O_COL + c * 16, o);
       tmem_wait_ld();
       if (qi < P) {
 #pragma unroll
@@ -278,19 +288,19 @@ __global__ void __launch_bounds__(192, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 1) tmem_dealloc(tmem, 512);
+  if (warp == 1) tmem_dealloc(tmem, A::TMEM_COLS);
 }
 
 // host ------------------------------------------------------------------------------------------
 void make_tmap_2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_bytes, uint32_t box_in,
                   uint32_t box_out);
 
-template <int D>
+template <int D, int NB>
 static void launch_tc(const bf16* qk, const bf16* vt, bf16* O, int rows, int heads, int C, int P, cudaStream_t st) {
-  using A = TcAttn<D>;
+  using A = TcAttn<D, NB>;
   static bool set = false;
   if (!set) {
-    SD_CUDA(cudaFuncSetAttribute(attn_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, A::SMEM));
+    SD_CUDA(cudaFuncSetAttribute(attn_tc_kernel<D, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, A::SMEM));
     set = true;
   }
   const long T = (long)rows * P;
@@ -299,7 +309,7 @@ static void launch_tc(const bf16* qk, const bf16* vt, bf16* O, int rows, int hea
   make_tmap_2d(&mvt, vt, (uint64_t)T, (uint64_t)C, (uint64_t)T * 2, 64, A::NPV);
   dim3 grid(cdiv(P, A::BQ), heads, rows);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)D);
-  attn_tc_kernel<D><<<grid, 192, A::SMEM, st>>>(mqk, mvt, O, C, C, P, P, scale_log2);
+  attn_tc_kernel<D, NB><<<grid, 192, A::SMEM, st>>>(mqk, mvt, O, C, C, P, P, scale_log2);
   SD_CHECK_LAUNCH();
 }
 
@@ -311,9 +321,9 @@ bool attention_tc_supported(int d, int P, int C) {
 void attention_tc(const bf16* qk, const bf16* vt, bf16* O, int rows, int heads, int d, int C, int P,
                   cudaStream_t st) {
   switch (d) {
-    case 40: launch_tc<40>(qk, vt, O, rows, heads, C, P, st); break;
-    case 64: launch_tc<64>(qk, vt, O, rows, heads, C, P, st); break;
-    case 80: launch_tc<80>(qk, vt, O, rows, heads, C, P, st); break;
+    case 40: launch_tc<40, 1>(qk, vt, O, rows, heads, C, P, st); break;
+    case 64: launch_tc<64, 1>(qk, vt, O, rows, heads, C, P, st); break;
+    case 80: launch_tc<80, 2>(qk, vt, O, rows, heads, C, P, st); break;
     default: throw CudaError("attention_tc: unsupported head dim");
   }
 }

@@ -42,6 +42,7 @@ struct GemmArgs {
   int ldr;
   int act;
   int tma_store;      // bf16 output through the per-warp smem slab + TMA store
+  int dbg;            // experiment switch (SD_EPI_DBG): 1 = no store, 2 = no bias, 3 = no TMEM load
 };
 
 template <int BN, int CG>
@@ -211,6 +212,19 @@ __device__ __forceinline__ void stage_store(const GemmArgs& g, const CUtensorMap
   ec.slot ^= 1;
 }
 
+// o[0..32) += p[0..32) with 16-byte read-only loads (p 16-byte aligned: bias / temb rows are)
+__device__ __forceinline__ void add32(float* o, const float* p) {
+  const float4* p4 = reinterpret_cast<const float4*>(p);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float4 v = __ldg(p4 + i);
+    o[4 * i] += v.x;
+    o[4 * i + 1] += v.y;
+    o[4 * i + 2] += v.z;
+    o[4 * i + 3] += v.w;
+  }
+}
+
 template <int BN>
 __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorMap* om, EpiCtx& ec, uint32_t tbase,
                                               int mbox, int n0, int q, int lane) {
@@ -251,16 +265,18 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
         const int ocol = (n0 >> 1) + j * 64 + h * 32;
         if (ocol >= (g.N >> 1)) continue;  // warp-uniform
         float o[32];
+        float vv[32], gg[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          float v = __uint_as_float(rv[i]) * g.alpha;
-          float gt = __uint_as_float(rg[i]) * g.alpha;
-          if (g.bias) {
-            v += g.bias[n0 + cv + i];
-            gt += g.bias[n0 + cgc + i];
-          }
-          o[i] = v * gelu_f(gt);
+          vv[i] = __uint_as_float(rv[i]) * g.alpha;
+          gg[i] = __uint_as_float(rg[i]) * g.alpha;
         }
+        if (g.bias) {
+          add32(vv, g.bias + n0 + cv);
+          add32(gg, g.bias + n0 + cgc);
+        }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o[i] = vv[i] * gelu_f(gg[i]);
         if (g.res && valid) {
           const bf16* rp = g.res + prow * g.ldr + ocol;
 #pragma unroll
@@ -274,27 +290,36 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
 #pragma unroll 1
   for (int c = 0; c < BN / 32; ++c) {
     uint32_t rv[32];
-    tmem_ld32(tbase + c * 32, rv);
+    if (g.dbg != 3) {
+      tmem_ld32(tbase + c * 32, rv);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) rv[i] = 0;
+    }
     const int col = n0 + c * 32;
     if (col >= g.N) continue;  // warp-uniform
     float o[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(rv[i]) * g.alpha;
     const bool full32 = col + 32 <= g.N;
-    if (g.bias) {
+    if (g.bias && g.dbg != 2) {
       if (g.bias_per_row) {
         const float bv = valid ? g.bias[prow] : 0.f;
 #pragma unroll
         for (int i = 0; i < 32; ++i) o[i] += bv;
+      } else if (full32) {
+        add32(o, g.bias + col);
       } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) o[i] += (full32 || col + i < g.N) ? g.bias[col + i] : 0.f;
+        for (int i = 0; i < 32 && col + i < g.N; ++i) o[i] += __ldg(g.bias + col + i);
       }
     }
     if (g.temb && valid) {
       const float* tp = g.temb + (long)img * g.ld_temb + col;
-#pragma unroll
-      for (int i = 0; i < 32; ++i) o[i] += (full32 || col + i < g.N) ? tp[i] : 0.f;
+      if (full32) {
+        add32(o, tp);
+      } else {
+        for (int i = 0; i < 32 && col + i < g.N; ++i) o[i] += __ldg(tp + i);
+      }
     }
     if (g.act == ACT_SILU) {
 #pragma unroll
@@ -315,7 +340,9 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
         for (int i = 0; i < 32 && col + i < g.N; ++i) o[i] += __bfloat162float(rp[i]);
       }
     }
-    if (g.tma_store) {
+    if (g.dbg == 1) {
+      if (o[0] == 12345.f) g.res ? (void)0 : __trap();
+    } else if (g.tma_store) {
       stage_store(g, om, ec, o, col, lane);
     } else if (valid) {
       if (g.out_f32) {
@@ -329,7 +356,15 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
         }
       } else {
         bf16* op = reinterpret_cast<bf16*>(g.out) + prow * g.ldo + g.col_off + col;
-        for (int i = 0; i < 32 && col + i < g.N; ++i) op[i] = __float2bfloat16(o[i]);
+        if (full32 && ((g.ldo | g.col_off) & 7) == 0) {
+          uint4* o4 = reinterpret_cast<uint4*>(op);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            o4[i] = make_uint4(pack_bf16(o[8 * i], o[8 * i + 1]), pack_bf16(o[8 * i + 2], o[8 * i + 3]),
+                               pack_bf16(o[8 * i + 4], o[8 * i + 5]), pack_bf16(o[8 * i + 6], o[8 * i + 7]));
+        } else {
+          for (int i = 0; i < 32 && col + i < g.N; ++i) op[i] = __float2bfloat16(o[i]);
+        }
       }
     }
   }
@@ -696,6 +731,15 @@ void gemm(const GemmDesc& d, cudaStream_t st) {
   // bf16 outputs go through the TMA store path (box = one warp's 32 rows × 32 columns)
   const int n_out = d.act == ACT_GEGLU ? d.N / 2 : d.N;
   a.tma_store = (!d.out_f32 && d.ldo % 8 == 0 && d.col_off % 8 == 0 && n_out % 8 == 0) ? 1 : 0;
+  {
+    static int dbg = -1;
+    if (dbg < 0) {
+      const char* s = getenv("SD_EPI_DBG");
+      dbg = s ? atoi(s) : 0;
+    }
+    a.dbg = dbg;
+    if (dbg == 4) a.tma_store = 0;  // direct stores
+  }
   if (a.tma_store) {
     const bf16* ob = reinterpret_cast<const bf16*>(d.out) + d.col_off;
     if (d.mode == GEMM_DENSE) {

@@ -15,7 +15,7 @@ struct GNPart {
   float mean, m2;
 };
 
-int gn_chunk_px(int C) { return C <= 256 ? 128 : C <= 512 ? 64 : C <= 1024 ? 32 : 16; }
+int gn_chunk_px(int C) { return C <= 512 ? 128 : C <= 1024 ? 64 : C <= 2048 ? 32 : 16; }
 
 static dim3 gn_block(int C) {
   const int V = C / 8;
@@ -89,55 +89,60 @@ __global__ void gn_stats_kernel(const bf16* __restrict__ x, int P, int C, int G,
   }
 }
 
+// finalize: one warp per (image, group): lane l merges chunks l, l+32, … sequentially, then a fixed
+// butterfly (Chan) — deterministic; writes (mean, rstd) for the apply kernels
+__global__ void gn_finalize_kernel(int P, int C, int G, int chunk_px, int nchunks, const GNPart* __restrict__ part,
+                                   float eps, float2* __restrict__ stats) {
+  const int lane = threadIdx.x & 31;
+  const int g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int b = blockIdx.y;
+  if (g >= G) return;
+  const int cg = C / G;
+  float n = 0.f, mean = 0.f, m2 = 0.f;
+  for (int k = lane; k < nchunks; k += 32) {
+    const GNPart pp = part[((long)b * nchunks + k) * G + g];
+    const float nb = (float)(min(P, (k + 1) * chunk_px) - k * chunk_px) * cg;
+    const float tot = n + nb;
+    const float d = pp.mean - mean;
+    mean += d * (nb / tot);
+    m2 += pp.m2 + d * d * (n * nb / tot);
+    n = tot;
+  }
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const float n2 = __shfl_xor_sync(0xffffffff, n, o);
+    const float mu2 = __shfl_xor_sync(0xffffffff, mean, o);
+    const float q2 = __shfl_xor_sync(0xffffffff, m2, o);
+    const bool lo = (lane & o) == 0;  // lower lane first: both partners compute the identical value
+    const float na = lo ? n : n2, ma = lo ? mean : mu2, qa = lo ? m2 : q2;
+    const float nb = lo ? n2 : n, mb = lo ? mu2 : mean, qb = lo ? q2 : m2;
+    const float tot = na + nb;
+    if (tot > 0.f) {
+      const float d = mb - ma;
+      mean = ma + d * (nb / tot);
+      m2 = qa + qb + d * d * (na * nb / tot);
+    } else {
+      mean = 0.f;
+      m2 = 0.f;
+    }
+    n = tot;
+  }
+  if (lane == 0) stats[(long)b * G + g] = make_float2(mean, rsqrtf(m2 / n + eps));
+}
+
 __global__ void gn_apply_kernel(const bf16* __restrict__ x, int P, int C, int G, int chunk_px, int c_base,
-                                int nchunks, const GNPart* __restrict__ part, const float* __restrict__ gamma,
-                                const float* __restrict__ beta, float eps, int silu, bf16* __restrict__ y) {
-  __shared__ float s_mean[64], s_rstd[64];
-  const int V = blockDim.x, R = blockDim.y;
+                                const float2* __restrict__ stats, const float* __restrict__ gamma,
+                                const float* __restrict__ beta, int silu, bf16* __restrict__ y) {
+  const int R = blockDim.y;
   const int v = threadIdx.x, ry = threadIdx.y;
   const int b = blockIdx.y, ch = blockIdx.x + c_base;
   const int cg = C / G;
-  const int tid = ry * V + v;
-  // merge the chunk partials of every group: one warp per group, lane l merges chunks l, l+32, …
-  // sequentially, then a fixed butterfly (Chan) — deterministic and latency-light
-  const int nwarps = (V * R) / 32, wid = tid >> 5, lane = tid & 31;
-  if (wid < nwarps) {
-    for (int g = wid; g < G; g += nwarps) {
-      float n = 0.f, mean = 0.f, m2 = 0.f;
-      for (int k = lane; k < nchunks; k += 32) {
-        const GNPart pp = part[((long)b * nchunks + k) * G + g];
-        const float nb = (float)(min(P, (k + 1) * chunk_px) - k * chunk_px) * cg;
-        const float tot = n + nb;
-        const float d = pp.mean - mean;
-        mean += d * (nb / tot);
-        m2 += pp.m2 + d * d * (n * nb / tot);
-        n = tot;
-      }
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const float n2 = __shfl_xor_sync(0xffffffff, n, o);
-        const float mu2 = __shfl_xor_sync(0xffffffff, mean, o);
-        const float q2 = __shfl_xor_sync(0xffffffff, m2, o);
-        // combine (lower lane first so both partners compute the identical value)
-        const bool lo = (lane & o) == 0;
-        const float na = lo ? n : n2, ma = lo ? mean : mu2, qa = lo ? m2 : q2;
-        const float nb = lo ? n2 : n, mb = lo ? mu2 : mean, qb = lo ? q2 : m2;
-        const float tot = na + nb;
-        if (tot > 0.f) {
-          const float d = mb - ma;
-          mean = ma + d * (nb / tot);
-          m2 = qa + qb + d * d * (na * nb / tot);
-        } else {
-          mean = 0.f;
-          m2 = 0.f;
-        }
-        n = tot;
-      }
-      if (lane == 0) {
-        s_mean[g] = mean;
-        s_rstd[g] = rsqrtf(m2 / n + eps);
-      }
-    }
+  __shared__ float s_mean[64], s_rstd[64];
+  const int tid = ry * blockDim.x + v;
+  if (tid < G) {
+    const float2 st = stats[(long)b * G + tid];
+    s_mean[tid] = st.x;
+    s_rstd[tid] = st.y;
   }
   __syncthreads();
   const int p0 = ch * chunk_px, p1 = min(P, p0 + chunk_px);
@@ -182,7 +187,18 @@ __global__ void gn_apply_kernel(const bf16* __restrict__ x, int P, int C, int G,
   }
 }
 
-size_t gn_workspace_bytes(int B, int P, int G) { return (size_t)B * cdiv(P, 16) * G * sizeof(GNPart) + 256; }
+static size_t gn_part_bytes(int B, int P, int G) {
+  return ((size_t)B * cdiv(P, 16) * G * sizeof(GNPart) + 255) & ~size_t(255);
+}
+size_t gn_workspace_bytes(int B, int P, int G) { return gn_part_bytes(B, P, G) + (size_t)B * G * sizeof(float2) + 256; }
+
+static void gn_finalize(int B, int P, int C, int G, int cp, void* ws, float eps, cudaStream_t st) {
+  const int wpb = 4;  // warps per block
+  gn_finalize_kernel<<<dim3(cdiv(G, wpb), B), 32 * wpb, 0, st>>>(
+      P, C, G, cp, cdiv(P, cp), reinterpret_cast<const GNPart*>(ws), eps,
+      reinterpret_cast<float2*>(reinterpret_cast<char*>(ws) + gn_part_bytes(B, P, G)));
+  SD_CHECK_LAUNCH();
+}
 
 static void check_gn(int C, int G) {
   if (C % 8 || C / 8 > 1024 || G > 64 || C % G) throw CudaError("group_norm: unsupported C/G");
@@ -205,9 +221,10 @@ void gn_apply_range(const bf16* x, bf16* y, int P, int C, int G, int p0, int p1,
   check_gn(C, G);
   const int cp = gn_chunk_px(C);
   const dim3 blk = gn_block(C);
-  gn_apply_kernel<<<dim3(cdiv(p1, cp) - p0 / cp, 1), blk, 0, st>>>(x, P, C, G, cp, p0 / cp, cdiv(P, cp),
-                                                                    reinterpret_cast<const GNPart*>(ws), gamma, beta,
-                                                                    eps, silu ? 1 : 0, y);
+  if (p0 == 0) gn_finalize(1, P, C, G, cp, ws, eps, st);  // bands run in order: finalize before band 0
+  gn_apply_kernel<<<dim3(cdiv(p1, cp) - p0 / cp, 1), blk, 0, st>>>(
+      x, P, C, G, cp, p0 / cp, reinterpret_cast<const float2*>(reinterpret_cast<char*>(ws) + gn_part_bytes(1, P, G)),
+      gamma, beta, silu ? 1 : 0, y);
   SD_CHECK_LAUNCH();
 }
 
@@ -221,7 +238,10 @@ void group_norm(const bf16* x, bf16* y, int B, int P, int C, int G, const float*
   const size_t sh = (size_t)blk.x * blk.y * 8 * 2 * sizeof(float);
   gn_stats_kernel<<<dim3(nch, B), blk, sh, st>>>(x, P, C, G, cp, 0, nch, part);
   SD_CHECK_LAUNCH();
-  gn_apply_kernel<<<dim3(nch, B), blk, 0, st>>>(x, P, C, G, cp, 0, nch, part, gamma, beta, eps, silu ? 1 : 0, y);
+  gn_finalize(B, P, C, G, cp, ws, eps, st);
+  gn_apply_kernel<<<dim3(nch, B), blk, 0, st>>>(
+      x, P, C, G, cp, 0, reinterpret_cast<const float2*>(reinterpret_cast<char*>(ws) + gn_part_bytes(B, P, G)), gamma,
+      beta, silu ? 1 : 0, y);
   SD_CHECK_LAUNCH();
 }
 

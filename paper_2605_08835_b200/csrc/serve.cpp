@@ -38,7 +38,7 @@ bool Loop::window(Exec& ex) {
   const int M = (int)batch.size();
   std::vector<STask*> dq = dec;
   std::sort(dq.begin(), dq.end(), [](const STask* a, const STask* b) { return a->A != b->A ? a->A < b->A : a->id < b->id; });
-  if ((int)dq.size() > cfg.b_max) dq.resize(cfg.b_max);
+  if ((int)dq.size() > std::min(cfg.b_max, cfg.n_max)) dq.resize(std::min(cfg.b_max, cfg.n_max));
   const int N = (int)dq.size();
   std::vector<uint8_t> elig(M);
   int K = 0;
@@ -160,6 +160,7 @@ extern "C" sd_status sd_serve_simulate(const sd_serve_config* cfg, const sd_tabl
   std::vector<STask> tasks(n);
   Loop L;
   L.cfg.b_max = cfg->b_max;
+  L.cfg.n_max = cfg->n_max > 0 ? cfg->n_max : cfg->b_max;
   L.cfg.a_num = cfg->a_num;
   L.cfg.a_den = cfg->a_den;
   L.cfg.dp_mode = cfg->dp_mode;

@@ -33,6 +33,7 @@ struct STask {
 
 struct LoopCfg {
   int b_max = 8;
+  int n_max = 8;  // decodes per window
   int a_num = 1, a_den = 10;
   int dp_mode = 0;
   int c_star = 1;

@@ -213,6 +213,7 @@ extern "C" sd_status sd_serve_start(sd_engine* e, const sd_serve_config* cfg) {
   S->e = &e->e;
   S->cfg = *cfg;
   S->loop.cfg.b_max = cfg->b_max;
+  S->loop.cfg.n_max = cfg->n_max > 0 ? cfg->n_max : cfg->b_max;
   S->loop.cfg.a_num = cfg->a_num;
   S->loop.cfg.a_den = cfg->a_den;
   S->loop.cfg.dp_mode = cfg->dp_mode;

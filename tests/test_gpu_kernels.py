@@ -121,7 +121,8 @@ def test_attention_mma(R, heads, d, L, S):
     C = heads * d
     q, k, v = (bf(torch.randn(R, n, C, generator=g)) for n in (L, S, S))
     o = torch.empty(R, L, C, device="cuda", dtype=torch.bfloat16)
-    B.call("sd_debug_attention", B._p(q.cuda()), B._p(k.cuda()), B._p(v.cuda()), B._p(o), R, heads, d, L, S, None)
+    qd, kd, vd = q.cuda(), k.cuda(), v.cuda()       # keep the device copies alive across the call
+    B.call("sd_debug_attention", B._p(qd), B._p(kd), B._p(vd), B._p(o), R, heads, d, L, S, None)
     torch.cuda.synchronize()
     assert rel(o.cpu(), _attn_ref(q.float(), k.float(), v.float(), heads)) < 1e-2
 
@@ -149,8 +150,8 @@ def test_groupnorm(nb, P, C, G, silu):
     if silu:
         ref = F.silu(ref)
     y = torch.empty(nb, P, C, device="cuda", dtype=torch.bfloat16)
-    B.call("sd_debug_groupnorm", B._p(x.cuda()), B._p(y), nb, P, C, G, B._p(gam.cuda()), B._p(bet.cuda()), 1e-5,
-           silu, None)
+    xd, gd, bd = x.cuda(), gam.cuda(), bet.cuda()
+    B.call("sd_debug_groupnorm", B._p(xd), B._p(y), nb, P, C, G, B._p(gd), B._p(bd), 1e-5, silu, None)
     torch.cuda.synchronize()
     assert rel(y.cpu(), ref) < 6e-3
 
@@ -162,6 +163,7 @@ def test_layernorm(T, C):
     gam, bet = 1 + 0.1 * torch.randn(C, generator=g), 0.1 * torch.randn(C, generator=g)
     ref = F.layer_norm(x.double(), (C,), gam.double(), bet.double(), 1e-5)
     y = torch.empty(T, C, device="cuda", dtype=torch.bfloat16)
-    B.call("sd_debug_layernorm", B._p(x.cuda()), B._p(y), T, C, B._p(gam.cuda()), B._p(bet.cuda()), 1e-5, None)
+    xd, gd, bd = x.cuda(), gam.cuda(), bet.cuda()
+    B.call("sd_debug_layernorm", B._p(xd), B._p(y), T, C, B._p(gd), B._p(bd), 1e-5, None)
     torch.cuda.synchronize()
     assert rel(y.cpu(), ref) < 6e-3
