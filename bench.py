@@ -177,20 +177,23 @@ def serving_bench(eng, world, rank, args):
     if world > 1:
         import ctypes as C
 
-        def control():  # C1: all-gather of per-rank loads, then sd_set_global_load
+        def control():
+            """C1: all-gather of per-rank loads {waiting, decode-pending, active, completed} (+ a done
+            flag so every rank leaves the loop after the same number of collectives), then
+            sd_set_global_load so each controller sees the global waiting queue."""
             mine = (C.c_int32 * 4)()
-            loads = torch.zeros(4, dtype=torch.int32, device=f"cuda:{rank}")
-            allv = torch.zeros(4 * world, dtype=torch.int32, device=f"cuda:{rank}")
+            loads = torch.zeros(5, dtype=torch.int32, device=f"cuda:{rank}")
+            allv = torch.zeros(5 * world, dtype=torch.int32, device=f"cuda:{rank}")
             epoch = 0
-            while not stop.is_set():
-                try:
-                    Bd.lib().sd_get_load(eng.h, mine)
-                    loads.copy_(torch.tensor(list(mine), dtype=torch.int32))
-                    dist.all_gather_into_tensor(allv, loads)
-                    arr = (C.c_int32 * (4 * world))(*allv.cpu().tolist())
-                    Bd.lib().sd_set_global_load(eng.h, arr, world, epoch)
-                except Exception:
-                    pass
+            while True:
+                Bd.lib().sd_get_load(eng.h, mine)
+                loads.copy_(torch.tensor(list(mine) + [1 if stop.is_set() else 0], dtype=torch.int32))
+                dist.all_gather_into_tensor(allv, loads)
+                v = allv.cpu().tolist()
+                if all(v[5 * r + 4] for r in range(world)):
+                    break
+                flat = [x for r in range(world) for x in v[5 * r:5 * r + 4]]
+                Bd.lib().sd_set_global_load(eng.h, (C.c_int32 * (4 * world))(*flat), world, epoch)
                 epoch += 1
                 time.sleep(0.05)
     cal_trace = [(i, 0, n) for (i, _, n) in serving.poisson_trace(16, 0.0, seed=11)]
@@ -205,7 +208,7 @@ def serving_bench(eng, world, rank, args):
     _, m = serving.run_trace(eng, h, mine_tr, LAT, N_REQ, c_star, c_max, n_max=3)
     stop.set()
     if th:
-        th.join(timeout=5)
+        th.join(timeout=600)  # leaves once every rank reported done (same number of collectives)
     Bd.lib().sd_table_free(h)
     out = {"workload": f"CFG#3-shaped: SD-1.5 512², Poisson λ = {args.rho}·C₁ per GPU, steps U{{20..50}}, g 7.5, "
                        f"controller on, c* = {c_star}, C_max = {c_max}, B_max = 8",

@@ -322,7 +322,7 @@ void attention_tc(const bf16* qk, const bf16* vt, bf16* O, int rows, int heads, 
                   cudaStream_t st) {
   switch (d) {
     case 40: launch_tc<40, 1>(qk, vt, O, rows, heads, C, P, st); break;
-    case 64: launch_tc<64, 1>(qk, vt, O, rows, heads, C, P, st); break;
+    case 64: launch_tc<64, 2>(qk, vt, O, rows, heads, C, P, st); break;  // measured: NB=2 1.18× faster at d=64
     case 80: launch_tc<80, 2>(qk, vt, O, rows, heads, C, P, st); break;
     default: throw CudaError("attention_tc: unsupported head dim");
   }

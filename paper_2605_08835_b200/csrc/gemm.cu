@@ -4,7 +4,7 @@
 //   warp 0      TMA producer   (one elected lane): A and B tiles into a STAGES-deep smem ring
 //   warp 1      MMA issuer     (one elected lane of the leader CTA): tcgen05.mma into a
 //                              double-buffered TMEM accumulator; also owns TMEM alloc/dealloc
-//   warps 2..5  epilogue       tcgen05.ld → bias / temb / act / residual → bf16|fp32 stores
+//   warps 2..9  epilogue       tcgen05.ld → bias / temb / act / residual → bf16|fp32 stores
 // CG = 1: one CTA computes a 128×BN tile.
 // CG = 2: a CTA pair (cluster of 2, cta_group::2) computes a 256×BN tile: each CTA loads its 128
 //         rows of A and half of B, the leader issues 256×BN×16 MMAs reading both CTAs' smem, and
@@ -52,10 +52,10 @@ struct Cfg {
   static constexpr int B_ROWS = BN / CG;                         // B rows loaded by this CTA
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (184 * 1024) / STAGE > 8 ? 8 : (184 * 1024) / STAGE;
+  static constexpr int STAGES = (192 * 1024) / STAGE > 8 ? 8 : (192 * 1024) / STAGE;
   static constexpr int TMEM_STRIDE = BN <= 64 ? 64 : (BN <= 128 ? 128 : 256);
   static constexpr int TMEM_COLS = 2 * TMEM_STRIDE;
-  static constexpr int STAGING = 4 * 2 * 2048;                   // 4 epilogue warps × 2 slabs
+  static constexpr int STAGING = 8 * 2 * 2048;                   // 8 epilogue warps × 2 slabs
   static constexpr int SMEM = 1024 + STAGES * STAGE + STAGING + 256;
   static_assert(B_BYTES % 1024 == 0, "B tile must be a whole number of 8-row swizzle groups");
 };
@@ -227,7 +227,7 @@ __device__ __forceinline__ void add32(float* o, const float* p) {
 
 template <int BN>
 __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorMap* om, EpiCtx& ec, uint32_t tbase,
-                                              int mbox, int n0, int q, int lane) {
+                                              int mbox, int n0, int q, int lane, int half) {
   const int r = q * 32 + lane;
   long prow;
   int img;
@@ -257,7 +257,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
 #pragma unroll 1
     for (int j = 0; j < BN / 128; ++j) {
 #pragma unroll 1
-      for (int h = 0; h < 2; ++h) {
+      for (int h = half; h < 2; h += 2) {  // the two epilogue warps of a lane quarter split the halves
         uint32_t rv[32], rg[32];
         const int cv = j * 128 + h * 32, cgc = cv + 64;
         tmem_ld32(tbase + cv, rv);
@@ -288,7 +288,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
     return;
   }
 #pragma unroll 1
-  for (int c = 0; c < BN / 32; ++c) {
+  for (int c = half; c < BN / 32; c += 2) {  // two epilogue warps per lane quarter: alternate chunks
     uint32_t rv[32];
     if (g.dbg != 3) {
       tmem_ld32(tbase + c * 32, rv);
@@ -371,7 +371,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
 }
 
 template <int BN, int CG>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ CUtensorMap ta1,
                 const __grid_constant__ CUtensorMap tb0, const __grid_constant__ CUtensorMap tb1,
                 const __grid_constant__ CUtensorMap tout, const GemmArgs g) {
@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 4 * CG);
+      mbar_init(&tempty[s], 8 * CG);
     }
     fence_mbar_init();
     tma_prefetch(&ta0);
@@ -504,7 +504,8 @@ __global__ void __launch_bounds__(192, 1)
     }
     __syncwarp();
   } else {
-    // ================= epilogue (warps 2..5 → TMEM lane quarters 2,3,0,1) =================
+    // ===== epilogue (warps 2..9 → TMEM lane quarters 2,3,0,1,2,3,0,1; two warps per quarter split
+    // the 32-column chunks, so the epilogue keeps up with short-K tiles) =====
     const int q = warp & 3;
     EpiCtx ec{sStage + (warp - 2) * 4096, 0, 0, 0, 0};
     int it = 0;
@@ -515,7 +516,7 @@ __global__ void __launch_bounds__(192, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * C::TMEM_STRIDE;
-      epilogue_tile<BN>(g, &tout, ec, tbase, mt * CG + (int)rank, nt * BN, q, lane);
+      epilogue_tile<BN>(g, &tout, ec, tbase, mt * CG + (int)rank, nt * BN, q, lane, (warp - 2) >> 2);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -619,7 +620,7 @@ static void launch(const CUtensorMap* m, const GemmArgs& a, cudaStream_t st) {
   if (workers <= 0) return;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(workers * CG);
-  cfg.blockDim = dim3(192);
+  cfg.blockDim = dim3(320);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];

@@ -20,6 +20,7 @@ enum { NBUF = 6 };
 
 struct DecodeState {
   int h = 0, w = 0, n_chunks = 0, next_chunk = 0;
+  bool banded = true;
   Arena ar;
   size_t buf_elems = 0;
   bf16* buf[NBUF];
@@ -30,7 +31,9 @@ struct DecodeState {
   std::vector<int> bounds;
 };
 
-static int band_rows(int H) { return H >= 64 ? 32 : std::max(8, H / 2); }
+// row bands of the tail layers: 32 rows (≥ 64-row layers) when the decode is chunked; one band per
+// layer for a whole decode (fewer launches; same values — banding is bitwise neutral, I6)
+static int band_rows(int H, bool banded) { return banded ? (H >= 64 ? 32 : std::max(8, H / 2)) : H; }
 
 static void conv_desc(GemmDesc& d, const bf16* x, int H, int W, int C, const bf16* w, int N, const float* b, void* out,
                       const bf16* res) {
@@ -164,7 +167,7 @@ static void build_items(Engine* e, DecodeState* s) {
       const int t2 = other({cur, t1});
       const int t3 = other({cur, t1, t2});
       const int y = other({cur, t1, t2, t3});
-      const int br = band_rows(H);
+      const int br = band_rows(H, s->banded);
       auto push_gn = [&](int src, int dst, const float* gam, const float* bet, int C) {
         for (int yy = 0; yy < H; yy += br) {
           VItem v{VOP_GN_STATS, src, dst, 0, gam, C, 0, H, W, yy, std::min(H, yy + br), gn_id, 1};
@@ -206,7 +209,7 @@ static void build_items(Engine* e, DecodeState* s) {
       const int C = u.ch;
       H *= 2;
       W *= 2;
-      const int br = band_rows(H);
+      const int br = band_rows(H, s->banded);
       for (int yy = 0; yy < H; yy += br) {
         VItem v{VOP_UPSAMPLE, cur, 5, -1, nullptr, C, C, H, W, yy, std::min(H, yy + br), 0, 0};
         it.push_back(v);
@@ -224,7 +227,7 @@ static void build_items(Engine* e, DecodeState* s) {
   const int C0 = c.block_out[0];
   const int t1 = other({cur});
   {
-    const int br = band_rows(H);
+    const int br = band_rows(H, s->banded);
     for (int yy = 0; yy < H; yy += br) {
       VItem v{VOP_GN_STATS, cur, t1, 0, e->V.nout_g, C0, 0, H, W, yy, std::min(H, yy + br), gn_id, 1};
       it.push_back(v);
@@ -376,6 +379,10 @@ void vae_decode_chunk(Engine* e, const float* z, int h, int w, int n_chunks, int
     if (!s) s = new_decode(e, h, w);
     s->n_chunks = n_chunks;
     s->next_chunk = 0;
+    if (s->banded != (n_chunks > 1)) {
+      s->banded = n_chunks > 1;
+      build_items(e, s);
+    }
     s->bounds = chunk_bounds(s->cost, n_chunks);
     *state = s;
   }
