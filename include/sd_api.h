@@ -225,6 +225,9 @@ sd_status sd_debug_layernorm(const void* x, void* y, int32_t T, int32_t C, const
                              float eps, void* stream);
 /* GEMM tile mode for the tests: 0 = heuristic, 1 = 128-row CTA tiles, 2 = 256-row CTA-pair tiles. */
 sd_status sd_debug_set_gemm_cg(int32_t cg);
+/* split-K of sd_debug_conv3x3: 0 = the production rule (conv layers of <= 64 pixels with >= 90 K
+ * blocks of 64 channels take 3 splits), 1 = off, 2..8 = forced; partials summed in split order. */
+sd_status sd_debug_set_conv_splits(int32_t splits);
 
 #ifdef __cplusplus
 }

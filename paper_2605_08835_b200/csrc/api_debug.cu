@@ -10,6 +10,8 @@ static thread_local std::string g_err;
 void set_error(const std::string& s) { g_err = s; }
 }  // namespace sd
 
+static int g_dbg_splits = 0;  // split-K of sd_debug_conv3x3 (0 = the production rule)
+
 extern "C" const char* sd_last_error(void) { return sd::g_err.c_str(); }
 
 extern "C" const char* sd_status_str(sd_status s) {
@@ -74,8 +76,19 @@ extern "C" sd_status sd_debug_conv3x3(const void* x, int32_t cin, const void* x2
   d.ld_temb = cout;
   d.res = static_cast<const bf16*>(res);
   d.ldr = cout;
-  sd::gemm(d, static_cast<cudaStream_t>(stream));
+  d.splits = g_dbg_splits;
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  d.split_ws_bytes = sd::gemm_split_ws_bytes(d);
+  if (d.split_ws_bytes) SD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d.split_ws), d.split_ws_bytes, st));
+  sd::gemm(d, st);
+  if (d.split_ws) SD_CUDA(cudaFreeAsync(d.split_ws, st));
   SD_API_END
+}
+
+extern "C" sd_status sd_debug_set_conv_splits(int32_t splits) {
+  SD_REQUIRE(splits >= 0 && splits <= 8, "sd_debug_set_conv_splits: 0 (auto), 1 (off) or 2..8");
+  g_dbg_splits = splits;
+  return SD_OK;
 }
 
 extern "C" sd_status sd_debug_set_gemm_cg(int32_t cg) {

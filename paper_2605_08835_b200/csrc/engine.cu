@@ -346,7 +346,9 @@ static size_t unet_ws_bytes(const Engine* e) {
   const int c0 = e->uc.block_out[0];
   // ≈ 60 tensors of R·P·c0 at the top level dominate (level k has P/4^k pixels, ≤ 4·c0 channels)
   const double top = (double)R * P * c0 * 2;
-  return (size_t)(top * 140) + ((size_t)512 << 20);
+  // + split-K partials of one ≤ 64-pixel conv (≤ 8 splits × R·64 rows × 2·c_max fp32)
+  const double split = 8.0 * R * 64 * 2 * e->uc.block_out.back() * 4;
+  return (size_t)(top * 140 + split) + ((size_t)512 << 20);
 }
 
 void build_engine(Engine* e) {
@@ -485,9 +487,13 @@ struct Fwd {
     d.res = res;
     d.ldr = N;
     d.out_f32 = out_f32;
+    const size_t mk = e->ws.mark();
+    d.split_ws_bytes = gemm_split_ws_bytes(d);
+    if (d.split_ws_bytes) d.split_ws = e->ws.get<float>(d.split_ws_bytes / sizeof(float));
     const int pi = e->prof.begin(PC_CONV, st, 2.0 * R * H * W * N * 9.0 * (c_real ? c_real : C));
     gemm(d, st);
     e->prof.end(pi, st);
+    e->ws.reset(mk);
   }
 
   bf16* resblock(const ResW& r, const bf16* x, int H, int W) {

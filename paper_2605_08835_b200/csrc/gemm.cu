@@ -43,7 +43,20 @@ struct GemmArgs {
   int act;
   int tma_store;      // bf16 output through the per-warp smem slab + TMA store
   int dbg;            // experiment switch (SD_EPI_DBG): 1 = no store, 2 = no bias, 3 = no TMEM load
+  int splits, kps;    // split-K: K blocks [s·kps, (s+1)·kps) of split s
+  float* part;        // split-K fp32 partials [splits][M][N] (raw accumulators)
 };
+
+// tile t → (M tile, N tile, K-block range); tiles of split s follow those of split s-1
+__device__ __forceinline__ void decode_tile(const GemmArgs& g, int t, int& mt, int& nt, int& s, int& kb0, int& kb1) {
+  const int per = g.m_tiles * g.n_tiles;
+  s = t / per;
+  const int r = t - s * per;
+  mt = g.m_tile_begin + r / g.n_tiles;
+  nt = r % g.n_tiles;
+  kb0 = s * g.kps;
+  kb1 = min(g.num_kb, kb0 + g.kps);
+}
 
 template <int BN, int CG>
 struct Cfg {
@@ -227,7 +240,7 @@ __device__ __forceinline__ void add32(float* o, const float* p) {
 
 template <int BN>
 __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorMap* om, EpiCtx& ec, uint32_t tbase,
-                                              int mbox, int n0, int q, int lane, int half) {
+                                              int mbox, int n0, int q, int lane, int half, int split) {
   const int r = q * 32 + lane;
   long prow;
   int img;
@@ -298,6 +311,22 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
     }
     const int col = n0 + c * 32;
     if (col >= g.N) continue;  // warp-uniform
+    if (g.splits > 1) {
+      // split-K: raw fp32 partial sums; bias / temb / act / residual are applied by splitk_reduce
+      if (valid) {
+        float* pp = g.part + ((long)split * g.M + prow) * g.N + col;
+        if (col + 32 <= g.N) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            reinterpret_cast<float4*>(pp)[i] =
+                make_float4(__uint_as_float(rv[4 * i]), __uint_as_float(rv[4 * i + 1]),
+                            __uint_as_float(rv[4 * i + 2]), __uint_as_float(rv[4 * i + 3]));
+        } else {
+          for (int i = 0; i < 32 && col + i < g.N; ++i) pp[i] = __uint_as_float(rv[i]);
+        }
+      }
+      continue;
+    }
     float o[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(rv[i]) * g.alpha;
@@ -415,7 +444,7 @@ __global__ void __launch_bounds__(320, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int total = g.m_tiles * g.n_tiles;
+  const int total = g.m_tiles * g.n_tiles * g.splits;
   const int worker = blockIdx.x / CG, nworkers = gridDim.x / CG;
 
   if (warp == 0) {
@@ -424,7 +453,8 @@ __global__ void __launch_bounds__(320, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = worker; t < total; t += nworkers) {
-        const int mt = g.m_tile_begin + t / g.n_tiles, nt = t % g.n_tiles;
+        int mt, nt, sp, kb0, kb1;
+        decode_tile(g, t, mt, nt, sp, kb0, kb1);
         const int mbox = mt * CG + (int)rank;  // this CTA's 128-row box
         const int n0 = nt * BN + (int)rank * C::B_ROWS;
         int m0 = 0, x0 = 0, y0 = 0, b0 = 0;
@@ -438,7 +468,7 @@ __global__ void __launch_bounds__(320, 1)
           y0 = ty * g.ht;
           b0 = tb * g.bt;
         }
-        for (int kb = 0; kb < g.num_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint32_t bar_l = 0;
           if (CG == 1) {
@@ -485,14 +515,17 @@ __global__ void __launch_bounds__(320, 1)
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * C::TMEM_STRIDE;
-        for (int kb = 0; kb < g.num_kb; ++kb) {
+        int mt, nt, sp, kb0, kb1;
+        decode_tile(g, t, mt, nt, sp, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
           const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
 #pragma unroll
           for (int k = 0; k < C::BK / 16; ++k)
-            mma<CG>(d, make_sdesc_sw128(a0 + k * 32), make_sdesc_sw128(b0 + k * 32), idesc, (kb | k) != 0);
+            mma<CG>(d, make_sdesc_sw128(a0 + k * 32), make_sdesc_sw128(b0 + k * 32), idesc,
+                    (kb != kb0 || k != 0) ? 1u : 0u);
           commit<CG>(&empty[stage]);
           if (++stage == C::STAGES) {
             stage = 0;
@@ -512,11 +545,12 @@ __global__ void __launch_bounds__(320, 1)
     for (int t = worker; t < total; t += nworkers, ++it) {
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
-      const int mt = g.m_tile_begin + t / g.n_tiles, nt = t % g.n_tiles;
+      int mt, nt, sp, kb0, kb1;
+      decode_tile(g, t, mt, nt, sp, kb0, kb1);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * C::TMEM_STRIDE;
-      epilogue_tile<BN>(g, &tout, ec, tbase, mt * CG + (int)rank, nt * BN, q, lane, (warp - 2) >> 2);
+      epilogue_tile<BN>(g, &tout, ec, tbase, mt * CG + (int)rank, nt * BN, q, lane, (warp - 2) >> 2, sp);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -606,6 +640,35 @@ void conv3_tile_geometry(int B, int H, int W, int* wt, int* ht, int* bt) {
 }
 
 
+// split-K reduction: out = epilogue(Σ_s part[s]) in fixed split order (deterministic)
+__global__ void splitk_reduce_kernel(const float* __restrict__ part, int S, long M, int N, const float* __restrict__ bias,
+                                     const float* __restrict__ temb, int ld_temb, int rows_per_img,
+                                     const bf16* __restrict__ res, int ldr, int act, float alpha, bf16* __restrict__ out,
+                                     int ldo, int col_off) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;  // one group of 4 columns
+  const int nq = N / 4;
+  if (i >= M * nq) return;
+  const long m = i / nq;
+  const int n = (int)(i % nq) * 4;
+  float4 acc = reinterpret_cast<const float4*>(part + m * N + n)[0];
+  for (int s = 1; s < S; ++s) {
+    const float4 v = reinterpret_cast<const float4*>(part + ((long)s * M + m) * N + n)[0];
+    acc.x += v.x;
+    acc.y += v.y;
+    acc.z += v.z;
+    acc.w += v.w;
+  }
+  float o[4] = {acc.x * alpha, acc.y * alpha, acc.z * alpha, acc.w * alpha};
+  for (int k = 0; k < 4; ++k) {
+    if (bias) o[k] += bias[n + k];
+    if (temb) o[k] += temb[(m / rows_per_img) * ld_temb + n + k];
+    if (act == ACT_SILU) o[k] = silu_f(o[k]);
+    if (res) o[k] += __bfloat162float(res[m * ldr + n + k]);
+  }
+  uint2 pk = make_uint2(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]));
+  *reinterpret_cast<uint2*>(out + m * ldo + col_off + n) = pk;
+}
+
 template <int BN, int CG>
 static void launch(const CUtensorMap* m, const GemmArgs& a, cudaStream_t st) {
   using C = Cfg<BN, CG>;
@@ -614,7 +677,7 @@ static void launch(const CUtensorMap* m, const GemmArgs& a, cudaStream_t st) {
     SD_CUDA(cudaFuncSetAttribute(gemm_kernel<BN, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr_set = true;
   }
-  const int total = a.m_tiles * a.n_tiles;
+  const int total = a.m_tiles * a.n_tiles * a.splits;
   int workers = num_sms() / CG;
   if (total < workers) workers = total;
   if (workers <= 0) return;
@@ -644,6 +707,39 @@ static int pick_bn(int N, int act) {
 }
 
 int g_cg_override = -1;  // 0 = heuristic, 1 / 2 = force (tests, SD_GEMM_CG)
+
+static int conv_num_kb(const GemmDesc& d) {
+  int kb = 0;
+  for (int s = 0; s < d.nsrc; ++s) kb += 9 * cdiv(d.cs[s], 64);
+  return kb;
+}
+
+int gemm_splits(const GemmDesc& d) {
+  static int env = -2;
+  if (env == -2) {
+    const char* s = getenv("SD_SPLITK");
+    env = s ? atoi(s) : -1;
+  }
+  if (d.splits == 1 || d.mode != GEMM_CONV3) return 1;
+  if (d.act == ACT_GEGLU || d.out_f32 || d.bias_per_row || d.N % 4 || d.ldo % 4 || d.col_off % 4) return 1;
+  const int kb = conv_num_kb(d);
+  int s = d.splits;
+  if (s == 0) {
+    // the 8×8 level of SD-1.5 (1280 / 2560 channels): 40 output tiles at 8 requests × CFG leave
+    // most of the 148 SMs idle over 180–360 K blocks; 3 splits make one full wave
+    if ((long)d.H * d.W > 64 || kb < 90) return 1;
+    s = env >= 0 ? env : 3;
+  }
+  s = std::max(1, std::min(s, std::min(8, kb)));
+  const int kps = cdiv(kb, s);
+  return cdiv(kb, kps);
+}
+
+size_t gemm_split_ws_bytes(const GemmDesc& d) {
+  const int s = gemm_splits(d);
+  if (s <= 1) return 0;
+  return (size_t)s * d.B * d.H * d.W * d.N * sizeof(float);
+}
 
 void gemm(const GemmDesc& d, cudaStream_t st) {
   if (g_cg_override < 0) {
@@ -680,6 +776,17 @@ void gemm(const GemmDesc& d, cudaStream_t st) {
       if (d.cs[s] % 8) throw CudaError("conv3: channels must be a multiple of 8");
       a.kb_src[s] = cdiv(d.cs[s], 64);
       a.num_kb += 9 * a.kb_src[s];
+    }
+  }
+  a.splits = 1;
+  a.kps = a.num_kb;
+  a.part = nullptr;
+  {
+    const int s = gemm_splits(d);
+    if (s > 1 && d.m_tile_count < 0 && d.split_ws && d.split_ws_bytes >= gemm_split_ws_bytes(d)) {
+      a.kps = cdiv(a.num_kb, s);
+      a.splits = s;
+      a.part = d.split_ws;
     }
   }
   int box_begin = d.m_tile_begin, box_count = d.m_tile_count >= 0 ? d.m_tile_count : m_boxes;
@@ -731,7 +838,7 @@ void gemm(const GemmDesc& d, cudaStream_t st) {
   a.act = d.act;
   // bf16 outputs go through the TMA store path (box = one warp's 32 rows × 32 columns)
   const int n_out = d.act == ACT_GEGLU ? d.N / 2 : d.N;
-  a.tma_store = (!d.out_f32 && d.ldo % 8 == 0 && d.col_off % 8 == 0 && n_out % 8 == 0) ? 1 : 0;
+  a.tma_store = (!d.out_f32 && d.ldo % 8 == 0 && d.col_off % 8 == 0 && n_out % 8 == 0 && a.splits == 1) ? 1 : 0;
   {
     static int dbg = -1;
     if (dbg < 0) {
@@ -770,6 +877,13 @@ void gemm(const GemmDesc& d, cudaStream_t st) {
     case 160 * 4 + 2: launch<160, 2>(maps, a, st); break;
     case 256 * 4 + 2: launch<256, 2>(maps, a, st); break;
     default: throw CudaError("unsupported BN/CG");
+  }
+  if (a.splits > 1) {
+    const long n4 = (long)a.M * (d.N / 4);
+    splitk_reduce_kernel<<<(unsigned)cdiv(n4, 256), 256, 0, st>>>(
+        a.part, a.splits, a.M, d.N, d.bias, d.temb, d.ld_temb, d.H * d.W, d.res, d.ldr, d.act, d.alpha,
+        reinterpret_cast<bf16*>(d.out), d.ldo, d.col_off);
+    SD_CHECK_LAUNCH();
   }
 }
 

@@ -44,9 +44,17 @@ struct GemmDesc {
   int act = ACT_NONE;
   int m_tile_begin = 0, m_tile_count = -1;  // restrict to a contiguous range of M tiles (bands)
   int bn = 0;                 // N tile (64/128/160/256), 0 = auto
+  // split-K (deterministic: fp32 partials per split, summed in split order by a reduce kernel).
+  // 0 = auto (conv3 layers of ≤ 64 pixels with ≥ 90 K blocks — a function of the layer only, so
+  // results stay batch-invariant), 1 = off. Needs split_ws of gemm_split_ws_bytes(d) bytes, else off.
+  int splits = 0;
+  float* split_ws = nullptr;
+  size_t split_ws_bytes = 0;
 };
 
 void gemm(const GemmDesc& d, cudaStream_t st);
+int gemm_splits(const GemmDesc& d);              // the split count gemm() will use given a workspace
+size_t gemm_split_ws_bytes(const GemmDesc& d);   // workspace bytes (0 when not split)
 // M tiles of a conv3 launch whose output rows lie in [y0, y1) of image 0 (used for bands).
 void conv3_tile_geometry(int B, int H, int W, int* wt, int* ht, int* bt);
 int num_sms();

@@ -91,6 +91,41 @@ def test_conv3x3(nb, h, w, cin, cout):
     assert rel(y.cpu(), ref) < 6e-3
 
 
+@pytest.mark.parametrize("splits", [2, 3, 5])
+@pytest.mark.parametrize("nb,h,w,c1,c2,cout", [(3, 5, 7, 200, 0, 100), (4, 8, 8, 640, 640, 320), (2, 8, 8, 1280, 0, 1280)])
+def test_conv3x3_splitk(splits, nb, h, w, c1, c2, cout):
+    """split-K (fp32 partials per K range, reduced in split order) vs fp64; deterministic and
+    batch-invariant: image 0 of a 1-image call equals image 0 of the nb-image call bit for bit."""
+    g = torch.Generator().manual_seed(splits * 100 + c1 + c2)
+    x1 = bf(torch.randn(nb, h, w, c1, generator=g))
+    x2 = bf(torch.randn(nb, h, w, c2, generator=g)) if c2 else None
+    cin = c1 + c2
+    wt = bf(torch.randn(cout, cin, 3, 3, generator=g) / (9 * cin) ** 0.5)
+    b = torch.randn(cout, generator=g)
+    temb = torch.randn(nb, cout, generator=g)
+    res = bf(torch.randn(nb, h, w, cout, generator=g))
+    xin = x1 if x2 is None else torch.cat([x1, x2], -1)
+    ref = _conv_ref(xin.float(), wt.float(), b, temb, res.float())
+    dev = dict(x1=x1.cuda(), x2=x2.cuda() if c2 else None, w1=_to_dev_w(wt[:, :c1]),
+               w2=_to_dev_w(wt[:, c1:]) if c2 else None, b=b.cuda(), temb=temb.cuda(), res=res.cuda())
+
+    def run(n):
+        y = torch.empty(n, h, w, cout, device="cuda", dtype=torch.bfloat16)
+        B.debug_conv3x3(dev["x1"][:n], c1, None if x2 is None else dev["x2"][:n], c2, dev["w1"], dev["w2"], dev["b"],
+                        dev["temb"][:n], dev["res"][:n], y, n, h, w, cout)
+        torch.cuda.synchronize()
+        return y.cpu()
+
+    B.call("sd_debug_set_conv_splits", splits)
+    try:
+        y, y_again, y1 = run(nb), run(nb), run(1)
+    finally:
+        B.call("sd_debug_set_conv_splits", 0)
+    assert rel(y, ref) < 6e-3
+    assert torch.equal(y, y_again)
+    assert torch.equal(y[:1], y1)
+
+
 def test_conv3x3_concat():
     nb, h, w, c1, c2, cout = 2, 16, 16, 320, 640, 320
     g = torch.Generator().manual_seed(9)
