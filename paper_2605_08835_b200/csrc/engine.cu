@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <stdlib.h>
 
+#include <nvtx3/nvToolsExt.h>
 #include "engine.h"
 
 namespace sd {
@@ -867,7 +868,19 @@ cudaEvent_t Prof::ev() {
   SD_CUDA(cudaEventCreate(&e));
   return e;
 }
+// SD_NVTX=1: one NVTX range per kernel class around each launch (eager mode), so that ncu can select
+// e.g. only the conv launches: ncu --nvtx --nvtx-include "conv/" …  (SD_NO_GRAPH=1)
+static int nvtx_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("SD_NVTX");
+    v = s && s[0] == '1';
+  }
+  return v;
+}
+static const char* const kClassName[] = {"conv", "gemm", "attn", "gn", "ln", "other", "vae", "other"};
 int Prof::begin(int cls, cudaStream_t st, double work) {
+  if (nvtx_on()) nvtxRangePushA(kClassName[cls & 7]);
   if (!on) return -1;
   std::vector<Rec>& dst = sink ? *sink : recs;
   Rec r{cls, ev(), ev(), work};
@@ -877,6 +890,7 @@ int Prof::begin(int cls, cudaStream_t st, double work) {
   return (int)dst.size() - 1;
 }
 void Prof::end(int idx, cudaStream_t st) {
+  if (nvtx_on()) nvtxRangePop();
   if (idx < 0) return;
   std::vector<Rec>& dst = sink ? *sink : recs;
   SD_CUDA(sink ? cudaEventRecordWithFlags(dst[idx].b, st, cudaEventRecordExternal) : cudaEventRecord(dst[idx].b, st));

@@ -1,6 +1,6 @@
 // tcgen05 / TMEM / TMA GEMM and implicit-GEMM 3x3 convolution for sm_100a.
 //
-// One persistent, warp-specialised kernel template gemm_kernel<BN, CG>:
+// One persistent, warp-specialised kernel template gemm_kernel<BN, CG, MODE> (MODE = dense / conv3):
 //   warp 0      TMA producer   (one elected lane): A and B tiles into a STAGES-deep smem ring
 //   warp 1      MMA issuer     (one elected lane of the leader CTA): tcgen05.mma into a
 //                              double-buffered TMEM accumulator; also owns TMEM alloc/dealloc
@@ -201,6 +201,7 @@ struct EpiCtx {
 };
 
 // write 32 fp32 values (this lane's row, columns [col, col+32)) to the staging slab and TMA-store it
+template <int MODE>
 __device__ __forceinline__ void stage_store(const GemmArgs& g, const CUtensorMap* om, EpiCtx& ec, const float* o,
                                             int col, int lane) {
   uint8_t* buf = ec.stage + ec.slot * 2048;
@@ -216,7 +217,7 @@ __device__ __forceinline__ void stage_store(const GemmArgs& g, const CUtensorMap
   fence_async_smem();
   __syncwarp();
   if (lane == 0) {
-    if (g.mode == GEMM_DENSE)
+    if (MODE == GEMM_DENSE)
       tma_store_2d(om, buf, col, ec.sx);
     else
       tma_store_4d(om, buf, col, ec.sx, ec.sy, ec.sb);
@@ -238,14 +239,14 @@ __device__ __forceinline__ void add32(float* o, const float* p) {
   }
 }
 
-template <int BN>
+template <int BN, int MODE>
 __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorMap* om, EpiCtx& ec, uint32_t tbase,
                                               int mbox, int n0, int q, int lane, int half, int split) {
   const int r = q * 32 + lane;
   long prow;
   int img;
   bool valid;
-  if (g.mode == GEMM_DENSE) {
+  if (MODE == GEMM_DENSE) {
     prow = (long)mbox * 128 + r;
     valid = prow < g.M;
     img = (int)(prow / g.rows_per_img);
@@ -295,7 +296,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
 #pragma unroll
           for (int i = 0; i < 32; ++i) o[i] += __bfloat162float(rp[i]);
         }
-        stage_store(g, om, ec, o, ocol, lane);
+        stage_store<MODE>(g, om, ec, o, ocol, lane);
       }
     }
     return;
@@ -372,7 +373,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
     if (g.dbg == 1) {
       if (o[0] == 12345.f) g.res ? (void)0 : __trap();
     } else if (g.tma_store) {
-      stage_store(g, om, ec, o, col, lane);
+      stage_store<MODE>(g, om, ec, o, col, lane);
     } else if (valid) {
       if (g.out_f32) {
         float* op = reinterpret_cast<float*>(g.out) + prow * g.ldo + g.col_off + col;
@@ -399,7 +400,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
   }
 }
 
-template <int BN, int CG>
+template <int BN, int CG, int MODE>
 __global__ void __launch_bounds__(320, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ CUtensorMap ta1,
                 const __grid_constant__ CUtensorMap tb0, const __grid_constant__ CUtensorMap tb1,
@@ -458,7 +459,7 @@ __global__ void __launch_bounds__(320, 1)
         const int mbox = mt * CG + (int)rank;  // this CTA's 128-row box
         const int n0 = nt * BN + (int)rank * C::B_ROWS;
         int m0 = 0, x0 = 0, y0 = 0, b0 = 0;
-        if (g.mode == GEMM_DENSE) {
+        if (MODE == GEMM_DENSE) {
           m0 = mbox * C::BM;
         } else {
           const int tx = mbox % g.tiles_x;
@@ -479,7 +480,7 @@ __global__ void __launch_bounds__(320, 1)
           }
           void* dA = sA + stage * C::A_BYTES;
           void* dB = sB + stage * C::B_BYTES;
-          if (g.mode == GEMM_DENSE) {
+          if (MODE == GEMM_DENSE) {
             tma2<CG>(dA, &ta0, &full[stage], bar_l, kb * C::BK, m0);
             tma2<CG>(dB, &tb0, &full[stage], bar_l, kb * C::BK, n0);
           } else {
@@ -550,7 +551,7 @@ __global__ void __launch_bounds__(320, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * C::TMEM_STRIDE;
-      epilogue_tile<BN>(g, &tout, ec, tbase, mt * CG + (int)rank, nt * BN, q, lane, (warp - 2) >> 2, sp);
+      epilogue_tile<BN, MODE>(g, &tout, ec, tbase, mt * CG + (int)rank, nt * BN, q, lane, (warp - 2) >> 2, sp);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -669,12 +670,12 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ part, int S, long
   *reinterpret_cast<uint2*>(out + m * ldo + col_off + n) = pk;
 }
 
-template <int BN, int CG>
+template <int BN, int CG, int MODE>
 static void launch(const CUtensorMap* m, const GemmArgs& a, cudaStream_t st) {
   using C = Cfg<BN, CG>;
   static bool attr_set = false;
   if (!attr_set) {
-    SD_CUDA(cudaFuncSetAttribute(gemm_kernel<BN, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    SD_CUDA(cudaFuncSetAttribute(gemm_kernel<BN, CG, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr_set = true;
   }
   const int total = a.m_tiles * a.n_tiles * a.splits;
@@ -693,8 +694,23 @@ static void launch(const CUtensorMap* m, const GemmArgs& a, cudaStream_t st) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  SD_CUDA(cudaLaunchKernelEx(&cfg, gemm_kernel<BN, CG>, m[0], m[1], m[2], m[3], m[4], a));
+  SD_CUDA(cudaLaunchKernelEx(&cfg, gemm_kernel<BN, CG, MODE>, m[0], m[1], m[2], m[3], m[4], a));
   SD_CHECK_LAUNCH();
+}
+
+// conv3 and dense launches are separate instantiations (distinct kernel names in launch lists)
+template <int MODE>
+static void dispatch(int bn, int cg, const CUtensorMap* maps, const GemmArgs& a, cudaStream_t st) {
+  switch (bn * 4 + cg) {
+    case 64 * 4 + 1: launch<64, 1, MODE>(maps, a, st); break;
+    case 128 * 4 + 1: launch<128, 1, MODE>(maps, a, st); break;
+    case 160 * 4 + 1: launch<160, 1, MODE>(maps, a, st); break;
+    case 256 * 4 + 1: launch<256, 1, MODE>(maps, a, st); break;
+    case 128 * 4 + 2: launch<128, 2, MODE>(maps, a, st); break;
+    case 160 * 4 + 2: launch<160, 2, MODE>(maps, a, st); break;
+    case 256 * 4 + 2: launch<256, 2, MODE>(maps, a, st); break;
+    default: throw CudaError("unsupported BN/CG");
+  }
 }
 
 static int pick_bn(int N, int act) {
@@ -867,17 +883,10 @@ void gemm(const GemmDesc& d, cudaStream_t st) {
     if (d.act == ACT_GEGLU) throw CudaError("GEGLU epilogue needs a bf16, 16-byte aligned output");
     maps[4] = maps[0];
   }
-  const int key = bn * 4 + cg;
-  switch (key) {
-    case 64 * 4 + 1: launch<64, 1>(maps, a, st); break;
-    case 128 * 4 + 1: launch<128, 1>(maps, a, st); break;
-    case 160 * 4 + 1: launch<160, 1>(maps, a, st); break;
-    case 256 * 4 + 1: launch<256, 1>(maps, a, st); break;
-    case 128 * 4 + 2: launch<128, 2>(maps, a, st); break;
-    case 160 * 4 + 2: launch<160, 2>(maps, a, st); break;
-    case 256 * 4 + 2: launch<256, 2>(maps, a, st); break;
-    default: throw CudaError("unsupported BN/CG");
-  }
+  if (d.mode == GEMM_DENSE)
+    dispatch<GEMM_DENSE>(bn, cg, maps, a, st);
+  else
+    dispatch<GEMM_CONV3>(bn, cg, maps, a, st);
   if (a.splits > 1) {
     const long n4 = (long)a.M * (d.N / 4);
     splitk_reduce_kernel<<<(unsigned)cdiv(n4, 256), 256, 0, st>>>(
