@@ -1,0 +1,117 @@
+"""Pins for oracle/serving.py (the continuous-batching semantics of SURVEY.md §8(c) steps 1-5).
+
+No paper value fixes a timeline on B200, so the simulator is pinned by closed forms on tables whose
+entries are chosen by hand, and by invariants any correct serving loop must satisfy:
+  * a lone request: U = n·τ¹(1,0,0), V = U + δ^c(0,1,0) (PAPER.md:289 U_i / V_i; Eq. 2 early release);
+  * lockstep requests share rounds (step-level batching);
+  * B_max refill happens only at window boundaries, FCFS by (A_i, id) (R16);
+  * time-shift invariance of an isolated request; every request takes exactly n_r steps;
+  * Skip-CFG only at s_r ≥ s_min_r and only in windows with N > 0 (R6, R8).
+"""
+import itertools
+
+from oracle import controller as ctl
+from oracle import sched, serving
+
+
+def table(B=8, c_values=(1, 2, 3, 4)):
+    """τ^c(m,n,k) = 1000·(2m−k) + 700·n + 50(c−1)·n µs; δ^c(m,n,k) = 600·n + 200·m + 10·k (n > 0)."""
+    tabs = {}
+    for c in c_values:
+        t = {}
+        for m, n in itertools.product(range(B + 1), range(B + 1)):
+            for k in range(m + 1):
+                if m == 0 and n == 0:
+                    continue
+                tau = 1000 * (2 * m - k) + 700 * n + 50 * (c - 1) * n
+                delta = 600 * n + 200 * m + 10 * k if n else 0
+                t[(m, n, k)] = (tau, delta)
+        tabs[c] = t
+    return tabs
+
+
+def test_lone_request_closed_form():
+    tabs = table()
+    for n in (1, 3, 20):
+        done = serving.simulate([(0, 0, n)], tabs)
+        t = done[0]
+        assert t.U == n * tabs[1][(1, 0, 0)][0]
+        assert t.V == t.U + tabs[1][(0, 1, 0)][1]
+        assert t.s == n and t.skips == []
+
+
+def test_time_shift_invariance():
+    tabs = table()
+    a = serving.simulate([(5, 0, 7)], tabs)[5]
+    b = serving.simulate([(5, 123_456, 7)], tabs)[5]
+    assert (b.U - b.A, b.V - b.A) == (a.U - a.A, a.V - a.A)
+
+
+def test_lockstep_requests_share_rounds():
+    tabs = table()
+    done = serving.simulate([(i, 0, 4) for i in range(3)], tabs)
+    tau3 = tabs[1][(3, 0, 0)][0]
+    assert all(done[i].U == 4 * tau3 for i in range(3))
+    # the three decodes start at U; whatever plan the DP picks, each ends at a stage start + δ ≥ U + δ(0,1,0)
+    assert all(done[i].V >= done[i].U + tabs[1][(0, 1, 0)][1] for i in range(3))
+
+
+def test_bmax_refill_fcfs():
+    """B_max = 2, three requests at t = 0 with one step each: ids 0 and 1 run the first round
+    together; id 2 is admitted at the next window boundary (FCFS by (A, id))."""
+    tabs = table(B=2, c_values=(1,))
+    log = []
+    done = serving.simulate([(2, 0, 1), (1, 0, 1), (0, 0, 1)], tabs, b_max=2, c_max=1, log=log)
+    tau2 = tabs[1][(2, 0, 0)][0]
+    assert done[0].U == done[1].U == tau2
+    assert log[0]["M"] == 2 and log[0]["N"] == 0
+    assert log[1]["now"] == tau2 and log[1]["M"] == 1 and log[1]["N"] == 2
+    assert done[2].U > tau2
+    assert all(w["M"] <= 2 and w["N"] <= 2 for w in log)
+
+
+def test_poisson_invariants():
+    tabs = table()
+    import random
+    rng = random.Random(3)
+    trace, t = [], 0
+    for i in range(60):
+        t += int(rng.expovariate(1 / 4000))
+        trace.append((i, t, rng.randint(20, 50)))
+    log = []
+    done = serving.simulate(trace, tabs, c_star=1, c_max=4, log=log)
+    assert sorted(done) == list(range(60))
+    for i, a, n in trace:
+        d = done[i]
+        assert d.A == a and d.s == n
+        assert a < d.U < d.V
+        assert d.U - a >= n * min(v[0] for v in tabs[1].values() if v[0] > 0) // 8
+        lv = [f for f in ctl.LEVELS if f is not None]
+        # a skipped step index is at least the loosest possible s_min
+        assert all(s >= ctl.s_min(min(lv), n) for s in d.skips)
+        assert len(set(d.skips)) == len(d.skips)
+    assert all(w["M"] <= 8 and w["K"] <= w["M"] for w in log)
+    # the overloaded trace makes the controller escalate at least once, and skips appear
+    assert any(w["level"] > 0 for w in log)
+    assert sum(len(d.skips) for d in done.values()) > 0
+
+
+def test_no_skip_without_decodes():
+    """R8: windows with N = 0 run (M, 0, 0); a request that never shares a window with a decode is
+    never skipped even under an escalated controller."""
+    tabs = table()
+    done = serving.simulate([(0, 0, 30)], tabs, ctl_kw=dict(up=(-1000, 1)))  # escalate on any slope
+    assert done[0].skips == []
+
+
+def test_metrics_definition():
+    tabs = table()
+    done = serving.simulate([(0, 0, 2), (1, 10_000, 2)], tabs)
+    m = serving.metrics(done)
+    e2e = sorted(d.V - d.A for d in done.values())
+    assert m["n"] == 2
+    assert m["mean_e2e_us"] == sum(e2e) / 2
+    assert m["p99_e2e_us"] == e2e[-1]            # ceil(0.99·2) = 2nd smallest
+    span = max(d.V for d in done.values()) - 0
+    assert abs(m["throughput_per_s"] - 2 / (span / 1e6)) < 1e-12
+    assert sched.p99(list(range(1, 101))) == 99
