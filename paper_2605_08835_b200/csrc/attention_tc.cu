@@ -20,7 +20,7 @@ namespace sd {
 // NB = number of S (TMEM) / P (smem) buffers. NB = 2: one CTA per SM, S_{j+1} computed while the
 // softmax works on S_j. NB = 1: 256 TMEM columns and ~105 KB smem so two CTAs share an SM and
 // interleave their MMA / softmax phases (the MMA of S_{j+1} still overlaps the tail of softmax_j).
-template <int D, int NB>
+template <int D, int NB, int SPLIT = 1, int EMU = 0>
 struct TcAttn {
   static constexpr int BQ = 128, BK = 128;
   static constexpr int KQ = (D + 63) / 64;       // 64-column blocks of the head dim (Q/K tiles)
@@ -32,7 +32,9 @@ struct TcAttn {
   static constexpr int STAGE = K_BYTES + V_BYTES;
   static constexpr int STAGES = (NB == 2 && D <= 64) ? 3 : 2;
   static constexpr int P_BYTES = 2 * BQ * 128;   // one P tile: 128 rows × 128 keys bf16
-  static constexpr int SMEM = 1024 + Q_BYTES + STAGES * STAGE + NB * P_BYTES + 256;
+  static constexpr int X_BYTES = 3 * 2 * 128 * 4;  // row-max / row-sum exchange of the SPLIT halves
+  static constexpr int SMEM = 1024 + Q_BYTES + STAGES * STAGE + NB * P_BYTES + X_BYTES + 256;
+  static constexpr int THREADS = 64 + 128 * SPLIT;
   static constexpr int TMEM_COLS = NB == 2 ? 512 : 256;
   static constexpr int O_COL = NB * 128;         // O accumulator after the S buffers
   static_assert(V_BYTES % 1024 == 0, "Vᵀ tile rows must be a multiple of 8");
@@ -62,17 +64,30 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-template <int D, int NB>
-__global__ void __launch_bounds__(192, 3 - NB)
+// 2^x on the FMA / ALU pipes (relieves MUFU, the bound of the softmax): x = j + f with j = rint(x)
+// (1.5·2²³ magic add), f ∈ [−½, ½]; 2^f by a degree-3 polynomial fitted for relative error
+// (max 1.2e-4 — far below bf16 P's 3.9e-3); 2^j added into the exponent field. x is clamped to −120
+// (the result is then < 1e-36, i.e. zero next to a row sum ≥ 1).
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -120.f);
+  const float t = x + 12582912.f;
+  const float f = x - (t - 12582912.f);
+  const float p = fmaf(fmaf(fmaf(0.05520857f, f, 0.24226530f), f, 0.69324851f), f, 1.0f);
+  return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
+}
+
+template <int D, int NB, int SPLIT, int EMU>
+__global__ void __launch_bounds__(64 + 128 * SPLIT, 3 - NB)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tqk, const __grid_constant__ CUtensorMap tvt, bf16* __restrict__ O,
                    int ldo, int C, int P, int Lk, float scale_log2) {
-  using A = TcAttn<D, NB>;
+  using A = TcAttn<D, NB, SPLIT, EMU>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
   uint8_t* sKV = sQ + A::Q_BYTES;
   uint8_t* sP = sKV + A::STAGES * A::STAGE;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + NB * A::P_BYTES);
+  float* sX = reinterpret_cast<float*>(sP + NB * A::P_BYTES);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + NB * A::P_BYTES + A::X_BYTES);
   uint64_t* q_full = bar;
   uint64_t* kv_full = bar + 1;
   uint64_t* kv_empty = kv_full + A::STAGES;
@@ -96,11 +111,11 @@ __global__ void __launch_bounds__(192, 3 - NB)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&s_full[s], 1);
-      mbar_init(&s_empty[s], 4);
-      mbar_init(&p_full[s], 4);
+      mbar_init(&s_empty[s], 4 * SPLIT);
+      mbar_init(&p_full[s], 4 * SPLIT);
     }
     mbar_init(pv_done, 1);
-    mbar_init(q_ready, 4);
+    mbar_init(q_ready, 4 * SPLIT);
     fence_mbar_init();
     tma_prefetch(&tqk);
     tma_prefetch(&tvt);
@@ -119,7 +134,7 @@ __global__ void __launch_bounds__(192, 3 - NB)
         tma_load_2d(sQ + kb * A::BQ * 128, &tqk, q_full, head * D + kb * 64, tok0 + q0);
       for (int j = 0; j < nb; ++j) {
         const int s = j % A::STAGES;
-        mbar_wait(&kv_empty[s], ((j / A::STAGES) & 1) ^ 1);
+        mbar_wait_sleep(&kv_empty[s], ((j / A::STAGES) & 1) ^ 1);
         mbar_expect_tx(&kv_full[s], A::STAGE);
         uint8_t* st = sKV + s * A::STAGE;
         for (int kb = 0; kb < A::KQ; ++kb)
@@ -139,8 +154,8 @@ __global__ void __launch_bounds__(192, 3 - NB)
       for (int j = 0; j <= nb; ++j) {
         if (j < nb) {
           const int s = j % A::STAGES, sb = j % NB;
-          mbar_wait(&kv_full[s], (j / A::STAGES) & 1);
-          if (j >= NB) mbar_wait(&s_empty[sb], (j / NB - 1) & 1);
+          mbar_wait_sleep(&kv_full[s], (j / A::STAGES) & 1);
+          if (j >= NB) mbar_wait_sleep(&s_empty[sb], (j / NB - 1) & 1);
           tc_fence_after();
           const uint32_t ak = smem_u32(sKV + s * A::STAGE);
 #pragma unroll
@@ -152,7 +167,7 @@ __global__ void __launch_bounds__(192, 3 - NB)
         }
         if (j >= 1) {
           const int jp = j - 1, pb = jp % NB, sp = jp % A::STAGES;
-          mbar_wait(&p_full[pb], (jp / NB) & 1);
+          mbar_wait_sleep(&p_full[pb], (jp / NB) & 1);
           tc_fence_after();
           const uint32_t ap = smem_u32(sP + pb * A::P_BYTES);
           const uint32_t av = smem_u32(sKV + sp * A::STAGE + A::K_BYTES);
@@ -169,13 +184,19 @@ __global__ void __launch_bounds__(192, 3 - NB)
     }
     __syncwarp();
   } else {
-    // ---------------- softmax warps: thread ↔ query row r ----------------
+    // ---------------- softmax warps: SPLIT threads per query row r ----------------
+    // warp w accesses TMEM lane quarter w % 4; with SPLIT = 2, warps w and w + 4 share the rows of a
+    // quarter and take the key columns [64h, 64h + 64) each (h = half), exchanging the row max
+    // through smem once per key block (named barrier per quarter)
+    constexpr int CPT = 128 / SPLIT, NCH = CPT / 32;
+    constexpr bool DBUF = !(NB == 1 && SPLIT == 1);
     const int q = warp & 3;
+    const int h = (warp - 2) >> 2;
     const int r = q * 32 + lane;
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     float m = -FLT_MAX, l = 0.f;
     mbar_wait(q_full, 0);
-    if (D % 16 != 0) {
+    if (D % 16 != 0 && h == 0) {
       // zero Q columns [D, 16·K16) of this thread's row: they belong to the next head and the
       // padded k-step of Q·Kᵀ reads them
       uint8_t* qrow = sQ + ((D / 64) * A::BQ * 128) + r * 128;
@@ -188,51 +209,85 @@ __global__ void __launch_bounds__(192, 3 - NB)
     if (lane == 0) mbar_arrive(q_ready);
     for (int j = 0; j < nb; ++j) {
       const int sb = j % NB;
-      mbar_wait(&s_full[sb], (j / NB) & 1);
+      mbar_wait_sleep(&s_full[sb], (j / NB) & 1);
       tc_fence_after();
-      // pass 1: row max over the 128 scores (TMEM is re-read in pass 2 instead of holding 128
-      // registers; keys beyond Lk are masked)
-      const bool ragged = (j + 1) * A::BK > Lk;
-      float mx = m;
+      const uint32_t sbase = tmem + lane_base + sb * 128 + h * CPT;
+      // Lk is a multiple of 128 (attention_tc_supported): no key block is ragged
+      uint32_t ta[32], tb[32];
+      // pass 1: row max over this thread's scores — 4 independent max chains, the next 32-column TMEM
+      // load in flight while this one is reduced (TMEM is re-read in pass 2)
+      float mx4[4] = {-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX};
+      tmem_ld32_nw(sbase, ta);
+      tmem_wait_ld_tied(ta);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t t[32];
-        tmem_ld32(tmem + lane_base + sb * 128 + c * 32, t);
+      for (int c = 0; c < NCH; ++c) {
+        // DBUF: the next chunk's load is in flight while this one is processed (needs 32 more registers)
+        uint32_t(&cur)[32] = (DBUF && (c & 1)) ? tb : ta;
+        uint32_t(&nxt)[32] = (c & 1) ? ta : tb;
+        if (DBUF && c < NCH - 1) tmem_ld32_nw(sbase + (c + 1) * 32, nxt);
+        if (!DBUF && c > 0) {
+          tmem_ld32_nw(sbase + c * 32, ta);
+          tmem_wait_ld_tied(ta);
+        }
 #pragma unroll
         for (int i = 0; i < 32; ++i)
-          if (!ragged || j * A::BK + c * 32 + i < Lk) mx = fmaxf(mx, __uint_as_float(t[i]));
+          mx4[i & 3] = fmaxf(mx4[i & 3], __uint_as_float(cur[i]));
+        if (DBUF && c < NCH - 1) tmem_wait_ld_tied(nxt);
       }
-      const float ms = mx * scale_log2;
-      const float alpha = ex2((m - mx) * scale_log2);
-      // pass 2: P = exp2(s·scale − m) packed to bf16
-      float sum = 0.f;
-      uint32_t pk[64];
+      float mxb = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+      if (SPLIT == 2) {
+        sX[((j & 1) * 2 + h) * 128 + r] = mxb;
+        named_bar_sync(1 + q, 64);
+        mxb = fmaxf(mxb, sX[((j & 1) * 2 + (h ^ 1)) * 128 + r]);
+      }
+      // lazy rescaling: the running max m only moves when the block max exceeds it by more than 8 in
+      // the exp2 domain (P ≤ 2⁸ stays exact in fp32 sums and bf16 P), so O is rarely rescaled
+      const bool upd = (mxb - m) * scale_log2 > 8.f;
+      const float mnew = upd ? mxb : m;
+      const float alpha = upd ? ex2((m - mnew) * scale_log2) : 1.f;
+      const float ms = mnew * scale_log2;
+      // pass 2: P = exp2(s·scale − m) packed to bf16; 8 independent partial sums
+      float sum8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      uint32_t pk[NCH * 16];
+      tmem_ld32_nw(sbase, ta);
+      tmem_wait_ld_tied(ta);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t t[32];
-        tmem_ld32(tmem + lane_base + sb * 128 + c * 32, t);
+      for (int c = 0; c < NCH; ++c) {
+        // DBUF: the next chunk's load is in flight while this one is processed (needs 32 more registers)
+        uint32_t(&cur)[32] = (DBUF && (c & 1)) ? tb : ta;
+        uint32_t(&nxt)[32] = (c & 1) ? ta : tb;
+        if (DBUF && c < NCH - 1) tmem_ld32_nw(sbase + (c + 1) * 32, nxt);
+        if (!DBUF && c > 0) {
+          tmem_ld32_nw(sbase + c * 32, ta);
+          tmem_wait_ld_tied(ta);
+        }
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          float s0 = __uint_as_float(t[2 * i]), s1 = __uint_as_float(t[2 * i + 1]);
-          if (ragged) {
-            if (j * A::BK + c * 32 + 2 * i >= Lk) s0 = -FLT_MAX;
-            if (j * A::BK + c * 32 + 2 * i + 1 >= Lk) s1 = -FLT_MAX;
+          const float s0 = __uint_as_float(cur[2 * i]), s1 = __uint_as_float(cur[2 * i + 1]);
+          const float x0 = fmaf(s0, scale_log2, -ms), x1 = fmaf(s1, scale_log2, -ms);
+          float p0, p1;
+          if (EMU > 0 && i % EMU == EMU - 1) {  // 1 pair in EMU on the FMA pipe
+            p0 = ex2_poly(x0);
+            p1 = ex2_poly(x1);
+          } else {
+            p0 = ex2(x0);
+            p1 = ex2(x1);
           }
-          const float p0 = ex2(fmaf(s0, scale_log2, -ms));
-          const float p1 = ex2(fmaf(s1, scale_log2, -ms));
-          sum += p0 + p1;
+          sum8[i & 7] += p0 + p1;
           pk[c * 16 + i] = pack_bf16(p0, p1);
         }
+        if (DBUF && c < NCH - 1) tmem_wait_ld_tied(nxt);
       }
+      const float sum = ((sum8[0] + sum8[1]) + (sum8[2] + sum8[3])) + ((sum8[4] + sum8[5]) + (sum8[6] + sum8[7]));
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_empty[sb]);
-      l = l * alpha + sum;
-      m = mx;
+      l = l * alpha + sum;  // this thread's columns; the halves are added after the last block
+      m = mnew;
       if (j >= 1) {
-        mbar_wait(pv_done, (j - 1) & 1);  // PV_{j-1} done: O is stable and P buffer (j&1) is free
+        mbar_wait_sleep(pv_done, (j - 1) & 1);  // PV_{j-1} done: O is stable and P buffer (j&1) is free
         tc_fence_after();
-        if (__any_sync(0xffffffff, alpha < 1.f)) {
+        if (h == 0 && __any_sync(0xffffffff, alpha < 1.f)) {
 #pragma unroll
           for (int c = 0; c < A::NPV / 16; ++c) {
             uint32_t o[16];
@@ -245,13 +300,14 @@ __global__ void __launch_bounds__(192, 3 - NB)
           tmem_wait_st();
         }
       }
-      // P row → swizzled smem (two 64-key K-blocks, 128 B per row, 16-byte chunk c at c ^ (r & 7))
+      // P row → swizzled smem (64-key K-blocks, 128 B per row, 16-byte chunk c at c ^ (r & 7))
       uint8_t* prow = sP + sb * A::P_BYTES + r * 128;
 #pragma unroll
-      for (int kb = 0; kb < 2; ++kb)
+      for (int kk = 0; kk < NCH / 2; ++kk)
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          const int i = kb * 32 + c * 4;
+          const int i = kk * 32 + c * 4;
+          const int kb = h * (NCH / 2) + kk;
           *reinterpret_cast<uint4*>(prow + kb * (A::BQ * 128) + ((c ^ (r & 7)) << 4)) =
               make_uint4(pk[i], pk[i + 1], pk[i + 2], pk[i + 3]);
         }
@@ -261,6 +317,11 @@ __global__ void __launch_bounds__(192, 3 - NB)
       if (lane == 0) mbar_arrive(&p_full[sb]);
     }
     // ---------------- epilogue: O / l → bf16 ----------------
+    if (SPLIT == 2) {
+      sX[(2 * 2 + h) * 128 + r] = l;  // rows of the exchange area not used by the last key blocks
+      named_bar_sync(1 + q, 64);
+      l = sX[(2 * 2 + 0) * 128 + r] + sX[(2 * 2 + 1) * 128 + r];
+    }
     mbar_wait(pv_done, (nb - 1) & 1);
     tc_fence_after();
     const float inv = 1.f / l;
@@ -268,6 +329,7 @@ __global__ void __launch_bounds__(192, 3 - NB)
     bf16* orow = O + (long)(tok0 + qi) * ldo + head * D;
 #pragma unroll
     for (int c = 0; c < A::NPV / 16; ++c) {
+      if (c % SPLIT != h) continue;
       uint32_t o[16];
       tmem_ld16(tmem + lane_base + A::O_COL + c * 16, o);
       tmem_wait_ld();
@@ -295,12 +357,13 @@ __global__ void __launch_bounds__(192, 3 - NB)
 void make_tmap_2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_bytes, uint32_t box_in,
                   uint32_t box_out);
 
-template <int D, int NB>
+template <int D, int NB, int SPLIT, int EMU = 0>
 static void launch_tc(const bf16* qk, const bf16* vt, bf16* O, int rows, int heads, int C, int P, cudaStream_t st) {
-  using A = TcAttn<D, NB>;
+  using A = TcAttn<D, NB, SPLIT, EMU>;
   static bool set = false;
   if (!set) {
-    SD_CUDA(cudaFuncSetAttribute(attn_tc_kernel<D, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, A::SMEM));
+    SD_CUDA(cudaFuncSetAttribute(attn_tc_kernel<D, NB, SPLIT, EMU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 A::SMEM));
     set = true;
   }
   const long T = (long)rows * P;
@@ -309,8 +372,41 @@ static void launch_tc(const bf16* qk, const bf16* vt, bf16* O, int rows, int hea
   make_tmap_2d(&mvt, vt, (uint64_t)T, (uint64_t)C, (uint64_t)T * 2, 64, A::NPV);
   dim3 grid(cdiv(P, A::BQ), heads, rows);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)D);
-  attn_tc_kernel<D, NB><<<grid, 192, A::SMEM, st>>>(mqk, mvt, O, C, C, P, P, scale_log2);
+  attn_tc_kernel<D, NB, SPLIT, EMU><<<grid, A::THREADS, A::SMEM, st>>>(mqk, mvt, O, C, C, P, P, scale_log2);
   SD_CHECK_LAUNCH();
+}
+
+// SD_ATTN_SPLIT=1|2: softmax threads per query row at d = 40 (default 2)
+static int attn_split() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SD_ATTN_SPLIT");
+    v = e ? atoi(e) : 2;
+    if (v != 1) v = 2;
+  }
+  return v;
+}
+
+// SD_ATTN_EMU=0|4: one exp2 pair in EMU on the FMA pipe (0 = all on MUFU, the default: r01 kbench
+// at d = 40 — emulating 1/4 of the exps costs 7 %, 1/3 costs 9 %: MUFU is not the binding limit)
+static int attn_emu() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SD_ATTN_EMU");
+    v = e ? atoi(e) : 0;
+    if (v != 4) v = 0;
+  }
+  return v;
+}
+// SD_ATTN_NB=1|2: S / P buffers at d = 40 (default 1: two CTAs per SM)
+static int attn_nb() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SD_ATTN_NB");
+    v = e ? atoi(e) : 1;
+    if (v != 2) v = 1;
+  }
+  return v;
 }
 
 bool attention_tc_supported(int d, int P, int C) {
@@ -321,9 +417,29 @@ bool attention_tc_supported(int d, int P, int C) {
 void attention_tc(const bf16* qk, const bf16* vt, bf16* O, int rows, int heads, int d, int C, int P,
                   cudaStream_t st) {
   switch (d) {
-    case 40: launch_tc<40, 1>(qk, vt, O, rows, heads, C, P, st); break;
-    case 64: launch_tc<64, 2>(qk, vt, O, rows, heads, C, P, st); break;  // measured: NB=2 1.18× faster at d=64
-    case 80: launch_tc<80, 2>(qk, vt, O, rows, heads, C, P, st); break;
+    case 40:
+      switch (attn_nb() * 100 + attn_split() * 10 + attn_emu()) {
+        case 110: launch_tc<40, 1, 1, 0>(qk, vt, O, rows, heads, C, P, st); break;
+        case 114: launch_tc<40, 1, 1, 4>(qk, vt, O, rows, heads, C, P, st); break;
+        case 124: launch_tc<40, 1, 2, 4>(qk, vt, O, rows, heads, C, P, st); break;
+        case 210: launch_tc<40, 2, 1, 0>(qk, vt, O, rows, heads, C, P, st); break;
+        case 220: launch_tc<40, 2, 2, 0>(qk, vt, O, rows, heads, C, P, st); break;
+        case 224: launch_tc<40, 2, 2, 4>(qk, vt, O, rows, heads, C, P, st); break;
+        default: launch_tc<40, 1, 2, 0>(qk, vt, O, rows, heads, C, P, st); break;
+      }
+      break;
+    case 64:  // measured: NB=2 1.18× faster at d=64
+      if (attn_emu() == 0)
+        launch_tc<64, 2, 1, 0>(qk, vt, O, rows, heads, C, P, st);
+      else
+        launch_tc<64, 2, 1, 4>(qk, vt, O, rows, heads, C, P, st);
+      break;
+    case 80:
+      if (attn_emu() == 0)
+        launch_tc<80, 2, 1, 0>(qk, vt, O, rows, heads, C, P, st);
+      else
+        launch_tc<80, 2, 1, 4>(qk, vt, O, rows, heads, C, P, st);
+      break;
     default: throw CudaError("attention_tc: unsupported head dim");
   }
 }

@@ -808,7 +808,18 @@ void gemm(const GemmDesc& d, cudaStream_t st) {
   int box_begin = d.m_tile_begin, box_count = d.m_tile_count >= 0 ? d.m_tile_count : m_boxes;
   // pair tiles (256 rows, half of B per CTA) when the weights dominate the operand traffic
   // (M ≤ 16·N; measured on B200: 16×16 / 8×8 / 32×32×1280 convs gain up to 1.4×, 64×64 ones lose)
-  int cg = ((long)box_count * 128 <= 16L * d.N && box_begin % 2 == 0 && bn >= 128) ? 2 : 1;
+  // pairs when the weights dominate the operand traffic (M ≤ 16·N: the 16×16 / 8×8 UNet levels gain
+  // up to 1.4×; short-K dense GEMMs at M = 65536 lose). conv3 layers of 64×64 … 256×256 pixels also
+  // take pairs (kbench r01: +3-5 %; at 32×32 and 512×512 they lose 1-11 %); SD_CONV_CG_OLD=1 = M-rule only.
+  static int conv_old = -1;
+  if (conv_old < 0) {
+    const char* s = getenv("SD_CONV_CG_OLD");
+    conv_old = s && s[0] == '1';
+  }
+  const bool pair_ok = box_begin % 2 == 0 && bn >= 128;
+  const long hw = (long)d.H * d.W;
+  const bool conv_pair = d.mode == GEMM_CONV3 && !conv_old && hw >= 4096 && hw <= 65536;
+  int cg = (pair_ok && (((long)box_count * 128 <= 16L * d.N) || conv_pair)) ? 2 : 1;
   if (g_cg_override == 1 || g_cg_override == 2) cg = g_cg_override;
   if (cg == 2 && (box_begin % 2 || bn < 128)) cg = 1;
   const uint32_t brows = (uint32_t)(bn / cg);

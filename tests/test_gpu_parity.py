@@ -205,3 +205,49 @@ def test_sd15_vae_parity(sd15):
     print(f"sd VAE 512² rel-L2 {r:.3e}")
     assert r <= TOL
     assert torch.equal(ch, whole)
+
+
+def test_sd15_768_step_and_vae_parity():
+    """CFG#4 resolution: SD-1.5 at 768² (latent 96×96: self-attention over 9216 / 2304 tokens on the
+    tcgen05 path, 576 / 144 on the mma path; conv tiles of 32×4 px). One CFG request, one step, vs
+    the oracle (ε-part at TOL·κ, x at TOL), then the 768² VAE decode (TOL) and chunked == whole."""
+    eng = Engine("sd15", max_latent_hw=96, b_max=1)
+    try:
+        ctx_u = synth.uncond_embedding(0, 77, 768)
+        eng.set_uncond(torch.from_numpy(ctx_u))
+        cfg = configs.SD15_UNET
+        P = configs.unet_params(cfg, 0, np.float32, bf16_weights=True)
+        ctx = synth.text_embedding(5, 0, 77, 768)
+        slot = eng.register(torch.from_numpy(ctx))
+        x0 = synth.initial_noise(5, 0, 96, 96)
+        lat = [torch.from_numpy(x0).cuda()]
+        step, g = 10, 7.5
+        eng.step(lat, [step], [50], [1], [g], [slot])
+        torch.cuda.synchronize()
+        t = int(sampling.timesteps(50)[step])
+        eps = unet.forward(P, cfg, np.stack([x0, x0]), np.array([t, t]),
+                           np.stack([synth.bf16_round(ctx), synth.bf16_round(ctx_u)]))
+        ec, eu = eps[0], eps[1]
+        et = sampling.cfg_combine(ec, eu, g, True)
+        exp = sampling.ddim_step(x0, et, 50, step)
+        kappa = (abs(1 - g) * np.linalg.norm(eu) + g * np.linalg.norm(ec)) / np.linalg.norm(et)
+        a, ap = sampling.ddim_alphas(50, step)
+        A = np.sqrt(ap / a)
+        got = lat[0].cpu().numpy()
+        r_x, r_eps = rel(got, exp), rel(got - A * x0, exp - A * x0)
+        print(f"sd15 768²: x rel-L2 {r_x:.3e}, eps-part {r_eps:.3e}, kappa {kappa:.2f}")
+        assert r_x <= TOL and r_eps <= TOL * kappa
+        V = configs.vae_params(configs.SD_VAE, 0, np.float32, bf16_weights=True)
+        z = synth.initial_noise(6, 0, 96, 96)
+        ref = vae.decode(V, configs.SD_VAE, z[None])[0]
+        zt = torch.from_numpy(z).cuda()
+        whole = eng.decode(zt, 1)
+        ch = eng.decode(zt, 3)
+        torch.cuda.synchronize()
+        r = rel(whole.cpu().numpy(), ref)
+        print(f"sd VAE 768² rel-L2 {r:.3e}")
+        assert r <= TOL
+        assert torch.equal(ch, whole)
+        eng.release(slot)
+    finally:
+        eng.close()

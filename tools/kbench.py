@@ -19,6 +19,10 @@ CONV = [  # (rows, H, W, Cin, Cout, count per UNet step)
     (16, 64, 64, 640, 320, 2), (16, 32, 32, 1280, 640, 1), (16, 16, 16, 2560, 1280, 2), (16, 8, 8, 2560, 1280, 3),
     (16, 64, 64, 640, 640, 1), (16, 32, 32, 1280, 1280, 1), (16, 64, 64, 960, 320, 2), (16, 32, 32, 1920, 640, 1),
 ]
+VAE = [  # SD VAE decoder convs at 512² (one image, B = 1): (rows, H, W, Cin, Cout, count per decode)
+    (1, 64, 64, 512, 512, 8), (1, 128, 128, 512, 512, 7), (1, 256, 256, 512, 256, 1), (1, 256, 256, 256, 256, 6),
+    (1, 512, 512, 256, 128, 1), (1, 512, 512, 128, 128, 5),
+]
 GEMM = [  # (M, N, K, act)
     (65536, 2560, 320, 2), (65536, 320, 1280, 0), (65536, 960, 320, 0), (65536, 320, 320, 0),
     (16384, 5120, 640, 2), (16384, 640, 2560, 0), (4096, 10240, 1280, 2), (4096, 1280, 5120, 0),
@@ -60,23 +64,28 @@ def main():
         peak = json.load(open(p)).get("bf16_tflops_sustained", peak)
     out = []
     tot_t = tot_f = 0.0
-    if args.only in ("", "conv"):
-        for i_, (R, H, W, ci, co, cnt) in enumerate(CONV):
+    for which, LIST in (("conv", CONV), ("vae", VAE)):
+        if args.only not in ("", which):
+            continue
+        tot_t = tot_f = 0.0
+        for i_, (R, H, W, ci, co, cnt) in enumerate(LIST):
             if args.pick >= 0 and i_ != args.pick:
                 continue
             x = torch.randn(R, H, W, ci, device="cuda").to(torch.bfloat16)
             w = (torch.randn(co, 9, ci, device="cuda") / (9 * ci) ** 0.5).to(torch.bfloat16)
             b = torch.zeros(co, device="cuda")
             y = torch.empty(R, H, W, co, device="cuda", dtype=torch.bfloat16)
-            ms = timeit(lambda: B.debug_conv3x3(x, ci, None, 0, w, None, b, None, None, y, R, H, W, co, stream=cur()), args.reps)
+            ms = timeit(lambda: B.debug_conv3x3(x, ci, None, 0, w, None, b, None, None, y, R, H, W, co, stream=cur()),
+                        args.reps)
             fl = 2.0 * R * H * W * co * 9 * ci
             tot_t += ms * cnt
             tot_f += fl * cnt
-            r = dict(kind="conv", shape=[R, H, W, ci, co], ms=ms, tflops=fl / ms / 1e9, frac=fl / ms / 1e9 / peak)
+            r = dict(kind=which, shape=[R, H, W, ci, co], ms=ms, tflops=fl / ms / 1e9, frac=fl / ms / 1e9 / peak)
             out.append(r)
             print(json.dumps(r), flush=True)
-        print(json.dumps({"conv_weighted_tflops": tot_f / tot_t / 1e9, "frac": tot_f / tot_t / 1e9 / peak,
-                          "conv_ms_per_step": tot_t}), flush=True)
+        if tot_t > 0:
+            print(json.dumps({which + "_weighted_tflops": tot_f / tot_t / 1e9, "frac": tot_f / tot_t / 1e9 / peak,
+                              "ms_per_unit": tot_t}), flush=True)
     if args.only in ("", "gemm"):
         for i_, (M, N, K, act) in enumerate(GEMM):
             if args.pick >= 0 and i_ != args.pick:
