@@ -30,10 +30,23 @@ class UNetConfig:
     eps_tf_gn: float = 1e-6
     eps_ln: float = 1e-5
     out_gain: float = 1.0       # R21 (conv_out gain), 1 unless conditioning requires otherwise
+    # SDXL generalisations (R1, App. C; diffusers UNet2DConditionModel config of SDXL-base):
+    tf_depth: tuple = ()        # BasicTransformerBlocks per Transformer2DModel at each level (() → 1)
+    mid_depth: int = 1          # ... in the mid block
+    head_dim: int = 0           # > 0: heads = C / head_dim per level (SDXL 64); 0: `heads` everywhere
+    linear_proj: bool = False   # proj_in / proj_out as Linear(C, C) (same values as a 1×1 conv)
+    add_time_dim: int = 0       # > 0: "text_time" added embedding: 6 time ids × add_time_dim sinusoids
+    pooled_dim: int = 0         #      ‖ pooled text embedding → Linear → SiLU → Linear → + temb
 
     @property
     def temb_dim(self):
         return 4 * self.block_out[0]
+
+    def depth(self, level):
+        return (self.tf_depth[level] if self.tf_depth else 1) if self.attn_levels[level] else 0
+
+    def heads_at(self, c):
+        return c // self.head_dim if self.head_dim else self.heads
 
 
 @dataclass(frozen=True)
@@ -58,6 +71,22 @@ SD15_UNET = UNetConfig("sd15", block_out=(320, 640, 1280, 1280), attn_levels=(Tr
                        layers_per_block=2, groups=32, heads=8, ctx_dim=768, ctx_len=77)
 SD_VAE = VAEConfig("sd", block_out=(128, 256, 512, 512), layers_per_block=2, groups=32,
                    scaling_factor=0.18215)
+
+# SDXL-base (PAPER.md:146 names SDXL; R1): block_out (320, 640, 1280), DownBlock2D + 2 CrossAttnDown,
+# transformer depth (0, 2, 10) (mid 10), head dim 64, ctx 77×2048, linear projections, "text_time"
+# added embedding (6 time ids × 256 ‖ pooled 1280 → 2816 → 1280). The VAE is the SD decoder with
+# scaling factor 0.13025.
+SDXL_UNET = UNetConfig("sdxl", block_out=(320, 640, 1280), attn_levels=(False, True, True), layers_per_block=2,
+                       groups=32, heads=0, ctx_dim=2048, ctx_len=77, tf_depth=(0, 2, 10), mid_depth=10,
+                       head_dim=64, linear_proj=True, add_time_dim=256, pooled_dim=1280)
+SDXL_VAE = VAEConfig("sdxl", block_out=(128, 256, 512, 512), layers_per_block=2, groups=32,
+                     scaling_factor=0.13025)
+# tiny SDXL-shaped config for parity (same code paths: no attention at level 0, depth 2 transformers,
+# head-dim heads, linear projections, added embedding)
+TINY_XL_UNET = UNetConfig("tinyxl", block_out=(32, 64), attn_levels=(False, True), layers_per_block=1,
+                          groups=8, heads=0, ctx_dim=48, ctx_len=8, tf_depth=(0, 2), mid_depth=2,
+                          head_dim=16, linear_proj=True, add_time_dim=8, pooled_dim=40)
+SDXL_TIME_IDS = (1024, 1024, 0, 0, 1024, 1024)   # R27: original size, crop top-left, target size
 
 
 # --------------------------------------------------------------------------------------------
@@ -95,18 +124,20 @@ def _resnet(p, cin, cout, temb_dim):
     return s
 
 
-def _transformer(p, c, ctx_dim):
-    s = _norm(p + ".norm", c) + _conv(p + ".proj_in", c, c, 1)
-    b = p + ".transformer_blocks.0"
-    s += _norm(b + ".norm1", c)
-    s += _lin(b + ".attn1.to_q", c, c, False) + _lin(b + ".attn1.to_k", c, c, False)
-    s += _lin(b + ".attn1.to_v", c, c, False) + _lin(b + ".attn1.to_out.0", c, c)
-    s += _norm(b + ".norm2", c)
-    s += _lin(b + ".attn2.to_q", c, c, False) + _lin(b + ".attn2.to_k", c, ctx_dim, False)
-    s += _lin(b + ".attn2.to_v", c, ctx_dim, False) + _lin(b + ".attn2.to_out.0", c, c)
-    s += _norm(b + ".norm3", c)
-    s += _lin(b + ".ff.net.0.proj", 8 * c, c) + _lin(b + ".ff.net.2", c, 4 * c)
-    s += _conv(p + ".proj_out", c, c, 1)
+def _transformer(p, c, ctx_dim, depth=1, linear_proj=False):
+    proj = (lambda q: _lin(q, c, c)) if linear_proj else (lambda q: _conv(q, c, c, 1))
+    s = _norm(p + ".norm", c) + proj(p + ".proj_in")
+    for d in range(depth):
+        b = p + f".transformer_blocks.{d}"
+        s += _norm(b + ".norm1", c)
+        s += _lin(b + ".attn1.to_q", c, c, False) + _lin(b + ".attn1.to_k", c, c, False)
+        s += _lin(b + ".attn1.to_v", c, c, False) + _lin(b + ".attn1.to_out.0", c, c)
+        s += _norm(b + ".norm2", c)
+        s += _lin(b + ".attn2.to_q", c, c, False) + _lin(b + ".attn2.to_k", c, ctx_dim, False)
+        s += _lin(b + ".attn2.to_v", c, ctx_dim, False) + _lin(b + ".attn2.to_out.0", c, c)
+        s += _norm(b + ".norm3", c)
+        s += _lin(b + ".ff.net.0.proj", 8 * c, c) + _lin(b + ".ff.net.2", c, 4 * c)
+    s += proj(p + ".proj_out")
     return s
 
 
@@ -142,23 +173,27 @@ def unet_param_specs(cfg: UNetConfig):
     T = cfg.temb_dim
     s = _conv("conv_in", C[0], cfg.in_ch, 3)
     s += _lin("time_embedding.linear_1", T, C[0]) + _lin("time_embedding.linear_2", T, T)
+    if cfg.add_time_dim:
+        s += _lin("add_embedding.linear_1", T, 6 * cfg.add_time_dim + cfg.pooled_dim) + _lin("add_embedding.linear_2", T, T)
     down, up = unet_structure(cfg)
+    L = len(C)
+    tf = lambda name, c, depth: _transformer(name, c, cfg.ctx_dim, depth, cfg.linear_proj)
     for i, blk in enumerate(down):
         for j, (ci, co) in enumerate(blk["res"]):
             s += _resnet(f"down_blocks.{i}.resnets.{j}", ci, co, T)
             if blk["attn"]:
-                s += _transformer(f"down_blocks.{i}.attentions.{j}", co, cfg.ctx_dim)
+                s += tf(f"down_blocks.{i}.attentions.{j}", co, cfg.depth(i))
         if blk["down"]:
             s += _conv(f"down_blocks.{i}.downsamplers.0.conv", blk["ch"], blk["ch"], 3)
     cm = C[-1]
     s += _resnet("mid_block.resnets.0", cm, cm, T)
-    s += _transformer("mid_block.attentions.0", cm, cfg.ctx_dim)
+    s += tf("mid_block.attentions.0", cm, cfg.mid_depth)
     s += _resnet("mid_block.resnets.1", cm, cm, T)
     for i, blk in enumerate(up):
         for j, (ci, co) in enumerate(blk["res"]):
             s += _resnet(f"up_blocks.{i}.resnets.{j}", ci, co, T)
             if blk["attn"]:
-                s += _transformer(f"up_blocks.{i}.attentions.{j}", co, cfg.ctx_dim)
+                s += tf(f"up_blocks.{i}.attentions.{j}", co, cfg.depth(L - 1 - i))
         if blk["up"]:
             s += _conv(f"up_blocks.{i}.upsamplers.0.conv", blk["ch"], blk["ch"], 3)
     s += _norm("conv_norm_out", C[0]) + _conv("conv_out", cfg.out_ch, C[0], 3)

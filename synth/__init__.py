@@ -138,6 +138,16 @@ def uncond_embedding(weight_seed: int, length: int, dim: int) -> np.ndarray:
     return normal(tensor_seed(weight_seed, "ctx/uncond"), length * dim).reshape(length, dim)
 
 
+def pooled_embedding(trace_seed: int, req_id: int, dim: int) -> np.ndarray:
+    """Synthetic pooled text embedding [dim] ~ N(0,1) for SDXL's added conditioning (R20, R27)."""
+    return normal(tensor_seed(trace_seed, f"pooled/{req_id}"), dim)
+
+
+def uncond_pooled(weight_seed: int, dim: int) -> np.ndarray:
+    """The unconditional pooled embedding (SDXL), fixed seed (R20)."""
+    return normal(tensor_seed(weight_seed, "pooled/uncond"), dim)
+
+
 def initial_noise(trace_seed: int, req_id: int, h: int, w: int) -> np.ndarray:
     """z ~ N(0,1) [4][h][w] per (trace seed, id) (R20)."""
     return normal(tensor_seed(trace_seed, f"noise/{req_id}"), 4 * h * w).reshape(4, h, w)

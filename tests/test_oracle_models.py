@@ -181,3 +181,55 @@ def test_chunk_ranges_minmax(rng):
         assert mx == best
         # ties cut earlier: lexicographically smallest optimal boundary vector
         assert b == min(p for v, p in opts if v == best)
+
+
+def test_sdxl_param_count():
+    # diffusers SDXL-base UNet2DConditionModel has 2,567,463,684 parameters (public count): pins the
+    # depth (0, 2, 10) / mid 10 transformers, head-dim heads, linear projections and the 2816-wide
+    # "text_time" added embedding of configs.SDXL_UNET
+    n = sum(int(np.prod(s[1])) for s in configs.unet_param_specs(configs.SDXL_UNET))
+    assert n == 2_567_463_684
+
+
+def test_generalised_path_reduces_to_sd15_path(P64):
+    """The SDXL generalisations with depth 1, linear projections (same values as a 1×1 conv: the
+    generator is indexed in canonical layout) and no added embedding are the SD-1.5 network."""
+    import dataclasses
+    T2 = dataclasses.replace(T, name="tiny_lin", linear_proj=True, tf_depth=(1, 1), mid_depth=1)
+    P2 = configs.unet_params(T2, 0, np.float64)
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((2, 4, 8, 8))
+    t = np.array([801, 41])
+    ctx = _ctx(2)
+    np.testing.assert_allclose(unet.forward(P2, T2, x, t, ctx), unet.forward(P64, T, x, t, ctx), rtol=1e-10,
+                               atol=1e-12)
+
+
+def _xl_inputs(n, seed=7):
+    X = configs.TINY_XL_UNET
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((n, 4, 8, 8))
+    ctx = np.stack([synth.text_embedding(seed, i, X.ctx_len, X.ctx_dim) for i in range(n)]).astype(np.float64)
+    pooled = np.stack([synth.pooled_embedding(seed, i, X.pooled_dim) for i in range(n)]).astype(np.float64)
+    return x, ctx, pooled
+
+
+def test_tinyxl_rows_depth_and_added_conditioning():
+    """I1 for the SDXL-shaped path; the output depends on the pooled embedding and on the time ids
+    (added conditioning reaches every ResBlock through temb), and fp32 agrees with fp64 (I2)."""
+    X = configs.TINY_XL_UNET
+    P = configs.unet_params(X, 0, np.float64)
+    x, ctx, pooled = _xl_inputs(3)
+    t = np.array([901, 401, 21])
+    e = unet.forward(P, X, x, t, ctx, pooled)
+    for i in range(3):
+        ei = unet.forward(P, X, x[i:i + 1], t[i:i + 1], ctx[i:i + 1], pooled[i:i + 1])
+        np.testing.assert_allclose(ei[0], e[i], rtol=1e-12, atol=1e-13)
+    e_p = unet.forward(P, X, x[:1], t[:1], ctx[:1], pooled[1:2])
+    assert np.linalg.norm(e_p[0] - e[0]) > 1e-4 * np.linalg.norm(e[0])
+    ids = np.array([[512, 512, 0, 0, 512, 512]], dtype=np.float64)
+    e_t = unet.forward(P, X, x[:1], t[:1], ctx[:1], pooled[:1], ids)
+    assert np.linalg.norm(e_t[0] - e[0]) > 1e-4 * np.linalg.norm(e[0])
+    P32 = configs.unet_params(X, 0, np.float32)
+    e32 = unet.forward(P32, X, x.astype(np.float32), t, ctx.astype(np.float32), pooled.astype(np.float32))
+    assert np.linalg.norm(e32 - e) / np.linalg.norm(e) < 1e-5
