@@ -40,7 +40,9 @@ enum {
   SD_E_NOTSUP = -6  /* configuration not supported by this build                            */
 };
 
-enum { SD_MODEL_TINY = 0, SD_MODEL_SD15 = 1 };          /* R1: diffusers SD-1.5 shapes; tiny = CFG#1 */
+/* R1: diffusers SD-1.5 / SDXL-base shapes (oracle/configs.py); tiny = CFG#1; tiny-XL = the SDXL code
+ * paths (no attention at level 0, depth-2 transformers, head-dim heads, added embedding) at tiny size */
+enum { SD_MODEL_TINY = 0, SD_MODEL_SD15 = 1, SD_MODEL_SDXL = 2, SD_MODEL_TINY_XL = 3 };
 enum { SD_PREC_BF16 = 0 };                               /* bf16 storage, fp32 accumulate (R19)       */
 enum { SD_SAMPLER_DDIM = 0, SD_SAMPLER_EULER = 1 };      /* R4 / R5                                  */
 
@@ -55,7 +57,7 @@ typedef struct sd_controller sd_controller;
  * ON THE DEVICE from the counter-based generator keyed by (weight_seed, parameter name) (R20,
  * synth/__init__.py documents the generator). */
 typedef struct {
-  int32_t model;          /* SD_MODEL_*                                        */
+  int32_t model;          /* SD_MODEL_* (SDXL: ~5.6 GB of bf16 weights)         */
   int32_t precision;      /* SD_PREC_BF16                                      */
   int32_t sampler;        /* SD_SAMPLER_*                                      */
   int32_t max_latent_hw;  /* e.g. 64 for 512x512 images                        */
@@ -87,6 +89,15 @@ sd_status sd_engine_profile_read(sd_engine* e, int32_t cls, double* ms_out, int6
 sd_status sd_ctx_register(sd_engine* e, const float* text_emb_dev, int32_t len, int32_t dim, int32_t* slot_out,
                           void* stream);
 sd_status sd_ctx_set_uncond(sd_engine* e, const float* text_emb_dev, int32_t len, int32_t dim, void* stream);
+/* SDXL variants (SD_MODEL_SDXL / SD_MODEL_TINY_XL need them; the two calls above return SD_E_INVAL
+ * for those models): pooled_dev = device fp32 [pooled_dim] pooled text embedding (1280 for SDXL).
+ * Besides the text K/V, the slot caches the prompt's "text_time" added embedding (R27: time ids
+ * (1024,1024,0,0,1024,1024), 256-d sinusoids ‖ pooled → Linear → SiLU → Linear, fp32 [1280]),
+ * which every UNet row of that prompt adds to linear_2 of the time embedding. */
+sd_status sd_ctx_register_pooled(sd_engine* e, const float* text_emb_dev, int32_t len, int32_t dim,
+                                 const float* pooled_dev, int32_t pooled_dim, int32_t* slot_out, void* stream);
+sd_status sd_ctx_set_uncond_pooled(sd_engine* e, const float* text_emb_dev, int32_t len, int32_t dim,
+                                   const float* pooled_dev, int32_t pooled_dim, void* stream);
 sd_status sd_ctx_release(sd_engine* e, int32_t slot);
 
 /* One UNet step for n_req requests at one resolution (R22). Rows: one conditional row per
@@ -173,6 +184,8 @@ typedef struct {
   float guidance;               /* g_i                                                           */
   const float* text_emb_host;   /* fp32 [emb_len][emb_dim], copied at submit                     */
   int32_t emb_len, emb_dim;
+  const float* pooled_host;     /* SDXL: fp32 [pooled_dim] pooled text embedding (else NULL / 0) */
+  int32_t pooled_dim;
 } sd_request;
 typedef struct {
   uint64_t id;

@@ -14,12 +14,13 @@ import numpy as np
 from . import sampling, unet
 
 
-def step_batch(P, cfg, reqs, ctx_uncond, sampler="ddim"):
-    """reqs: list of dict(x [4,h,w], ctx [L,D], step s_r, n_steps n_r, has_uncond, g). Returns new x list."""
+def step_batch(P, cfg, reqs, ctx_uncond, sampler="ddim", pooled_uncond=None):
+    """reqs: list of dict(x [4,h,w], ctx [L,D], step s_r, n_steps n_r, has_uncond, g[, pooled (SDXL)]).
+    Returns new x list."""
     if not reqs:
         return []
     dt = reqs[0]["x"].dtype
-    rows_x, rows_t, rows_c = [], [], []
+    rows_x, rows_t, rows_c, rows_p = [], [], [], []
     order = [(i, False) for i in range(len(reqs))] + [(i, True) for i, r in enumerate(reqs) if r["has_uncond"]]
     for i, unc in order:
         r = reqs[i]
@@ -27,7 +28,10 @@ def step_batch(P, cfg, reqs, ctx_uncond, sampler="ddim"):
         rows_x.append(r["x"] * dt.type(sampling.c_in(sampler, r["n_steps"], r["step"])))
         rows_t.append(t)
         rows_c.append(ctx_uncond if unc else r["ctx"])
-    eps = unet.forward(P, cfg, np.stack(rows_x), np.array(rows_t), np.stack(rows_c).astype(dt))
+        if cfg.add_time_dim:
+            rows_p.append(pooled_uncond if unc else r["pooled"])
+    pooled = np.stack(rows_p).astype(dt) if cfg.add_time_dim else None
+    eps = unet.forward(P, cfg, np.stack(rows_x), np.array(rows_t), np.stack(rows_c).astype(dt), pooled)
     out = []
     uidx = {i: len(reqs) + k for k, i in enumerate([i for i, u in order[len(reqs):]])}
     for i, r in enumerate(reqs):

@@ -14,7 +14,7 @@ from .build import LIB
 _lib = None
 
 SD_OK, SD_E_INVAL, SD_E_NOMEM, SD_E_CUDA, SD_E_AGAIN, SD_E_STATE, SD_E_NOTSUP = 0, -1, -2, -3, -4, -5, -6
-SD_MODEL_TINY, SD_MODEL_SD15 = 0, 1
+SD_MODEL_TINY, SD_MODEL_SD15, SD_MODEL_SDXL, SD_MODEL_TINY_XL = 0, 1, 2, 3
 SD_SAMPLER_DDIM, SD_SAMPLER_EULER = 0, 1
 ACT_NONE, ACT_SILU, ACT_GEGLU = 0, 1, 2
 
@@ -51,7 +51,8 @@ class ServeConfig(C.Structure):
 
 class Request(C.Structure):
     _fields_ = [("id", C.c_uint64), ("arrival_us", C.c_int64), ("n_steps", C.c_int32), ("guidance", C.c_float),
-                ("text_emb_host", C.c_void_p), ("emb_len", C.c_int32), ("emb_dim", C.c_int32)]
+                ("text_emb_host", C.c_void_p), ("emb_len", C.c_int32), ("emb_dim", C.c_int32),
+                ("pooled_host", C.c_void_p), ("pooled_dim", C.c_int32)]
 
 
 class Completion(C.Structure):
@@ -81,6 +82,8 @@ SIGNATURES = {
     "sd_engine_profile_read": [P, I32, C.POINTER(C.c_double), PI64, C.POINTER(C.c_double)],
     "sd_ctx_register": [P, P, I32, I32, PI32, P],
     "sd_ctx_set_uncond": [P, P, I32, I32, P],
+    "sd_ctx_register_pooled": [P, P, I32, I32, P, I32, PI32, P],
+    "sd_ctx_set_uncond_pooled": [P, P, I32, I32, P, I32, P],
     "sd_ctx_release": [P, I32],
     "sd_step_batch": [P, C.POINTER(Batch), P],
     "sd_sampler_init_sigma": [P, I32, C.POINTER(C.c_float)],

@@ -40,7 +40,9 @@ float init_sigma(int sampler, int n);
 
 extern "C" sd_status sd_engine_create(const sd_engine_config* cfg, int32_t dev, sd_engine** out) {
   SD_REQUIRE(cfg && out, "sd_engine_create: null argument");
-  SD_REQUIRE(cfg->model == SD_MODEL_TINY || cfg->model == SD_MODEL_SD15, "sd_engine_create: unknown model");
+  SD_REQUIRE(cfg->model == SD_MODEL_TINY || cfg->model == SD_MODEL_SD15 || cfg->model == SD_MODEL_SDXL ||
+                 cfg->model == SD_MODEL_TINY_XL,
+             "sd_engine_create: unknown model");
   SD_REQUIRE(cfg->precision == SD_PREC_BF16, "sd_engine_create: only SD_PREC_BF16 is built");
   SD_REQUIRE(cfg->sampler == SD_SAMPLER_DDIM || cfg->sampler == SD_SAMPLER_EULER, "sd_engine_create: sampler");
   SD_REQUIRE(cfg->max_latent_hw >= 8 && cfg->max_latent_hw <= 256, "sd_engine_create: max_latent_hw");
@@ -88,14 +90,36 @@ extern "C" sd_status sd_ctx_register(sd_engine* e, const float* emb, int32_t len
   ENGINE_GUARD(e);
   SD_REQUIRE(emb && slot_out, "sd_ctx_register: null argument");
   SD_REQUIRE(len == e->e.uc.ctx_len && dim == e->e.uc.ctx_dim, "sd_ctx_register: embedding shape");
-  ENGINE_BODY(e, { *slot_out = ctx_register(&e->e, emb, len, dim, -1, static_cast<cudaStream_t>(stream)); })
+  SD_REQUIRE(!e->e.uc.add_time_dim, "sd_ctx_register: this model needs sd_ctx_register_pooled");
+  ENGINE_BODY(e, { *slot_out = ctx_register(&e->e, emb, len, dim, nullptr, 0, -1, static_cast<cudaStream_t>(stream)); })
+}
+
+extern "C" sd_status sd_ctx_register_pooled(sd_engine* e, const float* emb, int32_t len, int32_t dim,
+                                            const float* pooled, int32_t pooled_dim, int32_t* slot_out, void* stream) {
+  ENGINE_GUARD(e);
+  SD_REQUIRE(emb && pooled && slot_out, "sd_ctx_register_pooled: null argument");
+  SD_REQUIRE(len == e->e.uc.ctx_len && dim == e->e.uc.ctx_dim, "sd_ctx_register_pooled: embedding shape");
+  SD_REQUIRE(e->e.uc.add_time_dim && pooled_dim == e->e.uc.pooled_dim, "sd_ctx_register_pooled: pooled shape/model");
+  ENGINE_BODY(e, {
+    *slot_out = ctx_register(&e->e, emb, len, dim, pooled, pooled_dim, -1, static_cast<cudaStream_t>(stream));
+  })
+}
+
+extern "C" sd_status sd_ctx_set_uncond_pooled(sd_engine* e, const float* emb, int32_t len, int32_t dim,
+                                              const float* pooled, int32_t pooled_dim, void* stream) {
+  ENGINE_GUARD(e);
+  SD_REQUIRE(emb && pooled, "sd_ctx_set_uncond_pooled: null argument");
+  SD_REQUIRE(len == e->e.uc.ctx_len && dim == e->e.uc.ctx_dim, "sd_ctx_set_uncond_pooled: embedding shape");
+  SD_REQUIRE(e->e.uc.add_time_dim && pooled_dim == e->e.uc.pooled_dim, "sd_ctx_set_uncond_pooled: pooled shape/model");
+  ENGINE_BODY(e, { ctx_register(&e->e, emb, len, dim, pooled, pooled_dim, 0, static_cast<cudaStream_t>(stream)); })
 }
 
 extern "C" sd_status sd_ctx_set_uncond(sd_engine* e, const float* emb, int32_t len, int32_t dim, void* stream) {
   ENGINE_GUARD(e);
   SD_REQUIRE(emb, "sd_ctx_set_uncond: null argument");
   SD_REQUIRE(len == e->e.uc.ctx_len && dim == e->e.uc.ctx_dim, "sd_ctx_set_uncond: embedding shape");
-  ENGINE_BODY(e, { ctx_register(&e->e, emb, len, dim, 0, static_cast<cudaStream_t>(stream)); })
+  SD_REQUIRE(!e->e.uc.add_time_dim, "sd_ctx_set_uncond: this model needs sd_ctx_set_uncond_pooled");
+  ENGINE_BODY(e, { ctx_register(&e->e, emb, len, dim, nullptr, 0, 0, static_cast<cudaStream_t>(stream)); })
 }
 
 extern "C" sd_status sd_ctx_release(sd_engine* e, int32_t slot) {

@@ -153,6 +153,19 @@ void f32_to_bf16(const float* x, bf16* y, long n, cudaStream_t st) {
   SD_CHECK_LAUNCH();
 }
 
+// dst[r][0..n) = src[idx[r]][0..n) (fp32): the SDXL added embedding of each row's prompt slot
+__global__ void gather_rows_f32_kernel(const float* __restrict__ src, const int* __restrict__ idx, int n,
+                                       float* __restrict__ dst) {
+  const int r = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[(long)r * n + i] = src[(long)idx[r] * n + i];
+}
+
+void gather_rows_f32(const float* src, const int* idx, int rows, int n, float* dst, cudaStream_t st) {
+  gather_rows_f32_kernel<<<dim3(cdiv(n, 256), rows), 256, 0, st>>>(src, idx, n, dst);
+  SD_CHECK_LAUNCH();
+}
+
 __global__ void latent_to_nhwc_kernel(const float* __restrict__ z, int hw, float scale, int cpad,
                                       bf16* __restrict__ out) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;

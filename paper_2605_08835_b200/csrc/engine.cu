@@ -25,7 +25,7 @@ UNetCfg unet_cfg(int model) {
     c.heads = 2;
     c.ctx_dim = 32;
     c.ctx_len = 8;
-  } else {
+  } else if (model == SD_MODEL_SD15) {
     c.block_out = {320, 640, 1280, 1280};
     c.attn = {1, 1, 1, 0};
     c.layers = 2;
@@ -33,13 +33,39 @@ UNetCfg unet_cfg(int model) {
     c.heads = 8;
     c.ctx_dim = 768;
     c.ctx_len = 77;
+  } else if (model == SD_MODEL_SDXL) {
+    c.block_out = {320, 640, 1280};
+    c.attn = {0, 1, 1};
+    c.depth = {0, 2, 10};
+    c.mid_depth = 10;
+    c.layers = 2;
+    c.groups = 32;
+    c.heads = 0;
+    c.head_dim = 64;
+    c.ctx_dim = 2048;
+    c.ctx_len = 77;
+    c.add_time_dim = 256;
+    c.pooled_dim = 1280;
+  } else {  // SD_MODEL_TINY_XL
+    c.block_out = {32, 64};
+    c.attn = {0, 1};
+    c.depth = {0, 2};
+    c.mid_depth = 2;
+    c.layers = 1;
+    c.groups = 8;
+    c.heads = 0;
+    c.head_dim = 16;
+    c.ctx_dim = 48;
+    c.ctx_len = 8;
+    c.add_time_dim = 8;
+    c.pooled_dim = 40;
   }
   return c;
 }
 
 VAECfg vae_cfg(int model) {
   VAECfg c;
-  if (model == SD_MODEL_TINY) {
+  if (model == SD_MODEL_TINY || model == SD_MODEL_TINY_XL) {
     c.block_out = {32, 64};
     c.layers = 1;
     c.groups = 8;
@@ -48,7 +74,7 @@ VAECfg vae_cfg(int model) {
     c.layers = 2;
     c.groups = 32;
   }
-  c.sf = 0.18215f;
+  c.sf = model == SD_MODEL_SDXL ? 0.13025f : 0.18215f;
   return c;
 }
 
@@ -160,34 +186,38 @@ static void build_res(Builder& B, const std::string& p, int cin, int cout, int* 
   if (cin != cout) r->wsc = B.lin(p + ".conv_shortcut", cout, cin, &r->bsc);
 }
 
-static void build_tf(Builder& B, const std::string& p, int C, int* kv_cursor, TfW* t) {
+static void build_tf(Builder& B, const std::string& p, int C, int depth, int* kv_cursor, TfW* t) {
   Engine* e = B.e;
   const int D = e->uc.ctx_dim;
   t->C = C;
   B.norm(p + ".norm", C, &t->gng, &t->gnb);
-  t->wpin = B.lin(p + ".proj_in", C, C, &t->bpin);
-  const std::string b = p + ".transformer_blocks.0";
-  B.norm(b + ".norm1", C, &t->l1g, &t->l1b);
-  t->wqkv = B.alloc<bf16>(3L * C * C);
-  B.lin(b + ".attn1.to_q", C, C, nullptr, t->wqkv);
-  B.lin(b + ".attn1.to_k", C, C, nullptr, t->wqkv + (long)C * C);
-  B.lin(b + ".attn1.to_v", C, C, nullptr, t->wqkv + 2L * C * C);
-  t->wo = B.lin(b + ".attn1.to_out.0", C, C, &t->bo);
-  B.norm(b + ".norm2", C, &t->l2g, &t->l2b);
-  t->wq2 = B.lin(b + ".attn2.to_q", C, C, nullptr);
-  t->koff = *kv_cursor;
-  B.lin(b + ".attn2.to_k", C, D, nullptr, e->U.kv_all_w + (long)t->koff * D);
-  t->voff = *kv_cursor + C;
-  B.lin(b + ".attn2.to_v", C, D, nullptr, e->U.kv_all_w + (long)t->voff * D);
-  *kv_cursor += 2 * C;
-  t->wo2 = B.lin(b + ".attn2.to_out.0", C, C, &t->bo2);
-  B.norm(b + ".norm3", C, &t->l3g, &t->l3b);
-  // GEGLU proj [8C][C] with rows interleaved per 64 (value | gate) for the fused epilogue
-  t->wff1 = B.alloc<bf16>(8L * C * C);
-  B.gen(b + ".ff.net.0.proj.weight", 8L * C * C, WK_UNIFORM, C, WL_GEGLU, t->wff1, nullptr, true, 0, 0, 0, 0, 4 * C);
-  t->bff1 = B.alloc<float>(8L * C);
-  B.gen(b + ".ff.net.0.proj.bias", 8L * C, WK_UNIFORM, C, WL_GEGLU, t->bff1, nullptr, false, 0, 0, 0, 0, 4 * C);
-  t->wff2 = B.lin(b + ".ff.net.2", C, 4 * C, &t->bff2);
+  t->wpin = B.lin(p + ".proj_in", C, C, &t->bpin);  // 1×1 conv or Linear: the same [C][C] values
+  for (int d = 0; d < depth; ++d) {
+    BlkW k{};
+    const std::string b = p + ".transformer_blocks." + std::to_string(d);
+    B.norm(b + ".norm1", C, &k.l1g, &k.l1b);
+    k.wqkv = B.alloc<bf16>(3L * C * C);
+    B.lin(b + ".attn1.to_q", C, C, nullptr, k.wqkv);
+    B.lin(b + ".attn1.to_k", C, C, nullptr, k.wqkv + (long)C * C);
+    B.lin(b + ".attn1.to_v", C, C, nullptr, k.wqkv + 2L * C * C);
+    k.wo = B.lin(b + ".attn1.to_out.0", C, C, &k.bo);
+    B.norm(b + ".norm2", C, &k.l2g, &k.l2b);
+    k.wq2 = B.lin(b + ".attn2.to_q", C, C, nullptr);
+    k.koff = *kv_cursor;
+    B.lin(b + ".attn2.to_k", C, D, nullptr, e->U.kv_all_w + (long)k.koff * D);
+    k.voff = *kv_cursor + C;
+    B.lin(b + ".attn2.to_v", C, D, nullptr, e->U.kv_all_w + (long)k.voff * D);
+    *kv_cursor += 2 * C;
+    k.wo2 = B.lin(b + ".attn2.to_out.0", C, C, &k.bo2);
+    B.norm(b + ".norm3", C, &k.l3g, &k.l3b);
+    // GEGLU proj [8C][C] with rows interleaved per 64 (value | gate) for the fused epilogue
+    k.wff1 = B.alloc<bf16>(8L * C * C);
+    B.gen(b + ".ff.net.0.proj.weight", 8L * C * C, WK_UNIFORM, C, WL_GEGLU, k.wff1, nullptr, true, 0, 0, 0, 0, 4 * C);
+    k.bff1 = B.alloc<float>(8L * C);
+    B.gen(b + ".ff.net.0.proj.bias", 8L * C, WK_UNIFORM, C, WL_GEGLU, k.bff1, nullptr, false, 0, 0, 0, 0, 4 * C);
+    k.wff2 = B.lin(b + ".ff.net.2", C, 4 * C, &k.bff2);
+    t->blk.push_back(k);
+  }
   t->wpout = B.lin(p + ".proj_out", C, C, &t->bpout);
 }
 
@@ -203,14 +233,14 @@ static void build_unet(Engine* e, cudaStream_t st) {
     for (int i = 0; i < L; ++i) {
       out = c.block_out[i];
       temb_total += c.layers * out;
-      if (c.attn[i]) kv_total += c.layers * 2 * out;
+      kv_total += c.layers * c.depth_at(i) * 2 * out;
     }
     temb_total += 2 * c.block_out[L - 1];
-    kv_total += 2 * c.block_out[L - 1];
+    kv_total += c.mid_depth * 2 * c.block_out[L - 1];
     for (int i = 0; i < L; ++i) {
       const int o = c.block_out[L - 1 - i];
       temb_total += (c.layers + 1) * o;
-      if (c.attn[L - 1 - i]) kv_total += (c.layers + 1) * 2 * o;
+      kv_total += (c.layers + 1) * c.depth_at(L - 1 - i) * 2 * o;
     }
   }
   UNetW& U = e->U;
@@ -225,6 +255,10 @@ static void build_unet(Engine* e, cudaStream_t st) {
   U.conv_in_w = B.conv3("conv_in", c.block_out[0], c.in_ch, 64, &U.conv_in_b);
   U.lin1_w = B.lin("time_embedding.linear_1", T, c.block_out[0], &U.lin1_b);
   U.lin2_w = B.lin("time_embedding.linear_2", T, T, &U.lin2_b);
+  if (c.add_time_dim) {
+    U.add1_w = B.lin("add_embedding.linear_1", T, c.add_in(), &U.add1_b);
+    U.add2_w = B.lin("add_embedding.linear_2", T, T, &U.add2_b);
+  }
   int out = c.block_out[0];
   for (int i = 0; i < L; ++i) {
     const int in = out;
@@ -239,7 +273,8 @@ static void build_unet(Engine* e, cudaStream_t st) {
       d.res.push_back(r);
       if (c.attn[i]) {
         TfW t;
-        build_tf(B, "down_blocks." + std::to_string(i) + ".attentions." + std::to_string(j), out, &kcur, &t);
+        build_tf(B, "down_blocks." + std::to_string(i) + ".attentions." + std::to_string(j), out, c.depth_at(i), &kcur,
+                 &t);
         d.tf.push_back(t);
       }
     }
@@ -248,7 +283,7 @@ static void build_unet(Engine* e, cudaStream_t st) {
   }
   const int cm = c.block_out[L - 1];
   build_res(B, "mid_block.resnets.0", cm, cm, &tcur, &U.mid0, true);
-  build_tf(B, "mid_block.attentions.0", cm, &kcur, &U.midtf);
+  build_tf(B, "mid_block.attentions.0", cm, c.mid_depth, &kcur, &U.midtf);
   build_res(B, "mid_block.resnets.1", cm, cm, &tcur, &U.mid1, true);
   out = c.block_out[L - 1];
   for (int i = 0; i < L; ++i) {
@@ -268,7 +303,8 @@ static void build_unet(Engine* e, cudaStream_t st) {
       u.res.push_back(r);
       if (c.attn[L - 1 - i]) {
         TfW t;
-        build_tf(B, "up_blocks." + std::to_string(i) + ".attentions." + std::to_string(j), out, &kcur, &t);
+        build_tf(B, "up_blocks." + std::to_string(i) + ".attentions." + std::to_string(j), out, c.depth_at(L - 1 - i),
+                 &kcur, &t);
         u.tf.push_back(t);
       }
     }
@@ -330,6 +366,7 @@ Engine::~Engine() {
   warena.release();
   ws.release();
   if (kv_cache) cudaFree(kv_cache);
+  if (aug_cache) cudaFree(aug_cache);
   if (meta_dev) cudaFree(meta_dev);
   for (auto& kv : graphs)
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
@@ -357,7 +394,9 @@ void build_engine(Engine* e) {
   e->uc = unet_cfg(e->cfg.model);
   e->vc = vae_cfg(e->cfg.model);
   e->max_rows = 2 * e->cfg.b_max;
-  const size_t wbytes = e->cfg.model == SD_MODEL_SD15 ? ((size_t)2200 << 20) : ((size_t)64 << 20);
+  const size_t wbytes = e->cfg.model == SD_MODEL_SD15   ? ((size_t)2200 << 20)
+                        : e->cfg.model == SD_MODEL_SDXL ? ((size_t)5600 << 20)
+                                                        : ((size_t)64 << 20);
   e->warena.init(wbytes);
   cudaStream_t st;
   SD_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
@@ -371,6 +410,10 @@ void build_engine(Engine* e) {
   e->slot_elems = (long)e->uc.ctx_len * e->U.kv_width;
   SD_CUDA(cudaMalloc(&e->kv_cache, (size_t)e->max_slots * e->slot_elems * 2));
   SD_CUDA(cudaMemset(e->kv_cache, 0, (size_t)e->max_slots * e->slot_elems * 2));
+  if (e->uc.add_time_dim) {
+    SD_CUDA(cudaMalloc(&e->aug_cache, (size_t)e->max_slots * e->uc.temb_dim() * sizeof(float)));
+    SD_CUDA(cudaMemset(e->aug_cache, 0, (size_t)e->max_slots * e->uc.temb_dim() * sizeof(float)));
+  }
   e->slot_used.assign(e->max_slots, 0);
   e->slot_used[0] = 1;
   e->meta_bytes = 64 << 10;
@@ -390,8 +433,56 @@ void build_engine(Engine* e) {
 // ---------------------------------------------------------------------------------------------
 // text K/V cache (computed once per prompt at admission; K/V do not depend on x or t)
 // ---------------------------------------------------------------------------------------------
-int ctx_register(Engine* e, const float* emb, int len, int dim, int slot, cudaStream_t st) {
+// SDXL "text_time" added embedding of one prompt (R27): [sinusoid_256(id_k) for the 6 time ids ‖
+// pooled] → Linear → SiLU → Linear, cached per slot in fp32 and added to linear_2's output per row
+static void added_embedding(Engine* e, const float* pooled, int slot, cudaStream_t st) {
+  const UNetCfg& c = e->uc;
+  const int T = c.temb_dim(), K = c.add_in(), td = c.add_time_dim;
+  static const float ids[6] = {1024.f, 1024.f, 0.f, 0.f, 1024.f, 1024.f};  // R27
+  float* ids_dev;
+  bf16 *row, *hid;
+  SD_CUDA(cudaMallocAsync(&ids_dev, sizeof(ids), st));
+  SD_CUDA(cudaMallocAsync(&row, (size_t)K * 2, st));
+  SD_CUDA(cudaMallocAsync(&hid, (size_t)T * 2, st));
+  SD_CUDA(cudaMemcpyAsync(ids_dev, ids, sizeof(ids), cudaMemcpyHostToDevice, st));
+  timestep_sinusoid(ids_dev, 6, td, row, st);      // [6][td] = one row of 6·td
+  f32_to_bf16(pooled, row + 6 * td, c.pooled_dim, st);
+  GemmDesc d;
+  d.A = row;
+  d.M = 1;
+  d.K = K;
+  d.lda = K;
+  d.Bw[0] = e->U.add1_w;
+  d.N = T;
+  d.ldb = K;
+  d.out = hid;
+  d.ldo = T;
+  d.bias = e->U.add1_b;
+  d.act = ACT_SILU;
+  gemm(d, st);
+  GemmDesc d2;
+  d2.A = hid;
+  d2.M = 1;
+  d2.K = T;
+  d2.lda = T;
+  d2.Bw[0] = e->U.add2_w;
+  d2.N = T;
+  d2.ldb = T;
+  d2.out = e->aug_cache + (long)slot * T;
+  d2.ldo = T;
+  d2.out_f32 = 1;
+  d2.bias = e->U.add2_b;
+  gemm(d2, st);
+  SD_CUDA(cudaFreeAsync(hid, st));
+  SD_CUDA(cudaFreeAsync(row, st));
+  SD_CUDA(cudaFreeAsync(ids_dev, st));
+}
+
+int ctx_register(Engine* e, const float* emb, int len, int dim, const float* pooled, int pooled_dim, int slot,
+                 cudaStream_t st) {
   if (len != e->uc.ctx_len || dim != e->uc.ctx_dim) throw std::invalid_argument("ctx shape mismatch");
+  if (e->uc.add_time_dim && (!pooled || pooled_dim != e->uc.pooled_dim))
+    throw std::invalid_argument("this model needs the pooled text embedding (SDXL added conditioning)");
   if (slot < 0) {
     std::lock_guard<std::mutex> g(e->mu);
     for (int s = 1; s < e->max_slots; ++s)
@@ -417,6 +508,7 @@ int ctx_register(Engine* e, const float* emb, int len, int dim, int slot, cudaSt
   d.ldo = e->U.kv_width;
   gemm(d, st);
   SD_CUDA(cudaFreeAsync(tmp, st));
+  if (e->uc.add_time_dim) added_embedding(e, pooled, slot, st);
   return slot;
 }
 
@@ -523,78 +615,83 @@ struct Fwd {
   bf16* transformer(const TfW& t, const bf16* x, int H, int W) {
     const int C = t.C, P = H * W;
     const long T = (long)R * P;
-    const int heads = e->uc.heads, dh = C / heads;
+    const int heads = e->uc.heads_at(C), dh = C / heads;
     bf16* out = buf(T * C);
     const size_t mk = e->ws.mark();
     bf16* a = buf(T * C);
     gn(x, a, P, C, t.gng, t.gnb, e->uc.eps_tf, false);
     bf16* h = buf(T * C);
     linear(a, T, C, t.wpin, C, t.bpin, h, C);
-    bf16* n = buf(T * C);
-    ln(h, n, T, C, t.l1g, t.l1b);
-    bf16* o = buf(T * C);
-    if (e->use_attn_tc && attention_tc_supported(dh, P, C)) {
-      // tcgen05 flash attention: q|k token-major from one GEMM, Vᵀ channel-major from another
-      bf16* qk = buf(T * 2 * C);
-      linear(n, T, C, t.wqkv, 2 * C, nullptr, qk, 2 * C);
-      bf16* vt = buf(T * C);
-      linear(t.wqkv + 2L * C * C, C, C, n, (int)T, nullptr, vt, (int)T);
-      const int pi = e->prof.begin(PC_ATTN, st, 4.0 * R * heads * (double)P * P * dh);
-      attention_tc(qk, vt, o, R, heads, dh, C, P, st);
-      e->prof.end(pi, st);
-    } else {
-    bf16* qkv = buf(T * 3 * C);
-    linear(n, T, C, t.wqkv, 3 * C, nullptr, qkv, 3 * C);
-    AttnDesc ad{};
-    ad.Q = qkv;
-    ad.ldq = 3 * C;
-    ad.q_bstride = (long)P * 3 * C;
-    ad.K = qkv + C;
-    ad.V = qkv + 2 * C;
-    ad.ldk = 3 * C;
-    ad.kv_bstride = (long)P * 3 * C;
-    ad.kv_index = nullptr;
-    ad.O = o;
-    ad.ldo = C;
-    ad.o_bstride = (long)P * C;
-    ad.rows = R;
-    ad.heads = heads;
-    ad.d = dh;
-    ad.Lq = P;
-    ad.Lk = P;
-    attn(ad);
+    bf16* hb = buf(T * C);  // ping-pong hidden state across blocks
+    for (const BlkW& k : t.blk) {
+      const size_t mb = e->ws.mark();
+      bf16* n = buf(T * C);
+      ln(h, n, T, C, k.l1g, k.l1b);
+      bf16* o = buf(T * C);
+      if (e->use_attn_tc && attention_tc_supported(dh, P, C)) {
+        // tcgen05 flash attention: q|k token-major from one GEMM, Vᵀ channel-major from another
+        bf16* qk = buf(T * 2 * C);
+        linear(n, T, C, k.wqkv, 2 * C, nullptr, qk, 2 * C);
+        bf16* vt = buf(T * C);
+        linear(k.wqkv + 2L * C * C, C, C, n, (int)T, nullptr, vt, (int)T);
+        const int pi = e->prof.begin(PC_ATTN, st, 4.0 * R * heads * (double)P * P * dh);
+        attention_tc(qk, vt, o, R, heads, dh, C, P, st);
+        e->prof.end(pi, st);
+      } else {
+        bf16* qkv = buf(T * 3 * C);
+        linear(n, T, C, k.wqkv, 3 * C, nullptr, qkv, 3 * C);
+        AttnDesc ad{};
+        ad.Q = qkv;
+        ad.ldq = 3 * C;
+        ad.q_bstride = (long)P * 3 * C;
+        ad.K = qkv + C;
+        ad.V = qkv + 2 * C;
+        ad.ldk = 3 * C;
+        ad.kv_bstride = (long)P * 3 * C;
+        ad.kv_index = nullptr;
+        ad.O = o;
+        ad.ldo = C;
+        ad.o_bstride = (long)P * C;
+        ad.rows = R;
+        ad.heads = heads;
+        ad.d = dh;
+        ad.Lq = P;
+        ad.Lk = P;
+        attn(ad);
+      }
+      bf16* h2 = buf(T * C);
+      linear(o, T, C, k.wo, C, k.bo, h2, C, h);
+      ln(h2, n, T, C, k.l2g, k.l2b);
+      bf16* q2 = buf(T * C);
+      linear(n, T, C, k.wq2, C, nullptr, q2, C);
+      AttnDesc cd{};
+      cd.Q = q2;
+      cd.ldq = C;
+      cd.q_bstride = (long)P * C;
+      cd.K = e->kv_cache + k.koff;
+      cd.V = e->kv_cache + k.voff;
+      cd.ldk = e->U.kv_width;
+      cd.kv_bstride = e->slot_elems;
+      cd.kv_index = kv_index;
+      cd.O = o;
+      cd.ldo = C;
+      cd.o_bstride = (long)P * C;
+      cd.rows = R;
+      cd.heads = heads;
+      cd.d = dh;
+      cd.Lq = P;
+      cd.Lk = e->uc.ctx_len;
+      attn(cd);
+      bf16* h3 = buf(T * C);
+      linear(o, T, C, k.wo2, C, k.bo2, h3, C, h2);
+      ln(h3, n, T, C, k.l3g, k.l3b);
+      bf16* gg = buf(T * 4 * C);
+      linear(n, T, C, k.wff1, 8 * C, k.bff1, gg, 4 * C, nullptr, ACT_GEGLU);
+      linear(gg, T, 4 * C, k.wff2, C, k.bff2, hb, C, h3);  // block output → hb
+      e->ws.reset(mb);
+      std::swap(h, hb);
     }
-    bf16* h2 = buf(T * C);
-    linear(o, T, C, t.wo, C, t.bo, h2, C, h);
-    ln(h2, n, T, C, t.l2g, t.l2b);
-    bf16* q2 = buf(T * C);
-    linear(n, T, C, t.wq2, C, nullptr, q2, C);
-    AttnDesc cd{};
-    cd.Q = q2;
-    cd.ldq = C;
-    cd.q_bstride = (long)P * C;
-    cd.K = e->kv_cache + t.koff;
-    cd.V = e->kv_cache + t.voff;
-    cd.ldk = e->U.kv_width;
-    cd.kv_bstride = e->slot_elems;
-    cd.kv_index = kv_index;
-    cd.O = o;
-    cd.ldo = C;
-    cd.o_bstride = (long)P * C;
-    cd.rows = R;
-    cd.heads = heads;
-    cd.d = dh;
-    cd.Lq = P;
-    cd.Lk = e->uc.ctx_len;
-    attn(cd);
-    bf16* h3 = buf(T * C);
-    linear(o, T, C, t.wo2, C, t.bo2, h3, C, h2);
-    ln(h3, n, T, C, t.l3g, t.l3b);
-    bf16* gg = buf(T * 4 * C);
-    linear(n, T, C, t.wff1, 8 * C, t.bff1, gg, 4 * C, nullptr, ACT_GEGLU);
-    bf16* h4 = buf(T * C);
-    linear(gg, T, 4 * C, t.wff2, C, t.bff2, h4, C, h3);
-    linear(h4, T, C, t.wpout, C, t.bpout, out, C, x);  // 3 LN + 2 attention
+    linear(h, T, C, t.wpout, C, t.bpout, out, C, x);  // proj_out + the transformer's input
     e->ws.reset(mk);
     return out;
   }
@@ -613,7 +710,31 @@ static void unet_forward(Engine* e, cudaStream_t st, int R, int H, int W, const 
   bf16* t1 = f.buf((long)R * T);
   f.linear(sinus, R, C0, U.lin1_w, T, U.lin1_b, t1, T, nullptr, ACT_SILU);
   bf16* t2 = f.buf((long)R * T);
-  f.linear(t1, R, T, U.lin2_w, T, U.lin2_b, t2, T, nullptr, ACT_SILU);
+  if (c.add_time_dim) {
+    // SDXL: temb = linear_2(·) + aug[slot(row)] (the prompt's cached added embedding), then SiLU
+    float* aug_rows = e->ws.get<float>((size_t)R * T);
+    gather_rows_f32(e->aug_cache, kv_index, R, T, aug_rows, st);
+    GemmDesc d;
+    d.A = t1;
+    d.M = R;
+    d.K = T;
+    d.lda = T;
+    d.Bw[0] = U.lin2_w;
+    d.N = T;
+    d.ldb = T;
+    d.out = t2;
+    d.ldo = T;
+    d.bias = U.lin2_b;
+    d.temb = aug_rows;
+    d.ld_temb = T;
+    d.rows_per_img = 1;
+    d.act = ACT_SILU;
+    const int pi = e->prof.begin(PC_GEMM, st, 2.0 * R * T * T);
+    gemm(d, st);
+    e->prof.end(pi, st);
+  } else {
+    f.linear(t1, R, T, U.lin2_w, T, U.lin2_b, t2, T, nullptr, ACT_SILU);
+  }
   float* temb_all = e->ws.get<float>((size_t)R * U.temb_all_n);
   f.linear(t2, R, T, U.temb_all_w, U.temb_all_n, U.temb_all_b, temb_all, U.temb_all_n, nullptr, ACT_NONE, 1);
   f.temb_all = temb_all;

@@ -20,7 +20,14 @@ struct UNetCfg {
   int layers, groups, heads, ctx_dim, ctx_len;
   float eps_res = 1e-5f, eps_tf = 1e-6f, eps_ln = 1e-5f;
   int in_ch = 4;
+  // SDXL generalisations (oracle/configs.py UNetConfig): transformer depth per level (empty → 1),
+  // mid depth, head-dim heads (0 → `heads`), "text_time" added embedding dims (0 → none)
+  std::vector<int> depth;
+  int mid_depth = 1, head_dim = 0, add_time_dim = 0, pooled_dim = 0;
   int temb_dim() const { return 4 * block_out[0]; }
+  int depth_at(int level) const { return attn[level] ? (depth.empty() ? 1 : depth[level]) : 0; }
+  int heads_at(int C) const { return head_dim ? C / head_dim : heads; }
+  int add_in() const { return 6 * add_time_dim + pooled_dim; }
 };
 struct VAECfg {
   std::vector<int> block_out;
@@ -49,11 +56,16 @@ struct ResW {
   float *n1g, *n1b, *b1, *n2g, *n2b, *b2, *bsc = nullptr;
   bf16 *w1, *w2, *wsc = nullptr;
 };
-struct TfW {
-  int C;
-  float *gng, *gnb, *bpin, *l1g, *l1b, *bo, *l2g, *l2b, *bo2, *l3g, *l3b, *bff1, *bff2, *bpout;
-  bf16 *wpin, *wqkv, *wo, *wq2, *wo2, *wff1, *wff2, *wpout;
+struct BlkW {  // one BasicTransformerBlock
+  float *l1g, *l1b, *bo, *l2g, *l2b, *bo2, *l3g, *l3b, *bff1, *bff2;
+  bf16 *wqkv, *wo, *wq2, *wo2, *wff1, *wff2;
   int koff, voff;  // column offsets of this block's K / V in the text K/V cache rows
+};
+struct TfW {  // one Transformer2DModel: GN → proj_in → blocks → proj_out (+ x)
+  int C;
+  float *gng, *gnb, *bpin, *bpout;
+  bf16 *wpin, *wpout;
+  std::vector<BlkW> blk;
 };
 struct DownW {
   std::vector<ResW> res;
@@ -83,8 +95,11 @@ struct UNetW {
   std::vector<UpW> up;
   float *nout_g, *nout_b, *conv_out_b;
   bf16* conv_out_w;
-  bf16* kv_all_w;   // [kv_width][ctx_dim]: for each transformer (forward order) K_j then V_j
+  bf16* kv_all_w;   // [kv_width][ctx_dim]: for each transformer block (forward order) K_j then V_j
   int kv_width = 0;
+  // SDXL added embedding: Linear(add_in → T) → SiLU → Linear(T → T); per prompt slot, cached
+  bf16 *add1_w = nullptr, *add2_w = nullptr;
+  float *add1_b = nullptr, *add2_b = nullptr;
 };
 struct VAEW {
   float *pq_b, *cin_b;
@@ -146,6 +161,7 @@ struct Engine {
   VAEW V{};
   // text K/V cache
   bf16* kv_cache = nullptr;
+  float* aug_cache = nullptr;  // SDXL: [max_slots][T] added embedding per prompt slot (fp32)
   int max_slots = 0;
   long slot_elems = 0;
   std::vector<int> slot_used;
@@ -183,7 +199,8 @@ struct Engine {
 
 void build_engine(Engine* e);
 void step_batch(Engine* e, const sd_batch* b, cudaStream_t st);
-int ctx_register(Engine* e, const float* emb, int len, int dim, int slot, cudaStream_t st);
+int ctx_register(Engine* e, const float* emb, int len, int dim, const float* pooled, int pooled_dim, int slot,
+                 cudaStream_t st);
 void vae_decode_chunk(Engine* e, const float* z, int h, int w, int n_chunks, int chunk, DecodeState** state,
                       float* image, cudaStream_t st);
 void destroy_decode(Engine* e, DecodeState* d);

@@ -65,6 +65,7 @@ void upsample2x(const bf16* x, bf16* y, int B, int H, int W, int C, cudaStream_t
 void im2col_s2(const bf16* x, bf16* y, int B, int H, int W, int C, cudaStream_t st);  // 3x3 stride 2 pad 1
 void concat_channels(const bf16* a, int ca, const bf16* b, int cb, bf16* y, long P, cudaStream_t st);
 void f32_to_bf16(const float* x, bf16* y, long n, cudaStream_t st);
+void gather_rows_f32(const float* src, const int* idx, int rows, int n, float* dst, cudaStream_t st);
 // VAE head input: z fp32 [4][h][w] → bf16 NHWC [h][w][cpad] of z·scale (zeros in channels ≥ 4)
 void latent_to_nhwc(const float* z, int hw, float scale, int cpad, bf16* out, cudaStream_t st);
 // image NHWC fp32 [P][ld] (first 3 channels) → NCHW fp32 [3][P]

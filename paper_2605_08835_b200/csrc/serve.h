@@ -19,6 +19,7 @@ struct STask {
   float g = 7.5f;
   uint64_t noise_seed = 0;
   std::vector<float> emb;
+  std::vector<float> pooled;  // SDXL added conditioning (empty otherwise)
   int emb_len = 0, emb_dim = 0;
   int s = 0;
   int64_t U = -1, V = -1;

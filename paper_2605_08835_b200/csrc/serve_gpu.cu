@@ -95,10 +95,13 @@ void GpuExec::admit(STask* t) {
   for (int i = 0; i < 4 * hw; ++i) S->pinned_noise[i] *= sig;
   SD_CUDA(cudaMemcpyAsync(t->lat, S->pinned_noise, (size_t)4 * hw * 4, cudaMemcpyHostToDevice, S->hi));
   memcpy(S->pinned_emb, t->emb.data(), t->emb.size() * 4);
+  if (!t->pooled.empty()) memcpy(S->pinned_emb + t->emb.size(), t->pooled.data(), t->pooled.size() * 4);
+  const size_t nf = t->emb.size() + t->pooled.size();
   float* emb_dev;
-  SD_CUDA(cudaMallocAsync(&emb_dev, t->emb.size() * 4, S->hi));
-  SD_CUDA(cudaMemcpyAsync(emb_dev, S->pinned_emb, t->emb.size() * 4, cudaMemcpyHostToDevice, S->hi));
-  t->slot = ctx_register(e, emb_dev, t->emb_len, t->emb_dim, -1, S->hi);
+  SD_CUDA(cudaMallocAsync(&emb_dev, nf * 4, S->hi));
+  SD_CUDA(cudaMemcpyAsync(emb_dev, S->pinned_emb, nf * 4, cudaMemcpyHostToDevice, S->hi));
+  t->slot = ctx_register(e, emb_dev, t->emb_len, t->emb_dim, t->pooled.empty() ? nullptr : emb_dev + t->emb.size(),
+                         (int)t->pooled.size(), -1, S->hi);
   SD_CUDA(cudaFreeAsync(emb_dev, S->hi));
   SD_CUDA(cudaStreamSynchronize(S->hi));  // pinned staging is reused by the next admission
 }
@@ -231,7 +234,7 @@ extern "C" sd_status sd_serve_start(sd_engine* e, const sd_serve_config* cfg) {
   SD_CUDA(cudaEventCreateWithFlags(&S->ev_lo, cudaEventDisableTiming));
   const size_t hw = (size_t)cfg->latent_hw * cfg->latent_hw;
   SD_CUDA(cudaMallocHost(&S->pinned_noise, 4 * hw * 4));
-  SD_CUDA(cudaMallocHost(&S->pinned_emb, (size_t)e->e.uc.ctx_len * e->e.uc.ctx_dim * 4));
+  SD_CUDA(cudaMallocHost(&S->pinned_emb, ((size_t)e->e.uc.ctx_len * e->e.uc.ctx_dim + e->e.uc.pooled_dim) * 4));
   S->t0 = std::chrono::steady_clock::now();
   e->e.server = S;
   S->th = std::thread([S] { S->run(); });
@@ -243,6 +246,9 @@ extern "C" sd_status sd_submit(sd_engine* e, const sd_request* r) {
   SD_REQUIRE(r->n_steps >= 1 && r->n_steps <= 1000 && r->arrival_us >= 0, "sd_submit: bad request");
   SD_REQUIRE(r->text_emb_host && r->emb_len == e->e.uc.ctx_len && r->emb_dim == e->e.uc.ctx_dim,
              "sd_submit: embedding shape");
+  SD_REQUIRE(e->e.uc.add_time_dim == 0 ? (r->pooled_dim == 0)
+                                        : (r->pooled_host && r->pooled_dim == e->e.uc.pooled_dim),
+             "sd_submit: pooled embedding (required for SDXL, absent otherwise)");
   Server* S = server_of(e);
   if (e->e.failed) {
     set_error("engine FAILED: " + S->error);
@@ -257,6 +263,7 @@ extern "C" sd_status sd_submit(sd_engine* e, const sd_request* r) {
   t->emb.assign(r->text_emb_host, r->text_emb_host + (size_t)r->emb_len * r->emb_dim);
   t->emb_len = r->emb_len;
   t->emb_dim = r->emb_dim;
+  if (r->pooled_dim) t->pooled.assign(r->pooled_host, r->pooled_host + r->pooled_dim);
   std::lock_guard<std::mutex> g(S->mu);
   if (S->owned.count(r->id)) {
     delete t;

@@ -20,10 +20,12 @@ def _stream(s):
 class Engine:
     def __init__(self, model="tiny", sampler="ddim", max_latent_hw=None, b_max=8, c_max=16, weight_seed=0,
                  device=0):
-        m = {"tiny": B.SD_MODEL_TINY, "sd15": B.SD_MODEL_SD15}[model]
+        m = {"tiny": B.SD_MODEL_TINY, "sd15": B.SD_MODEL_SD15, "sdxl": B.SD_MODEL_SDXL,
+             "tinyxl": B.SD_MODEL_TINY_XL}[model]
         sm = {"ddim": B.SD_SAMPLER_DDIM, "euler": B.SD_SAMPLER_EULER}[sampler]
+        tiny = model in ("tiny", "tinyxl")
         if max_latent_hw is None:
-            max_latent_hw = 8 if model == "tiny" else 64
+            max_latent_hw = 8 if tiny else (128 if model == "sdxl" else 64)
         cfg = B.EngineConfig(m, 0, sm, max_latent_hw, b_max, c_max, weight_seed)
         h = C.c_void_p()
         B.call("sd_engine_create", C.byref(cfg), device, C.byref(h))
@@ -31,8 +33,9 @@ class Engine:
         self.model = model
         self.sampler = sampler
         self.device = device
-        self.ctx_len, self.ctx_dim = (8, 32) if model == "tiny" else (77, 768)
-        self.upscale = 2 if model == "tiny" else 8      # VAE decoder: 2^(levels-1)
+        self.ctx_len, self.ctx_dim, self.pooled_dim = {"tiny": (8, 32, 0), "sd15": (77, 768, 0),
+                                                       "sdxl": (77, 2048, 1280), "tinyxl": (8, 48, 40)}[model]
+        self.upscale = 2 if tiny else 8      # VAE decoder: 2^(levels-1)
 
     def close(self):
         if self.h:
@@ -59,15 +62,28 @@ class Engine:
         B.call("sd_engine_profile_read", self.h, cls, C.byref(ms), C.byref(n), C.byref(w))
         return ms.value, n.value, w.value
 
-    def set_uncond(self, emb: torch.Tensor, stream=None):
-        emb = emb.to(device=f"cuda:{self.device}", dtype=torch.float32).contiguous()
-        B.call("sd_ctx_set_uncond", self.h, B._p(emb), emb.shape[0], emb.shape[1], _stream(stream))
+    def _dev(self, t):
+        return t.to(device=f"cuda:{self.device}", dtype=torch.float32).contiguous()
+
+    def set_uncond(self, emb: torch.Tensor, pooled: torch.Tensor = None, stream=None):
+        emb = self._dev(emb)
+        if self.pooled_dim:
+            pooled = self._dev(pooled)
+            B.call("sd_ctx_set_uncond_pooled", self.h, B._p(emb), emb.shape[0], emb.shape[1], B._p(pooled),
+                   pooled.numel(), _stream(stream))
+        else:
+            B.call("sd_ctx_set_uncond", self.h, B._p(emb), emb.shape[0], emb.shape[1], _stream(stream))
         torch.cuda.current_stream().synchronize() if stream is None else stream.synchronize()
 
-    def register(self, emb: torch.Tensor, stream=None) -> int:
-        emb = emb.to(device=f"cuda:{self.device}", dtype=torch.float32).contiguous()
+    def register(self, emb: torch.Tensor, pooled: torch.Tensor = None, stream=None) -> int:
+        emb = self._dev(emb)
         slot = C.c_int32()
-        B.call("sd_ctx_register", self.h, B._p(emb), emb.shape[0], emb.shape[1], C.byref(slot), _stream(stream))
+        if self.pooled_dim:
+            pooled = self._dev(pooled)
+            B.call("sd_ctx_register_pooled", self.h, B._p(emb), emb.shape[0], emb.shape[1], B._p(pooled),
+                   pooled.numel(), C.byref(slot), _stream(stream))
+        else:
+            B.call("sd_ctx_register", self.h, B._p(emb), emb.shape[0], emb.shape[1], C.byref(slot), _stream(stream))
         (torch.cuda.current_stream() if stream is None else stream).synchronize()
         return slot.value
 

@@ -251,3 +251,76 @@ def test_sd15_768_step_and_vae_parity():
         eng.release(slot)
     finally:
         eng.close()
+
+
+def _xl_step_check(eng, cfg, P, lat_hw, reqs_spec, seed):
+    """One ragged step of an SDXL-shaped engine vs the oracle: reqs_spec = [(step, has_uncond, g)];
+    ε-part at TOL·κ, x at TOL."""
+    n = len(reqs_spec)
+    ctx_u = synth.uncond_embedding(0, cfg.ctx_len, cfg.ctx_dim)
+    pu = synth.uncond_pooled(0, cfg.pooled_dim)
+    eng.set_uncond(torch.from_numpy(ctx_u), torch.from_numpy(pu))
+    ctx = [synth.text_embedding(seed, i, cfg.ctx_len, cfg.ctx_dim) for i in range(n)]
+    pooled = [synth.pooled_embedding(seed, i, cfg.pooled_dim) for i in range(n)]
+    slots = [eng.register(torch.from_numpy(c), torch.from_numpy(p)) for c, p in zip(ctx, pooled)]
+    x0 = [synth.initial_noise(seed, i, lat_hw, lat_hw) for i in range(n)]
+    lat = [torch.from_numpy(x).cuda() for x in x0]
+    steps = [r[0] for r in reqs_spec]
+    hu = [r[1] for r in reqs_spec]
+    g = [r[2] for r in reqs_spec]
+    eng.step(lat, steps, [50] * n, hu, g, slots)
+    torch.cuda.synchronize()
+    cb = [synth.bf16_round(c) for c in ctx]
+    cub = synth.bf16_round(ctx_u)
+    worst = 0.0
+    for i in range(n):
+        t = int(sampling.timesteps(50)[steps[i]])
+        rx = np.stack([x0[i], x0[i]])
+        eps = unet.forward(P, cfg, rx, np.array([t, t]), np.stack([cb[i], cub]), np.stack([pooled[i], pu]))
+        ec, eu = eps[0], eps[1]
+        et = sampling.cfg_combine(ec, eu if hu[i] else None, g[i], bool(hu[i]))
+        exp = sampling.ddim_step(x0[i], et, 50, steps[i])
+        kappa = ((abs(1 - g[i]) * np.linalg.norm(eu) + g[i] * np.linalg.norm(ec)) / np.linalg.norm(et)) if hu[i] else 1.0
+        a, ap = sampling.ddim_alphas(50, steps[i])
+        A = np.sqrt(ap / a)
+        got = lat[i].cpu().numpy()
+        r_x, r_eps = rel(got, exp), rel(got - A * x0[i], exp - A * x0[i])
+        print(f"{cfg.name} {lat_hw}² req {i} (step {steps[i]}, cfg {hu[i]}): x {r_x:.3e}, eps-part {r_eps:.3e}, "
+              f"kappa {kappa:.2f}")
+        worst = max(worst, r_x / TOL, r_eps / (TOL * kappa))
+    for s in slots:
+        eng.release(s)
+    return worst
+
+
+def test_tinyxl_step_parity():
+    """SDXL code paths at tiny size: no attention at level 0, depth-2 transformers, head-dim heads,
+    linear projections, the added (pooled ‖ time ids) embedding per prompt slot."""
+    eng = Engine("tinyxl", max_latent_hw=16, b_max=4)
+    try:
+        P = configs.unet_params(configs.TINY_XL_UNET, 0, np.float32, bf16_weights=True)
+        worst = _xl_step_check(eng, configs.TINY_XL_UNET, P, 16, [(3, 1, 7.5), (30, 0, 7.5), (44, 1, 3.0)], 11)
+        assert worst <= 1.0
+    finally:
+        eng.close()
+
+
+def test_sdxl_step_and_vae_parity():
+    """SDXL-base shapes (2.57 B parameters) at latent 64×64: self-attention on the tcgen05 path at
+    d = 64 (1024 / 256 tokens), cross-attention to 77×2048 text, the 10-block transformers; then the
+    SDXL VAE (scaling factor 0.13025) at latent 32×32."""
+    eng = Engine("sdxl", max_latent_hw=64, b_max=2)
+    try:
+        P = configs.unet_params(configs.SDXL_UNET, 0, np.float32, bf16_weights=True)
+        worst = _xl_step_check(eng, configs.SDXL_UNET, P, 64, [(12, 1, 7.5), (40, 0, 5.0)], 13)
+        assert worst <= 1.0
+        V = configs.vae_params(configs.SDXL_VAE, 0, np.float32, bf16_weights=True)
+        z = synth.initial_noise(8, 0, 32, 32)
+        ref = vae.decode(V, configs.SDXL_VAE, z[None])[0]
+        img = eng.decode(torch.from_numpy(z).cuda(), 1)
+        torch.cuda.synchronize()
+        r = rel(img.cpu().numpy(), ref)
+        print(f"sdxl VAE 256² rel-L2 {r:.3e}")
+        assert r <= TOL
+    finally:
+        eng.close()
