@@ -43,7 +43,11 @@ enum {
 /* R1: diffusers SD-1.5 / SDXL-base shapes (oracle/configs.py); tiny = CFG#1; tiny-XL = the SDXL code
  * paths (no attention at level 0, depth-2 transformers, head-dim heads, added embedding) at tiny size */
 enum { SD_MODEL_TINY = 0, SD_MODEL_SD15 = 1, SD_MODEL_SDXL = 2, SD_MODEL_TINY_XL = 3 };
-enum { SD_PREC_BF16 = 0 };                               /* bf16 storage, fp32 accumulate (R19)       */
+/* R19: SD_PREC_BF16 = the product path (bf16 weights / activations, fp32 accumulation and statistics,
+ * tcgen05 tensor cores). SD_PREC_FP32 = the parity mode of SURVEY §8(c) ("fp32 mode: everything fp32",
+ * rel-L2 ≤ 1e-4 vs the oracle): fp32 weights and activations, SIMT FP32 kernels (no tensor cores, no
+ * split-K), same graph, same chunking; ~2x the weight memory. */
+enum { SD_PREC_BF16 = 0, SD_PREC_FP32 = 1 };
 enum { SD_SAMPLER_DDIM = 0, SD_SAMPLER_EULER = 1 };      /* R4 / R5                                  */
 
 typedef struct sd_engine sd_engine;
@@ -58,7 +62,7 @@ typedef struct sd_controller sd_controller;
  * synth/__init__.py documents the generator). */
 typedef struct {
   int32_t model;          /* SD_MODEL_* (SDXL: ~5.6 GB of bf16 weights)         */
-  int32_t precision;      /* SD_PREC_BF16                                      */
+  int32_t precision;      /* SD_PREC_BF16 | SD_PREC_FP32 (parity mode)         */
   int32_t sampler;        /* SD_SAMPLER_*                                      */
   int32_t max_latent_hw;  /* e.g. 64 for 512x512 images                        */
   int32_t b_max;          /* max requests per UNet call (paper: BS = 8) */

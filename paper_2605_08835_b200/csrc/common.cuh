@@ -206,6 +206,31 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// activation element type T ∈ {bf16 (product path), float (fp32 parity mode, R19)}: scalar and
+// 8-element (16 / 32-byte) vector conversions
+__device__ __forceinline__ float act_ld(const bf16* p) { return __bfloat162float(*p); }
+__device__ __forceinline__ float act_ld(const float* p) { return *p; }
+__device__ __forceinline__ void act_st(bf16* p, float v) { *p = __float2bfloat16(v); }
+__device__ __forceinline__ void act_st(float* p, float v) { *p = v; }
+__device__ __forceinline__ void load8(const bf16* p, float (&f)[8]) {
+  const uint4 u = *reinterpret_cast<const uint4*>(p);
+  const bf16* e = reinterpret_cast<const bf16*>(&u);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) f[i] = __bfloat162float(e[i]);
+}
+__device__ __forceinline__ void load8(const float* p, float (&f)[8]) {
+  const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+  f[0] = a.x, f[1] = a.y, f[2] = a.z, f[3] = a.w, f[4] = b.x, f[5] = b.y, f[6] = b.z, f[7] = b.w;
+}
+__device__ __forceinline__ void store8(bf16* p, const float (&o)[8]) {
+  *reinterpret_cast<uint4*>(p) =
+      make_uint4(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]), pack_bf16(o[4], o[5]), pack_bf16(o[6], o[7]));
+}
+__device__ __forceinline__ void store8(float* p, const float (&o)[8]) {
+  reinterpret_cast<float4*>(p)[0] = make_float4(o[0], o[1], o[2], o[3]);
+  reinterpret_cast<float4*>(p)[1] = make_float4(o[4], o[5], o[6], o[7]);
+}
+
 #endif  // __CUDACC__
 
 }  // namespace sd

@@ -6,26 +6,29 @@
 
 namespace sd {
 
-// K11: UNet input rows. Row ρ belongs to request r = row_req[ρ]; writes bf16(c_in_r · x_r) NHWC
+// K11: UNet input rows. Row ρ belongs to request r = row_req[ρ]; writes T(c_in_r · x_r) NHWC
 // with channels [4, cpad) zero.  (R26 row order is encoded in row_req.)
-__global__ void gather_rows_kernel(RowMap m, int rows, int hw, int cpad, bf16* __restrict__ out) {
+// T = bf16 on the product path, float in the fp32 parity mode (R19); likewise below.
+template <class T>
+__global__ void gather_rows_kernel(RowMap m, int rows, int hw, int cpad, T* __restrict__ out) {
   const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;  // one pixel of one row
   if (i >= (long)rows * hw) return;
   const int rho = (int)(i / hw), p = (int)(i % hw);
   const int r = m.row_req[rho];
   const float* x = m.latents[r];
   const float c = m.c_in[r];
-  bf16* o = out + i * cpad;
-  o[0] = __float2bfloat16(c * x[p]);
-  o[1] = __float2bfloat16(c * x[hw + p]);
-  o[2] = __float2bfloat16(c * x[2 * hw + p]);
-  o[3] = __float2bfloat16(c * x[3 * hw + p]);
-  for (int k = 4; k < cpad; ++k) o[k] = __float2bfloat16(0.f);
+  T* o = out + i * cpad;
+  act_st(o + 0, c * x[p]);
+  act_st(o + 1, c * x[hw + p]);
+  act_st(o + 2, c * x[2 * hw + p]);
+  act_st(o + 3, c * x[3 * hw + p]);
+  for (int k = 4; k < cpad; ++k) act_st(o + k, 0.f);
 }
 
-void gather_rows(const RowMap& m, int rows, int hw, int cpad, bf16* out, cudaStream_t st) {
+template <class T>
+void gather_rows(const RowMap& m, int rows, int hw, int cpad, T* out, cudaStream_t st) {
   const long n = (long)rows * hw;
-  gather_rows_kernel<<<cdiv(n, 256), 256, 0, st>>>(m, rows, hw, cpad, out);
+  gather_rows_kernel<T><<<cdiv(n, 256), 256, 0, st>>>(m, rows, hw, cpad, out);
   SD_CHECK_LAUNCH();
 }
 
@@ -59,24 +62,26 @@ void combine_update(const RowMap& m, int n_req, int hw, const float* eps, int ld
   SD_CHECK_LAUNCH();
 }
 
-// K10 front: [cos(t·f_k) ‖ sin(t·f_k)], f_k = exp(−ln(10⁴)·k/half) (flip_sin_to_cos, R27), bf16.
-__global__ void sinusoid_kernel(const float* __restrict__ t, int rows, int dim, bf16* __restrict__ out) {
+// K10 front: [cos(t·f_k) ‖ sin(t·f_k)], f_k = exp(−ln(10⁴)·k/half) (flip_sin_to_cos, R27).
+template <class T>
+__global__ void sinusoid_kernel(const float* __restrict__ t, int rows, int dim, T* __restrict__ out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int half = dim / 2;
   if (i >= rows * half) return;
   const int r = i / half, k = i % half;
   const float f = expf(-9.210340371976184f * (float)k / (float)half);
   const float arg = t[r] * f;
-  out[(long)r * dim + k] = __float2bfloat16(cosf(arg));
-  out[(long)r * dim + half + k] = __float2bfloat16(sinf(arg));
+  act_st(out + (long)r * dim + k, cosf(arg));
+  act_st(out + (long)r * dim + half + k, sinf(arg));
 }
 
-void timestep_sinusoid(const float* t_row, int rows, int dim, bf16* out, cudaStream_t st) {
-  sinusoid_kernel<<<cdiv(rows * dim / 2, 256), 256, 0, st>>>(t_row, rows, dim, out);
+template <class T>
+void timestep_sinusoid(const float* t_row, int rows, int dim, T* out, cudaStream_t st) {
+  sinusoid_kernel<T><<<cdiv(rows * dim / 2, 256), 256, 0, st>>>(t_row, rows, dim, out);
   SD_CHECK_LAUNCH();
 }
 
-// nearest 2× upsample, NHWC bf16, 16-byte vectors
+// nearest 2× upsample, NHWC, 16-byte vectors
 __global__ void upsample2x_kernel(const uint4* __restrict__ x, uint4* __restrict__ y, int B, int H, int W, int V) {
   const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
   const long n = (long)B * 2 * H * 2 * W * V;
@@ -90,8 +95,9 @@ __global__ void upsample2x_kernel(const uint4* __restrict__ x, uint4* __restrict
   y[i] = x[(((long)b * H + yo / 2) * W + xo / 2) * V + v];
 }
 
-void upsample2x(const bf16* x, bf16* y, int B, int H, int W, int C, cudaStream_t st) {
-  const int V = C / 8;
+template <class T>
+void upsample2x(const T* x, T* y, int B, int H, int W, int C, cudaStream_t st) {
+  const int V = C * (int)sizeof(T) / 16;
   const long n = (long)B * 4 * H * W * V;
   upsample2x_kernel<<<cdiv(n, 256), 256, 0, st>>>(reinterpret_cast<const uint4*>(x), reinterpret_cast<uint4*>(y), B,
                                                   H, W, V);
@@ -118,8 +124,9 @@ __global__ void im2col_s2_kernel(const uint4* __restrict__ x, uint4* __restrict_
   y[i] = val;
 }
 
-void im2col_s2(const bf16* x, bf16* y, int B, int H, int W, int C, cudaStream_t st) {
-  const int V = C / 8;
+template <class T>
+void im2col_s2(const T* x, T* y, int B, int H, int W, int C, cudaStream_t st) {
+  const int V = C * (int)sizeof(T) / 16;
   const long n = (long)B * ((H + 1) / 2) * ((W + 1) / 2) * 9 * V;
   im2col_s2_kernel<<<cdiv(n, 256), 256, 0, st>>>(reinterpret_cast<const uint4*>(x), reinterpret_cast<uint4*>(y), B,
                                                  H, W, V);
@@ -136,10 +143,13 @@ __global__ void concat_kernel(const uint4* __restrict__ a, int va, const uint4* 
   y[i] = v < va ? a[p * va + v] : b[p * vb + (v - va)];
 }
 
-void concat_channels(const bf16* a, int ca, const bf16* b, int cb, bf16* y, long P, cudaStream_t st) {
-  const long n = P * (ca + cb) / 8;
-  concat_kernel<<<cdiv(n, 256), 256, 0, st>>>(reinterpret_cast<const uint4*>(a), ca / 8,
-                                              reinterpret_cast<const uint4*>(b), cb / 8, reinterpret_cast<uint4*>(y), P);
+template <class T>
+void concat_channels(const T* a, int ca, const T* b, int cb, T* y, long P, cudaStream_t st) {
+  const int per = 16 / (int)sizeof(T);  // elements per 16-byte vector
+  const long n = P * (ca + cb) / per;
+  concat_kernel<<<cdiv(n, 256), 256, 0, st>>>(reinterpret_cast<const uint4*>(a), ca / per,
+                                              reinterpret_cast<const uint4*>(b), cb / per, reinterpret_cast<uint4*>(y),
+                                              P);
   SD_CHECK_LAUNCH();
 }
 
@@ -151,6 +161,10 @@ __global__ void f32_to_bf16_kernel(const float* __restrict__ x, bf16* __restrict
 void f32_to_bf16(const float* x, bf16* y, long n, cudaStream_t st) {
   f32_to_bf16_kernel<<<cdiv(n, 256), 256, 0, st>>>(x, y, n);
   SD_CHECK_LAUNCH();
+}
+
+void f32_to_act(const float* x, float* y, long n, cudaStream_t st) {
+  SD_CUDA(cudaMemcpyAsync(y, x, (size_t)n * sizeof(float), cudaMemcpyDeviceToDevice, st));
 }
 
 // dst[r][0..n) = src[idx[r]][0..n) (fp32): the SDXL added embedding of each row's prompt slot
@@ -166,16 +180,17 @@ void gather_rows_f32(const float* src, const int* idx, int rows, int n, float* d
   SD_CHECK_LAUNCH();
 }
 
-__global__ void latent_to_nhwc_kernel(const float* __restrict__ z, int hw, float scale, int cpad,
-                                      bf16* __restrict__ out) {
+template <class T>
+__global__ void latent_to_nhwc_kernel(const float* __restrict__ z, int hw, float scale, int cpad, T* __restrict__ out) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= hw) return;
-  bf16* o = out + (long)p * cpad;
-  for (int c = 0; c < cpad; ++c) o[c] = __float2bfloat16(c < 4 ? z[(long)c * hw + p] * scale : 0.f);
+  T* o = out + (long)p * cpad;
+  for (int c = 0; c < cpad; ++c) act_st(o + c, c < 4 ? z[(long)c * hw + p] * scale : 0.f);
 }
 
-void latent_to_nhwc(const float* z, int hw, float scale, int cpad, bf16* out, cudaStream_t st) {
-  latent_to_nhwc_kernel<<<cdiv(hw, 256), 256, 0, st>>>(z, hw, scale, cpad, out);
+template <class T>
+void latent_to_nhwc(const float* z, int hw, float scale, int cpad, T* out, cudaStream_t st) {
+  latent_to_nhwc_kernel<T><<<cdiv(hw, 256), 256, 0, st>>>(z, hw, scale, cpad, out);
   SD_CHECK_LAUNCH();
 }
 
@@ -190,5 +205,15 @@ void nhwc_to_nchw3(const float* x, int ld, long P, float* y, cudaStream_t st) {
   nhwc_to_nchw3_kernel<<<cdiv(P, 256), 256, 0, st>>>(x, ld, P, y);
   SD_CHECK_LAUNCH();
 }
+
+#define SD_EW_INST(T)                                                                              \
+  template void gather_rows<T>(const RowMap&, int, int, int, T*, cudaStream_t);                    \
+  template void timestep_sinusoid<T>(const float*, int, int, T*, cudaStream_t);                   \
+  template void upsample2x<T>(const T*, T*, int, int, int, int, cudaStream_t);                    \
+  template void im2col_s2<T>(const T*, T*, int, int, int, int, cudaStream_t);                     \
+  template void concat_channels<T>(const T*, int, const T*, int, T*, long, cudaStream_t);         \
+  template void latent_to_nhwc<T>(const float*, int, float, int, T*, cudaStream_t);
+SD_EW_INST(bf16)
+SD_EW_INST(float)
 
 }  // namespace sd

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <stdlib.h>
+#include <type_traits>
 
 #include <nvtx3/nvToolsExt.h>
 #include "engine.h"
@@ -121,6 +122,10 @@ struct Builder {
     T* p = e->warena.get<T>((size_t)n);
     return p;
   }
+  // weight matrices in the engine precision (bf16, or fp32 in the parity mode)
+  wptr walloc(long n) { return e->warena.alloc((size_t)n * e->esize); }
+  wptr woff(wptr base, long elems) const { return static_cast<char*>(base) + elems * (long)e->esize; }
+  bool wbf() const { return !e->f32; }
   // canonical tensor `name` of n elements → generated into dst (layout given)
   void gen(const std::string& name, long n, int kind, long fan_in, int layout, void* d0, void* d1, bool bf,
            int O = 0, int I = 0, int I1 = 0, int Ipad = 0, int F = 0) {
@@ -153,17 +158,17 @@ struct Builder {
     gen(p + ".bias", c, WK_BETA, 1, WL_PLAIN, *b, nullptr, false);
   }
   // conv3x3 [O][I][3][3] → [O][9][Ipad] bf16
-  bf16* conv3(const std::string& p, int O, int I, int Ipad, float** b) {
-    bf16* w = alloc<bf16>((long)O * 9 * Ipad);
-    if (Ipad != I) SD_CUDA(cudaMemsetAsync(w, 0, (size_t)O * 9 * Ipad * 2, st));
-    gen(p + ".weight", (long)O * I * 9, WK_UNIFORM, (long)I * 9, WL_CONV3, w, nullptr, true, O, I, I, Ipad);
+  wptr conv3(const std::string& p, int O, int I, int Ipad, float** b) {
+    wptr w = walloc((long)O * 9 * Ipad);
+    if (Ipad != I) SD_CUDA(cudaMemsetAsync(w, 0, (size_t)O * 9 * Ipad * e->esize, st));
+    gen(p + ".weight", (long)O * I * 9, WK_UNIFORM, (long)I * 9, WL_CONV3, w, nullptr, wbf(), O, I, I, Ipad);
     if (b) *b = bias(p + ".bias", O, (long)I * 9);
     return w;
   }
-  // linear / 1x1 conv [O][I] → bf16 (optionally into dst rows)
-  bf16* lin(const std::string& p, int O, int I, float** b, bf16* dst = nullptr, float* bdst = nullptr) {
-    bf16* w = dst ? dst : alloc<bf16>((long)O * I);
-    gen(p + ".weight", (long)O * I, WK_UNIFORM, I, WL_PLAIN, w, nullptr, true);
+  // linear / 1x1 conv [O][I] (optionally into dst rows)
+  wptr lin(const std::string& p, int O, int I, float** b, wptr dst = nullptr, float* bdst = nullptr) {
+    wptr w = dst ? dst : walloc((long)O * I);
+    gen(p + ".weight", (long)O * I, WK_UNIFORM, I, WL_PLAIN, w, nullptr, wbf());
     if (b) *b = bias(p + ".bias", O, I, bdst);
     return w;
   }
@@ -177,7 +182,7 @@ static void build_res(Builder& B, const std::string& p, int cin, int cout, int* 
   if (temb) {
     const int T = B.e->uc.temb_dim();
     r->temb_off = *temb_cursor;
-    B.lin(p + ".time_emb_proj", cout, T, nullptr, B.e->U.temb_all_w + (long)r->temb_off * T, nullptr);
+    B.lin(p + ".time_emb_proj", cout, T, nullptr, B.woff(B.e->U.temb_all_w, (long)r->temb_off * T), nullptr);
     B.bias(p + ".time_emb_proj.bias", cout, T, B.e->U.temb_all_b + r->temb_off);
     *temb_cursor += cout;
   }
@@ -196,23 +201,23 @@ static void build_tf(Builder& B, const std::string& p, int C, int depth, int* kv
     BlkW k{};
     const std::string b = p + ".transformer_blocks." + std::to_string(d);
     B.norm(b + ".norm1", C, &k.l1g, &k.l1b);
-    k.wqkv = B.alloc<bf16>(3L * C * C);
+    k.wqkv = B.walloc(3L * C * C);
     B.lin(b + ".attn1.to_q", C, C, nullptr, k.wqkv);
-    B.lin(b + ".attn1.to_k", C, C, nullptr, k.wqkv + (long)C * C);
-    B.lin(b + ".attn1.to_v", C, C, nullptr, k.wqkv + 2L * C * C);
+    B.lin(b + ".attn1.to_k", C, C, nullptr, B.woff(k.wqkv, (long)C * C));
+    B.lin(b + ".attn1.to_v", C, C, nullptr, B.woff(k.wqkv, 2L * C * C));
     k.wo = B.lin(b + ".attn1.to_out.0", C, C, &k.bo);
     B.norm(b + ".norm2", C, &k.l2g, &k.l2b);
     k.wq2 = B.lin(b + ".attn2.to_q", C, C, nullptr);
     k.koff = *kv_cursor;
-    B.lin(b + ".attn2.to_k", C, D, nullptr, e->U.kv_all_w + (long)k.koff * D);
+    B.lin(b + ".attn2.to_k", C, D, nullptr, B.woff(e->U.kv_all_w, (long)k.koff * D));
     k.voff = *kv_cursor + C;
-    B.lin(b + ".attn2.to_v", C, D, nullptr, e->U.kv_all_w + (long)k.voff * D);
+    B.lin(b + ".attn2.to_v", C, D, nullptr, B.woff(e->U.kv_all_w, (long)k.voff * D));
     *kv_cursor += 2 * C;
     k.wo2 = B.lin(b + ".attn2.to_out.0", C, C, &k.bo2);
     B.norm(b + ".norm3", C, &k.l3g, &k.l3b);
     // GEGLU proj [8C][C] with rows interleaved per 64 (value | gate) for the fused epilogue
-    k.wff1 = B.alloc<bf16>(8L * C * C);
-    B.gen(b + ".ff.net.0.proj.weight", 8L * C * C, WK_UNIFORM, C, WL_GEGLU, k.wff1, nullptr, true, 0, 0, 0, 0, 4 * C);
+    k.wff1 = B.walloc(8L * C * C);
+    B.gen(b + ".ff.net.0.proj.weight", 8L * C * C, WK_UNIFORM, C, WL_GEGLU, k.wff1, nullptr, B.wbf(), 0, 0, 0, 0, 4 * C);
     k.bff1 = B.alloc<float>(8L * C);
     B.gen(b + ".ff.net.0.proj.bias", 8L * C, WK_UNIFORM, C, WL_GEGLU, k.bff1, nullptr, false, 0, 0, 0, 0, 4 * C);
     k.wff2 = B.lin(b + ".ff.net.2", C, 4 * C, &k.bff2);
@@ -245,10 +250,10 @@ static void build_unet(Engine* e, cudaStream_t st) {
   }
   UNetW& U = e->U;
   U.temb_all_n = temb_total;
-  U.temb_all_w = B.alloc<bf16>((long)temb_total * T);
+  U.temb_all_w = B.walloc((long)temb_total * T);
   U.temb_all_b = B.alloc<float>(temb_total);
   U.kv_width = kv_total;
-  U.kv_all_w = B.alloc<bf16>((long)kv_total * c.ctx_dim);
+  U.kv_all_w = B.walloc((long)kv_total * c.ctx_dim);
   int tcur = 0, kcur = 0;
 
   // conv_in: input padded to 64 channels (zeros) so every TMA box is 128-byte aligned
@@ -324,9 +329,10 @@ static void build_vae(Engine* e, cudaStream_t st) {
   V.pq_w = B.lin("post_quant_conv", 4, 4, &V.pq_b);
   // pq is applied by a tiny dense GEMM on 64-channel-padded input: store [4][64]
   {
-    bf16* w64 = B.alloc<bf16>(16 * 64);  // N padded to 16 rows
-    SD_CUDA(cudaMemsetAsync(w64, 0, 16 * 64 * 2, st));
-    SD_CUDA(cudaMemcpy2DAsync(w64, 64 * 2, V.pq_w, 4 * 2, 4 * 2, 4, cudaMemcpyDeviceToDevice, st));
+    const size_t es = e->esize;
+    wptr w64 = B.walloc(16 * 64);  // N padded to 16 rows
+    SD_CUDA(cudaMemsetAsync(w64, 0, 16 * 64 * es, st));
+    SD_CUDA(cudaMemcpy2DAsync(w64, 64 * es, V.pq_w, 4 * es, 4 * es, 4, cudaMemcpyDeviceToDevice, st));
     V.pq_w = w64;
   }
   V.cin_w = B.conv3("decoder.conv_in", cm, 4, 64, &V.cin_b);
@@ -383,7 +389,7 @@ static size_t unet_ws_bytes(const Engine* e) {
   const long R = e->max_rows;
   const int c0 = e->uc.block_out[0];
   // ≈ 60 tensors of R·P·c0 at the top level dominate (level k has P/4^k pixels, ≤ 4·c0 channels)
-  const double top = (double)R * P * c0 * 2;
+  const double top = (double)R * P * c0 * e->esize;
   // + split-K partials of one ≤ 64-pixel conv (≤ 8 splits × R·64 rows × 2·c_max fp32)
   const double split = 8.0 * R * 64 * 2 * e->uc.block_out.back() * 4;
   return (size_t)(top * 140 + split) + ((size_t)512 << 20);
@@ -394,9 +400,12 @@ void build_engine(Engine* e) {
   e->uc = unet_cfg(e->cfg.model);
   e->vc = vae_cfg(e->cfg.model);
   e->max_rows = 2 * e->cfg.b_max;
-  const size_t wbytes = e->cfg.model == SD_MODEL_SD15   ? ((size_t)2200 << 20)
-                        : e->cfg.model == SD_MODEL_SDXL ? ((size_t)5600 << 20)
-                                                        : ((size_t)64 << 20);
+  e->f32 = e->cfg.precision == SD_PREC_FP32;
+  e->esize = e->f32 ? 4 : 2;
+  const size_t wbytes = (e->cfg.model == SD_MODEL_SD15   ? ((size_t)2200 << 20)
+                         : e->cfg.model == SD_MODEL_SDXL ? ((size_t)5600 << 20)
+                                                         : ((size_t)64 << 20)) *
+                        (e->f32 ? 2 : 1);
   e->warena.init(wbytes);
   cudaStream_t st;
   SD_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
@@ -408,8 +417,8 @@ void build_engine(Engine* e) {
   // text K/V cache slots (slot 0 = unconditional)
   e->max_slots = 4 * e->cfg.b_max + 8;
   e->slot_elems = (long)e->uc.ctx_len * e->U.kv_width;
-  SD_CUDA(cudaMalloc(&e->kv_cache, (size_t)e->max_slots * e->slot_elems * 2));
-  SD_CUDA(cudaMemset(e->kv_cache, 0, (size_t)e->max_slots * e->slot_elems * 2));
+  SD_CUDA(cudaMalloc(&e->kv_cache, (size_t)e->max_slots * e->slot_elems * e->esize));
+  SD_CUDA(cudaMemset(e->kv_cache, 0, (size_t)e->max_slots * e->slot_elems * e->esize));
   if (e->uc.add_time_dim) {
     SD_CUDA(cudaMalloc(&e->aug_cache, (size_t)e->max_slots * e->uc.temb_dim() * sizeof(float)));
     SD_CUDA(cudaMemset(e->aug_cache, 0, (size_t)e->max_slots * e->uc.temb_dim() * sizeof(float)));
@@ -427,7 +436,7 @@ void build_engine(Engine* e) {
   const char* ng = getenv("SD_NO_GRAPH");
   e->use_graphs = !(ng && ng[0] == '1');
   const char* at = getenv("SD_ATTN_TC");
-  e->use_attn_tc = !(at && at[0] == '0');
+  e->use_attn_tc = !(at && at[0] == '0') && !e->f32;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -435,24 +444,25 @@ void build_engine(Engine* e) {
 // ---------------------------------------------------------------------------------------------
 // SDXL "text_time" added embedding of one prompt (R27): [sinusoid_256(id_k) for the 6 time ids ‖
 // pooled] → Linear → SiLU → Linear, cached per slot in fp32 and added to linear_2's output per row
+template <class AT>
 static void added_embedding(Engine* e, const float* pooled, int slot, cudaStream_t st) {
   const UNetCfg& c = e->uc;
   const int T = c.temb_dim(), K = c.add_in(), td = c.add_time_dim;
   static const float ids[6] = {1024.f, 1024.f, 0.f, 0.f, 1024.f, 1024.f};  // R27
   float* ids_dev;
-  bf16 *row, *hid;
+  AT *row, *hid;
   SD_CUDA(cudaMallocAsync(&ids_dev, sizeof(ids), st));
-  SD_CUDA(cudaMallocAsync(&row, (size_t)K * 2, st));
-  SD_CUDA(cudaMallocAsync(&hid, (size_t)T * 2, st));
+  SD_CUDA(cudaMallocAsync(&row, (size_t)K * sizeof(AT), st));
+  SD_CUDA(cudaMallocAsync(&hid, (size_t)T * sizeof(AT), st));
   SD_CUDA(cudaMemcpyAsync(ids_dev, ids, sizeof(ids), cudaMemcpyHostToDevice, st));
   timestep_sinusoid(ids_dev, 6, td, row, st);      // [6][td] = one row of 6·td
-  f32_to_bf16(pooled, row + 6 * td, c.pooled_dim, st);
-  GemmDesc d;
+  f32_to_act(pooled, row + 6 * td, c.pooled_dim, st);
+  GemmDescT<AT> d;
   d.A = row;
   d.M = 1;
   d.K = K;
   d.lda = K;
-  d.Bw[0] = e->U.add1_w;
+  d.Bw[0] = wt<AT>(e->U.add1_w);
   d.N = T;
   d.ldb = K;
   d.out = hid;
@@ -460,12 +470,12 @@ static void added_embedding(Engine* e, const float* pooled, int slot, cudaStream
   d.bias = e->U.add1_b;
   d.act = ACT_SILU;
   gemm(d, st);
-  GemmDesc d2;
+  GemmDescT<AT> d2;
   d2.A = hid;
   d2.M = 1;
   d2.K = T;
   d2.lda = T;
-  d2.Bw[0] = e->U.add2_w;
+  d2.Bw[0] = wt<AT>(e->U.add2_w);
   d2.N = T;
   d2.ldb = T;
   d2.out = e->aug_cache + (long)slot * T;
@@ -476,6 +486,26 @@ static void added_embedding(Engine* e, const float* pooled, int slot, cudaStream
   SD_CUDA(cudaFreeAsync(hid, st));
   SD_CUDA(cudaFreeAsync(row, st));
   SD_CUDA(cudaFreeAsync(ids_dev, st));
+}
+
+template <class AT>
+static void ctx_kv(Engine* e, const float* emb, int len, int dim, const float* pooled, int slot, cudaStream_t st) {
+  AT* tmp;
+  SD_CUDA(cudaMallocAsync(&tmp, (size_t)len * dim * sizeof(AT), st));
+  f32_to_act(emb, tmp, (long)len * dim, st);
+  GemmDescT<AT> d;
+  d.A = tmp;
+  d.M = len;
+  d.K = dim;
+  d.lda = dim;
+  d.Bw[0] = wt<AT>(e->U.kv_all_w);
+  d.N = e->U.kv_width;
+  d.ldb = dim;
+  d.out = static_cast<AT*>(e->kv_cache) + (long)slot * e->slot_elems;
+  d.ldo = e->U.kv_width;
+  gemm(d, st);
+  SD_CUDA(cudaFreeAsync(tmp, st));
+  if (e->uc.add_time_dim) added_embedding<AT>(e, pooled, slot, st);
 }
 
 int ctx_register(Engine* e, const float* emb, int len, int dim, const float* pooled, int pooled_dim, int slot,
@@ -493,28 +523,17 @@ int ctx_register(Engine* e, const float* emb, int len, int dim, const float* poo
     if (slot < 0) throw std::runtime_error("no free ctx slot");
     e->slot_used[slot] = 1;
   }
-  bf16* tmp;
-  SD_CUDA(cudaMallocAsync(&tmp, (size_t)len * dim * 2, st));
-  f32_to_bf16(emb, tmp, (long)len * dim, st);
-  GemmDesc d;
-  d.A = tmp;
-  d.M = len;
-  d.K = dim;
-  d.lda = dim;
-  d.Bw[0] = e->U.kv_all_w;
-  d.N = e->U.kv_width;
-  d.ldb = dim;
-  d.out = e->kv_cache + (long)slot * e->slot_elems;
-  d.ldo = e->U.kv_width;
-  gemm(d, st);
-  SD_CUDA(cudaFreeAsync(tmp, st));
-  if (e->uc.add_time_dim) added_embedding(e, pooled, slot, st);
+  if (e->f32)
+    ctx_kv<float>(e, emb, len, dim, pooled, slot, st);
+  else
+    ctx_kv<bf16>(e, emb, len, dim, pooled, slot, st);
   return slot;
 }
 
 // ---------------------------------------------------------------------------------------------
 // UNet forward over `rows` rows at h×w (activations NHWC bf16)
 // ---------------------------------------------------------------------------------------------
+template <class AT>
 struct Fwd {
   Engine* e;
   cudaStream_t st;
@@ -523,26 +542,26 @@ struct Fwd {
   const int* kv_index;    // [R] ctx slot per row
   void* gn_ws;
 
-  bf16* buf(long elems) { return e->ws.get<bf16>((size_t)elems); }
+  AT* buf(long elems) { return e->ws.get<AT>((size_t)elems); }
 
-  void gn(const bf16* x, bf16* y, int P, int C, const float* g, const float* b, float eps, bool silu) {
+  void gn(const AT* x, AT* y, int P, int C, const float* g, const float* b, float eps, bool silu) {
     const int pi = e->prof.begin(PC_GN, st, 3.0 * R * P * C * 2);
     group_norm(x, y, R, P, C, e->uc.groups, g, b, eps, silu, gn_ws, st);
     e->prof.end(pi, st);
   }
-  void ln(const bf16* x, bf16* y, long T, int C, const float* g, const float* b) {
+  void ln(const AT* x, AT* y, long T, int C, const float* g, const float* b) {
     const int pi = e->prof.begin(PC_LN, st, 2.0 * T * C * 2);
     layer_norm(x, y, (int)T, C, g, b, e->uc.eps_ln, st);
     e->prof.end(pi, st);
   }
-  void attn(const AttnDesc& a) {
+  void attn(const AttnDescT<AT>& a) {
     const int pi = e->prof.begin(PC_ATTN, st, 4.0 * a.rows * a.heads * (double)a.Lq * a.Lk * a.d);
     attention(a, st);
     e->prof.end(pi, st);
   }
-  void linear(const bf16* A, long M, int K, const bf16* W, int N, const float* bias, void* out, int ldo,
-              const bf16* res = nullptr, int act = ACT_NONE, int out_f32 = 0) {
-    GemmDesc d;
+  void linear(const AT* A, long M, int K, const AT* W, int N, const float* bias, void* out, int ldo,
+              const AT* res = nullptr, int act = ACT_NONE, int out_f32 = 0) {
+    GemmDescT<AT> d;
     d.A = A;
     d.M = (int)M;
     d.K = K;
@@ -561,9 +580,9 @@ struct Fwd {
     gemm(d, st);
     e->prof.end(pi, st);
   }
-  void conv(const bf16* x, int H, int W, int C, const bf16* w, int N, const float* bias, void* out,
-            const float* temb = nullptr, const bf16* res = nullptr, int out_f32 = 0, int ldo = 0, int c_real = 0) {
-    GemmDesc d;
+  void conv(const AT* x, int H, int W, int C, const AT* w, int N, const float* bias, void* out,
+            const float* temb = nullptr, const AT* res = nullptr, int out_f32 = 0, int ldo = 0, int c_real = 0) {
+    GemmDescT<AT> d;
     d.mode = GEMM_CONV3;
     d.xs[0] = x;
     d.cs[0] = C;
@@ -589,58 +608,60 @@ struct Fwd {
     e->ws.reset(mk);
   }
 
-  bf16* resblock(const ResW& r, const bf16* x, int H, int W) {
+  AT* resblock(const ResW& r, const AT* x, int H, int W) {
     const int P = H * W;
     const size_t mk = e->ws.mark();
-    bf16* out = buf((long)R * P * r.cout);  // allocated below the scratch mark
+    AT* out = buf((long)R * P * r.cout);  // allocated below the scratch mark
     const size_t mk2 = e->ws.mark();
     (void)mk;
-    bf16* a = buf((long)R * P * r.cin);
+    AT* a = buf((long)R * P * r.cin);
     gn(x, a, P, r.cin, r.n1g, r.n1b, e->uc.eps_res, true);
-    bf16* h1 = buf((long)R * P * r.cout);
-    conv(a, H, W, r.cin, r.w1, r.cout, r.b1, h1, temb_all + r.temb_off);
-    bf16* a2 = buf((long)R * P * r.cout);
+    AT* h1 = buf((long)R * P * r.cout);
+    conv(a, H, W, r.cin, wt<AT>(r.w1), r.cout, r.b1, h1, temb_all + r.temb_off);
+    AT* a2 = buf((long)R * P * r.cout);
     gn(h1, a2, P, r.cout, r.n2g, r.n2b, e->uc.eps_res, true);
-    const bf16* sc = x;
+    const AT* sc = x;
     if (r.wsc) {
-      bf16* s = buf((long)R * P * r.cout);
-      linear(x, (long)R * P, r.cin, r.wsc, r.cout, r.bsc, s, r.cout);
+      AT* s = buf((long)R * P * r.cout);
+      linear(x, (long)R * P, r.cin, wt<AT>(r.wsc), r.cout, r.bsc, s, r.cout);
       sc = s;
     }
-    conv(a2, H, W, r.cout, r.w2, r.cout, r.b2, out, nullptr, sc);
+    conv(a2, H, W, r.cout, wt<AT>(r.w2), r.cout, r.b2, out, nullptr, sc);
     e->ws.reset(mk2);
     return out;
   }
 
-  bf16* transformer(const TfW& t, const bf16* x, int H, int W) {
+  AT* transformer(const TfW& t, const AT* x, int H, int W) {
     const int C = t.C, P = H * W;
     const long T = (long)R * P;
     const int heads = e->uc.heads_at(C), dh = C / heads;
-    bf16* out = buf(T * C);
+    AT* out = buf(T * C);
     const size_t mk = e->ws.mark();
-    bf16* a = buf(T * C);
+    AT* a = buf(T * C);
     gn(x, a, P, C, t.gng, t.gnb, e->uc.eps_tf, false);
-    bf16* h = buf(T * C);
-    linear(a, T, C, t.wpin, C, t.bpin, h, C);
-    bf16* hb = buf(T * C);  // ping-pong hidden state across blocks
+    AT* h = buf(T * C);
+    linear(a, T, C, wt<AT>(t.wpin), C, t.bpin, h, C);
+    AT* hb = buf(T * C);  // ping-pong hidden state across blocks
     for (const BlkW& k : t.blk) {
       const size_t mb = e->ws.mark();
-      bf16* n = buf(T * C);
+      AT* n = buf(T * C);
       ln(h, n, T, C, k.l1g, k.l1b);
-      bf16* o = buf(T * C);
-      if (e->use_attn_tc && attention_tc_supported(dh, P, C)) {
+      AT* o = buf(T * C);
+      bool tc = false;
+      if constexpr (std::is_same<AT, bf16>::value) tc = e->use_attn_tc && attention_tc_supported(dh, P, C);
+      if (tc) {
         // tcgen05 flash attention: q|k token-major from one GEMM, Vᵀ channel-major from another
-        bf16* qk = buf(T * 2 * C);
-        linear(n, T, C, k.wqkv, 2 * C, nullptr, qk, 2 * C);
-        bf16* vt = buf(T * C);
-        linear(k.wqkv + 2L * C * C, C, C, n, (int)T, nullptr, vt, (int)T);
+        AT* qk = buf(T * 2 * C);
+        linear(n, T, C, wt<AT>(k.wqkv), 2 * C, nullptr, qk, 2 * C);
+        AT* vt = buf(T * C);
+        linear(wt<AT>(k.wqkv) + 2L * C * C, C, C, n, (int)T, nullptr, vt, (int)T);
         const int pi = e->prof.begin(PC_ATTN, st, 4.0 * R * heads * (double)P * P * dh);
-        attention_tc(qk, vt, o, R, heads, dh, C, P, st);
+        if constexpr (std::is_same<AT, bf16>::value) attention_tc(qk, vt, o, R, heads, dh, C, P, st);
         e->prof.end(pi, st);
       } else {
-        bf16* qkv = buf(T * 3 * C);
-        linear(n, T, C, k.wqkv, 3 * C, nullptr, qkv, 3 * C);
-        AttnDesc ad{};
+        AT* qkv = buf(T * 3 * C);
+        linear(n, T, C, wt<AT>(k.wqkv), 3 * C, nullptr, qkv, 3 * C);
+        AttnDescT<AT> ad{};
         ad.Q = qkv;
         ad.ldq = 3 * C;
         ad.q_bstride = (long)P * 3 * C;
@@ -659,17 +680,17 @@ struct Fwd {
         ad.Lk = P;
         attn(ad);
       }
-      bf16* h2 = buf(T * C);
-      linear(o, T, C, k.wo, C, k.bo, h2, C, h);
+      AT* h2 = buf(T * C);
+      linear(o, T, C, wt<AT>(k.wo), C, k.bo, h2, C, h);
       ln(h2, n, T, C, k.l2g, k.l2b);
-      bf16* q2 = buf(T * C);
-      linear(n, T, C, k.wq2, C, nullptr, q2, C);
-      AttnDesc cd{};
+      AT* q2 = buf(T * C);
+      linear(n, T, C, wt<AT>(k.wq2), C, nullptr, q2, C);
+      AttnDescT<AT> cd{};
       cd.Q = q2;
       cd.ldq = C;
       cd.q_bstride = (long)P * C;
-      cd.K = e->kv_cache + k.koff;
-      cd.V = e->kv_cache + k.voff;
+      cd.K = static_cast<const AT*>(e->kv_cache) + k.koff;
+      cd.V = static_cast<const AT*>(e->kv_cache) + k.voff;
       cd.ldk = e->U.kv_width;
       cd.kv_bstride = e->slot_elems;
       cd.kv_index = kv_index;
@@ -682,44 +703,45 @@ struct Fwd {
       cd.Lq = P;
       cd.Lk = e->uc.ctx_len;
       attn(cd);
-      bf16* h3 = buf(T * C);
-      linear(o, T, C, k.wo2, C, k.bo2, h3, C, h2);
+      AT* h3 = buf(T * C);
+      linear(o, T, C, wt<AT>(k.wo2), C, k.bo2, h3, C, h2);
       ln(h3, n, T, C, k.l3g, k.l3b);
-      bf16* gg = buf(T * 4 * C);
-      linear(n, T, C, k.wff1, 8 * C, k.bff1, gg, 4 * C, nullptr, ACT_GEGLU);
-      linear(gg, T, 4 * C, k.wff2, C, k.bff2, hb, C, h3);  // block output → hb
+      AT* gg = buf(T * 4 * C);
+      linear(n, T, C, wt<AT>(k.wff1), 8 * C, k.bff1, gg, 4 * C, nullptr, ACT_GEGLU);
+      linear(gg, T, 4 * C, wt<AT>(k.wff2), C, k.bff2, hb, C, h3);  // block output → hb
       e->ws.reset(mb);
       std::swap(h, hb);
     }
-    linear(h, T, C, t.wpout, C, t.bpout, out, C, x);  // proj_out + the transformer's input
+    linear(h, T, C, wt<AT>(t.wpout), C, t.bpout, out, C, x);  // proj_out + the transformer's input
     e->ws.reset(mk);
     return out;
   }
 };
 
-static void unet_forward(Engine* e, cudaStream_t st, int R, int H, int W, const bf16* x_in, const float* t_row,
+template <class AT>
+static void unet_forward(Engine* e, cudaStream_t st, int R, int H, int W, const AT* x_in, const float* t_row,
                          const int* kv_index, float* eps_out) {
   const UNetCfg& c = e->uc;
   UNetW& U = e->U;
-  Fwd f{e, st, R, nullptr, kv_index, nullptr};
+  Fwd<AT> f{e, st, R, nullptr, kv_index, nullptr};
   f.gn_ws = e->ws.alloc(gn_workspace_bytes(R, H * W * 4, 64) + (1 << 20));
   const int T = c.temb_dim(), C0 = c.block_out[0];
   // time embedding: sinusoid → linear_1 → SiLU → linear_2 → SiLU (the ResBlocks consume SiLU(temb))
-  bf16* sinus = f.buf((long)R * C0);
+  AT* sinus = f.buf((long)R * C0);
   timestep_sinusoid(t_row, R, C0, sinus, st);
-  bf16* t1 = f.buf((long)R * T);
-  f.linear(sinus, R, C0, U.lin1_w, T, U.lin1_b, t1, T, nullptr, ACT_SILU);
-  bf16* t2 = f.buf((long)R * T);
+  AT* t1 = f.buf((long)R * T);
+  f.linear(sinus, R, C0, wt<AT>(U.lin1_w), T, U.lin1_b, t1, T, nullptr, ACT_SILU);
+  AT* t2 = f.buf((long)R * T);
   if (c.add_time_dim) {
     // SDXL: temb = linear_2(·) + aug[slot(row)] (the prompt's cached added embedding), then SiLU
     float* aug_rows = e->ws.get<float>((size_t)R * T);
     gather_rows_f32(e->aug_cache, kv_index, R, T, aug_rows, st);
-    GemmDesc d;
+    GemmDescT<AT> d;
     d.A = t1;
     d.M = R;
     d.K = T;
     d.lda = T;
-    d.Bw[0] = U.lin2_w;
+    d.Bw[0] = wt<AT>(U.lin2_w);
     d.N = T;
     d.ldb = T;
     d.out = t2;
@@ -733,17 +755,17 @@ static void unet_forward(Engine* e, cudaStream_t st, int R, int H, int W, const 
     gemm(d, st);
     e->prof.end(pi, st);
   } else {
-    f.linear(t1, R, T, U.lin2_w, T, U.lin2_b, t2, T, nullptr, ACT_SILU);
+    f.linear(t1, R, T, wt<AT>(U.lin2_w), T, U.lin2_b, t2, T, nullptr, ACT_SILU);
   }
   float* temb_all = e->ws.get<float>((size_t)R * U.temb_all_n);
-  f.linear(t2, R, T, U.temb_all_w, U.temb_all_n, U.temb_all_b, temb_all, U.temb_all_n, nullptr, ACT_NONE, 1);
+  f.linear(t2, R, T, wt<AT>(U.temb_all_w), U.temb_all_n, U.temb_all_b, temb_all, U.temb_all_n, nullptr, ACT_NONE, 1);
   f.temb_all = temb_all;
 
   int h = H, w = W;
-  bf16* x = f.buf((long)R * h * w * C0);
-  f.conv(x_in, h, w, 64, U.conv_in_w, C0, U.conv_in_b, x, nullptr, nullptr, 0, 0, c.in_ch);
+  AT* x = f.buf((long)R * h * w * C0);
+  f.conv(x_in, h, w, 64, wt<AT>(U.conv_in_w), C0, U.conv_in_b, x, nullptr, nullptr, 0, 0, c.in_ch);
   struct Skip {
-    bf16* p;
+    AT* p;
     int C;
   };
   std::vector<Skip> skips;
@@ -759,11 +781,11 @@ static void unet_forward(Engine* e, cudaStream_t st, int R, int H, int W, const 
     if (d.down) {
       const int ho = (h + 1) / 2, wo = (w + 1) / 2;
       const size_t mk = e->ws.mark();
-      bf16* out = f.buf((long)R * ho * wo * C);
+      AT* out = f.buf((long)R * ho * wo * C);
       const size_t mk2 = e->ws.mark();
-      bf16* cols = f.buf((long)R * ho * wo * 9 * C);
+      AT* cols = f.buf((long)R * ho * wo * 9 * C);
       im2col_s2(x, cols, R, h, w, C, st);
-      f.linear(cols, (long)R * ho * wo, 9 * C, d.wdown, C, d.bdown, out, C);
+      f.linear(cols, (long)R * ho * wo, 9 * C, wt<AT>(d.wdown), C, d.bdown, out, C);
       e->ws.reset(mk2);
       (void)mk;
       x = out;
@@ -780,25 +802,25 @@ static void unet_forward(Engine* e, cudaStream_t st, int R, int H, int W, const 
       Skip s = skips.back();
       skips.pop_back();
       const int Ccat = C + s.C;
-      bf16* cat = f.buf((long)R * h * w * Ccat);
+      AT* cat = f.buf((long)R * h * w * Ccat);
       concat_channels(x, C, s.p, s.C, cat, (long)R * h * w, st);
       x = f.resblock(u.res[j], cat, h, w);
       C = u.res[j].cout;
       if (!u.tf.empty()) x = f.transformer(u.tf[j], x, h, w);
     }
     if (u.up) {
-      bf16* upx = f.buf((long)R * 4 * h * w * C);
+      AT* upx = f.buf((long)R * 4 * h * w * C);
       upsample2x(x, upx, R, h, w, C, st);
       h *= 2;
       w *= 2;
-      bf16* out = f.buf((long)R * h * w * C);
-      f.conv(upx, h, w, C, u.wup, C, u.bup, out);
+      AT* out = f.buf((long)R * h * w * C);
+      f.conv(upx, h, w, C, wt<AT>(u.wup), C, u.bup, out);
       x = out;
     }
   }
-  bf16* a = f.buf((long)R * h * w * C);
+  AT* a = f.buf((long)R * h * w * C);
   f.gn(x, a, h * w, C, U.nout_g, U.nout_b, c.eps_res, true);
-  f.conv(a, h, w, C, U.conv_out_w, 4, U.conv_out_b, eps_out, nullptr, nullptr, 1, 4);
+  f.conv(a, h, w, C, wt<AT>(U.conv_out_w), 4, U.conv_out_b, eps_out, nullptr, nullptr, 1, 4);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -920,10 +942,18 @@ void step_batch(Engine* e, const sd_batch* b, cudaStream_t st) {
   auto run = [&](cudaStream_t s) {
     SD_CUDA(cudaMemcpyAsync(e->meta_dev, e->meta_pinned[par], off, cudaMemcpyHostToDevice, s));
     e->ws.reset(0);
-    bf16* x_in = e->ws.get<bf16>((size_t)R * hw * 64);
-    gather_rows(m, R, hw, 64, x_in, s);
-    float* eps = e->ws.get<float>((size_t)R * hw * 4);
-    unet_forward(e, s, R, h, w, x_in, m.t_row, kv_dev, eps);
+    float* eps;
+    if (e->f32) {
+      float* x_in = e->ws.get<float>((size_t)R * hw * 64);
+      gather_rows(m, R, hw, 64, x_in, s);
+      eps = e->ws.get<float>((size_t)R * hw * 4);
+      unet_forward<float>(e, s, R, h, w, x_in, m.t_row, kv_dev, eps);
+    } else {
+      bf16* x_in = e->ws.get<bf16>((size_t)R * hw * 64);
+      gather_rows(m, R, hw, 64, x_in, s);
+      eps = e->ws.get<float>((size_t)R * hw * 4);
+      unet_forward<bf16>(e, s, R, h, w, x_in, m.t_row, kv_dev, eps);
+    }
     combine_update(m, n, hw, eps, 4, reinterpret_cast<float* const*>(db + o_lat), s);
   };
   const bool use_graph = e->use_graphs;

@@ -38,6 +38,14 @@ struct VAECfg {
 UNetCfg unet_cfg(int model);
 VAECfg vae_cfg(int model);
 
+// Weight matrices are stored in the engine's activation precision: bf16 (SD_PREC_BF16) or fp32
+// (SD_PREC_FP32 parity mode). `wptr` is the untyped device pointer; wt<T>(p) views it as T.
+using wptr = void*;
+template <class T>
+static inline const T* wt(const void* p) {
+  return static_cast<const T*>(p);
+}
+
 // bump allocator over one cudaMalloc'd block
 struct Arena {
   char* base = nullptr;
@@ -54,24 +62,24 @@ struct Arena {
 struct ResW {
   int cin, cout, temb_off;
   float *n1g, *n1b, *b1, *n2g, *n2b, *b2, *bsc = nullptr;
-  bf16 *w1, *w2, *wsc = nullptr;
+  wptr w1, w2, wsc = nullptr;
 };
 struct BlkW {  // one BasicTransformerBlock
   float *l1g, *l1b, *bo, *l2g, *l2b, *bo2, *l3g, *l3b, *bff1, *bff2;
-  bf16 *wqkv, *wo, *wq2, *wo2, *wff1, *wff2;
+  wptr wqkv, wo, wq2, wo2, wff1, wff2;
   int koff, voff;  // column offsets of this block's K / V in the text K/V cache rows
 };
 struct TfW {  // one Transformer2DModel: GN → proj_in → blocks → proj_out (+ x)
   int C;
   float *gng, *gnb, *bpin, *bpout;
-  bf16 *wpin, *wpout;
+  wptr wpin, wpout;
   std::vector<BlkW> blk;
 };
 struct DownW {
   std::vector<ResW> res;
   std::vector<TfW> tf;
   bool down;
-  bf16* wdown = nullptr;
+  wptr wdown = nullptr;
   float* bdown = nullptr;
   int ch;
 };
@@ -79,14 +87,14 @@ struct UpW {
   std::vector<ResW> res;
   std::vector<TfW> tf;
   bool up;
-  bf16* wup = nullptr;
+  wptr wup = nullptr;
   float* bup = nullptr;
   int ch;
 };
 struct UNetW {
-  bf16* conv_in_w;
+  wptr conv_in_w;
   float* conv_in_b;
-  bf16 *lin1_w, *lin2_w, *temb_all_w;
+  wptr lin1_w, lin2_w, temb_all_w;
   float *lin1_b, *lin2_b, *temb_all_b;
   int temb_all_n = 0;
   std::vector<DownW> down;
@@ -94,22 +102,22 @@ struct UNetW {
   TfW midtf;
   std::vector<UpW> up;
   float *nout_g, *nout_b, *conv_out_b;
-  bf16* conv_out_w;
-  bf16* kv_all_w;   // [kv_width][ctx_dim]: for each transformer block (forward order) K_j then V_j
+  wptr conv_out_w;
+  wptr kv_all_w;   // [kv_width][ctx_dim]: for each transformer block (forward order) K_j then V_j
   int kv_width = 0;
   // SDXL added embedding: Linear(add_in → T) → SiLU → Linear(T → T); per prompt slot, cached
-  bf16 *add1_w = nullptr, *add2_w = nullptr;
+  wptr add1_w = nullptr, add2_w = nullptr;
   float *add1_b = nullptr, *add2_b = nullptr;
 };
 struct VAEW {
   float *pq_b, *cin_b;
-  bf16 *pq_w, *cin_w;
+  wptr pq_w, cin_w;
   ResW mid0, mid1;
   float *ag, *ab, *bq, *bk, *bv, *bo;
-  bf16 *wq, *wk, *wv, *wo;
+  wptr wq, wk, wv, wo;
   std::vector<UpW> up;
   float *nout_g, *nout_b, *cout_b;
-  bf16* cout_w;
+  wptr cout_w;
 };
 
 // one VAE work item: op over a band of output rows [y0, y1) (R7 V1)
@@ -159,8 +167,10 @@ struct Engine {
   Arena ws;              // UNet workspace (reset every step)
   UNetW U{};
   VAEW V{};
-  // text K/V cache
-  bf16* kv_cache = nullptr;
+  bool f32 = false;       // SD_PREC_FP32: fp32 weights / activations, SIMT kernels (fp32.cu)
+  size_t esize = 2;       // bytes per weight / activation element
+  // text K/V cache (activation precision)
+  void* kv_cache = nullptr;
   float* aug_cache = nullptr;  // SDXL: [max_slots][T] added embedding per prompt slot (fp32)
   int max_slots = 0;
   long slot_elems = 0;

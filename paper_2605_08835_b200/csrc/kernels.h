@@ -21,15 +21,19 @@ enum { GEMM_DENSE = 0, GEMM_CONV3 = 1 };
 // Epilogue: v = alpha·acc + bias[n] (or bias[m] if bias_per_row) + temb[img][n];
 //           act (SiLU, or GEGLU over column pairs (c, c+64) of every 128-column group);
 //           + res[m][n]; stored bf16 or fp32 at out[m·ldo + col_off + n].
-struct GemmDesc {
+// GemmDescT<bf16> drives the tcgen05 kernel (gemm.cu); GemmDescT<float> the fp32 parity-mode SIMT
+// kernel (fp32.cu, R19 "fp32 mode"), which has the same operand layouts and epilogue. In the fp32
+// kernel m_tile_begin / m_tile_count count output PIXELS (rows of image 0) instead of 128-row boxes.
+template <class T>
+struct GemmDescT {
   int mode = GEMM_DENSE;
-  const bf16* A = nullptr;
+  const T* A = nullptr;
   int M = 0, K = 0, lda = 0;
   int nsrc = 1;
-  const bf16* xs[2] = {nullptr, nullptr};
+  const T* xs[2] = {nullptr, nullptr};
   int cs[2] = {0, 0};
   int B = 0, H = 0, W = 0;
-  const bf16* Bw[2] = {nullptr, nullptr};
+  const T* Bw[2] = {nullptr, nullptr};
   int N = 0, ldb = 0;
   void* out = nullptr;
   int ldo = 0, col_off = 0, out_f32 = 0;
@@ -39,7 +43,7 @@ struct GemmDesc {
   const float* temb = nullptr;
   int ld_temb = 0;
   int rows_per_img = 1;       // dense mode: image index = m / rows_per_img (for temb)
-  const bf16* res = nullptr;
+  const T* res = nullptr;
   int ldr = 0;
   int act = ACT_NONE;
   int m_tile_begin = 0, m_tile_count = -1;  // restrict to a contiguous range of M tiles (bands)
@@ -52,7 +56,12 @@ struct GemmDesc {
   size_t split_ws_bytes = 0;
 };
 
+using GemmDesc = GemmDescT<bf16>;
+using GemmDescF = GemmDescT<float>;
+
 void gemm(const GemmDesc& d, cudaStream_t st);
+void gemm(const GemmDescF& d, cudaStream_t st);  // fp32 parity mode (fp32.cu)
+inline size_t gemm_split_ws_bytes(const GemmDescF&) { return 0; }
 int gemm_splits(const GemmDesc& d);              // the split count gemm() will use given a workspace
 size_t gemm_split_ws_bytes(const GemmDesc& d);   // workspace bytes (0 when not split)
 // M tiles of a conv3 launch whose output rows lie in [y0, y1) of image 0 (used for bands).

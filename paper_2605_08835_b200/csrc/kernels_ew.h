@@ -9,35 +9,43 @@ typedef __nv_bfloat16 bf16;
 
 namespace sd {
 
-// ---- norms (norm.cu) ----
+// ---- norms (norm.cu) ----  bf16 activations (the product path) and fp32 (parity mode, R19); both
+// element types share the kernels, the workspace layout and the fixed reduction order
 size_t gn_workspace_bytes(int B, int P, int G);
-// x, y: [B][P][C] bf16 (may alias? no: y != x required only if silu chain needs x later)
-void group_norm(const bf16* x, bf16* y, int B, int P, int C, int G, const float* gamma, const float* beta, float eps,
-                bool silu, void* ws, cudaStream_t st);
 int gn_chunk_px(int C);  // pixels per statistics chunk (divides 128)
+// x, y: [B][P][C]
+template <class T>
+void group_norm(const T* x, T* y, int B, int P, int C, int G, const float* gamma, const float* beta, float eps,
+                bool silu, void* ws, cudaStream_t st);
 // pixel ranges [p0, p1) must be multiples of 128 (or end at P)
-void gn_stats_range(const bf16* x, int P, int C, int G, int p0, int p1, void* ws, cudaStream_t st);
-void gn_apply_range(const bf16* x, bf16* y, int P, int C, int G, int p0, int p1, const float* gamma, const float* beta,
+template <class T>
+void gn_stats_range(const T* x, int P, int C, int G, int p0, int p1, void* ws, cudaStream_t st);
+template <class T>
+void gn_apply_range(const T* x, T* y, int P, int C, int G, int p0, int p1, const float* gamma, const float* beta,
                     float eps, bool silu, void* ws, cudaStream_t st);
-void layer_norm(const bf16* x, bf16* y, int T, int C, const float* gamma, const float* beta, float eps,
-                cudaStream_t st);
+template <class T>
+void layer_norm(const T* x, T* y, int T_, int C, const float* gamma, const float* beta, float eps, cudaStream_t st);
 
 // ---- attention (attention.cu): O = softmax(Q Kᵀ/√d) V per (batch row, head) ----
-struct AttnDesc {
-  const bf16* Q;
+template <class T>
+struct AttnDescT {
+  const T* Q;
   int ldq;           // elements between consecutive tokens
   long q_bstride;    // elements between batch rows
-  const bf16* K;
-  const bf16* V;
+  const T* K;
+  const T* V;
   int ldk;
   long kv_bstride;
   const int* kv_index;  // optional per-row batch index for K/V (cross-attention ctx slots)
-  bf16* O;
+  T* O;
   int ldo;
   long o_bstride;
   int rows, heads, d, Lq, Lk;
 };
+using AttnDesc = AttnDescT<bf16>;
 void attention(const AttnDesc& a, cudaStream_t st);
+// fp32 parity mode (fp32.cu): one warp per query, fp32 online softmax; any d ≤ 512
+void attention(const AttnDescT<float>& a, cudaStream_t st);
 
 // tcgen05 flash attention (attention_tc.cu): qk [rows·P][2C] (q | k), vt [C][rows·P], O [rows·P][C]
 bool attention_tc_supported(int d, int P, int C);
@@ -57,17 +65,25 @@ struct RowMap {                 // device-side per-step metadata (uploaded once 
   const float* coef_a;          // [n_req] x ← a·x + b·ε̃
   const float* coef_b;          // [n_req]
 };
-void gather_rows(const RowMap& m, int rows, int hw, int cpad, bf16* out, cudaStream_t st);
+template <class T>
+void gather_rows(const RowMap& m, int rows, int hw, int cpad, T* out, cudaStream_t st);
 void combine_update(const RowMap& m, int n_req, int hw, const float* eps, int ld_eps, float* const* latents_dev,
                     cudaStream_t st);
-void timestep_sinusoid(const float* t_row, int rows, int dim, bf16* out, cudaStream_t st);
-void upsample2x(const bf16* x, bf16* y, int B, int H, int W, int C, cudaStream_t st);
-void im2col_s2(const bf16* x, bf16* y, int B, int H, int W, int C, cudaStream_t st);  // 3x3 stride 2 pad 1
-void concat_channels(const bf16* a, int ca, const bf16* b, int cb, bf16* y, long P, cudaStream_t st);
+template <class T>
+void timestep_sinusoid(const float* t_row, int rows, int dim, T* out, cudaStream_t st);
+template <class T>
+void upsample2x(const T* x, T* y, int B, int H, int W, int C, cudaStream_t st);
+template <class T>
+void im2col_s2(const T* x, T* y, int B, int H, int W, int C, cudaStream_t st);  // 3x3 stride 2 pad 1
+template <class T>
+void concat_channels(const T* a, int ca, const T* b, int cb, T* y, long P, cudaStream_t st);
 void f32_to_bf16(const float* x, bf16* y, long n, cudaStream_t st);
+inline void f32_to_act(const float* x, bf16* y, long n, cudaStream_t st) { f32_to_bf16(x, y, n, st); }
+void f32_to_act(const float* x, float* y, long n, cudaStream_t st);  // device copy
 void gather_rows_f32(const float* src, const int* idx, int rows, int n, float* dst, cudaStream_t st);
-// VAE head input: z fp32 [4][h][w] → bf16 NHWC [h][w][cpad] of z·scale (zeros in channels ≥ 4)
-void latent_to_nhwc(const float* z, int hw, float scale, int cpad, bf16* out, cudaStream_t st);
+// VAE head input: z fp32 [4][h][w] → NHWC [h][w][cpad] of z·scale (zeros in channels ≥ 4)
+template <class T>
+void latent_to_nhwc(const float* z, int hw, float scale, int cpad, T* out, cudaStream_t st);
 // image NHWC fp32 [P][ld] (first 3 channels) → NCHW fp32 [3][P]
 void nhwc_to_nchw3(const float* x, int ld, long P, float* y, cudaStream_t st);
 

@@ -10,6 +10,7 @@
 // is bitwise equal to the whole decode (I6).
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 
 #include "engine.h"
 
@@ -23,7 +24,7 @@ struct DecodeState {
   bool banded = true;
   Arena ar;
   size_t buf_elems = 0;
-  bf16* buf[NBUF];
+  void* buf[NBUF];  // activation precision of the engine (bf16, or fp32 in the parity mode)
   float* img_nhwc = nullptr;
   void* gn_ws = nullptr;
   std::vector<VItem> items;
@@ -35,8 +36,14 @@ struct DecodeState {
 // layer for a whole decode (fewer launches; same values — banding is bitwise neutral, I6)
 static int band_rows(int H, bool banded) { return banded ? (H >= 64 ? 32 : std::max(8, H / 2)) : H; }
 
-static void conv_desc(GemmDesc& d, const bf16* x, int H, int W, int C, const bf16* w, int N, const float* b, void* out,
-                      const bf16* res) {
+template <class AT>
+static AT* sb(DecodeState* s, int i) {
+  return static_cast<AT*>(s->buf[i]);
+}
+
+template <class AT>
+static void conv_desc(GemmDescT<AT>& d, const AT* x, int H, int W, int C, const AT* w, int N, const float* b, void* out,
+                      const AT* res) {
   d.mode = GEMM_CONV3;
   d.xs[0] = x;
   d.cs[0] = C;
@@ -52,66 +59,76 @@ static void conv_desc(GemmDesc& d, const bf16* x, int H, int W, int C, const bf1
   d.ldr = N;
 }
 
-static void run_conv_band(Engine* e, const bf16* x, int H, int W, int C, const bf16* w, int N, const float* b, void* out,
-                          const bf16* res, int y0, int y1, int out_f32, cudaStream_t st) {
-  GemmDesc d;
-  conv_desc(d, x, H, W, C, w, N, b, out, res);
-  d.out_f32 = out_f32;
+// restrict a conv launch to output rows [y0, y1) of image 0: 128-pixel boxes of the tcgen05 kernel,
+// output pixels of the fp32 kernel (kernels.h)
+static void set_band(GemmDesc& d, int H, int W, int y0, int y1) {
   int wt, ht, bt;
   conv3_tile_geometry(1, H, W, &wt, &ht, &bt);
   const int tx = cdiv(W, wt);
   if (y0 % ht || (y1 % ht && y1 != H)) throw CudaError("vae band not aligned to conv tile height");
   d.m_tile_begin = (y0 / ht) * tx;
   d.m_tile_count = cdiv(y1 - y0, ht) * tx;
+}
+static void set_band(GemmDescF& d, int H, int W, int y0, int y1) {
+  (void)H;
+  d.m_tile_begin = y0 * W;
+  d.m_tile_count = (y1 - y0) * W;
+}
+
+template <class AT>
+static void run_conv_band(Engine* e, const AT* x, int H, int W, int C, const AT* w, int N, const float* b, void* out,
+                          const AT* res, int y0, int y1, int out_f32, cudaStream_t st) {
+  (void)e;
+  GemmDescT<AT> d;
+  conv_desc(d, x, H, W, C, w, N, b, out, res);
+  d.out_f32 = out_f32;
+  set_band(d, H, W, y0, y1);
   gemm(d, st);
 }
 
 // whole-tensor resblock at the latent resolution (head)
-static void head_res(Engine* e, DecodeState* s, const ResW& r, bf16* x, bf16* out, bf16* t1, bf16* t2, int H, int W,
+template <class AT>
+static void head_res(Engine* e, DecodeState* s, const ResW& r, AT* x, AT* out, AT* t1, AT* t2, int H, int W,
                      cudaStream_t st) {
   const int P = H * W, G = e->vc.groups;
   group_norm(x, t1, 1, P, r.cin, G, r.n1g, r.n1b, e->vc.eps, true, s->gn_ws, st);
-  run_conv_band(e, t1, H, W, r.cin, r.w1, r.cout, r.b1, t2, nullptr, 0, H, 0, st);
+  run_conv_band(e, t1, H, W, r.cin, wt<AT>(r.w1), r.cout, r.b1, t2, (const AT*)nullptr, 0, H, 0, st);
   group_norm(t2, t1, 1, P, r.cout, G, r.n2g, r.n2b, e->vc.eps, true, s->gn_ws, st);
-  run_conv_band(e, t1, H, W, r.cout, r.w2, r.cout, r.b2, out, x, 0, H, 0, st);
+  run_conv_band(e, t1, H, W, r.cout, wt<AT>(r.w2), r.cout, r.b2, out, (const AT*)x, 0, H, 0, st);
 }
 
+template <class AT>
 static void run_head(Engine* e, DecodeState* s, const float* z, cudaStream_t st) {
   const int H = s->h, W = s->w, P = H * W;
   const int cm = e->vc.block_out.back();
   VAEW& V = e->V;
   size_t mk = s->ar.mark();
-  bf16* zin = s->ar.get<bf16>((size_t)P * 64);
+  AT* zin = s->ar.get<AT>((size_t)P * 64);
   latent_to_nhwc(z, P, 1.f / e->vc.sf, 64, zin, st);
-  bf16* hq = s->ar.get<bf16>((size_t)P * 64);
-  SD_CUDA(cudaMemsetAsync(hq, 0, (size_t)P * 64 * 2, st));
-  GemmDesc d;
+  AT* hq = s->ar.get<AT>((size_t)P * 64);
+  SD_CUDA(cudaMemsetAsync(hq, 0, (size_t)P * 64 * sizeof(AT), st));
+  GemmDescT<AT> d;
   d.A = zin;
   d.M = P;
   d.K = 64;
   d.lda = 64;
-  d.Bw[0] = V.pq_w;
+  d.Bw[0] = wt<AT>(V.pq_w);
   d.N = 4;
   d.ldb = 64;
   d.out = hq;
   d.ldo = 64;
   d.bias = V.pq_b;
   gemm(d, st);
-  bf16* x0 = s->buf[1];
-  run_conv_band(e, hq, H, W, 64, V.cin_w, cm, V.cin_b, x0, nullptr, 0, H, 0, st);
-  bf16* x1 = s->buf[2];
-  head_res(e, s, V.mid0, x0, x1, s->buf[3], s->buf[4], H, W, st);
-  // single-head attention, d = cm, via GEMMs: S = QKᵀ/√d (fp32), P = softmax(S), O = P·V
-  bf16* a = s->buf[3];
+  AT* x0 = sb<AT>(s, 1);
+  run_conv_band(e, (const AT*)hq, H, W, 64, wt<AT>(V.cin_w), cm, V.cin_b, x0, (const AT*)nullptr, 0, H, 0, st);
+  AT* x1 = sb<AT>(s, 2);
+  head_res(e, s, V.mid0, x0, x1, sb<AT>(s, 3), sb<AT>(s, 4), H, W, st);
+  // single-head attention, d = cm
+  AT* a = sb<AT>(s, 3);
   group_norm(x1, a, 1, P, cm, e->vc.groups, V.ag, V.ab, e->vc.eps, false, s->gn_ws, st);
-  bf16* q = s->ar.get<bf16>((size_t)P * cm);
-  bf16* k = s->ar.get<bf16>((size_t)P * cm);
-  bf16* vt = s->ar.get<bf16>((size_t)P * cm);
-  float* S = s->ar.get<float>((size_t)P * P);
-  bf16* Pm = s->ar.get<bf16>((size_t)P * P);
-  auto lin = [&](const bf16* A, int M, int K, const bf16* Wt, int N, const float* b, void* out, int ldo,
-                 const bf16* res, int bias_row, float alpha, int f32) {
-    GemmDesc g;
+  auto lin = [&](const AT* A, int M, int K, const AT* Wt, int N, const float* b, void* out, int ldo, const AT* res,
+                 int bias_row, float alpha, int f32) {
+    GemmDescT<AT> g;
     g.A = A;
     g.M = M;
     g.K = K;
@@ -129,16 +146,46 @@ static void run_head(Engine* e, DecodeState* s, const float* z, cudaStream_t st)
     g.out_f32 = f32;
     gemm(g, st);
   };
-  lin(a, P, cm, V.wq, cm, V.bq, q, cm, nullptr, 0, 1.f, 0);
-  lin(a, P, cm, V.wk, cm, V.bk, k, cm, nullptr, 0, 1.f, 0);
-  lin(V.wv, cm, cm, a, P, V.bv, vt, P, nullptr, 1, 1.f, 0);            // Vᵀ = Wv·aᵀ (+bv per row)
-  lin(q, P, cm, k, P, nullptr, S, P, nullptr, 0, 1.f / sqrtf((float)cm), 1);
-  softmax_rows(S, Pm, P, P, st);
-  bf16* o = s->buf[4];
-  lin(Pm, P, P, vt, cm, nullptr, o, cm, nullptr, 0, 1.f, 0);
-  bf16* x2 = s->buf[1];
-  lin(o, P, cm, V.wo, cm, V.bo, x2, cm, x1, 0, 1.f, 0);
-  head_res(e, s, V.mid1, x2, s->buf[0], s->buf[3], s->buf[4], H, W, st);
+  AT* q = s->ar.get<AT>((size_t)P * cm);
+  AT* k = s->ar.get<AT>((size_t)P * cm);
+  AT* o = sb<AT>(s, 4);
+  lin(a, P, cm, wt<AT>(V.wq), cm, V.bq, q, cm, nullptr, 0, 1.f, 0);
+  lin(a, P, cm, wt<AT>(V.wk), cm, V.bk, k, cm, nullptr, 0, 1.f, 0);
+  if constexpr (std::is_same<AT, bf16>::value) {
+    // via tcgen05 GEMMs: S = QKᵀ/√d (fp32), P = softmax(S), O = P·Vᵀᵀ
+    AT* vt = s->ar.get<AT>((size_t)P * cm);
+    float* S = s->ar.get<float>((size_t)P * P);
+    AT* Pm = s->ar.get<AT>((size_t)P * P);
+    lin(wt<AT>(V.wv), cm, cm, a, P, V.bv, vt, P, nullptr, 1, 1.f, 0);  // Vᵀ = Wv·aᵀ (+bv per row)
+    lin(q, P, cm, k, P, nullptr, S, P, nullptr, 0, 1.f / sqrtf((float)cm), 1);
+    softmax_rows(S, Pm, P, P, st);
+    lin(Pm, P, P, vt, cm, nullptr, o, cm, nullptr, 0, 1.f, 0);
+  } else {
+    // fp32 parity mode: V token-major and the fp32 attention kernel
+    AT* v = s->ar.get<AT>((size_t)P * cm);
+    lin(a, P, cm, wt<AT>(V.wv), cm, V.bv, v, cm, nullptr, 0, 1.f, 0);
+    AttnDescT<AT> ad{};
+    ad.Q = q;
+    ad.ldq = cm;
+    ad.q_bstride = (long)P * cm;
+    ad.K = k;
+    ad.V = v;
+    ad.ldk = cm;
+    ad.kv_bstride = (long)P * cm;
+    ad.kv_index = nullptr;
+    ad.O = o;
+    ad.ldo = cm;
+    ad.o_bstride = (long)P * cm;
+    ad.rows = 1;
+    ad.heads = 1;
+    ad.d = cm;
+    ad.Lq = P;
+    ad.Lk = P;
+    attention(ad, st);
+  }
+  AT* x2 = sb<AT>(s, 1);
+  lin(o, P, cm, wt<AT>(V.wo), cm, V.bo, x2, cm, x1, 0, 1.f, 0);
+  head_res(e, s, V.mid1, x2, sb<AT>(s, 0), sb<AT>(s, 3), sb<AT>(s, 4), H, W, st);
   s->ar.reset(mk);
 }
 
@@ -250,58 +297,56 @@ static void build_items(Engine* e, DecodeState* s) {
   cost.push_back(1);
 }
 
+template <class AT>
 static void run_item(Engine* e, DecodeState* s, const VItem& v, const float* z, float* image, cudaStream_t st) {
   const int G = e->vc.groups;
   switch (v.op) {
-    case VOP_HEAD: run_head(e, s, z, st); break;
+    case VOP_HEAD: run_head<AT>(e, s, z, st); break;
     case VOP_GN_STATS: {
       const int P = v.H * v.W;
-      gn_stats_range(s->buf[v.a], P, v.C, G, v.y0 * v.W, v.y1 * v.W, s->gn_ws, st);
+      gn_stats_range(sb<AT>(s, v.a), P, v.C, G, v.y0 * v.W, v.y1 * v.W, s->gn_ws, st);
       break;
     }
     case VOP_GN_APPLY: {
       const int P = v.H * v.W;
       const float* gam = static_cast<const float*>(v.p0);
-      gn_apply_range(s->buf[v.a], s->buf[v.b], P, v.C, G, v.y0 * v.W, v.y1 * v.W, gam,
+      gn_apply_range(sb<AT>(s, v.a), sb<AT>(s, v.b), P, v.C, G, v.y0 * v.W, v.y1 * v.W, gam,
                      static_cast<const float*>(v.p1), e->vc.eps, v.silu != 0, s->gn_ws, st);
       break;
     }
     case VOP_CONV: {
-      const bf16* res = v.c >= 0 ? s->buf[v.c] : nullptr;
+      const AT* res = v.c >= 0 ? sb<AT>(s, v.c) : nullptr;
+      const AT* x = sb<AT>(s, v.a);
       if (v.gn == 1) {
         const ResW* r = static_cast<const ResW*>(v.p0);
-        run_conv_band(e, s->buf[v.a], v.H, v.W, v.C, r->w1, v.C2, r->b1, s->buf[v.b], res, v.y0, v.y1, 0, st);
+        run_conv_band(e, x, v.H, v.W, v.C, wt<AT>(r->w1), v.C2, r->b1, sb<AT>(s, v.b), res, v.y0, v.y1, 0, st);
       } else if (v.gn == 2) {
         const ResW* r = static_cast<const ResW*>(v.p0);
-        run_conv_band(e, s->buf[v.a], v.H, v.W, v.C, r->w2, v.C2, r->b2, s->buf[v.b], res, v.y0, v.y1, 0, st);
+        run_conv_band(e, x, v.H, v.W, v.C, wt<AT>(r->w2), v.C2, r->b2, sb<AT>(s, v.b), res, v.y0, v.y1, 0, st);
       } else if (v.gn == 3) {
         const UpW* u = static_cast<const UpW*>(v.p0);
-        run_conv_band(e, s->buf[v.a], v.H, v.W, v.C, u->wup, v.C2, u->bup, s->buf[v.b], res, v.y0, v.y1, 0, st);
+        run_conv_band(e, x, v.H, v.W, v.C, wt<AT>(u->wup), v.C2, u->bup, sb<AT>(s, v.b), res, v.y0, v.y1, 0, st);
       } else {
-        GemmDesc d;
-        conv_desc(d, s->buf[v.a], v.H, v.W, v.C, e->V.cout_w, 3, e->V.cout_b, s->img_nhwc, nullptr);
+        GemmDescT<AT> d;
+        conv_desc(d, x, v.H, v.W, v.C, wt<AT>(e->V.cout_w), 3, e->V.cout_b, s->img_nhwc, (const AT*)nullptr);
         d.out_f32 = 1;
         d.ldo = 3;
-        int wt, ht, bt;
-        conv3_tile_geometry(1, v.H, v.W, &wt, &ht, &bt);
-        const int tx = cdiv(v.W, wt);
-        d.m_tile_begin = (v.y0 / ht) * tx;
-        d.m_tile_count = cdiv(v.y1 - v.y0, ht) * tx;
+        set_band(d, v.H, v.W, v.y0, v.y1);
         gemm(d, st);
       }
       break;
     }
     case VOP_SHORTCUT: {
       const ResW* r = static_cast<const ResW*>(v.p0);
-      GemmDesc d;
-      d.A = s->buf[v.a] + (long)v.y0 * v.W * v.C;
+      GemmDescT<AT> d;
+      d.A = sb<AT>(s, v.a) + (long)v.y0 * v.W * v.C;
       d.M = (v.y1 - v.y0) * v.W;
       d.K = v.C;
       d.lda = v.C;
-      d.Bw[0] = r->wsc;
+      d.Bw[0] = wt<AT>(r->wsc);
       d.N = v.C2;
       d.ldb = v.C;
-      d.out = s->buf[v.b] + (long)v.y0 * v.W * v.C2;
+      d.out = sb<AT>(s, v.b) + (long)v.y0 * v.W * v.C2;
       d.ldo = v.C2;
       d.bias = r->bsc;
       gemm(d, st);
@@ -309,8 +354,8 @@ static void run_item(Engine* e, DecodeState* s, const VItem& v, const float* z, 
     }
     case VOP_UPSAMPLE: {
       const int Wi = v.W / 2;
-      upsample2x(s->buf[v.a] + (long)(v.y0 / 2) * Wi * v.C, s->buf[v.b] + (long)v.y0 * v.W * v.C, 1, (v.y1 - v.y0) / 2,
-                 Wi, v.C, st);
+      upsample2x(sb<AT>(s, v.a) + (long)(v.y0 / 2) * Wi * v.C, sb<AT>(s, v.b) + (long)v.y0 * v.W * v.C, 1,
+                 (v.y1 - v.y0) / 2, Wi, v.C, st);
       break;
     }
     case VOP_FINAL:
@@ -348,8 +393,8 @@ static DecodeState* new_decode(Engine* e, int h, int w) {
   const size_t head = P * 64 * 2 * 2 + P * cm * 2 * 3 + P * P * 6 + ((size_t)8 << 20);
   const size_t img = (size_t)64 * P * 3 * 4;
   const size_t gnb = gn_workspace_bytes(1, (int)(64 * P), 64);
-  s->ar.init(NBUF * (s->buf_elems * 2 + 4096) + head + img + gnb + ((size_t)16 << 20));
-  for (int i = 0; i < NBUF; ++i) s->buf[i] = s->ar.get<bf16>(s->buf_elems);
+  s->ar.init(NBUF * (s->buf_elems * e->esize + 4096) + head * (e->esize / 2) + img + gnb + ((size_t)16 << 20));
+  for (int i = 0; i < NBUF; ++i) s->buf[i] = s->ar.alloc(s->buf_elems * e->esize);
   s->img_nhwc = s->ar.get<float>(64 * P * 3);
   s->gn_ws = s->ar.alloc(gnb);
   build_items(e, s);
@@ -390,7 +435,12 @@ void vae_decode_chunk(Engine* e, const float* z, int h, int w, int n_chunks, int
     throw std::logic_error("VAE chunk out of order");
   const int nb = (int)s->bounds.size() - 1;
   if (chunk < nb)
-    for (int i = s->bounds[chunk]; i < s->bounds[chunk + 1]; ++i) run_item(e, s, s->items[i], z, image, st);
+    for (int i = s->bounds[chunk]; i < s->bounds[chunk + 1]; ++i) {
+      if (e->f32)
+        run_item<float>(e, s, s->items[i], z, image, st);
+      else
+        run_item<bf16>(e, s, s->items[i], z, image, st);
+    }
   s->next_chunk++;
   if (s->next_chunk == n_chunks) {
     std::lock_guard<std::mutex> g(e->dmu);

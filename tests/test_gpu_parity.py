@@ -324,3 +324,41 @@ def test_sdxl_step_and_vae_parity():
         assert r <= TOL
     finally:
         eng.close()
+
+
+def test_sd15_bench_launch_config(sd15):
+    """The launch configuration bench.py times (CFG#2: 8 requests in lockstep, CFG on every row → 16
+    UNet rows at latent 64×64). The oracle cannot run all 16 rows in seconds, so: request 0 is checked
+    against the oracle (its cond + uncond rows; ε-part at TOL·κ, x at TOL), and every other request's
+    update inside the 16-row batch must equal its update alone bitwise (I5), which pins each of them to
+    the oracle-checked single-request path."""
+    eng, ctx_u = sd15
+    cfg = configs.SD15_UNET
+    n, step, g = 8, 7, 7.5
+    ctx = [synth.text_embedding(9, i, 77, 768) for i in range(n)]
+    slots = [eng.register(torch.from_numpy(c)) for c in ctx]
+    x0 = [synth.initial_noise(9, i, 64, 64) for i in range(n)]
+    lat = [torch.from_numpy(x).cuda() for x in x0]
+    eng.step(lat, [step] * n, [50] * n, [1] * n, [g] * n, slots)
+    torch.cuda.synchronize()
+    for i in (3, 7):
+        alone = [torch.from_numpy(x0[i]).cuda()]
+        eng.step(alone, [step], [50], [1], [g], [slots[i]])
+        torch.cuda.synchronize()
+        assert torch.equal(alone[0], lat[i]), i
+    P = configs.unet_params(cfg, 0, np.float32, bf16_weights=True)
+    t = int(sampling.timesteps(50)[step])
+    eps = unet.forward(P, cfg, np.stack([x0[0], x0[0]]), np.array([t, t]),
+                       np.stack([synth.bf16_round(ctx[0]), ctx_u]))
+    ec, eu = eps[0], eps[1]
+    et = sampling.cfg_combine(ec, eu, g, True)
+    exp = sampling.ddim_step(x0[0], et, 50, step)
+    kappa = (abs(1 - g) * np.linalg.norm(eu) + g * np.linalg.norm(ec)) / np.linalg.norm(et)
+    a, ap = sampling.ddim_alphas(50, step)
+    A = np.sqrt(ap / a)
+    got = lat[0].cpu().numpy()
+    r_x, r_eps = rel(got, exp), rel(got - A * x0[0], exp - A * x0[0])
+    print(f"sd15 16-row bench launch, request 0: x {r_x:.3e}, eps-part {r_eps:.3e}, kappa {kappa:.2f}")
+    for s in slots:
+        eng.release(s)
+    assert r_x <= TOL and r_eps <= TOL * kappa
