@@ -166,6 +166,7 @@ def serving_bench(eng, world, rank, args):
     from paper_2605_08835_b200 import binding as Bd
     from paper_2605_08835_b200 import profiler, serving
     t0 = time.perf_counter()
+    eng.warmup(LAT, LAT, N_REQ, n_dec=3)  # every step-shape graph + pooled decode states, before any timing
     prof = profiler.Profiler(eng, LAT, LAT, N_REQ, reps=1)
     tab = prof.measure([1, 2], b_max=N_REQ, n_max=3)
     prof.close()

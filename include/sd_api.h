@@ -84,6 +84,11 @@ sd_status sd_engine_launch_count(sd_engine* e, int64_t* out);
  * synchronises on the recorded events. */
 sd_status sd_engine_profile(sd_engine* e, int32_t enable);
 sd_status sd_engine_profile_read(sd_engine* e, int32_t cls, double* ms_out, int64_t* launches_out, double* work_out);
+/* Pre-builds what a server at latent h x w touches on first use, so no serving window pays for it:
+ * the CUDA graph of every step shape (1..max_req requests, any number of Skip-CFG rows) and n_dec
+ * pooled VAE decode states (whole and 2-chunk). Runs real kernels on scratch latents (ctx slot 0);
+ * synchronous on `stream`. SD_E_INVAL on bad sizes; SD_E_CUDA on a CUDA error. */
+sd_status sd_engine_warmup(sd_engine* e, int32_t h, int32_t w, int32_t max_req, int32_t n_dec, void* stream);
 
 /* ---- data plane: one step-level batched denoising iteration ---------
  * sd_ctx_register: cache the cross-attention K/V of one prompt embedding (text_emb_dev: device
@@ -180,7 +185,19 @@ typedef struct {
   int32_t latent_hw;            /* GPU mode: one resolution per server (R22)                     */
   uint64_t trace_seed;          /* GPU mode: initial noise z ~ N(0,1) keyed by (trace_seed, id)  */
   int32_t n_max;                /* max decodes planned per window (0 = b_max); the table needs n ≤ n_max */
+  int32_t policy;               /* SD_POLICY_*: SynerDiff, or a baseline of P:316-324           */
+  int32_t ablation;             /* SD_ABL_* bits (SynerDiff only); no chunking = c_max 1 */
+  int64_t dyn_window_us;        /* Dynamic Batching collection window (0 = 500 000)        */
 } sd_serve_config;
+/* Serving policies (§IV Baselines; semantics in oracle/serving.py):
+ *  SYNERDIFF  the method: threshold-aware plan, Skip-CFG, VAE chunking, feedback controller;
+ *  NAIVE      InstGenIE-like continuous batching with direct UNet-VAE concurrency: one stage
+ *             (M, min(N, M), 0) per window, c = 1, no Skip-CFG, no controller;
+ *  DYNAMIC    Dynamic Batching: 0.5 s collection window, lockstep until every member is done,
+ *             synchronous release;
+ *  SERIAL     Diffusers, BS = 1: denoise then decode, one request at a time. */
+enum { SD_POLICY_SYNERDIFF = 0, SD_POLICY_NAIVE = 1, SD_POLICY_DYNAMIC = 2, SD_POLICY_SERIAL = 3 };
+enum { SD_ABL_NO_SKIP = 1, SD_ABL_NO_CTL = 2 };
 typedef struct {
   uint64_t id;
   int64_t arrival_us;           /* A_i, µs since sd_serve_start; not admitted before it          */

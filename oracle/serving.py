@@ -16,6 +16,21 @@ Per window:
      a task reaching n_r stamps U_r at that round's end and becomes decode-pending; each of the
      stage's decodes completes at stage start + δ^c(m,n,k) (Eq. 2) and stamps V_r;
   5. the controller observes (now, waiting queue) after the window (R15).
+
+Baseline policies and ablations (PAPER.md:316-324 §IV Baselines, :395-397 §IV-E Ablation; SURVEY
+§8(f) rank 1), on the same table and clock:
+  "serial"   Diffusers, BS = 1: FCFS, one request at a time, every step a (1, 0, 0) round,
+             then its whole decode (0, 1, 0); the next request is admitted after the decode.
+  "dynamic"  Dynamic Batching: a batch is collected for 0.5 s after its oldest request
+             (or until B_max have arrived) — dispatched at max(now, min(A_first + W, A_{B_max-th})) —
+             then stepped in lockstep rounds (m_active, 0, 0) until EVERY member is done (all-in-
+             all-out: finished members wait, the straggler effect P:40); then the batch is decoded
+             in stages (0, ≤ n_max, 0) and released together (every V_i = the release time).
+  "naive"    InstGenIE: continuous batching with direct UNet-VAE concurrency — per window one
+             stage (M, min(N, M), 0) (or (0, N, 0) with no UNet work), c = 1, no Skip-CFG, no
+             threshold plan, no controller.
+  ablations  of "synerdiff": no_skip (level pinned to 0: no Skip-CFG), no_ctl (controller frozen at
+             its initial state); "no chunking" is c_star = c_max = 1.
 """
 from __future__ import annotations
 
@@ -38,9 +53,15 @@ class Task:
 
 
 def simulate(trace, tables, b_max=8, a_num=1, a_den=10, mode="exact", c_star=1, c_max=4, ctl_kw=None,
-             log=None):
+             log=None, policy="synerdiff", no_skip=False, no_ctl=False, dyn_window_us=500_000, n_max=None):
     """trace: [(id, arrival_us, n_steps)], tables: {c: {(m,n,k): (tau_us, delta_us)}}.
     Returns {id: Task}. `log` (list) receives one dict per window."""
+    n_max = b_max if n_max is None else n_max
+    if policy == "serial":
+        return _serial(trace, tables)
+    if policy == "dynamic":
+        return _dynamic(trace, tables, b_max, n_max, dyn_window_us)
+    naive = policy == "naive"
     pending = sorted((Task(i, a, n) for i, a, n in trace), key=lambda t: (t.A, t.id))
     pi = 0
     batch, dec, done = [], [], {}
@@ -54,14 +75,20 @@ def simulate(trace, tables, b_max=8, a_num=1, a_den=10, mode="exact", c_star=1, 
             now = pending[pi].A
             continue
         level, c = C.level, C.c
+        if no_skip or naive:
+            level = 0
+        if naive:
+            c = 1
         f = ctl.LEVELS[level]
         M = len(batch)
-        dq = sorted(dec, key=lambda t: (t.A, t.id))[:b_max]
+        dq = sorted(dec, key=lambda t: (t.A, t.id))[:min(b_max, n_max)]
         N = len(dq)
         elig = [t.s >= ctl.s_min(f, t.n) for t in batch]
         K = sum(elig)
         if N == 0:
             stages, tc, rounds = ((M, 0, 0),), 1, 1
+        elif naive:
+            stages, tc, rounds = (((M, min(N, M), 0),) if M else ((0, N, 0),)), 1, 1
         else:
             stages = sched.plan_window(tables[c], M, N, K, a_num, a_den, mode)
             tc, rounds = c, c
@@ -94,7 +121,55 @@ def simulate(trace, tables, b_max=8, a_num=1, a_den=10, mode="exact", c_star=1, 
                 dec.remove(t)
                 done[t.id] = t
         waiting = sum(1 for t in pending[pi:] if t.A <= now)
-        C.decide(now, waiting)
+        if not (naive or no_ctl):
+            C.decide(now, waiting)
+    return done
+
+
+def _serial(trace, tables):
+    """Diffusers baseline: BS = 1, FCFS, denoise then decode, one request at a time."""
+    tab = tables[1]
+    done, now = {}, 0
+    for t in sorted((Task(i, a, n) for i, a, n in trace), key=lambda t: (t.A, t.id)):
+        now = max(now, t.A)
+        tau, _ = tab[(1, 0, 0)]
+        for _ in range(t.n):
+            now += tau
+            t.s += 1
+        t.U = now
+        tau, delta = tab[(0, 1, 0)]
+        t.V = now + delta
+        now += tau
+        done[t.id] = t
+    return done
+
+
+def _dynamic(trace, tables, b_max, n_max, window_us):
+    """Dynamic Batching baseline: collection window, lockstep, synchronous release."""
+    tab = tables[1]
+    pending = sorted((Task(i, a, n) for i, a, n in trace), key=lambda t: (t.A, t.id))
+    done, now, pi = {}, 0, 0
+    while pi < len(pending):
+        first = pending[pi].A
+        full = pending[pi + b_max - 1].A if pi + b_max - 1 < len(pending) else None
+        close = first + window_us if full is None else min(first + window_us, full)
+        now = max(now, close)
+        batch = []
+        while pi < len(pending) and len(batch) < b_max and pending[pi].A <= now:
+            batch.append(pending[pi])
+            pi += 1
+        while any(t.s < t.n for t in batch):
+            active = [t for t in batch if t.s < t.n]
+            now += tab[(len(active), 0, 0)][0]
+            for t in active:
+                t.s += 1
+                if t.s == t.n:
+                    t.U = now
+        for j in range(0, len(batch), n_max):
+            now += tab[(0, min(n_max, len(batch) - j), 0)][0]
+        for t in batch:
+            t.V = now
+            done[t.id] = t
     return done
 
 

@@ -47,7 +47,14 @@ class ControllerConfig(C.Structure):
 class ServeConfig(C.Structure):
     _fields_ = [("b_max", C.c_int32), ("a_num", C.c_int32), ("a_den", C.c_int32), ("dp_mode", C.c_int32),
                 ("c_star", C.c_int32), ("ctl", ControllerConfig), ("table", C.c_void_p), ("latent_hw", C.c_int32),
-                ("trace_seed", C.c_uint64), ("n_max", C.c_int32)]
+                ("trace_seed", C.c_uint64), ("n_max", C.c_int32), ("policy", C.c_int32), ("ablation", C.c_int32),
+                ("dyn_window_us", C.c_int64)]
+
+
+SD_POLICY_SYNERDIFF, SD_POLICY_NAIVE, SD_POLICY_DYNAMIC, SD_POLICY_SERIAL = 0, 1, 2, 3
+SD_ABL_NO_SKIP, SD_ABL_NO_CTL = 1, 2
+POLICIES = {"synerdiff": SD_POLICY_SYNERDIFF, "naive": SD_POLICY_NAIVE, "dynamic": SD_POLICY_DYNAMIC,
+            "serial": SD_POLICY_SERIAL}
 
 
 class Request(C.Structure):
@@ -97,6 +104,7 @@ SIGNATURES = {
     "sd_controller_decide": [P, I64, I32, C.POINTER(Directive)],
     "sd_controller_free": [P],
     "sd_chunk_ranges": [PI64, I32, I32, PI32],
+    "sd_engine_warmup": [P, I32, I32, I32, I32, P],
     "sd_serve_start": [P, C.POINTER(ServeConfig)],
     "sd_submit": [P, C.POINTER(Request)],
     "sd_poll": [P, C.POINTER(Completion), I32, PI32, I32],

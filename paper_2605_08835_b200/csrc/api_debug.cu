@@ -140,7 +140,7 @@ extern "C" sd_status sd_debug_groupnorm(const void* x, void* y, int32_t nb, int3
   SD_API_BEGIN
   void* ws = nullptr;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  SD_CUDA(cudaMallocAsync(&ws, sd::gn_workspace_bytes(nb, P, G), st));
+  SD_CUDA(cudaMallocAsync(&ws, sd::gn_workspace_bytes(nb, P, G, C), st));
   sd::group_norm(static_cast<const bf16*>(x), static_cast<bf16*>(y), nb, P, C, G, gamma, beta, eps, silu != 0, ws, st);
   SD_CUDA(cudaFreeAsync(ws, st));
   SD_API_END

@@ -1,4 +1,7 @@
 // C ABI of the engine (include/sd_api.h: engine, data plane, chunked VAE decode).
+#include <algorithm>
+#include <vector>
+
 #include "api_common.h"
 #include "engine.h"
 
@@ -188,4 +191,49 @@ extern "C" sd_status sd_engine_profile_read(sd_engine* e, int32_t cls, double* m
     e->e.prof.read(cls, ms, &c, work);
     *n = c;
   })
+}
+
+// Pre-builds everything a server at latent h×w touches on its first use, so no serving window pays
+// for it: the step graph of every batch shape (n_req ≤ max_req, any number of Skip-CFG rows; two
+// calls each — the eager run, then the capture), and n_dec pooled decode states (whole and chunked).
+// Runs real kernels on scratch latents; synchronous on `stream`.
+static void warmup_impl(Engine* e, int h, int w, int max_req, int n_dec, cudaStream_t st) {
+  const size_t lat_bytes = (size_t)4 * h * w * sizeof(float);
+  const int nbuf = std::max(max_req, n_dec);
+  std::vector<float*> lat(nbuf, nullptr);
+  for (auto& p : lat) {
+    SD_CUDA(cudaMallocAsync(&p, lat_bytes, st));
+    SD_CUDA(cudaMemsetAsync(p, 0, lat_bytes, st));
+  }
+  std::vector<int32_t> step(max_req + 1, 0), nst(max_req + 1, 50), slot(max_req + 1, 0);
+  std::vector<float> g(max_req + 1, 7.5f);
+  for (int n = 1; n <= max_req; ++n)
+    for (int k = 0; k <= n; ++k) {
+      std::vector<uint8_t> hu(n, 1);
+      for (int i = 0; i < k; ++i) hu[i] = 0;
+      sd_batch b{n, h, w, lat.data(), step.data(), nst.data(), hu.data(), g.data(), slot.data()};
+      for (int rep = 0; rep < 2; ++rep) step_batch(e, &b, st);
+    }
+  if (n_dec > 0) {
+    float* img;
+    const size_t img_elems = (size_t)3 * e->upscale() * h * e->upscale() * w;
+    SD_CUDA(cudaMallocAsync(&img, img_elems * sizeof(float) * n_dec, st));
+    for (int c = 1; c <= std::min(2, std::max(1, e->cfg.c_max)); ++c) {
+      std::vector<DecodeState*> ds(n_dec, nullptr);
+      for (int j = 0; j < c; ++j)
+        for (int i = 0; i < n_dec; ++i) vae_decode_chunk(e, lat[i], h, w, c, j, &ds[i], img + i * img_elems, st);
+    }
+    SD_CUDA(cudaFreeAsync(img, st));
+  }
+  for (auto p : lat) SD_CUDA(cudaFreeAsync(p, st));
+  SD_CUDA(cudaStreamSynchronize(st));
+}
+
+extern "C" sd_status sd_engine_warmup(sd_engine* e, int32_t h, int32_t w, int32_t max_req, int32_t n_dec,
+                                      void* stream) {
+  ENGINE_GUARD(e);
+  SD_REQUIRE(h >= 8 && w >= 8 && h <= e->e.cfg.max_latent_hw && w <= e->e.cfg.max_latent_hw,
+             "sd_engine_warmup: latent size");
+  SD_REQUIRE(max_req >= 0 && max_req <= e->e.cfg.b_max && n_dec >= 0 && n_dec <= 64, "sd_engine_warmup: counts");
+  ENGINE_BODY(e, { warmup_impl(&e->e, h, w, max_req, n_dec, static_cast<cudaStream_t>(stream)); })
 }

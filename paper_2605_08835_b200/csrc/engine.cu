@@ -724,7 +724,7 @@ static void unet_forward(Engine* e, cudaStream_t st, int R, int H, int W, const 
   const UNetCfg& c = e->uc;
   UNetW& U = e->U;
   Fwd<AT> f{e, st, R, nullptr, kv_index, nullptr};
-  f.gn_ws = e->ws.alloc(gn_workspace_bytes(R, H * W * 4, 64) + (1 << 20));
+  f.gn_ws = e->ws.alloc(gn_workspace_bytes(R, H * W * 4, 64, 4096) + (1 << 20));
   const int T = c.temb_dim(), C0 = c.block_out[0];
   // time embedding: sinusoid → linear_1 → SiLU → linear_2 → SiLU (the ResBlocks consume SiLU(temb))
   AT* sinus = f.buf((long)R * C0);
@@ -937,10 +937,11 @@ void step_batch(Engine* e, const sd_batch* b, cudaStream_t st) {
   m.coef_b = reinterpret_cast<const float*>(db + o_b);
   const int* kv_dev = reinterpret_cast<const int*>(db + o_kv);
 
-  // the whole step: metadata H2D → K11 gather → UNet → K12 combine + sampler. Deterministic arena
-  // addresses for a given (n_req, rows, h, w), so it is captured once as a CUDA graph and replayed.
+  // the metadata H2D runs on the caller's stream ahead of the step (outside the graph, so one graph
+  // serves both staging buffers); the step itself — K11 gather → UNet → K12 combine + sampler — has
+  // deterministic arena addresses for a given (n_req, rows, h, w): captured once, then replayed.
+  SD_CUDA(cudaMemcpyAsync(e->meta_dev, e->meta_pinned[par], off, cudaMemcpyHostToDevice, st));
   auto run = [&](cudaStream_t s) {
-    SD_CUDA(cudaMemcpyAsync(e->meta_dev, e->meta_pinned[par], off, cudaMemcpyHostToDevice, s));
     e->ws.reset(0);
     float* eps;
     if (e->f32) {
@@ -962,7 +963,7 @@ void step_batch(Engine* e, const sd_batch* b, cudaStream_t st) {
     run(st);
   } else {
     // profiled graphs (event-record nodes around every launch) are cached separately
-    auto& g = e->graphs[std::make_tuple(n, R, h, w, par + (prof ? 2 : 0))];
+    auto& g = e->graphs[std::make_tuple(n, R, h, w, prof ? 1 : 0)];
     if (!g.seen) {
       run(st);  // first call runs eagerly (sets kernel attributes, validates), capture next time
       g.seen = true;

@@ -11,7 +11,7 @@ namespace sd {
 
 // ---- norms (norm.cu) ----  bf16 activations (the product path) and fp32 (parity mode, R19); both
 // element types share the kernels, the workspace layout and the fixed reduction order
-size_t gn_workspace_bytes(int B, int P, int G);
+size_t gn_workspace_bytes(int B, int P, int G, int C);  // C = the largest channel count normalised
 int gn_chunk_px(int C);  // pixels per statistics chunk (divides 128)
 // x, y: [B][P][C]
 template <class T>

@@ -1,12 +1,17 @@
-// GroupNorm (+SiLU) and LayerNorm on NHWC / token-major bf16 activations.
+// GroupNorm (+SiLU) and LayerNorm on NHWC / token-major activations;
+// bf16 on the product path, fp32 in the parity mode (R19).
 //
-// GroupNorm is two launches: `gn_stats` writes deterministic per-(image, pixel-chunk, group)
-// partials (mean, M2) from fp32 register sums (one warp per group reduces the block's rows and
-// channels); `gn_apply` merges the partials of its image in fixed chunk order (Chan et al.; a
-// separate finalize launch instead when an image has more than 128 chunks), then normalises, applies γ/β (+SiLU) and writes bf16 with 16-byte
-// vector accesses. Thread (v, r) of a block always owns channel vector v, so the reduction order
-// is fixed and never depends on the batch (batch invariance, I5) or on banding (I6).
-// Chunk size adapts to C (≈ 32 K elements per chunk) so every block has enough loads in flight.
+// GroupNorm is three launches:
+//   gn_stats     deterministic per-(image, pixel-chunk, group) partials (mean, M2) from fp32 register
+//                sums: thread (v, r) of a block always owns channel vector v and issues 8 independent
+//                16-byte loads per batch; one warp per group then reduces the block's rows and
+//                channels in a fixed order.
+//   gn_finalize  one warp per (image, group) merges the chunk partials in fixed order (Chan et al.)
+//                and writes the per-(image, channel) affine table scale = γ·rstd, shift = β − μ·scale.
+//   gn_apply     a flat, coalesced elementwise pass y = x·scale + shift (+SiLU): 4 independent
+//                vectors in flight per thread, the table read from L1/L2.
+// The reduction order depends only on (P, C, G) — never on the batch (I5) or on banding (I6).
+// Chunk size adapts to C (≈ 40 K elements per chunk).
 #include "common.cuh"
 #include "kernels_ew.h"
 
@@ -18,18 +23,44 @@ struct GNPart {
 
 int gn_chunk_px(int C) { return C <= 512 ? 128 : C <= 1024 ? 64 : C <= 2048 ? 32 : 16; }
 
-static dim3 gn_block(int C) {
+static dim3 gn_stats_block(int C) {
   const int V = C / 8;
-  int R = 512 / V;
+  int R = 256 / V;
   if (R < 1) R = 1;
+  if (V * R < 32) R = cdiv(32, V);
   return dim3(V, R);
 }
 
+// raw 8-element vectors: loads stay in flight without conversion registers
+template <class T>
+struct Raw8;
+template <>
+struct Raw8<bf16> {
+  uint4 u;
+  __device__ __forceinline__ void ld(const bf16* p) { u = __ldg(reinterpret_cast<const uint4*>(p)); }
+  __device__ __forceinline__ void get(float (&f)[8]) const {
+    const bf16* e = reinterpret_cast<const bf16*>(&u);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) f[i] = __bfloat162float(e[i]);
+  }
+};
+template <>
+struct Raw8<float> {
+  float4 a, b;
+  __device__ __forceinline__ void ld(const float* p) {
+    a = __ldg(reinterpret_cast<const float4*>(p));
+    b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+  }
+  __device__ __forceinline__ void get(float (&f)[8]) const {
+    f[0] = a.x, f[1] = a.y, f[2] = a.z, f[3] = a.w, f[4] = b.x, f[5] = b.y, f[6] = b.z, f[7] = b.w;
+  }
+};
+
 // block (V, R): V = C/8 vector lanes, R pixel rows; grid (chunks in range, B)
 template <class T>
-__global__ void gn_stats_kernel(const T* __restrict__ x, int P, int C, int G, int chunk_px, int c_base,
-                                int nch_total, GNPart* __restrict__ part) {
-  extern __shared__ float sh[];  // [R][V][8] sums, then sumsq
+__global__ void __launch_bounds__(512) gn_stats_kernel(const T* __restrict__ x, int P, int C, int G, int chunk_px,
+                                                       int c_base, int nch_total, GNPart* __restrict__ part) {
+  extern __shared__ float sh[];  // [R][C] sums, then [R][C] sums of squares
   const int V = blockDim.x, R = blockDim.y;
   const int v = threadIdx.x, ry = threadIdx.y;
   const int b = blockIdx.y, ch = blockIdx.x + c_base;
@@ -38,26 +69,23 @@ __global__ void gn_stats_kernel(const T* __restrict__ x, int P, int C, int G, in
 #pragma unroll
   for (int i = 0; i < 8; ++i) s[i] = q[i] = 0.f;
   const T* xb = x + (long)b * P * C + v * 8;
-  int p = p0 + ry;
-  for (; p + 3 * R < p1; p += 4 * R) {  // 4 independent vector loads in flight
-    float f[4][8];
+  for (int p = p0 + ry; p < p1; p += 8 * R) {  // 8 independent vector loads in flight
+    // unconditional loads from clamped rows (the compiler keeps all 8 in flight); rows past the
+    // chunk are masked out afterwards
+    Raw8<T> u[8];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) load8(xb + (long)(p + k * R) * C, f[k]);
+    for (int k = 0; k < 8; ++k) u[k].ld(xb + (long)min(p + k * R, p1 - 1) * C);
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
+    for (int k = 0; k < 8; ++k) {
+      if (p + k * R < p1) {
+        float f[8];
+        u[k].get(f);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        s[i] += f[k][i];
-        q[i] += f[k][i] * f[k][i];
+        for (int i = 0; i < 8; ++i) {
+          s[i] += f[i];
+          q[i] += f[i] * f[i];
+        }
       }
-  }
-  for (; p < p1; p += R) {
-    float f[8];
-    load8(xb + (long)p * C, f);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      s[i] += f[i];
-      q[i] += f[i] * f[i];
     }
   }
   float* ss = sh;
@@ -71,9 +99,9 @@ __global__ void gn_stats_kernel(const T* __restrict__ x, int P, int C, int G, in
   // one warp per group: lanes stride the R × cg (row, channel) partials in a fixed order, then a
   // xor butterfly (both partners add the same two values, so every lane holds the same bits)
   const int cg = C / G;
-  const int tid = ry * V + v, lane = tid & 31, nw = (V * R) >> 5;
+  const int tid = ry * V + v, lane = tid & 31, nw = (V * R) >> 5;  // full warps only (V·R ≥ 32)
   const int ne = R * cg;
-  for (int g = tid >> 5; g < G; g += nw) {
+  for (int g = tid >> 5; g < G && (tid >> 5) < nw; g += nw) {
     float S = 0.f, Q = 0.f;
     for (int e = lane; e < ne; e += 32) {
       const int r = e / cg, c = g * cg + e % cg;
@@ -97,11 +125,14 @@ __global__ void gn_stats_kernel(const T* __restrict__ x, int P, int C, int G, in
 }
 
 // finalize: one warp per (image, group): lane l merges chunks l, l+32, … sequentially, then a fixed
-// butterfly (Chan) — deterministic; writes (mean, rstd) for the apply kernels
-// (the same function serves the separate finalize kernel and the in-block merge of gn_apply, so
-// both produce identical bits)
-__device__ __forceinline__ float2 gn_merge(int P, int C, int G, int chunk_px, int nchunks,
-                                           const GNPart* __restrict__ part, float eps, int b, int g, int lane) {
+// butterfly (Chan) — deterministic; writes the affine table (scale, shift) of the group's channels
+__global__ void gn_finalize_kernel(int P, int C, int G, int chunk_px, int nchunks, const GNPart* __restrict__ part,
+                                   float eps, const float* __restrict__ gamma, const float* __restrict__ beta,
+                                   float2* __restrict__ tab) {
+  const int lane = threadIdx.x & 31;
+  const int g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int b = blockIdx.y;
+  if (g >= G) return;
   const int cg = C / G;
   float n = 0.f, mean = 0.f, m2 = 0.f;
   for (int k = lane; k < nchunks; k += 32) {
@@ -132,147 +163,112 @@ __device__ __forceinline__ float2 gn_merge(int P, int C, int G, int chunk_px, in
     }
     n = tot;
   }
-  return make_float2(mean, rsqrtf(m2 / n + eps));
+  const float rstd = rsqrtf(m2 / n + eps);
+  for (int c = g * cg + lane; c < (g + 1) * cg; c += 32) {
+    const float sc = gamma[c] * rstd;  // y = x·(γ·rstd) + (β − mean·γ·rstd)
+    tab[(long)b * C + c] = make_float2(sc, beta[c] - mean * sc);
+  }
 }
 
-__global__ void gn_finalize_kernel(int P, int C, int G, int chunk_px, int nchunks, const GNPart* __restrict__ part,
-                                   float eps, float2* __restrict__ stats) {
-  const int lane = threadIdx.x & 31;
-  const int g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int b = blockIdx.y;
-  if (g >= G) return;
-  const float2 r = gn_merge(P, C, G, chunk_px, nchunks, part, eps, b, g, lane);
-  if (lane == 0) stats[(long)b * G + g] = r;
-}
-
+// apply: flat over the 8-element vectors [v_begin, v_end) of x viewed as [B·P][C/8]; each thread
+// handles 4 vectors blockDim apart (coalesced), all loads issued before any math
 template <class T>
-__global__ void gn_apply_kernel(const T* __restrict__ x, int P, int C, int G, int chunk_px, int c_base,
-                                const float2* __restrict__ stats, const GNPart* __restrict__ part, int nchunks,
-                                float eps, const float* __restrict__ gamma, const float* __restrict__ beta, int silu,
-                                T* __restrict__ y) {
-  const int R = blockDim.y;
-  const int v = threadIdx.x, ry = threadIdx.y;
-  const int b = blockIdx.y, ch = blockIdx.x + c_base;
-  const int cg = C / G;
-  __shared__ float s_mean[64], s_rstd[64];
-  const int tid = ry * blockDim.x + v;
-  if (part) {
-    // few partials: every block merges its image's chunk partials itself (no finalize launch)
-    const int nw = (blockDim.x * R) >> 5;
-    for (int g = tid >> 5; g < G; g += nw) {
-      const float2 st = gn_merge(P, C, G, chunk_px, nchunks, part, eps, b, g, tid & 31);
-      if ((tid & 31) == 0) {
-        s_mean[g] = st.x;
-        s_rstd[g] = st.y;
-      }
+__global__ void __launch_bounds__(256) gn_apply_kernel(const T* __restrict__ x, long v_begin, long v_end, int P, int V,
+                                                       const float2* __restrict__ tab, int silu, T* __restrict__ y) {
+  constexpr int U = 4;
+  const long base = v_begin + (long)blockIdx.x * blockDim.x * U + threadIdx.x;
+  Raw8<T> u[U];
+#pragma unroll
+  for (int k = 0; k < U; ++k) u[k].ld(x + min(base + (long)k * blockDim.x, v_end - 1) * 8);  // all in flight
+#pragma unroll
+  for (int k = 0; k < U; ++k) {
+    const long i = base + (long)k * blockDim.x;
+    if (i >= v_end) break;
+    const unsigned pix = (unsigned)i / (unsigned)V;  // < 2^31 vectors per launch (checked on the host)
+    const int vc = (int)((unsigned)i - pix * (unsigned)V);
+    const int b = (int)(pix / (unsigned)P);
+    const float4* t4 = reinterpret_cast<const float4*>(tab + (long)b * V * 8 + vc * 8);
+    float f[8], o[8];
+    u[k].get(f);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float4 t = __ldg(t4 + j);  // (scale, shift) of channels 2j, 2j+1
+      const float a0 = f[2 * j] * t.x + t.y, a1 = f[2 * j + 1] * t.z + t.w;
+      o[2 * j] = silu ? silu_f(a0) : a0;
+      o[2 * j + 1] = silu ? silu_f(a1) : a1;
     }
-  } else if (tid < G) {
-    const float2 st = stats[(long)b * G + tid];
-    s_mean[tid] = st.x;
-    s_rstd[tid] = st.y;
-  }
-  __syncthreads();
-  const int p0 = ch * chunk_px, p1 = min(P, p0 + chunk_px);
-  float ga[8], be[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int c = v * 8 + i;
-    const float rs = s_rstd[c / cg];
-    ga[i] = gamma[c] * rs;                      // y = x·(γ·rstd) + (β − mean·γ·rstd)
-    be[i] = beta[c] - s_mean[c / cg] * ga[i];
-  }
-  const long base = (long)b * P * C + v * 8;
-  int p = p0 + ry;
-  for (; p + R < p1; p += 2 * R) {
-    float u[2][8];
-#pragma unroll
-    for (int k = 0; k < 2; ++k) load8(x + base + (long)(p + k * R) * C, u[k]);
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      float o[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float f = u[k][i] * ga[i] + be[i];
-        o[i] = silu ? silu_f(f) : f;
-      }
-      store8(y + base + (long)(p + k * R) * C, o);
-    }
-  }
-  for (; p < p1; p += R) {
-    float u[8];
-    load8(x + base + (long)p * C, u);
-    float o[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const float f = u[i] * ga[i] + be[i];
-      o[i] = silu ? silu_f(f) : f;
-    }
-    store8(y + base + (long)p * C, o);
+    store8(y + i * 8, o);
   }
 }
 
 static size_t gn_part_bytes(int B, int P, int G) {
   return ((size_t)B * cdiv(P, 16) * G * sizeof(GNPart) + 255) & ~size_t(255);
 }
-size_t gn_workspace_bytes(int B, int P, int G) { return gn_part_bytes(B, P, G) + (size_t)B * G * sizeof(float2) + 256; }
+size_t gn_workspace_bytes(int B, int P, int G, int C) {
+  return gn_part_bytes(B, P, G) + (size_t)B * C * sizeof(float2) + 256;
+}
+static float2* gn_tab(void* ws, int B, int P, int G) {
+  return reinterpret_cast<float2*>(reinterpret_cast<char*>(ws) + gn_part_bytes(B, P, G));
+}
 
-static void gn_finalize(int B, int P, int C, int G, int cp, void* ws, float eps, cudaStream_t st) {
+static void gn_finalize(int B, int P, int C, int G, int cp, void* ws, float eps, const float* gamma, const float* beta,
+                        cudaStream_t st) {
   const int wpb = 4;  // warps per block
   gn_finalize_kernel<<<dim3(cdiv(G, wpb), B), 32 * wpb, 0, st>>>(
-      P, C, G, cp, cdiv(P, cp), reinterpret_cast<const GNPart*>(ws), eps,
-      reinterpret_cast<float2*>(reinterpret_cast<char*>(ws) + gn_part_bytes(B, P, G)));
+      P, C, G, cp, cdiv(P, cp), reinterpret_cast<const GNPart*>(ws), eps, gamma, beta, gn_tab(ws, B, P, G));
+  SD_CHECK_LAUNCH();
+}
+
+template <class T>
+static void gn_apply(const T* x, T* y, long v0, long v1, int P, int C, const float2* tab, bool silu,
+                     cudaStream_t st) {
+  const int threads = 256;
+  const long n = v1 - v0;
+  if (n <= 0) return;
+  if (v1 >= (1L << 31)) throw CudaError("group_norm: tensor too large");
+  gn_apply_kernel<T><<<cdiv(n, threads * 4), threads, 0, st>>>(x, v0, v1, P, C / 8, tab, silu ? 1 : 0, y);
   SD_CHECK_LAUNCH();
 }
 
 static void check_gn(int C, int G) {
-  if (C % 8 || C / 8 > 1024 || G > 64 || C % G) throw CudaError("group_norm: unsupported C/G");
+  if (C % 8 || C / 8 > 512 || G > 64 || C % G) throw CudaError("group_norm: unsupported C/G");
+}
+
+template <class T>
+static void gn_stats(const T* x, int B, int P, int C, int G, int c0, int c1, void* ws, cudaStream_t st) {
+  const int cp = gn_chunk_px(C);
+  const dim3 blk = gn_stats_block(C);
+  const size_t sh = (size_t)blk.x * blk.y * 8 * 2 * sizeof(float);
+  gn_stats_kernel<<<dim3(c1 - c0, B), blk, sh, st>>>(x, P, C, G, cp, c0, cdiv(P, cp), reinterpret_cast<GNPart*>(ws));
+  SD_CHECK_LAUNCH();
 }
 
 // band-restricted halves of group_norm (B = 1) over pixels [p0, p1) (multiples of 128): stats of the
-// chunks in the range; normalisation of the chunks in the range with ALL chunk partials merged in
+// chunks in the range; normalisation of the pixels in the range with ALL chunk partials merged in
 // fixed order — a banded GN is bitwise equal to the whole-tensor GN (R7 V1).
 template <class T>
 void gn_stats_range(const T* x, int P, int C, int G, int p0, int p1, void* ws, cudaStream_t st) {
   check_gn(C, G);
   const int cp = gn_chunk_px(C);
-  const dim3 blk = gn_block(C);
-  const size_t sh = (size_t)blk.x * blk.y * 8 * 2 * sizeof(float);
-  gn_stats_kernel<<<dim3(cdiv(p1, cp) - p0 / cp, 1), blk, sh, st>>>(x, P, C, G, cp, p0 / cp, cdiv(P, cp),
-                                                                     reinterpret_cast<GNPart*>(ws));
-  SD_CHECK_LAUNCH();
+  gn_stats(x, 1, P, C, G, p0 / cp, cdiv(p1, cp), ws, st);
 }
 template <class T>
 void gn_apply_range(const T* x, T* y, int P, int C, int G, int p0, int p1, const float* gamma, const float* beta,
                     float eps, bool silu, void* ws, cudaStream_t st) {
   check_gn(C, G);
   const int cp = gn_chunk_px(C);
-  const dim3 blk = gn_block(C);
-  if (p0 == 0) gn_finalize(1, P, C, G, cp, ws, eps, st);  // bands run in order: finalize before band 0
-  gn_apply_kernel<<<dim3(cdiv(p1, cp) - p0 / cp, 1), blk, 0, st>>>(
-      x, P, C, G, cp, p0 / cp, reinterpret_cast<const float2*>(reinterpret_cast<char*>(ws) + gn_part_bytes(1, P, G)),
-      nullptr, 0, eps, gamma, beta, silu ? 1 : 0, y);
-  SD_CHECK_LAUNCH();
+  if (p0 == 0) gn_finalize(1, P, C, G, cp, ws, eps, gamma, beta, st);  // bands run in order
+  gn_apply(x, y, (long)p0 * (C / 8), (long)p1 * (C / 8), P, C, gn_tab(ws, 1, P, G), silu, st);
 }
 
 template <class T>
 void group_norm(const T* x, T* y, int B, int P, int C, int G, const float* gamma, const float* beta, float eps,
                 bool silu, void* ws, cudaStream_t st) {
   check_gn(C, G);
-  const dim3 blk = gn_block(C);
   const int cp = gn_chunk_px(C);
-  const int nch = cdiv(P, cp);
-  GNPart* part = reinterpret_cast<GNPart*>(ws);
-  const size_t sh = (size_t)blk.x * blk.y * 8 * 2 * sizeof(float);
-  gn_stats_kernel<<<dim3(nch, B), blk, sh, st>>>(x, P, C, G, cp, 0, nch, part);
-  SD_CHECK_LAUNCH();
-  // ≤ 128 chunk partials per (image, group) (every UNet GN up to a 128×128 latent): merged inside the
-  // apply blocks; more (the VAE's large images): one finalize launch first
-  const bool inline_merge = nch <= 128;
-  if (!inline_merge) gn_finalize(B, P, C, G, cp, ws, eps, st);
-  gn_apply_kernel<<<dim3(nch, B), blk, 0, st>>>(
-      x, P, C, G, cp, 0, reinterpret_cast<const float2*>(reinterpret_cast<char*>(ws) + gn_part_bytes(B, P, G)),
-      inline_merge ? part : nullptr, nch, eps, gamma, beta, silu ? 1 : 0, y);
-  SD_CHECK_LAUNCH();
+  gn_stats(x, B, P, C, G, 0, cdiv(P, cp), ws, st);
+  gn_finalize(B, P, C, G, cp, ws, eps, gamma, beta, st);
+  gn_apply(x, y, 0, (long)B * P * (C / 8), P, C, gn_tab(ws, B, P, G), silu, st);
 }
 
 // ---- LayerNorm: LANES lanes per token (NV 16-byte vectors each), two-pass in registers ----------

@@ -24,7 +24,106 @@ static int s_min(int level, int n) {
   return (n + 1) / 2;                       // ⌈0.5 n⌉
 }
 
+int64_t Loop::dynamic_dispatch_time() const {
+  // the batch closes W after its oldest request, or when B_max requests have arrived
+  const int64_t first = pending.front()->A;
+  int64_t close = first + cfg.dyn_window_us;
+  if ((int)pending.size() >= cfg.b_max) close = std::min(close, pending[cfg.b_max - 1]->A);
+  return close;
+}
+
+int64_t Loop::next_event() const {
+  if (pending.empty()) return -1;
+  if (cfg.policy == SD_POLICY_DYNAMIC && batch.empty() && dec.empty()) return dynamic_dispatch_time();
+  return next_arrival();
+}
+
+// one c = 1 round of stage (m, n, k) with the given tasks; returns the round end
+int64_t Loop::stage_round(Exec& ex, int m, int n, int k, const std::vector<STask*>& step,
+                          const std::vector<uint8_t>& skip, const std::vector<STask*>& decs,
+                          std::vector<int64_t>* dd) {
+  int64_t tau, delta;
+  if (!table->get(1, m, n, k, &tau, &delta))
+    throw std::invalid_argument("latency table miss (c,m,n,k)=(1," + std::to_string(m) + "," + std::to_string(n) +
+                                "," + std::to_string(k) + ")");
+  dd->assign(decs.size(), -1);
+  return ex.round(step, skip, decs, 0, 1, ex.now(), tau, delta, dd);
+}
+
+// Diffusers baseline: BS = 1, FCFS; every step a (1,0,0) round, then the whole decode
+bool Loop::serial_window(Exec& ex) {
+  const int64_t now = ex.now();
+  if (batch.empty() && dec.empty()) {
+    if (pending.empty() || pending.front()->A > now) return false;
+    batch.push_back(pending.front());
+    ex.admit(pending.front());
+    pending.erase(pending.begin());
+  }
+  std::vector<int64_t> dd;
+  if (!dec.empty()) {
+    STask* t = dec.front();
+    stage_round(ex, 0, 1, 0, {}, {}, {t}, &dd);
+    t->V = dd[0];
+    dec.clear();
+    ex.complete(t);
+    return true;
+  }
+  STask* t = batch.front();
+  const int64_t end = stage_round(ex, 1, 0, 0, {t}, {0}, {}, &dd);
+  if (++t->s == t->n) {
+    t->U = end;
+    batch.clear();
+    dec.push_back(t);
+  }
+  return true;
+}
+
+// Dynamic Batching baseline: collect, step in lockstep until every member is done (finished
+// members wait), decode in stages of ≤ n_max, release the whole batch together
+bool Loop::dynamic_window(Exec& ex) {
+  const int64_t now = ex.now();
+  if (batch.empty() && dec.empty()) {
+    if (pending.empty() || now < dynamic_dispatch_time()) return false;
+    size_t taken = 0;
+    while (taken < pending.size() && (int)batch.size() < cfg.b_max && pending[taken]->A <= now) {
+      batch.push_back(pending[taken]);
+      ex.admit(pending[taken]);
+      ++taken;
+    }
+    pending.erase(pending.begin(), pending.begin() + taken);
+  }
+  std::vector<int64_t> dd;
+  std::vector<STask*> active;
+  for (auto* t : batch)
+    if (t->s < t->n) active.push_back(t);
+  if (!active.empty()) {
+    const int64_t end =
+        stage_round(ex, (int)active.size(), 0, 0, active, std::vector<uint8_t>(active.size(), 0), {}, &dd);
+    for (auto* t : active)
+      if (++t->s == t->n) t->U = end;
+    return true;
+  }
+  // all members done: decode the next ≤ n_max of them (dec holds the decoded ones)
+  std::vector<STask*> todo;
+  for (auto* t : batch)
+    if (std::find(dec.begin(), dec.end(), t) == dec.end() && (int)todo.size() < cfg.n_max) todo.push_back(t);
+  const int64_t end = stage_round(ex, 0, (int)todo.size(), 0, {}, {}, todo, &dd);
+  dec.insert(dec.end(), todo.begin(), todo.end());
+  if (dec.size() == batch.size()) {  // synchronous release
+    for (auto* t : batch) {
+      t->V = end;
+      ex.complete(t);
+    }
+    batch.clear();
+    dec.clear();
+  }
+  return true;
+}
+
 bool Loop::window(Exec& ex) {
+  if (cfg.policy == SD_POLICY_SERIAL) return serial_window(ex);
+  if (cfg.policy == SD_POLICY_DYNAMIC) return dynamic_window(ex);
+  const bool naive = cfg.policy == SD_POLICY_NAIVE;
   int64_t now = ex.now();
   size_t taken = 0;
   while (taken < pending.size() && pending[taken]->A <= now && (int)batch.size() < cfg.b_max) {
@@ -34,7 +133,7 @@ bool Loop::window(Exec& ex) {
   }
   pending.erase(pending.begin(), pending.begin() + taken);
   if (batch.empty() && dec.empty()) return false;
-  const int level = ctl.level, c = ctl.c;
+  const int level = (naive || cfg.no_skip) ? 0 : ctl.level, c = naive ? 1 : ctl.c;
   const int M = (int)batch.size();
   std::vector<STask*> dq = dec;
   std::sort(dq.begin(), dq.end(), [](const STask* a, const STask* b) { return a->A != b->A ? a->A < b->A : a->id < b->id; });
@@ -50,6 +149,8 @@ bool Loop::window(Exec& ex) {
   int tc = 1, rounds = 1;
   if (N == 0) {
     plan.stages.push_back({M, 0, 0});
+  } else if (naive) {  // InstGenIE: the whole batch with the oldest decodes, no plan, no skip
+    plan.stages.push_back({M, M ? std::min(N, M) : N, 0});
   } else {
     plan_window(*table, M, N, K, c, cfg.a_num, cfg.a_den, cfg.dp_mode, &plan);
     tc = c;
@@ -123,7 +224,8 @@ bool Loop::window(Exec& ex) {
   int64_t waiting = 0;
   for (auto* t : pending)
     if (t->A <= now) ++waiting;
-  ctl.decide(now, (int32_t)ex.global_waiting(waiting));
+  const int64_t gw = ex.global_waiting(waiting);
+  if (!(naive || cfg.no_ctl)) ctl.decide(now, (int32_t)gw);
   return true;
 }
 
@@ -143,6 +245,15 @@ struct VirtualExec : Exec {
   void complete(STask* x) override { done.push_back(x); }
 };
 
+}  // namespace sd
+
+namespace sd {
+void set_policy(LoopCfg& c, const sd_serve_config* cfg) {
+  c.policy = cfg->policy;
+  c.no_skip = (cfg->ablation & SD_ABL_NO_SKIP) != 0;
+  c.no_ctl = (cfg->ablation & SD_ABL_NO_CTL) != 0;
+  c.dyn_window_us = cfg->dyn_window_us > 0 ? cfg->dyn_window_us : 500000;
+}
 }  // namespace sd
 
 using namespace sd;
@@ -169,6 +280,7 @@ extern "C" sd_status sd_serve_simulate(const sd_serve_config* cfg, const sd_tabl
   L.ctl.cfg = cfg->ctl;
   L.ctl.cfg.c_star = cfg->c_star;
   L.ctl.c = cfg->c_star;
+  set_policy(L.cfg, cfg);
   for (int i = 0; i < n; ++i) {
     tasks[i].id = ids[i];
     tasks[i].A = arrival_us[i];
@@ -179,7 +291,7 @@ extern "C" sd_status sd_serve_simulate(const sd_serve_config* cfg, const sd_tabl
   int windows = 0;
   while (!L.pending.empty() || !L.batch.empty() || !L.dec.empty()) {
     if (!L.window(ex)) {
-      ex.t = L.next_arrival();
+      ex.t = std::max(ex.t, L.next_event());
       continue;
     }
     ++windows;

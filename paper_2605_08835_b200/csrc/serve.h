@@ -39,6 +39,10 @@ struct LoopCfg {
   int dp_mode = 0;
   int c_star = 1;
   sd_controller_config ctl{};
+  // baseline policies and ablations (oracle/serving.py documents them)
+  int policy = SD_POLICY_SYNERDIFF;
+  bool no_skip = false, no_ctl = false;
+  int64_t dyn_window_us = 500000;
 };
 
 struct WindowLog {
@@ -69,11 +73,22 @@ struct Loop {
   std::vector<STask*> pending;  // sorted by (A, id)
   std::vector<STask*> batch, dec;
   std::vector<WindowLog>* log = nullptr;
-  // one window; returns false if there was nothing to do (caller waits for arrivals)
+  // one window; returns false if there was nothing to do (the caller waits until next_event())
   bool window(Exec& ex);
   int64_t next_arrival() const { return pending.empty() ? -1 : pending.front()->A; }
+  // earliest time window() can make progress when idle: the next arrival, or for Dynamic Batching
+  // the dispatch time of the batch being collected
+  int64_t next_event() const;
+
+ private:
+  bool serial_window(Exec& ex);
+  bool dynamic_window(Exec& ex);
+  int64_t dynamic_dispatch_time() const;
+  int64_t stage_round(Exec& ex, int m, int n, int k, const std::vector<STask*>& step, const std::vector<uint8_t>& skip,
+                      const std::vector<STask*>& decs, std::vector<int64_t>* dd);
 };
 
 void insert_pending(std::vector<STask*>& pending, STask* t);
+void set_policy(LoopCfg& c, const sd_serve_config* cfg);
 
 }  // namespace sd

@@ -76,6 +76,22 @@ struct Server {
   int P = 0;
   float* pinned_noise = nullptr;
   float* pinned_emb = nullptr;
+  // per-request buffers are recycled (cudaMalloc / cudaFree / cudaMallocHost in the loop would
+  // stall it; cudaFree synchronises the whole device, i.e. the concurrent UNet round too)
+  std::vector<float*> pool_lat, pool_img, pool_host;
+  float* take(std::vector<float*>& pool, size_t bytes, bool host) {
+    if (!pool.empty()) {
+      float* p = pool.back();
+      pool.pop_back();
+      return p;
+    }
+    float* p = nullptr;
+    if (host)
+      SD_CUDA(cudaMallocHost(&p, bytes));
+    else
+      SD_CUDA(cudaMalloc(&p, bytes));
+    return p;
+  }
 
   void run();
 };
@@ -87,9 +103,12 @@ int64_t GpuExec::now() {
 void GpuExec::admit(STask* t) {
   Engine* e = S->e;
   const int hw = t->h * t->w;
-  SD_CUDA(cudaMalloc(&t->lat, (size_t)4 * hw * 4));
-  SD_CUDA(cudaMalloc(&t->img_dev, (size_t)3 * 64 * hw * 4));
-  SD_CUDA(cudaMallocHost(&t->img_host, (size_t)3 * 64 * hw * 4));
+  {
+    std::lock_guard<std::mutex> g(S->mu);  // pool_host is refilled by sd_release
+    t->lat = S->take(S->pool_lat, (size_t)4 * hw * 4, false);
+    t->img_dev = S->take(S->pool_img, (size_t)3 * 64 * hw * 4, false);
+    t->img_host = S->take(S->pool_host, (size_t)3 * 64 * hw * 4, true);
+  }
   initial_noise(S->cfg.trace_seed, t->id, 4 * hw, S->pinned_noise);
   const float sig = init_sigma(e->cfg.sampler, t->n);
   for (int i = 0; i < 4 * hw; ++i) S->pinned_noise[i] *= sig;
@@ -152,10 +171,10 @@ void GpuExec::complete(STask* t) {
     std::lock_guard<std::mutex> g(S->e->mu);
     if (t->slot > 0) S->e->slot_used[t->slot] = 0;
   }
-  cudaFree(t->lat);
-  cudaFree(t->img_dev);
-  t->lat = t->img_dev = nullptr;
   std::lock_guard<std::mutex> g(S->mu);
+  S->pool_lat.push_back(t->lat);
+  S->pool_img.push_back(t->img_dev);
+  t->lat = t->img_dev = nullptr;
   S->completed.push_back(t);
   S->counters[3]++;
   S->cv_done.notify_all();
@@ -184,7 +203,7 @@ void Server::run() {
       }
       if (!loop.window(ex)) {
         std::unique_lock<std::mutex> g(mu);
-        const int64_t na = loop.next_arrival();
+        const int64_t na = loop.next_event();
         const int64_t wait_us = na < 0 ? 2000 : std::max<int64_t>(0, na - ex.now());
         cv_sub.wait_for(g, std::chrono::microseconds(std::min<int64_t>(wait_us, 2000)),
                         [&] { return stop || !inbox.empty(); });
@@ -221,6 +240,7 @@ extern "C" sd_status sd_serve_start(sd_engine* e, const sd_serve_config* cfg) {
   S->loop.cfg.a_den = cfg->a_den;
   S->loop.cfg.dp_mode = cfg->dp_mode;
   S->loop.cfg.c_star = cfg->c_star;
+  set_policy(S->loop.cfg, cfg);
   S->loop.table = &cfg->table->t;
   S->loop.ctl.cfg = cfg->ctl;
   S->loop.ctl.cfg.c_star = cfg->c_star;
@@ -311,7 +331,7 @@ extern "C" sd_status sd_release(sd_engine* e, uint64_t id) {
   std::lock_guard<std::mutex> g(S->mu);
   auto it = S->owned.find(id);
   SD_REQUIRE(it != S->owned.end() && it->second->V >= 0, "sd_release: unknown or unfinished id");
-  if (it->second->img_host) cudaFreeHost(it->second->img_host);
+  if (it->second->img_host) S->pool_host.push_back(it->second->img_host);
   delete it->second;
   S->owned.erase(it);
   return SD_OK;
@@ -336,6 +356,9 @@ extern "C" sd_status sd_serve_stop(sd_engine* e) {
     if (t->decode) destroy_decode(&e->e, reinterpret_cast<DecodeState*>(t->decode));
     delete t;
   }
+  for (float* p : S->pool_lat) cudaFree(p);
+  for (float* p : S->pool_img) cudaFree(p);
+  for (float* p : S->pool_host) cudaFreeHost(p);
   cudaFreeHost(S->pinned_noise);
   cudaFreeHost(S->pinned_emb);
   cudaEventDestroy(S->ev_hi);

@@ -392,7 +392,7 @@ static DecodeState* new_decode(Engine* e, int h, int w) {
   const int cm = e->vc.block_out.back();
   const size_t head = P * 64 * 2 * 2 + P * cm * 2 * 3 + P * P * 6 + ((size_t)8 << 20);
   const size_t img = (size_t)64 * P * 3 * 4;
-  const size_t gnb = gn_workspace_bytes(1, (int)(64 * P), 64);
+  const size_t gnb = gn_workspace_bytes(1, (int)(64 * P), 64, 1024);
   s->ar.init(NBUF * (s->buf_elems * e->esize + 4096) + head * (e->esize / 2) + img + gnb + ((size_t)16 << 20));
   for (int i = 0; i < NBUF; ++i) s->buf[i] = s->ar.alloc(s->buf_elems * e->esize);
   s->img_nhwc = s->ar.get<float>(64 * P * 3);

@@ -33,6 +33,7 @@ class Engine:
         B.call("sd_engine_create", C.byref(cfg), device, C.byref(h))
         self.h = h
         self.model = model
+        self.b_max = b_max
         self.precision = precision
         self.sampler = sampler
         self.device = device
@@ -55,6 +56,10 @@ class Engine:
         v = C.c_int64()
         B.call("sd_engine_launch_count", self.h, C.byref(v))
         return v.value
+
+    def warmup(self, h, w, max_req=None, n_dec=0, stream=None):
+        """sd_engine_warmup: capture every step-shape graph at h×w and pool n_dec decode states."""
+        B.call("sd_engine_warmup", self.h, h, w, self.b_max if max_req is None else max_req, n_dec, _stream(stream))
 
     def profile(self, enable: bool):
         B.call("sd_engine_profile", self.h, 1 if enable else 0)

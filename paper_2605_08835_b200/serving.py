@@ -45,12 +45,15 @@ def p99(values):
 
 
 def run_trace(eng, table_h, trace, latent_hw=64, b_max=8, c_star=1, c_max=2, dp_mode=0, guidance=7.5,
-              trace_seed=7, ctl=None, timeout_s=600, n_max=None):
+              trace_seed=7, ctl=None, timeout_s=600, n_max=None, policy="synerdiff", ablation=0,
+              dyn_window_us=500_000):
     """Serve `trace` [(id, arrival_us, n_steps)] on `eng`; returns per-request records and metrics.
     Arrival times are relative to sd_serve_start; all requests are submitted up front and admitted
-    by the server when their arrival time has passed."""
+    by the server when their arrival time has passed. `policy` selects SynerDiff or one of the
+    paper's baselines, `ablation` the SD_ABL_* bits."""
     ctl = ctl or B.ControllerConfig(c_star, c_max, 10, 3, 1, 2, -1, 5)
-    cfg = B.ServeConfig(b_max, 1, 10, dp_mode, c_star, ctl, table_h, latent_hw, trace_seed, n_max or 0)
+    cfg = B.ServeConfig(b_max, 1, 10, dp_mode, c_star, ctl, table_h, latent_hw, trace_seed, n_max or 0,
+                        B.POLICIES[policy], ablation, dyn_window_us)
     embs = {i: np.ascontiguousarray(synth.text_embedding(trace_seed, i, eng.ctx_len, eng.ctx_dim)) for i, _, _ in trace}
     B.call("sd_serve_start", eng.h, C.byref(cfg))
     try:

@@ -227,3 +227,36 @@ def test_serving_simulation_bitexact(rate, mode, cstar):
     if rate >= 12:
         assert any(w["level"] > 0 for w in log) and sum(ns) > 0     # the controller engaged Skip-CFG
     B.lib().sd_table_free(h)
+
+
+@pytest.mark.parametrize("policy,ablation,cstar,cmax", [("serial", 0, 1, 1), ("dynamic", 0, 1, 1), ("naive", 0, 2, 4),
+                                                         ("synerdiff", 1, 1, 4), ("synerdiff", 2, 2, 4),
+                                                         ("synerdiff", 0, 1, 1)])
+def test_serving_policies_bitexact(policy, ablation, cstar, cmax):
+    """Baselines and ablations: the C++ loop on the virtual clock equals
+    oracle/serving.py for every request's (U, V, #skips) and the number of windows."""
+    from oracle import serving
+    rng = np.random.default_rng(len(policy) * 7 + ablation)
+    tabs = serve_table(rng)
+    h = make_multi_table(tabs)
+    n = 90
+    gaps = rng.exponential(1e6 / 8.0, n)
+    arr = np.cumsum(gaps).astype(np.int64)
+    steps = rng.integers(20, 51, n)
+    trace = [(i, int(arr[i]), int(steps[i])) for i in range(n)]
+    ctl_cfg = B.ControllerConfig(cstar, cmax, 10, 3, 1, 2, -1, 5)
+    cfg = B.ServeConfig(8, 1, 10, 0, cstar, ctl_cfg, h, 64, 1, 4, B.POLICIES[policy], ablation, 300_000)
+    U, V = (C.c_int64 * n)(), (C.c_int64 * n)()
+    ns, win = (C.c_int32 * n)(), C.c_int32()
+    B.call("sd_serve_simulate", C.byref(cfg), h, n, (C.c_uint64 * n)(*range(n)), (C.c_int64 * n)(*arr.tolist()),
+           (C.c_int32 * n)(*steps.tolist()), U, V, ns, C.byref(win))
+    done = serving.simulate(trace, tabs, b_max=8, c_star=cstar, c_max=cmax, policy=policy,
+                            no_skip=bool(ablation & B.SD_ABL_NO_SKIP), no_ctl=bool(ablation & B.SD_ABL_NO_CTL),
+                            dyn_window_us=300_000, n_max=4)
+    assert len(done) == n
+    for i in range(n):
+        t = done[i]
+        assert (U[i], V[i], ns[i]) == (t.U, t.V, len(t.skips)), (policy, i)
+    if ablation & B.SD_ABL_NO_SKIP or policy != "synerdiff":
+        assert sum(ns) == 0
+    B.lib().sd_table_free(h)

@@ -109,3 +109,55 @@ def test_serving_tiny_matches_oracle_alone(cstar):
     print(f"serving: worst image rel-L2 {worst:.3e} (4 steps), {worst_long:.3e} (5-6 steps); skips {total_skips}")
     assert worst <= 3e-2
     B.lib().sd_table_free(tab)
+
+
+@pytest.mark.parametrize("policy", ["naive", "dynamic", "serial"])
+def test_serving_baseline_policies_tiny(policy):
+    """The baselines of PAPER.md:316-324 on the GPU server: every request completes with A ≤ U ≤ V,
+    none takes a Skip-CFG step, the served image equals the request run alone (bitwise), and the
+    policy's shape holds (serial: no two requests overlap; dynamic: synchronous batch release)."""
+    eng = Engine("tiny", max_latent_hw=8, b_max=4, c_max=3)
+    ctx_u = synth.uncond_embedding(0, 8, 32)
+    eng.set_uncond(torch.from_numpy(ctx_u))
+    tab = _table()
+    ctl = B.ControllerConfig(1, 3, 4, 1, 1, 1_000_000, -1, 5)
+    cfg = B.ServeConfig(4, 1, 10, 0, 1, ctl, tab, 8, 5, 0, B.POLICIES[policy], 0, 20_000)
+    B.call("sd_serve_start", eng.h, C.byref(cfg))
+    n = 7
+    embs = [synth.text_embedding(5, i, 8, 32) for i in range(n)]
+    steps = [4, 5, 4, 6, 4, 5, 4]
+    for i in range(n):
+        r = B.Request(i, 3000 * i, steps[i], 7.5, embs[i].ctypes.data, 8, 32)
+        B.call("sd_submit", eng.h, C.byref(r))
+    got = {}
+    out = (B.Completion * 16)()
+    cnt = C.c_int32()
+    for _ in range(600):
+        B.call("sd_poll", eng.h, out, 16, C.byref(cnt), 50)
+        for j in range(cnt.value):
+            c_ = out[j]
+            img = np.ctypeslib.as_array(C.cast(c_.image_host, C.POINTER(C.c_float)), shape=(3, c_.h, c_.w)).copy()
+            got[c_.id] = (c_.arrival_us, c_.denoise_done_us, c_.decode_done_us, c_.n_skipped, img)
+            B.call("sd_release", eng.h, c_.id)
+        if len(got) == n:
+            break
+    B.call("sd_serve_stop", eng.h)
+    assert len(got) == n
+    for i in range(n):
+        A, U, Vt, ns, img = got[i]
+        assert A <= U <= Vt and ns == 0
+        slot = eng.register(torch.from_numpy(embs[i]))
+        lat = [torch.from_numpy(synth.initial_noise(5, i, 8, 8)).cuda()]
+        for s in range(steps[i]):
+            eng.step(lat, [s], [steps[i]], [1], [7.5], [slot])
+        alone = eng.decode(lat[0], 1)
+        torch.cuda.synchronize()
+        eng.release(slot)
+        assert np.array_equal(alone.cpu().numpy(), img), (policy, i)
+    if policy == "serial":
+        order = sorted(got.values(), key=lambda r: r[0])
+        assert all(a[2] <= b[1] for a, b in zip(order, order[1:]))
+    if policy == "dynamic":
+        assert len({r[2] for r in got.values()}) < n          # members of a batch share V (release)
+    eng.close()
+    B.lib().sd_table_free(tab)

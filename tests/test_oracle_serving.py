@@ -115,3 +115,75 @@ def test_metrics_definition():
     span = max(d.V for d in done.values()) - 0
     assert abs(m["throughput_per_s"] - 2 / (span / 1e6)) < 1e-12
     assert sched.p99(list(range(1, 101))) == 99
+
+
+# ---- baseline policies and ablations -------------------------------
+def test_serial_closed_form():
+    """Diffusers BS = 1: request j starts when request j−1's decode round ends."""
+    tabs = table()
+    tu, (td_tau, td_delta) = tabs[1][(1, 0, 0)][0], tabs[1][(0, 1, 0)]
+    done = serving.simulate([(0, 0, 3), (1, 0, 5), (2, 10**9, 2)], tabs, policy="serial")
+    assert done[0].U == 3 * tu and done[0].V == done[0].U + td_delta
+    assert done[1].U == done[0].U + td_tau + 5 * tu and done[1].V == done[1].U + td_delta
+    assert done[2].U == 10**9 + 2 * tu                        # idle server: starts at its arrival
+    assert all(t.skips == [] for t in done.values())
+
+
+def test_dynamic_batching_closed_form():
+    """Dynamic Batching: 0.5 s collection after the oldest request, lockstep until every
+    member is done (finished members wait: the straggler effect), synchronous release."""
+    tabs = table()
+    W = 500_000
+    done = serving.simulate([(0, 0, 3), (1, 100_000, 5), (2, 700_000, 2)], tabs, policy="dynamic",
+                            dyn_window_us=W)
+    t2, t1 = tabs[1][(2, 0, 0)][0], tabs[1][(1, 0, 0)][0]
+    assert done[0].U == W + 3 * t2                             # both step together for 3 rounds
+    assert done[1].U == done[0].U + 2 * t1                     # the straggler runs on alone
+    rel = done[1].U + tabs[1][(0, 2, 0)][0]                    # one decode stage for both
+    assert done[0].V == done[1].V == rel                       # all-in-all-out release
+    # request 2 arrived during the first batch; its window closes 0.5 s after its arrival
+    assert done[2].U == max(rel, 700_000 + W) + 2 * t1
+    # a full batch (B_max arrivals) dispatches at the B_max-th arrival, without waiting W
+    done = serving.simulate([(i, 1000 * i, 2) for i in range(4)], tabs, b_max=4, policy="dynamic")
+    assert done[0].U == 3000 + 2 * tabs[1][(4, 0, 0)][0]
+
+
+def test_naive_concurrency_runs_full_batch_with_decodes():
+    """InstGenIE: every window is one stage (M, min(N, M), 0) at c = 1, never a skip."""
+    tabs = table()
+    log = []
+    trace = [(i, 300_000 * i, 20 + (7 * i) % 13) for i in range(30)]
+    done = serving.simulate(trace, tabs, policy="naive", c_star=2, log=log)
+    assert len(done) == 30 and all(t.skips == [] for t in done.values())
+    for w in log:
+        assert w["c"] == 1 and w["level"] == 0
+        assert w["stages"] == (((w["M"], min(w["N"], w["M"]), 0),) if w["N"] and w["M"] else
+                               ((0, w["N"], 0),) if w["N"] else ((w["M"], 0, 0),))
+
+
+def test_ablations_disable_their_component():
+    tabs = table()
+    trace = [(i, 40_000 * i, 20 + (5 * i) % 31) for i in range(60)]          # overload: queue grows
+    full = serving.simulate(trace, tabs, c_star=1, c_max=4, ctl_kw=dict(up=(-1000, 1)))
+    assert sum(len(t.skips) for t in full.values()) > 0                      # the method skips
+    log = []
+    no_skip = serving.simulate(trace, tabs, c_star=1, c_max=4, ctl_kw=dict(up=(-1000, 1)), no_skip=True, log=log)
+    assert sum(len(t.skips) for t in no_skip.values()) == 0
+    assert any(w["c"] > 1 for w in log)                                      # the controller still chunks
+    log = []
+    no_ctl = serving.simulate(trace, tabs, c_star=1, c_max=4, ctl_kw=dict(up=(-1000, 1)), no_ctl=True, log=log)
+    assert all(w["c"] == 1 and w["level"] == 0 for w in log)                 # frozen at its initial state
+    for d in (full, no_skip, no_ctl):
+        assert len(d) == 60 and all(t.s == t.n and t.A <= t.U <= t.V for t in d.values())
+
+
+def test_policies_complete_every_request_fcfs_invariants():
+    tabs = table()
+    trace = [(i, 150_000 * i + (i % 3) * 7, 20 + (11 * i) % 31) for i in range(40)]
+    for pol in ("synerdiff", "naive", "dynamic", "serial"):
+        done = serving.simulate(trace, tabs, policy=pol)
+        assert sorted(done) == list(range(40))
+        assert all(t.s == t.n and t.A <= t.U <= t.V for t in done.values()), pol
+        if pol == "serial":  # FCFS, one at a time: completions in arrival order, no overlap
+            order = sorted(done.values(), key=lambda t: (t.A, t.id))
+            assert all(a.V <= b.U for a, b in zip(order, order[1:]))
