@@ -7,6 +7,10 @@
 // in TMEM, softmax warps, polynomial exp2 offload) is the planned replacement — see DESIGN.md.
 #include <float.h>
 
+#include <stdlib.h>
+
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels_ew.h"
 
@@ -213,6 +217,174 @@ __global__ void __launch_bounds__(128) attn_kernel(const AttnDesc a, float scale
   }
 }
 
+// ---- short-context attention (cross-attention to the ≤ 80 cached text tokens, R28) -------------
+// All keys fit one tile, so the softmax is exact in one pass (no running max / rescale), and a block
+// keeps its (row, head)'s K and V resident in shared memory while it walks QT query tiles of 64
+// (Q double-buffered with cp.async): K/V are read once per block instead of once per 64 queries,
+// and no MMA is spent on a second, mostly masked key tile. NW warps × 16 query rows, mma.sync.
+template <int D, int LKP, int NW>  // padded head dim, padded key count (multiples of 16); warps per block
+struct XAttnSmem {
+  static constexpr int BM = 16 * NW, LD = D + 8;
+  static constexpr int Q_ELEMS = BM * LD, KV_ELEMS = LKP * LD;
+  static constexpr int BYTES = (2 * Q_ELEMS + 2 * KV_ELEMS) * 2;
+};
+
+template <int D, int LKP, int NW>
+__global__ void __launch_bounds__(32 * NW) xattn_kernel(const AttnDesc a, float scale_log2, int qt_per_block) {
+  using S = XAttnSmem<D, LKP, NW>;
+  constexpr int NT = 32 * NW;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  bf16* sQ = reinterpret_cast<bf16*>(smem_raw);  // [2][BM][LD]
+  bf16* sK = sQ + 2 * S::Q_ELEMS;                // [LKP][LD]
+  bf16* sV = sK + S::KV_ELEMS;                   // [LKP][LD]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int head = blockIdx.y, row = blockIdx.z;
+  const int d = a.d;
+  const int kvb = a.kv_index ? a.kv_index[row] : row;
+  const bf16* Qg = a.Q + (long)row * a.q_bstride + (long)head * d;
+  const bf16* Kg = a.K + (long)kvb * a.kv_bstride + (long)head * d;
+  const bf16* Vg = a.V + (long)kvb * a.kv_bstride + (long)head * d;
+  const int nchunk = d / 8;
+  const int t_begin = blockIdx.x * qt_per_block;
+  const int t_end = min(t_begin + qt_per_block, (a.Lq + S::BM - 1) / S::BM);
+  if (t_begin >= t_end) return;
+  // zero the pad columns [d, D) of every buffer (never written by cp.async)
+  if (d < D)
+    for (int i = tid; i < (2 * S::BM + 2 * LKP) * (D - d); i += NT) {
+      const int r = i / (D - d), c = d + i % (D - d);
+      sQ[r * S::LD + c] = __float2bfloat16(0.f);
+    }
+  for (int i = tid; i < LKP * nchunk; i += NT) {  // K and V once; keys ≥ Lk zero-filled
+    const int r = i / nchunk, c = (i % nchunk) * 8;
+    const bool ok = r < a.Lk;
+    const long off = (long)(ok ? r : 0) * a.ldk + c;
+    cp_async16(sK + r * S::LD + c, Kg + off, ok);
+    cp_async16(sV + r * S::LD + c, Vg + off, ok);
+  }
+  auto load_q = [&](int t, int buf) {
+    const int q0 = t * S::BM;
+    bf16* dq = sQ + buf * S::Q_ELEMS;
+    for (int i = tid; i < S::BM * nchunk; i += NT) {
+      const int r = i / nchunk, c = (i % nchunk) * 8;
+      const bool ok = q0 + r < a.Lq;
+      cp_async16(dq + r * S::LD + c, Qg + (long)(ok ? q0 + r : 0) * a.ldq + c, ok);
+    }
+  };
+  load_q(t_begin, 0);
+  cp_async_commit();
+  const int g = lane >> 2, t4 = lane & 3;
+  bf16* Og = a.O + (long)row * a.o_bstride + (long)head * d;
+  for (int t = t_begin; t < t_end; ++t) {
+    const int buf = (t - t_begin) & 1;
+    if (t + 1 < t_end) load_q(t + 1, buf ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const bf16* cQ = sQ + buf * S::Q_ELEMS;
+    // ---- S = Q Kᵀ: 16 rows × LKP keys per warp ----
+    float s[LKP / 8][4];
+#pragma unroll
+    for (int n = 0; n < LKP / 8; ++n) s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < D / 16; ++kk) {
+      uint32_t a0, a1, a2, a3;
+      ldsm_x4(smem_u32(cQ + (warp * 16 + (lane & 15)) * S::LD + kk * 16 + (lane >> 4) * 8), a0, a1, a2, a3);
+#pragma unroll
+      for (int np = 0; np < LKP / 16; ++np) {
+        uint32_t b0, b1, b2, b3;
+        const int key = np * 16 + (lane >> 4) * 8 + (lane & 7);
+        const int col = kk * 16 + ((lane >> 3) & 1) * 8;
+        ldsm_x4(smem_u32(sK + key * S::LD + col), b0, b1, b2, b3);
+        mma16816(s[2 * np], a0, a1, a2, a3, b0, b1);
+        mma16816(s[2 * np + 1], a0, a1, a2, a3, b2, b3);
+      }
+    }
+    // ---- exact softmax over the (masked) keys, rows g and g + 8 ----
+    float mx[2] = {-FLT_MAX, -FLT_MAX};
+#pragma unroll
+    for (int n = 0; n < LKP / 8; ++n) {
+      const int c0 = n * 8 + 2 * t4;
+      if (c0 >= a.Lk) s[n][0] = s[n][2] = -FLT_MAX;
+      if (c0 + 1 >= a.Lk) s[n][1] = s[n][3] = -FLT_MAX;
+      mx[0] = fmaxf(mx[0], fmaxf(s[n][0], s[n][1]));
+      mx[1] = fmaxf(mx[1], fmaxf(s[n][2], s[n][3]));
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffff, mx[r], 1));
+      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffff, mx[r], 2));
+    }
+    const float ms0 = mx[0] * scale_log2, ms1 = mx[1] * scale_log2;
+    float rs[2] = {0.f, 0.f};
+#pragma unroll
+    for (int n = 0; n < LKP / 8; ++n) {
+      s[n][0] = exp2f(s[n][0] * scale_log2 - ms0);
+      s[n][1] = exp2f(s[n][1] * scale_log2 - ms0);
+      s[n][2] = exp2f(s[n][2] * scale_log2 - ms1);
+      s[n][3] = exp2f(s[n][3] * scale_log2 - ms1);
+      rs[0] += s[n][0] + s[n][1];
+      rs[1] += s[n][2] + s[n][3];
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      rs[r] += __shfl_xor_sync(0xffffffff, rs[r], 1);
+      rs[r] += __shfl_xor_sync(0xffffffff, rs[r], 2);
+    }
+    // ---- O = P V ----
+    float o[D / 8][4];
+#pragma unroll
+    for (int i = 0; i < D / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < LKP / 16; ++kk) {
+      const uint32_t p0 = pack_bf16(s[2 * kk][0], s[2 * kk][1]);
+      const uint32_t p1 = pack_bf16(s[2 * kk][2], s[2 * kk][3]);
+      const uint32_t p2 = pack_bf16(s[2 * kk + 1][0], s[2 * kk + 1][1]);
+      const uint32_t p3 = pack_bf16(s[2 * kk + 1][2], s[2 * kk + 1][3]);
+#pragma unroll
+      for (int dp = 0; dp < D / 16; ++dp) {
+        uint32_t b0, b1, b2, b3;
+        const int key = kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+        const int col = dp * 16 + (lane >> 4) * 8;
+        ldsm_x4_t(smem_u32(sV + key * S::LD + col), b0, b1, b2, b3);
+        mma16816(o[2 * dp], p0, p1, p2, p3, b0, b1);
+        mma16816(o[2 * dp + 1], p0, p1, p2, p3, b2, b3);
+      }
+    }
+    const float inv0 = 1.f / rs[0], inv1 = 1.f / rs[1];
+    const int r0 = t * S::BM + warp * 16 + g, r1 = r0 + 8;
+#pragma unroll
+    for (int i = 0; i < D / 8; ++i) {
+      const int c = i * 8 + 2 * t4;
+      if (c < d) {
+        if (r0 < a.Lq)
+          *reinterpret_cast<uint32_t*>(Og + (long)r0 * a.ldo + c) = pack_bf16(o[i][0] * inv0, o[i][1] * inv0);
+        if (r1 < a.Lq)
+          *reinterpret_cast<uint32_t*>(Og + (long)r1 * a.ldo + c) = pack_bf16(o[i][2] * inv1, o[i][3] * inv1);
+      }
+    }
+    __syncthreads();  // the buffer of tile t is refilled by the next iteration's prefetch
+  }
+}
+
+template <int D, int LKP, int NW = 4>
+static void launch_xattn(const AttnDesc& a, cudaStream_t st) {
+  using S = XAttnSmem<D, LKP, NW>;
+  static bool set = false;
+  if (!set) {
+    SD_CUDA(cudaFuncSetAttribute(xattn_kernel<D, LKP, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES));
+    set = true;
+  }
+  const int tiles = cdiv(a.Lq, S::BM);
+  // enough blocks for ~4 waves of 148 SMs, each walking a contiguous run of query tiles
+  const long pairs = (long)a.rows * a.heads;
+  int per = (int)std::max<long>(1, (long)tiles * pairs / (148L * 16));
+  per = std::min(per, 16);
+  dim3 grid(cdiv(tiles, per), a.heads, a.rows);
+  const float scale_log2 = 1.4426950408889634f / sqrtf((float)a.d);
+  xattn_kernel<D, LKP, NW><<<grid, 32 * NW, S::BYTES, st>>>(a, scale_log2, per);
+  SD_CHECK_LAUNCH();
+}
+
 template <int D>
 static void launch_attn(const AttnDesc& a, cudaStream_t st) {
   using S = AttnSmem<D>;
@@ -229,6 +401,24 @@ static void launch_attn(const AttnDesc& a, cudaStream_t st) {
 
 void attention(const AttnDesc& a, cudaStream_t st) {
   if (a.d % 8 || (a.ldq | a.ldk | a.ldo) % 8) throw CudaError("attention: d and strides must be multiples of 8");
+  static int nw = -1;  // SD_XATTN_NW=4|8: warps per short-context block (4: kbench r01, 53 vs 75 µs at 64²)
+  if (nw < 0) {
+    const char* e = getenv("SD_XATTN_NW");
+    nw = e && atoi(e) == 8 ? 8 : 4;
+  }
+  if (a.Lk <= 16 || (a.Lk <= 80 && a.d > 16)) {  // short context (the cached text tokens): one key tile
+#define SD_XA(D_, L_) return nw == 4 ? launch_xattn<D_, L_, 4>(a, st) : launch_xattn<D_, L_, 8>(a, st)
+    if (a.Lk <= 16) {
+      if (a.d <= 16) SD_XA(16, 16);
+      if (a.d <= 32) SD_XA(32, 16);
+    } else {
+      if (a.d <= 48) SD_XA(48, 80);
+      if (a.d <= 64) SD_XA(64, 80);
+      if (a.d <= 80) SD_XA(80, 80);
+      if (a.d <= 160) SD_XA(160, 80);
+    }
+#undef SD_XA
+  }
   if (a.d <= 16) launch_attn<16>(a, st);
   else if (a.d <= 32) launch_attn<32>(a, st);
   else if (a.d <= 48) launch_attn<48>(a, st);

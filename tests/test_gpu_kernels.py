@@ -150,7 +150,12 @@ def _attn_ref(q, k, v, heads):
 
 
 @pytest.mark.parametrize("R,heads,d,L,S", [(2, 8, 40, 256, 256), (1, 8, 80, 128, 77), (3, 2, 16, 64, 8),
-                                           (2, 8, 160, 64, 64), (1, 10, 64, 200, 130)])
+                                           (2, 8, 160, 64, 64), (1, 10, 64, 200, 130),
+                                           # short-context kernel (cross-attention to 77 text tokens):
+                                           # ragged query tiles, every head dim of SD-1.5 / SDXL / tiny
+                                           (2, 8, 40, 4096, 77), (3, 8, 160, 64, 77), (2, 10, 64, 1000, 77),
+                                           (2, 20, 64, 300, 77), (1, 2, 32, 100, 8), (2, 4, 16, 70, 16),
+                                           (1, 8, 48, 130, 80)])
 def test_attention_mma(R, heads, d, L, S):
     g = torch.Generator().manual_seed(L + S + d)
     C = heads * d

@@ -120,6 +120,19 @@ def main():
             by = 2.0 * x.numel() * 2
             print(json.dumps(dict(kind="layernorm", shape=[nb * P, C], ms=ms, gbs=by / ms / 1e6,
                                   frac=by / ms / 1e6 / hbm)), flush=True)
+    if args.only in ("", "xattn"):  # cross-attention to 77 cached text tokens (SD-1.5 levels)
+        for i_, (R, heads, d, P) in enumerate([(16, 8, 40, 4096), (16, 8, 80, 1024), (16, 8, 160, 256),
+                                                (16, 8, 160, 64)]):
+            if args.pick >= 0 and i_ != args.pick:
+                continue
+            C = heads * d
+            q = torch.randn(R, P, C, device="cuda").to(torch.bfloat16)
+            k, v = (torch.randn(R, 77, C, device="cuda").to(torch.bfloat16) for _ in range(2))
+            o = torch.empty(R, P, C, device="cuda", dtype=torch.bfloat16)
+            ms = timeit(lambda: B.call("sd_debug_attention", B._p(q), B._p(k), B._p(v), B._p(o), R, heads, d, P, 77,
+                                       B._p(cur())), args.reps)
+            by = 2.0 * q.numel() * 2
+            print(json.dumps(dict(kind="xattn", shape=[R, heads, d, P, 77], ms=ms, gbs=by / ms / 1e6)), flush=True)
     if args.only in ("", "attn"):
         for i_, (R, heads, d, P) in enumerate([(16, 8, 40, 4096), (16, 8, 80, 1024), (16, 10, 64, 4096)]):
             if args.pick >= 0 and i_ != args.pick:
