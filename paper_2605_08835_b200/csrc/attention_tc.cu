@@ -82,7 +82,9 @@ __global__ void __launch_bounds__(64 + 128 * SPLIT, 3 - NB)
                    int ldo, int C, int P, int Lk, float scale_log2) {
   using A = TcAttn<D, NB, SPLIT, EMU>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned (SWIZZLE_128B atoms); offsetting the shared array itself keeps the pointer in the
+  // shared state space, so the compiler emits STS / LDS rather than generic ST / LD
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sQ = smem;
   uint8_t* sKV = sQ + A::Q_BYTES;
   uint8_t* sP = sKV + A::STAGES * A::STAGE;

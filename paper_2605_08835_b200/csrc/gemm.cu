@@ -435,7 +435,9 @@ __global__ void __launch_bounds__(320, 1)
                 const __grid_constant__ CUtensorMap tout, const GemmArgs g) {
   using C = Cfg<BN, CG>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned (SWIZZLE_128B atoms); offsetting the shared array itself keeps the pointer in the
+  // shared state space, so the compiler emits STS / LDS rather than generic ST / LD
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
   uint8_t* sStage = sB + C::STAGES * C::B_BYTES;
