@@ -6,9 +6,12 @@
 //               produced directly by the V GEMM) tiles into a STAGES-deep ring
 //   warp 1      MMA: S_j = Q·K_jᵀ (M=128, N=128, K=d) into TMEM (double-buffered), then
 //               O += P_{j-1}·V_{j-1} (M=128, N=dpad, K=128) into a TMEM accumulator
-//   warps 2..5  softmax: one query row per thread — tcgen05.ld of S, running max / sum in fp32,
-//               P = exp2(s·log2e/√d − m) as bf16 into a swizzled smem tile (A operand of the PV
-//               MMA), and O ← α·O in TMEM when the running max grows; finally O/l → bf16.
+//   softmax     SPLIT threads per query row (d = 40: 2, each owning 64 key columns) — tcgen05.ld of
+//               S, running max / sum in fp32, P = exp2(s·log2e/√d − m) as bf16 into a swizzled smem
+//               tile (A operand of the PV MMA), and O ← α·O in TMEM when the running max grows
+//               (lazily, threshold 2⁸); finally O/l → bf16. At d = 40 the scores are read from TMEM
+//               once, the S buffer is handed back before the exps, and 1/8 of the exps run on the
+//               FMA pipe (ex2_poly) to relieve MUFU (SD_ATTN_EMU, below).
 // S never leaves the SM; P never leaves shared memory. Bound: MUFU exp2 (16/clk/SM) at d ≤ 80.
 #include <float.h>
 
@@ -76,7 +79,10 @@ __device__ __forceinline__ float ex2_poly(float x) {
   return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
 }
 
-template <int D, int NB, int SPLIT, int EMU>
+// OP = 1 (SPLIT = 2 only): the thread's 64 scores are read from TMEM once and kept in registers for
+// both passes, and the S buffer is released to the MMA warp right after the loads, so S_{j+1} is
+// computed while this block's exps run; P is packed in place over the scores (register budget)
+template <int D, int NB, int SPLIT, int EMU, int OP = 0>
 __global__ void __launch_bounds__(64 + 128 * SPLIT, 3 - NB)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tqk, const __grid_constant__ CUtensorMap tvt, bf16* __restrict__ O,
                    int ldo, int C, int P, int Lk, float scale_log2) {
@@ -216,6 +222,83 @@ __global__ void __launch_bounds__(64 + 128 * SPLIT, 3 - NB)
       const uint32_t sbase = tmem + lane_base + sb * 128 + h * CPT;
       // Lk is a multiple of 128 (attention_tc_supported): no key block is ragged
       uint32_t ta[32], tb[32];
+      if constexpr (OP >= 1) {
+        static_assert(SPLIT == 2, "one-pass softmax needs 64 columns per thread");  // OP ≥ 1
+        tmem_ld32_nw(sbase, ta);
+        tmem_ld32_nw(sbase + 32, tb);
+        tmem_wait_ld_tied(ta);
+        tmem_wait_ld_tied(tb);
+        tc_fence_before();  // the scores are in registers: S buffer free for S_{j+1}
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[sb]);
+        float mx4[4] = {-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX};
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          mx4[i & 3] = fmaxf(mx4[i & 3], __uint_as_float(ta[i]));
+          mx4[(i + 2) & 3] = fmaxf(mx4[(i + 2) & 3], __uint_as_float(tb[i]));
+        }
+        float mxb = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+        sX[((j & 1) * 2 + h) * 128 + r] = mxb;
+        named_bar_sync(1 + q, 64);
+        mxb = fmaxf(mxb, sX[((j & 1) * 2 + (h ^ 1)) * 128 + r]);
+        const bool upd = (mxb - m) * scale_log2 > 8.f;
+        const float mnew = upd ? mxb : m;
+        const float alpha = upd ? ex2((m - mnew) * scale_log2) : 1.f;
+        const float ms = mnew * scale_log2;
+        float sum8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {  // P packed in place: ta[i] ← bf16x2(p(ta[2i]), p(ta[2i+1]))
+          const float x0 = fmaf(__uint_as_float(ta[2 * i]), scale_log2, -ms);
+          const float x1 = fmaf(__uint_as_float(ta[2 * i + 1]), scale_log2, -ms);
+          const bool emu = OP >= 2 && (i % (OP == 2 ? 8 : 4)) == 3;  // OP 2 / 3: 1/8 / 1/4 on the FMA pipe
+          const float p0 = emu ? ex2_poly(x0) : ex2(x0);
+          const float p1 = emu ? ex2_poly(x1) : ex2(x1);
+          sum8[i & 7] += p0 + p1;
+          ta[i] = pack_bf16(p0, p1);
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float x0 = fmaf(__uint_as_float(tb[2 * i]), scale_log2, -ms);
+          const float x1 = fmaf(__uint_as_float(tb[2 * i + 1]), scale_log2, -ms);
+          const bool emu = OP >= 2 && (i % (OP == 2 ? 8 : 4)) == 1;
+          const float p0 = emu ? ex2_poly(x0) : ex2(x0);
+          const float p1 = emu ? ex2_poly(x1) : ex2(x1);
+          sum8[i & 7] += p0 + p1;
+          tb[i] = pack_bf16(p0, p1);
+        }
+        const float sum = ((sum8[0] + sum8[1]) + (sum8[2] + sum8[3])) + ((sum8[4] + sum8[5]) + (sum8[6] + sum8[7]));
+        l = l * alpha + sum;
+        m = mnew;
+        if (j >= 1) {
+          mbar_wait_sleep(pv_done, (j - 1) & 1);
+          tc_fence_after();
+          if (h == 0 && __any_sync(0xffffffff, alpha < 1.f)) {
+#pragma unroll
+            for (int c = 0; c < A::NPV / 16; ++c) {
+              uint32_t o[16];
+              tmem_ld16(tmem + lane_base + A::O_COL + c * 16, o);
+              tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+              tmem_st16(tmem + lane_base + A::O_COL + c * 16, o);
+            }
+            tmem_wait_st();
+          }
+        }
+        uint8_t* prow = sP + sb * A::P_BYTES + h * (A::BQ * 128) + r * 128;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) << 4)) =
+              make_uint4(ta[c * 4], ta[c * 4 + 1], ta[c * 4 + 2], ta[c * 4 + 3]);
+          *reinterpret_cast<uint4*>(prow + (((c + 4) ^ (r & 7)) << 4)) =
+              make_uint4(tb[c * 4], tb[c * 4 + 1], tb[c * 4 + 2], tb[c * 4 + 3]);
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[sb]);
+        continue;
+      }
       // pass 1: row max over this thread's scores — 4 independent max chains, the next 32-column TMEM
       // load in flight while this one is reduced (TMEM is re-read in pass 2)
       float mx4[4] = {-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX};
@@ -359,12 +442,12 @@ __global__ void __launch_bounds__(64 + 128 * SPLIT, 3 - NB)
 void make_tmap_2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_bytes, uint32_t box_in,
                   uint32_t box_out);
 
-template <int D, int NB, int SPLIT, int EMU = 0>
+template <int D, int NB, int SPLIT, int EMU = 0, int OP = 0>
 static void launch_tc(const bf16* qk, const bf16* vt, bf16* O, int rows, int heads, int C, int P, cudaStream_t st) {
   using A = TcAttn<D, NB, SPLIT, EMU>;
   static bool set = false;
   if (!set) {
-    SD_CUDA(cudaFuncSetAttribute(attn_tc_kernel<D, NB, SPLIT, EMU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SD_CUDA(cudaFuncSetAttribute(attn_tc_kernel<D, NB, SPLIT, EMU, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  A::SMEM));
     set = true;
   }
@@ -374,7 +457,7 @@ static void launch_tc(const bf16* qk, const bf16* vt, bf16* O, int rows, int hea
   make_tmap_2d(&mvt, vt, (uint64_t)T, (uint64_t)C, (uint64_t)T * 2, 64, A::NPV);
   dim3 grid(cdiv(P, A::BQ), heads, rows);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)D);
-  attn_tc_kernel<D, NB, SPLIT, EMU><<<grid, A::THREADS, A::SMEM, st>>>(mqk, mvt, O, C, C, P, P, scale_log2);
+  attn_tc_kernel<D, NB, SPLIT, EMU, OP><<<grid, A::THREADS, A::SMEM, st>>>(mqk, mvt, O, C, C, P, P, scale_log2);
   SD_CHECK_LAUNCH();
 }
 
@@ -389,14 +472,18 @@ static int attn_split() {
   return v;
 }
 
-// SD_ATTN_EMU=0|4: one exp2 pair in EMU on the FMA pipe (0 = all on MUFU, the default: r01 kbench
-// at d = 40 — emulating 1/4 of the exps costs 7 %, 1/3 costs 9 %: MUFU is not the binding limit)
+// SD_ATTN_EMU selects the d = 40 softmax variant (kbench r01, [16, 8, 40, 4096]):
+//   0  two TMEM passes, all exps on MUFU                          0.794 ms
+//   4  two passes, 1/4 of the exps on the FMA pipe (ex2_poly)     slower
+//   5  one TMEM pass (OP 1), S released before the exps           0.784 ms
+//   6  one pass + 1/8 of the exps on the FMA pipe (OP 2, default) 0.773 ms
+//   7  one pass + 1/4 on the FMA pipe (OP 3)                      0.804 ms
 static int attn_emu() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("SD_ATTN_EMU");
-    v = e ? atoi(e) : 0;
-    if (v != 4) v = 0;
+    v = e ? atoi(e) : 6;
+    if (v != 0 && v != 4 && (v < 5 || v > 7)) v = 6;
   }
   return v;
 }
@@ -427,17 +514,21 @@ void attention_tc(const bf16* qk, const bf16* vt, bf16* O, int rows, int heads, 
         case 210: launch_tc<40, 2, 1, 0>(qk, vt, O, rows, heads, C, P, st); break;
         case 220: launch_tc<40, 2, 2, 0>(qk, vt, O, rows, heads, C, P, st); break;
         case 224: launch_tc<40, 2, 2, 4>(qk, vt, O, rows, heads, C, P, st); break;
+        case 125: launch_tc<40, 1, 2, 0, 1>(qk, vt, O, rows, heads, C, P, st); break;  // SD_ATTN_EMU=5: one-pass
+        case 225: launch_tc<40, 2, 2, 0, 1>(qk, vt, O, rows, heads, C, P, st); break;
+        case 126: launch_tc<40, 1, 2, 0, 2>(qk, vt, O, rows, heads, C, P, st); break;
+        case 127: launch_tc<40, 1, 2, 0, 3>(qk, vt, O, rows, heads, C, P, st); break;
         default: launch_tc<40, 1, 2, 0>(qk, vt, O, rows, heads, C, P, st); break;
       }
       break;
     case 64:  // measured: NB=2 1.18× faster at d=64
-      if (attn_emu() == 0)
+      if (attn_emu() != 4)
         launch_tc<64, 2, 1, 0>(qk, vt, O, rows, heads, C, P, st);
       else
         launch_tc<64, 2, 1, 4>(qk, vt, O, rows, heads, C, P, st);
       break;
     case 80:
-      if (attn_emu() == 0)
+      if (attn_emu() != 4)
         launch_tc<80, 2, 1, 0>(qk, vt, O, rows, heads, C, P, st);
       else
         launch_tc<80, 2, 1, 4>(qk, vt, O, rows, heads, C, P, st);

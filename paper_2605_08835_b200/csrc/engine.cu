@@ -373,6 +373,9 @@ Engine::~Engine() {
   ws.release();
   if (kv_cache) cudaFree(kv_cache);
   if (aug_cache) cudaFree(aug_cache);
+  if (reg_scratch) cudaFree(reg_scratch);
+  if (time_ids) cudaFree(time_ids);
+  if (reg_ev) cudaEventDestroy(reg_ev);
   if (meta_dev) cudaFree(meta_dev);
   for (auto& kv : graphs)
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
@@ -381,6 +384,10 @@ Engine::~Engine() {
     if (meta_ev[i]) cudaEventDestroy(meta_ev[i]);
   }
   if (cap_stream) cudaStreamDestroy(cap_stream);
+}
+
+static size_t reg_emb_bytes(const Engine* e) {
+  return (((size_t)e->uc.ctx_len * e->uc.ctx_dim * e->esize) + 255) & ~size_t(255);
 }
 
 static size_t unet_ws_bytes(const Engine* e) {
@@ -423,6 +430,15 @@ void build_engine(Engine* e) {
     SD_CUDA(cudaMalloc(&e->aug_cache, (size_t)e->max_slots * e->uc.temb_dim() * sizeof(float)));
     SD_CUDA(cudaMemset(e->aug_cache, 0, (size_t)e->max_slots * e->uc.temb_dim() * sizeof(float)));
   }
+  {
+    const UNetCfg& c = e->uc;
+    const size_t extra = c.add_time_dim ? ((size_t)((c.add_in() + 127) & ~127) + c.temb_dim()) * e->esize : 0;
+    SD_CUDA(cudaMalloc(&e->reg_scratch, reg_emb_bytes(e) + extra + 256));
+    SD_CUDA(cudaEventCreateWithFlags(&e->reg_ev, cudaEventDisableTiming));
+    static const float ids[6] = {1024.f, 1024.f, 0.f, 0.f, 1024.f, 1024.f};  // R27 (orig, crop, target)
+    SD_CUDA(cudaMalloc(&e->time_ids, sizeof(ids)));
+    SD_CUDA(cudaMemcpy(e->time_ids, ids, sizeof(ids), cudaMemcpyHostToDevice));
+  }
   e->slot_used.assign(e->max_slots, 0);
   e->slot_used[0] = 1;
   e->meta_bytes = 64 << 10;
@@ -448,14 +464,10 @@ template <class AT>
 static void added_embedding(Engine* e, const float* pooled, int slot, cudaStream_t st) {
   const UNetCfg& c = e->uc;
   const int T = c.temb_dim(), K = c.add_in(), td = c.add_time_dim;
-  static const float ids[6] = {1024.f, 1024.f, 0.f, 0.f, 1024.f, 1024.f};  // R27
-  float* ids_dev;
-  AT *row, *hid;
-  SD_CUDA(cudaMallocAsync(&ids_dev, sizeof(ids), st));
-  SD_CUDA(cudaMallocAsync(&row, (size_t)K * sizeof(AT), st));
-  SD_CUDA(cudaMallocAsync(&hid, (size_t)T * sizeof(AT), st));
-  SD_CUDA(cudaMemcpyAsync(ids_dev, ids, sizeof(ids), cudaMemcpyHostToDevice, st));
-  timestep_sinusoid(ids_dev, 6, td, row, st);      // [6][td] = one row of 6·td
+  // scratch rows after the embedding copy (ctx_kv): [K] then [T], activation precision
+  AT* row = reinterpret_cast<AT*>(e->reg_scratch + reg_emb_bytes(e));
+  AT* hid = row + ((K + 127) & ~127);
+  timestep_sinusoid(e->time_ids, 6, td, row, st);  // [6][td] = one row of 6·td (R27 time ids)
   f32_to_act(pooled, row + 6 * td, c.pooled_dim, st);
   GemmDescT<AT> d;
   d.A = row;
@@ -483,15 +495,13 @@ static void added_embedding(Engine* e, const float* pooled, int slot, cudaStream
   d2.out_f32 = 1;
   d2.bias = e->U.add2_b;
   gemm(d2, st);
-  SD_CUDA(cudaFreeAsync(hid, st));
-  SD_CUDA(cudaFreeAsync(row, st));
-  SD_CUDA(cudaFreeAsync(ids_dev, st));
 }
 
 template <class AT>
 static void ctx_kv(Engine* e, const float* emb, int len, int dim, const float* pooled, int slot, cudaStream_t st) {
-  AT* tmp;
-  SD_CUDA(cudaMallocAsync(&tmp, (size_t)len * dim * sizeof(AT), st));
+  std::lock_guard<std::mutex> g(e->reg_mu);
+  if (e->reg_ev_valid) SD_CUDA(cudaStreamWaitEvent(st, e->reg_ev, 0));  // the previous user is done
+  AT* tmp = reinterpret_cast<AT*>(e->reg_scratch);
   f32_to_act(emb, tmp, (long)len * dim, st);
   GemmDescT<AT> d;
   d.A = tmp;
@@ -504,8 +514,9 @@ static void ctx_kv(Engine* e, const float* emb, int len, int dim, const float* p
   d.out = static_cast<AT*>(e->kv_cache) + (long)slot * e->slot_elems;
   d.ldo = e->U.kv_width;
   gemm(d, st);
-  SD_CUDA(cudaFreeAsync(tmp, st));
   if (e->uc.add_time_dim) added_embedding<AT>(e, pooled, slot, st);
+  SD_CUDA(cudaEventRecord(e->reg_ev, st));
+  e->reg_ev_valid = true;
 }
 
 int ctx_register(Engine* e, const float* emb, int len, int dim, const float* pooled, int pooled_dim, int slot,

@@ -172,6 +172,14 @@ struct Engine {
   // text K/V cache (activation precision)
   void* kv_cache = nullptr;
   float* aug_cache = nullptr;  // SDXL: [max_slots][T] added embedding per prompt slot (fp32)
+  // admission scratch (the activation-precision copy of a prompt embedding, the added-embedding
+  // rows, the constant time ids): reused by every sd_ctx_register; the event orders reuse across
+  // streams (no stream-ordered allocation on the admission path)
+  char* reg_scratch = nullptr;
+  float* time_ids = nullptr;
+  cudaEvent_t reg_ev = nullptr;
+  bool reg_ev_valid = false;
+  std::mutex reg_mu;
   int max_slots = 0;
   long slot_elems = 0;
   std::vector<int> slot_used;

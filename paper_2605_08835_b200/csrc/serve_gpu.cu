@@ -76,6 +76,7 @@ struct Server {
   int P = 0;
   float* pinned_noise = nullptr;
   float* pinned_emb = nullptr;
+  float* emb_dev = nullptr;  // device copy of one admission's embedding (+ pooled)
   // per-request buffers are recycled (cudaMalloc / cudaFree / cudaMallocHost in the loop would
   // stall it; cudaFree synchronises the whole device, i.e. the concurrent UNet round too)
   std::vector<float*> pool_lat, pool_img, pool_host;
@@ -116,12 +117,10 @@ void GpuExec::admit(STask* t) {
   memcpy(S->pinned_emb, t->emb.data(), t->emb.size() * 4);
   if (!t->pooled.empty()) memcpy(S->pinned_emb + t->emb.size(), t->pooled.data(), t->pooled.size() * 4);
   const size_t nf = t->emb.size() + t->pooled.size();
-  float* emb_dev;
-  SD_CUDA(cudaMallocAsync(&emb_dev, nf * 4, S->hi));
+  float* emb_dev = S->emb_dev;  // reused: admit ends with a stream synchronize
   SD_CUDA(cudaMemcpyAsync(emb_dev, S->pinned_emb, nf * 4, cudaMemcpyHostToDevice, S->hi));
   t->slot = ctx_register(e, emb_dev, t->emb_len, t->emb_dim, t->pooled.empty() ? nullptr : emb_dev + t->emb.size(),
                          (int)t->pooled.size(), -1, S->hi);
-  SD_CUDA(cudaFreeAsync(emb_dev, S->hi));
   SD_CUDA(cudaStreamSynchronize(S->hi));  // pinned staging is reused by the next admission
 }
 
@@ -255,6 +254,7 @@ extern "C" sd_status sd_serve_start(sd_engine* e, const sd_serve_config* cfg) {
   const size_t hw = (size_t)cfg->latent_hw * cfg->latent_hw;
   SD_CUDA(cudaMallocHost(&S->pinned_noise, 4 * hw * 4));
   SD_CUDA(cudaMallocHost(&S->pinned_emb, ((size_t)e->e.uc.ctx_len * e->e.uc.ctx_dim + e->e.uc.pooled_dim) * 4));
+  SD_CUDA(cudaMalloc(&S->emb_dev, ((size_t)e->e.uc.ctx_len * e->e.uc.ctx_dim + e->e.uc.pooled_dim) * 4));
   S->t0 = std::chrono::steady_clock::now();
   e->e.server = S;
   S->th = std::thread([S] { S->run(); });
@@ -361,6 +361,7 @@ extern "C" sd_status sd_serve_stop(sd_engine* e) {
   for (float* p : S->pool_host) cudaFreeHost(p);
   cudaFreeHost(S->pinned_noise);
   cudaFreeHost(S->pinned_emb);
+  cudaFree(S->emb_dev);
   cudaEventDestroy(S->ev_hi);
   cudaEventDestroy(S->ev_lo);
   cudaStreamDestroy(S->hi);
