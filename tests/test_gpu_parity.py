@@ -362,3 +362,41 @@ def test_sd15_bench_launch_config(sd15):
     for s in slots:
         eng.release(s)
     assert r_x <= TOL and r_eps <= TOL * kappa
+
+
+def test_sdxl_1024_full_size_properties():
+    """CFG#5 at its full size (SDXL-base, 1024², latent 128×128), where the oracle cannot run in seconds:
+    properties that hold at any size. (1) A ragged 2-request step (one CFG, one Skip-CFG; 3 UNet rows)
+    equals each request stepped alone, bitwise (I5). (2) The 1024² decode chunked into c = 4, 8, 16
+    work-item ranges equals the whole decode bitwise (I6, the paper's 4-16 chunk sweep). (3) Outputs
+    are finite and the decoded image is not constant."""
+    eng = Engine("sdxl", max_latent_hw=128, b_max=2, c_max=16)
+    try:
+        cfg = configs.SDXL_UNET
+        ctx_u = synth.uncond_embedding(0, cfg.ctx_len, cfg.ctx_dim)
+        pu = synth.uncond_pooled(0, cfg.pooled_dim)
+        eng.set_uncond(torch.from_numpy(ctx_u), torch.from_numpy(pu))
+        ctx = [synth.text_embedding(21, i, cfg.ctx_len, cfg.ctx_dim) for i in range(2)]
+        pooled = [synth.pooled_embedding(21, i, cfg.pooled_dim) for i in range(2)]
+        slots = [eng.register(torch.from_numpy(c), torch.from_numpy(p)) for c, p in zip(ctx, pooled)]
+        x0 = [synth.initial_noise(21, i, 128, 128) for i in range(2)]
+        lat = [torch.from_numpy(x).cuda() for x in x0]
+        steps, hu, g = [10, 40], [1, 0], [7.5, 7.5]
+        eng.step(lat, steps, [50, 50], hu, g, slots)
+        for i in range(2):
+            alone = [torch.from_numpy(x0[i]).cuda()]
+            eng.step(alone, [steps[i]], [50], [hu[i]], [g[i]], [slots[i]])
+            torch.cuda.synchronize()
+            assert torch.equal(alone[0], lat[i]), i
+            assert torch.isfinite(lat[i]).all()
+        whole = eng.decode(lat[0], 1)
+        torch.cuda.synchronize()
+        assert whole.shape == (3, 1024, 1024) and torch.isfinite(whole).all() and whole.std() > 1e-3
+        for c in (4, 8, 16):
+            ch = eng.decode(lat[0], c)
+            torch.cuda.synchronize()
+            assert torch.equal(ch, whole), c
+        for s in slots:
+            eng.release(s)
+    finally:
+        eng.close()

@@ -8,7 +8,7 @@ SD-1.5-shaped UNet + VAE at 512² (latent 64×64), B_max = 8, steps U{20..50}, g
      (sd_serve_start / sd_submit / sd_poll): images/s, mean and P99 E2E (R18);
   4. the same traces on the virtual clock (sd_serve_simulate on the measured table) beside them.
 
-  python tools/policy_sweep.py [--requests 48] [--rho 0.5 0.8 1.1] [--out profiles/r01/policy_sweep.json]
+  python tools/policy_sweep.py [--requests 48] [--rho 0.5 0.8 1.1 1.5] [--burst] [--out profiles/r01/policy_sweep.json]
 """
 import argparse
 import ctypes as C
@@ -55,7 +55,10 @@ def simulate(h, trace, policy, ablation, c_star, c_max):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--requests", type=int, default=48)
-    ap.add_argument("--rho", type=float, nargs="+", default=[0.5, 0.8, 1.1])
+    ap.add_argument("--rho", type=float, nargs="+", default=[0.5, 0.8, 1.1, 1.5])
+    ap.add_argument("--burst", action="store_true",
+                    help="also a burst trace: half the requests inside a window at 2·C₁ on a 0.5·C₁ background "
+                         "(PAPER.md:315 burst traffic)")
     ap.add_argument("--arms", nargs="+", default=list(ARMS))
     ap.add_argument("--out", default="profiles/r01/policy_sweep.json")
     args = ap.parse_args()
@@ -81,8 +84,12 @@ def main():
                         f"{args.requests} Poisson requests per load, λ = ρ·C₁",
                c1_images_per_s=c1, c_star=c_star, c_max=c_max,
                table={f"{k}": v for k, v in sorted(tab.items())}, loads={})
-    for rho in args.rho:
-        trace = serving.poisson_trace(args.requests, rho * c1, seed=7)
+    loads = [(str(rho), serving.poisson_trace(args.requests, rho * c1, seed=7)) for rho in args.rho]
+    if args.burst:
+        nb = args.requests // 2
+        loads.append(("burst", serving.burst_trace(args.requests, 0.5 * c1, frac=0.5,
+                                                   span_us=int(nb / (2.0 * c1) * 1e6), seed=7)))
+    for rho, trace in loads:
         row = {}
         for name in args.arms:
             pol, abl, chunk = ARMS[name]
@@ -94,7 +101,7 @@ def main():
             print(f"rho {rho}: {name:26s} {g['images_per_s']:.3f} img/s, mean {g['mean_e2e_ms']:.0f} ms, "
                   f"P99 {g['p99_e2e_ms']:.0f} ms, skips {g['skipped_steps']} | sim {sim['images_per_s']:.3f} img/s, "
                   f"mean {sim['mean_e2e_ms']:.0f}, P99 {sim['p99_e2e_ms']:.0f} ({time.time() - t1:.0f} s)", flush=True)
-        res["loads"][str(rho)] = row
+        res["loads"][rho] = row
     B.lib().sd_table_free(h)
     eng.close()
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
