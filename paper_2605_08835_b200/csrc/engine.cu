@@ -374,6 +374,7 @@ Engine::~Engine() {
   if (kv_cache) cudaFree(kv_cache);
   if (aug_cache) cudaFree(aug_cache);
   if (reg_scratch) cudaFree(reg_scratch);
+  if (gn_ws) cudaFree(gn_ws);
   if (time_ids) cudaFree(time_ids);
   if (reg_ev) cudaEventDestroy(reg_ev);
   if (meta_dev) cudaFree(meta_dev);
@@ -421,6 +422,11 @@ void build_engine(Engine* e) {
   SD_CUDA(cudaStreamSynchronize(st));
   SD_CUDA(cudaStreamDestroy(st));
   e->ws.init(unet_ws_bytes(e));
+  {
+    const size_t gb = gn_workspace_bytes(e->max_rows, e->cfg.max_latent_hw * e->cfg.max_latent_hw * 4, 64, 4096);
+    SD_CUDA(cudaMalloc(&e->gn_ws, gb));
+    SD_CUDA(cudaMemset(e->gn_ws, 0, gb));
+  }
   // text K/V cache slots (slot 0 = unconditional)
   e->max_slots = 4 * e->cfg.b_max + 8;
   e->slot_elems = (long)e->uc.ctx_len * e->U.kv_width;
@@ -735,7 +741,7 @@ static void unet_forward(Engine* e, cudaStream_t st, int R, int H, int W, const 
   const UNetCfg& c = e->uc;
   UNetW& U = e->U;
   Fwd<AT> f{e, st, R, nullptr, kv_index, nullptr};
-  f.gn_ws = e->ws.alloc(gn_workspace_bytes(R, H * W * 4, 64, 4096) + (1 << 20));
+  f.gn_ws = e->gn_ws;
   const int T = c.temb_dim(), C0 = c.block_out[0];
   // time embedding: sinusoid → linear_1 → SiLU → linear_2 → SiLU (the ResBlocks consume SiLU(temb))
   AT* sinus = f.buf((long)R * C0);

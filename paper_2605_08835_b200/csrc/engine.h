@@ -176,6 +176,7 @@ struct Engine {
   // rows, the constant time ids): reused by every sd_ctx_register; the event orders reuse across
   // streams (no stream-ordered allocation on the admission path)
   char* reg_scratch = nullptr;
+  void* gn_ws = nullptr;  // UNet GroupNorm workspace (partials + affine table), persistent
   float* time_ids = nullptr;
   cudaEvent_t reg_ev = nullptr;
   bool reg_ev_valid = false;

@@ -6,12 +6,15 @@
 //                sums: thread (v, r) of a block always owns channel vector v and issues 8 independent
 //                16-byte loads per batch; one warp per group then reduces the block's rows and
 //                channels in a fixed order.
-//   gn_finalize  one warp per (image, group) merges the chunk partials in fixed order (Chan et al.)
-//                and writes the per-(image, channel) affine table scale = γ·rstd, shift = β − μ·scale.
-//   gn_apply     a flat, coalesced elementwise pass y = x·scale + shift (+SiLU): 4 independent
-//                vectors in flight per thread, the table read from L1/L2.
+//   merge        one warp per (image, group) merges the chunk partials in fixed order (Chan et al.)
+//                and writes the per-(image, channel) affine table scale = γ·rstd, shift = β − μ·scale;
+//                (gn_finalize launch).
+//   gn_apply     y = x·scale + shift (+SiLU): each thread owns one channel vector (its table entries
+//                stay in registers), 4 pixel rows in flight per thread, grid-stride.
 // The reduction order depends only on (P, C, G) — never on the batch (I5) or on banding (I6).
 // Chunk size adapts to C (≈ 40 K elements per chunk).
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels_ew.h"
 
@@ -56,7 +59,58 @@ struct Raw8<float> {
   }
 };
 
+// Chan merge of one (image, group)'s chunk partials by one warp (weights by the fast MUFU division:
+// the merge is a latency chain, and every path uses this same function, so results stay bitwise
+// consistent across batch sizes, bands and launch paths): lane l merges chunks l, l+32, …
+// sequentially, then a fixed butterfly in which both partners compute the identical value —
+// deterministic, independent of which block runs it. Writes the group's affine table entries
+// (scale = γ·rstd, shift = β − μ·scale). Partials are read through L2 (written by other SMs).
+__device__ __forceinline__ void gn_merge_group(int P, int C, int G, int chunk_px, int nchunks,
+                                               const GNPart* __restrict__ part, float eps,
+                                               const float* __restrict__ gamma, const float* __restrict__ beta,
+                                               float2* __restrict__ tab, int b, int g, int lane) {
+  const int cg = C / G;
+  float n = 0.f, mean = 0.f, m2 = 0.f;
+  for (int k = lane; k < nchunks; k += 32) {
+    const float2 pp = __ldcg(reinterpret_cast<const float2*>(part + ((long)b * nchunks + k) * G + g));
+    const float nb = (float)(min(P, (k + 1) * chunk_px) - k * chunk_px) * cg;
+    const float tot = n + nb;
+    const float d = pp.x - mean;
+    const float w = __fdividef(nb, tot);
+    mean += d * w;
+    m2 += pp.y + d * d * (n * w);
+    n = tot;
+  }
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const float n2 = __shfl_xor_sync(0xffffffff, n, o);
+    const float mu2 = __shfl_xor_sync(0xffffffff, mean, o);
+    const float q2 = __shfl_xor_sync(0xffffffff, m2, o);
+    const bool lo = (lane & o) == 0;  // lower lane first: both partners compute the identical value
+    const float na = lo ? n : n2, ma = lo ? mean : mu2, qa = lo ? m2 : q2;
+    const float nb = lo ? n2 : n, mb = lo ? mu2 : mean, qb = lo ? q2 : m2;
+    const float tot = na + nb;
+    if (tot > 0.f) {
+      const float d = mb - ma;
+      const float w = __fdividef(nb, tot);
+      mean = ma + d * w;
+      m2 = qa + qb + d * d * (na * w);
+    } else {
+      mean = 0.f;
+      m2 = 0.f;
+    }
+    n = tot;
+  }
+  const float rstd = rsqrtf(m2 / n + eps);
+  for (int c = g * cg + lane; c < (g + 1) * cg; c += 32) {
+    const float sc = gamma[c] * rstd;  // y = x·(γ·rstd) + (β − mean·γ·rstd)
+    tab[(long)b * C + c] = make_float2(sc, beta[c] - mean * sc);
+  }
+}
+
 // block (V, R): V = C/8 vector lanes, R pixel rows; grid (chunks in range, B)
+// (measured: merging in the last-arriving stats block instead of a finalize launch serialises the
+// 32 group merges on one block — 2.1 vs 1.8 ms of GN per 16-row SD-1.5 step)
 template <class T>
 __global__ void __launch_bounds__(512) gn_stats_kernel(const T* __restrict__ x, int P, int C, int G, int chunk_px,
                                                        int c_base, int nch_total, GNPart* __restrict__ part) {
@@ -69,7 +123,7 @@ __global__ void __launch_bounds__(512) gn_stats_kernel(const T* __restrict__ x, 
 #pragma unroll
   for (int i = 0; i < 8; ++i) s[i] = q[i] = 0.f;
   const T* xb = x + (long)b * P * C + v * 8;
-  for (int p = p0 + ry; p < p1; p += 8 * R) {  // 8 independent vector loads in flight
+  for (int p = p0 + ry; p < p1; p += 8 * R) {
     // unconditional loads from clamped rows (the compiler keeps all 8 in flight); rows past the
     // chunk are masked out afterwards
     Raw8<T> u[8];
@@ -124,8 +178,7 @@ __global__ void __launch_bounds__(512) gn_stats_kernel(const T* __restrict__ x, 
   }
 }
 
-// finalize: one warp per (image, group): lane l merges chunks l, l+32, … sequentially, then a fixed
-// butterfly (Chan) — deterministic; writes the affine table (scale, shift) of the group's channels
+// finalize: one warp per (image, group)
 __global__ void gn_finalize_kernel(int P, int C, int G, int chunk_px, int nchunks, const GNPart* __restrict__ part,
                                    float eps, const float* __restrict__ gamma, const float* __restrict__ beta,
                                    float2* __restrict__ tab) {
@@ -133,80 +186,58 @@ __global__ void gn_finalize_kernel(int P, int C, int G, int chunk_px, int nchunk
   const int g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int b = blockIdx.y;
   if (g >= G) return;
-  const int cg = C / G;
-  float n = 0.f, mean = 0.f, m2 = 0.f;
-  for (int k = lane; k < nchunks; k += 32) {
-    const GNPart pp = part[((long)b * nchunks + k) * G + g];
-    const float nb = (float)(min(P, (k + 1) * chunk_px) - k * chunk_px) * cg;
-    const float tot = n + nb;
-    const float d = pp.mean - mean;
-    mean += d * (nb / tot);
-    m2 += pp.m2 + d * d * (n * nb / tot);
-    n = tot;
-  }
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const float n2 = __shfl_xor_sync(0xffffffff, n, o);
-    const float mu2 = __shfl_xor_sync(0xffffffff, mean, o);
-    const float q2 = __shfl_xor_sync(0xffffffff, m2, o);
-    const bool lo = (lane & o) == 0;  // lower lane first: both partners compute the identical value
-    const float na = lo ? n : n2, ma = lo ? mean : mu2, qa = lo ? m2 : q2;
-    const float nb = lo ? n2 : n, mb = lo ? mu2 : mean, qb = lo ? q2 : m2;
-    const float tot = na + nb;
-    if (tot > 0.f) {
-      const float d = mb - ma;
-      mean = ma + d * (nb / tot);
-      m2 = qa + qb + d * d * (na * nb / tot);
-    } else {
-      mean = 0.f;
-      m2 = 0.f;
-    }
-    n = tot;
-  }
-  const float rstd = rsqrtf(m2 / n + eps);
-  for (int c = g * cg + lane; c < (g + 1) * cg; c += 32) {
-    const float sc = gamma[c] * rstd;  // y = x·(γ·rstd) + (β − mean·γ·rstd)
-    tab[(long)b * C + c] = make_float2(sc, beta[c] - mean * sc);
-  }
+  gn_merge_group(P, C, G, chunk_px, nchunks, part, eps, gamma, beta, tab, b, g, lane);
 }
 
-// apply: flat over the 8-element vectors [v_begin, v_end) of x viewed as [B·P][C/8]; each thread
-// handles 4 vectors blockDim apart (coalesced), all loads issued before any math
+// apply over pixels [p_begin, p_end) of x viewed as [B·P][V vectors of 8]: block (V, R); thread
+// (v, r) always owns channel vector v, so its 8 (scale, shift) pairs stay in registers (reloaded
+// only when its pixel crosses into the next image); U pixel rows per thread per iteration, all
+// loads issued before any math; grid-stride over blocks of R·U pixels.
 template <class T>
-__global__ void __launch_bounds__(256) gn_apply_kernel(const T* __restrict__ x, long v_begin, long v_end, int P, int V,
+__global__ void __launch_bounds__(512) gn_apply_kernel(const T* __restrict__ x, long p_begin, long p_end, int P, int V,
                                                        const float2* __restrict__ tab, int silu, T* __restrict__ y) {
   constexpr int U = 4;
-  const long base = v_begin + (long)blockIdx.x * blockDim.x * U + threadIdx.x;
-  Raw8<T> u[U];
+  const int v = threadIdx.x, R = blockDim.y;
+  int b_cur = -1;
+  float sc[8], sf[8];
+  for (long pb = p_begin + (long)blockIdx.x * R * U + threadIdx.y; pb < p_end; pb += (long)gridDim.x * R * U) {
+    Raw8<T> u[U];
 #pragma unroll
-  for (int k = 0; k < U; ++k) u[k].ld(x + min(base + (long)k * blockDim.x, v_end - 1) * 8);  // all in flight
+    for (int k = 0; k < U; ++k) u[k].ld(x + (min(pb + (long)k * R, p_end - 1) * V + v) * 8);
 #pragma unroll
-  for (int k = 0; k < U; ++k) {
-    const long i = base + (long)k * blockDim.x;
-    if (i >= v_end) break;
-    const unsigned pix = (unsigned)i / (unsigned)V;  // < 2^31 vectors per launch (checked on the host)
-    const int vc = (int)((unsigned)i - pix * (unsigned)V);
-    const int b = (int)(pix / (unsigned)P);
-    const float4* t4 = reinterpret_cast<const float4*>(tab + (long)b * V * 8 + vc * 8);
-    float f[8], o[8];
-    u[k].get(f);
+    for (int k = 0; k < U; ++k) {
+      const long p = pb + (long)k * R;
+      if (p >= p_end) break;
+      const int b = (int)((unsigned)p / (unsigned)P);  // < 2^31 pixels (checked on the host)
+      if (b != b_cur) {
+        const float4* t4 = reinterpret_cast<const float4*>(tab + ((long)b * V + v) * 8);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float4 t = __ldg(t4 + j);  // (scale, shift) of channels 2j, 2j+1
-      const float a0 = f[2 * j] * t.x + t.y, a1 = f[2 * j + 1] * t.z + t.w;
-      o[2 * j] = silu ? silu_f(a0) : a0;
-      o[2 * j + 1] = silu ? silu_f(a1) : a1;
+        for (int j = 0; j < 4; ++j) {
+          const float4 t = __ldg(t4 + j);
+          sc[2 * j] = t.x, sf[2 * j] = t.y, sc[2 * j + 1] = t.z, sf[2 * j + 1] = t.w;
+        }
+        b_cur = b;
+      }
+      float f[8], o[8];
+      u[k].get(f);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float a = f[j] * sc[j] + sf[j];
+        o[j] = silu ? silu_f(a) : a;
+      }
+      store8(y + (p * V + v) * 8, o);
     }
-    store8(y + i * 8, o);
   }
 }
 
+// workspace: [partials] [affine table]
 static size_t gn_part_bytes(int B, int P, int G) {
   return ((size_t)B * cdiv(P, 16) * G * sizeof(GNPart) + 255) & ~size_t(255);
 }
 size_t gn_workspace_bytes(int B, int P, int G, int C) {
   return gn_part_bytes(B, P, G) + (size_t)B * C * sizeof(float2) + 256;
 }
+static GNPart* gn_parts(void* ws) { return reinterpret_cast<GNPart*>(ws); }
 static float2* gn_tab(void* ws, int B, int P, int G) {
   return reinterpret_cast<float2*>(reinterpret_cast<char*>(ws) + gn_part_bytes(B, P, G));
 }
@@ -214,20 +245,25 @@ static float2* gn_tab(void* ws, int B, int P, int G) {
 static void gn_finalize(int B, int P, int C, int G, int cp, void* ws, float eps, const float* gamma, const float* beta,
                         cudaStream_t st) {
   const int wpb = 4;  // warps per block
-  gn_finalize_kernel<<<dim3(cdiv(G, wpb), B), 32 * wpb, 0, st>>>(
-      P, C, G, cp, cdiv(P, cp), reinterpret_cast<const GNPart*>(ws), eps, gamma, beta, gn_tab(ws, B, P, G));
+  gn_finalize_kernel<<<dim3(cdiv(G, wpb), B), 32 * wpb, 0, st>>>(P, C, G, cp, cdiv(P, cp), gn_parts(ws), eps, gamma,
+                                                                  beta, gn_tab(ws, B, P, G));
   SD_CHECK_LAUNCH();
 }
 
 template <class T>
-static void gn_apply(const T* x, T* y, long v0, long v1, int P, int C, const float2* tab, bool silu,
+static void gn_apply(const T* x, T* y, long p0, long p1, int B, int P, int C, const float2* tab, bool silu,
                      cudaStream_t st) {
-  const int threads = 256;
-  const long n = v1 - v0;
-  if (n <= 0) return;
-  if (v1 >= (1L << 31)) throw CudaError("group_norm: tensor too large");
-  gn_apply_kernel<T><<<cdiv(n, threads * 4), threads, 0, st>>>(x, v0, v1, P, C / 8, tab, silu ? 1 : 0, y);
+  if (p1 <= p0) return;
+  if (p1 >= (1L << 31)) throw CudaError("group_norm: tensor too large");
+  const dim3 blk = gn_stats_block(C);
+  const long rows = (long)blk.y * 4;
+  static int sms = 0;
+  if (!sms) SD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  const long want = (p1 - p0 + rows - 1) / rows;
+  const int grid = (int)std::min<long>(want, (long)sms * (2048 / (blk.x * blk.y)));
+  gn_apply_kernel<T><<<grid, blk, 0, st>>>(x, p0, p1, P, C / 8, tab, silu ? 1 : 0, y);
   SD_CHECK_LAUNCH();
+  (void)B;
 }
 
 static void check_gn(int C, int G) {
@@ -239,7 +275,7 @@ static void gn_stats(const T* x, int B, int P, int C, int G, int c0, int c1, voi
   const int cp = gn_chunk_px(C);
   const dim3 blk = gn_stats_block(C);
   const size_t sh = (size_t)blk.x * blk.y * 8 * 2 * sizeof(float);
-  gn_stats_kernel<<<dim3(c1 - c0, B), blk, sh, st>>>(x, P, C, G, cp, c0, cdiv(P, cp), reinterpret_cast<GNPart*>(ws));
+  gn_stats_kernel<<<dim3(c1 - c0, B), blk, sh, st>>>(x, P, C, G, cp, c0, cdiv(P, cp), gn_parts(ws));
   SD_CHECK_LAUNCH();
 }
 
@@ -258,7 +294,7 @@ void gn_apply_range(const T* x, T* y, int P, int C, int G, int p0, int p1, const
   check_gn(C, G);
   const int cp = gn_chunk_px(C);
   if (p0 == 0) gn_finalize(1, P, C, G, cp, ws, eps, gamma, beta, st);  // bands run in order
-  gn_apply(x, y, (long)p0 * (C / 8), (long)p1 * (C / 8), P, C, gn_tab(ws, 1, P, G), silu, st);
+  gn_apply(x, y, p0, p1, 1, P, C, gn_tab(ws, 1, P, G), silu, st);
 }
 
 template <class T>
@@ -268,7 +304,7 @@ void group_norm(const T* x, T* y, int B, int P, int C, int G, const float* gamma
   const int cp = gn_chunk_px(C);
   gn_stats(x, B, P, C, G, 0, cdiv(P, cp), ws, st);
   gn_finalize(B, P, C, G, cp, ws, eps, gamma, beta, st);
-  gn_apply(x, y, 0, (long)B * P * (C / 8), P, C, gn_tab(ws, B, P, G), silu, st);
+  gn_apply(x, y, 0, (long)B * P, B, P, C, gn_tab(ws, B, P, G), silu, st);
 }
 
 // ---- LayerNorm: LANES lanes per token (NV 16-byte vectors each), two-pass in registers ----------

@@ -397,6 +397,7 @@ static DecodeState* new_decode(Engine* e, int h, int w) {
   for (int i = 0; i < NBUF; ++i) s->buf[i] = s->ar.alloc(s->buf_elems * e->esize);
   s->img_nhwc = s->ar.get<float>(64 * P * 3);
   s->gn_ws = s->ar.alloc(gnb);
+
   build_items(e, s);
   return s;
 }
