@@ -259,6 +259,10 @@ sd_status sd_debug_layernorm(const void* x, void* y, int32_t T, int32_t C, const
                              float eps, void* stream);
 /* GEMM tile mode for the tests: 0 = heuristic, 1 = 128-row CTA tiles, 2 = 256-row CTA-pair tiles. */
 sd_status sd_debug_set_gemm_cg(int32_t cg);
+/* 3x3 / stride 2 / pad 1 conv (the UNet downsamplers) by TMA boxes with element stride 2: x bf16
+ * [nb][h_in][w_in][cin] (h_in, w_in even), weights bf16 [cout][9][cin], y bf16 [nb][h_in/2][w_in/2][cout]. */
+sd_status sd_debug_conv3x3_s2(const void* x, int32_t cin, const void* w, const float* bias, void* y, int32_t nb,
+                              int32_t h_in, int32_t w_in, int32_t cout, void* stream);
 /* split-K of sd_debug_conv3x3: 0 = the production rule (conv layers of <= 64 pixels with >= 90 K
  * blocks of 64 channels take 3 splits), 1 = off, 2..8 = forced; partials summed in split order. */
 sd_status sd_debug_set_conv_splits(int32_t splits);

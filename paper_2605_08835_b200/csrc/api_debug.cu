@@ -85,6 +85,29 @@ extern "C" sd_status sd_debug_conv3x3(const void* x, int32_t cin, const void* x2
   SD_API_END
 }
 
+extern "C" sd_status sd_debug_conv3x3_s2(const void* x, int32_t cin, const void* w, const float* bias, void* y,
+                                         int32_t nb, int32_t h_in, int32_t w_in, int32_t cout, void* stream) {
+  SD_REQUIRE(x && w && y && cin > 0 && cout > 0 && nb > 0 && h_in > 0 && w_in > 0 && h_in % 2 == 0 && w_in % 2 == 0,
+             "sd_debug_conv3x3_s2: bad arguments");
+  SD_API_BEGIN
+  sd::GemmDesc d;
+  d.mode = sd::GEMM_CONV3;
+  d.stride = 2;
+  d.xs[0] = static_cast<const bf16*>(x);
+  d.cs[0] = cin;
+  d.Bw[0] = static_cast<const bf16*>(w);
+  d.B = nb;
+  d.H = h_in / 2;
+  d.W = w_in / 2;
+  d.N = cout;
+  d.out = y;
+  d.ldo = cout;
+  d.bias = bias;
+  d.splits = 1;
+  sd::gemm(d, static_cast<cudaStream_t>(stream));
+  SD_API_END
+}
+
 extern "C" sd_status sd_debug_set_conv_splits(int32_t splits) {
   SD_REQUIRE(splits >= 0 && splits <= 8, "sd_debug_set_conv_splits: 0 (auto), 1 (off) or 2..8");
   g_dbg_splits = splits;

@@ -9,26 +9,31 @@ namespace sd {
 // K11: UNet input rows. Row ρ belongs to request r = row_req[ρ]; writes T(c_in_r · x_r) NHWC
 // with channels [4, cpad) zero.  (R26 row order is encoded in row_req.)
 // T = bf16 on the product path, float in the fp32 parity mode (R19); likewise below.
+// one thread per (pixel, 8-channel vector): vector 0 carries the 4 latent channels, the rest of the
+// cpad-channel row is zero; 16/32-byte stores
 template <class T>
-__global__ void gather_rows_kernel(RowMap m, int rows, int hw, int cpad, T* __restrict__ out) {
-  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;  // one pixel of one row
-  if (i >= (long)rows * hw) return;
-  const int rho = (int)(i / hw), p = (int)(i % hw);
-  const int r = m.row_req[rho];
-  const float* x = m.latents[r];
-  const float c = m.c_in[r];
-  T* o = out + i * cpad;
-  act_st(o + 0, c * x[p]);
-  act_st(o + 1, c * x[hw + p]);
-  act_st(o + 2, c * x[2 * hw + p]);
-  act_st(o + 3, c * x[3 * hw + p]);
-  for (int k = 4; k < cpad; ++k) act_st(o + k, 0.f);
+__global__ void gather_rows_kernel(RowMap m, int rows, int hw, int nv, T* __restrict__ out) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;  // (pixel of a row, vector)
+  if (i >= (long)rows * hw * nv) return;
+  const long px = i / nv;
+  const int v = (int)(i - px * nv);
+  float o[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (v == 0) {
+    const int rho = (int)(px / hw), p = (int)(px % hw);
+    const int r = m.row_req[rho];
+    const float* x = m.latents[r];
+    const float c = m.c_in[r];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) o[k] = c * x[(long)k * hw + p];
+  }
+  store8(out + i * 8, o);
 }
 
 template <class T>
 void gather_rows(const RowMap& m, int rows, int hw, int cpad, T* out, cudaStream_t st) {
-  const long n = (long)rows * hw;
-  gather_rows_kernel<T><<<cdiv(n, 256), 256, 0, st>>>(m, rows, hw, cpad, out);
+  if (cpad % 8) throw CudaError("gather_rows: cpad must be a multiple of 8");
+  const long n = (long)rows * hw * (cpad / 8);
+  gather_rows_kernel<T><<<cdiv(n, 256), 256, 0, st>>>(m, rows, hw, cpad / 8, out);
   SD_CHECK_LAUNCH();
 }
 

@@ -597,10 +597,13 @@ struct Fwd {
     gemm(d, st);
     e->prof.end(pi, st);
   }
+  // 3×3 conv, pad 1; H × W is the OUTPUT size (the input is stride·H × stride·W)
   void conv(const AT* x, int H, int W, int C, const AT* w, int N, const float* bias, void* out,
-            const float* temb = nullptr, const AT* res = nullptr, int out_f32 = 0, int ldo = 0, int c_real = 0) {
+            const float* temb = nullptr, const AT* res = nullptr, int out_f32 = 0, int ldo = 0, int c_real = 0,
+            int stride = 1) {
     GemmDescT<AT> d;
     d.mode = GEMM_CONV3;
+    d.stride = stride;
     d.xs[0] = x;
     d.cs[0] = C;
     d.B = R;
@@ -800,9 +803,16 @@ static void unet_forward(Engine* e, cudaStream_t st, int R, int H, int W, const 
       const size_t mk = e->ws.mark();
       AT* out = f.buf((long)R * ho * wo * C);
       const size_t mk2 = e->ws.mark();
-      AT* cols = f.buf((long)R * ho * wo * 9 * C);
-      im2col_s2(x, cols, R, h, w, C, st);
-      f.linear(cols, (long)R * ho * wo, 9 * C, wt<AT>(d.wdown), C, d.bdown, out, C);
+      if constexpr (std::is_same<AT, bf16>::value) {
+        // 3×3 / stride 2 / pad 1 as an implicit GEMM whose TMA boxes step 2 input pixels per output
+        // pixel (element strides), so the taps are never materialised
+        if (h % 2 || w % 2) throw std::invalid_argument("downsampler: odd spatial size");
+        f.conv(x, ho, wo, C, wt<AT>(d.wdown), C, d.bdown, out, nullptr, nullptr, 0, 0, 0, 2);
+      } else {
+        AT* cols = f.buf((long)R * ho * wo * 9 * C);
+        im2col_s2(x, cols, R, h, w, C, st);
+        f.linear(cols, (long)R * ho * wo, 9 * C, wt<AT>(d.wdown), C, d.bdown, out, C);
+      }
       e->ws.reset(mk2);
       (void)mk;
       x = out;

@@ -201,7 +201,7 @@ void gemm(const GemmDescF& d, cudaStream_t st) {
     g.K = d.K;
     g.ldb = d.ldb ? d.ldb : d.K;
   } else {
-    if (d.nsrc != 1) throw CudaError("fp32 conv3: one source only");
+    if (d.nsrc != 1 || d.stride != 1) throw CudaError("fp32 conv3: one source, stride 1");
     g.x = d.xs[0];
     g.Cin = d.cs[0];
     g.B = d.B;

@@ -27,6 +27,7 @@ struct GemmArgs {
   int mode;
   int M, N;
   int B, H, W, wt, ht, bt, tiles_x, tiles_y;
+  int stride;         // conv3: input pixel = stride·output pixel + tap offset
   int kb_src[2];      // K blocks (of 64 channels) per tap for each source
   int nsrc;
   int num_kb;         // K blocks per tile
@@ -523,7 +524,7 @@ __global__ void __launch_bounds__(320, 1)
             const int dy = tap / 3 - 1, dx = tap % 3 - 1;
             const CUtensorMap* ma = src ? &ta1 : &ta0;
             const CUtensorMap* mb = src ? &tb1 : &tb0;
-            tma4<CG>(dA, ma, &full[stage], bar_l, cb * C::BK, x0 + dx, y0 + dy, b0);
+            tma4<CG>(dA, ma, &full[stage], bar_l, cb * C::BK, g.stride * x0 + dx, g.stride * y0 + dy, b0);
             tma3<CG>(dB, mb, &full[stage], bar_l, cb * C::BK, tap, n0);
           }
           if (++stage == C::STAGES) {
@@ -624,13 +625,14 @@ static EncodeTiledFn encode_fn() {
 }
 
 static void make_map(CUtensorMap* m, const void* ptr, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
-                     const uint32_t* box, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+                     const uint32_t* box, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B,
+                     const uint32_t* elem_strides = nullptr) {
   cuuint64_t gd[5], gs[5];
   cuuint32_t bx[5], es[5];
   for (int i = 0; i < rank; ++i) {
     gd[i] = dims[i];
     bx[i] = box[i];
-    es[i] = 1;
+    es[i] = elem_strides ? elem_strides[i] : 1;
     if (i + 1 < rank) gs[i] = strides_bytes[i];
   }
   CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), gd, gs, bx, es,
@@ -807,9 +809,11 @@ void gemm(const GemmDesc& d, cudaStream_t st) {
     a.num_kb = cdiv(d.K, 64);
     a.nsrc = 1;
   } else {
+    if (d.stride != 1 && (d.stride != 2 || d.nsrc != 1)) throw CudaError("conv3: stride 1, or 2 with one source");
     a.B = d.B;
     a.H = d.H;
     a.W = d.W;
+    a.stride = d.stride;
     a.M = d.B * d.H * d.W;
     conv3_tile_geometry(d.B, d.H, d.W, &a.wt, &a.ht, &a.bt);
     a.tiles_x = cdiv(d.W, a.wt);
@@ -862,11 +866,14 @@ void gemm(const GemmDesc& d, cudaStream_t st) {
     maps[1] = maps[0];
     maps[3] = maps[2];
   } else {
+    const int sd = d.stride;  // stride 2: the box spans 2·wt × 2·ht input pixels, every second one loaded
+    const uint64_t Wi = (uint64_t)d.W * sd, Hi = (uint64_t)d.H * sd;
     for (int s = 0; s < d.nsrc; ++s) {
-      uint64_t dA[4] = {(uint64_t)d.cs[s], (uint64_t)d.W, (uint64_t)d.H, (uint64_t)d.B};
-      uint64_t sA[3] = {(uint64_t)d.cs[s] * 2, (uint64_t)d.cs[s] * 2 * d.W, (uint64_t)d.cs[s] * 2 * d.W * d.H};
-      uint32_t bA[4] = {64, (uint32_t)a.wt, (uint32_t)a.ht, (uint32_t)a.bt};
-      make_map(&maps[s], d.xs[s], 4, dA, sA, bA);
+      uint64_t dA[4] = {(uint64_t)d.cs[s], Wi, Hi, (uint64_t)d.B};
+      uint64_t sA[3] = {(uint64_t)d.cs[s] * 2, (uint64_t)d.cs[s] * 2 * Wi, (uint64_t)d.cs[s] * 2 * Wi * Hi};
+      uint32_t bA[4] = {64, (uint32_t)(a.wt * sd), (uint32_t)(a.ht * sd), (uint32_t)a.bt};
+      uint32_t eA[4] = {1, (uint32_t)sd, (uint32_t)sd, 1};
+      make_map(&maps[s], d.xs[s], 4, dA, sA, bA, CU_TENSOR_MAP_SWIZZLE_128B, eA);
       uint64_t dB[3] = {(uint64_t)d.cs[s], 9, (uint64_t)d.N};
       uint64_t sB[2] = {(uint64_t)d.cs[s] * 2, (uint64_t)d.cs[s] * 2 * 9};
       uint32_t bB[3] = {64, 1, brows};

@@ -32,7 +32,9 @@ struct GemmDescT {
   int nsrc = 1;
   const T* xs[2] = {nullptr, nullptr};
   int cs[2] = {0, 0};
-  int B = 0, H = 0, W = 0;
+  int B = 0, H = 0, W = 0;   // conv3: batch and OUTPUT spatial size
+  int stride = 1;            // conv3: 1, or 2 (input 2H×2W, pad 1: the UNet downsamplers) — tcgen05 kernel only;
+                             // the taps are read by TMA boxes with element strides 2 (no im2col)
   const T* Bw[2] = {nullptr, nullptr};
   int N = 0, ldb = 0;
   void* out = nullptr;

@@ -91,6 +91,23 @@ def test_conv3x3(nb, h, w, cin, cout):
     assert rel(y.cpu(), ref) < 6e-3
 
 
+@pytest.mark.parametrize("nb,h,w,cin,cout", [(16, 64, 64, 320, 320), (16, 32, 32, 640, 640), (2, 16, 16, 1280, 1280),
+                                             (3, 12, 20, 64, 128), (1, 8, 8, 320, 64)])
+def test_conv3x3_stride2(nb, h, w, cin, cout):
+    """The UNet downsampler (3×3, stride 2, pad 1) read by TMA boxes with element stride 2 — no
+    im2col — against torch conv2d in fp64 (h, w = input size)."""
+    g = torch.Generator().manual_seed(nb * 7 + h + cin)
+    x = bf(torch.randn(nb, h, w, cin, generator=g))
+    wt = bf(torch.randn(cout, cin, 3, 3, generator=g) / (9 * cin) ** 0.5)
+    b = torch.randn(cout, generator=g)
+    ref = F.conv2d(x.double().permute(0, 3, 1, 2), wt.double(), b.double(), stride=2, padding=1).permute(0, 2, 3, 1)
+    y = torch.empty(nb, h // 2, w // 2, cout, device="cuda", dtype=torch.bfloat16)
+    xd, wd, bd = x.cuda(), _to_dev_w(wt), b.cuda()
+    B.call("sd_debug_conv3x3_s2", B._p(xd), cin, B._p(wd), B._p(bd), B._p(y), nb, h, w, cout, None)
+    torch.cuda.synchronize()
+    assert rel(y.cpu(), ref) < 6e-3
+
+
 @pytest.mark.parametrize("splits", [2, 3, 5])
 @pytest.mark.parametrize("nb,h,w,c1,c2,cout", [(3, 5, 7, 200, 0, 100), (4, 8, 8, 640, 640, 320), (2, 8, 8, 1280, 0, 1280)])
 def test_conv3x3_splitk(splits, nb, h, w, c1, c2, cout):
