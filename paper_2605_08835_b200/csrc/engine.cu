@@ -628,20 +628,51 @@ struct Fwd {
     e->ws.reset(mk);
   }
 
-  AT* resblock(const ResW& r, const AT* x, int H, int W) {
+  // x1 != nullptr: the block's input is the channel concat [x (C0 = r.cin − C1) | x1 (C1)] (up blocks),
+  // read by the two-source GroupNorm and shortcut GEMM instead of being materialised
+  AT* resblock(const ResW& r, const AT* x, int H, int W, const AT* x1 = nullptr, int C1 = 0) {
     const int P = H * W;
     const size_t mk = e->ws.mark();
     AT* out = buf((long)R * P * r.cout);  // allocated below the scratch mark
     const size_t mk2 = e->ws.mark();
     (void)mk;
     AT* a = buf((long)R * P * r.cin);
-    gn(x, a, P, r.cin, r.n1g, r.n1b, e->uc.eps_res, true);
+    if (x1) {
+      if (!r.wsc) throw std::logic_error("two-source resblock needs the 1x1 shortcut");
+      const int pi = e->prof.begin(PC_GN, st, 3.0 * R * P * r.cin * 2);
+      group_norm2(x, r.cin - C1, x1, C1, a, R, P, e->uc.groups, r.n1g, r.n1b, e->uc.eps_res, true, gn_ws, st);
+      e->prof.end(pi, st);
+    } else {
+      gn(x, a, P, r.cin, r.n1g, r.n1b, e->uc.eps_res, true);
+    }
     AT* h1 = buf((long)R * P * r.cout);
     conv(a, H, W, r.cin, wt<AT>(r.w1), r.cout, r.b1, h1, temb_all + r.temb_off);
     AT* a2 = buf((long)R * P * r.cout);
     gn(h1, a2, P, r.cout, r.n2g, r.n2b, e->uc.eps_res, true);
     const AT* sc = x;
-    if (r.wsc) {
+    if (r.wsc && x1) {
+      AT* s = buf((long)R * P * r.cout);
+      GemmDescT<AT> d;  // shortcut over the concat: K = [x | x1], weight columns split the same way
+      d.nsrc = 2;
+      d.xs[0] = x;
+      d.cs[0] = r.cin - C1;
+      d.xs[1] = x1;
+      d.cs[1] = C1;
+      d.M = (int)((long)R * P);
+      d.K = r.cin;
+      d.lda = r.cin;
+      d.Bw[0] = wt<AT>(r.wsc);
+      d.Bw[1] = wt<AT>(r.wsc) + (r.cin - C1);
+      d.N = r.cout;
+      d.ldb = r.cin;
+      d.out = s;
+      d.ldo = r.cout;
+      d.bias = r.bsc;
+      const int pi = e->prof.begin(PC_GEMM, st, 2.0 * R * P * r.cout * r.cin);
+      gemm(d, st);
+      e->prof.end(pi, st);
+      sc = s;
+    } else if (r.wsc) {
       AT* s = buf((long)R * P * r.cout);
       linear(x, (long)R * P, r.cin, wt<AT>(r.wsc), r.cout, r.bsc, s, r.cout);
       sc = s;
@@ -828,10 +859,14 @@ static void unet_forward(Engine* e, cudaStream_t st, int R, int H, int W, const 
     for (size_t j = 0; j < u.res.size(); ++j) {
       Skip s = skips.back();
       skips.pop_back();
-      const int Ccat = C + s.C;
-      AT* cat = f.buf((long)R * h * w * Ccat);
-      concat_channels(x, C, s.p, s.C, cat, (long)R * h * w, st);
-      x = f.resblock(u.res[j], cat, h, w);
+      if constexpr (std::is_same<AT, bf16>::value) {
+        x = f.resblock(u.res[j], x, h, w, s.p, s.C);  // concat [x | skip] read as two sources
+      } else {  // fp32 parity mode: its SIMT GEMM takes one source
+        const int Ccat = C + s.C;
+        AT* cat = f.buf((long)R * h * w * Ccat);
+        concat_channels(x, C, s.p, s.C, cat, (long)R * h * w, st);
+        x = f.resblock(u.res[j], cat, h, w);
+      }
       C = u.res[j].cout;
       if (!u.tf.empty()) x = f.transformer(u.tf[j], x, h, w);
     }

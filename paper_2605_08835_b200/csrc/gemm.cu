@@ -512,8 +512,11 @@ __global__ void __launch_bounds__(320, 1)
           void* dA = sA + stage * C::A_BYTES;
           void* dB = sB + stage * C::B_BYTES;
           if (MODE == GEMM_DENSE) {
-            tma2<CG>(dA, &ta0, &full[stage], bar_l, kb * C::BK, m0);
-            tma2<CG>(dB, &tb0, &full[stage], bar_l, kb * C::BK, n0);
+            // two sources (a channel concat never materialised): K blocks [0, kb_src0) from source 0
+            const bool s1 = g.nsrc > 1 && kb >= g.kb_src[0];
+            const int kk = s1 ? kb - g.kb_src[0] : kb;
+            tma2<CG>(dA, s1 ? &ta1 : &ta0, &full[stage], bar_l, kk * C::BK, m0);
+            tma2<CG>(dB, s1 ? &tb1 : &tb0, &full[stage], bar_l, kk * C::BK, n0);
           } else {
             int r = kb, src = 0;
             if (r >= 9 * g.kb_src[0]) {
@@ -806,8 +809,15 @@ void gemm(const GemmDesc& d, cudaStream_t st) {
     if (d.K % 8 || d.lda % 8 || d.ldb % 8) throw CudaError("dense GEMM: K/lda/ldb must be multiples of 8");
     a.M = d.M;
     m_boxes = cdiv(d.M, 128);
-    a.num_kb = cdiv(d.K, 64);
-    a.nsrc = 1;
+    a.nsrc = d.nsrc;
+    if (d.nsrc == 2) {  // A = [xs[0] | xs[1]] (cs[0] + cs[1] = K columns), B = [Bw[0] | Bw[1]] (row stride ldb)
+      if (d.cs[0] % 8 || d.cs[1] % 8 || d.cs[0] + d.cs[1] != d.K) throw CudaError("dense GEMM: bad source split");
+      a.kb_src[0] = cdiv(d.cs[0], 64);
+      a.kb_src[1] = cdiv(d.cs[1], 64);
+      a.num_kb = a.kb_src[0] + a.kb_src[1];
+    } else {
+      a.num_kb = cdiv(d.K, 64);
+    }
   } else {
     if (d.stride != 1 && (d.stride != 2 || d.nsrc != 1)) throw CudaError("conv3: stride 1, or 2 with one source");
     a.B = d.B;
@@ -856,7 +866,16 @@ void gemm(const GemmDesc& d, cudaStream_t st) {
   if (g_cg_override == 1 || g_cg_override == 2) cg = g_cg_override;
   if (cg == 2 && (box_begin % 2 || bn < 128)) cg = 1;
   const uint32_t brows = (uint32_t)(bn / cg);
-  if (d.mode == GEMM_DENSE) {
+  if (d.mode == GEMM_DENSE && d.nsrc == 2) {
+    for (int s = 0; s < 2; ++s) {  // source s: its own activation tensor [M][cs] and weight columns
+      uint64_t dA[2] = {(uint64_t)d.cs[s], (uint64_t)d.M}, sA[1] = {(uint64_t)d.cs[s] * 2};
+      uint32_t bA[2] = {64, 128};
+      make_map(&maps[s], d.xs[s], 2, dA, sA, bA);
+      uint64_t dB[2] = {(uint64_t)d.cs[s], (uint64_t)d.N}, sB[1] = {(uint64_t)d.ldb * 2};
+      uint32_t bB[2] = {64, brows};
+      make_map(&maps[2 + s], d.Bw[s], 2, dB, sB, bB);
+    }
+  } else if (d.mode == GEMM_DENSE) {
     uint64_t dA[2] = {(uint64_t)d.K, (uint64_t)d.M}, sA[1] = {(uint64_t)d.lda * 2};
     uint32_t bA[2] = {64, 128};
     make_map(&maps[0], d.A, 2, dA, sA, bA);

@@ -29,7 +29,7 @@ struct GemmDescT {
   int mode = GEMM_DENSE;
   const T* A = nullptr;
   int M = 0, K = 0, lda = 0;
-  int nsrc = 1;
+  int nsrc = 1;             // conv3: two sources = implicit channel concat; dense: A = [xs[0] | xs[1]]
   const T* xs[2] = {nullptr, nullptr};
   int cs[2] = {0, 0};
   int B = 0, H = 0, W = 0;   // conv3: batch and OUTPUT spatial size

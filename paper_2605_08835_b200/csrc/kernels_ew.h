@@ -17,6 +17,11 @@ int gn_chunk_px(int C);  // pixels per statistics chunk (divides 128)
 template <class T>
 void group_norm(const T* x, T* y, int B, int P, int C, int G, const float* gamma, const float* beta, float eps,
                 bool silu, void* ws, cudaStream_t st);
+// GroupNorm over the channel concat [x0 (C0 channels) | x1 (C1 channels)] of two [B][P][·] tensors,
+// written to y [B][P][C0 + C1] — the up-block concat is never materialised
+template <class T>
+void group_norm2(const T* x0, int C0, const T* x1, int C1, T* y, int B, int P, int G, const float* gamma,
+                 const float* beta, float eps, bool silu, void* ws, cudaStream_t st);
 // pixel ranges [p0, p1) must be multiples of 128 (or end at P)
 template <class T>
 void gn_stats_range(const T* x, int P, int C, int G, int p0, int p1, void* ws, cudaStream_t st);

@@ -111,9 +111,22 @@ __device__ __forceinline__ void gn_merge_group(int P, int C, int G, int chunk_px
 // block (V, R): V = C/8 vector lanes, R pixel rows; grid (chunks in range, B)
 // (measured: merging in the last-arriving stats block instead of a finalize launch serialises the
 // 32 group merges on one block — 2.1 vs 1.8 ms of GN per 16-row SD-1.5 step)
+// Two sources (x1 != nullptr): the channels are the concat [x (V0 vectors) | x1 (V − V0 vectors)], each
+// source contiguous in its own [B][P][channels] layout — the up-block concat is never materialised.
 template <class T>
-__global__ void __launch_bounds__(512) gn_stats_kernel(const T* __restrict__ x, int P, int C, int G, int chunk_px,
-                                                       int c_base, int nch_total, GNPart* __restrict__ part) {
+__device__ __forceinline__ const T* gn_src(const T* x, const T* x1, int V0, int V, int b, int P, int v, int& ld) {
+  if (!x1 || v < V0) {
+    ld = (x1 ? V0 : V) * 8;
+    return x + (long)b * P * ld + v * 8;
+  }
+  ld = (V - V0) * 8;
+  return x1 + (long)b * P * ld + (v - V0) * 8;
+}
+
+template <class T>
+__global__ void __launch_bounds__(512) gn_stats_kernel(const T* __restrict__ x, const T* __restrict__ x1, int V0, int P,
+                                                       int C, int G, int chunk_px, int c_base, int nch_total,
+                                                       GNPart* __restrict__ part) {
   extern __shared__ float sh[];  // [R][C] sums, then [R][C] sums of squares
   const int V = blockDim.x, R = blockDim.y;
   const int v = threadIdx.x, ry = threadIdx.y;
@@ -122,13 +135,14 @@ __global__ void __launch_bounds__(512) gn_stats_kernel(const T* __restrict__ x, 
   float s[8], q[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) s[i] = q[i] = 0.f;
-  const T* xb = x + (long)b * P * C + v * 8;
+  int ld;
+  const T* xb = gn_src(x, x1, V0, V, b, P, v, ld);
   for (int p = p0 + ry; p < p1; p += 8 * R) {
     // unconditional loads from clamped rows (the compiler keeps all 8 in flight); rows past the
     // chunk are masked out afterwards
     Raw8<T> u[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) u[k].ld(xb + (long)min(p + k * R, p1 - 1) * C);
+    for (int k = 0; k < 8; ++k) u[k].ld(xb + (long)min(p + k * R, p1 - 1) * ld);
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       if (p + k * R < p1) {
@@ -194,16 +208,22 @@ __global__ void gn_finalize_kernel(int P, int C, int G, int chunk_px, int nchunk
 // only when its pixel crosses into the next image); U pixel rows per thread per iteration, all
 // loads issued before any math; grid-stride over blocks of R·U pixels.
 template <class T>
-__global__ void __launch_bounds__(512) gn_apply_kernel(const T* __restrict__ x, long p_begin, long p_end, int P, int V,
+__global__ void __launch_bounds__(512) gn_apply_kernel(const T* __restrict__ x, const T* __restrict__ x1, int V0,
+                                                       long p_begin, long p_end, int P, int V,
                                                        const float2* __restrict__ tab, int silu, T* __restrict__ y) {
   constexpr int U = 4;
   const int v = threadIdx.x, R = blockDim.y;
+  // source of this thread's channel vector; pixel p of the flat [B·P] range sits at row p of it
+  const bool second = x1 && v >= V0;
+  const T* xs = second ? x1 : x;
+  const int ldv = x1 ? (second ? V - V0 : V0) : V;  // vectors per pixel row of the source
+  const int vs = second ? v - V0 : v;
   int b_cur = -1;
   float sc[8], sf[8];
   for (long pb = p_begin + (long)blockIdx.x * R * U + threadIdx.y; pb < p_end; pb += (long)gridDim.x * R * U) {
     Raw8<T> u[U];
 #pragma unroll
-    for (int k = 0; k < U; ++k) u[k].ld(x + (min(pb + (long)k * R, p_end - 1) * V + v) * 8);
+    for (int k = 0; k < U; ++k) u[k].ld(xs + (min(pb + (long)k * R, p_end - 1) * ldv + vs) * 8);
 #pragma unroll
     for (int k = 0; k < U; ++k) {
       const long p = pb + (long)k * R;
@@ -251,8 +271,8 @@ static void gn_finalize(int B, int P, int C, int G, int cp, void* ws, float eps,
 }
 
 template <class T>
-static void gn_apply(const T* x, T* y, long p0, long p1, int B, int P, int C, const float2* tab, bool silu,
-                     cudaStream_t st) {
+static void gn_apply(const T* x, const T* x1, int C0, T* y, long p0, long p1, int B, int P, int C, const float2* tab,
+                     bool silu, cudaStream_t st) {
   if (p1 <= p0) return;
   if (p1 >= (1L << 31)) throw CudaError("group_norm: tensor too large");
   const dim3 blk = gn_stats_block(C);
@@ -261,7 +281,7 @@ static void gn_apply(const T* x, T* y, long p0, long p1, int B, int P, int C, co
   if (!sms) SD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   const long want = (p1 - p0 + rows - 1) / rows;
   const int grid = (int)std::min<long>(want, (long)sms * (2048 / (blk.x * blk.y)));
-  gn_apply_kernel<T><<<grid, blk, 0, st>>>(x, p0, p1, P, C / 8, tab, silu ? 1 : 0, y);
+  gn_apply_kernel<T><<<grid, blk, 0, st>>>(x, x1, C0 / 8, p0, p1, P, C / 8, tab, silu ? 1 : 0, y);
   SD_CHECK_LAUNCH();
   (void)B;
 }
@@ -271,11 +291,12 @@ static void check_gn(int C, int G) {
 }
 
 template <class T>
-static void gn_stats(const T* x, int B, int P, int C, int G, int c0, int c1, void* ws, cudaStream_t st) {
+static void gn_stats(const T* x, const T* x1, int C0, int B, int P, int C, int G, int c0, int c1, void* ws,
+                     cudaStream_t st) {
   const int cp = gn_chunk_px(C);
   const dim3 blk = gn_stats_block(C);
   const size_t sh = (size_t)blk.x * blk.y * 8 * 2 * sizeof(float);
-  gn_stats_kernel<<<dim3(c1 - c0, B), blk, sh, st>>>(x, P, C, G, cp, c0, cdiv(P, cp), gn_parts(ws));
+  gn_stats_kernel<<<dim3(c1 - c0, B), blk, sh, st>>>(x, x1, C0 / 8, P, C, G, cp, c0, cdiv(P, cp), gn_parts(ws));
   SD_CHECK_LAUNCH();
 }
 
@@ -286,7 +307,7 @@ template <class T>
 void gn_stats_range(const T* x, int P, int C, int G, int p0, int p1, void* ws, cudaStream_t st) {
   check_gn(C, G);
   const int cp = gn_chunk_px(C);
-  gn_stats(x, 1, P, C, G, p0 / cp, cdiv(p1, cp), ws, st);
+  gn_stats(x, (const T*)nullptr, C, 1, P, C, G, p0 / cp, cdiv(p1, cp), ws, st);
 }
 template <class T>
 void gn_apply_range(const T* x, T* y, int P, int C, int G, int p0, int p1, const float* gamma, const float* beta,
@@ -294,17 +315,25 @@ void gn_apply_range(const T* x, T* y, int P, int C, int G, int p0, int p1, const
   check_gn(C, G);
   const int cp = gn_chunk_px(C);
   if (p0 == 0) gn_finalize(1, P, C, G, cp, ws, eps, gamma, beta, st);  // bands run in order
-  gn_apply(x, y, p0, p1, 1, P, C, gn_tab(ws, 1, P, G), silu, st);
+  gn_apply(x, (const T*)nullptr, C, y, p0, p1, 1, P, C, gn_tab(ws, 1, P, G), silu, st);
 }
 
 template <class T>
 void group_norm(const T* x, T* y, int B, int P, int C, int G, const float* gamma, const float* beta, float eps,
                 bool silu, void* ws, cudaStream_t st) {
+  group_norm2(x, C, (const T*)nullptr, 0, y, B, P, G, gamma, beta, eps, silu, ws, st);
+}
+
+template <class T>
+void group_norm2(const T* x0, int C0, const T* x1, int C1, T* y, int B, int P, int G, const float* gamma,
+                 const float* beta, float eps, bool silu, void* ws, cudaStream_t st) {
+  const int C = C0 + C1;
   check_gn(C, G);
+  if (x1 && (C0 % 8 || C1 % 8)) throw CudaError("group_norm2: source channels must be multiples of 8");
   const int cp = gn_chunk_px(C);
-  gn_stats(x, B, P, C, G, 0, cdiv(P, cp), ws, st);
+  gn_stats(x0, x1, C0, B, P, C, G, 0, cdiv(P, cp), ws, st);
   gn_finalize(B, P, C, G, cp, ws, eps, gamma, beta, st);
-  gn_apply(x, y, 0, (long)B * P, B, P, C, gn_tab(ws, B, P, G), silu, st);
+  gn_apply(x0, x1, C0, y, 0, (long)B * P, B, P, C, gn_tab(ws, B, P, G), silu, st);
 }
 
 // ---- LayerNorm: LANES lanes per token (NV 16-byte vectors each), two-pass in registers ----------
@@ -401,7 +430,9 @@ void layer_norm(const E* x, E* y, int T, int C, const float* gamma, const float*
   template void gn_stats_range<T>(const T*, int, int, int, int, int, void*, cudaStream_t);                   \
   template void gn_apply_range<T>(const T*, T*, int, int, int, int, int, const float*, const float*, float, bool, \
                                   void*, cudaStream_t);                                                      \
-  template void layer_norm<T>(const T*, T*, int, int, const float*, const float*, float, cudaStream_t);
+  template void layer_norm<T>(const T*, T*, int, int, const float*, const float*, float, cudaStream_t);   \
+  template void group_norm2<T>(const T*, int, const T*, int, T*, int, int, int, const float*, const float*, float, \
+                               bool, void*, cudaStream_t);
 SD_NORM_INST(bf16)
 SD_NORM_INST(float)
 
