@@ -10,8 +10,9 @@
 //               S, running max / sum in fp32, P = exp2(s·log2e/√d − m) as bf16 into a swizzled smem
 //               tile (A operand of the PV MMA), and O ← α·O in TMEM when the running max grows
 //               (lazily, threshold 2⁸); finally O/l → bf16. At d = 40 the scores are read from TMEM
-//               once, the S buffer is handed back before the exps, and 1/8 of the exps run on the
-//               FMA pipe (ex2_poly) to relieve MUFU (SD_ATTN_EMU, below).
+//               once, the S buffer is handed back before the exps, 1/8 of the exps run on the FMA
+//               pipe (ex2_poly) to relieve MUFU, and P goes back to TMEM (tcgen05.st) as the A
+//               operand of the PV MMA instead of through shared memory (SD_ATTN_EMU, below).
 // S never leaves the SM; P never leaves shared memory. Bound: MUFU exp2 (16/clk/SM) at d ≤ 80.
 #include <float.h>
 
@@ -40,6 +41,7 @@ struct TcAttn {
   static constexpr int THREADS = 64 + 128 * SPLIT;
   static constexpr int TMEM_COLS = NB == 2 ? 512 : 256;
   static constexpr int O_COL = NB * 128;         // O accumulator after the S buffers
+  static constexpr int P_COL = 192;              // P (bf16, 2 per column) in TMEM for the OP = 4 variant (NB = 1)
   static_assert(V_BYTES % 1024 == 0, "Vᵀ tile rows must be a multiple of 8");
   static_assert(NPV <= 128, "O must fit beside the S buffers");
 };
@@ -60,6 +62,17 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
       : "memory");
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// D[tmem] (+)= A[tmem] · B[smem]ᵀ (kind::f16): A read from Tensor Memory, M rows = lanes, K packed
+// two bf16 per 32-bit column
+__device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -183,7 +196,12 @@ __global__ void __launch_bounds__(64 + 128 * SPLIT, 3 - NB)
           for (int k = 0; k < 8; ++k) {
             const uint32_t offp = (k >> 2) * (A::BQ * 128) + (k & 3) * 32;
             const uint32_t offv = (k >> 2) * (A::NPV * 128) + (k & 3) * 32;
-            umma_bf16(tmem + A::O_COL, make_sdesc_sw128(ap + offp), make_sdesc_sw128(av + offv), id_pv, (jp | k) != 0);
+            if constexpr (OP == 4)  // A = P from TMEM: 16 keys = 8 packed columns per k-step
+              umma_bf16_ts(tmem + A::O_COL, tmem + A::P_COL + k * 8, make_sdesc_sw128(av + offv), id_pv,
+                           (jp | k) != 0);
+            else
+              umma_bf16(tmem + A::O_COL, make_sdesc_sw128(ap + offp), make_sdesc_sw128(av + offv), id_pv,
+                        (jp | k) != 0);
           }
           umma_commit(&kv_empty[sp]);
           umma_commit(pv_done);
@@ -250,7 +268,7 @@ __global__ void __launch_bounds__(64 + 128 * SPLIT, 3 - NB)
         for (int i = 0; i < 16; ++i) {  // P packed in place: ta[i] ← bf16x2(p(ta[2i]), p(ta[2i+1]))
           const float x0 = fmaf(__uint_as_float(ta[2 * i]), scale_log2, -ms);
           const float x1 = fmaf(__uint_as_float(ta[2 * i + 1]), scale_log2, -ms);
-          const bool emu = OP >= 2 && (i % (OP == 2 ? 8 : 4)) == 3;  // OP 2 / 3: 1/8 / 1/4 on the FMA pipe
+          const bool emu = OP >= 2 && (i % (OP == 3 ? 4 : 8)) == 3;  // OP 2, 4 / 3: 1/8 / 1/4 on the FMA pipe
           const float p0 = emu ? ex2_poly(x0) : ex2(x0);
           const float p1 = emu ? ex2_poly(x1) : ex2(x1);
           sum8[i & 7] += p0 + p1;
@@ -260,7 +278,7 @@ __global__ void __launch_bounds__(64 + 128 * SPLIT, 3 - NB)
         for (int i = 0; i < 16; ++i) {
           const float x0 = fmaf(__uint_as_float(tb[2 * i]), scale_log2, -ms);
           const float x1 = fmaf(__uint_as_float(tb[2 * i + 1]), scale_log2, -ms);
-          const bool emu = OP >= 2 && (i % (OP == 2 ? 8 : 4)) == 1;
+          const bool emu = OP >= 2 && (i % (OP == 3 ? 4 : 8)) == 1;
           const float p0 = emu ? ex2_poly(x0) : ex2(x0);
           const float p1 = emu ? ex2_poly(x1) : ex2(x1);
           sum8[i & 7] += p0 + p1;
@@ -285,15 +303,24 @@ __global__ void __launch_bounds__(64 + 128 * SPLIT, 3 - NB)
             tmem_wait_st();
           }
         }
-        uint8_t* prow = sP + sb * A::P_BYTES + h * (A::BQ * 128) + r * 128;
+        if constexpr (OP == 4) {
+          // P stays in TMEM (the A operand of the PV MMA): this thread's 64 keys = 32 packed columns
+          uint32_t (&pa)[16] = reinterpret_cast<uint32_t(&)[16]>(ta);
+          uint32_t (&pb)[16] = reinterpret_cast<uint32_t(&)[16]>(tb);
+          tmem_st16(tmem + lane_base + A::P_COL + h * 32, pa);
+          tmem_st16(tmem + lane_base + A::P_COL + h * 32 + 16, pb);
+          tmem_wait_st();
+        } else {
+          uint8_t* prow = sP + sb * A::P_BYTES + h * (A::BQ * 128) + r * 128;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) << 4)) =
-              make_uint4(ta[c * 4], ta[c * 4 + 1], ta[c * 4 + 2], ta[c * 4 + 3]);
-          *reinterpret_cast<uint4*>(prow + (((c + 4) ^ (r & 7)) << 4)) =
-              make_uint4(tb[c * 4], tb[c * 4 + 1], tb[c * 4 + 2], tb[c * 4 + 3]);
+          for (int c = 0; c < 4; ++c) {
+            *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) << 4)) =
+                make_uint4(ta[c * 4], ta[c * 4 + 1], ta[c * 4 + 2], ta[c * 4 + 3]);
+            *reinterpret_cast<uint4*>(prow + (((c + 4) ^ (r & 7)) << 4)) =
+                make_uint4(tb[c * 4], tb[c * 4 + 1], tb[c * 4 + 2], tb[c * 4 + 3]);
+          }
+          fence_proxy_async_smem();
         }
-        fence_proxy_async_smem();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[sb]);
@@ -473,17 +500,19 @@ static int attn_split() {
 }
 
 // SD_ATTN_EMU selects the d = 40 softmax variant (kbench r01, [16, 8, 40, 4096]):
-//   0  two TMEM passes, all exps on MUFU                          0.794 ms
+//   0  two TMEM passes, all exps on MUFU, P through smem          0.794 ms
 //   4  two passes, 1/4 of the exps on the FMA pipe (ex2_poly)     slower
 //   5  one TMEM pass (OP 1), S released before the exps           0.784 ms
-//   6  one pass + 1/8 of the exps on the FMA pipe (OP 2, default) 0.773 ms
+//   6  one pass + 1/8 of the exps on the FMA pipe (OP 2)          0.769 ms
 //   7  one pass + 1/4 on the FMA pipe (OP 3)                      0.804 ms
+//   8  OP 2 + P kept in TMEM as the A operand of the PV MMA       0.751 ms (default; no P smem
+//      stores, no async-proxy fence)
 static int attn_emu() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("SD_ATTN_EMU");
-    v = e ? atoi(e) : 6;
-    if (v != 0 && v != 4 && (v < 5 || v > 7)) v = 6;
+    v = e ? atoi(e) : 8;
+    if (v != 0 && v != 4 && (v < 5 || v > 8)) v = 8;
   }
   return v;
 }
@@ -518,6 +547,7 @@ void attention_tc(const bf16* qk, const bf16* vt, bf16* O, int rows, int heads, 
         case 225: launch_tc<40, 2, 2, 0, 1>(qk, vt, O, rows, heads, C, P, st); break;
         case 126: launch_tc<40, 1, 2, 0, 2>(qk, vt, O, rows, heads, C, P, st); break;
         case 127: launch_tc<40, 1, 2, 0, 3>(qk, vt, O, rows, heads, C, P, st); break;
+        case 128: launch_tc<40, 1, 2, 0, 4>(qk, vt, O, rows, heads, C, P, st); break;  // SD_ATTN_EMU=8: P in TMEM
         default: launch_tc<40, 1, 2, 0>(qk, vt, O, rows, heads, C, P, st); break;
       }
       break;
