@@ -41,7 +41,7 @@ struct TcAttn {
   static constexpr int THREADS = 64 + 128 * SPLIT;
   static constexpr int TMEM_COLS = NB == 2 ? 512 : 256;
   static constexpr int O_COL = NB * 128;         // O accumulator after the S buffers
-  static constexpr int P_COL = 192;              // P (bf16, 2 per column) in TMEM for the OP = 4 variant (NB = 1)
+  static constexpr int P_COL = NB == 1 ? 192 : 384;  // P (bf16, 2 per column) in TMEM (OP 4 / 5)
   static_assert(V_BYTES % 1024 == 0, "Vᵀ tile rows must be a multiple of 8");
   static_assert(NPV <= 128, "O must fit beside the S buffers");
 };
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(64 + 128 * SPLIT, 3 - NB)
           for (int k = 0; k < 8; ++k) {
             const uint32_t offp = (k >> 2) * (A::BQ * 128) + (k & 3) * 32;
             const uint32_t offv = (k >> 2) * (A::NPV * 128) + (k & 3) * 32;
-            if constexpr (OP == 4)  // A = P from TMEM: 16 keys = 8 packed columns per k-step
+            if constexpr (OP == 4 || OP == 5)  // A = P from TMEM: 16 keys = 8 packed columns per k-step
               umma_bf16_ts(tmem + A::O_COL, tmem + A::P_COL + k * 8, make_sdesc_sw128(av + offv), id_pv,
                            (jp | k) != 0);
             else
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(64 + 128 * SPLIT, 3 - NB)
       const uint32_t sbase = tmem + lane_base + sb * 128 + h * CPT;
       // Lk is a multiple of 128 (attention_tc_supported): no key block is ragged
       uint32_t ta[32], tb[32];
-      if constexpr (OP >= 1) {
+      if constexpr (OP >= 1 && OP <= 4) {
         static_assert(SPLIT == 2, "one-pass softmax needs 64 columns per thread");  // OP ≥ 1
         tmem_ld32_nw(sbase, ta);
         tmem_ld32_nw(sbase + 32, tb);
@@ -412,18 +412,27 @@ __global__ void __launch_bounds__(64 + 128 * SPLIT, 3 - NB)
           tmem_wait_st();
         }
       }
-      // P row → swizzled smem (64-key K-blocks, 128 B per row, 16-byte chunk c at c ^ (r & 7))
-      uint8_t* prow = sP + sb * A::P_BYTES + r * 128;
+      if constexpr (OP == 5) {
+        // P back to TMEM (A operand of the PV MMA): this thread's CPT keys = CPT / 2 packed columns
 #pragma unroll
-      for (int kk = 0; kk < NCH / 2; ++kk)
+        for (int c = 0; c < NCH; ++c)
+          tmem_st16(tmem + lane_base + A::P_COL + h * (CPT / 2) + c * 16,
+                    reinterpret_cast<uint32_t(&)[16]>(pk[c * 16]));
+        tmem_wait_st();
+      } else {
+        // P row → swizzled smem (64-key K-blocks, 128 B per row, 16-byte chunk c at c ^ (r & 7))
+        uint8_t* prow = sP + sb * A::P_BYTES + r * 128;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const int i = kk * 32 + c * 4;
-          const int kb = h * (NCH / 2) + kk;
-          *reinterpret_cast<uint4*>(prow + kb * (A::BQ * 128) + ((c ^ (r & 7)) << 4)) =
-              make_uint4(pk[i], pk[i + 1], pk[i + 2], pk[i + 3]);
-        }
-      fence_proxy_async_smem();
+        for (int kk = 0; kk < NCH / 2; ++kk)
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const int i = kk * 32 + c * 4;
+            const int kb = h * (NCH / 2) + kk;
+            *reinterpret_cast<uint4*>(prow + kb * (A::BQ * 128) + ((c ^ (r & 7)) << 4)) =
+                make_uint4(pk[i], pk[i + 1], pk[i + 2], pk[i + 3]);
+          }
+        fence_proxy_async_smem();
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[sb]);
@@ -551,14 +560,18 @@ void attention_tc(const bf16* qk, const bf16* vt, bf16* O, int rows, int heads, 
         default: launch_tc<40, 1, 2, 0>(qk, vt, O, rows, heads, C, P, st); break;
       }
       break;
-    case 64:  // measured: NB=2 1.18× faster at d=64
-      if (attn_emu() != 4)
+    case 64:  // measured: NB=2 1.18× faster at d=64; OP 5 = P in TMEM (SD_ATTN_EMU=8, the default)
+      if (attn_emu() == 8)
+        launch_tc<64, 2, 1, 0, 5>(qk, vt, O, rows, heads, C, P, st);
+      else if (attn_emu() != 4)
         launch_tc<64, 2, 1, 0>(qk, vt, O, rows, heads, C, P, st);
       else
         launch_tc<64, 2, 1, 4>(qk, vt, O, rows, heads, C, P, st);
       break;
     case 80:
-      if (attn_emu() != 4)
+      if (attn_emu() == 8)
+        launch_tc<80, 2, 1, 0, 5>(qk, vt, O, rows, heads, C, P, st);
+      else if (attn_emu() != 4)
         launch_tc<80, 2, 1, 0>(qk, vt, O, rows, heads, C, P, st);
       else
         launch_tc<80, 2, 1, 4>(qk, vt, O, rows, heads, C, P, st);
