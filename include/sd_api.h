@@ -136,6 +136,15 @@ sd_status sd_sampler_init_sigma(sd_engine* e, int32_t n_steps, float* out);
  * n_chunks == 1 is a whole-image decode. Any n_chunks gives the same image (I6). */
 sd_status sd_vae_decode_chunked(sd_engine* e, const float* latent_dev, int32_t h, int32_t w, int32_t n_chunks,
                                 int32_t chunk, sd_decode** state, float* image_dev, void* stream);
+/* V2 independent-tile decode (reading R7 V2), the north star's literal "latent
+ * split into halo-padded tiles, decoded tile by tile and stitched": every tile x tile block of the
+ * latent is decoded on its own from its halo-padded window (clipped at the border), so GroupNorm and
+ * the mid-block attention are tile-local (an APPROXIMATION of the whole decode, unlike the exact V1
+ * sd_vae_decode_chunked); its own image region is written into image_dev [3][8h][8w] (disjoint
+ * writes). h, w, tile, halo: multiples of 8. tile >= h, w or halo >= h, w reproduces the whole decode.
+ * Asynchronous on `stream`; the engine owns the window scratch. */
+sd_status sd_vae_decode_tiled(sd_engine* e, const float* latent_dev, int32_t h, int32_t w, int32_t tile,
+                              int32_t halo, float* image_dev, void* stream);
 
 /* ---- pure host control plane -------------------------------------------
  * Latency table: CSV "c,m,n,k,tau_us,delta_us" (integers, µs; R11). */

@@ -245,3 +245,36 @@ def decode_chunked(P, cfg: VAEConfig, z, n_chunks=2, n_bands=4, halo=1, costs=No
                     out = out + buf[a["res"]][:, :, y0:y1, :]
                 buf[a["dst"]][:, :, y0:y1, :] = out
     return buf["img"]
+
+
+# ---------------------------------------------------------------------------------------------
+# V2 independent-tile decode — an approximation, separate code path
+# ---------------------------------------------------------------------------------------------
+
+def tile_windows(h, w, tile, halo):
+    """The tiles of a V2 decode in row-major order: (y0, y1, x0, x1) latent rows / columns the tile
+    owns, and (a0, a1, b0, b1) the halo-padded window it is decoded from (clipped at the border)."""
+    out = []
+    for y0 in range(0, h, tile):
+        for x0 in range(0, w, tile):
+            y1, x1 = min(h, y0 + tile), min(w, x0 + tile)
+            out.append(((y0, y1, x0, x1), (max(0, y0 - halo), min(h, y1 + halo), max(0, x0 - halo), min(w, x1 + halo))))
+    return out
+
+
+def decode_tiled(P, cfg: VAEConfig, z, tile, halo):
+    """Reading V2 of R7: the north star's literal "latent split into halo-padded tiles, decoded tile
+    by tile and stitched". Every `tile`×`tile` block of latent pixels is decoded ON ITS OWN from its
+    `halo`-padded window — GroupNorm statistics and the mid-block attention see only that window, so
+    unlike V1 this approximates decode() — and the block's own image region (upscale× its latent
+    extent) is cut out of the window's decode and written into the output (stitching = disjoint
+    writes, no blending). tile ≥ image, or halo ≥ image, reduces to decode() exactly."""
+    N, _, h, w = z.shape
+    f = 2 ** (len(cfg.block_out) - 1)
+    out = None
+    for (y0, y1, x0, x1), (a0, a1, b0, b1) in tile_windows(h, w, tile, halo):
+        img = decode(P, cfg, np.ascontiguousarray(z[:, :, a0:a1, b0:b1]))
+        if out is None:
+            out = np.zeros((N, img.shape[1], f * h, f * w), img.dtype)
+        out[:, :, f * y0:f * y1, f * x0:f * x1] = img[:, :, f * (y0 - a0):f * (y1 - a0), f * (x0 - b0):f * (x1 - b0)]
+    return out

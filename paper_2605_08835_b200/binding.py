@@ -105,6 +105,7 @@ SIGNATURES = {
     "sd_controller_free": [P],
     "sd_chunk_ranges": [PI64, I32, I32, PI32],
     "sd_engine_warmup": [P, I32, I32, I32, I32, P],
+    "sd_vae_decode_tiled": [P, P, I32, I32, I32, I32, P, P],
     "sd_serve_start": [P, C.POINTER(ServeConfig)],
     "sd_submit": [P, C.POINTER(Request)],
     "sd_poll": [P, C.POINTER(Completion), I32, PI32, I32],

@@ -175,6 +175,17 @@ extern "C" sd_status sd_vae_decode_chunked(sd_engine* e, const float* z, int32_t
   })
 }
 
+extern "C" sd_status sd_vae_decode_tiled(sd_engine* e, const float* z, int32_t h, int32_t w, int32_t tile,
+                                        int32_t halo, float* image, void* stream) {
+  ENGINE_GUARD(e);
+  SD_REQUIRE(z && image, "sd_vae_decode_tiled: null argument");
+  SD_REQUIRE(h >= 8 && w >= 8 && h <= e->e.cfg.max_latent_hw && w <= e->e.cfg.max_latent_hw && h % 8 == 0 &&
+                 w % 8 == 0,
+             "sd_vae_decode_tiled: latent size (multiples of 8)");
+  SD_REQUIRE(tile >= 8 && tile % 8 == 0 && halo >= 0 && halo % 8 == 0, "sd_vae_decode_tiled: tile / halo");
+  ENGINE_BODY(e, { vae_decode_tiled(&e->e, z, h, w, tile, halo, image, static_cast<cudaStream_t>(stream)); })
+}
+
 extern "C" sd_status sd_engine_profile(sd_engine* e, int32_t enable) {
   ENGINE_GUARD(e);
   ENGINE_BODY(e, {

@@ -375,6 +375,7 @@ Engine::~Engine() {
   if (aug_cache) cudaFree(aug_cache);
   if (reg_scratch) cudaFree(reg_scratch);
   if (gn_ws) cudaFree(gn_ws);
+  if (tile_scratch) cudaFree(tile_scratch);
   if (time_ids) cudaFree(time_ids);
   if (reg_ev) cudaEventDestroy(reg_ev);
   if (meta_dev) cudaFree(meta_dev);

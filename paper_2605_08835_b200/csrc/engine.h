@@ -211,6 +211,8 @@ struct Engine {
   // VAE decode slots
   std::vector<DecodeState*> free_decodes;
   std::mutex dmu;
+  void* tile_scratch = nullptr;  // V2 tiled decode: window latent + window image (grown on demand)
+  size_t tile_scratch_bytes = 0;
   void* server = nullptr;  // serve_gpu.cu Server while serving
   int upscale() const { return 1 << ((int)vc.block_out.size() - 1); }
   ~Engine();
@@ -223,6 +225,7 @@ int ctx_register(Engine* e, const float* emb, int len, int dim, const float* poo
 void vae_decode_chunk(Engine* e, const float* z, int h, int w, int n_chunks, int chunk, DecodeState** state,
                       float* image, cudaStream_t st);
 void destroy_decode(Engine* e, DecodeState* d);
+void vae_decode_tiled(Engine* e, const float* z, int h, int w, int tile, int halo, float* image, cudaStream_t st);
 
 }  // namespace sd
 

@@ -21,7 +21,7 @@ enum { NBUF = 6 };
 
 struct DecodeState {
   int h = 0, w = 0, n_chunks = 0, next_chunk = 0;
-  bool banded = true;
+  int nbands = 1;  // row bands per tail layer (band_rows)
   Arena ar;
   size_t buf_elems = 0;
   void* buf[NBUF];  // activation precision of the engine (bf16, or fp32 in the parity mode)
@@ -34,7 +34,19 @@ struct DecodeState {
 
 // row bands of the tail layers: 32 rows (≥ 64-row layers) when the decode is chunked; one band per
 // layer for a whole decode (fewer launches; same values — banding is bitwise neutral, I6)
-static int band_rows(int H, bool banded) { return banded ? (H >= 64 ? 32 : std::max(8, H / 2)) : H; }
+// Row bands of the tail layers. The items only need to be fine enough for the min-max partition into
+// c chunks to balance: with whole layers every item is ≤ ~3-5 % of an SD decode, so c ≤ 8 uses one
+// band per layer (fewest launches); larger c splits every layer into ⌈c/8⌉ bands, in multiples of
+// the minimum aligned band (32 rows at ≥ 64-row layers, else max(8, H/2): conv tile rows and GN
+// 128-pixel chunks stay whole). Banding is bitwise neutral (I6). Measured (r01, SD VAE at latent
+// 128², c = 4): 32-row bands everywhere cost 48.8 ms vs 14.7 ms for the whole decode.
+static int bands_for(int n_chunks) { return std::min(4, std::max(1, (n_chunks + 7) / 8)); }
+static int band_rows(int H, int nbands) {
+  if (nbands <= 1) return H;
+  const int unit = H >= 64 ? 32 : std::max(8, H / 2);
+  const int rows = (H + nbands - 1) / nbands;
+  return std::max(unit, (rows + unit - 1) / unit * unit);
+}
 
 template <class AT>
 static AT* sb(DecodeState* s, int i) {
@@ -214,7 +226,7 @@ static void build_items(Engine* e, DecodeState* s) {
       const int t2 = other({cur, t1});
       const int t3 = other({cur, t1, t2});
       const int y = other({cur, t1, t2, t3});
-      const int br = band_rows(H, s->banded);
+      const int br = band_rows(H, s->nbands);
       auto push_gn = [&](int src, int dst, const float* gam, const float* bet, int C) {
         for (int yy = 0; yy < H; yy += br) {
           VItem v{VOP_GN_STATS, src, dst, 0, gam, C, 0, H, W, yy, std::min(H, yy + br), gn_id, 1};
@@ -256,7 +268,7 @@ static void build_items(Engine* e, DecodeState* s) {
       const int C = u.ch;
       H *= 2;
       W *= 2;
-      const int br = band_rows(H, s->banded);
+      const int br = band_rows(H, s->nbands);
       for (int yy = 0; yy < H; yy += br) {
         VItem v{VOP_UPSAMPLE, cur, 5, -1, nullptr, C, C, H, W, yy, std::min(H, yy + br), 0, 0};
         it.push_back(v);
@@ -274,7 +286,7 @@ static void build_items(Engine* e, DecodeState* s) {
   const int C0 = c.block_out[0];
   const int t1 = other({cur});
   {
-    const int br = band_rows(H, s->banded);
+    const int br = band_rows(H, s->nbands);
     for (int yy = 0; yy < H; yy += br) {
       VItem v{VOP_GN_STATS, cur, t1, 0, e->V.nout_g, C0, 0, H, W, yy, std::min(H, yy + br), gn_id, 1};
       it.push_back(v);
@@ -425,8 +437,8 @@ void vae_decode_chunk(Engine* e, const float* z, int h, int w, int n_chunks, int
     if (!s) s = new_decode(e, h, w);
     s->n_chunks = n_chunks;
     s->next_chunk = 0;
-    if (s->banded != (n_chunks > 1)) {
-      s->banded = n_chunks > 1;
+    if (s->nbands != bands_for(n_chunks)) {
+      s->nbands = bands_for(n_chunks);
       build_items(e, s);
     }
     s->bounds = chunk_bounds(s->cost, n_chunks);
@@ -448,6 +460,48 @@ void vae_decode_chunk(Engine* e, const float* z, int h, int w, int n_chunks, int
     e->free_decodes.push_back(s);
     *state = nullptr;
   }
+}
+
+// V2 independent-tile decode (R7 V2; oracle/vae.py decode_tiled): each
+// tile × tile block of the latent is decoded on its own from its halo-padded window (clipped at the
+// border) — tile-local GroupNorm and attention, an approximation of the whole decode — and its own
+// image region is cut out and written into the output (disjoint writes, no blending). Windows are
+// copied to a contiguous scratch latent; each window decode is a whole decode on the pooled states.
+void vae_decode_tiled(Engine* e, const float* z, int h, int w, int tile, int halo, float* image, cudaStream_t st) {
+  const int f = e->upscale();
+  const int wmax = std::min(h, tile + 2 * halo), vmax = std::min(w, tile + 2 * halo);
+  const size_t lat_elems = (size_t)4 * wmax * vmax, img_elems = (size_t)3 * f * wmax * f * vmax;
+  {
+    std::lock_guard<std::mutex> g(e->dmu);
+    const size_t need = (lat_elems + img_elems) * sizeof(float) + 256;
+    if (e->tile_scratch_bytes < need) {
+      if (e->tile_scratch) {
+        SD_CUDA(cudaStreamSynchronize(st));
+        cudaFree(e->tile_scratch);
+      }
+      SD_CUDA(cudaMalloc(&e->tile_scratch, need));
+      e->tile_scratch_bytes = need;
+    }
+  }
+  float* win = reinterpret_cast<float*>(e->tile_scratch);
+  float* timg = win + ((lat_elems + 63) & ~size_t(63));
+  for (int y0 = 0; y0 < h; y0 += tile)
+    for (int x0 = 0; x0 < w; x0 += tile) {
+      const int y1 = std::min(h, y0 + tile), x1 = std::min(w, x0 + tile);
+      const int a0 = std::max(0, y0 - halo), a1 = std::min(h, y1 + halo);
+      const int b0 = std::max(0, x0 - halo), b1 = std::min(w, x1 + halo);
+      const int wh = a1 - a0, ww = b1 - b0;
+      for (int c = 0; c < 4; ++c)
+        SD_CUDA(cudaMemcpy2DAsync(win + (size_t)c * wh * ww, (size_t)ww * 4, z + (size_t)c * h * w + (size_t)a0 * w + b0,
+                                  (size_t)w * 4, (size_t)ww * 4, wh, cudaMemcpyDeviceToDevice, st));
+      DecodeState* ds = nullptr;
+      vae_decode_chunk(e, win, wh, ww, 1, 0, &ds, timg, st);
+      const int H = f * h, W = f * w, TH = f * wh, TW = f * ww;
+      for (int c = 0; c < 3; ++c)
+        SD_CUDA(cudaMemcpy2DAsync(image + (size_t)c * H * W + (size_t)f * y0 * W + f * x0, (size_t)W * 4,
+                                  timg + (size_t)c * TH * TW + (size_t)f * (y0 - a0) * TW + f * (x0 - b0), (size_t)TW * 4,
+                                  (size_t)f * (x1 - x0) * 4, f * (y1 - y0), cudaMemcpyDeviceToDevice, st));
+    }
 }
 
 // min-max contiguous partition, boundaries placed as early as possible (oracle/vae.py chunk_ranges

@@ -124,6 +124,15 @@ class Engine:
             self.decode_chunk(latent, n_chunks, j, st, image, stream)
         return image
 
+    def decode_tiled(self, latent: torch.Tensor, tile: int, halo: int, image=None, stream=None):
+        """V2 independent-tile decode (an approximation; sd_vae_decode_tiled)."""
+        h, w = latent.shape[-2:]
+        if image is None:
+            f = self.upscale
+            image = torch.empty(3, f * h, f * w, device=latent.device, dtype=torch.float32)
+        B.call("sd_vae_decode_tiled", self.h, B._p(latent), h, w, tile, halo, B._p(image), _stream(stream))
+        return image
+
     def decode_chunk(self, latent, n_chunks, chunk, state: C.c_void_p, image, stream=None):
         h, w = latent.shape[-2:]
         B.call("sd_vae_decode_chunked", self.h, B._p(latent), h, w, n_chunks, chunk, C.byref(state), B._p(image),

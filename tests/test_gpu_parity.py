@@ -400,3 +400,48 @@ def test_sdxl_1024_full_size_properties():
             eng.release(s)
     finally:
         eng.close()
+
+
+def test_vae_tiled_v2(tiny):
+    """V2 independent tiles (R7 V2) on the GPU: equals the oracle's decode_tiled
+    on the same inputs (north-star 2e-2); reproduces the whole decode bitwise when the tile or the
+    halo covers the latent; and with a small halo it is the approximation it is meant to be (error
+    vs the whole decode > 0, shrinking as the halo grows)."""
+    eng, P, V, ctx_u = tiny
+    z = synth.initial_noise(7, 0, 16, 16)
+    zt = torch.from_numpy(z).cuda()
+    whole = eng.decode(zt, 1)
+    torch.cuda.synchronize()
+    assert torch.equal(eng.decode_tiled(zt, 16, 0), whole)
+    assert torch.equal(eng.decode_tiled(zt, 8, 8), whole)       # every window is the whole latent
+    errs = []
+    for halo in (0, 8):
+        t = eng.decode_tiled(zt, 8, halo)
+        torch.cuda.synchronize()
+        errs.append(rel(t.cpu().numpy(), whole.cpu().numpy()))
+    ref = vae.decode_tiled(V, configs.TINY_VAE, z[None], tile=8, halo=0)[0]
+    got = eng.decode_tiled(zt, 8, 0)
+    torch.cuda.synchronize()
+    r = rel(got.cpu().numpy(), ref)
+    print(f"tiled V2 tiny: vs oracle {r:.3e}; error vs whole decode halo 0: {errs[0]:.3e}, halo 8: {errs[1]:.3e}")
+    assert r <= TOL
+    assert errs[0] > 1e-3 and errs[1] == 0.0
+
+
+def test_vae_tiled_v2_sd_shape(sd15):
+    """V2 on the SD VAE at latent 32×32 (256² image): vs the oracle's decode_tiled (tile 16, halo 8;
+    four 24×24 windows) within 2e-2, and bitwise equal to the whole decode when tile ≥ latent."""
+    eng, _ = sd15
+    V = configs.vae_params(configs.SD_VAE, 0, np.float32, bf16_weights=True)
+    z = synth.initial_noise(7, 1, 32, 32)
+    zt = torch.from_numpy(z).cuda()
+    whole = eng.decode(zt, 1)
+    torch.cuda.synchronize()
+    assert torch.equal(eng.decode_tiled(zt, 32, 8), whole)
+    got = eng.decode_tiled(zt, 16, 8)
+    torch.cuda.synchronize()
+    ref = vae.decode_tiled(V, configs.SD_VAE, z[None], tile=16, halo=8)[0]
+    r = rel(got.cpu().numpy(), ref)
+    e = rel(got.cpu().numpy(), whole.cpu().numpy())
+    print(f"tiled V2 SD 32²: vs oracle {r:.3e}; vs whole decode {e:.3e}")
+    assert r <= TOL

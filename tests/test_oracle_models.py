@@ -161,6 +161,26 @@ def test_vae_halo0_negative_control(V64):
     assert np.linalg.norm(bad - whole) / np.linalg.norm(whole) > 1e-3
 
 
+def test_vae_tiled_v2_reductions_and_error(V64):
+    """V2 independent tiles (R7 V2). Pins: (1) a tile covering the image, or a
+    halo covering it, reduces to the whole decode exactly (each window IS the whole latent); (2) the
+    tile windows partition the latent (every latent pixel owned once, windows clipped at borders);
+    (3) it is an approximation — tile-local GroupNorm / attention — so with a small halo it differs
+    from the whole decode, and widening the halo brings it closer (the error-vs-halo curve)."""
+    z = synth.initial_noise(2, 0, 16, 16).astype(np.float64)[None]
+    whole = vae.decode(V64, TV, z)
+    np.testing.assert_allclose(vae.decode_tiled(V64, TV, z, tile=16, halo=0), whole, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(vae.decode_tiled(V64, TV, z, tile=8, halo=16), whole, rtol=1e-12, atol=1e-12)
+    owned = np.zeros((16, 16), int)
+    for (y0, y1, x0, x1), (a0, a1, b0, b1) in vae.tile_windows(16, 16, 8, 4):
+        owned[y0:y1, x0:x1] += 1
+        assert 0 <= a0 <= y0 < y1 <= a1 <= 16 and 0 <= b0 <= x0 < x1 <= b1 <= 16
+    assert (owned == 1).all()
+    err = [np.linalg.norm(vae.decode_tiled(V64, TV, z, tile=8, halo=h) - whole) / np.linalg.norm(whole)
+           for h in (0, 4, 8)]
+    assert err[0] > 1e-3 and err[2] < err[0] and err[2] == 0.0   # halo 8 ≥ image − tile: exact
+
+
 def _all_partitions(n, c):
     from itertools import combinations
     for cuts in combinations(range(1, n), c - 1):
