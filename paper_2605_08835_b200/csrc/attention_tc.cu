@@ -24,7 +24,8 @@ namespace sd {
 // NB = number of S (TMEM) / P (smem) buffers. NB = 2: one CTA per SM, S_{j+1} computed while the
 // softmax works on S_j. NB = 1: 256 TMEM columns and ~105 KB smem so two CTAs share an SM and
 // interleave their MMA / softmax phases (the MMA of S_{j+1} still overlaps the tail of softmax_j).
-template <int D, int NB, int SPLIT = 1, int EMU = 0>
+// PT = 1: P lives in TMEM (OP 4 / 5) — no P tile in smem, whose space goes to a deeper K/V ring
+template <int D, int NB, int SPLIT = 1, int EMU = 0, int PT = 0>
 struct TcAttn {
   static constexpr int BQ = 128, BK = 128;
   static constexpr int KQ = (D + 63) / 64;       // 64-column blocks of the head dim (Q/K tiles)
@@ -34,8 +35,8 @@ struct TcAttn {
   static constexpr int K_BYTES = KQ * BK * 128;
   static constexpr int V_BYTES = 2 * NPV * 128;  // two 64-key blocks of Vᵀ rows
   static constexpr int STAGE = K_BYTES + V_BYTES;
-  static constexpr int STAGES = (NB == 2 && D <= 64) ? 3 : 2;
-  static constexpr int P_BYTES = 2 * BQ * 128;   // one P tile: 128 rows × 128 keys bf16
+  static constexpr int STAGES = PT ? (NB == 2 && D <= 64 ? 4 : 3) : ((NB == 2 && D <= 64) ? 3 : 2);
+  static constexpr int P_BYTES = PT ? 0 : 2 * BQ * 128;  // one P tile: 128 rows × 128 keys bf16
   static constexpr int X_BYTES = 3 * 2 * 128 * 4;  // row-max / row-sum exchange of the SPLIT halves
   static constexpr int SMEM = 1024 + Q_BYTES + STAGES * STAGE + NB * P_BYTES + X_BYTES + 256;
   static constexpr int THREADS = 64 + 128 * SPLIT;
@@ -99,7 +100,7 @@ template <int D, int NB, int SPLIT, int EMU, int OP = 0>
 __global__ void __launch_bounds__(64 + 128 * SPLIT, 3 - NB)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tqk, const __grid_constant__ CUtensorMap tvt, bf16* __restrict__ O,
                    int ldo, int C, int P, int Lk, float scale_log2) {
-  using A = TcAttn<D, NB, SPLIT, EMU>;
+  using A = TcAttn<D, NB, SPLIT, EMU, (OP == 4 || OP == 5) ? 1 : 0>;
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned (SWIZZLE_128B atoms); offsetting the shared array itself keeps the pointer in the
   // shared state space, so the compiler emits STS / LDS rather than generic ST / LD
@@ -480,7 +481,7 @@ void make_tmap_2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t oute
 
 template <int D, int NB, int SPLIT, int EMU = 0, int OP = 0>
 static void launch_tc(const bf16* qk, const bf16* vt, bf16* O, int rows, int heads, int C, int P, cudaStream_t st) {
-  using A = TcAttn<D, NB, SPLIT, EMU>;
+  using A = TcAttn<D, NB, SPLIT, EMU, (OP == 4 || OP == 5) ? 1 : 0>;
   static bool set = false;
   if (!set) {
     SD_CUDA(cudaFuncSetAttribute(attn_tc_kernel<D, NB, SPLIT, EMU, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -514,8 +515,8 @@ static int attn_split() {
 //   5  one TMEM pass (OP 1), S released before the exps           0.784 ms
 //   6  one pass + 1/8 of the exps on the FMA pipe (OP 2)          0.769 ms
 //   7  one pass + 1/4 on the FMA pipe (OP 3)                      0.804 ms
-//   8  OP 2 + P kept in TMEM as the A operand of the PV MMA       0.751 ms (default; no P smem
-//      stores, no async-proxy fence)
+//   8  OP 2 + P kept in TMEM as the A operand of the PV MMA       0.751 ms → 0.664 ms once the freed
+//      P smem became a third K/V stage (default; no P smem stores, no async-proxy fence)
 static int attn_emu() {
   static int v = -1;
   if (v < 0) {

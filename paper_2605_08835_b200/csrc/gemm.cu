@@ -801,7 +801,12 @@ void gemm(const GemmDesc& d, cudaStream_t st) {
   memset(maps, 0, sizeof(maps));
   a.mode = d.mode;
   a.N = d.N;
-  int bn = d.bn ? d.bn : pick_bn(d.N, d.act);
+  static int bn_env = -1;  // SD_GEMM_BN: force the N tile of dense GEMMs (experiments)
+  if (bn_env < 0) {
+    const char* e = getenv("SD_GEMM_BN");
+    bn_env = e ? atoi(e) : 0;
+  }
+  int bn = d.bn ? d.bn : (bn_env && d.mode == GEMM_DENSE && d.act != ACT_GEGLU ? bn_env : pick_bn(d.N, d.act));
   if (d.act == ACT_GEGLU && bn % 128) throw CudaError("GEGLU needs BN multiple of 128");
   a.n_tiles = cdiv(d.N, bn);
   int m_boxes = 0;

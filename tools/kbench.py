@@ -26,6 +26,9 @@ VAE = [  # SD VAE decoder convs at 512² (one image, B = 1): (rows, H, W, Cin, C
 GEMM = [  # (M, N, K, act)
     (65536, 2560, 320, 2), (65536, 320, 1280, 0), (65536, 960, 320, 0), (65536, 320, 320, 0),
     (16384, 5120, 640, 2), (16384, 640, 2560, 0), (4096, 10240, 1280, 2), (4096, 1280, 5120, 0),
+    # 32×32 / 16×16 / 8×8 transformer projections (16 rows)
+    (16384, 640, 640, 0), (16384, 1280, 640, 0), (4096, 1280, 1280, 0), (4096, 2560, 1280, 0),
+    (1024, 1280, 1280, 0), (1024, 10240, 1280, 2),
 ]
 
 
