@@ -197,6 +197,12 @@ typedef struct {
   int32_t policy;               /* SD_POLICY_*: SynerDiff, or a baseline of P:316-324           */
   int32_t ablation;             /* SD_ABL_* bits (SynerDiff only); no chunking = c_max 1 */
   int64_t dyn_window_us;        /* Dynamic Batching collection window (0 = 500 000)        */
+  /* mixed resolutions: n_res tables, res_tables[i] profiled at latent res_hw[i];
+   * a window plans with the table of the largest resolution among its batch and decode-pending
+   * requests ("max multiplier"); n_res = 0: `table` for every request */
+  int32_t n_res;
+  const int32_t* res_hw;
+  const sd_table* const* res_tables;
 } sd_serve_config;
 /* Serving policies (§IV Baselines; semantics in oracle/serving.py):
  *  SYNERDIFF  the method: threshold-aware plan, Skip-CFG, VAE chunking, feedback controller;
@@ -216,6 +222,9 @@ typedef struct {
   int32_t emb_len, emb_dim;
   const float* pooled_host;     /* SDXL: fp32 [pooled_dim] pooled text embedding (else NULL / 0) */
   int32_t pooled_dim;
+  int32_t latent_hw;            /* this request's latent size (0 = the server's latent_hw); a
+                                   multiple of 8, <= the engine's max_latent_hw, with a table when
+                                   the server is mixed-resolution                                  */
 } sd_request;
 typedef struct {
   uint64_t id;
@@ -241,6 +250,10 @@ sd_status sd_get_load(sd_engine* e, int32_t* out4);
 sd_status sd_serve_simulate(const sd_serve_config* cfg, const sd_table* t, int32_t n, const uint64_t* ids,
                             const int64_t* arrival_us, const int32_t* n_steps, int64_t* U_out, int64_t* V_out,
                             int32_t* n_skips_out, int32_t* windows_out);
+/* The same with a latent size per request (mixed-resolution config: cfg->n_res tables). */
+sd_status sd_serve_simulate_mixed(const sd_serve_config* cfg, int32_t n, const uint64_t* ids, const int64_t* arrival_us,
+                                  const int32_t* n_steps, const int32_t* latent_hw, int64_t* U_out, int64_t* V_out,
+                                  int32_t* n_skips_out, int32_t* windows_out);
 
 /* ---- test-only exports (same library): single kernels on caller-owned device buffers --------- */
 /* D[M][N] = A[M][K] · B[N][K]^T + bias[N] (bf16 in, fp32 accumulate, bf16 or fp32 out). */

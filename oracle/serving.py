@@ -31,6 +31,13 @@ Baseline policies and ablations (PAPER.md:316-324 §IV Baselines, :395-397 §IV-
              threshold plan, no controller.
   ablations  of "synerdiff": no_skip (level pinned to 0: no Skip-CFG), no_ctl (controller frozen at
              its initial state); "no chunking" is c_star = c_max = 1.
+
+Mixed resolutions (PAPER.md:315 mixes 512/768/1024; reading R22 extended by the
+build): trace entries may carry a 4th field, the request's latent size r. With `res_tables`
+{r: {c: table}}, every window plans and times its stages with the table of the LARGEST resolution
+among its batch and its decode-pending requests (SPEC's "max multiplier"); the serial policy
+uses each request's own table, dynamic batching the batch's largest. On the GPU a round runs one
+sd_step_batch per resolution group of the stepping tasks.
 """
 from __future__ import annotations
 
@@ -45,6 +52,7 @@ class Task:
     id: int
     A: int
     n: int
+    r: int = 0          # latent size (mixed-resolution traces); 0 = the single table
     g: float = 7.5
     s: int = 0
     U: int | None = None
@@ -52,17 +60,24 @@ class Task:
     skips: list = field(default_factory=list)
 
 
+def _tasks(trace):
+    return sorted((Task(e[0], e[1], e[2], e[3] if len(e) > 3 else 0) for e in trace), key=lambda t: (t.A, t.id))
+
+
 def simulate(trace, tables, b_max=8, a_num=1, a_den=10, mode="exact", c_star=1, c_max=4, ctl_kw=None,
-             log=None, policy="synerdiff", no_skip=False, no_ctl=False, dyn_window_us=500_000, n_max=None):
-    """trace: [(id, arrival_us, n_steps)], tables: {c: {(m,n,k): (tau_us, delta_us)}}.
+             log=None, policy="synerdiff", no_skip=False, no_ctl=False, dyn_window_us=500_000, n_max=None,
+             res_tables=None):
+    """trace: [(id, arrival_us, n_steps[, latent_r])], tables: {c: {(m,n,k): (tau_us, delta_us)}};
+    res_tables (mixed resolutions): {r: {c: {...}}} — then `tables` is unused.
     Returns {id: Task}. `log` (list) receives one dict per window."""
     n_max = b_max if n_max is None else n_max
+    pick = (lambda ts: res_tables[max(t.r for t in ts)]) if res_tables else (lambda ts: tables)
     if policy == "serial":
-        return _serial(trace, tables)
+        return _serial(trace, pick)
     if policy == "dynamic":
-        return _dynamic(trace, tables, b_max, n_max, dyn_window_us)
+        return _dynamic(trace, pick, b_max, n_max, dyn_window_us)
     naive = policy == "naive"
-    pending = sorted((Task(i, a, n) for i, a, n in trace), key=lambda t: (t.A, t.id))
+    pending = _tasks(trace)
     pi = 0
     batch, dec, done = [], [], {}
     now = 0
@@ -83,6 +98,7 @@ def simulate(trace, tables, b_max=8, a_num=1, a_den=10, mode="exact", c_star=1, 
         M = len(batch)
         dq = sorted(dec, key=lambda t: (t.A, t.id))[:min(b_max, n_max)]
         N = len(dq)
+        tabs_w = pick(batch + dq)   # mixed resolutions: the table of the window's largest resolution
         elig = [t.s >= ctl.s_min(f, t.n) for t in batch]
         K = sum(elig)
         if N == 0:
@@ -90,9 +106,9 @@ def simulate(trace, tables, b_max=8, a_num=1, a_den=10, mode="exact", c_star=1, 
         elif naive:
             stages, tc, rounds = (((M, min(N, M), 0),) if M else ((0, N, 0),)), 1, 1
         else:
-            stages = sched.plan_window(tables[c], M, N, K, a_num, a_den, mode)
+            stages = sched.plan_window(tabs_w[c], M, N, K, a_num, a_den, mode)
             tc, rounds = c, c
-        tab = tables[tc]
+        tab = tabs_w[tc]
         mapping = sched.map_tasks(stages, [(t.id, t.s, t.n, e) for t, e in zip(batch, elig)],
                                   [(t.id, t.A) for t in dq])
         by_id = {t.id: t for t in batch + dq}
@@ -126,11 +142,11 @@ def simulate(trace, tables, b_max=8, a_num=1, a_den=10, mode="exact", c_star=1, 
     return done
 
 
-def _serial(trace, tables):
+def _serial(trace, pick):
     """Diffusers baseline: BS = 1, FCFS, denoise then decode, one request at a time."""
-    tab = tables[1]
     done, now = {}, 0
-    for t in sorted((Task(i, a, n) for i, a, n in trace), key=lambda t: (t.A, t.id)):
+    for t in _tasks(trace):
+        tab = pick([t])[1]
         now = max(now, t.A)
         tau, _ = tab[(1, 0, 0)]
         for _ in range(t.n):
@@ -144,10 +160,9 @@ def _serial(trace, tables):
     return done
 
 
-def _dynamic(trace, tables, b_max, n_max, window_us):
+def _dynamic(trace, pick, b_max, n_max, window_us):
     """Dynamic Batching baseline: collection window, lockstep, synchronous release."""
-    tab = tables[1]
-    pending = sorted((Task(i, a, n) for i, a, n in trace), key=lambda t: (t.A, t.id))
+    pending = _tasks(trace)
     done, now, pi = {}, 0, 0
     while pi < len(pending):
         first = pending[pi].A
@@ -158,6 +173,7 @@ def _dynamic(trace, tables, b_max, n_max, window_us):
         while pi < len(pending) and len(batch) < b_max and pending[pi].A <= now:
             batch.append(pending[pi])
             pi += 1
+        tab = pick(batch)[1]
         while any(t.s < t.n for t in batch):
             active = [t for t in batch if t.s < t.n]
             now += tab[(len(active), 0, 0)][0]

@@ -48,7 +48,8 @@ class ServeConfig(C.Structure):
     _fields_ = [("b_max", C.c_int32), ("a_num", C.c_int32), ("a_den", C.c_int32), ("dp_mode", C.c_int32),
                 ("c_star", C.c_int32), ("ctl", ControllerConfig), ("table", C.c_void_p), ("latent_hw", C.c_int32),
                 ("trace_seed", C.c_uint64), ("n_max", C.c_int32), ("policy", C.c_int32), ("ablation", C.c_int32),
-                ("dyn_window_us", C.c_int64)]
+                ("dyn_window_us", C.c_int64), ("n_res", C.c_int32), ("res_hw", C.POINTER(C.c_int32)),
+                ("res_tables", C.POINTER(C.c_void_p))]
 
 
 SD_POLICY_SYNERDIFF, SD_POLICY_NAIVE, SD_POLICY_DYNAMIC, SD_POLICY_SERIAL = 0, 1, 2, 3
@@ -60,7 +61,7 @@ POLICIES = {"synerdiff": SD_POLICY_SYNERDIFF, "naive": SD_POLICY_NAIVE, "dynamic
 class Request(C.Structure):
     _fields_ = [("id", C.c_uint64), ("arrival_us", C.c_int64), ("n_steps", C.c_int32), ("guidance", C.c_float),
                 ("text_emb_host", C.c_void_p), ("emb_len", C.c_int32), ("emb_dim", C.c_int32),
-                ("pooled_host", C.c_void_p), ("pooled_dim", C.c_int32)]
+                ("pooled_host", C.c_void_p), ("pooled_dim", C.c_int32), ("latent_hw", C.c_int32)]
 
 
 class Completion(C.Structure):
@@ -114,6 +115,8 @@ SIGNATURES = {
     "sd_set_global_load": [P, PI32, I32, C.c_uint64],
     "sd_get_load": [P, PI32],
     "sd_serve_simulate": [C.POINTER(ServeConfig), P, I32, C.POINTER(C.c_uint64), PI64, PI32, PI64, PI64, PI32, PI32],
+    "sd_serve_simulate_mixed": [C.POINTER(ServeConfig), I32, C.POINTER(C.c_uint64), PI64, PI32, PI32, PI64, PI64, PI32,
+                                PI32],
     "sd_debug_gemm": [P, P, P, P, I32, I32, I32, I32, I32, P],
     "sd_debug_set_gemm_cg": [I32],
     "sd_debug_set_conv_splits": [I32],

@@ -38,12 +38,22 @@ int64_t Loop::next_event() const {
   return next_arrival();
 }
 
+const Table* Loop::table_for(const std::vector<STask*>& a, const std::vector<STask*>& b) const {
+  if (res_tables.empty()) return table;
+  int r = 0;
+  for (auto* t : a) r = std::max(r, t->h);
+  for (auto* t : b) r = std::max(r, t->h);
+  for (auto& kv : res_tables)
+    if (kv.first == r) return kv.second;
+  throw std::invalid_argument("no latency table for latent " + std::to_string(r));
+}
+
 // one c = 1 round of stage (m, n, k) with the given tasks; returns the round end
-int64_t Loop::stage_round(Exec& ex, int m, int n, int k, const std::vector<STask*>& step,
+int64_t Loop::stage_round(Exec& ex, const Table* tb, int m, int n, int k, const std::vector<STask*>& step,
                           const std::vector<uint8_t>& skip, const std::vector<STask*>& decs,
                           std::vector<int64_t>* dd) {
   int64_t tau, delta;
-  if (!table->get(1, m, n, k, &tau, &delta))
+  if (!tb->get(1, m, n, k, &tau, &delta))
     throw std::invalid_argument("latency table miss (c,m,n,k)=(1," + std::to_string(m) + "," + std::to_string(n) +
                                 "," + std::to_string(k) + ")");
   dd->assign(decs.size(), -1);
@@ -62,14 +72,14 @@ bool Loop::serial_window(Exec& ex) {
   std::vector<int64_t> dd;
   if (!dec.empty()) {
     STask* t = dec.front();
-    stage_round(ex, 0, 1, 0, {}, {}, {t}, &dd);
+    stage_round(ex, table_for({t}, {}), 0, 1, 0, {}, {}, {t}, &dd);
     t->V = dd[0];
     dec.clear();
     ex.complete(t);
     return true;
   }
   STask* t = batch.front();
-  const int64_t end = stage_round(ex, 1, 0, 0, {t}, {0}, {}, &dd);
+  const int64_t end = stage_round(ex, table_for({t}, {}), 1, 0, 0, {t}, {0}, {}, &dd);
   if (++t->s == t->n) {
     t->U = end;
     batch.clear();
@@ -93,12 +103,13 @@ bool Loop::dynamic_window(Exec& ex) {
     pending.erase(pending.begin(), pending.begin() + taken);
   }
   std::vector<int64_t> dd;
+  const Table* tb = table_for(batch, {});
   std::vector<STask*> active;
   for (auto* t : batch)
     if (t->s < t->n) active.push_back(t);
   if (!active.empty()) {
     const int64_t end =
-        stage_round(ex, (int)active.size(), 0, 0, active, std::vector<uint8_t>(active.size(), 0), {}, &dd);
+        stage_round(ex, tb, (int)active.size(), 0, 0, active, std::vector<uint8_t>(active.size(), 0), {}, &dd);
     for (auto* t : active)
       if (++t->s == t->n) t->U = end;
     return true;
@@ -107,7 +118,7 @@ bool Loop::dynamic_window(Exec& ex) {
   std::vector<STask*> todo;
   for (auto* t : batch)
     if (std::find(dec.begin(), dec.end(), t) == dec.end() && (int)todo.size() < cfg.n_max) todo.push_back(t);
-  const int64_t end = stage_round(ex, 0, (int)todo.size(), 0, {}, {}, todo, &dd);
+  const int64_t end = stage_round(ex, tb, 0, (int)todo.size(), 0, {}, {}, todo, &dd);
   dec.insert(dec.end(), todo.begin(), todo.end());
   if (dec.size() == batch.size()) {  // synchronous release
     for (auto* t : batch) {
@@ -139,6 +150,7 @@ bool Loop::window(Exec& ex) {
   std::sort(dq.begin(), dq.end(), [](const STask* a, const STask* b) { return a->A != b->A ? a->A < b->A : a->id < b->id; });
   if ((int)dq.size() > std::min(cfg.b_max, cfg.n_max)) dq.resize(std::min(cfg.b_max, cfg.n_max));
   const int N = (int)dq.size();
+  const Table* tb = table_for(batch, dq);  // mixed resolutions: the window's largest latent
   std::vector<uint8_t> elig(M);
   int K = 0;
   for (int i = 0; i < M; ++i) {
@@ -152,7 +164,7 @@ bool Loop::window(Exec& ex) {
   } else if (naive) {  // InstGenIE: the whole batch with the oldest decodes, no plan, no skip
     plan.stages.push_back({M, M ? std::min(N, M) : N, 0});
   } else {
-    plan_window(*table, M, N, K, c, cfg.a_num, cfg.a_den, cfg.dp_mode, &plan);
+    plan_window(*tb, M, N, K, c, cfg.a_num, cfg.a_den, cfg.dp_mode, &plan);
     tc = c;
     rounds = c;
   }
@@ -186,7 +198,7 @@ bool Loop::window(Exec& ex) {
     }
     for (int q = 0; q < n; ++q) d_ids.push_back(dq[di++]);
     int64_t tau, delta;
-    if (!table->get(tc, m, n, k, &tau, &delta))
+    if (!tb->get(tc, m, n, k, &tau, &delta))
       throw std::invalid_argument("latency table miss (c,m,n,k)=(" + std::to_string(tc) + "," + std::to_string(m) + "," +
                                   std::to_string(n) + "," + std::to_string(k) + ")");
     const int64_t t0 = ex.now();
@@ -248,6 +260,11 @@ struct VirtualExec : Exec {
 }  // namespace sd
 
 namespace sd {
+void set_tables(Loop& L, const sd_serve_config* cfg) {
+  L.res_tables.clear();
+  for (int i = 0; i < cfg->n_res; ++i) L.res_tables.push_back({cfg->res_hw[i], &cfg->res_tables[i]->t});
+}
+
 void set_policy(LoopCfg& c, const sd_serve_config* cfg) {
   c.policy = cfg->policy;
   c.no_skip = (cfg->ablation & SD_ABL_NO_SKIP) != 0;
@@ -259,13 +276,14 @@ void set_policy(LoopCfg& c, const sd_serve_config* cfg) {
 using namespace sd;
 
 
-extern "C" sd_status sd_serve_simulate(const sd_serve_config* cfg, const sd_table* table, int32_t n,
-                                       const uint64_t* ids, const int64_t* arrival_us, const int32_t* n_steps,
-                                       int64_t* U_out, int64_t* V_out, int32_t* n_skips_out, int32_t* windows_out) {
-  SD_REQUIRE(cfg && table && n >= 0 && (n == 0 || (ids && arrival_us && n_steps && U_out && V_out)),
+static sd_status simulate_impl(const sd_serve_config* cfg, const sd_table* table, int32_t n, const uint64_t* ids,
+                               const int64_t* arrival_us, const int32_t* n_steps, const int32_t* latent_hw,
+                               int64_t* U_out, int64_t* V_out, int32_t* n_skips_out, int32_t* windows_out) {
+  SD_REQUIRE(cfg && (table || cfg->n_res > 0) && n >= 0 && (n == 0 || (ids && arrival_us && n_steps && U_out && V_out)),
              "sd_serve_simulate: bad args");
   SD_REQUIRE(cfg->b_max >= 1 && cfg->a_den > 0 && cfg->c_star >= 1 && cfg->ctl.c_max >= cfg->c_star,
              "sd_serve_simulate: bad config");
+  SD_REQUIRE(cfg->n_res == 0 || (cfg->res_hw && cfg->res_tables && latent_hw), "sd_serve_simulate: mixed tables");
   for (int i = 0; i < n; ++i) SD_REQUIRE(n_steps[i] >= 1 && arrival_us[i] >= 0, "sd_serve_simulate: bad request");
   SD_API_BEGIN
   std::vector<STask> tasks(n);
@@ -276,15 +294,17 @@ extern "C" sd_status sd_serve_simulate(const sd_serve_config* cfg, const sd_tabl
   L.cfg.a_den = cfg->a_den;
   L.cfg.dp_mode = cfg->dp_mode;
   L.cfg.c_star = cfg->c_star;
-  L.table = &table->t;
+  L.table = table ? &table->t : nullptr;
   L.ctl.cfg = cfg->ctl;
   L.ctl.cfg.c_star = cfg->c_star;
   L.ctl.c = cfg->c_star;
   set_policy(L.cfg, cfg);
+  set_tables(L, cfg);
   for (int i = 0; i < n; ++i) {
     tasks[i].id = ids[i];
     tasks[i].A = arrival_us[i];
     tasks[i].n = n_steps[i];
+    tasks[i].h = tasks[i].w = latent_hw ? latent_hw[i] : 0;
     insert_pending(L.pending, &tasks[i]);
   }
   VirtualExec ex;
@@ -303,4 +323,19 @@ extern "C" sd_status sd_serve_simulate(const sd_serve_config* cfg, const sd_tabl
   }
   if (windows_out) *windows_out = windows;
   SD_API_END
+}
+
+extern "C" sd_status sd_serve_simulate(const sd_serve_config* cfg, const sd_table* table, int32_t n,
+                                       const uint64_t* ids, const int64_t* arrival_us, const int32_t* n_steps,
+                                       int64_t* U_out, int64_t* V_out, int32_t* n_skips_out, int32_t* windows_out) {
+  SD_REQUIRE(table, "sd_serve_simulate: null table");
+  return simulate_impl(cfg, table, n, ids, arrival_us, n_steps, nullptr, U_out, V_out, n_skips_out, windows_out);
+}
+
+extern "C" sd_status sd_serve_simulate_mixed(const sd_serve_config* cfg, int32_t n, const uint64_t* ids,
+                                             const int64_t* arrival_us, const int32_t* n_steps,
+                                             const int32_t* latent_hw, int64_t* U_out, int64_t* V_out,
+                                             int32_t* n_skips_out, int32_t* windows_out) {
+  SD_REQUIRE(cfg && cfg->n_res > 0, "sd_serve_simulate_mixed: the config needs n_res tables");
+  return simulate_impl(cfg, nullptr, n, ids, arrival_us, n_steps, latent_hw, U_out, V_out, n_skips_out, windows_out);
 }

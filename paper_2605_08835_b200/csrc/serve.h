@@ -69,6 +69,7 @@ struct Exec {
 struct Loop {
   LoopCfg cfg;
   const Table* table = nullptr;
+  std::vector<std::pair<int, const Table*>> res_tables;  // mixed resolutions: latent hw → table
   Controller ctl;
   std::vector<STask*> pending;  // sorted by (A, id)
   std::vector<STask*> batch, dec;
@@ -81,14 +82,17 @@ struct Loop {
   int64_t next_event() const;
 
  private:
+  // the table of the largest latent among `a` and `b` (mixed resolutions), else `table`
+  const Table* table_for(const std::vector<STask*>& a, const std::vector<STask*>& b) const;
   bool serial_window(Exec& ex);
   bool dynamic_window(Exec& ex);
   int64_t dynamic_dispatch_time() const;
-  int64_t stage_round(Exec& ex, int m, int n, int k, const std::vector<STask*>& step, const std::vector<uint8_t>& skip,
-                      const std::vector<STask*>& decs, std::vector<int64_t>* dd);
+  int64_t stage_round(Exec& ex, const Table* tb, int m, int n, int k, const std::vector<STask*>& step,
+                      const std::vector<uint8_t>& skip, const std::vector<STask*>& decs, std::vector<int64_t>* dd);
 };
 
 void insert_pending(std::vector<STask*>& pending, STask* t);
 void set_policy(LoopCfg& c, const sd_serve_config* cfg);
+void set_tables(Loop& L, const sd_serve_config* cfg);
 
 }  // namespace sd

@@ -5,7 +5,9 @@
 #include <math.h>
 #include <string.h>
 
+#include <algorithm>
 #include <chrono>
+#include <map>
 #include <condition_variable>
 #include <deque>
 #include <thread>
@@ -77,10 +79,13 @@ struct Server {
   float* pinned_noise = nullptr;
   float* pinned_emb = nullptr;
   float* emb_dev = nullptr;  // device copy of one admission's embedding (+ pooled)
+  std::vector<int> res_hw;   // mixed resolutions: the latent sizes with a table (copied at start)
   // per-request buffers are recycled (cudaMalloc / cudaFree / cudaMallocHost in the loop would
   // stall it; cudaFree synchronises the whole device, i.e. the concurrent UNet round too)
-  std::vector<float*> pool_lat, pool_img, pool_host;
-  float* take(std::vector<float*>& pool, size_t bytes, bool host) {
+  // keyed by buffer size (mixed resolutions)
+  std::map<size_t, std::vector<float*>> pool_lat, pool_img, pool_host;
+  float* take(std::map<size_t, std::vector<float*>>& pools, size_t bytes, bool host) {
+    auto& pool = pools[bytes];
     if (!pool.empty()) {
       float* p = pool.back();
       pool.pop_back();
@@ -128,21 +133,27 @@ int64_t GpuExec::round(const std::vector<STask*>& step, const std::vector<uint8_
                        const std::vector<STask*>& decs, int rho, int rounds, int64_t, int64_t, int64_t,
                        std::vector<int64_t>* dd) {
   Engine* e = S->e;
-  if (!step.empty()) {
-    const int n = (int)step.size();
-    std::vector<float*> lat(n);
-    std::vector<int32_t> s(n), ns(n), slot(n);
-    std::vector<uint8_t> hu(n);
-    std::vector<float> g(n);
-    for (int i = 0; i < n; ++i) {
-      lat[i] = step[i]->lat;
-      s[i] = step[i]->s;
-      ns[i] = step[i]->n;
-      hu[i] = skip[i] ? 0 : 1;
-      g[i] = step[i]->g;
-      slot[i] = step[i]->slot;
+  // one sd_step_batch per resolution group of the stepping tasks (ascending latent size; batch order
+  // within a group) — a single group unless the server is mixed-resolution
+  std::vector<int> sizes;
+  for (STask* t : step)
+    if (std::find(sizes.begin(), sizes.end(), t->h) == sizes.end()) sizes.push_back(t->h);
+  std::sort(sizes.begin(), sizes.end());
+  for (int hw : sizes) {
+    std::vector<float*> lat;
+    std::vector<int32_t> s, ns, slot;
+    std::vector<uint8_t> hu;
+    std::vector<float> g;
+    for (size_t i = 0; i < step.size(); ++i) {
+      if (step[i]->h != hw) continue;
+      lat.push_back(step[i]->lat);
+      s.push_back(step[i]->s);
+      ns.push_back(step[i]->n);
+      hu.push_back(skip[i] ? 0 : 1);
+      g.push_back(step[i]->g);
+      slot.push_back(step[i]->slot);
     }
-    sd_batch b{n, step[0]->h, step[0]->w, lat.data(), s.data(), ns.data(), hu.data(), g.data(), slot.data()};
+    sd_batch b{(int)lat.size(), hw, hw, lat.data(), s.data(), ns.data(), hu.data(), g.data(), slot.data()};
     step_batch(e, &b, S->hi);
   }
   for (STask* t : decs) {
@@ -171,8 +182,8 @@ void GpuExec::complete(STask* t) {
     if (t->slot > 0) S->e->slot_used[t->slot] = 0;
   }
   std::lock_guard<std::mutex> g(S->mu);
-  S->pool_lat.push_back(t->lat);
-  S->pool_img.push_back(t->img_dev);
+  S->pool_lat[(size_t)4 * t->h * t->w * 4].push_back(t->lat);
+  S->pool_img[bytes].push_back(t->img_dev);
   t->lat = t->img_dev = nullptr;
   S->completed.push_back(t);
   S->counters[3]++;
@@ -223,7 +234,8 @@ using namespace sd;
 static Server* server_of(sd_engine* e) { return reinterpret_cast<Server*>(e->e.server); }
 
 extern "C" sd_status sd_serve_start(sd_engine* e, const sd_serve_config* cfg) {
-  SD_REQUIRE(e && cfg && cfg->table, "sd_serve_start: bad args");
+  SD_REQUIRE(e && cfg && (cfg->table || cfg->n_res > 0), "sd_serve_start: bad args");
+  SD_REQUIRE(cfg->n_res == 0 || (cfg->res_hw && cfg->res_tables), "sd_serve_start: mixed-resolution tables");
   SD_REQUIRE(!e->e.server, "sd_serve_start: already serving");
   SD_REQUIRE(cfg->b_max >= 1 && cfg->b_max <= e->e.cfg.b_max, "sd_serve_start: b_max exceeds the engine's");
   SD_REQUIRE(cfg->latent_hw >= 8 && cfg->latent_hw <= e->e.cfg.max_latent_hw, "sd_serve_start: latent_hw");
@@ -240,6 +252,10 @@ extern "C" sd_status sd_serve_start(sd_engine* e, const sd_serve_config* cfg) {
   S->loop.cfg.dp_mode = cfg->dp_mode;
   S->loop.cfg.c_star = cfg->c_star;
   set_policy(S->loop.cfg, cfg);
+  set_tables(S->loop, cfg);
+  S->res_hw.assign(cfg->res_hw, cfg->res_hw + cfg->n_res);
+  S->cfg.res_hw = nullptr;  // the caller's arrays need not outlive sd_serve_start (tables must)
+  S->cfg.res_tables = nullptr;
   S->loop.table = &cfg->table->t;
   S->loop.ctl.cfg = cfg->ctl;
   S->loop.ctl.cfg.c_star = cfg->c_star;
@@ -251,7 +267,7 @@ extern "C" sd_status sd_serve_start(sd_engine* e, const sd_serve_config* cfg) {
   SD_CUDA(cudaStreamCreateWithPriority(&S->lo, cudaStreamNonBlocking, lo_p));
   SD_CUDA(cudaEventCreateWithFlags(&S->ev_hi, cudaEventDisableTiming));
   SD_CUDA(cudaEventCreateWithFlags(&S->ev_lo, cudaEventDisableTiming));
-  const size_t hw = (size_t)cfg->latent_hw * cfg->latent_hw;
+  const size_t hw = (size_t)e->e.cfg.max_latent_hw * e->e.cfg.max_latent_hw;  // any request resolution
   SD_CUDA(cudaMallocHost(&S->pinned_noise, 4 * hw * 4));
   SD_CUDA(cudaMallocHost(&S->pinned_emb, ((size_t)e->e.uc.ctx_len * e->e.uc.ctx_dim + e->e.uc.pooled_dim) * 4));
   SD_CUDA(cudaMalloc(&S->emb_dev, ((size_t)e->e.uc.ctx_len * e->e.uc.ctx_dim + e->e.uc.pooled_dim) * 4));
@@ -270,6 +286,15 @@ extern "C" sd_status sd_submit(sd_engine* e, const sd_request* r) {
                                         : (r->pooled_host && r->pooled_dim == e->e.uc.pooled_dim),
              "sd_submit: pooled embedding (required for SDXL, absent otherwise)");
   Server* S = server_of(e);
+  {
+    const int hw = r->latent_hw > 0 ? r->latent_hw : S->cfg.latent_hw;
+    const int L = (int)e->e.uc.block_out.size();
+    SD_REQUIRE(hw >= 8 && hw <= e->e.cfg.max_latent_hw && hw % (1 << (L - 1)) == 0 && hw % 8 == 0,
+               "sd_submit: latent_hw");
+    bool ok = S->res_hw.empty() ? hw == S->cfg.latent_hw : false;
+    for (int r : S->res_hw) ok = ok || r == hw;
+    SD_REQUIRE(ok, "sd_submit: no latency table for this latent size");
+  }
   if (e->e.failed) {
     set_error("engine FAILED: " + S->error);
     return SD_E_STATE;
@@ -279,7 +304,7 @@ extern "C" sd_status sd_submit(sd_engine* e, const sd_request* r) {
   t->A = r->arrival_us;
   t->n = r->n_steps;
   t->g = r->guidance;
-  t->h = t->w = S->cfg.latent_hw;
+  t->h = t->w = r->latent_hw > 0 ? r->latent_hw : S->cfg.latent_hw;
   t->emb.assign(r->text_emb_host, r->text_emb_host + (size_t)r->emb_len * r->emb_dim);
   t->emb_len = r->emb_len;
   t->emb_dim = r->emb_dim;
@@ -331,7 +356,8 @@ extern "C" sd_status sd_release(sd_engine* e, uint64_t id) {
   std::lock_guard<std::mutex> g(S->mu);
   auto it = S->owned.find(id);
   SD_REQUIRE(it != S->owned.end() && it->second->V >= 0, "sd_release: unknown or unfinished id");
-  if (it->second->img_host) S->pool_host.push_back(it->second->img_host);
+  if (it->second->img_host)
+    S->pool_host[(size_t)3 * 64 * it->second->h * it->second->w * 4].push_back(it->second->img_host);
   delete it->second;
   S->owned.erase(it);
   return SD_OK;
@@ -356,9 +382,12 @@ extern "C" sd_status sd_serve_stop(sd_engine* e) {
     if (t->decode) destroy_decode(&e->e, reinterpret_cast<DecodeState*>(t->decode));
     delete t;
   }
-  for (float* p : S->pool_lat) cudaFree(p);
-  for (float* p : S->pool_img) cudaFree(p);
-  for (float* p : S->pool_host) cudaFreeHost(p);
+  for (auto& kv : S->pool_lat)
+    for (float* p : kv.second) cudaFree(p);
+  for (auto& kv : S->pool_img)
+    for (float* p : kv.second) cudaFree(p);
+  for (auto& kv : S->pool_host)
+    for (float* p : kv.second) cudaFreeHost(p);
   cudaFreeHost(S->pinned_noise);
   cudaFreeHost(S->pinned_emb);
   cudaFree(S->emb_dev);

@@ -260,3 +260,36 @@ def test_serving_policies_bitexact(policy, ablation, cstar, cmax):
     if ablation & B.SD_ABL_NO_SKIP or policy != "synerdiff":
         assert sum(ns) == 0
     B.lib().sd_table_free(h)
+
+
+@pytest.mark.parametrize("policy", ["synerdiff", "naive", "dynamic", "serial"])
+def test_serving_mixed_resolution_bitexact(policy):
+    """Mixed-resolution traces: the C++ loop with per-resolution tables equals
+    oracle/serving.py (largest-resolution table per window) for every request's (U, V, #skips)."""
+    from oracle import serving
+    rng = np.random.default_rng(31 + len(policy))
+    tabs = {64: serve_table(rng), 96: serve_table(rng)}
+    for r in tabs[96]:  # the 768² table is slower
+        tabs[96][r] = {k: (2 * v[0] + 100, 2 * v[1] + 50) for k, v in tabs[96][r].items()}
+    handles = {r: make_multi_table(t) for r, t in tabs.items()}
+    n = 80
+    arr = np.cumsum(rng.exponential(1e6 / 6.0, n)).astype(np.int64)
+    steps = rng.integers(20, 51, n)
+    res = rng.choice([64, 96], n)
+    ctl_cfg = B.ControllerConfig(1, 4, 10, 3, 1, 2, -1, 5)
+    hw = (C.c_int32 * 2)(64, 96)
+    tbl = (C.c_void_p * 2)(handles[64].value, handles[96].value)
+    cfg = B.ServeConfig(8, 1, 10, 0, 1, ctl_cfg, None, 64, 1, 4, B.POLICIES[policy], 0, 300_000, 2,
+                        C.cast(hw, C.POINTER(C.c_int32)), C.cast(tbl, C.POINTER(C.c_void_p)))
+    U, V = (C.c_int64 * n)(), (C.c_int64 * n)()
+    ns, win = (C.c_int32 * n)(), C.c_int32()
+    B.call("sd_serve_simulate_mixed", C.byref(cfg), n, (C.c_uint64 * n)(*range(n)), (C.c_int64 * n)(*arr.tolist()),
+           (C.c_int32 * n)(*steps.tolist()), (C.c_int32 * n)(*res.tolist()), U, V, ns, C.byref(win))
+    trace = [(i, int(arr[i]), int(steps[i]), int(res[i])) for i in range(n)]
+    done = serving.simulate(trace, None, b_max=8, c_star=1, c_max=4, policy=policy, dyn_window_us=300_000, n_max=4,
+                            res_tables=tabs)
+    for i in range(n):
+        t = done[i]
+        assert (U[i], V[i], ns[i]) == (t.U, t.V, len(t.skips)), (policy, i)
+    for h in handles.values():
+        B.lib().sd_table_free(h)

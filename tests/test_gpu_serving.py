@@ -161,3 +161,55 @@ def test_serving_baseline_policies_tiny(policy):
         assert len({r[2] for r in got.values()}) < n          # members of a batch share V (release)
     eng.close()
     B.lib().sd_table_free(tab)
+
+
+def test_serving_mixed_resolutions_tiny():
+    """Mixed-resolution serving: requests at latent 8 and 16 share the batch; each
+    round runs one sd_step_batch per resolution group; every image equals the request run alone at
+    its own resolution (bitwise) and has that resolution's size."""
+    eng = Engine("tiny", max_latent_hw=16, b_max=4, c_max=3)
+    ctx_u = synth.uncond_embedding(0, 8, 32)
+    eng.set_uncond(torch.from_numpy(ctx_u))
+    t8, t16 = _table(), _table()
+    hw = (C.c_int32 * 2)(8, 16)
+    tbl = (C.c_void_p * 2)(t8.value, t16.value)
+    ctl = B.ControllerConfig(1, 3, 4, 1, 1, 1_000_000, -1, 5)
+    cfg = B.ServeConfig(4, 1, 10, 0, 1, ctl, None, 8, 5, 0, B.POLICIES["synerdiff"], 0, 0, 2,
+                        C.cast(hw, C.POINTER(C.c_int32)), C.cast(tbl, C.POINTER(C.c_void_p)))
+    B.call("sd_serve_start", eng.h, C.byref(cfg))
+    n = 8
+    embs = [synth.text_embedding(6, i, 8, 32) for i in range(n)]
+    steps = [4, 5, 4, 6, 4, 5, 4, 6]
+    res = [8, 16, 16, 8, 16, 8, 8, 16]
+    for i in range(n):
+        r = B.Request(i, 1500 * i, steps[i], 7.5, embs[i].ctypes.data, 8, 32, None, 0, res[i])
+        B.call("sd_submit", eng.h, C.byref(r))
+    got = {}
+    out = (B.Completion * 16)()
+    cnt = C.c_int32()
+    for _ in range(600):
+        B.call("sd_poll", eng.h, out, 16, C.byref(cnt), 50)
+        for j in range(cnt.value):
+            c_ = out[j]
+            img = np.ctypeslib.as_array(C.cast(c_.image_host, C.POINTER(C.c_float)), shape=(3, c_.h, c_.w)).copy()
+            skips = [c_.skipped_steps[q] for q in range(c_.n_skipped)]
+            got[c_.id] = (c_.arrival_us, c_.denoise_done_us, c_.decode_done_us, skips, img)
+            B.call("sd_release", eng.h, c_.id)
+        if len(got) == n:
+            break
+    B.call("sd_serve_stop", eng.h)
+    assert len(got) == n
+    for i in range(n):
+        A, U, Vt, skips, img = got[i]
+        assert A <= U <= Vt and img.shape == (3, 2 * res[i], 2 * res[i])
+        slot = eng.register(torch.from_numpy(embs[i]))
+        lat = [torch.from_numpy(synth.initial_noise(5, i, res[i], res[i])).cuda()]
+        for s in range(steps[i]):
+            eng.step(lat, [s], [steps[i]], [0 if s in skips else 1], [7.5], [slot])
+        alone = eng.decode(lat[0], 1)
+        torch.cuda.synchronize()
+        eng.release(slot)
+        assert np.array_equal(alone.cpu().numpy(), img), i
+    eng.close()
+    B.lib().sd_table_free(t8)
+    B.lib().sd_table_free(t16)

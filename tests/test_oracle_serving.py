@@ -187,3 +187,20 @@ def test_policies_complete_every_request_fcfs_invariants():
         if pol == "serial":  # FCFS, one at a time: completions in arrival order, no overlap
             order = sorted(done.values(), key=lambda t: (t.A, t.id))
             assert all(a.V <= b.U for a, b in zip(order, order[1:]))
+
+
+# ---- mixed resolutions ----------------------------------------------------
+def test_mixed_resolution_window_uses_largest_table():
+    """A window plans and times with the table of its largest resolution (SPEC S:152 max multiplier):
+    a lone small request runs at the small table's τ; once a large request shares its windows, every
+    round runs at the large table's τ; a single-resolution trace reproduces the plain simulation."""
+    small, big = table(), {c: {k: (3 * v[0], 3 * v[1]) for k, v in t.items()} for c, t in table().items()}
+    res = {8: small, 16: big}
+    done = serving.simulate([(0, 0, 4, 8)], None, res_tables=res)
+    assert done[0].U == 4 * small[1][(1, 0, 0)][0]
+    done = serving.simulate([(0, 0, 4, 8), (1, 0, 4, 16)], None, res_tables=res)
+    assert done[0].U == done[1].U == 4 * big[1][(2, 0, 0)][0]
+    tr = [(i, 200_000 * i, 20 + (7 * i) % 13) for i in range(20)]
+    a = serving.simulate(tr, small)
+    b = serving.simulate([(i, A, n, 8) for i, A, n in tr], None, res_tables=res)
+    assert all((a[i].U, a[i].V) == (b[i].U, b[i].V) for i in a)
