@@ -46,19 +46,30 @@ def p99(values):
 
 def run_trace(eng, table_h, trace, latent_hw=64, b_max=8, c_star=1, c_max=2, dp_mode=0, guidance=7.5,
               trace_seed=7, ctl=None, timeout_s=600, n_max=None, policy="synerdiff", ablation=0,
-              dyn_window_us=500_000):
-    """Serve `trace` [(id, arrival_us, n_steps)] on `eng`; returns per-request records and metrics.
+              dyn_window_us=500_000, res_tables=None):
+    """Serve `trace` [(id, arrival_us, n_steps[, latent_hw])] on `eng`; returns per-request records and
+    metrics. `res_tables` {latent_hw: table handle} makes the server mixed-resolution.
     Arrival times are relative to sd_serve_start; all requests are submitted up front and admitted
     by the server when their arrival time has passed. `policy` selects SynerDiff or one of the
     paper's baselines, `ablation` the SD_ABL_* bits."""
     ctl = ctl or B.ControllerConfig(c_star, c_max, 10, 3, 1, 2, -1, 5)
     cfg = B.ServeConfig(b_max, 1, 10, dp_mode, c_star, ctl, table_h, latent_hw, trace_seed, n_max or 0,
                         B.POLICIES[policy], ablation, dyn_window_us)
-    embs = {i: np.ascontiguousarray(synth.text_embedding(trace_seed, i, eng.ctx_len, eng.ctx_dim)) for i, _, _ in trace}
+    if res_tables:
+        keys = sorted(res_tables)
+        hw_arr = (C.c_int32 * len(keys))(*keys)
+        tb_arr = (C.c_void_p * len(keys))(*[res_tables[k].value for k in keys])
+        cfg.n_res = len(keys)
+        cfg.res_hw = C.cast(hw_arr, C.POINTER(C.c_int32))
+        cfg.res_tables = C.cast(tb_arr, C.POINTER(C.c_void_p))
+    embs = {e[0]: np.ascontiguousarray(synth.text_embedding(trace_seed, e[0], eng.ctx_len, eng.ctx_dim))
+            for e in trace}
     B.call("sd_serve_start", eng.h, C.byref(cfg))
     try:
-        for i, a, n in trace:
-            r = B.Request(i, a, n, guidance, embs[i].ctypes.data, eng.ctx_len, eng.ctx_dim)
+        for e in trace:
+            i, a, n = e[:3]
+            r = B.Request(i, a, n, guidance, embs[i].ctypes.data, eng.ctx_len, eng.ctx_dim, None, 0,
+                          e[3] if len(e) > 3 else 0)
             B.call("sd_submit", eng.h, C.byref(r))
         out = (B.Completion * 64)()
         cnt = C.c_int32()
@@ -78,5 +89,5 @@ def run_trace(eng, table_h, trace, latent_hw=64, b_max=8, c_star=1, c_max=2, dp_
     span = max(r["V"] for r in recs.values()) - min(r["A"] for r in recs.values())
     metrics = dict(n=len(e2e), images_per_s=len(e2e) / (span / 1e6), mean_e2e_ms=float(np.mean(e2e)) / 1e3,
                    p99_e2e_ms=p99(e2e) / 1e3, skipped_steps=int(sum(r["skips"] for r in recs.values())),
-                   denoise_steps=int(sum(n for _, _, n in trace)))
+                   denoise_steps=int(sum(e[2] for e in trace)))
     return recs, metrics
