@@ -35,7 +35,8 @@ class Profiler:
         self.dec = [torch.randn(4, h, w, generator=g).to(dev) for _ in range(b_max)]
         self.img = [torch.empty(3, eng.upscale * h, eng.upscale * w, device=dev) for _ in range(b_max)]
         emb = torch.randn(eng.ctx_len, eng.ctx_dim, generator=g)
-        self.slots = [eng.register(emb) for _ in range(b_max)]
+        pooled = torch.randn(eng.pooled_dim, generator=g) if eng.pooled_dim else None  # SDXL added conditioning
+        self.slots = [eng.register(emb, pooled) for _ in range(b_max)]
 
     def close(self):
         for s in self.slots:

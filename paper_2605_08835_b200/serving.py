@@ -64,12 +64,14 @@ def run_trace(eng, table_h, trace, latent_hw=64, b_max=8, c_star=1, c_max=2, dp_
         cfg.res_tables = C.cast(tb_arr, C.POINTER(C.c_void_p))
     embs = {e[0]: np.ascontiguousarray(synth.text_embedding(trace_seed, e[0], eng.ctx_len, eng.ctx_dim))
             for e in trace}
+    pooled = {e[0]: np.ascontiguousarray(synth.pooled_embedding(trace_seed, e[0], eng.pooled_dim))
+              for e in trace} if eng.pooled_dim else {}
     B.call("sd_serve_start", eng.h, C.byref(cfg))
     try:
         for e in trace:
             i, a, n = e[:3]
-            r = B.Request(i, a, n, guidance, embs[i].ctypes.data, eng.ctx_len, eng.ctx_dim, None, 0,
-                          e[3] if len(e) > 3 else 0)
+            r = B.Request(i, a, n, guidance, embs[i].ctypes.data, eng.ctx_len, eng.ctx_dim,
+                          pooled[i].ctypes.data if pooled else None, eng.pooled_dim, e[3] if len(e) > 3 else 0)
             B.call("sd_submit", eng.h, C.byref(r))
         out = (B.Completion * 64)()
         cnt = C.c_int32()
