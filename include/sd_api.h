@@ -240,6 +240,12 @@ sd_status sd_submit(sd_engine* e, const sd_request* r);    /* thread-safe; copie
 sd_status sd_poll(sd_engine* e, sd_completion* out, int32_t max, int32_t* n_out, int32_t timeout_ms);
 sd_status sd_release(sd_engine* e, uint64_t id);           /* frees the completion's image        */
 sd_status sd_serve_stop(sd_engine* e);                     /* drains nothing; stops the thread    */
+/* Controller trajectory (one record per planned window, in order): start / end µs, M, N, K, the level
+ * and chunk count the window ran with, the waiting queue the controller then observed, its new level
+ * and chunk count. Any output array may be NULL. Call before sd_serve_stop. */
+sd_status sd_serve_window_log(sd_engine* e, int32_t max, int64_t* t_start, int64_t* t_end, int32_t* m, int32_t* n,
+                              int32_t* k, int32_t* level, int32_t* c, int32_t* waiting, int32_t* level_after,
+                              int32_t* c_after, int32_t* n_out);
 /* loads = int32 [P][4] {waiting, decode-pending, active, completed} all-gathered over ranks (C1);
  * the controller then sums `waiting` over ranks. sd_get_load returns this rank's 4 counters. */
 sd_status sd_set_global_load(sd_engine* e, const int32_t* loads, int32_t P, uint64_t epoch);

@@ -112,6 +112,7 @@ SIGNATURES = {
     "sd_poll": [P, C.POINTER(Completion), I32, PI32, I32],
     "sd_release": [P, C.c_uint64],
     "sd_serve_stop": [P],
+    "sd_serve_window_log": [P, I32, PI64, PI64, PI32, PI32, PI32, PI32, PI32, PI32, PI32, PI32, PI32],
     "sd_set_global_load": [P, PI32, I32, C.c_uint64],
     "sd_get_load": [P, PI32],
     "sd_serve_simulate": [C.POINTER(ServeConfig), P, I32, C.POINTER(C.c_uint64), PI64, PI32, PI64, PI64, PI32, PI32],

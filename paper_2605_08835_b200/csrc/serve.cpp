@@ -168,7 +168,11 @@ bool Loop::window(Exec& ex) {
     tc = c;
     rounds = c;
   }
-  if (log) log->push_back(WindowLog{now, M, N, K, level, c, plan.stages});
+  if (log) {
+    std::unique_lock<std::mutex> g;
+    if (log_mu) g = std::unique_lock<std::mutex>(*log_mu);
+    log->push_back(WindowLog{now, M, N, K, level, c, plan.stages});
+  }
   // task mapping E (R14)
   std::vector<STask*> el;
   for (int i = 0; i < M; ++i)
@@ -238,6 +242,15 @@ bool Loop::window(Exec& ex) {
     if (t->A <= now) ++waiting;
   const int64_t gw = ex.global_waiting(waiting);
   if (!(naive || cfg.no_ctl)) ctl.decide(now, (int32_t)gw);
+  if (log) {
+    std::unique_lock<std::mutex> g;
+    if (log_mu) g = std::unique_lock<std::mutex>(*log_mu);
+    WindowLog& w = log->back();
+    w.end = now;
+    w.waiting = (int)gw;
+    w.level_after = ctl.level;
+    w.c_after = ctl.c;
+  }
   return true;
 }
 

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <functional>
+#include <mutex>
 #include <vector>
 
 #include "control.h"
@@ -49,6 +50,9 @@ struct WindowLog {
   int64_t now;
   int M, N, K, level, c;
   std::vector<std::array<int, 3>> stages;
+  // after the window: its end, the waiting queue the controller observed, and its new state
+  int64_t end = 0;
+  int waiting = 0, level_after = 0, c_after = 0;
 };
 
 // Executor interface: the loop is identical for the GPU and the virtual clock.
@@ -74,6 +78,7 @@ struct Loop {
   std::vector<STask*> pending;  // sorted by (A, id)
   std::vector<STask*> batch, dec;
   std::vector<WindowLog>* log = nullptr;
+  std::mutex* log_mu = nullptr;  // GPU server: the log is read by another thread
   // one window; returns false if there was nothing to do (the caller waits until next_event())
   bool window(Exec& ex);
   int64_t next_arrival() const { return pending.empty() ? -1 : pending.front()->A; }

@@ -80,6 +80,7 @@ struct Server {
   float* pinned_emb = nullptr;
   float* emb_dev = nullptr;  // device copy of one admission's embedding (+ pooled)
   std::vector<int> res_hw;   // mixed resolutions: the latent sizes with a table (copied at start)
+  std::vector<WindowLog> wlog;  // one entry per planned window (controller trajectory)
   // per-request buffers are recycled (cudaMalloc / cudaFree / cudaMallocHost in the loop would
   // stall it; cudaFree synchronises the whole device, i.e. the concurrent UNet round too)
   // keyed by buffer size (mixed resolutions)
@@ -253,6 +254,8 @@ extern "C" sd_status sd_serve_start(sd_engine* e, const sd_serve_config* cfg) {
   S->loop.cfg.c_star = cfg->c_star;
   set_policy(S->loop.cfg, cfg);
   set_tables(S->loop, cfg);
+  S->loop.log = &S->wlog;
+  S->loop.log_mu = &S->mu;
   S->res_hw.assign(cfg->res_hw, cfg->res_hw + cfg->n_res);
   S->cfg.res_hw = nullptr;  // the caller's arrays need not outlive sd_serve_start (tables must)
   S->cfg.res_tables = nullptr;
@@ -422,5 +425,32 @@ extern "C" sd_status sd_get_load(sd_engine* e, int32_t* out4) {
   for (auto* t : S->inbox) waiting += 1;
   for (int i = 0; i < 4; ++i) out4[i] = S->counters[i];
   out4[0] = std::max(out4[0], waiting);
+  return SD_OK;
+}
+
+// Controller trajectory of the running server (one record per planned window): window start / end
+// (µs), M, N, K, the level and chunk count the window ran with, the waiting queue the controller then
+// observed and its new level / chunk count. Call before sd_serve_stop; copies min(max, windows).
+extern "C" sd_status sd_serve_window_log(sd_engine* e, int32_t max, int64_t* t_start, int64_t* t_end, int32_t* m,
+                                         int32_t* n, int32_t* k, int32_t* level, int32_t* c, int32_t* waiting,
+                                         int32_t* level_after, int32_t* c_after, int32_t* n_out) {
+  SD_REQUIRE(e && server_of(e) && n_out && max >= 0, "sd_serve_window_log: bad args");
+  Server* S = server_of(e);
+  std::lock_guard<std::mutex> g(S->mu);
+  const int cnt = std::min<int>(max, (int)S->wlog.size());
+  for (int i = 0; i < cnt; ++i) {
+    const WindowLog& w = S->wlog[i];
+    if (t_start) t_start[i] = w.now;
+    if (t_end) t_end[i] = w.end;
+    if (m) m[i] = w.M;
+    if (n) n[i] = w.N;
+    if (k) k[i] = w.K;
+    if (level) level[i] = w.level;
+    if (c) c[i] = w.c;
+    if (waiting) waiting[i] = w.waiting;
+    if (level_after) level_after[i] = w.level_after;
+    if (c_after) c_after[i] = w.c_after;
+  }
+  *n_out = cnt;
   return SD_OK;
 }

@@ -46,9 +46,10 @@ def p99(values):
 
 def run_trace(eng, table_h, trace, latent_hw=64, b_max=8, c_star=1, c_max=2, dp_mode=0, guidance=7.5,
               trace_seed=7, ctl=None, timeout_s=600, n_max=None, policy="synerdiff", ablation=0,
-              dyn_window_us=500_000, res_tables=None):
+              dyn_window_us=500_000, res_tables=None, trajectory=None):
     """Serve `trace` [(id, arrival_us, n_steps[, latent_hw])] on `eng`; returns per-request records and
-    metrics. `res_tables` {latent_hw: table handle} makes the server mixed-resolution.
+    metrics. `res_tables` {latent_hw: table handle} makes the server mixed-resolution. A list passed as
+    `trajectory` receives the controller trajectory (one dict per planned window, sd_serve_window_log).
     Arrival times are relative to sd_serve_start; all requests are submitted up front and admitted
     by the server when their arrival time has passed. `policy` selects SynerDiff or one of the
     paper's baselines, `ablation` the SD_ABL_* bits."""
@@ -83,6 +84,13 @@ def run_trace(eng, table_h, trace, latent_hw=64, b_max=8, c_star=1, c_max=2, dp_
                 c = out[j]
                 recs[c.id] = dict(A=c.arrival_us, U=c.denoise_done_us, V=c.decode_done_us, skips=c.n_skipped)
                 B.call("sd_release", eng.h, c.id)
+        if trajectory is not None:
+            cap = 1 << 16
+            cols = {k: (C.c_int64 * cap)() if k in ("t0", "t1") else (C.c_int32 * cap)()
+                    for k in ("t0", "t1", "M", "N", "K", "level", "c", "waiting", "level_after", "c_after")}
+            nw = C.c_int32()
+            B.call("sd_serve_window_log", eng.h, cap, *cols.values(), C.byref(nw))
+            trajectory.extend({k: int(v[i]) for k, v in cols.items()} for i in range(nw.value))
     finally:
         B.call("sd_serve_stop", eng.h)
     if len(recs) < len(trace):
