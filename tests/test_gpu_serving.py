@@ -67,8 +67,17 @@ def test_serving_tiny_matches_oracle_alone(cstar):
             B.call("sd_release", eng.h, c_.id)
         if len(got) == n:
             break
+    # controller trajectory (sd_serve_window_log): ordered windows; the aggressive controller escalates
+    cap = 4096
+    t0, t1 = (C.c_int64 * cap)(), (C.c_int64 * cap)()
+    lv, la, cc, wt = (C.c_int32 * cap)(), (C.c_int32 * cap)(), (C.c_int32 * cap)(), (C.c_int32 * cap)()
+    nw = C.c_int32()
+    B.call("sd_serve_window_log", eng.h, cap, t0, t1, None, None, None, lv, cc, wt, la, None, C.byref(nw))
     B.call("sd_serve_stop", eng.h)
     assert len(got) == n
+    assert nw.value > 0
+    assert all(t0[i] <= t1[i] <= t0[i + 1] for i in range(nw.value - 1))
+    assert all(la[i] == lv[i + 1] for i in range(nw.value - 1))       # the next window runs the decision
     # (1) exact: each served image equals the same engine running the request alone through
     # sd_step_batch with the recorded skip schedule and a whole decode (batch invariance I5 and
     # chunked == whole I6, bitwise on the GPU)
