@@ -561,8 +561,12 @@ void attention_tc(const bf16* qk, const bf16* vt, bf16* O, int rows, int heads, 
         default: launch_tc<40, 1, 2, 0>(qk, vt, O, rows, heads, C, P, st); break;
       }
       break;
-    case 64:  // measured: NB=2 1.18× faster at d=64; OP 5 = P in TMEM (SD_ATTN_EMU=8, the default)
+    case 64:  // SD_ATTN_EMU=8 (default): the d = 40 structure — two CTAs per SM, two softmax threads per
+              // row, one TMEM pass, P in TMEM (S 128 | O 64 | P 64 columns): SDXL [16,10,64,4096] 1.27 → 1.16
+              // ms vs NB = 2 / one thread per row (which was 1.18× faster than NB = 1 with P in smem)
       if (attn_emu() == 8)
+        launch_tc<64, 1, 2, 0, 4>(qk, vt, O, rows, heads, C, P, st);
+      else if (attn_emu() == 5)
         launch_tc<64, 2, 1, 0, 5>(qk, vt, O, rows, heads, C, P, st);
       else if (attn_emu() != 4)
         launch_tc<64, 2, 1, 0>(qk, vt, O, rows, heads, C, P, st);

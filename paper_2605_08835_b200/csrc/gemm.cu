@@ -240,15 +240,13 @@ __device__ __forceinline__ void add32(float* o, const float* p) {
   }
 }
 
-// residual of 32 columns of one row (16-byte loads, issued early: their latency hides behind the
-// accumulator wait / the previous chunk's math)
+// residual of 32 columns of one row (16-byte read-only loads)
 __device__ __forceinline__ void res_load32(uint4 (&r)[4], const bf16* rp) {
 #pragma unroll
   for (int i = 0; i < 4; ++i) r[i] = __ldg(reinterpret_cast<const uint4*>(rp) + i);
 }
 
-// `tfull` / `tphase`: the accumulator-ready barrier, waited on here after the first residual chunk
-// has been requested
+// `tfull` / `tphase`: the accumulator-ready barrier of this tile
 template <int BN, int MODE>
 __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorMap* om, EpiCtx& ec, uint32_t tbase,
                                               int mbox, int n0, int q, int lane, int half, int split, uint64_t* tfull,
@@ -277,10 +275,6 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
     ec.sy = ty * g.ht + (r0 / g.wt) % g.ht;
     ec.sb = tb * g.bt + r0 / (g.wt * g.ht);
   }
-  // residual prefetch (plain path, full 32-column chunks, 16-byte aligned rows)
-  const bool res_pf = g.res && g.act != ACT_GEGLU && g.splits == 1 && (g.ldr & 7) == 0;
-  uint4 rcur[4];
-  if (res_pf && valid && n0 + half * 32 + 32 <= g.N) res_load32(rcur, g.res + prow * g.ldr + n0 + half * 32);
   mbar_wait(tfull, tphase);
   tc_fence_after();
   if (g.act == ACT_GEGLU) {
@@ -320,9 +314,6 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
   }
 #pragma unroll 1
   for (int c = half; c < BN / 32; c += 2) {  // two epilogue warps per lane quarter: alternate chunks
-    uint4 rnext[4];
-    const int cn = n0 + (c + 2) * 32;
-    if (res_pf && valid && c + 2 < BN / 32 && cn + 32 <= g.N) res_load32(rnext, g.res + prow * g.ldr + cn);
     uint32_t rv[32];
     if (g.dbg != 3) {
       tmem_ld32(tbase + c * 32, rv);
@@ -379,12 +370,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
       const bf16* rp = g.res + prow * g.ldr + col;
       if (full32) {
         uint4 u4[4];
-        if (res_pf) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) u4[i] = rcur[i];
-        } else {
-          res_load32(u4, rp);
-        }
+        res_load32(u4, rp);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const bf16* e = reinterpret_cast<const bf16*>(&u4[i]);
@@ -394,10 +380,6 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
       } else {
         for (int i = 0; i < 32 && col + i < g.N; ++i) o[i] += __bfloat162float(rp[i]);
       }
-    }
-    if (res_pf) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) rcur[i] = rnext[i];
     }
     if (g.dbg == 1) {
       if (o[0] == 12345.f) g.res ? (void)0 : __trap();
