@@ -40,9 +40,9 @@ struct TcAttn {
   static constexpr int X_BYTES = 3 * 2 * 128 * 4;  // row-max / row-sum exchange of the SPLIT halves
   static constexpr int SMEM = 1024 + Q_BYTES + STAGES * STAGE + NB * P_BYTES + X_BYTES + 256;
   static constexpr int THREADS = 64 + 128 * SPLIT;
-  static constexpr int TMEM_COLS = NB == 2 ? 512 : 256;
+  static constexpr int TMEM_COLS = (NB == 2 || (PT && NPV > 64)) ? 512 : 256;  // S | O | P must fit
   static constexpr int O_COL = NB * 128;         // O accumulator after the S buffers
-  static constexpr int P_COL = NB == 1 ? 192 : 384;  // P (bf16, 2 per column) in TMEM (OP 4 / 5)
+  static constexpr int P_COL = NB == 1 ? (NPV <= 64 ? 192 : 256) : 384;  // P (bf16, 2 per column) in TMEM (OP ≥ 4)
   static_assert(V_BYTES % 1024 == 0, "Vᵀ tile rows must be a multiple of 8");
   static_assert(NPV <= 128, "O must fit beside the S buffers");
 };
@@ -573,8 +573,11 @@ void attention_tc(const bf16* qk, const bf16* vt, bf16* O, int rows, int heads, 
       else
         launch_tc<64, 2, 1, 4>(qk, vt, O, rows, heads, C, P, st);
       break;
-    case 80:
+    case 80:  // SD_ATTN_EMU=8 (default): two softmax threads per row, one TMEM pass, P in TMEM; S | O | P
+              // need 272 columns, so one CTA per SM (512 allocated): [16,8,80,1024] 87.9 → 83.1 µs
       if (attn_emu() == 8)
+        launch_tc<80, 1, 2, 0, 4>(qk, vt, O, rows, heads, C, P, st);
+      else if (attn_emu() == 5)
         launch_tc<80, 2, 1, 0, 5>(qk, vt, O, rows, heads, C, P, st);
       else if (attn_emu() != 4)
         launch_tc<80, 2, 1, 0>(qk, vt, O, rows, heads, C, P, st);
