@@ -95,6 +95,21 @@ def test_tiny_unet_cfg_on_off(tiny, sampler):
     assert final <= TOL and worst <= 1.0
 
 
+def test_tiny_unet_euler():
+    """R5 Euler (ε-prediction, σ grid on the same timesteps) through the bf16 path: 4 steps with CFG /
+    Skip-CFG mixes vs the oracle (final latents and teacher-forced ε-parts)."""
+    eng = Engine("tiny", max_latent_hw=16, b_max=4, sampler="euler")
+    try:
+        ctx_u = synth.uncond_embedding(0, 8, 32)
+        eng.set_uncond(torch.from_numpy(ctx_u))
+        P = configs.unet_params(configs.TINY_UNET, 0, np.float32, bf16_weights=True)
+        final, worst, _, _ = _run_tiny(eng, P, synth.bf16_round(ctx_u), "euler", [[1, 1], [1, 0], [0, 1], [0, 0]])
+        print(f"tiny Euler final rel-L2 {final:.3e}, worst per-step error / bound {worst:.3f}")
+        assert final <= TOL and worst <= 1.0
+    finally:
+        eng.close()
+
+
 def test_tiny_batch_invariance(tiny):
     """I5 on the GPU: a request's update in a batch equals its update alone (bitwise)."""
     eng, P, V, ctx_u = tiny
