@@ -265,6 +265,10 @@ sd_status sd_serve_simulate_mixed(const sd_serve_config* cfg, int32_t n, const u
 /* D[M][N] = A[M][K] · B[N][K]^T + bias[N] (bf16 in, fp32 accumulate, bf16 or fp32 out). */
 sd_status sd_debug_gemm(const void* A, const void* B, const float* bias, void* D, int32_t M, int32_t N, int32_t K,
                         int32_t out_f32, int32_t act, void* stream);
+/* D[M][N] = A·B^T + bias + res (res bf16 [M][ldr], may alias D when ldr == N): the residual
+ * epilogue of the transformer projections. */
+sd_status sd_debug_gemm_res(const void* A, const void* B, const float* bias, const void* res, int32_t ldr, void* D,
+                            int32_t M, int32_t N, int32_t K, void* stream);
 /* 3x3 / stride 1 / pad 1 conv over NHWC bf16 x [nb][h][w][cin] (+ optional second source x2 with
  * cin2 channels, concatenated after x), weights bf16 [cout][9][cin] (and [cout][9][cin2]),
  * bias fp32, optional temb fp32 [nb][cout], optional residual bf16 [nb][h][w][cout]. */

@@ -119,6 +119,7 @@ SIGNATURES = {
     "sd_serve_simulate_mixed": [C.POINTER(ServeConfig), I32, C.POINTER(C.c_uint64), PI64, PI32, PI32, PI64, PI64, PI32,
                                 PI32],
     "sd_debug_gemm": [P, P, P, P, I32, I32, I32, I32, I32, P],
+    "sd_debug_gemm_res": [P, P, P, P, I32, P, I32, I32, I32, P],
     "sd_debug_set_gemm_cg": [I32],
     "sd_debug_set_conv_splits": [I32],
     "sd_debug_attention": [P, P, P, P, I32, I32, I32, I32, I32, P],

@@ -50,6 +50,29 @@ extern "C" sd_status sd_debug_gemm(const void* A, const void* B, const float* bi
   SD_API_END
 }
 
+extern "C" sd_status sd_debug_gemm_res(const void* A, const void* B, const float* bias, const void* res, int32_t ldr,
+                                       void* D, int32_t M, int32_t N, int32_t K, void* stream) {
+  SD_REQUIRE(A && B && D && res && M > 0 && N > 0 && K > 0 && ldr >= N, "sd_debug_gemm_res: bad arguments");
+  SD_REQUIRE(K % 8 == 0, "sd_debug_gemm_res: K must be a multiple of 8");
+  SD_API_BEGIN
+  sd::GemmDesc d;
+  d.mode = sd::GEMM_DENSE;
+  d.A = static_cast<const bf16*>(A);
+  d.M = M;
+  d.K = K;
+  d.lda = K;
+  d.Bw[0] = static_cast<const bf16*>(B);
+  d.N = N;
+  d.ldb = K;
+  d.out = D;
+  d.ldo = N;
+  d.bias = bias;
+  d.res = static_cast<const bf16*>(res);
+  d.ldr = ldr;
+  sd::gemm(d, static_cast<cudaStream_t>(stream));
+  SD_API_END
+}
+
 extern "C" sd_status sd_debug_conv3x3(const void* x, int32_t cin, const void* x2, int32_t cin2, const void* w,
                                       const void* w2, const float* bias, const float* temb, const void* res, void* y,
                                       int32_t nb, int32_t h, int32_t wd, int32_t cout, void* stream) {

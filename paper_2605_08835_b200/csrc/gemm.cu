@@ -43,6 +43,8 @@ struct GemmArgs {
   int ldr;
   int act;
   int tma_store;      // bf16 output through the per-warp smem slab + TMA store
+  int res_tma;        // dense: the residual sub-tile arrives by TMA in the staging slab (coalesced)
+  int wstat;          // dense, short K: each worker keeps one N tile, its B blocks stay in smem (B slot kb)
   int dbg;            // experiment switch (SD_EPI_DBG): 1 = no store, 2 = no bias, 3 = no TMEM load
   int splits, kps;    // split-K: K blocks [s·kps, (s+1)·kps) of split s
   float* part;        // split-K fp32 partials [splits][M][N] (raw accumulators)
@@ -70,7 +72,7 @@ struct Cfg {
   static constexpr int TMEM_STRIDE = BN <= 64 ? 64 : (BN <= 128 ? 128 : 256);
   static constexpr int TMEM_COLS = 2 * TMEM_STRIDE;
   static constexpr int STAGING = 8 * 2 * 2048;                   // 8 epilogue warps × 2 slabs
-  static constexpr int SMEM = 1024 + STAGES * STAGE + STAGING + 256;
+  static constexpr int SMEM = 1024 + STAGES * STAGE + STAGING + 512;
   static_assert(B_BYTES % 1024 == 0, "B tile must be a whole number of 8-row swizzle groups");
 };
 
@@ -199,15 +201,19 @@ struct EpiCtx {
   uint8_t* stage;   // this warp's 2 × 2 KB staging slabs
   int slot;         // alternating slab
   int sx, sy, sb;   // this warp's slab origin (conv: pixel coords; dense: row in sx)
+  uint64_t* rbar;   // this warp's 2 residual-arrival barriers (one per slab)
+  uint32_t rph;     // their phase bits
 };
 
 // write 32 fp32 values (this lane's row, columns [col, col+32)) to the staging slab and TMA-store it
 template <int MODE>
 __device__ __forceinline__ void stage_store(const GemmArgs& g, const CUtensorMap* om, EpiCtx& ec, const float* o,
-                                            int col, int lane) {
+                                            int col, int lane, bool slab_ready = false) {
   uint8_t* buf = ec.stage + ec.slot * 2048;
-  if (lane == 0) bulk_wait_read<1>();      // the store issued two chunks ago has finished reading
-  __syncwarp();
+  if (!slab_ready) {
+    if (lane == 0) bulk_wait_read<1>();    // the store issued two chunks ago has finished reading
+    __syncwarp();
+  }
   const int sw = (lane >> 1) & 3;
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
@@ -248,7 +254,8 @@ __device__ __forceinline__ void res_load32(uint4 (&r)[4], const bf16* rp) {
 
 // `tfull` / `tphase`: the accumulator-ready barrier of this tile
 template <int BN, int MODE>
-__device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorMap* om, EpiCtx& ec, uint32_t tbase,
+__device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorMap* om, const CUtensorMap* res_map,
+                                              EpiCtx& ec, uint32_t tbase,
                                               int mbox, int n0, int q, int lane, int half, int split, uint64_t* tfull,
                                               uint32_t tphase) {
   const int r = q * 32 + lane;
@@ -315,6 +322,17 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
 #pragma unroll 1
   for (int c = half; c < BN / 32; c += 2) {  // two epilogue warps per lane quarter: alternate chunks
     uint32_t rv[32];
+    const bool rt = g.res_tma && n0 + c * 32 < g.N;  // warp-uniform
+    if (rt) {
+      // the slab is free once the store issued from it two chunks ago has read it; the 32×32 residual
+      // sub-tile then lands in it (same 64B swizzle as the output box) while the accumulator is read
+      if (lane == 0) {
+        bulk_wait_read<1>();
+        mbar_expect_tx(&ec.rbar[ec.slot], 2048);
+        tma_load_2d(ec.stage + ec.slot * 2048, res_map, &ec.rbar[ec.slot], n0 + c * 32, ec.sx);
+      }
+      __syncwarp();
+    }
     if (g.dbg != 3) {
       tmem_ld32(tbase + c * 32, rv);
     } else {
@@ -366,7 +384,19 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
 #pragma unroll
       for (int i = 0; i < 32; ++i) o[i] = silu_f(o[i]);
     }
-    if (g.res && valid) {
+    if (rt) {
+      mbar_wait(&ec.rbar[ec.slot], (ec.rph >> ec.slot) & 1);
+      ec.rph ^= 1u << ec.slot;
+      const uint8_t* buf = ec.stage + ec.slot * 2048;
+      const int sw = (lane >> 1) & 3;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint4 u = *reinterpret_cast<const uint4*>(buf + lane * 64 + ((i ^ sw) << 4));
+        const bf16* e = reinterpret_cast<const bf16*>(&u);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) o[8 * i + k] += __bfloat162float(e[k]);
+      }
+    } else if (g.res && valid) {
       const bf16* rp = g.res + prow * g.ldr + col;
       if (full32) {
         uint4 u4[4];
@@ -384,7 +414,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
     if (g.dbg == 1) {
       if (o[0] == 12345.f) g.res ? (void)0 : __trap();
     } else if (g.tma_store) {
-      stage_store<MODE>(g, om, ec, o, col, lane);
+      stage_store<MODE>(g, om, ec, o, col, lane, rt);
     } else if (valid) {
       if (g.out_f32) {
         float* op = reinterpret_cast<float*>(g.out) + prow * g.ldo + g.col_off + col;
@@ -415,7 +445,8 @@ template <int BN, int CG, int MODE>
 __global__ void __launch_bounds__(320, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ CUtensorMap ta1,
                 const __grid_constant__ CUtensorMap tb0, const __grid_constant__ CUtensorMap tb1,
-                const __grid_constant__ CUtensorMap tout, const GemmArgs g) {
+                const __grid_constant__ CUtensorMap tout, const __grid_constant__ CUtensorMap tres,
+                const GemmArgs g) {
   using C = Cfg<BN, CG>;
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned (SWIZZLE_128B atoms); offsetting the shared array itself keeps the pointer in the
@@ -428,7 +459,8 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* rbar = tempty + 2;  // [8 epilogue warps][2 slabs]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 16);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = CG == 2 ? cluster_rank() : 0;
@@ -441,6 +473,7 @@ __global__ void __launch_bounds__(320, 1)
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 8 * CG);
     }
+    for (int s = 0; s < 16; ++s) mbar_init(&rbar[s], 1);
     fence_mbar_init();
     tma_prefetch(&ta0);
     tma_prefetch(&tb0);
@@ -448,6 +481,7 @@ __global__ void __launch_bounds__(320, 1)
       tma_prefetch(&ta1);
       tma_prefetch(&tb1);
     }
+    if (g.res_tma) tma_prefetch(&tres);
   }
   if (warp == 1) tmem_alloc_cg<CG>(tmem_slot, C::TMEM_COLS);
   tc_fence_before();
@@ -466,6 +500,7 @@ __global__ void __launch_bounds__(320, 1)
       // ================= TMA producer (both CTAs of a pair load their halves) =================
       int stage = 0;
       uint32_t phase = 0;
+      bool b_resident = false;  // weight-stationary: B blocks loaded with the worker's first tile
       for (int t = worker; t < total; t += nworkers) {
         int mt, nt, sp, kb0, kb1;
         decode_tile(g, t, mt, nt, sp, kb0, kb1);
@@ -486,19 +521,19 @@ __global__ void __launch_bounds__(320, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           uint32_t bar_l = 0;
           if (CG == 1) {
-            mbar_expect_tx(&full[stage], C::STAGE);
+            mbar_expect_tx(&full[stage], b_resident ? C::A_BYTES : C::STAGE);
           } else {
             bar_l = leader_addr(&full[stage]);
             if (rank == 0) mbar_expect_tx(&full[stage], 2 * C::STAGE);
           }
           void* dA = sA + stage * C::A_BYTES;
-          void* dB = sB + stage * C::B_BYTES;
+          void* dB = sB + (g.wstat ? kb : stage) * C::B_BYTES;
           if (MODE == GEMM_DENSE) {
             // two sources (a channel concat never materialised): K blocks [0, kb_src0) from source 0
             const bool s1 = g.nsrc > 1 && kb >= g.kb_src[0];
             const int kk = s1 ? kb - g.kb_src[0] : kb;
             tma2<CG>(dA, s1 ? &ta1 : &ta0, &full[stage], bar_l, kk * C::BK, m0);
-            tma2<CG>(dB, s1 ? &tb1 : &tb0, &full[stage], bar_l, kk * C::BK, n0);
+            if (!b_resident) tma2<CG>(dB, s1 ? &tb1 : &tb0, &full[stage], bar_l, kk * C::BK, n0);
           } else {
             int r = kb, src = 0;
             if (r >= 9 * g.kb_src[0]) {
@@ -517,6 +552,7 @@ __global__ void __launch_bounds__(320, 1)
             phase ^= 1;
           }
         }
+        b_resident = g.wstat != 0;
       }
     }
   } else if (warp == 1) {
@@ -538,7 +574,7 @@ __global__ void __launch_bounds__(320, 1)
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
-          const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
+          const uint32_t b0 = smem_u32(sB + (g.wstat ? kb : stage) * C::B_BYTES);
 #pragma unroll
           for (int k = 0; k < C::BK / 16; ++k)
             mma<CG>(d, make_sdesc_sw128(a0 + k * 32), make_sdesc_sw128(b0 + k * 32), idesc,
@@ -557,7 +593,7 @@ __global__ void __launch_bounds__(320, 1)
     // ===== epilogue (warps 2..9 → TMEM lane quarters 2,3,0,1,2,3,0,1; two warps per quarter split
     // the 32-column chunks, so the epilogue keeps up with short-K tiles) =====
     const int q = warp & 3;
-    EpiCtx ec{sStage + (warp - 2) * 4096, 0, 0, 0, 0};
+    EpiCtx ec{sStage + (warp - 2) * 4096, 0, 0, 0, 0, rbar + (warp - 2) * 2, 0u};
     int it = 0;
     for (int t = worker; t < total; t += nworkers, ++it) {
       const int acc = it & 1;
@@ -565,7 +601,7 @@ __global__ void __launch_bounds__(320, 1)
       int mt, nt, sp, kb0, kb1;
       decode_tile(g, t, mt, nt, sp, kb0, kb1);
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * C::TMEM_STRIDE;
-      epilogue_tile<BN, MODE>(g, &tout, ec, tbase, mt * CG + (int)rank, nt * BN, q, lane, (warp - 2) >> 2, sp,
+      epilogue_tile<BN, MODE>(g, &tout, &tres, ec, tbase, mt * CG + (int)rank, nt * BN, q, lane, (warp - 2) >> 2, sp,
                               &tfull[acc], acc_phase);
       tc_fence_before();
       __syncwarp();
@@ -696,6 +732,7 @@ static void launch(const CUtensorMap* m, const GemmArgs& a, cudaStream_t st) {
   }
   const int total = a.m_tiles * a.n_tiles * a.splits;
   int workers = num_sms() / CG;
+  if (a.wstat) workers = workers / a.n_tiles * a.n_tiles;  // every worker keeps one N tile
   if (total < workers) workers = total;
   if (workers <= 0) return;
   cudaLaunchConfig_t cfg{};
@@ -710,7 +747,7 @@ static void launch(const CUtensorMap* m, const GemmArgs& a, cudaStream_t st) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  SD_CUDA(cudaLaunchKernelEx(&cfg, gemm_kernel<BN, CG, MODE>, m[0], m[1], m[2], m[3], m[4], a));
+  SD_CUDA(cudaLaunchKernelEx(&cfg, gemm_kernel<BN, CG, MODE>, m[0], m[1], m[2], m[3], m[4], m[5], a));
   SD_CHECK_LAUNCH();
 }
 
@@ -730,7 +767,14 @@ static void dispatch(int bn, int cg, const CUtensorMap* maps, const GemmArgs& a,
 }
 
 static int pick_bn(int N, int act) {
-  if (act == ACT_GEGLU) return N % 256 == 0 ? 256 : 128;
+  if (act == ACT_GEGLU) {
+    static int e = -1;  // SD_GEGLU_BN=128 (experiments)
+    if (e < 0) {
+      const char* s = getenv("SD_GEGLU_BN");
+      e = s ? atoi(s) : 0;
+    }
+    return (e == 128 || N % 256) ? 128 : 256;
+  }
   if (N <= 64) return 64;
   if (N % 256 == 0) return 256;
   if (N % 160 == 0) return 160;
@@ -779,7 +823,7 @@ void gemm(const GemmDesc& d, cudaStream_t st) {
     g_cg_override = s ? atoi(s) : 0;
   }
   GemmArgs a{};
-  CUtensorMap maps[5];
+  CUtensorMap maps[6];
   memset(maps, 0, sizeof(maps));
   a.mode = d.mode;
   a.N = d.N;
@@ -935,6 +979,36 @@ void gemm(const GemmDesc& d, cudaStream_t st) {
   } else {
     if (d.act == ACT_GEGLU) throw CudaError("GEGLU epilogue needs a bf16, 16-byte aligned output");
     maps[4] = maps[0];
+  }
+  // dense residual through TMA (the per-lane row loads cost one L1 wavefront per row: 32 per warp
+  // instruction); SD_RES_TMA=0 keeps the direct loads (A/B)
+  static int res_tma_env = -1;
+  if (res_tma_env < 0) {
+    const char* e = getenv("SD_RES_TMA");
+    res_tma_env = e ? atoi(e) : 1;
+  }
+  maps[5] = maps[0];
+  if (res_tma_env && a.tma_store && d.res && d.mode == GEMM_DENSE && d.act != ACT_GEGLU && d.ldr % 8 == 0 &&
+      (reinterpret_cast<uintptr_t>(d.res) & 15) == 0 && a.dbg == 0) {
+    uint64_t dR[2] = {(uint64_t)d.N, (uint64_t)d.M}, sR[1] = {(uint64_t)d.ldr * 2};
+    uint32_t bR[2] = {32, 32};
+    make_map(&maps[5], d.res, 2, dR, sR, bR, CU_TENSOR_MAP_SWIZZLE_64B);
+    a.res_tma = 1;
+  }
+  // weight-stationary short-K dense GEMMs: with n_tiles dividing the worker count, worker w only ever
+  // computes N tile w mod n_tiles, so its B blocks (num_kb ≤ STAGES of them) are loaded once into the
+  // B ring slots and only A streams — per-tile L2 traffic drops from A + B to A (the K = 320
+  // projections at 64×64 were L2-throughput-bound). SD_GEMM_WSTAT=0 disables (A/B).
+  static int wstat_env = -1;
+  if (wstat_env < 0) {
+    const char* e = getenv("SD_GEMM_WSTAT");
+    wstat_env = e ? atoi(e) : 0;
+  }
+  if (wstat_env && d.mode == GEMM_DENSE && cg == 1 && a.splits == 1 && a.n_tiles <= num_sms()) {
+    const int stage_bytes = 128 * 64 * 2 + bn * 64 * 2;
+    const int stages = std::min(8, 192 * 1024 / stage_bytes);
+    const int workers = num_sms() / a.n_tiles * a.n_tiles;
+    if (a.num_kb <= stages && (long)a.m_tiles * a.n_tiles >= 2L * workers) a.wstat = 1;
   }
   if (d.mode == GEMM_DENSE)
     dispatch<GEMM_DENSE>(bn, cg, maps, a, st);

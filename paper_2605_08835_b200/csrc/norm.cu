@@ -65,14 +65,16 @@ struct Raw8<float> {
 // sequentially, then a fixed butterfly in which both partners compute the identical value —
 // deterministic, independent of which block runs it. Writes the group's affine table entries
 // (scale = γ·rstd, shift = β − μ·scale). Partials are read through L2 (written by other SMs).
-__device__ __forceinline__ void gn_merge_group(int P, int C, int G, int chunk_px, int nchunks,
-                                               const GNPart* __restrict__ part, float eps,
+// `ld(k)` returns chunk k's partial (global through L2, or a shared-memory copy); `tab` = the image's
+// C table entries.
+template <class LD>
+__device__ __forceinline__ void gn_merge_group(int P, int C, int G, int chunk_px, int nchunks, LD ld, float eps,
                                                const float* __restrict__ gamma, const float* __restrict__ beta,
-                                               float2* __restrict__ tab, int b, int g, int lane) {
+                                               float2* __restrict__ tab, int g, int lane) {
   const int cg = C / G;
   float n = 0.f, mean = 0.f, m2 = 0.f;
   for (int k = lane; k < nchunks; k += 32) {
-    const float2 pp = __ldcg(reinterpret_cast<const float2*>(part + ((long)b * nchunks + k) * G + g));
+    const float2 pp = ld(k);
     const float nb = (float)(min(P, (k + 1) * chunk_px) - k * chunk_px) * cg;
     const float tot = n + nb;
     const float d = pp.x - mean;
@@ -104,13 +106,15 @@ __device__ __forceinline__ void gn_merge_group(int P, int C, int G, int chunk_px
   const float rstd = rsqrtf(m2 / n + eps);
   for (int c = g * cg + lane; c < (g + 1) * cg; c += 32) {
     const float sc = gamma[c] * rstd;  // y = x·(γ·rstd) + (β − mean·γ·rstd)
-    tab[(long)b * C + c] = make_float2(sc, beta[c] - mean * sc);
+    tab[c] = make_float2(sc, beta[c] - mean * sc);
   }
 }
 
 // block (V, R): V = C/8 vector lanes, R pixel rows; grid (chunks in range, B)
 // (measured: merging in the last-arriving stats block instead of a finalize launch serialises the
-// 32 group merges on one block — 2.1 vs 1.8 ms of GN per 16-row SD-1.5 step)
+// 32 group merges on one block — 2.1 vs 1.8 ms of GN per 16-row SD-1.5 step; merging redundantly in
+// every apply block — partials staged in smem, one launch fewer — costs 2.0-2.3 vs 1.9 ms: the
+// per-block merge prologue outweighs the saved launch)
 // Two sources (x1 != nullptr): the channels are the concat [x (V0 vectors) | x1 (V − V0 vectors)], each
 // source contiguous in its own [B][P][channels] layout — the up-block concat is never materialised.
 template <class T>
@@ -200,7 +204,10 @@ __global__ void gn_finalize_kernel(int P, int C, int G, int chunk_px, int nchunk
   const int g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int b = blockIdx.y;
   if (g >= G) return;
-  gn_merge_group(P, C, G, chunk_px, nchunks, part, eps, gamma, beta, tab, b, g, lane);
+  const GNPart* pb = part + (long)b * nchunks * G + g;
+  gn_merge_group(
+      P, C, G, chunk_px, nchunks, [&](int k) { return __ldcg(reinterpret_cast<const float2*>(pb + (long)k * G)); },
+      eps, gamma, beta, tab + (long)b * C, g, lane);
 }
 
 // apply over pixels [p_begin, p_end) of x viewed as [B·P][V vectors of 8]: block (V, R); thread

@@ -27,7 +27,9 @@ def bf(x):
 
 
 @pytest.mark.parametrize("M,N,K", [(128, 64, 64), (300, 320, 320), (1000, 1280, 640), (77, 256, 768),
-                                   (4096, 160, 2880), (200, 128, 32), (129, 16, 64), (513, 4, 128)])
+                                   (4096, 160, 2880), (200, 128, 32), (129, 16, 64), (513, 4, 128),
+                                   # weight-stationary (short K, many M tiles; ragged last tile)
+                                   (40000, 320, 320), (20000, 960, 320), (38000, 64, 256)])
 @pytest.mark.parametrize("out_f32", [0, 1])
 def test_gemm_dense(M, N, K, out_f32):
     g = torch.Generator().manual_seed(M * 7 + N + K)
@@ -40,6 +42,23 @@ def test_gemm_dense(M, N, K, out_f32):
     B.debug_gemm(Ad, Wd, bias.cuda(), D, M, N, K, out_f32=out_f32)
     torch.cuda.synchronize()
     assert rel(D.cpu(), ref) < (1e-5 if out_f32 else 6e-3)
+
+
+@pytest.mark.parametrize("M,N,K,ldr,inplace", [(300, 320, 320, 320, 0), (4096, 640, 640, 640, 1),
+                                                 (1000, 1280, 640, 1280, 1), (129, 96, 64, 104, 0),
+                                                 (257, 40, 128, 40, 0), (40000, 320, 320, 320, 1)])
+def test_gemm_residual(M, N, K, ldr, inplace):
+    """Dense GEMM + bias + bf16 residual (TMA-staged residual when the row stride allows; in place)."""
+    g = torch.Generator().manual_seed(M + N + K + ldr)
+    A, Wt = torch.randn(M, K, generator=g), torch.randn(N, K, generator=g) / K ** 0.5
+    bias, res = torch.randn(N, generator=g), bf(torch.randn(M, ldr, generator=g))
+    ref = bf(A).double() @ bf(Wt).double().T + bias.double() + res[:, :N].double()
+    Ad, Wd, bd, resd = bf(A).cuda(), bf(Wt).cuda(), bias.cuda(), res.cuda()  # kept alive across the call
+    D = resd if inplace else torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    B.call("sd_debug_gemm_res", B._p(Ad), B._p(Wd), B._p(bd), B._p(resd), ldr, B._p(D), M, N, K, None)
+    torch.cuda.synchronize()
+    out = D.cpu()[:, :N] if inplace else D.cpu()
+    assert rel(out, ref) < 6e-3
 
 
 def test_gemm_geglu_and_silu():
@@ -198,7 +217,8 @@ def test_attention_tcgen05(R, heads, d, P):
 
 
 @pytest.mark.parametrize("nb,P,C,G,silu", [(2, 4096, 320, 32, 1), (3, 256, 1280, 32, 0), (1, 64, 2560, 32, 1),
-                                           (2, 64, 32, 8, 1), (1, 16384, 128, 32, 1)])
+                                           (2, 64, 32, 8, 1), (1, 16384, 128, 32, 1),
+                                           (3, 1000, 320, 32, 1), (5, 200, 640, 32, 0)])
 def test_groupnorm(nb, P, C, G, silu):
     g = torch.Generator().manual_seed(P + C)
     x = bf(torch.randn(nb, P, C, generator=g) * 2 + 0.5)

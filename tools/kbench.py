@@ -104,6 +104,21 @@ def main():
             print(json.dumps(r), flush=True)
 
 
+    if args.only in ("", "gemmres"):  # residual epilogues (attention out-projection, FF2, proj_out)
+        for i_, (M, N, K) in enumerate([(65536, 320, 320), (65536, 320, 1280), (16384, 640, 640), (4096, 1280, 1280)]):
+            if args.pick >= 0 and i_ != args.pick:
+                continue
+            A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+            Wt = (torch.randn(N, K, device="cuda") / K ** 0.5).to(torch.bfloat16)
+            b = torch.zeros(N, device="cuda")
+            R = torch.randn(M, N, device="cuda").to(torch.bfloat16)
+            D = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+            ms = timeit(lambda: B.call("sd_debug_gemm_res", B._p(A), B._p(Wt), B._p(b), B._p(R), N, B._p(D), M, N, K,
+                                       B._p(cur())), args.reps)
+            fl = 2.0 * M * N * K
+            print(json.dumps(dict(kind="gemm_res", shape=[M, N, K], ms=ms, tflops=fl / ms / 1e9,
+                                  frac=fl / ms / 1e9 / peak)), flush=True)
+
     if args.only in ("", "norm"):
         hbm = 6446.9
         for i_, (nb, P, C) in enumerate([(16, 4096, 320), (16, 1024, 640), (16, 256, 1280), (16, 4096, 640),
