@@ -44,7 +44,7 @@ struct GemmArgs {
   int act;
   int tma_store;      // bf16 output through the per-warp smem slab + TMA store
   int res_tma;        // dense: the residual sub-tile arrives by TMA in the staging slab (coalesced)
-  int wstat;          // dense, short K: each worker keeps one N tile, its B blocks stay in smem (B slot kb)
+  int gelu_tanh;      // GEGLU: tanh form of GELU on MUFU tanh.approx (default; SD_GELU_TANH=0 = erf form)
   int dbg;            // experiment switch (SD_EPI_DBG): 1 = no store, 2 = no bias, 3 = no TMEM load
   int splits, kps;    // split-K: K blocks [s·kps, (s+1)·kps) of split s
   float* part;        // split-K fp32 partials [splits][M][N] (raw accumulators)
@@ -307,8 +307,24 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
           add32(vv, g.bias + n0 + cv);
           add32(gg, g.bias + n0 + cgc);
         }
+        if (g.gelu_tanh) {
+          // GELU(x) ≈ ½x(1 + tanh(√(2/π)(x + 0.044715x³))): |Δ| ≤ 4.7e-4 from the erf form, plus the
+          // tanh.approx error (≤ ½|x|·2^-10.9) — below one bf16 ulp of the output; 6 instructions instead
+          // of the 15 of the erf polynomial (the FF1 epilogue was issue-bound: 64 % issue, 36 % tensor
+          // pipe) → FF1 at 64×64: 135 → 109 µs
 #pragma unroll
-        for (int i = 0; i < 32; ++i) o[i] = vv[i] * gelu_f(gg[i]);
+          for (int i = 0; i < 32; ++i) {
+            const float x = gg[i];
+            const float u = x * fmaf(0.0356774081f * x, x, 0.7978845608f);  // √(2/π)·(x + 0.044715·x³)
+            float t;
+            asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(u));
+            const float hx = 0.5f * x;
+            o[i] = vv[i] * fmaf(hx, t, hx);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = vv[i] * gelu_f(gg[i]);
+        }
         if (g.res && valid) {
           const bf16* rp = g.res + prow * g.ldr + ocol;
 #pragma unroll
@@ -500,7 +516,6 @@ __global__ void __launch_bounds__(320, 1)
       // ================= TMA producer (both CTAs of a pair load their halves) =================
       int stage = 0;
       uint32_t phase = 0;
-      bool b_resident = false;  // weight-stationary: B blocks loaded with the worker's first tile
       for (int t = worker; t < total; t += nworkers) {
         int mt, nt, sp, kb0, kb1;
         decode_tile(g, t, mt, nt, sp, kb0, kb1);
@@ -521,19 +536,19 @@ __global__ void __launch_bounds__(320, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           uint32_t bar_l = 0;
           if (CG == 1) {
-            mbar_expect_tx(&full[stage], b_resident ? C::A_BYTES : C::STAGE);
+            mbar_expect_tx(&full[stage], C::STAGE);
           } else {
             bar_l = leader_addr(&full[stage]);
             if (rank == 0) mbar_expect_tx(&full[stage], 2 * C::STAGE);
           }
           void* dA = sA + stage * C::A_BYTES;
-          void* dB = sB + (g.wstat ? kb : stage) * C::B_BYTES;
+          void* dB = sB + stage * C::B_BYTES;
           if (MODE == GEMM_DENSE) {
             // two sources (a channel concat never materialised): K blocks [0, kb_src0) from source 0
             const bool s1 = g.nsrc > 1 && kb >= g.kb_src[0];
             const int kk = s1 ? kb - g.kb_src[0] : kb;
             tma2<CG>(dA, s1 ? &ta1 : &ta0, &full[stage], bar_l, kk * C::BK, m0);
-            if (!b_resident) tma2<CG>(dB, s1 ? &tb1 : &tb0, &full[stage], bar_l, kk * C::BK, n0);
+            tma2<CG>(dB, s1 ? &tb1 : &tb0, &full[stage], bar_l, kk * C::BK, n0);
           } else {
             int r = kb, src = 0;
             if (r >= 9 * g.kb_src[0]) {
@@ -552,7 +567,6 @@ __global__ void __launch_bounds__(320, 1)
             phase ^= 1;
           }
         }
-        b_resident = g.wstat != 0;
       }
     }
   } else if (warp == 1) {
@@ -574,7 +588,7 @@ __global__ void __launch_bounds__(320, 1)
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
-          const uint32_t b0 = smem_u32(sB + (g.wstat ? kb : stage) * C::B_BYTES);
+          const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
 #pragma unroll
           for (int k = 0; k < C::BK / 16; ++k)
             mma<CG>(d, make_sdesc_sw128(a0 + k * 32), make_sdesc_sw128(b0 + k * 32), idesc,
@@ -732,7 +746,6 @@ static void launch(const CUtensorMap* m, const GemmArgs& a, cudaStream_t st) {
   }
   const int total = a.m_tiles * a.n_tiles * a.splits;
   int workers = num_sms() / CG;
-  if (a.wstat) workers = workers / a.n_tiles * a.n_tiles;  // every worker keeps one N tile
   if (total < workers) workers = total;
   if (workers <= 0) return;
   cudaLaunchConfig_t cfg{};
@@ -768,7 +781,7 @@ static void dispatch(int bn, int cg, const CUtensorMap* maps, const GemmArgs& a,
 
 static int pick_bn(int N, int act) {
   if (act == ACT_GEGLU) {
-    static int e = -1;  // SD_GEGLU_BN=128 (experiments)
+    static int e = -1;  // SD_GEGLU_BN=128 (experiments; measured 1.4× slower at 64×64)
     if (e < 0) {
       const char* s = getenv("SD_GEGLU_BN");
       e = s ? atoi(s) : 0;
@@ -949,6 +962,14 @@ void gemm(const GemmDesc& d, cudaStream_t st) {
   a.res = d.res;
   a.ldr = d.ldr;
   a.act = d.act;
+  {
+    static int gt = -1;
+    if (gt < 0) {
+      const char* e = getenv("SD_GELU_TANH");
+      gt = e ? atoi(e) : 1;
+    }
+    a.gelu_tanh = gt;
+  }
   // bf16 outputs go through the TMA store path (box = one warp's 32 rows × 32 columns)
   const int n_out = d.act == ACT_GEGLU ? d.N / 2 : d.N;
   a.tma_store = (!d.out_f32 && d.ldo % 8 == 0 && d.col_off % 8 == 0 && n_out % 8 == 0 && a.splits == 1) ? 1 : 0;
@@ -994,21 +1015,6 @@ void gemm(const GemmDesc& d, cudaStream_t st) {
     uint32_t bR[2] = {32, 32};
     make_map(&maps[5], d.res, 2, dR, sR, bR, CU_TENSOR_MAP_SWIZZLE_64B);
     a.res_tma = 1;
-  }
-  // weight-stationary short-K dense GEMMs: with n_tiles dividing the worker count, worker w only ever
-  // computes N tile w mod n_tiles, so its B blocks (num_kb ≤ STAGES of them) are loaded once into the
-  // B ring slots and only A streams — per-tile L2 traffic drops from A + B to A (the K = 320
-  // projections at 64×64 were L2-throughput-bound). SD_GEMM_WSTAT=0 disables (A/B).
-  static int wstat_env = -1;
-  if (wstat_env < 0) {
-    const char* e = getenv("SD_GEMM_WSTAT");
-    wstat_env = e ? atoi(e) : 0;
-  }
-  if (wstat_env && d.mode == GEMM_DENSE && cg == 1 && a.splits == 1 && a.n_tiles <= num_sms()) {
-    const int stage_bytes = 128 * 64 * 2 + bn * 64 * 2;
-    const int stages = std::min(8, 192 * 1024 / stage_bytes);
-    const int workers = num_sms() / a.n_tiles * a.n_tiles;
-    if (a.num_kb <= stages && (long)a.m_tiles * a.n_tiles >= 2L * workers) a.wstat = 1;
   }
   if (d.mode == GEMM_DENSE)
     dispatch<GEMM_DENSE>(bn, cg, maps, a, st);

@@ -28,7 +28,7 @@ def bf(x):
 
 @pytest.mark.parametrize("M,N,K", [(128, 64, 64), (300, 320, 320), (1000, 1280, 640), (77, 256, 768),
                                    (4096, 160, 2880), (200, 128, 32), (129, 16, 64), (513, 4, 128),
-                                   # weight-stationary (short K, many M tiles; ragged last tile)
+                                   # short K, many M tiles per SM, ragged last tile
                                    (40000, 320, 320), (20000, 960, 320), (38000, 64, 256)])
 @pytest.mark.parametrize("out_f32", [0, 1])
 def test_gemm_dense(M, N, K, out_f32):
