@@ -28,6 +28,28 @@ def test_sd15_param_count():
     assert n == 859_520_964
 
 
+def test_sd_vae_param_count():
+    """The SD AutoencoderKL has 83,653,863 parameters (the widely published count). The oracle builds
+    only post_quant_conv + decoder; the encoder + quant_conv side is counted here from the standard
+    SD encoder layout (conv_in 3→128; down blocks 128/256/512/512 × 2 ResNets, 3 downsamplers; mid
+    ResNet-attention-ResNet at 512; GN + conv_out 512→8; quant_conv 8→8), independently of oracle/.
+    A dropped or mis-shaped decoder layer breaks the exact total."""
+
+    def res(ci, co):  # GN, 3×3 conv, GN, 3×3 conv, 1×1 shortcut when the width changes
+        return 2 * ci + co * ci * 9 + co + 2 * co + co * co * 9 + co + (co * ci + co if ci != co else 0)
+
+    enc, prev, ch = 3 * 128 * 9 + 128, 128, (128, 256, 512, 512)
+    for i, co in enumerate(ch):
+        enc += res(prev, co) + res(co, co)
+        prev = co
+        if i != len(ch) - 1:
+            enc += co * co * 9 + co
+    enc += 2 * res(512, 512) + 2 * 512 + 4 * (512 * 512 + 512)
+    enc += 2 * 512 + 8 * 512 * 9 + 8 + (8 * 8 + 8)
+    dec = sum(int(np.prod(s[1])) for s in configs.vae_param_specs(configs.SD_VAE))
+    assert enc + dec == 83_653_863
+
+
 def test_generator_deterministic_and_bounded():
     a = synth.weight(0, "conv_in.weight", (32, 4, 3, 3), synth.KIND_UNIFORM_FANIN, 36)
     b = synth.weight(0, "conv_in.weight", (32, 4, 3, 3), synth.KIND_UNIFORM_FANIN, 36)
