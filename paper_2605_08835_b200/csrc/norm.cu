@@ -14,6 +14,8 @@
 // The reduction order depends only on (P, C, G) — never on the batch (I5) or on banding (I6).
 // Chunk size adapts to C (≈ 40 K elements per chunk).
 #include <algorithm>
+#include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels_ew.h"
@@ -210,6 +212,15 @@ __global__ void gn_finalize_kernel(int P, int C, int G, int chunk_px, int nchunk
       eps, gamma, beta, tab + (long)b * C, g, lane);
 }
 
+// SiLU(x) = x·σ(x) = ½x + ½x·tanh(x/2) on MUFU tanh.approx: error ≤ ½|x|·2^-10.9, under one bf16 ulp
+// of the stored output (bf16 path only)
+__device__ __forceinline__ float silu_tanh(float x) {
+  const float hx = 0.5f * x;
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(hx));
+  return fmaf(hx, t, hx);
+}
+
 // apply over pixels [p_begin, p_end) of x viewed as [B·P][V vectors of 8]: block (V, R); thread
 // (v, r) always owns channel vector v, so its 8 (scale, shift) pairs stay in registers (reloaded
 // only when its pixel crosses into the next image); U pixel rows per thread per iteration, all
@@ -250,7 +261,7 @@ __global__ void __launch_bounds__(512) gn_apply_kernel(const T* __restrict__ x, 
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const float a = f[j] * sc[j] + sf[j];
-        o[j] = silu ? silu_f(a) : a;
+        o[j] = silu == 2 ? silu_tanh(a) : silu ? silu_f(a) : a;
       }
       store8(y + (p * V + v) * 8, o);
     }
@@ -288,7 +299,16 @@ static void gn_apply(const T* x, const T* x1, int C0, T* y, long p0, long p1, in
   if (!sms) SD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   const long want = (p1 - p0 + rows - 1) / rows;
   const int grid = (int)std::min<long>(want, (long)sms * (2048 / (blk.x * blk.y)));
-  gn_apply_kernel<T><<<grid, blk, 0, st>>>(x, x1, C0 / 8, p0, p1, P, C / 8, tab, silu ? 1 : 0, y);
+  // bf16 outputs: SiLU through one MUFU tanh instead of ex2 + rcp (the apply pass was partly
+  // MUFU-bound: 2 MUFU ops per element); fp32 outputs (the 1e-4 parity mode) keep the exact form.
+  // SD_SILU_TANH=0 restores ex2 + rcp for bf16 too.
+  static int st_env = -1;
+  if (st_env < 0) {
+    const char* e = getenv("SD_SILU_TANH");
+    st_env = e ? atoi(e) : 1;
+  }
+  const int sm = !silu ? 0 : (std::is_same<T, bf16>::value && st_env) ? 2 : 1;
+  gn_apply_kernel<T><<<grid, blk, 0, st>>>(x, x1, C0 / 8, p0, p1, P, C / 8, tab, sm, y);
   SD_CHECK_LAUNCH();
   (void)B;
 }
