@@ -158,8 +158,6 @@ def serving_bench(eng, world, rank, args):
       1. offline profiler: τ/δ table for c ∈ {1, 2}, m ≤ 8, n ≤ 3 on two streams (§III-C)
       2. C₁ = saturation throughput (16 requests arriving at t = 0)
       3. a Poisson trace at λ = ρ·C₁ per GPU, steps U{20..50}, g = 7.5 → images/s, mean / P99 E2E."""
-    import threading
-
     import torch
     import torch.distributed as dist
 
@@ -174,29 +172,9 @@ def serving_bench(eng, world, rank, args):
     c_max, c_star, _ = profiler.chunk_choice(tab, [1, 2], m=N_REQ, n=1)
     c_max = max(c_max, c_star)
     t_prof = time.perf_counter() - t0
-    stop = threading.Event()
     if world > 1:
-        import ctypes as C
-
-        def control():
-            """C1: all-gather of per-rank loads {waiting, decode-pending, active, completed} (+ a done
-            flag so every rank leaves the loop after the same number of collectives), then
-            sd_set_global_load so each controller sees the global waiting queue."""
-            mine = (C.c_int32 * 4)()
-            loads = torch.zeros(5, dtype=torch.int32, device=f"cuda:{rank}")
-            allv = torch.zeros(5 * world, dtype=torch.int32, device=f"cuda:{rank}")
-            epoch = 0
-            while True:
-                Bd.lib().sd_get_load(eng.h, mine)
-                loads.copy_(torch.tensor(list(mine) + [1 if stop.is_set() else 0], dtype=torch.int32))
-                dist.all_gather_into_tensor(allv, loads)
-                v = allv.cpu().tolist()
-                if all(v[5 * r + 4] for r in range(world)):
-                    break
-                flat = [x for r in range(world) for x in v[5 * r:5 * r + 4]]
-                Bd.lib().sd_set_global_load(eng.h, (C.c_int32 * (4 * world))(*flat), world, epoch)
-                epoch += 1
-                time.sleep(0.05)
+        from paper_2605_08835_b200 import control_plane
+        ctl = control_plane.LoadGather(eng, world, rank, group=args.ctl_group, device=rank)
     cal_trace = [(i, 0, n) for (i, _, n) in serving.poisson_trace(16, 0.0, seed=11)]
     # the first pass captures the CUDA graphs of the batch shapes the trace visits; the second is timed
     serving.run_trace(eng, h, cal_trace, LAT, N_REQ, c_star, c_max, n_max=3)
@@ -204,14 +182,12 @@ def serving_bench(eng, world, rank, args):
     c1 = cal["images_per_s"]
     full = serving.poisson_trace(args.serving_requests * world, args.rho * c1 * world, seed=7)
     mine_tr = [(i, a, n) for (i, a, n) in full if i % world == rank]
-    th = None
     if world > 1:
-        th = threading.Thread(target=control, daemon=True)
-        th.start()
+        ctl.start()
     _, m = serving.run_trace(eng, h, mine_tr, LAT, N_REQ, c_star, c_max, n_max=3)
-    stop.set()
-    if th:
-        th.join(timeout=600)  # leaves once every rank reported done (same number of collectives)
+    if world > 1:
+        ctl.stop()  # leaves once every rank reported done (same number of collectives)
+        m["allgather_us_mean"] = ctl.mean_us()
     Bd.lib().sd_table_free(h)
     out = {"workload": f"CFG#3-shaped: SD-1.5 512², Poisson λ = {args.rho}·C₁ per GPU, steps U{{20..50}}, g 7.5, "
                        f"controller on, c* = {c_star}, C_max = {c_max}, B_max = 8",
@@ -262,8 +238,12 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    args.ctl_group = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        # C1 runs on its own communicator (and, in control_plane, its own stream and thread), so the
+        # lockstep data plane below never waits on a peer
+        args.ctl_group = dist.new_group(backend="nccl")
     dev = torch.device(f"cuda:{local}")
     nsteps = args.denoise_steps
 
@@ -281,8 +261,6 @@ def main():
     slots = [eng.register(emb_d[i]) for i in range(N_REQ)]
     lat = torch.empty_like(z_d)
     imgs = torch.empty(N_REQ, 3, 8 * LAT, 8 * LAT, device=dev)
-    loads = torch.zeros(4, dtype=torch.int32, device=dev)
-    gathered = torch.zeros(world * 4, dtype=torch.int32, device=dev)
 
     def denoise_and_decode(slot_ids):
         with torch.cuda.stream(st):
@@ -290,10 +268,6 @@ def main():
             views = [lat[i] for i in range(N_REQ)]
             for s in range(nsteps):
                 eng.step(views, [s] * N_REQ, [nsteps] * N_REQ, [1] * N_REQ, [G] * N_REQ, slot_ids, stream=st)
-                if world > 1 and s % 10 == 0:
-                    # C1: all-gather of per-rank loads (waiting, decode-pending, active, completed)
-                    loads.fill_(N_REQ)
-                    dist.all_gather_into_tensor(gathered, loads)
             for i in range(N_REQ):
                 eng.decode(lat[i], 1, image=imgs[i], stream=st)
 

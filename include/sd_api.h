@@ -238,7 +238,10 @@ typedef struct {
 sd_status sd_serve_start(sd_engine* e, const sd_serve_config* cfg);
 sd_status sd_submit(sd_engine* e, const sd_request* r);    /* thread-safe; copies the embedding */
 sd_status sd_poll(sd_engine* e, sd_completion* out, int32_t max, int32_t* n_out, int32_t timeout_ms);
-sd_status sd_release(sd_engine* e, uint64_t id);           /* frees the completion's image        */
+/* sd_release: returns the completion's image buffer to the engine. Only ids already handed out by
+ * sd_poll may be released (SD_E_INVAL otherwise: unknown id, or completed but not yet polled);
+ * image_host / skipped_steps of that completion are invalid afterwards. */
+sd_status sd_release(sd_engine* e, uint64_t id);
 sd_status sd_serve_stop(sd_engine* e);                     /* drains nothing; stops the thread    */
 /* Controller trajectory (one record per planned window, in order): start / end µs, M, N, K, the level
  * and chunk count the window ran with, the waiting queue the controller then observed, its new level
@@ -289,6 +292,16 @@ sd_status sd_debug_groupnorm(const void* x, void* y, int32_t nb, int32_t P, int3
                              const float* beta, float eps, int32_t silu, void* stream);
 sd_status sd_debug_layernorm(const void* x, void* y, int32_t T, int32_t C, const float* gamma, const float* beta,
                              float eps, void* stream);
+/* sd_debug_step_eps: the UNet part of sd_step_batch only (K11 gather → UNet), with the same rows as
+ * sd_step_batch (cond rows in batch order, then uncond rows, R26): writes eps_dev = device fp32
+ * [rows][h][w][4] (NHWC, the UNet's output layout) and leaves the latents unchanged. Lets the parity
+ * tests compare ε_c and ε_u of every row on their own. Runs eagerly (no graph).
+ * sd_debug_combine_update: the K12 kernel only — ε̃ = has_uncond ? ε_u + g(ε_c − ε_u) : ε_c, then the
+ * DDIM / Euler update of latents[r] (R2-R5) — with an injected eps_dev in the same layout (rows as
+ * sd_step_batch would form them; b->ctx_slot may be NULL). This is how the closed forms of SURVEY
+ * §8(c) I7 (DDIM ε ≡ 0 telescoping; Euler constant ε) run through the GPU kernel. */
+sd_status sd_debug_step_eps(sd_engine* e, const sd_batch* b, float* eps_dev, void* stream);
+sd_status sd_debug_combine_update(sd_engine* e, const sd_batch* b, const float* eps_dev, void* stream);
 /* GEMM tile mode for the tests: 0 = heuristic, 1 = 128-row CTA tiles, 2 = 256-row CTA-pair tiles. */
 sd_status sd_debug_set_gemm_cg(int32_t cg);
 /* 3x3 / stride 2 / pad 1 conv (the UNet downsamplers) by TMA boxes with element stride 2: x bf16

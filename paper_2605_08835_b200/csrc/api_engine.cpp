@@ -133,8 +133,7 @@ extern "C" sd_status sd_ctx_release(sd_engine* e, int32_t slot) {
   return SD_OK;
 }
 
-extern "C" sd_status sd_step_batch(sd_engine* e, const sd_batch* b, void* stream) {
-  ENGINE_GUARD(e);
+static sd_status check_batch(sd_engine* e, const sd_batch* b, bool need_slots) {
   SD_REQUIRE(b && b->n_req >= 1 && b->n_req <= e->e.cfg.b_max, "sd_step_batch: n_req out of range [1, b_max]");
   SD_REQUIRE(b->latent_h >= 1 && b->latent_w >= 1 && b->latent_h <= e->e.cfg.max_latent_hw &&
                  b->latent_w <= e->e.cfg.max_latent_hw,
@@ -142,16 +141,40 @@ extern "C" sd_status sd_step_batch(sd_engine* e, const sd_batch* b, void* stream
   const int L = (int)e->e.uc.block_out.size();
   SD_REQUIRE(b->latent_h % (1 << (L - 1)) == 0 && b->latent_w % (1 << (L - 1)) == 0,
              "sd_step_batch: latent size must be divisible by 2^(levels-1)");
-  SD_REQUIRE(b->latents && b->step && b->n_steps && b->has_uncond && b->guidance && b->ctx_slot,
+  SD_REQUIRE(b->latents && b->step && b->n_steps && b->has_uncond && b->guidance && (b->ctx_slot || !need_slots),
              "sd_step_batch: null array");
   for (int r = 0; r < b->n_req; ++r) {
     SD_REQUIRE(b->latents[r], "sd_step_batch: null latent");
     SD_REQUIRE(b->n_steps[r] >= 1 && b->n_steps[r] <= 1000, "sd_step_batch: n_steps");
     SD_REQUIRE(b->step[r] >= 0 && b->step[r] < b->n_steps[r], "sd_step_batch: step index");
-    SD_REQUIRE(b->ctx_slot[r] >= 0 && b->ctx_slot[r] < e->e.max_slots && e->e.slot_used[b->ctx_slot[r]],
-               "sd_step_batch: ctx slot not registered");
+    if (need_slots)
+      SD_REQUIRE(b->ctx_slot[r] >= 0 && b->ctx_slot[r] < e->e.max_slots && e->e.slot_used[b->ctx_slot[r]],
+                 "sd_step_batch: ctx slot not registered");
   }
+  return SD_OK;
+}
+
+extern "C" sd_status sd_step_batch(sd_engine* e, const sd_batch* b, void* stream) {
+  ENGINE_GUARD(e);
+  const sd_status s = check_batch(e, b, true);
+  if (s != SD_OK) return s;
   ENGINE_BODY(e, { step_batch(&e->e, b, static_cast<cudaStream_t>(stream)); })
+}
+
+extern "C" sd_status sd_debug_step_eps(sd_engine* e, const sd_batch* b, float* eps_dev, void* stream) {
+  ENGINE_GUARD(e);
+  const sd_status s = check_batch(e, b, true);
+  if (s != SD_OK) return s;
+  SD_REQUIRE(eps_dev, "sd_debug_step_eps: null eps");
+  ENGINE_BODY(e, { step_batch(&e->e, b, static_cast<cudaStream_t>(stream), eps_dev, nullptr); })
+}
+
+extern "C" sd_status sd_debug_combine_update(sd_engine* e, const sd_batch* b, const float* eps_dev, void* stream) {
+  ENGINE_GUARD(e);
+  const sd_status s = check_batch(e, b, false);
+  if (s != SD_OK) return s;
+  SD_REQUIRE(eps_dev, "sd_debug_combine_update: null eps");
+  ENGINE_BODY(e, { step_batch(&e->e, b, static_cast<cudaStream_t>(stream), nullptr, eps_dev); })
 }
 
 extern "C" sd_status sd_sampler_init_sigma(sd_engine* e, int32_t n_steps, float* out) {

@@ -376,6 +376,7 @@ Engine::~Engine() {
   if (reg_scratch) cudaFree(reg_scratch);
   if (gn_ws) cudaFree(gn_ws);
   if (tile_scratch) cudaFree(tile_scratch);
+  if (tile_ev) cudaEventDestroy(tile_ev);
   if (time_ids) cudaFree(time_ids);
   if (reg_ev) cudaEventDestroy(reg_ev);
   if (meta_dev) cudaFree(meta_dev);
@@ -939,7 +940,10 @@ float init_sigma(int sampler, int n) {
 // ---------------------------------------------------------------------------------------------
 // sd_step_batch
 // ---------------------------------------------------------------------------------------------
-void step_batch(Engine* e, const sd_batch* b, cudaStream_t st) {
+// eps_dump (debug): run the gather and the UNet only, copy ε (fp32 NHWC [rows][h][w][4], rows in R26
+// order) to eps_dump and leave the latents alone. eps_inject (debug): skip the UNet and apply the K12
+// combine + sampler to the given ε (same layout). Both run eagerly (no graph).
+void step_batch(Engine* e, const sd_batch* b, cudaStream_t st, float* eps_dump, const float* eps_inject) {
   const int n = b->n_req, h = b->latent_h, w = b->latent_w, hw = h * w;
   std::vector<int> row_req, unc_row(n, -1);
   for (int r = 0; r < n; ++r) row_req.push_back(r);
@@ -972,7 +976,7 @@ void step_batch(Engine* e, const sd_batch* b, cudaStream_t st) {
   for (int k = 0; k < R; ++k) {
     const int r = row_req[k];
     t_row[k] = t_row[r];
-    kv[k] = k < n ? b->ctx_slot[r] : 0;
+    kv[k] = (k < n && b->ctx_slot) ? b->ctx_slot[r] : 0;
   }
   const size_t o_lat = put(lat.data(), n * sizeof(float*));
   const size_t o_cin = put(c_in.data(), n * 4);
@@ -1007,6 +1011,10 @@ void step_batch(Engine* e, const sd_batch* b, cudaStream_t st) {
   auto run = [&](cudaStream_t s) {
     e->ws.reset(0);
     float* eps;
+    if (eps_inject) {
+      combine_update(m, n, hw, eps_inject, 4, reinterpret_cast<float* const*>(db + o_lat), s);
+      return;
+    }
     if (e->f32) {
       float* x_in = e->ws.get<float>((size_t)R * hw * 64);
       gather_rows(m, R, hw, 64, x_in, s);
@@ -1018,9 +1026,13 @@ void step_batch(Engine* e, const sd_batch* b, cudaStream_t st) {
       eps = e->ws.get<float>((size_t)R * hw * 4);
       unet_forward<bf16>(e, s, R, h, w, x_in, m.t_row, kv_dev, eps);
     }
+    if (eps_dump) {
+      SD_CUDA(cudaMemcpyAsync(eps_dump, eps, (size_t)R * hw * 4 * sizeof(float), cudaMemcpyDeviceToDevice, s));
+      return;
+    }
     combine_update(m, n, hw, eps, 4, reinterpret_cast<float* const*>(db + o_lat), s);
   };
-  const bool use_graph = e->use_graphs;
+  const bool use_graph = e->use_graphs && !eps_dump && !eps_inject;
   const bool prof = e->prof.on;
   if (!use_graph) {
     run(st);

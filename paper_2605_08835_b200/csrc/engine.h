@@ -213,13 +213,16 @@ struct Engine {
   std::mutex dmu;
   void* tile_scratch = nullptr;  // V2 tiled decode: window latent + window image (grown on demand)
   size_t tile_scratch_bytes = 0;
+  cudaEvent_t tile_ev = nullptr;  // recorded after the last use of tile_scratch; the next user waits on it
+  std::mutex tile_mu;             // one tiled decode enqueues at a time
   void* server = nullptr;  // serve_gpu.cu Server while serving
   int upscale() const { return 1 << ((int)vc.block_out.size() - 1); }
   ~Engine();
 };
 
 void build_engine(Engine* e);
-void step_batch(Engine* e, const sd_batch* b, cudaStream_t st);
+void step_batch(Engine* e, const sd_batch* b, cudaStream_t st, float* eps_dump = nullptr,
+                const float* eps_inject = nullptr);
 int ctx_register(Engine* e, const float* emb, int len, int dim, const float* pooled, int pooled_dim, int slot,
                  cudaStream_t st);
 void vae_decode_chunk(Engine* e, const float* z, int h, int w, int n_chunks, int chunk, DecodeState** state,

@@ -31,6 +31,7 @@ struct STask {
   void* decode = nullptr;
   float* img_dev = nullptr;
   float* img_host = nullptr;
+  bool delivered = false;  // handed out by sd_poll (under Server::mu); sd_release requires it
 };
 
 struct LoopCfg {

@@ -347,6 +347,7 @@ extern "C" sd_status sd_poll(sd_engine* e, sd_completion* out, int32_t max, int3
     out[n].w = S->e->upscale() * t->w;
     out[n].image_host = t->img_host;
     out[n].skipped_steps = t->skips.data();
+    t->delivered = true;
     ++n;
   }
   *n_out = n;
@@ -358,7 +359,10 @@ extern "C" sd_status sd_release(sd_engine* e, uint64_t id) {
   Server* S = server_of(e);
   std::lock_guard<std::mutex> g(S->mu);
   auto it = S->owned.find(id);
-  SD_REQUIRE(it != S->owned.end() && it->second->V >= 0, "sd_release: unknown or unfinished id");
+  // only a task sd_poll has handed out may be released: complete() pushed it to `completed` under mu
+  // after its D2H finished, and sd_poll set `delivered` under mu, so nothing else still touches it
+  // (V is written by the loop thread outside mu and is not a safe completion flag)
+  SD_REQUIRE(it != S->owned.end() && it->second->delivered, "sd_release: unknown id, or not yet returned by sd_poll");
   if (it->second->img_host)
     S->pool_host[(size_t)3 * 64 * it->second->h * it->second->w * 4].push_back(it->second->img_host);
   delete it->second;

@@ -30,6 +30,9 @@ struct DecodeState {
   std::vector<VItem> items;
   std::vector<int64_t> cost;
   std::vector<int> bounds;
+  // recorded on the decode's stream when its last chunk has been enqueued and the state goes back to
+  // the pool; the next owner (possibly on another stream) waits on it before touching the buffers
+  cudaEvent_t done = nullptr;
 };
 
 // row bands of the tail layers: 32 rows (≥ 64-row layers) when the decode is chunked; one band per
@@ -416,6 +419,7 @@ static DecodeState* new_decode(Engine* e, int h, int w) {
 
 void destroy_decode(Engine* e, DecodeState* d) {
   (void)e;
+  if (d->done) cudaEventDestroy(d->done);
   d->ar.release();
   delete d;
 }
@@ -434,7 +438,10 @@ void vae_decode_chunk(Engine* e, const float* z, int h, int w, int n_chunks, int
           break;
         }
     }
-    if (!s) s = new_decode(e, h, w);
+    if (!s)
+      s = new_decode(e, h, w);
+    else
+      SD_CUDA(cudaStreamWaitEvent(st, s->done, 0));  // the previous owner's kernels may still run
     s->n_chunks = n_chunks;
     s->next_chunk = 0;
     if (s->nbands != bands_for(n_chunks)) {
@@ -456,6 +463,8 @@ void vae_decode_chunk(Engine* e, const float* z, int h, int w, int n_chunks, int
     }
   s->next_chunk++;
   if (s->next_chunk == n_chunks) {
+    if (!s->done) SD_CUDA(cudaEventCreateWithFlags(&s->done, cudaEventDisableTiming));
+    SD_CUDA(cudaEventRecord(s->done, st));
     std::lock_guard<std::mutex> g(e->dmu);
     e->free_decodes.push_back(s);
     *state = nullptr;
@@ -471,11 +480,16 @@ void vae_decode_tiled(Engine* e, const float* z, int h, int w, int tile, int hal
   const int f = e->upscale();
   const int wmax = std::min(h, tile + 2 * halo), vmax = std::min(w, tile + 2 * halo);
   const size_t lat_elems = (size_t)4 * wmax * vmax, img_elems = (size_t)3 * f * wmax * f * vmax;
+  // one scratch per engine, serialised across callers: a tiled decode enqueues under tile_mu, and the
+  // next caller's stream waits on tile_ev (the previous decode's last enqueued work)
+  std::unique_lock<std::mutex> tile_lock(e->tile_mu);
+  if (!e->tile_ev) SD_CUDA(cudaEventCreateWithFlags(&e->tile_ev, cudaEventDisableTiming));
+  else SD_CUDA(cudaStreamWaitEvent(st, e->tile_ev, 0));
   {
-    std::lock_guard<std::mutex> g(e->dmu);
     const size_t need = (lat_elems + img_elems) * sizeof(float) + 256;
     if (e->tile_scratch_bytes < need) {
       if (e->tile_scratch) {
+        SD_CUDA(cudaEventSynchronize(e->tile_ev));
         SD_CUDA(cudaStreamSynchronize(st));
         cudaFree(e->tile_scratch);
       }
@@ -502,6 +516,7 @@ void vae_decode_tiled(Engine* e, const float* z, int h, int w, int tile, int hal
                                   timg + (size_t)c * TH * TW + (size_t)f * (y0 - a0) * TW + f * (x0 - b0), (size_t)TW * 4,
                                   (size_t)f * (x1 - x0) * 4, f * (y1 - y0), cudaMemcpyDeviceToDevice, st));
     }
+  SD_CUDA(cudaEventRecord(e->tile_ev, st));
 }
 
 // min-max contiguous partition, boundaries placed as early as possible (oracle/vae.py chunk_ranges

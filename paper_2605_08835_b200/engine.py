@@ -103,15 +103,38 @@ class Engine:
         B.call("sd_sampler_init_sigma", self.h, n_steps, C.byref(v))
         return v.value
 
-    def step(self, latents, steps, n_steps, has_uncond, guidance, slots, stream=None):
-        """One sd_step_batch call. latents: list of cuda fp32 [4,h,w] tensors (updated in place)."""
+    @staticmethod
+    def _batch(latents, steps, n_steps, has_uncond, guidance, slots):
         n = len(latents)
         h, w = latents[0].shape[-2:]
         ptrs = (C.c_void_p * n)(*[t.data_ptr() for t in latents])
         b = B.Batch(n, h, w, C.cast(ptrs, C.POINTER(C.c_void_p)),
                     (C.c_int32 * n)(*steps), (C.c_int32 * n)(*n_steps), (C.c_uint8 * n)(*[int(x) for x in has_uncond]),
-                    (C.c_float * n)(*guidance), (C.c_int32 * n)(*slots))
+                    (C.c_float * n)(*guidance), (C.c_int32 * n)(*slots) if slots is not None else None)
+        return b, ptrs
+
+    def step(self, latents, steps, n_steps, has_uncond, guidance, slots, stream=None):
+        """One sd_step_batch call. latents: list of cuda fp32 [4,h,w] tensors (updated in place)."""
+        b, _keep = self._batch(latents, steps, n_steps, has_uncond, guidance, slots)
         B.call("sd_step_batch", self.h, C.byref(b), _stream(stream))
+
+    def step_eps(self, latents, steps, n_steps, has_uncond, guidance, slots, stream=None):
+        """sd_debug_step_eps: the UNet ε of every row of this step (cond rows, then uncond rows, R26),
+        returned as fp32 [rows, 4, h, w]; the latents are not updated."""
+        b, _keep = self._batch(latents, steps, n_steps, has_uncond, guidance, slots)
+        h, w = latents[0].shape[-2:]
+        rows = len(latents) + sum(1 for x in has_uncond if x)
+        eps = torch.empty(rows, h, w, 4, device=latents[0].device, dtype=torch.float32)
+        B.call("sd_debug_step_eps", self.h, C.byref(b), B._p(eps), _stream(stream))
+        return eps.permute(0, 3, 1, 2)
+
+    def combine_update(self, latents, steps, n_steps, has_uncond, guidance, eps, stream=None):
+        """sd_debug_combine_update: the K12 kernel alone with an injected ε (fp32 [rows, 4, h, w], rows
+        as sd_step_batch forms them); latents are updated in place."""
+        b, _keep = self._batch(latents, steps, n_steps, has_uncond, guidance, None)
+        e = eps.permute(0, 2, 3, 1).contiguous()
+        B.call("sd_debug_combine_update", self.h, C.byref(b), B._p(e), _stream(stream))
+        (torch.cuda.current_stream() if stream is None else stream).synchronize()
 
     def decode(self, latent: torch.Tensor, n_chunks=1, image=None, stream=None):
         """Whole or chunked VAE decode of one fp32 [4,h,w] latent → fp32 [3,8h,8w]."""
