@@ -259,6 +259,27 @@ sd_status sd_get_load(sd_engine* e, int32_t* out4);
 sd_status sd_serve_simulate(const sd_serve_config* cfg, const sd_table* t, int32_t n, const uint64_t* ids,
                             const int64_t* arrival_us, const int32_t* n_steps, int64_t* U_out, int64_t* V_out,
                             int32_t* n_skips_out, int32_t* windows_out);
+/* Stepping virtual-clock server: the same loop as sd_serve_start's, on the table's clock, advanced one
+ * window at a time by the caller — so P of them (one per rank, each on its shard id mod P, R32) can run
+ * in lockstep with the C1 all-gather of their loads between windows (tests). Policies
+ * SynerDiff and naive. sd_vserve_window: *state_out = 1 a window ran, 0 nothing was admitted and the
+ * clock jumped to the next arrival, -1 every request is done (no-op). sd_vserve_get_load: this server's
+ * {waiting (arrived, not admitted), decode-pending, active, completed} now. sd_vserve_set_global_load:
+ * the [P][4] snapshot; for P > 1 the controller then observes the snapshot's summed waiting queue (the
+ * GPU server's rule). sd_vserve_results: U_i, V_i, Skip-CFG steps per request in creation order, the
+ * clock and the window count. sd_vserve_trajectory: per window, the waiting queue the controller observed
+ * and its level / chunk count after deciding. */
+typedef struct sd_vserver sd_vserver;
+sd_status sd_vserve_create(const sd_serve_config* cfg, const sd_table* t, int32_t n, const uint64_t* ids,
+                           const int64_t* arrival_us, const int32_t* n_steps, sd_vserver** out);
+sd_status sd_vserve_window(sd_vserver* v, int32_t* state_out);
+sd_status sd_vserve_get_load(sd_vserver* v, int32_t* out4);
+sd_status sd_vserve_set_global_load(sd_vserver* v, const int32_t* loads, int32_t P, uint64_t epoch);
+sd_status sd_vserve_results(sd_vserver* v, int64_t* U_out, int64_t* V_out, int32_t* n_skips_out, int64_t* now_out,
+                            int32_t* windows_out);
+sd_status sd_vserve_trajectory(sd_vserver* v, int32_t max, int32_t* waiting, int32_t* level_after, int32_t* c_after,
+                               int32_t* n_out);
+sd_status sd_vserve_free(sd_vserver* v);
 /* The same with a latent size per request (mixed-resolution config: cfg->n_res tables). */
 sd_status sd_serve_simulate_mixed(const sd_serve_config* cfg, int32_t n, const uint64_t* ids, const int64_t* arrival_us,
                                   const int32_t* n_steps, const int32_t* latent_hw, int64_t* U_out, int64_t* V_out,

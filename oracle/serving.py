@@ -76,29 +76,59 @@ def simulate(trace, tables, b_max=8, a_num=1, a_den=10, mode="exact", c_star=1, 
         return _serial(trace, pick)
     if policy == "dynamic":
         return _dynamic(trace, pick, b_max, n_max, dyn_window_us)
-    naive = policy == "naive"
-    pending = _tasks(trace)
-    pi = 0
-    batch, dec, done = [], [], {}
-    now = 0
-    C = ctl.Controller(c_star=c_star, c_max=c_max, **(ctl_kw or {}))
-    while pi < len(pending) or batch or dec:
-        while pi < len(pending) and pending[pi].A <= now and len(batch) < b_max:
-            batch.append(pending[pi])
-            pi += 1
+    srv = Server(trace, pick, b_max, a_num, a_den, mode, c_star, c_max, ctl_kw, log, policy, no_skip, no_ctl, n_max)
+    while srv.window() != "done":
+        pass
+    return srv.done
+
+
+class Server:
+    """The SynerDiff / naive loop of `simulate` as a stepping object, so several of them (one per rank,
+    SURVEY §8(e)) can run in lockstep with the C1 all-gather between windows. window() runs one
+    window ("ran"), or, with nothing admitted, jumps the clock to the next arrival ("idle"), or reports
+    "done". With a global snapshot set (set_global_load, P > 1) the controller observes the summed
+    waiting queue of the snapshot instead of this server's own (R15; the GPU server's rule)."""
+
+    def __init__(self, trace, pick, b_max, a_num, a_den, mode, c_star, c_max, ctl_kw, log, policy, no_skip, no_ctl,
+                 n_max):
+        self.pick, self.b_max, self.a_num, self.a_den, self.mode = pick, b_max, a_num, a_den, mode
+        self.log, self.naive, self.no_skip, self.no_ctl, self.n_max = log, policy == "naive", no_skip, no_ctl, n_max
+        self.pending = _tasks(trace)
+        self.pi = 0
+        self.batch, self.dec, self.done = [], [], {}
+        self.now = 0
+        self.C = ctl.Controller(c_star=c_star, c_max=c_max, **(ctl_kw or {}))
+        self.global_load = None
+
+    def set_global_load(self, loads):
+        """loads: [P][4] ints (waiting, decode-pending, active, completed) — the C1 snapshot."""
+        self.global_load = [list(r) for r in loads]
+
+    def load(self):
+        waiting = sum(1 for t in self.pending[self.pi:] if t.A <= self.now)
+        return [waiting, len(self.dec), len(self.batch), len(self.done)]
+
+    def window(self):
+        if not (self.pi < len(self.pending) or self.batch or self.dec):
+            return "done"
+        pending, b_max, naive = self.pending, self.b_max, self.naive
+        batch, dec = self.batch, self.dec
+        while self.pi < len(pending) and pending[self.pi].A <= self.now and len(batch) < b_max:
+            batch.append(pending[self.pi])
+            self.pi += 1
         if not batch and not dec:
-            now = pending[pi].A
-            continue
-        level, c = C.level, C.c
-        if no_skip or naive:
+            self.now = pending[self.pi].A
+            return "idle"
+        level, c = self.C.level, self.C.c
+        if self.no_skip or naive:
             level = 0
         if naive:
             c = 1
         f = ctl.LEVELS[level]
         M = len(batch)
-        dq = sorted(dec, key=lambda t: (t.A, t.id))[:min(b_max, n_max)]
+        dq = sorted(dec, key=lambda t: (t.A, t.id))[:min(b_max, self.n_max)]
         N = len(dq)
-        tabs_w = pick(batch + dq)   # mixed resolutions: the table of the window's largest resolution
+        tabs_w = self.pick(batch + dq)   # mixed resolutions: the table of the window's largest resolution
         elig = [t.s >= ctl.s_min(f, t.n) for t in batch]
         K = sum(elig)
         if N == 0:
@@ -106,20 +136,20 @@ def simulate(trace, tables, b_max=8, a_num=1, a_den=10, mode="exact", c_star=1, 
         elif naive:
             stages, tc, rounds = (((M, min(N, M), 0),) if M else ((0, N, 0),)), 1, 1
         else:
-            stages = sched.plan_window(tabs_w[c], M, N, K, a_num, a_den, mode)
+            stages = sched.plan_window(tabs_w[c], M, N, K, self.a_num, self.a_den, self.mode)
             tc, rounds = c, c
         tab = tabs_w[tc]
         mapping = sched.map_tasks(stages, [(t.id, t.s, t.n, e) for t, e in zip(batch, elig)],
                                   [(t.id, t.A) for t in dq])
         by_id = {t.id: t for t in batch + dq}
-        if log is not None:
-            log.append(dict(now=now, M=M, N=N, K=K, level=level, c=c, stages=tuple(stages)))
+        if self.log is not None:
+            self.log.append(dict(now=self.now, M=M, N=N, K=K, level=level, c=c, stages=tuple(stages)))
         for (m, n, k), (u_ids, skip_ids, d_ids) in zip(stages, mapping):
             tau, delta = tab[(m, n, k)]
-            t0 = now
+            t0 = self.now
             per, rem = divmod(tau, rounds)
             for rho in range(rounds):
-                now += per + (rem if rho == rounds - 1 else 0)
+                self.now += per + (rem if rho == rounds - 1 else 0)
                 for uid in u_ids:
                     t = by_id[uid]
                     if t.s >= t.n:
@@ -128,18 +158,45 @@ def simulate(trace, tables, b_max=8, a_num=1, a_den=10, mode="exact", c_star=1, 
                         t.skips.append(t.s)
                     t.s += 1
                     if t.s == t.n:
-                        t.U = now
+                        t.U = self.now
                         batch.remove(t)
                         dec.append(t)
             for did in d_ids:
                 t = by_id[did]
                 t.V = t0 + delta
                 dec.remove(t)
-                done[t.id] = t
-        waiting = sum(1 for t in pending[pi:] if t.A <= now)
-        if not (naive or no_ctl):
-            C.decide(now, waiting)
-    return done
+                self.done[t.id] = t
+        waiting = sum(1 for t in pending[self.pi:] if t.A <= self.now)
+        gw = waiting if not self.global_load or len(self.global_load) <= 1 else sum(r[0] for r in self.global_load)
+        if not (naive or self.no_ctl):
+            self.C.decide(self.now, gw)
+        if self.log is not None:
+            self.log[-1].update(end=self.now, waiting=gw, level_after=self.C.level, c_after=self.C.c)
+        return "ran"
+
+
+def simulate_sharded(trace, P, tables, max_epochs=1_000_000, **kw):
+    """SURVEY §8(e) on a virtual clock: P servers, each on the shard {id : id mod P = rank} (R32), run in
+    lockstep epochs; in each epoch every server runs one window step (Server.window), then the C1
+    all-gather hands every server the same [P][4] snapshot of all loads (taken after the epoch).
+    Returns ({id: Task} per rank, [per-rank window logs])."""
+    pick = lambda ts: tables  # noqa: E731 (one resolution)
+    logs = [[] for _ in range(P)]
+    args = dict(b_max=8, a_num=1, a_den=10, mode="exact", c_star=1, c_max=4, ctl_kw=None, policy="synerdiff",
+                no_skip=False, no_ctl=False, n_max=None)
+    args.update(kw)
+    args["n_max"] = args["b_max"] if args["n_max"] is None else args["n_max"]
+    srv = [Server([e for e in trace if e[0] % P == r], pick, args["b_max"], args["a_num"], args["a_den"],
+                  args["mode"], args["c_star"], args["c_max"], args["ctl_kw"], logs[r], args["policy"],
+                  args["no_skip"], args["no_ctl"], args["n_max"]) for r in range(P)]
+    for _ in range(max_epochs):
+        states = [s.window() for s in srv]
+        if all(x == "done" for x in states):
+            break
+        snap = [s.load() for s in srv]
+        for s in srv:
+            s.set_global_load(snap)
+    return [s.done for s in srv], logs
 
 
 def _serial(trace, pick):

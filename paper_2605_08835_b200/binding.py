@@ -118,6 +118,13 @@ SIGNATURES = {
     "sd_serve_simulate": [C.POINTER(ServeConfig), P, I32, C.POINTER(C.c_uint64), PI64, PI32, PI64, PI64, PI32, PI32],
     "sd_serve_simulate_mixed": [C.POINTER(ServeConfig), I32, C.POINTER(C.c_uint64), PI64, PI32, PI32, PI64, PI64, PI32,
                                 PI32],
+    "sd_vserve_create": [C.POINTER(ServeConfig), P, I32, C.POINTER(C.c_uint64), PI64, PI32, C.POINTER(P)],
+    "sd_vserve_window": [P, PI32],
+    "sd_vserve_get_load": [P, PI32],
+    "sd_vserve_set_global_load": [P, PI32, I32, C.c_uint64],
+    "sd_vserve_results": [P, PI64, PI64, PI32, PI64, PI32],
+    "sd_vserve_trajectory": [P, I32, PI32, PI32, PI32, PI32],
+    "sd_vserve_free": [P],
     "sd_debug_gemm": [P, P, P, P, I32, I32, I32, I32, I32, P],
     "sd_debug_gemm_res": [P, P, P, P, I32, P, I32, I32, I32, P],
     "sd_debug_set_gemm_cg": [I32],

@@ -352,3 +352,135 @@ extern "C" sd_status sd_serve_simulate_mixed(const sd_serve_config* cfg, int32_t
   SD_REQUIRE(cfg && cfg->n_res > 0, "sd_serve_simulate_mixed: the config needs n_res tables");
   return simulate_impl(cfg, nullptr, n, ids, arrival_us, n_steps, latent_hw, U_out, V_out, n_skips_out, windows_out);
 }
+
+// ---- stepping virtual-clock server (multi-rank tests of C1) ----------------------
+namespace sd {
+struct VServer;
+struct VSExec : VirtualExec {
+  VServer* S = nullptr;
+  int64_t global_waiting(int64_t local) override;
+};
+struct VServer {
+  sd_serve_config cfg;
+  std::vector<STask> tasks;
+  Loop L;
+  VSExec ex;
+  std::vector<int32_t> global;  // [P][4] snapshot (sd_vserve_set_global_load)
+  int P = 0;
+  int windows = 0;
+  std::vector<WindowLog> wlog;
+};
+int64_t VSExec::global_waiting(int64_t local) {
+  if (S->P <= 1) return local;
+  int64_t sum = 0;
+  for (int r = 0; r < S->P; ++r) sum += S->global[4 * r];
+  return sum;
+}
+}  // namespace sd
+
+extern "C" sd_status sd_vserve_create(const sd_serve_config* cfg, const sd_table* table, int32_t n, const uint64_t* ids,
+                                      const int64_t* arrival_us, const int32_t* n_steps, sd_vserver** out) {
+  SD_REQUIRE(cfg && table && out && n >= 0 && (n == 0 || (ids && arrival_us && n_steps)), "sd_vserve_create: bad args");
+  SD_REQUIRE(cfg->b_max >= 1 && cfg->a_den > 0 && cfg->c_star >= 1 && cfg->ctl.c_max >= cfg->c_star,
+             "sd_vserve_create: bad config");
+  SD_REQUIRE(cfg->policy == SD_POLICY_SYNERDIFF || cfg->policy == SD_POLICY_NAIVE,
+             "sd_vserve_create: SynerDiff or naive policy");
+  for (int i = 0; i < n; ++i) SD_REQUIRE(n_steps[i] >= 1 && arrival_us[i] >= 0, "sd_vserve_create: bad request");
+  SD_API_BEGIN
+  auto* V = new VServer();
+  V->cfg = *cfg;
+  V->tasks.resize(n);
+  Loop& L = V->L;
+  L.cfg.b_max = cfg->b_max;
+  L.cfg.n_max = cfg->n_max > 0 ? cfg->n_max : cfg->b_max;
+  L.cfg.a_num = cfg->a_num;
+  L.cfg.a_den = cfg->a_den;
+  L.cfg.dp_mode = cfg->dp_mode;
+  L.cfg.c_star = cfg->c_star;
+  L.table = &table->t;
+  L.ctl.cfg = cfg->ctl;
+  L.ctl.cfg.c_star = cfg->c_star;
+  L.ctl.c = cfg->c_star;
+  set_policy(L.cfg, cfg);
+  L.log = &V->wlog;
+  for (int i = 0; i < n; ++i) {
+    V->tasks[i].id = ids[i];
+    V->tasks[i].A = arrival_us[i];
+    V->tasks[i].n = n_steps[i];
+    insert_pending(L.pending, &V->tasks[i]);
+  }
+  V->ex.S = V;
+  *out = reinterpret_cast<sd_vserver*>(V);
+  SD_API_END
+}
+
+extern "C" sd_status sd_vserve_window(sd_vserver* h, int32_t* state_out) {
+  SD_REQUIRE(h && state_out, "sd_vserve_window: bad args");
+  SD_API_BEGIN
+  auto* V = reinterpret_cast<VServer*>(h);
+  Loop& L = V->L;
+  if (L.pending.empty() && L.batch.empty() && L.dec.empty()) {
+    *state_out = -1;
+  } else if (L.window(V->ex)) {
+    ++V->windows;
+    *state_out = 1;
+  } else {
+    V->ex.t = std::max(V->ex.t, L.next_event());
+    *state_out = 0;
+  }
+  SD_API_END
+}
+
+extern "C" sd_status sd_vserve_get_load(sd_vserver* h, int32_t* out4) {
+  SD_REQUIRE(h && out4, "sd_vserve_get_load: bad args");
+  auto* V = reinterpret_cast<VServer*>(h);
+  int32_t waiting = 0;
+  for (auto* t : V->L.pending)
+    if (t->A <= V->ex.t) ++waiting;
+  out4[0] = waiting;
+  out4[1] = (int32_t)V->L.dec.size();
+  out4[2] = (int32_t)V->L.batch.size();
+  out4[3] = (int32_t)V->ex.done.size();
+  return SD_OK;
+}
+
+extern "C" sd_status sd_vserve_set_global_load(sd_vserver* h, const int32_t* loads, int32_t P, uint64_t) {
+  SD_REQUIRE(h && loads && P >= 1, "sd_vserve_set_global_load: bad args");
+  auto* V = reinterpret_cast<VServer*>(h);
+  V->global.assign(loads, loads + 4 * P);
+  V->P = P;
+  return SD_OK;
+}
+
+extern "C" sd_status sd_vserve_results(sd_vserver* h, int64_t* U_out, int64_t* V_out, int32_t* n_skips_out,
+                                       int64_t* now_out, int32_t* windows_out) {
+  SD_REQUIRE(h, "sd_vserve_results: bad args");
+  auto* V = reinterpret_cast<VServer*>(h);
+  for (size_t i = 0; i < V->tasks.size(); ++i) {
+    if (U_out) U_out[i] = V->tasks[i].U;
+    if (V_out) V_out[i] = V->tasks[i].V;
+    if (n_skips_out) n_skips_out[i] = (int32_t)V->tasks[i].skips.size();
+  }
+  if (now_out) *now_out = V->ex.t;
+  if (windows_out) *windows_out = V->windows;
+  return SD_OK;
+}
+
+extern "C" sd_status sd_vserve_trajectory(sd_vserver* h, int32_t max, int32_t* waiting, int32_t* level_after,
+                                          int32_t* c_after, int32_t* n_out) {
+  SD_REQUIRE(h && n_out && max >= 0, "sd_vserve_trajectory: bad args");
+  auto* V = reinterpret_cast<VServer*>(h);
+  const int cnt = std::min<int>(max, (int)V->wlog.size());
+  for (int i = 0; i < cnt; ++i) {
+    if (waiting) waiting[i] = V->wlog[i].waiting;
+    if (level_after) level_after[i] = V->wlog[i].level_after;
+    if (c_after) c_after[i] = V->wlog[i].c_after;
+  }
+  *n_out = cnt;
+  return SD_OK;
+}
+
+extern "C" sd_status sd_vserve_free(sd_vserver* h) {
+  delete reinterpret_cast<VServer*>(h);
+  return SD_OK;
+}
