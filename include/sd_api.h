@@ -177,6 +177,17 @@ sd_status sd_controller_create(const sd_controller_config* cfg, sd_controller** 
 sd_status sd_controller_decide(sd_controller* c, int64_t now_us, int32_t global_queue, sd_directive* out);
 sd_status sd_controller_free(sd_controller* c);
 
+/* Task mapping E of Problem P ("(S, E)"; R14) for the stages S of a window: each decode goes to
+ * the stages in (arrival_us, id) order; the sum_t k_t Skip-CFG slots go to the eligible UNet tasks with
+ * the largest s/n_steps (ties: smaller id), the other UNet slots to the remaining tasks in the given
+ * (batch) order. Writes each UNet task's stage index and skip flag and each decode's stage index.
+ * SD_E_INVAL if the stages do not cover the window (sum m = n_unet, sum n = n_dec, sum k <= #eligible)
+ * or an array is NULL. Pure host function. */
+sd_status sd_map_tasks(const int32_t* stages, int32_t n_stages, int32_t n_unet, const uint64_t* unet_id,
+                       const int32_t* unet_s, const int32_t* unet_n, const uint8_t* unet_eligible, int32_t n_dec,
+                       const uint64_t* dec_id, const int64_t* dec_arrival, int32_t* unet_stage_out,
+                       uint8_t* unet_skip_out, int32_t* dec_stage_out);
+
 /* Min-max partition of the ordered VAE work list into c chunks (R7): boundaries[0..c]. */
 sd_status sd_chunk_ranges(const int64_t* costs, int32_t n_items, int32_t c, int32_t* boundaries_out);
 
@@ -249,6 +260,19 @@ sd_status sd_serve_stop(sd_engine* e);                     /* drains nothing; st
 sd_status sd_serve_window_log(sd_engine* e, int32_t max, int64_t* t_start, int64_t* t_end, int32_t* m, int32_t* n,
                               int32_t* k, int32_t* level, int32_t* c, int32_t* waiting, int32_t* level_after,
                               int32_t* c_after, int32_t* n_out);
+/* The decision record of window `window` (T5 replay, "scheduler's batch/chunk decisions"): the
+ * stages S the loop ran, and per task the inputs and output of the mapping E — UNet tasks in batch
+ * order {id, s (steps done), n_steps, eligible (s >= s_min at the window's level), stage, skip}, and the
+ * window's decodes in (A, id) order {id, A, stage} (stage -1: not planned in this window, naive policy).
+ * Together with sd_serve_window_log's M, N, K, level and c, the plan can be recomputed from the table
+ * and compared bit for bit; level_out / c_out (may be NULL) = the controller level and chunk count the
+ * window ran with. SD_E_INVAL for an unknown window or arrays shorter than the record. */
+typedef struct { uint64_t id; int32_t s, n_steps, eligible, stage, skip, pad_; } sd_logged_unet;
+typedef struct { uint64_t id; int64_t arrival_us; int32_t stage, pad_; } sd_logged_decode;
+sd_status sd_serve_window_plan(sd_engine* e, int32_t window, int32_t* stages_out, int32_t max_stages,
+                               int32_t* n_stages, sd_logged_unet* unet_out, int32_t max_unet, int32_t* n_unet,
+                               sd_logged_decode* dec_out, int32_t max_dec, int32_t* n_dec,
+                               int32_t* level_out, int32_t* c_out);
 /* loads = int32 [P][4] {waiting, decode-pending, active, completed} all-gathered over ranks (C1);
  * the controller then sums `waiting` over ranks. sd_get_load returns this rank's 4 counters. */
 sd_status sd_set_global_load(sd_engine* e, const int32_t* loads, int32_t P, uint64_t epoch);
@@ -280,6 +304,11 @@ sd_status sd_vserve_results(sd_vserver* v, int64_t* U_out, int64_t* V_out, int32
 sd_status sd_vserve_trajectory(sd_vserver* v, int32_t max, int32_t* waiting, int32_t* level_after, int32_t* c_after,
                                int32_t* n_out);
 sd_status sd_vserve_free(sd_vserver* v);
+/* sd_serve_window_plan for the stepping virtual-clock server. */
+sd_status sd_vserve_window_plan(sd_vserver* v, int32_t window, int32_t* stages_out, int32_t max_stages,
+                                int32_t* n_stages, sd_logged_unet* unet_out, int32_t max_unet, int32_t* n_unet,
+                                sd_logged_decode* dec_out, int32_t max_dec, int32_t* n_dec,
+                                int32_t* level_out, int32_t* c_out);
 /* The same with a latent size per request (mixed-resolution config: cfg->n_res tables). */
 sd_status sd_serve_simulate_mixed(const sd_serve_config* cfg, int32_t n, const uint64_t* ids, const int64_t* arrival_us,
                                   const int32_t* n_steps, const int32_t* latent_hw, int64_t* U_out, int64_t* V_out,

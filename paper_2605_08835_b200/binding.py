@@ -70,6 +70,15 @@ class Completion(C.Structure):
                 ("image_host", C.c_void_p), ("skipped_steps", C.POINTER(C.c_int32))]
 
 
+class LoggedUnet(C.Structure):
+    _fields_ = [("id", C.c_uint64), ("s", C.c_int32), ("n_steps", C.c_int32), ("eligible", C.c_int32),
+                ("stage", C.c_int32), ("skip", C.c_int32), ("pad_", C.c_int32)]
+
+
+class LoggedDecode(C.Structure):
+    _fields_ = [("id", C.c_uint64), ("arrival_us", C.c_int64), ("stage", C.c_int32), ("pad_", C.c_int32)]
+
+
 class Directive(C.Structure):
     _fields_ = [("level", C.c_int32), ("c", C.c_int32), ("changed", C.c_int32)]
 
@@ -125,6 +134,12 @@ SIGNATURES = {
     "sd_vserve_results": [P, PI64, PI64, PI32, PI64, PI32],
     "sd_vserve_trajectory": [P, I32, PI32, PI32, PI32, PI32],
     "sd_vserve_free": [P],
+    "sd_map_tasks": [PI32, I32, I32, C.POINTER(C.c_uint64), PI32, PI32, C.POINTER(C.c_uint8), I32,
+                     C.POINTER(C.c_uint64), PI64, PI32, C.POINTER(C.c_uint8), PI32],
+    "sd_serve_window_plan": [P, I32, PI32, I32, PI32, C.POINTER(LoggedUnet), I32, PI32, C.POINTER(LoggedDecode), I32,
+                             PI32, PI32, PI32],
+    "sd_vserve_window_plan": [P, I32, PI32, I32, PI32, C.POINTER(LoggedUnet), I32, PI32, C.POINTER(LoggedDecode),
+                              I32, PI32, PI32, PI32],
     "sd_debug_gemm": [P, P, P, P, I32, I32, I32, I32, I32, P],
     "sd_debug_gemm_res": [P, P, P, P, I32, P, I32, I32, I32, P],
     "sd_debug_set_gemm_cg": [I32],
@@ -173,6 +188,20 @@ def check(fn, status):
 
 def call(name, *args):
     return check(name, getattr(lib(), name)(*args))
+
+
+def window_plan(fn, handle, window):
+    """sd_serve_window_plan / sd_vserve_window_plan → (level, c, stages, [unet records], [decode records]):
+    unet (id, s, n_steps, eligible, stage, skip) in batch order, decode (id, arrival_us, stage) in (A, id) order."""
+    st = (C.c_int32 * 96)()
+    us = (LoggedUnet * 32)()
+    ds = (LoggedDecode * 32)()
+    ns, nu, nd, lv, c = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+    call(fn, handle, window, st, 32, C.byref(ns), us, 32, C.byref(nu), ds, 32, C.byref(nd), C.byref(lv), C.byref(c))
+    stages = tuple(tuple(st[3 * i:3 * i + 3]) for i in range(ns.value))
+    unet = [(u.id, u.s, u.n_steps, u.eligible, u.stage, u.skip) for u in us[:nu.value]]
+    dec = [(d.id, d.arrival_us, d.stage) for d in ds[:nd.value]]
+    return lv.value, c.value, stages, unet, dec
 
 
 def _p(x):

@@ -359,6 +359,80 @@ extern "C" sd_status sd_plan(const sd_table* t, int32_t M, int32_t N, int32_t K,
   SD_API_END
 }
 
+std::vector<StageMap> sd::map_tasks(const std::vector<std::array<int, 3>>& stages, const std::vector<MapTask>& unet,
+                                int n_dec) {
+  std::vector<int> el;
+  for (int i = 0; i < (int)unet.size(); ++i)
+    if (unet[i].eligible) el.push_back(i);
+  std::stable_sort(el.begin(), el.end(), [&](int a, int b) {
+    const int64_t l = (int64_t)unet[a].s * unet[b].n, r = (int64_t)unet[b].s * unet[a].n;  // s_a/n_a vs s_b/n_b
+    return l != r ? l > r : unet[a].id < unet[b].id;
+  });
+  int nskip = 0, nm = 0, nn = 0;
+  for (auto& st : stages) nskip += st[2], nm += st[0], nn += st[1];
+  if (nm != (int)unet.size() || nn != n_dec || nskip > (int)el.size())
+    throw std::invalid_argument("map_tasks: stages do not cover the window (sum m = M, sum n = N, sum k <= K)");
+  std::vector<int> skippers(el.begin(), el.begin() + nskip);
+  std::vector<uint8_t> is_skipper(unet.size(), 0);
+  for (int i : skippers) is_skipper[i] = 1;
+  std::vector<int> rest;
+  for (int i = 0; i < (int)unet.size(); ++i)
+    if (!is_skipper[i]) rest.push_back(i);
+  std::vector<StageMap> out;
+  size_t si = 0, ri = 0;
+  int di = 0;
+  for (auto& st : stages) {
+    StageMap sm;
+    for (int q = 0; q < st[2]; ++q) {
+      sm.unet.push_back(skippers[si++]);
+      sm.skip.push_back(1);
+    }
+    for (int q = 0; q < st[0] - st[2]; ++q) {
+      sm.unet.push_back(rest[ri++]);
+      sm.skip.push_back(0);
+    }
+    for (int q = 0; q < st[1]; ++q) sm.dec.push_back(di++);
+    out.push_back(std::move(sm));
+  }
+  return out;
+}
+
+// Task mapping E (R14) for given stages: decodes are ordered by (A_i, id) here; returns each task's
+// stage index and skip flag.
+extern "C" sd_status sd_map_tasks(const int32_t* stages, int32_t n_stages, int32_t n_unet, const uint64_t* unet_id,
+                                  const int32_t* unet_s, const int32_t* unet_n, const uint8_t* unet_eligible,
+                                  int32_t n_dec, const uint64_t* dec_id, const int64_t* dec_arrival,
+                                  int32_t* unet_stage_out, uint8_t* unet_skip_out, int32_t* dec_stage_out) {
+  SD_REQUIRE(n_stages >= 0 && n_unet >= 0 && n_dec >= 0 && (n_stages == 0 || stages), "sd_map_tasks: bad args");
+  SD_REQUIRE(n_unet == 0 || (unet_id && unet_s && unet_n && unet_eligible && unet_stage_out && unet_skip_out),
+             "sd_map_tasks: bad unet arrays");
+  SD_REQUIRE(n_dec == 0 || (dec_id && dec_arrival && dec_stage_out), "sd_map_tasks: bad decode arrays");
+  for (int i = 0; i < n_unet; ++i) SD_REQUIRE(unet_n[i] >= 1 && unet_s[i] >= 0, "sd_map_tasks: bad step counts");
+  for (int t = 0; t < n_stages; ++t)
+    SD_REQUIRE(stages[3 * t] >= 0 && stages[3 * t + 1] >= 0 && stages[3 * t + 2] >= 0 &&
+                   stages[3 * t + 2] <= stages[3 * t],
+               "sd_map_tasks: bad stage");
+  SD_API_BEGIN
+  std::vector<std::array<int, 3>> st(n_stages);
+  for (int t = 0; t < n_stages; ++t) st[t] = {stages[3 * t], stages[3 * t + 1], stages[3 * t + 2]};
+  std::vector<MapTask> u(n_unet);
+  for (int i = 0; i < n_unet; ++i) u[i] = MapTask{unet_id[i], unet_s[i], unet_n[i], unet_eligible[i] != 0};
+  std::vector<int> order(n_dec);
+  for (int i = 0; i < n_dec; ++i) order[i] = i;
+  std::sort(order.begin(), order.end(), [&](int a, int b) {
+    return dec_arrival[a] != dec_arrival[b] ? dec_arrival[a] < dec_arrival[b] : dec_id[a] < dec_id[b];
+  });
+  const auto E = map_tasks(st, u, n_dec);
+  for (int t = 0; t < n_stages; ++t) {
+    for (size_t q = 0; q < E[t].unet.size(); ++q) {
+      unet_stage_out[E[t].unet[q]] = t;
+      unet_skip_out[E[t].unet[q]] = E[t].skip[q];
+    }
+    for (int d : E[t].dec) dec_stage_out[order[d]] = t;
+  }
+  SD_API_END
+}
+
 extern "C" sd_status sd_controller_create(const sd_controller_config* cfg, sd_controller** out) {
   SD_REQUIRE(cfg && out && cfg->c_star >= 1 && cfg->c_max >= cfg->c_star && cfg->window >= 2 &&
                  cfg->hysteresis >= 1 && cfg->up_den > 0 && cfg->down_den > 0,

@@ -28,6 +28,23 @@ struct PlanOut {
 int64_t t_lim(int64_t tau, int a_num, int a_den);
 bool plan_window(const Table& T, int M, int N, int K, int c, int a_num, int a_den, int mode, PlanOut* out);
 
+// Task mapping E of Problem P (R14). unet = the batch in batch order, dec = the window's
+// decodes already ordered by (A_i, id). Skip slots go to the eligible tasks with the largest s/n
+// (then id); the remaining UNet slots follow batch order. Per stage: indexes into unet (skippers
+// first, in progress order, then the rest in batch order), their skip flags, and indexes into dec.
+struct MapTask {
+  uint64_t id;
+  int s, n;
+  bool eligible;
+};
+struct StageMap {
+  std::vector<int> unet;
+  std::vector<uint8_t> skip;
+  std::vector<int> dec;
+};
+std::vector<StageMap> map_tasks(const std::vector<std::array<int, 3>>& stages, const std::vector<MapTask>& unet,
+                                int n_dec);
+
 struct Controller {
   sd_controller_config cfg{};
   int level = 0, c = 1, n_up = 0, n_down = 0;

@@ -168,39 +168,40 @@ bool Loop::window(Exec& ex) {
     tc = c;
     rounds = c;
   }
+  // task mapping E (R14)
+  std::vector<MapTask> mt(M);
+  for (int i = 0; i < M; ++i) mt[i] = MapTask{batch[i]->id, batch[i]->s, batch[i]->n, elig[i] != 0};
+  int n_planned = 0;  // naive policy: only min(N, M) decodes join the window
+  for (auto& st : plan.stages) n_planned += st[1];
+  const std::vector<StageMap> E = map_tasks(plan.stages, mt, n_planned);
+  const std::vector<STask*> bsnap = batch;  // tasks leave `batch` as they finish below
   if (log) {
+    WindowLog wl{now, M, N, K, level, c, plan.stages};
+    wl.unet = mt;
+    wl.unet_stage.assign(M, -1);
+    wl.unet_skip.assign(M, 0);
+    for (size_t t = 0; t < E.size(); ++t)
+      for (size_t q = 0; q < E[t].unet.size(); ++q) {
+        wl.unet_stage[E[t].unet[q]] = (int)t;
+        wl.unet_skip[E[t].unet[q]] = E[t].skip[q];
+      }
+    for (auto* d : dq) {
+      wl.dec_id.push_back(d->id);
+      wl.dec_A.push_back(d->A);
+    }
+    wl.dec_stage.assign(N, -1);
+    for (size_t t = 0; t < E.size(); ++t)
+      for (int d : E[t].dec) wl.dec_stage[d] = (int)t;
     std::unique_lock<std::mutex> g;
     if (log_mu) g = std::unique_lock<std::mutex>(*log_mu);
-    log->push_back(WindowLog{now, M, N, K, level, c, plan.stages});
+    log->push_back(std::move(wl));
   }
-  // task mapping E (R14)
-  std::vector<STask*> el;
-  for (int i = 0; i < M; ++i)
-    if (elig[i]) el.push_back(batch[i]);
-  std::stable_sort(el.begin(), el.end(), [](const STask* a, const STask* b) {
-    const int64_t l = (int64_t)a->s * b->n, r = (int64_t)b->s * a->n;  // a.s/a.n vs b.s/b.n
-    return l != r ? l > r : a->id < b->id;
-  });
-  int nskip = 0;
-  for (auto& st : plan.stages) nskip += st[2];
-  std::vector<STask*> skippers(el.begin(), el.begin() + std::min<size_t>(nskip, el.size()));
-  std::vector<STask*> rest;
-  for (auto* t : batch)
-    if (std::find(skippers.begin(), skippers.end(), t) == skippers.end()) rest.push_back(t);
-  size_t si = 0, ri = 0, di = 0;
-  for (auto& st : plan.stages) {
-    const int m = st[0], n = st[1], k = st[2];
+  for (size_t ti = 0; ti < plan.stages.size(); ++ti) {
+    const int m = plan.stages[ti][0], n = plan.stages[ti][1], k = plan.stages[ti][2];
     std::vector<STask*> u_ids, d_ids;
-    std::vector<uint8_t> is_skip;
-    for (int q = 0; q < k; ++q) {
-      u_ids.push_back(skippers[si++]);
-      is_skip.push_back(1);
-    }
-    for (int q = 0; q < m - k; ++q) {
-      u_ids.push_back(rest[ri++]);
-      is_skip.push_back(0);
-    }
-    for (int q = 0; q < n; ++q) d_ids.push_back(dq[di++]);
+    std::vector<uint8_t> is_skip = E[ti].skip;
+    for (int q : E[ti].unet) u_ids.push_back(bsnap[q]);
+    for (int q : E[ti].dec) d_ids.push_back(dq[q]);
     int64_t tau, delta;
     if (!tb->get(tc, m, n, k, &tau, &delta))
       throw std::invalid_argument("latency table miss (c,m,n,k)=(" + std::to_string(tc) + "," + std::to_string(m) + "," +
@@ -478,6 +479,40 @@ extern "C" sd_status sd_vserve_trajectory(sd_vserver* h, int32_t max, int32_t* w
   }
   *n_out = cnt;
   return SD_OK;
+}
+
+namespace sd {
+sd_status window_plan_copy(const WindowLog& w, int32_t* stages_out, int32_t max_stages, int32_t* n_stages,
+                           sd_logged_unet* unet_out, int32_t max_unet, int32_t* n_unet, sd_logged_decode* dec_out,
+                           int32_t max_dec, int32_t* n_dec, int32_t* level_out, int32_t* c_out) {
+  if ((int)w.stages.size() > max_stages || (int)w.unet.size() > max_unet || (int)w.dec_id.size() > max_dec)
+    throw std::invalid_argument("window plan: output arrays too small");
+  for (size_t t = 0; t < w.stages.size(); ++t)
+    for (int q = 0; q < 3; ++q) stages_out[3 * t + q] = w.stages[t][q];
+  *n_stages = (int32_t)w.stages.size();
+  for (size_t i = 0; i < w.unet.size(); ++i)
+    unet_out[i] = sd_logged_unet{w.unet[i].id, w.unet[i].s, w.unet[i].n, w.unet[i].eligible ? 1 : 0,
+                                 w.unet_stage[i], w.unet_skip[i], 0};
+  *n_unet = (int32_t)w.unet.size();
+  for (size_t i = 0; i < w.dec_id.size(); ++i) dec_out[i] = sd_logged_decode{w.dec_id[i], w.dec_A[i], w.dec_stage[i], 0};
+  *n_dec = (int32_t)w.dec_id.size();
+  if (level_out) *level_out = w.level;
+  if (c_out) *c_out = w.c;
+  return SD_OK;
+}
+}  // namespace sd
+
+extern "C" sd_status sd_vserve_window_plan(sd_vserver* h, int32_t window, int32_t* stages_out, int32_t max_stages,
+                                           int32_t* n_stages, sd_logged_unet* unet_out, int32_t max_unet,
+                                           int32_t* n_unet, sd_logged_decode* dec_out, int32_t max_dec,
+                                           int32_t* n_dec, int32_t* level_out, int32_t* c_out) {
+  SD_REQUIRE(h && stages_out && n_stages && unet_out && n_unet && dec_out && n_dec, "sd_vserve_window_plan: bad args");
+  auto* V = reinterpret_cast<VServer*>(h);
+  SD_REQUIRE(window >= 0 && window < (int)V->wlog.size(), "sd_vserve_window_plan: no such window");
+  SD_API_BEGIN
+  window_plan_copy(V->wlog[window], stages_out, max_stages, n_stages, unet_out, max_unet, n_unet, dec_out, max_dec,
+                   n_dec, level_out, c_out);
+  SD_API_END
 }
 
 extern "C" sd_status sd_vserve_free(sd_vserver* h) {

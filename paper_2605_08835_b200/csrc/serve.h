@@ -51,6 +51,12 @@ struct WindowLog {
   int64_t now;
   int M, N, K, level, c;
   std::vector<std::array<int, 3>> stages;
+  // the window's task records and the mapping E the loop ran (T5 replay): batch order / (A, id) order
+  std::vector<MapTask> unet;
+  std::vector<int> unet_stage, unet_skip;
+  std::vector<uint64_t> dec_id;
+  std::vector<int64_t> dec_A;
+  std::vector<int> dec_stage;
   // after the window: its end, the waiting queue the controller observed, and its new state
   int64_t end = 0;
   int waiting = 0, level_after = 0, c_after = 0;
@@ -97,6 +103,9 @@ struct Loop {
                       const std::vector<uint8_t>& skip, const std::vector<STask*>& decs, std::vector<int64_t>* dd);
 };
 
+sd_status window_plan_copy(const WindowLog& w, int32_t* stages_out, int32_t max_stages, int32_t* n_stages,
+                           sd_logged_unet* unet_out, int32_t max_unet, int32_t* n_unet, sd_logged_decode* dec_out,
+                           int32_t max_dec, int32_t* n_dec, int32_t* level_out, int32_t* c_out);
 void insert_pending(std::vector<STask*>& pending, STask* t);
 void set_policy(LoopCfg& c, const sd_serve_config* cfg);
 void set_tables(Loop& L, const sd_serve_config* cfg);

@@ -432,6 +432,21 @@ extern "C" sd_status sd_get_load(sd_engine* e, int32_t* out4) {
   return SD_OK;
 }
 
+extern "C" sd_status sd_serve_window_plan(sd_engine* e, int32_t window, int32_t* stages_out, int32_t max_stages,
+                                          int32_t* n_stages, sd_logged_unet* unet_out, int32_t max_unet,
+                                          int32_t* n_unet, sd_logged_decode* dec_out, int32_t max_dec,
+                                          int32_t* n_dec, int32_t* level_out, int32_t* c_out) {
+  SD_REQUIRE(e && server_of(e) && stages_out && n_stages && unet_out && n_unet && dec_out && n_dec,
+             "sd_serve_window_plan: bad args");
+  Server* S = server_of(e);
+  std::lock_guard<std::mutex> g(S->mu);
+  SD_REQUIRE(window >= 0 && window < (int)S->wlog.size(), "sd_serve_window_plan: no such window");
+  SD_API_BEGIN
+  window_plan_copy(S->wlog[window], stages_out, max_stages, n_stages, unet_out, max_unet, n_unet, dec_out, max_dec,
+                   n_dec, level_out, c_out);
+  SD_API_END
+}
+
 // Controller trajectory of the running server (one record per planned window): window start / end
 // (µs), M, N, K, the level and chunk count the window ran with, the waiting queue the controller then
 // observed and its new level / chunk count. Call before sd_serve_stop; copies min(max, windows).

@@ -293,3 +293,107 @@ def test_serving_mixed_resolution_bitexact(policy):
         assert (U[i], V[i], ns[i]) == (t.U, t.V, len(t.skips)), (policy, i)
     for h in handles.values():
         B.lib().sd_table_free(h)
+
+
+def test_plan_alg1_hand_trace():
+    """sd_plan in both modes on the hand-traced Alg. 1 window (tests/golden/alg1_trace.json)."""
+    import json
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "alg1_trace.json")))
+    tab = {tuple(e["mnk"]): (e["tau"], e["delta"]) for e in g["table"]}
+    h = make_table(tab)
+    w = g["window"]
+    for mode, key in ((1, "alg1_result"), (0, "exact_result")):
+        st, cost, tm = cplan(h, w["M"], w["N"], w["K"], mode=mode)
+        r = g[key]
+        assert (st, cost, tm) == (tuple(tuple(s) for s in r["stages"]), r["cost"], r["time"]), key
+    B.lib().sd_table_free(h)
+
+
+def test_map_tasks_bitexact_vs_oracle():
+    """Task mapping E (R14): sd_map_tasks equals oracle.sched.map_tasks on random windows."""
+    rng = np.random.default_rng(11)
+    tab = random_table(rng)
+    checked = 0
+    for trial in range(300):
+        M = int(rng.integers(1, 7))
+        N = int(rng.integers(0, M + 1))
+        ns_ = rng.integers(2, 40, M)
+        ss = [int(rng.integers(0, n)) for n in ns_]
+        elig = [int(rng.random() < 0.6) for _ in range(M)]
+        K = sum(elig)
+        ids = [int(x) for x in rng.permutation(100)[:M]]
+        dids = [int(x) for x in rng.permutation(100)[:N]]
+        darr = [int(x) for x in rng.integers(0, 5, N)]                       # ties on A → id decides
+        stages = sched.plan_window(tab, M, N, K) if N else ((M, 0, 0),)
+        E = sched.map_tasks(stages, [(ids[i], ss[i], int(ns_[i]), bool(elig[i])) for i in range(M)],
+                            [(dids[j], darr[j]) for j in range(N)])
+        want_u = {}
+        want_d = {}
+        for t, (u_ids, skip_ids, d_ids) in enumerate(E):
+            for x in u_ids:
+                want_u[x] = (t, int(x in skip_ids))
+            for x in d_ids:
+                want_d[x] = t
+        T = len(stages)
+        us, sk, ds = (C.c_int32 * M)(), (C.c_uint8 * M)(), (C.c_int32 * max(N, 1))()
+        B.call("sd_map_tasks", (C.c_int32 * (3 * T))(*[v for s in stages for v in s]), T, M,
+               (C.c_uint64 * M)(*ids), (C.c_int32 * M)(*ss), (C.c_int32 * M)(*[int(x) for x in ns_]),
+               (C.c_uint8 * M)(*elig), N, (C.c_uint64 * max(N, 1))(*dids), (C.c_int64 * max(N, 1))(*darr),
+               us, sk, ds)
+        assert [(us[i], sk[i]) for i in range(M)] == [want_u[x] for x in ids]
+        assert [ds[j] for j in range(N)] == [want_d[x] for x in dids]
+        checked += 1
+    assert checked == 300
+    bad = B.lib().sd_map_tasks((C.c_int32 * 3)(2, 0, 0), 1, 1, (C.c_uint64 * 1)(0), (C.c_int32 * 1)(0),
+                               (C.c_int32 * 1)(5), (C.c_uint8 * 1)(0), 0, None, None, (C.c_int32 * 1)(),
+                               (C.c_uint8 * 1)(), None)
+    assert bad == B.SD_E_INVAL
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_vserve_decision_replay(mode):
+    """T5 on the virtual clock: every window's logged decision (stages S and mapping E) is recomputed from
+    the logged window inputs by oracle.sched.plan_window and oracle.sched.map_tasks and must be equal bit
+    for bit (PAPER.md:289-307, :327-349)."""
+    from oracle import sched as osched
+    rng = np.random.default_rng(5 + mode)
+    tabs = serve_table(rng)
+    h = make_multi_table(tabs)
+    n = 150
+    arr = np.cumsum(rng.exponential(1e6 / 9.0, n)).astype(np.int64)
+    steps = rng.integers(20, 51, n)
+    ctl_cfg = B.ControllerConfig(1, 4, 10, 3, 1, 2, -1, 5)
+    cfg = B.ServeConfig(8, 1, 10, mode, 1, ctl_cfg, h, 64, 1)
+    v = C.c_void_p()
+    B.call("sd_vserve_create", C.byref(cfg), h, n, (C.c_uint64 * n)(*range(n)), (C.c_int64 * n)(*arr.tolist()),
+           (C.c_int32 * n)(*steps.tolist()), C.byref(v))
+    state = C.c_int32()
+    windows = 0
+    while True:
+        B.call("sd_vserve_window", v, C.byref(state))
+        if state.value < 0:
+            break
+        windows += state.value
+    assert windows > 100
+    n_skipping = n_chunked = 0
+    for w in range(windows):
+        level, c, stages, unet, dec = B.window_plan("sd_vserve_window_plan", v, w)
+        M, N = len(unet), len(dec)
+        K = sum(u[3] for u in unet)
+        smin = {0: None, 1: lambda n_: -(-7 * n_ // 10), 2: lambda n_: -(-n_ // 2)}[level]
+        assert [u[3] for u in unet] == [int(smin is not None and u[1] >= smin(u[2])) for u in unet]   # R6
+        want = osched.plan_window(tabs[c], M, N, K, mode="exact" if mode == 0 else "alg1")
+        assert stages == want, (w, M, N, K, c, stages, want)
+        E = osched.map_tasks(stages, [(u[0], u[1], u[2], bool(u[3])) for u in unet], [(d[0], d[1]) for d in dec])
+        got_u = {u[0]: (u[4], u[5]) for u in unet}
+        got_d = {d[0]: d[2] for d in dec}
+        for t, (u_ids, skip_ids, d_ids) in enumerate(E):
+            for x in u_ids:
+                assert got_u[x] == (t, int(x in skip_ids)), (w, x)
+            for x in d_ids:
+                assert got_d[x] == t, (w, x)
+        n_skipping += sum(s[2] for s in stages) > 0
+        n_chunked += c > 1 and N > 0
+    assert n_skipping > 0 and n_chunked > 0     # the trace exercises Skip-CFG slots and c > 1 plans
+    B.lib().sd_vserve_free(v)
+    B.lib().sd_table_free(h)

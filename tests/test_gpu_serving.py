@@ -17,7 +17,7 @@ from paper_2605_08835_b200 import binding as B  # noqa: E402
 from paper_2605_08835_b200.engine import Engine  # noqa: E402
 
 
-def _table(cmax=3, bmax=4):
+def _rows(cmax=3, bmax=4):
     rows = []
     for c in range(1, cmax + 1):
         for m in range(0, bmax + 1):
@@ -30,12 +30,36 @@ def _table(cmax=3, bmax=4):
                     tau = sum(max(tu, tv) for _ in range(c)) if n else c * tu
                     delta = (c - 1) * max(tu, tv) + tv if n else 0
                     rows.append((c, m, n, k, tau, delta))
+    return rows
+
+
+def _table(cmax=3, bmax=4):
+    rows = _rows(cmax, bmax)
     n = len(rows)
     h = C.c_void_p()
     col = lambda i, t: (t * n)(*[r[i] for r in rows])
     B.call("sd_table_from_arrays", n, col(0, C.c_int32), col(1, C.c_int32), col(2, C.c_int32), col(3, C.c_int32),
            col(4, C.c_int64), col(5, C.c_int64), C.byref(h))
     return h
+
+
+def _replay(plans, rows):
+    """T5 (north star: "the scheduler's batch/chunk decisions bit-exact"): every window
+    the GPU server ran is re-planned from its logged inputs (M, N, K, c) by oracle.sched.plan_window, and
+    its task mapping E by oracle.sched.map_tasks; both must equal what the server executed."""
+    from oracle import sched
+    tabs = {}
+    for c, m, n, k, tau, delta in rows:
+        tabs.setdefault(c, {})[(m, n, k)] = (tau, delta)
+    for w, (level, c, stages, unet, dec) in enumerate(plans):
+        K = sum(u[3] for u in unet)
+        assert stages == sched.plan_window(tabs[c], len(unet), len(dec), K), w
+        E = sched.map_tasks(stages, [(u[0], u[1], u[2], bool(u[3])) for u in unet], [(d[0], d[1]) for d in dec])
+        got_u = {u[0]: (u[4], u[5]) for u in unet}
+        got_d = {d[0]: d[2] for d in dec}
+        for t, (u_ids, skip_ids, d_ids) in enumerate(E):
+            assert all(got_u[x] == (t, int(x in skip_ids)) for x in u_ids), w
+            assert all(got_d[x] == t for x in d_ids), w
 
 
 @pytest.mark.parametrize("cstar", [1, 2])
@@ -73,7 +97,9 @@ def test_serving_tiny_matches_oracle_alone(cstar):
     lv, la, cc, wt = (C.c_int32 * cap)(), (C.c_int32 * cap)(), (C.c_int32 * cap)(), (C.c_int32 * cap)()
     nw = C.c_int32()
     B.call("sd_serve_window_log", eng.h, cap, t0, t1, None, None, None, lv, cc, wt, la, None, C.byref(nw))
+    plans = [B.window_plan("sd_serve_window_plan", eng.h, w) for w in range(nw.value)]
     B.call("sd_serve_stop", eng.h)
+    _replay(plans, _rows())
     assert len(got) == n
     assert nw.value > 0
     assert all(t0[i] <= t1[i] <= t0[i + 1] for i in range(nw.value - 1))

@@ -102,6 +102,26 @@ def test_gelu_silu():
     np.testing.assert_allclose(nn.silu(x), x / (1 + np.exp(-x)), rtol=1e-15)
 
 
+def test_silu_closed_values():
+    """SiLU(x) = x·σ(x) (R30) pinned by values and identities that do not restate the formula:
+    σ(0) = 1/2 ⇒ SiLU(0) = 0 and SiLU'(0) = 1/2; σ(ln 3) = 3/4 ⇒ SiLU(ln 3) = (3/4)·ln 3 and
+    SiLU(−ln 3) = −(1/4)·ln 3; σ(x) + σ(−x) = 1 ⇒ SiLU(x) − SiLU(−x) = x; SiLU(x) → x (x → +∞) and
+    → 0 (x → −∞); the minimum satisfies x* = −1 − W(1/e), where SiLU(x*) = x* + 1 = −W(1/e)
+    = −0.2784645427610738 (Lambert W; omega-constant relation W(1/e)·e^{W(1/e)} = 1/e)."""
+    ln3 = math.log(3.0)
+    assert nn.silu(np.array([0.0]))[0] == 0.0
+    assert nn.silu(np.array([ln3]))[0] == pytest.approx(0.75 * ln3, rel=1e-15)
+    assert nn.silu(np.array([-ln3]))[0] == pytest.approx(-0.25 * ln3, rel=1e-15)
+    x = np.linspace(-8, 8, 65)
+    np.testing.assert_allclose(nn.silu(x) - nn.silu(-x), x, atol=1e-14)
+    assert nn.silu(np.array([40.0]))[0] == pytest.approx(40.0, rel=1e-15)
+    assert abs(nn.silu(np.array([-40.0]))[0]) < 1e-15
+    h = 1e-6
+    assert (nn.silu(np.array([h]))[0] - nn.silu(np.array([-h]))[0]) / (2 * h) == pytest.approx(0.5, rel=1e-9)
+    g = np.linspace(-1.4, -1.2, 200001)
+    assert nn.silu(g).min() == pytest.approx(-0.2784645427610738, abs=1e-12)
+
+
 def test_upsample():
     x = np.arange(4.0).reshape(1, 1, 2, 2)
     np.testing.assert_array_equal(nn.upsample_nearest2x(x)[0, 0],

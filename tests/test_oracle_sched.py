@@ -180,3 +180,29 @@ def test_controller_quiescence():
 def test_s_min():
     assert controller.s_min(Fraction(7, 10), 35) == 25 and controller.s_min(Fraction(1, 2), 21) == 11
     assert controller.s_min(None, 30) == 31
+
+
+ALG1 = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "alg1_trace.json")))
+
+
+def _alg1_table():
+    return {tuple(e["mnk"]): (e["tau"], e["delta"]) for e in ALG1["table"]}
+
+
+def test_alg1_hand_trace():
+    """Alg. 1 against a run traced by hand (tests/golden/alg1_trace.json): every
+    successful relaxation in visit order, the strict '<' on line 9, the smallest-u backtrack tie on
+    line 16, and the result — which differs from the exact DP's by that tie (R10)."""
+    tab, w = _alg1_table(), ALG1["window"]
+    lim = sched.t_lim(sched.tau_ref(tab, w["M"], w["N"], w["K"]))
+    assert lim == w["T_lim"]
+    trace = []
+    got = sched.solve_alg1(tab, w["M"], w["N"], w["K"], lim, trace=trace)
+    want = [(tuple(r["to"]), r["cost"], r["time"], tuple(r["from"]), tuple(r["action"])) for r in ALG1["relaxations"]]
+    assert trace == want
+    r = ALG1["alg1_result"]
+    assert got == (r["cost"], r["time"], tuple(tuple(s) for s in r["stages"]))
+    e = ALG1["exact_result"]
+    assert sched.solve_exact(tab, w["M"], w["N"], w["K"], lim) == (e["cost"], e["time"],
+                                                                    tuple(tuple(s) for s in e["stages"]))
+    assert sched.plan_window(tab, w["M"], w["N"], w["K"], mode="alg1") == tuple(tuple(s) for s in r["stages"])
