@@ -72,6 +72,15 @@ typedef struct {
 
 sd_status sd_engine_create(const sd_engine_config* cfg, int32_t cuda_device, sd_engine** out);
 sd_status sd_engine_destroy(sd_engine* e);
+/* sd_engine_set_weight (parity tests): overwrite one parameter, named as in diffusers'
+ * UNet2DConditionModel / AutoencoderKL decoder ("down_blocks.0.resnets.0.conv1.weight",
+ * "decoder.mid_block.attentions.0.to_q.bias", ...; the list is oracle/configs.py's), from host fp32
+ * values in that parameter's PyTorch layout ([O][I][3][3] conv, [O][I] linear, [C] norm / bias). The
+ * engine converts them to its own layout and precision (bf16 RNE, or fp32) with the same transform as
+ * its weight generator. Synchronous (the device is idle afterwards w.r.t. this call). Call it before
+ * sd_ctx_register / sd_ctx_set_uncond: cached text K/V of registered prompts are NOT recomputed.
+ * SD_E_INVAL: unknown name, or bytes != 4 x the parameter's element count. */
+sd_status sd_engine_set_weight(sd_engine* e, const char* name, const void* host, size_t bytes);
 const char* sd_last_error(void);
 const char* sd_status_str(sd_status s);
 /* Number of kernels this engine launched since creation (for the bench's gpu_launches claim). */
@@ -187,6 +196,18 @@ sd_status sd_map_tasks(const int32_t* stages, int32_t n_stages, int32_t n_unet, 
                        const int32_t* unet_s, const int32_t* unet_n, const uint8_t* unet_eligible, int32_t n_dec,
                        const uint64_t* dec_id, const int64_t* dec_arrival, int32_t* unet_stage_out,
                        uint8_t* unet_skip_out, int32_t* dec_stage_out);
+
+/* Offline chunk-granularity selection (Eq. 1; P:248 the C_max rule; R31), from a profiled
+ * table, for a window of m UNet requests and n decodes, over the candidate counts c_values[0..n_c):
+ *   T_u(c) = tau^c(m, n, 0), T_v(c) = delta^c(m, n, 0)                     (Eq. 2, measured)
+ *   T_u0(c) = c * tau^1(m, 0, 0)   the UNet alone over the same c rounds
+ *   T_v0    = delta^1(0, n, 0)     the decodes alone (delta^1(n, n, 0) if the table has no decode-only row)
+ *   L(c) = lam (T_u(c) - T_u0)/T_u0 + (1 - lam)(T_v(c) - T_v0)/T_v0,  lam = lam_num/lam_den (paper: 0.5)
+ *   c* = argmin L(c), ties to the smaller c;  C_max = the largest c with tau^c(m,n,0)/c <= 1.05 tau^1(m,0,0)
+ *   (else the smallest candidate). All comparisons are exact (integer µs, 128-bit rationals); cost_out
+ * (may be NULL) receives L(c) per candidate as double, for reporting. SD_E_INVAL on a missing table row. */
+sd_status sd_chunk_choice(const sd_table* t, int32_t m, int32_t n, const int32_t* c_values, int32_t n_c,
+                          int32_t lam_num, int32_t lam_den, int32_t* c_max_out, int32_t* c_star_out, double* cost_out);
 
 /* Min-max partition of the ordered VAE work list into c chunks (R7): boundaries[0..c]. */
 sd_status sd_chunk_ranges(const int64_t* costs, int32_t n_items, int32_t c, int32_t* boundaries_out);

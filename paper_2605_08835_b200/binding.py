@@ -96,6 +96,7 @@ SIGNATURES = {
     "sd_last_error": [],
     "sd_status_str": [I32],
     "sd_engine_launch_count": [P, PI64],
+    "sd_engine_set_weight": [P, C.c_char_p, P, C.c_size_t],
     "sd_engine_profile": [P, I32],
     "sd_engine_profile_read": [P, I32, C.POINTER(C.c_double), PI64, C.POINTER(C.c_double)],
     "sd_ctx_register": [P, P, I32, I32, PI32, P],
@@ -114,6 +115,7 @@ SIGNATURES = {
     "sd_controller_decide": [P, I64, I32, C.POINTER(Directive)],
     "sd_controller_free": [P],
     "sd_chunk_ranges": [PI64, I32, I32, PI32],
+    "sd_chunk_choice": [P, I32, I32, PI32, I32, I32, I32, PI32, PI32, C.POINTER(C.c_double)],
     "sd_engine_warmup": [P, I32, I32, I32, I32, P],
     "sd_vae_decode_tiled": [P, P, I32, I32, I32, I32, P, P],
     "sd_serve_start": [P, C.POINTER(ServeConfig)],

@@ -82,6 +82,12 @@ extern "C" sd_status sd_engine_destroy(sd_engine* e) {
   return SD_OK;
 }
 
+extern "C" sd_status sd_engine_set_weight(sd_engine* e, const char* name, const void* host, size_t bytes) {
+  ENGINE_GUARD(e);
+  SD_REQUIRE(name && host, "sd_engine_set_weight: null argument");
+  ENGINE_BODY(e, set_weight(&e->e, name, static_cast<const float*>(host), bytes));
+}
+
 extern "C" sd_status sd_engine_launch_count(sd_engine* e, int64_t* out) {
   SD_REQUIRE(e && out, "bad args");
   *out = (int64_t)g_launches.load();

@@ -433,6 +433,46 @@ extern "C" sd_status sd_map_tasks(const int32_t* stages, int32_t n_stages, int32
   SD_API_END
 }
 
+// Offline chunk selection (Eq. 1, P:248 the C_max 5 % rule, R31), exact in rationals.
+extern "C" sd_status sd_chunk_choice(const sd_table* t, int32_t m, int32_t n, const int32_t* c_values, int32_t n_c,
+                                     int32_t lam_num, int32_t lam_den, int32_t* c_max_out, int32_t* c_star_out,
+                                     double* cost_out) {
+  SD_REQUIRE(t && c_values && n_c >= 1 && c_max_out && c_star_out && m >= 1 && n >= 1 && n <= m,
+             "sd_chunk_choice: bad args");
+  SD_REQUIRE(lam_den > 0 && lam_num >= 0 && lam_num <= lam_den, "sd_chunk_choice: lambda must be in [0, 1]");
+  for (int i = 0; i < n_c; ++i) SD_REQUIRE(c_values[i] >= 1, "sd_chunk_choice: c >= 1");
+  SD_API_BEGIN
+  int64_t tu1, dummy, tv0;
+  if (!t->t.get(1, m, 0, 0, &tu1, &dummy)) throw std::invalid_argument("sd_chunk_choice: table lacks (1, m, 0, 0)");
+  if (!t->t.get(1, 0, n, 0, &dummy, &tv0) && !t->t.get(1, n, n, 0, &dummy, &tv0))
+    throw std::invalid_argument("sd_chunk_choice: table lacks (1, 0, n, 0) and (1, n, n, 0)");
+  if (tu1 <= 0 || tv0 <= 0) throw std::invalid_argument("sd_chunk_choice: zero baseline");
+  typedef __int128 i128;
+  int best = -1, cmax = -1;
+  i128 bn = 0, bd = 1;
+  for (int i = 0; i < n_c; ++i) {
+    const int c = c_values[i];
+    int64_t tau, delta;
+    if (!t->t.get(c, m, n, 0, &tau, &delta)) throw std::invalid_argument("sd_chunk_choice: table lacks (c, m, n, 0)");
+    const i128 tu0 = (i128)c * tu1;  // the UNet alone over the same c rounds
+    // L(c) = lam (Tu - Tu0)/Tu0 + (1 - lam)(Tv - Tv0)/Tv0 = num / den
+    const i128 num = (i128)lam_num * (tau - tu0) * tv0 + (i128)(lam_den - lam_num) * (delta - tv0) * tu0;
+    const i128 den = (i128)lam_den * tu0 * tv0;
+    if (cost_out) cost_out[i] = (double)num / (double)den;
+    if (best < 0 || num * bd < bn * den || (num * bd == bn * den && c < best)) {
+      best = c;
+      bn = num;
+      bd = den;
+    }
+    // C_max: concurrent UNet round tau/c <= (1 + 5 %) solo round tu1
+    if ((i128)tau * 100 <= (i128)c * tu1 * 105) cmax = std::max(cmax, c);
+  }
+  if (cmax < 0) cmax = *std::min_element(c_values, c_values + n_c);
+  *c_max_out = cmax;
+  *c_star_out = best;
+  SD_API_END
+}
+
 extern "C" sd_status sd_controller_create(const sd_controller_config* cfg, sd_controller** out) {
   SD_REQUIRE(cfg && out && cfg->c_star >= 1 && cfg->c_max >= cfg->c_star && cfg->window >= 2 &&
                  cfg->hysteresis >= 1 && cfg->up_den > 0 && cfg->down_den > 0,

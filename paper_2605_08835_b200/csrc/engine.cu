@@ -143,7 +143,9 @@ struct Builder {
     w.dst0 = d0;
     w.dst1 = d1;
     w.out_bf16 = bf ? 1 : 0;
+    w.src = nullptr;
     init_weight(w, st);
+    e->wreg[name] = w;
     n_params += n;
   }
   float* bias(const std::string& name, int n, long fan_in, float* dst = nullptr) {
@@ -334,6 +336,11 @@ static void build_vae(Engine* e, cudaStream_t st) {
     SD_CUDA(cudaMemsetAsync(w64, 0, 16 * 64 * es, st));
     SD_CUDA(cudaMemcpy2DAsync(w64, 64 * es, V.pq_w, 4 * es, 4 * es, 4, cudaMemcpyDeviceToDevice, st));
     V.pq_w = w64;
+    WeightInit& r = e->wreg["post_quant_conv.weight"];
+    r.layout = WL_ROWS;
+    r.dst0 = w64;
+    r.I = 4;
+    r.Ipad = 64;
   }
   V.cin_w = B.conv3("decoder.conv_in", cm, 4, 64, &V.cin_b);
   int dummy = 0;
@@ -403,6 +410,28 @@ static size_t unet_ws_bytes(const Engine* e) {
   // + split-K partials of one ≤ 64-pixel conv (≤ 8 splits × R·64 rows × 2·c_max fp32)
   const double split = 8.0 * R * 64 * 2 * e->uc.block_out.back() * 4;
   return (size_t)(top * 140 + split) + ((size_t)512 << 20);
+}
+
+// sd_engine_set_weight: canonical fp32 values (PyTorch layout of the named diffusers parameter) →
+// the kernel-side layout, through the generator kernel's own layout transform (weights.cu)
+void set_weight(Engine* e, const std::string& name, const float* host, size_t bytes) {
+  auto it = e->wreg.find(name);
+  if (it == e->wreg.end()) throw std::invalid_argument("sd_engine_set_weight: unknown parameter '" + name + "'");
+  WeightInit w = it->second;
+  if (bytes != (size_t)w.n * sizeof(float))
+    throw std::invalid_argument("sd_engine_set_weight: '" + name + "' has " + std::to_string(w.n) +
+                                " fp32 elements, got " + std::to_string(bytes) + " bytes");
+  SD_CUDA(cudaSetDevice(e->device));
+  float* d = nullptr;
+  SD_CUDA(cudaMalloc(&d, bytes));
+  cudaStream_t st;
+  SD_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  SD_CUDA(cudaMemcpyAsync(d, host, bytes, cudaMemcpyHostToDevice, st));
+  w.src = d;
+  init_weight(w, st);
+  SD_CUDA(cudaStreamSynchronize(st));
+  SD_CUDA(cudaStreamDestroy(st));
+  SD_CUDA(cudaFree(d));
 }
 
 void build_engine(Engine* e) {

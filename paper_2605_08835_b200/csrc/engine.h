@@ -2,6 +2,7 @@
 #pragma once
 #include <atomic>
 #include <map>
+#include <unordered_map>
 #include <mutex>
 #include <string>
 #include <tuple>
@@ -164,6 +165,9 @@ struct Engine {
   UNetCfg uc;
   VAECfg vc;
   Arena warena;          // weights
+  // canonical parameter name (diffusers naming, oracle/configs.py) → where and how it is stored
+  // (sd_engine_set_weight rewrites a tensor through the same layout transform as the generator)
+  std::unordered_map<std::string, WeightInit> wreg;
   Arena ws;              // UNet workspace (reset every step)
   UNetW U{};
   VAEW V{};
@@ -221,6 +225,7 @@ struct Engine {
 };
 
 void build_engine(Engine* e);
+void set_weight(Engine* e, const std::string& name, const float* host, size_t bytes);
 void step_batch(Engine* e, const sd_batch* b, cudaStream_t st, float* eps_dump = nullptr,
                 const float* eps_inject = nullptr);
 int ctx_register(Engine* e, const float* emb, int len, int dim, const float* pooled, int pooled_dim, int slot,

@@ -93,7 +93,7 @@ void latent_to_nhwc(const float* z, int hw, float scale, int cpad, T* out, cudaS
 void nhwc_to_nchw3(const float* x, int ld, long P, float* y, cudaStream_t st);
 
 // ---- weight init (weights.cu) — counter-based generator shared in spec with synth/ ----
-enum { WL_PLAIN = 0, WL_CONV3 = 1, WL_GEGLU = 2, WL_CONV1 = 3 };
+enum { WL_PLAIN = 0, WL_CONV3 = 1, WL_GEGLU = 2, WL_ROWS = 4 };  // WL_ROWS: [O][I] into rows of Ipad
 enum { WK_UNIFORM = 0, WK_GAMMA = 1, WK_BETA = 2 };
 struct WeightInit {
   uint64_t tseed;      // tensor_seed(global_seed, name)
@@ -107,6 +107,7 @@ struct WeightInit {
   void* dst0;
   void* dst1;
   int out_bf16;
+  const float* src;    // nullptr: generate; else canonical fp32 values (sd_engine_set_weight)
 };
 void init_weight(const WeightInit& w, cudaStream_t st);
 

@@ -25,7 +25,7 @@ __device__ __forceinline__ float gen(const WeightInit& w, long i) {
 __global__ void init_weight_kernel(const WeightInit w) {
   const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= w.n) return;
-  const float v = gen(w, i);
+  const float v = w.src ? w.src[i] : gen(w, i);
   void* dst = w.dst0;
   long off = i;
   if (w.layout == WL_CONV3) {
@@ -47,6 +47,8 @@ __global__ void init_weight_kernel(const WeightInit w) {
     const int j = (int)(gate ? row - w.F : row);
     const long drow = (long)(j / 64) * 128 + (gate ? 64 : 0) + (j % 64);
     off = drow * cols + c;
+  } else if (w.layout == WL_ROWS) {
+    off = (i / w.I) * w.Ipad + (i % w.I);
   }
   if (w.out_bf16)
     reinterpret_cast<bf16*>(dst)[off] = __float2bfloat16_rn(v);

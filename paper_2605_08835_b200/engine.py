@@ -52,6 +52,12 @@ class Engine:
         except Exception:
             pass
 
+    def set_weight(self, name, values):
+        """sd_engine_set_weight: host fp32 values in the parameter's PyTorch layout (numpy or torch CPU)."""
+        import numpy as np
+        a = np.ascontiguousarray(np.asarray(values, dtype=np.float32))
+        B.call("sd_engine_set_weight", self.h, name.encode(), C.c_void_p(a.ctypes.data), a.nbytes)
+
     def launch_count(self):
         v = C.c_int64()
         B.call("sd_engine_launch_count", self.h, C.byref(v))

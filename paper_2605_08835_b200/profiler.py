@@ -120,16 +120,15 @@ def write_csv(tab, path):
             f.write(f"{k[0]},{k[1]},{k[2]},{k[3]},{tab[k][0]},{tab[k][1]}\n")
 
 
-def chunk_choice(tab, c_values, m, n=1, lam=0.5):
-    """C_max (5 % rule) and c* = argmin Eq. 1 L(c) at (m, n, 0) against solo baselines."""
-    tu0 = tab[(1, m, 0, 0)][0]
-    tv0 = tab[(1, 0, n, 0)][1] if (1, 0, n, 0) in tab else tab[(1, n, n, 0)][1]
-    cost, conc = {}, {}
-    for c in c_values:
-        tau, delta = tab[(c, m, n, 0)]
-        conc[c] = tau / c
-        cost[c] = lam * (tau - c * tu0) / (c * tu0) + (1 - lam) * (delta - tv0) / tv0
-    ok = [c for c in c_values if conc[c] * 100 <= tu0 * 105]
-    c_max = max(ok) if ok else min(c_values)
-    c_star = min(sorted(cost), key=lambda c: (cost[c], c))
-    return c_max, c_star, cost
+def chunk_choice(tab, c_values, m, n=1, lam=(1, 2)):
+    """C_max (5 % rule) and c* = argmin Eq. 1 L(c) at (m, n, 0) against solo baselines —
+    computed by sd_chunk_choice in libsynerdiff.so (exact rationals); lam = λ as (num, den), paper 0.5."""
+    h = to_table_handle(tab)
+    try:
+        k = len(c_values)
+        cmax, cstar, cost = C.c_int32(), C.c_int32(), (C.c_double * k)()
+        B.call("sd_chunk_choice", h, m, n, (C.c_int32 * k)(*c_values), k, lam[0], lam[1], C.byref(cmax),
+               C.byref(cstar), cost)
+    finally:
+        B.lib().sd_table_free(h)
+    return cmax.value, cstar.value, {c: cost[i] for i, c in enumerate(c_values)}

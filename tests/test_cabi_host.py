@@ -397,3 +397,33 @@ def test_vserve_decision_replay(mode):
     assert n_skipping > 0 and n_chunked > 0     # the trace exercises Skip-CFG slots and c > 1 plans
     B.lib().sd_vserve_free(v)
     B.lib().sd_table_free(h)
+
+
+def test_chunk_choice_bitexact_vs_oracle():
+    """sd_chunk_choice (Eq. 1 L(c), c* = argmin with ties to the smaller c, and the C_max 5 % rule of
+    PAPER.md:248; R31) equals oracle.sched.chunk_cost / select_c / find_c_max evaluated in exact Fractions
+    on random profiled tables, including constructed exact ties."""
+    from fractions import Fraction as F
+    from paper_2605_08835_b200 import profiler
+    rng = np.random.default_rng(3)
+    for trial in range(200):
+        cs = [1, 2, 3, 4]
+        m, n = int(rng.integers(1, 9)), 1
+        n = int(rng.integers(1, m + 1))
+        tab = {}
+        tu1 = int(rng.integers(20_000, 80_000))
+        tab[(1, m, 0, 0)] = (tu1, 0)
+        tab[(1, 0, n, 0)] = (int(rng.integers(30_000, 90_000)), int(rng.integers(30_000, 90_000)))
+        for c in cs:
+            tau = int(c * tu1 * rng.uniform(0.98, 1.2))
+            tab[(c, m, n, 0)] = (tau, int(tau * rng.uniform(0.3, 1.0)))
+        if trial % 5 == 0:                 # exact tie between c = 1 and c = 2 → the smaller c
+            tau1, d1 = tab[(1, m, n, 0)]
+            tab[(2, m, n, 0)] = (2 * tau1, d1)   # (2τ − 2tu1)/(2tu1) = (τ − tu1)/tu1; same δ
+        cmax, cstar, cost = profiler.chunk_choice(tab, cs, m=m, n=n)
+        tv0 = tab[(1, 0, n, 0)][1]
+        L = {c: sched.chunk_cost(F(1, 2), tab[(c, m, n, 0)][0], tab[(c, m, n, 0)][1], c * tu1, tv0) for c in cs}
+        assert cstar == sched.select_c(L), trial
+        assert cmax == sched.find_c_max({c: F(tab[(c, m, n, 0)][0], c) for c in cs}, tu1), trial
+        for c in cs:
+            assert cost[c] == pytest.approx(float(L[c]), rel=1e-12, abs=1e-15)

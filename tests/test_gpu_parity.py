@@ -460,3 +460,52 @@ def test_vae_tiled_v2_sd_shape(sd15):
     e = rel(got.cpu().numpy(), whole.cpu().numpy())
     print(f"tiled V2 SD 32²: vs oracle {r:.3e}; vs whole decode {e:.3e}")
     assert r <= TOL
+
+
+@pytest.mark.parametrize("model", ["tiny", "tinyxl"])
+def test_set_weight_every_parameter(model):
+    """sd_engine_set_weight: EVERY oracle parameter of a seed-7 model is loaded into a
+    seed-0 engine by name in its PyTorch layout; one ragged step's per-row ε and a 2-chunk decode then
+    match the seed-7 oracle — so every name, layout transform (conv tap-major, GEGLU interleave, the
+    fused temb / text-K/V rows, padded channels) round-trips. Unknown names and wrong sizes are rejected."""
+    from paper_2605_08835_b200 import binding as B
+    ucfg = configs.TINY_UNET if model == "tiny" else configs.TINY_XL_UNET
+    vcfg = configs.TINY_VAE
+    eng = Engine(model, max_latent_hw=8, b_max=4, weight_seed=0)
+    try:
+        P7 = configs.unet_params(ucfg, 7, np.float32, bf16_weights=True)
+        V7 = configs.vae_params(vcfg, 7, np.float32, bf16_weights=True)
+        for name, val in list(P7.items()) + list(V7.items()):
+            eng.set_weight(name, val)
+        with pytest.raises(B.SDError):
+            eng.set_weight("no.such.parameter", np.zeros(4, np.float32))
+        with pytest.raises(B.SDError):
+            eng.set_weight("conv_in.bias", np.zeros(3, np.float32))
+        xl = ucfg.pooled_dim > 0
+        ctx_u = synth.uncond_embedding(0, ucfg.ctx_len, ucfg.ctx_dim)
+        pu = synth.uncond_pooled(0, ucfg.pooled_dim) if xl else None
+        eng.set_uncond(torch.from_numpy(ctx_u), torch.from_numpy(pu) if xl else None)
+        ctx = [synth.text_embedding(9, i, ucfg.ctx_len, ucfg.ctx_dim) for i in range(2)]
+        pc = [synth.pooled_embedding(9, i, ucfg.pooled_dim) if xl else None for i in range(2)]
+        slots = [eng.register(torch.from_numpy(c), torch.from_numpy(p) if xl else None) for c, p in zip(ctx, pc)]
+        x0 = [synth.initial_noise(9, i, 8, 8) for i in range(2)]
+        lat = [torch.from_numpy(x).cuda() for x in x0]
+        eps = eng.step_eps(lat, [0, 2], [4, 4], [1, 0], [7.5, 7.5], slots)
+        z = synth.initial_noise(9, 5, 8, 8)
+        img = eng.decode(torch.from_numpy(z).cuda(), 2)
+        torch.cuda.synchronize()
+        ts = sampling.timesteps(4)
+        order = [0, 1, 0]                       # R26: cond rows (requests 0, 1), then request 0's uncond row
+        cb = [synth.bf16_round(ctx[0]), synth.bf16_round(ctx[1]), synth.bf16_round(ctx_u)]
+        pooled = np.stack([pc[0], pc[1], pu]) if xl else None
+        ref = unet.forward(P7, ucfg, np.stack([x0[i] for i in order]), np.array([ts[0], ts[2], ts[0]]),
+                           np.stack(cb), pooled)
+        got = eps.cpu().numpy()
+        errs = [rel(got[k], ref[k]) for k in range(3)]
+        r_img = rel(img.cpu().numpy(), vae.decode(V7, vcfg, z[None])[0])
+        print(f"{model} set_weight: per-row eps rel-L2 {['%.2e' % e for e in errs]}, image {r_img:.2e}")
+        assert max(errs) <= TOL and r_img <= TOL
+        for s in slots:
+            eng.release(s)
+    finally:
+        eng.close()
