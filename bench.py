@@ -216,6 +216,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--denoise-steps", type=int, default=N_STEPS)
+    ap.add_argument("--precision", default="fp16", choices=["bf16", "fp16"],
+                    help="16-bit operand / storage type of the UNet and VAE kernels (fp32 accumulation either way; "
+                         "the weights are the bf16 values of R20 in both). fp16 (default): the paper's FP16 (P:315), "
+                         "8x lower error than bf16 at the same tensor-core rate")
+    ap.add_argument("--no-alt-precision", action="store_true",
+                    help="skip the second timed leg in the other 16-bit precision")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-serving", action="store_true")
@@ -247,7 +253,7 @@ def main():
     dev = torch.device(f"cuda:{local}")
     nsteps = args.denoise_steps
 
-    eng = Engine("sd15", max_latent_hw=LAT, b_max=N_REQ, device=local)
+    eng = Engine("sd15", max_latent_hw=LAT, b_max=N_REQ, device=local, precision=args.precision)
     eng.set_uncond(torch.from_numpy(synth.uncond_embedding(0, 77, 768)))
     st = torch.cuda.Stream(device=dev)
     ids = [rank * N_REQ + i for i in range(N_REQ)]
@@ -303,7 +309,7 @@ def main():
         for _ in range(args.steps):
             denoise_and_decode(slots)
     torch.cuda.synchronize()
-    prof = {c: eng.profile_read(c) for c in range(5)}
+    prof = {c: eng.profile_read(c) for c in (0, 1, 2, 3, 4, 7)}
     eng.profile(False)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -350,6 +356,36 @@ def main():
         except Exception as ex:  # the serving leg must never sink the bench line
             serving_out = {"error": repr(ex)}
 
+    # ---- the same device-resident step in the other 16-bit precision (same kernels; BASELINE's config
+    # names bf16, the product default is fp16 — both are reported, the headline is --precision) ----
+    alt = None
+    if not args.no_alt_precision:
+        for s_ in slots:
+            eng.release(s_)
+        eng.close()
+        torch.cuda.synchronize()
+        other = "bf16" if args.precision == "fp16" else "fp16"
+        eng = Engine("sd15", max_latent_hw=LAT, b_max=N_REQ, device=local, precision=other)
+        eng.set_uncond(torch.from_numpy(synth.uncond_embedding(0, 77, 768)))
+        slots = [eng.register(emb_d[i]) for i in range(N_REQ)]
+        for _ in range(args.warmup):
+            denoise_and_decode(slots)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(st)
+        for _ in range(args.steps):
+            denoise_and_decode(slots)
+        a1.record(st)
+        torch.cuda.synchronize()
+        ta = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(ta, op=dist.ReduceOp.MAX)
+        alt = {"dtype": other, "value": N_REQ * world * args.steps / (float(ta.item()) / 1e3), "unit": UNIT,
+               "ms_per_step": float(ta.item()) / args.steps,
+               "note": "same workload, kernels and timing rules; only the 16-bit operand / storage type differs"}
+
     if rank == 0:
         sus, burst, hbm, src = peaks()
         conv_ms, conv_n, conv_flops = prof[0]
@@ -360,6 +396,11 @@ def main():
             rate = w_ / (m_ / 1e3) if m_ > 0 else 0.0
             kern[name] = {"ms_per_step": m_ / args.steps, "launches": n_,
                           ("tflops" if c < 3 else "gbs"): rate / (1e12 if c < 3 else 1e9)}
+        m7, n7, w7 = prof[7]
+        kern["conv1x1_gemm"] = {"ms_per_step": m7 / args.steps, "launches": n7,
+                                "tflops": w7 / (m7 / 1e3) / 1e12 if m7 > 0 else 0.0}
+        # SURVEY §8(d) UNet conv fraction: conv3x3/up/down AND the 1×1 shortcut / proj_in / proj_out convs
+        conv_all = (conv_flops + w7) / ((conv_ms + m7) / 1e3) / 1e12 if conv_ms + m7 > 0 else 0.0
         traffic = None
         tp = os.path.join(ROOT, "profiles", "conv_traffic.json")
         if os.path.exists(tp):
@@ -367,13 +408,17 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded; random-init weights)",
+            "vs_baseline": None, "dtype": args.precision, "data": "synthetic (seeded; random-init weights)",
             "config": config(world),
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": sus, "unit": "TFLOP/s",
                          "frac": achieved / sus, "traffic": traffic,
                          "kernel": "conv3x3 implicit GEMM (tcgen05/TMEM/TMA), all UNet conv3x3 launches",
                          "peak_source": f"{src}, sustained bf16 (kernel timed inside a long step)",
-                         "launches": conv_n, "flops_per_launch": conv_flops / max(conv_n, 1)},
+                         "launches": conv_n, "flops_per_launch": conv_flops / max(conv_n, 1),
+                         "unet_conv_all": {"achieved": conv_all, "frac": conv_all / sus,
+                                           "gflop_per_unet_step": (conv_flops + w7) / args.steps / args.denoise_steps / 1e9,
+                                           "note": "SURVEY 8(d) definition: conv3x3 + 1x1 shortcut / proj_in / "
+                                                   "proj_out, all UNet launches"}},
             "kernels": kern,
             "e2e": e2e,
             "gpu_launches": n_launch,
@@ -381,6 +426,9 @@ def main():
             "latency_ms": {"mean_e2e": ms_max / args.steps, "p99_e2e": ms_max / args.steps,
                            "note": "lockstep batch: all 8 images of a step complete together"},
             "serving": serving_out,
+            "precision_alt": alt,
+            "precision_note": ("fp16 = fp16 operands / activations with the bf16-valued R20 weights held exactly; "
+                               "fp32 accumulation, statistics, latents and eps in both"),
         }
         if not args.no_cpu_baseline:
             try:

@@ -46,8 +46,11 @@ enum { SD_MODEL_TINY = 0, SD_MODEL_SD15 = 1, SD_MODEL_SDXL = 2, SD_MODEL_TINY_XL
 /* R19: SD_PREC_BF16 = the product path (bf16 weights / activations, fp32 accumulation and statistics,
  * tcgen05 tensor cores). SD_PREC_FP32 = the parity mode of SURVEY §8(c) ("fp32 mode: everything fp32",
  * rel-L2 ≤ 1e-4 vs the oracle): fp32 weights and activations, SIMT FP32 kernels (no tensor cores, no
- * split-K), same graph, same chunking; ~2x the weight memory. */
-enum { SD_PREC_BF16 = 0, SD_PREC_FP32 = 1 };
+ * split-K), same graph, same chunking; ~2x the weight memory. SD_PREC_FP16 = the bf16 path's kernels,
+ * graph and layouts with fp16 operands and storage (fp32 accumulation and statistics unchanged): the
+ * same tensor-core rate and bytes as bf16 with 3 more significand bits (the paper serves in FP16,
+ * P:315); the weights are still the R20 bf16 values, held in fp16 (exact for |w| >= 2^-17). */
+enum { SD_PREC_BF16 = 0, SD_PREC_FP32 = 1, SD_PREC_FP16 = 2 };
 enum { SD_SAMPLER_DDIM = 0, SD_SAMPLER_EULER = 1 };      /* R4 / R5                                  */
 
 typedef struct sd_engine sd_engine;
@@ -62,7 +65,7 @@ typedef struct sd_controller sd_controller;
  * synth/__init__.py documents the generator). */
 typedef struct {
   int32_t model;          /* SD_MODEL_* (SDXL: ~5.6 GB of bf16 weights)         */
-  int32_t precision;      /* SD_PREC_BF16 | SD_PREC_FP32 (parity mode)         */
+  int32_t precision;      /* SD_PREC_BF16 | SD_PREC_FP16 | SD_PREC_FP32 (parity) */
   int32_t sampler;        /* SD_SAMPLER_*                                      */
   int32_t max_latent_hw;  /* e.g. 64 for 512x512 images                        */
   int32_t b_max;          /* max requests per UNet call (paper: BS = 8) */
@@ -88,7 +91,8 @@ sd_status sd_engine_launch_count(sd_engine* e, int64_t* out);
 
 /* Device timing per kernel class, CUDA events on the launching stream around every launch
  * (used by bench.py for the live roofline). enable != 0 starts recording (and clears old records).
- * Classes: 0 conv3x3 implicit GEMM, 1 dense GEMM, 2 attention, 3 GroupNorm, 4 LayerNorm.
+ * Classes: 0 conv3x3 implicit GEMM, 1 dense GEMM, 2 attention, 3 GroupNorm, 4 LayerNorm, 5 other,
+ * 6 VAE, 7 the UNet's 1x1 convolutions (shortcuts, proj_in / proj_out; dense GEMMs, not in class 1).
  * work_out = algorithmic FLOPs (classes 0-2) or bytes (3-4) of the recorded launches. Reading
  * synchronises on the recorded events. */
 sd_status sd_engine_profile(sd_engine* e, int32_t enable);
@@ -358,6 +362,14 @@ sd_status sd_debug_attention(const void* q, const void* k, const void* v, void* 
  * o bf16 [rows*P][heads*d]; d in {40, 64, 80}, P % 128 == 0. */
 sd_status sd_debug_attention_tc(const void* qk, const void* vt, void* o, int32_t rows, int32_t heads, int32_t d,
                                 int32_t P, void* stream);
+/* tcgen05 cross-attention over a text K / Vᵀ cache: q [rows*P][heads*d]; kc [n_slots*Lk][ldk]
+ * with the K of head h at columns kcol + h*d; vtc [vt_rows][ld_keys] with Vᵀ of head h at rows vrow + h*d and
+ * key j of slot s at column s*ceil8(Lk) + j (slot stride rounded up to 8 keys: 16-byte aligned TMA boxes); kv_index (device int32 [rows]) = slot per batch row; o [rows*P][heads*d].
+ * f16 != 0: fp16 operands (SD_PREC_FP16), else bf16. d in {40, 64, 80, 160}; any Lk (masked in-kernel). */
+sd_status sd_debug_xattention_tc(const void* q, const void* kc, int32_t ldk, int32_t n_slots, int32_t kcol,
+                                 const void* vtc, int32_t vt_rows, int32_t ld_keys, int32_t vrow,
+                                 const int32_t* kv_index, int32_t Lk, void* o, int32_t rows, int32_t heads, int32_t d,
+                                 int32_t P, int32_t f16, void* stream);
 /* GroupNorm(+SiLU) over x bf16 [nb][P][C] (NHWC), G groups, fp32 gamma/beta; LayerNorm over x [T][C]. */
 sd_status sd_debug_groupnorm(const void* x, void* y, int32_t nb, int32_t P, int32_t C, int32_t G, const float* gamma,
                              const float* beta, float eps, int32_t silu, void* stream);

@@ -15,7 +15,7 @@ _lib = None
 
 SD_OK, SD_E_INVAL, SD_E_NOMEM, SD_E_CUDA, SD_E_AGAIN, SD_E_STATE, SD_E_NOTSUP = 0, -1, -2, -3, -4, -5, -6
 SD_MODEL_TINY, SD_MODEL_SD15, SD_MODEL_SDXL, SD_MODEL_TINY_XL = 0, 1, 2, 3
-SD_PREC_BF16, SD_PREC_FP32 = 0, 1
+SD_PREC_BF16, SD_PREC_FP32, SD_PREC_FP16 = 0, 1, 2
 SD_SAMPLER_DDIM, SD_SAMPLER_EULER = 0, 1
 ACT_NONE, ACT_SILU, ACT_GEGLU = 0, 1, 2
 
@@ -148,6 +148,7 @@ SIGNATURES = {
     "sd_debug_set_conv_splits": [I32],
     "sd_debug_attention": [P, P, P, P, I32, I32, I32, I32, I32, P],
     "sd_debug_attention_tc": [P, P, P, I32, I32, I32, I32, P],
+    "sd_debug_xattention_tc": [P, P, I32, I32, I32, P, I32, I32, I32, P, I32, P, I32, I32, I32, I32, I32, P],
     "sd_debug_groupnorm": [P, P, I32, I32, I32, I32, P, P, C.c_float, I32, P],
     "sd_debug_layernorm": [P, P, I32, I32, P, P, C.c_float, P],
     "sd_debug_conv3x3": [P, I32, P, I32, P, P, P, P, P, P, I32, I32, I32, I32, P],

@@ -172,10 +172,31 @@ extern "C" sd_status sd_debug_attention(const void* q, const void* k, const void
 extern "C" sd_status sd_debug_attention_tc(const void* qk, const void* vt, void* o, int32_t rows, int32_t heads,
                                            int32_t d, int32_t P, void* stream) {
   SD_REQUIRE(qk && vt && o && rows > 0 && heads > 0, "sd_debug_attention_tc: bad arguments");
-  SD_REQUIRE(sd::attention_tc_supported(d, P, heads * d), "sd_debug_attention_tc: d in {40,64,80}, P % 128 == 0");
+  SD_REQUIRE(sd::attention_tc_supported(d, P, heads * d), "sd_debug_attention_tc: d in {40,64,80,160}, P % 8 == 0");
   SD_API_BEGIN
   sd::attention_tc(static_cast<const bf16*>(qk), static_cast<const bf16*>(vt), static_cast<bf16*>(o), rows, heads, d,
                    heads * d, P, static_cast<cudaStream_t>(stream));
+  SD_API_END
+}
+
+extern "C" sd_status sd_debug_xattention_tc(const void* q, const void* kc, int32_t ldk, int32_t n_slots, int32_t kcol,
+                                            const void* vtc, int32_t vt_rows, int32_t ld_keys, int32_t vrow,
+                                            const int32_t* kv_index, int32_t Lk, void* o, int32_t rows, int32_t heads,
+                                            int32_t d, int32_t P, int32_t use_f16, void* stream) {
+  SD_REQUIRE(q && kc && vtc && kv_index && o && rows > 0 && heads > 0 && Lk > 0 && n_slots > 0,
+             "sd_debug_xattention_tc: bad arguments");
+  SD_REQUIRE(sd::attention_tc_supported(d, 128, heads * d) && ldk % 8 == 0 && ld_keys % 8 == 0,
+             "sd_debug_xattention_tc: d in {40,64,80,160}, ldk and ld_keys multiples of 8");
+  SD_API_BEGIN
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (use_f16)
+    sd::xattention_tc(static_cast<const f16*>(q), static_cast<const f16*>(kc), ldk, n_slots, kcol,
+                      static_cast<const f16*>(vtc), vt_rows, ld_keys, vrow, kv_index, Lk, static_cast<f16*>(o), rows,
+                      heads, d, heads * d, P, st);
+  else
+    sd::xattention_tc(static_cast<const bf16*>(q), static_cast<const bf16*>(kc), ldk, n_slots, kcol,
+                      static_cast<const bf16*>(vtc), vt_rows, ld_keys, vrow, kv_index, Lk, static_cast<bf16*>(o), rows,
+                      heads, d, heads * d, P, st);
   SD_API_END
 }
 

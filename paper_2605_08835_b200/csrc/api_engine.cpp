@@ -46,7 +46,8 @@ extern "C" sd_status sd_engine_create(const sd_engine_config* cfg, int32_t dev, 
   SD_REQUIRE(cfg->model == SD_MODEL_TINY || cfg->model == SD_MODEL_SD15 || cfg->model == SD_MODEL_SDXL ||
                  cfg->model == SD_MODEL_TINY_XL,
              "sd_engine_create: unknown model");
-  SD_REQUIRE(cfg->precision == SD_PREC_BF16 || cfg->precision == SD_PREC_FP32, "sd_engine_create: precision");
+  SD_REQUIRE(cfg->precision == SD_PREC_BF16 || cfg->precision == SD_PREC_FP32 ||
+                 cfg->precision == SD_PREC_FP16, "sd_engine_create: precision");
   SD_REQUIRE(cfg->sampler == SD_SAMPLER_DDIM || cfg->sampler == SD_SAMPLER_EULER, "sd_engine_create: sampler");
   SD_REQUIRE(cfg->max_latent_hw >= 8 && cfg->max_latent_hw <= 256, "sd_engine_create: max_latent_hw");
   SD_REQUIRE(cfg->b_max >= 1 && cfg->b_max <= 32, "sd_engine_create: b_max");

@@ -11,6 +11,8 @@
 
 #include <algorithm>
 
+#include <string.h>
+
 #include "common.cuh"
 #include "kernels_ew.h"
 
@@ -37,13 +39,21 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t&
                : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
                : "r"(addr));
 }
+template <bool F16>  // fp16 operands (SD_PREC_FP16) or bf16
 __device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
                                          uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+  if (F16)
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+  else
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
 template <int D>  // padded head dim (multiple of 16)
@@ -53,8 +63,9 @@ struct AttnSmem {
   static constexpr int BYTES = (Q_ELEMS + 4 * KV_ELEMS) * 2;
 };
 
-template <int D>
+template <int D, bool F16>
 __global__ void __launch_bounds__(128) attn_kernel(const AttnDesc a, float scale_log2) {
+  pdl_wait();
   using S = AttnSmem<D>;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   bf16* sQ = reinterpret_cast<bf16*>(smem_raw);
@@ -126,8 +137,8 @@ __global__ void __launch_bounds__(128) attn_kernel(const AttnDesc a, float scale
         const int key = np * 16 + (lane >> 4) * 8 + (lane & 7);
         const int col = kk * 16 + ((lane >> 3) & 1) * 8;
         ldsm_x4(smem_u32(cK + key * S::LD + col), b0, b1, b2, b3);
-        mma16816(s[2 * np], a0, a1, a2, a3, b0, b1);
-        mma16816(s[2 * np + 1], a0, a1, a2, a3, b2, b3);
+        mma16816<F16>(s[2 * np], a0, a1, a2, a3, b0, b1);
+        mma16816<F16>(s[2 * np + 1], a0, a1, a2, a3, b2, b3);
       }
     }
     // mask keys beyond Lk
@@ -180,18 +191,18 @@ __global__ void __launch_bounds__(128) attn_kernel(const AttnDesc a, float scale
     // ---- O += P V ----
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk) {  // 16 keys per step
-      const uint32_t p0 = pack_bf16(s[2 * kk][0], s[2 * kk][1]);
-      const uint32_t p1 = pack_bf16(s[2 * kk][2], s[2 * kk][3]);
-      const uint32_t p2 = pack_bf16(s[2 * kk + 1][0], s[2 * kk + 1][1]);
-      const uint32_t p3 = pack_bf16(s[2 * kk + 1][2], s[2 * kk + 1][3]);
+      const uint32_t p0 = pack16(s[2 * kk][0], s[2 * kk][1], F16);
+      const uint32_t p1 = pack16(s[2 * kk][2], s[2 * kk][3], F16);
+      const uint32_t p2 = pack16(s[2 * kk + 1][0], s[2 * kk + 1][1], F16);
+      const uint32_t p3 = pack16(s[2 * kk + 1][2], s[2 * kk + 1][3], F16);
 #pragma unroll
       for (int dp = 0; dp < D / 16; ++dp) {
         uint32_t b0, b1, b2, b3;
         const int key = kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
         const int col = dp * 16 + (lane >> 4) * 8;
         ldsm_x4_t(smem_u32(cV + key * S::LD + col), b0, b1, b2, b3);
-        mma16816(o[2 * dp], p0, p1, p2, p3, b0, b1);
-        mma16816(o[2 * dp + 1], p0, p1, p2, p3, b2, b3);
+        mma16816<F16>(o[2 * dp], p0, p1, p2, p3, b0, b1);
+        mma16816<F16>(o[2 * dp + 1], p0, p1, p2, p3, b2, b3);
       }
     }
     __syncthreads();
@@ -210,9 +221,9 @@ __global__ void __launch_bounds__(128) attn_kernel(const AttnDesc a, float scale
     const int c = i * 8 + 2 * t4;
     if (c < d) {
       if (r0 < a.Lq)
-        *reinterpret_cast<uint32_t*>(Og + (long)r0 * a.ldo + c) = pack_bf16(o[i][0] * inv0, o[i][1] * inv0);
+        *reinterpret_cast<uint32_t*>(Og + (long)r0 * a.ldo + c) = pack16(o[i][0] * inv0, o[i][1] * inv0, F16);
       if (r1 < a.Lq)
-        *reinterpret_cast<uint32_t*>(Og + (long)r1 * a.ldo + c) = pack_bf16(o[i][2] * inv1, o[i][3] * inv1);
+        *reinterpret_cast<uint32_t*>(Og + (long)r1 * a.ldo + c) = pack16(o[i][2] * inv1, o[i][3] * inv1, F16);
     }
   }
 }
@@ -229,8 +240,9 @@ struct XAttnSmem {
   static constexpr int BYTES = (2 * Q_ELEMS + 2 * KV_ELEMS) * 2;
 };
 
-template <int D, int LKP, int NW>
+template <int D, int LKP, int NW, bool F16>
 __global__ void __launch_bounds__(32 * NW) xattn_kernel(const AttnDesc a, float scale_log2, int qt_per_block) {
+  pdl_wait();
   using S = XAttnSmem<D, LKP, NW>;
   constexpr int NT = 32 * NW;
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -295,8 +307,8 @@ __global__ void __launch_bounds__(32 * NW) xattn_kernel(const AttnDesc a, float 
         const int key = np * 16 + (lane >> 4) * 8 + (lane & 7);
         const int col = kk * 16 + ((lane >> 3) & 1) * 8;
         ldsm_x4(smem_u32(sK + key * S::LD + col), b0, b1, b2, b3);
-        mma16816(s[2 * np], a0, a1, a2, a3, b0, b1);
-        mma16816(s[2 * np + 1], a0, a1, a2, a3, b2, b3);
+        mma16816<F16>(s[2 * np], a0, a1, a2, a3, b0, b1);
+        mma16816<F16>(s[2 * np + 1], a0, a1, a2, a3, b2, b3);
       }
     }
     // ---- exact softmax over the (masked) keys, rows g and g + 8 ----
@@ -336,18 +348,18 @@ __global__ void __launch_bounds__(32 * NW) xattn_kernel(const AttnDesc a, float 
     for (int i = 0; i < D / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
 #pragma unroll
     for (int kk = 0; kk < LKP / 16; ++kk) {
-      const uint32_t p0 = pack_bf16(s[2 * kk][0], s[2 * kk][1]);
-      const uint32_t p1 = pack_bf16(s[2 * kk][2], s[2 * kk][3]);
-      const uint32_t p2 = pack_bf16(s[2 * kk + 1][0], s[2 * kk + 1][1]);
-      const uint32_t p3 = pack_bf16(s[2 * kk + 1][2], s[2 * kk + 1][3]);
+      const uint32_t p0 = pack16(s[2 * kk][0], s[2 * kk][1], F16);
+      const uint32_t p1 = pack16(s[2 * kk][2], s[2 * kk][3], F16);
+      const uint32_t p2 = pack16(s[2 * kk + 1][0], s[2 * kk + 1][1], F16);
+      const uint32_t p3 = pack16(s[2 * kk + 1][2], s[2 * kk + 1][3], F16);
 #pragma unroll
       for (int dp = 0; dp < D / 16; ++dp) {
         uint32_t b0, b1, b2, b3;
         const int key = kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
         const int col = dp * 16 + (lane >> 4) * 8;
         ldsm_x4_t(smem_u32(sV + key * S::LD + col), b0, b1, b2, b3);
-        mma16816(o[2 * dp], p0, p1, p2, p3, b0, b1);
-        mma16816(o[2 * dp + 1], p0, p1, p2, p3, b2, b3);
+        mma16816<F16>(o[2 * dp], p0, p1, p2, p3, b0, b1);
+        mma16816<F16>(o[2 * dp + 1], p0, p1, p2, p3, b2, b3);
       }
     }
     const float inv0 = 1.f / rs[0], inv1 = 1.f / rs[1];
@@ -357,21 +369,21 @@ __global__ void __launch_bounds__(32 * NW) xattn_kernel(const AttnDesc a, float 
       const int c = i * 8 + 2 * t4;
       if (c < d) {
         if (r0 < a.Lq)
-          *reinterpret_cast<uint32_t*>(Og + (long)r0 * a.ldo + c) = pack_bf16(o[i][0] * inv0, o[i][1] * inv0);
+          *reinterpret_cast<uint32_t*>(Og + (long)r0 * a.ldo + c) = pack16(o[i][0] * inv0, o[i][1] * inv0, F16);
         if (r1 < a.Lq)
-          *reinterpret_cast<uint32_t*>(Og + (long)r1 * a.ldo + c) = pack_bf16(o[i][2] * inv1, o[i][3] * inv1);
+          *reinterpret_cast<uint32_t*>(Og + (long)r1 * a.ldo + c) = pack16(o[i][2] * inv1, o[i][3] * inv1, F16);
       }
     }
     __syncthreads();  // the buffer of tile t is refilled by the next iteration's prefetch
   }
 }
 
-template <int D, int LKP, int NW = 4>
+template <int D, int LKP, int NW, bool F16>
 static void launch_xattn(const AttnDesc& a, cudaStream_t st) {
   using S = XAttnSmem<D, LKP, NW>;
   static bool set = false;
   if (!set) {
-    SD_CUDA(cudaFuncSetAttribute(xattn_kernel<D, LKP, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES));
+    SD_CUDA(cudaFuncSetAttribute(xattn_kernel<D, LKP, NW, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES));
     set = true;
   }
   const int tiles = cdiv(a.Lq, S::BM);
@@ -381,25 +393,26 @@ static void launch_xattn(const AttnDesc& a, cudaStream_t st) {
   per = std::min(per, 16);
   dim3 grid(cdiv(tiles, per), a.heads, a.rows);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)a.d);
-  xattn_kernel<D, LKP, NW><<<grid, 32 * NW, S::BYTES, st>>>(a, scale_log2, per);
+  launch_k(xattn_kernel<D, LKP, NW, F16>, grid, 32 * NW, S::BYTES, st, a, scale_log2, per);
   SD_CHECK_LAUNCH();
 }
 
-template <int D>
+template <int D, bool F16>
 static void launch_attn(const AttnDesc& a, cudaStream_t st) {
   using S = AttnSmem<D>;
   static bool set = false;
   if (!set) {
-    SD_CUDA(cudaFuncSetAttribute(attn_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES));
+    SD_CUDA(cudaFuncSetAttribute(attn_kernel<D, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES));
     set = true;
   }
   dim3 grid(cdiv(a.Lq, S::BM), a.heads, a.rows);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)a.d);
-  attn_kernel<D><<<grid, 128, S::BYTES, st>>>(a, scale_log2);
+  launch_k(attn_kernel<D, F16>, grid, 128, S::BYTES, st, a, scale_log2);
   SD_CHECK_LAUNCH();
 }
 
-void attention(const AttnDesc& a, cudaStream_t st) {
+template <bool F16>
+static void attention16(const AttnDesc& a, cudaStream_t st) {
   if (a.d % 8 || (a.ldq | a.ldk | a.ldo) % 8) throw CudaError("attention: d and strides must be multiples of 8");
   static int nw = -1;  // SD_XATTN_NW=4|8: warps per short-context block (4: kbench r01, 53 vs 75 µs at 64²)
   if (nw < 0) {
@@ -407,7 +420,7 @@ void attention(const AttnDesc& a, cudaStream_t st) {
     nw = e && atoi(e) == 8 ? 8 : 4;
   }
   if (a.Lk <= 16 || (a.Lk <= 80 && a.d > 16)) {  // short context (the cached text tokens): one key tile
-#define SD_XA(D_, L_) return nw == 4 ? launch_xattn<D_, L_, 4>(a, st) : launch_xattn<D_, L_, 8>(a, st)
+#define SD_XA(D_, L_) return nw == 4 ? launch_xattn<D_, L_, 4, F16>(a, st) : launch_xattn<D_, L_, 8, F16>(a, st)
     if (a.Lk <= 16) {
       if (a.d <= 16) SD_XA(16, 16);
       if (a.d <= 32) SD_XA(32, 16);
@@ -419,18 +432,27 @@ void attention(const AttnDesc& a, cudaStream_t st) {
     }
 #undef SD_XA
   }
-  if (a.d <= 16) launch_attn<16>(a, st);
-  else if (a.d <= 32) launch_attn<32>(a, st);
-  else if (a.d <= 48) launch_attn<48>(a, st);
-  else if (a.d <= 64) launch_attn<64>(a, st);
-  else if (a.d <= 80) launch_attn<80>(a, st);
-  else if (a.d <= 128) launch_attn<128>(a, st);
-  else if (a.d <= 160) launch_attn<160>(a, st);
+  if (a.d <= 16) launch_attn<16, F16>(a, st);
+  else if (a.d <= 32) launch_attn<32, F16>(a, st);
+  else if (a.d <= 48) launch_attn<48, F16>(a, st);
+  else if (a.d <= 64) launch_attn<64, F16>(a, st);
+  else if (a.d <= 80) launch_attn<80, F16>(a, st);
+  else if (a.d <= 128) launch_attn<128, F16>(a, st);
+  else if (a.d <= 160) launch_attn<160, F16>(a, st);
   else throw CudaError("attention: head dim > 160 uses the GEMM path");
 }
 
+void attention(const AttnDesc& a, cudaStream_t st) { attention16<false>(a, st); }
+void attention(const AttnDescT<f16>& a, cudaStream_t st) {
+  static_assert(sizeof(AttnDescT<f16>) == sizeof(AttnDesc), "AttnDescT layouts must match");
+  AttnDesc b;
+  memcpy(static_cast<void*>(&b), static_cast<const void*>(&a), sizeof(b));
+  attention16<true>(b, st);
+}
+
 // ---- row softmax (VAE single-head attention, d = 512, via GEMMs) ------------------------------
-__global__ void softmax_rows_kernel(const float* __restrict__ S, bf16* __restrict__ P, int cols) {
+__global__ void softmax_rows_kernel(const float* __restrict__ S, bf16* __restrict__ P, int cols, int is_f16) {
+  pdl_wait();
   const long r = blockIdx.x;
   const float* s = S + r * cols;
   __shared__ float red[32];
@@ -459,11 +481,15 @@ __global__ void softmax_rows_kernel(const float* __restrict__ S, bf16* __restric
   }
   __syncthreads();
   const float inv = 1.f / red[0];
-  for (int c = threadIdx.x; c < cols; c += blockDim.x) P[r * cols + c] = __float2bfloat16(__expf(s[c] - m) * inv);
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) P[r * cols + c] = to16(__expf(s[c] - m) * inv, is_f16);
 }
 
 void softmax_rows(const float* S, bf16* P, int rows, int cols, cudaStream_t st) {
-  softmax_rows_kernel<<<rows, 256, 0, st>>>(S, P, cols);
+  launch_k(softmax_rows_kernel, rows, 256, 0, st, S, P, cols, 0);
+  SD_CHECK_LAUNCH();
+}
+void softmax_rows(const float* S, f16* P, int rows, int cols, cudaStream_t st) {
+  launch_k(softmax_rows_kernel, rows, 256, 0, st, S, reinterpret_cast<bf16*>(P), cols, 1);
   SD_CHECK_LAUNCH();
 }
 

@@ -16,6 +16,8 @@
 // S never leaves the SM; P never leaves shared memory. Bound: MUFU exp2 (16/clk/SM) at d ≤ 80.
 #include <float.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels_ew.h"
 
@@ -28,23 +30,27 @@ namespace sd {
 template <int D, int NB, int SPLIT = 1, int EMU = 0, int PT = 0>
 struct TcAttn {
   static constexpr int BQ = 128, BK = 128;
-  static constexpr int KQ = (D + 63) / 64;       // 64-column blocks of the head dim (Q/K tiles)
-  static constexpr int K16 = (D + 15) / 16;      // MMA k-steps of Q·Kᵀ
+  // T64 (d = 160): two 64-column SW128 blocks + one 32-column SW64 tail per Q / K tile, so that two K/V
+  // stages fit in shared memory (three full blocks would need 233.7 KB)
+  static constexpr bool T64 = D == 160;
+  static constexpr int KQ = T64 ? 2 : (D + 63) / 64;  // full 64-column blocks of the head dim (Q/K tiles)
+  static constexpr int K16 = (D + 15) / 16;           // MMA k-steps of Q·Kᵀ
   static constexpr int NPV = (D + 15) / 16 * 16; // N of the PV MMA (d padded to 16)
-  static constexpr int Q_BYTES = KQ * BQ * 128;
-  static constexpr int K_BYTES = KQ * BK * 128;
+  static constexpr int Q_BYTES = KQ * BQ * 128 + (T64 ? BQ * 64 : 0);
+  static constexpr int K_BYTES = KQ * BK * 128 + (T64 ? BK * 64 : 0);
   static constexpr int V_BYTES = 2 * NPV * 128;  // two 64-key blocks of Vᵀ rows
   static constexpr int STAGE = K_BYTES + V_BYTES;
-  static constexpr int STAGES = PT ? (NB == 2 && D <= 64 ? 4 : 3) : ((NB == 2 && D <= 64) ? 3 : 2);
+  static constexpr int STAGES = D > 128 ? 2 : PT ? (NB == 2 && D <= 64 ? 4 : 3) : ((NB == 2 && D <= 64) ? 3 : 2);
   static constexpr int P_BYTES = PT ? 0 : 2 * BQ * 128;  // one P tile: 128 rows × 128 keys bf16
   static constexpr int X_BYTES = 3 * 2 * 128 * 4;  // row-max / row-sum exchange of the SPLIT halves
   static constexpr int SMEM = 1024 + Q_BYTES + STAGES * STAGE + NB * P_BYTES + X_BYTES + 256;
   static constexpr int THREADS = 64 + 128 * SPLIT;
   static constexpr int TMEM_COLS = (NB == 2 || (PT && NPV > 64)) ? 512 : 256;  // S | O | P must fit
   static constexpr int O_COL = NB * 128;         // O accumulator after the S buffers
-  static constexpr int P_COL = NB == 1 ? (NPV <= 64 ? 192 : 256) : 384;  // P (bf16, 2 per column) in TMEM (OP ≥ 4)
+  static constexpr int P_COL =  // P (16-bit, 2 per column) in TMEM (OP ≥ 4), after O
+      NB == 1 ? (NPV <= 64 ? 192 : (NPV <= 128 ? 256 : 128 + NPV)) : 384;
   static_assert(V_BYTES % 1024 == 0, "Vᵀ tile rows must be a multiple of 8");
-  static_assert(NPV <= 128, "O must fit beside the S buffers");
+  static_assert(NPV <= 128 || (NB == 1 && PT && P_COL + 64 <= 512), "O must fit beside the S buffers");
 };
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
@@ -96,10 +102,29 @@ __device__ __forceinline__ float ex2_poly(float x) {
 // OP = 1 (SPLIT = 2 only): the thread's 64 scores are read from TMEM once and kept in registers for
 // both passes, and the S buffer is released to the MMA warp right after the loads, so S_{j+1} is
 // computed while this block's exps run; P is packed in place over the scores (register budget)
-template <int D, int NB, int SPLIT, int EMU, int OP = 0>
+// Where Q, K and Vᵀ come from. Self-attention: tq = tk = the fused q|k buffer (K at column C), Vᵀ
+// [C][rows·P]; keys of batch row r start at token r·P. Cross-attention (K7): tq = the Q projection,
+// tk = the text-K cache [slots·Lk][kv_width] and tvt = the text-Vᵀ cache [kv_width][ldkeys], both
+// written once per prompt at admission; batch row r reads the Lk keys of prompt slot kv_index[r].
+struct AttnTcArgs {
+  bf16* O;
+  int ldo, P, Lk;
+  float scale_log2;
+  int qcol0, kcol0, vrow0;  // column of head 0 in tq / tk; row of head 0's channels in tvt
+  const int* kv_index;      // nullptr: self-attention
+  int vt_slot;              // cross-attention: key columns per slot in tvt (Lk rounded up to 8: TMA needs the
+                            // inner box start 16-byte aligned)
+};
+
+template <int D, int NB, int SPLIT, int EMU, int OP, bool F16>  // F16: fp16 operands (SD_PREC_FP16)
 __global__ void __launch_bounds__(64 + 128 * SPLIT, 3 - NB)
-    attn_tc_kernel(const __grid_constant__ CUtensorMap tqk, const __grid_constant__ CUtensorMap tvt, bf16* __restrict__ O,
-                   int ldo, int C, int P, int Lk, float scale_log2) {
+    attn_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+                   const __grid_constant__ CUtensorMap tvt, const __grid_constant__ CUtensorMap tq_t,
+                   const __grid_constant__ CUtensorMap tk_t, const AttnTcArgs a) {
+  const int P = a.P, Lk = a.Lk, ldo = a.ldo;
+  constexpr bool is_f16 = F16;
+  const float scale_log2 = a.scale_log2;
+  bf16* __restrict__ O = a.O;
   using A = TcAttn<D, NB, SPLIT, EMU, (OP == 4 || OP == 5) ? 1 : 0>;
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned (SWIZZLE_128B atoms); offsetting the shared array itself keeps the pointer in the
@@ -125,6 +150,7 @@ __global__ void __launch_bounds__(64 + 128 * SPLIT, 3 - NB)
   const int q0 = qt * A::BQ;
   const int nb = (Lk + A::BK - 1) / A::BK;
   const int tok0 = row * P;  // first token of this batch row in the token-major buffers
+
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
     for (int s = 0; s < A::STAGES; ++s) {
@@ -139,7 +165,12 @@ __global__ void __launch_bounds__(64 + 128 * SPLIT, 3 - NB)
     mbar_init(pv_done, 1);
     mbar_init(q_ready, 4 * SPLIT);
     fence_mbar_init();
-    tma_prefetch(&tqk);
+    tma_prefetch(&tq);
+    if (A::T64) {
+      tma_prefetch(&tq_t);
+      tma_prefetch(&tk_t);
+    }
+    tma_prefetch(&tk);
     tma_prefetch(&tvt);
   }
   if (warp == 1) tmem_alloc(tmem_slot, A::TMEM_COLS);
@@ -147,29 +178,39 @@ __global__ void __launch_bounds__(64 + 128 * SPLIT, 3 - NB)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;  // S buffers at columns 0 / 128, O at 256
+  pdl_wait();  // the prologue above overlapped the previous grid's tail (PDL)
+  // first key row of this batch row in tk / first key column in tvt
+  const int slot = a.kv_index ? __ldg(a.kv_index + row) : 0;
+  const int key0 = a.kv_index ? slot * Lk : tok0;
+  const int vkey0 = a.kv_index ? slot * a.vt_slot : tok0;
 
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer ----------------
       mbar_expect_tx(q_full, A::Q_BYTES);
       for (int kb = 0; kb < A::KQ; ++kb)
-        tma_load_2d(sQ + kb * A::BQ * 128, &tqk, q_full, head * D + kb * 64, tok0 + q0);
+        tma_load_2d(sQ + kb * A::BQ * 128, &tq, q_full, a.qcol0 + head * D + kb * 64, tok0 + q0);
+      if (A::T64) tma_load_2d(sQ + A::KQ * A::BQ * 128, &tq_t, q_full, a.qcol0 + head * D + A::KQ * 64, tok0 + q0);
       for (int j = 0; j < nb; ++j) {
         const int s = j % A::STAGES;
         mbar_wait_sleep(&kv_empty[s], ((j / A::STAGES) & 1) ^ 1);
         mbar_expect_tx(&kv_full[s], A::STAGE);
         uint8_t* st = sKV + s * A::STAGE;
         for (int kb = 0; kb < A::KQ; ++kb)
-          tma_load_2d(st + kb * A::BK * 128, &tqk, &kv_full[s], C + head * D + kb * 64, tok0 + j * A::BK);
+          tma_load_2d(st + kb * A::BK * 128, &tk, &kv_full[s], a.kcol0 + head * D + kb * 64, key0 + j * A::BK);
+        if (A::T64)
+          tma_load_2d(st + A::KQ * A::BK * 128, &tk_t, &kv_full[s], a.kcol0 + head * D + A::KQ * 64,
+                      key0 + j * A::BK);
         for (int h = 0; h < 2; ++h)
-          tma_load_2d(st + A::K_BYTES + h * A::NPV * 128, &tvt, &kv_full[s], tok0 + j * A::BK + h * 64, head * D);
+          tma_load_2d(st + A::K_BYTES + h * A::NPV * 128, &tvt, &kv_full[s], vkey0 + j * A::BK + h * 64,
+                      a.vrow0 + head * D);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       // ---------------- MMA issuer ----------------
-      constexpr uint32_t id_s = make_idesc_bf16(128, 128);
-      constexpr uint32_t id_pv = make_idesc_bf16(128, A::NPV);
+      constexpr uint32_t id_s = make_idesc16(128, 128, F16);
+      constexpr uint32_t id_pv = make_idesc16(128, A::NPV, F16);
       mbar_wait(q_ready, 0);  // Q landed and its padded columns were zeroed by the softmax warps
       tc_fence_after();
       const uint32_t aq = smem_u32(sQ);
@@ -182,8 +223,13 @@ __global__ void __launch_bounds__(64 + 128 * SPLIT, 3 - NB)
           const uint32_t ak = smem_u32(sKV + s * A::STAGE);
 #pragma unroll
           for (int k = 0; k < A::K16; ++k) {
-            const uint32_t off = (k >> 2) * (A::BQ * 128) + (k & 3) * 32;
-            umma_bf16(tmem + sb * 128, make_sdesc_sw128(aq + off), make_sdesc_sw128(ak + off), id_s, k > 0);
+            if (A::T64 && k >= 4 * A::KQ) {  // the 32-column SW64 tail: 64-byte rows, k-steps 32 bytes apart
+              const uint32_t off = A::KQ * (A::BQ * 128) + (k - 4 * A::KQ) * 32;
+              umma_bf16(tmem + sb * 128, make_sdesc_sw64(aq + off), make_sdesc_sw64(ak + off), id_s, 1);
+            } else {
+              const uint32_t off = (k >> 2) * (A::BQ * 128) + (k & 3) * 32;
+              umma_bf16(tmem + sb * 128, make_sdesc_sw128(aq + off), make_sdesc_sw128(ak + off), id_s, k > 0);
+            }
           }
           umma_commit(&s_full[sb]);
         }
@@ -239,7 +285,6 @@ __global__ void __launch_bounds__(64 + 128 * SPLIT, 3 - NB)
       mbar_wait_sleep(&s_full[sb], (j / NB) & 1);
       tc_fence_after();
       const uint32_t sbase = tmem + lane_base + sb * 128 + h * CPT;
-      // Lk is a multiple of 128 (attention_tc_supported): no key block is ragged
       uint32_t ta[32], tb[32];
       if constexpr (OP >= 1 && OP <= 4) {
         static_assert(SPLIT == 2, "one-pass softmax needs 64 columns per thread");  // OP ≥ 1
@@ -250,6 +295,16 @@ __global__ void __launch_bounds__(64 + 128 * SPLIT, 3 - NB)
         tc_fence_before();  // the scores are in registers: S buffer free for S_{j+1}
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_empty[sb]);
+        if (j == nb - 1 && (Lk & (A::BK - 1))) {
+          // ragged last key block (cross-attention: 77 text tokens; the 8×8 mid block: 64 tokens):
+          // keys ≥ Lk get −∞ (P = 0; their K / Vᵀ rows are finite memory beyond the valid keys)
+          const int valid = Lk - j * A::BK - h * 64;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            if (i >= valid) ta[i] = __float_as_uint(-INFINITY);
+            if (32 + i >= valid) tb[i] = __float_as_uint(-INFINITY);
+          }
+        }
         float mx4[4] = {-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX};
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
@@ -273,7 +328,7 @@ __global__ void __launch_bounds__(64 + 128 * SPLIT, 3 - NB)
           const float p0 = emu ? ex2_poly(x0) : ex2(x0);
           const float p1 = emu ? ex2_poly(x1) : ex2(x1);
           sum8[i & 7] += p0 + p1;
-          ta[i] = pack_bf16(p0, p1);
+          ta[i] = pack16(p0, p1, is_f16);
         }
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
@@ -283,7 +338,7 @@ __global__ void __launch_bounds__(64 + 128 * SPLIT, 3 - NB)
           const float p0 = emu ? ex2_poly(x0) : ex2(x0);
           const float p1 = emu ? ex2_poly(x1) : ex2(x1);
           sum8[i & 7] += p0 + p1;
-          tb[i] = pack_bf16(p0, p1);
+          tb[i] = pack16(p0, p1, is_f16);
         }
         const float sum = ((sum8[0] + sum8[1]) + (sum8[2] + sum8[3])) + ((sum8[4] + sum8[5]) + (sum8[6] + sum8[7]));
         l = l * alpha + sum;
@@ -387,7 +442,7 @@ __global__ void __launch_bounds__(64 + 128 * SPLIT, 3 - NB)
             p1 = ex2(x1);
           }
           sum8[i & 7] += p0 + p1;
-          pk[c * 16 + i] = pack_bf16(p0, p1);
+          pk[c * 16 + i] = pack16(p0, p1, is_f16);
         }
         if (DBUF && c < NCH - 1) tmem_wait_ld_tied(nxt);
       }
@@ -461,10 +516,10 @@ __global__ void __launch_bounds__(64 + 128 * SPLIT, 3 - NB)
           const int col = c * 16 + i;
           if (col + 8 <= D)
             *reinterpret_cast<uint4*>(orow + col) =
-                make_uint4(pack_bf16(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv),
-                           pack_bf16(__uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv),
-                           pack_bf16(__uint_as_float(o[i + 4]) * inv, __uint_as_float(o[i + 5]) * inv),
-                           pack_bf16(__uint_as_float(o[i + 6]) * inv, __uint_as_float(o[i + 7]) * inv));
+                make_uint4(pack16(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv, is_f16),
+                           pack16(__uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv, is_f16),
+                           pack16(__uint_as_float(o[i + 4]) * inv, __uint_as_float(o[i + 5]) * inv, is_f16),
+                           pack16(__uint_as_float(o[i + 6]) * inv, __uint_as_float(o[i + 7]) * inv, is_f16));
         }
       }
     }
@@ -477,24 +532,61 @@ __global__ void __launch_bounds__(64 + 128 * SPLIT, 3 - NB)
 
 // host ------------------------------------------------------------------------------------------
 void make_tmap_2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_bytes, uint32_t box_in,
-                  uint32_t box_out);
+                  uint32_t box_out, bool is_f16, bool swz64 = false);
+
+// the three operand tensors of one launch (host side)
+struct TcSrc {
+  const void* q;
+  long q_rows;
+  int ldq;
+  const void* k;
+  long k_rows;
+  int ldk;
+  const void* vt;
+  long vt_rows, ld_keys;
+  int qcol0, kcol0, vrow0, Lk;
+  const int* kv_index;
+};
 
 template <int D, int NB, int SPLIT, int EMU = 0, int OP = 0>
-static void launch_tc(const bf16* qk, const bf16* vt, bf16* O, int rows, int heads, int C, int P, cudaStream_t st) {
+static void launch_tc(const TcSrc& sr, bf16* O, int ldo, int rows, int heads, int P, cudaStream_t st, bool f16) {
   using A = TcAttn<D, NB, SPLIT, EMU, (OP == 4 || OP == 5) ? 1 : 0>;
   static bool set = false;
   if (!set) {
-    SD_CUDA(cudaFuncSetAttribute(attn_tc_kernel<D, NB, SPLIT, EMU, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 A::SMEM));
+    SD_CUDA(cudaFuncSetAttribute(attn_tc_kernel<D, NB, SPLIT, EMU, OP, false>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, A::SMEM));
+    SD_CUDA(cudaFuncSetAttribute(attn_tc_kernel<D, NB, SPLIT, EMU, OP, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, A::SMEM));
     set = true;
   }
-  const long T = (long)rows * P;
-  CUtensorMap mqk, mvt;
-  make_tmap_2d(&mqk, qk, (uint64_t)2 * C, (uint64_t)T, (uint64_t)2 * C * 2, 64, 128);
-  make_tmap_2d(&mvt, vt, (uint64_t)T, (uint64_t)C, (uint64_t)T * 2, 64, A::NPV);
+  CUtensorMap mq, mk, mvt;
+  make_tmap_2d(&mq, sr.q, (uint64_t)sr.ldq, (uint64_t)sr.q_rows, (uint64_t)sr.ldq * 2, 64, 128, f16);
+  if (sr.k == sr.q && sr.ldk == sr.ldq && sr.k_rows == sr.q_rows)
+    mk = mq;
+  else
+    make_tmap_2d(&mk, sr.k, (uint64_t)sr.ldk, (uint64_t)sr.k_rows, (uint64_t)sr.ldk * 2, 64, 128, f16);
+  make_tmap_2d(&mvt, sr.vt, (uint64_t)sr.ld_keys, (uint64_t)sr.vt_rows, (uint64_t)sr.ld_keys * 2, 64, A::NPV, f16);
+  CUtensorMap mq_t = mq, mk_t = mk;  // d = 160: 32-column SW64 tail boxes of Q and K
+  if (A::T64) {
+    make_tmap_2d(&mq_t, sr.q, (uint64_t)sr.ldq, (uint64_t)sr.q_rows, (uint64_t)sr.ldq * 2, 32, 128, f16, true);
+    make_tmap_2d(&mk_t, sr.k, (uint64_t)sr.ldk, (uint64_t)sr.k_rows, (uint64_t)sr.ldk * 2, 32, 128, f16, true);
+  }
   dim3 grid(cdiv(P, A::BQ), heads, rows);
-  const float scale_log2 = 1.4426950408889634f / sqrtf((float)D);
-  attn_tc_kernel<D, NB, SPLIT, EMU, OP><<<grid, A::THREADS, A::SMEM, st>>>(mqk, mvt, O, C, C, P, P, scale_log2);
+  AttnTcArgs a;
+  a.O = O;
+  a.ldo = ldo;
+  a.P = P;
+  a.Lk = sr.Lk;
+  a.scale_log2 = 1.4426950408889634f / sqrtf((float)D);
+  a.qcol0 = sr.qcol0;
+  a.kcol0 = sr.kcol0;
+  a.vrow0 = sr.vrow0;
+  a.kv_index = sr.kv_index;
+  a.vt_slot = (sr.Lk + 7) / 8 * 8;
+  if (f16)
+    launch_k(attn_tc_kernel<D, NB, SPLIT, EMU, OP, true>, grid, A::THREADS, A::SMEM, st, mq, mk, mvt, mq_t, mk_t, a);
+  else
+    launch_k(attn_tc_kernel<D, NB, SPLIT, EMU, OP, false>, grid, A::THREADS, A::SMEM, st, mq, mk, mvt, mq_t, mk_t, a);
   SD_CHECK_LAUNCH();
 }
 
@@ -537,55 +629,127 @@ static int attn_nb() {
   return v;
 }
 
+static bool env_on(const char* name) {
+  const char* e = getenv(name);
+  return !(e && e[0] == '0');
+}
+
 bool attention_tc_supported(int d, int P, int C) {
-  return (d == 40 || d == 64 || d == 80) && P % 128 == 0 && C % 8 == 0;
+  static const bool d160 = env_on("SD_ATTN160_TC");  // SD_ATTN160_TC=0: d = 160 on the mma.sync kernel
+  if (d == 160 && !d160) return false;
+  // ragged key blocks (P % 128 != 0) are masked by the default OP-4 softmax only
+  // self-attention Vᵀ key columns start at row·P: 16-byte aligned needs P % 8 == 0
+  return (d == 40 || d == 64 || d == 80 || d == 160) && (P % 128 == 0 || (attn_emu() == 8 && P % 8 == 0)) &&
+         C % 8 == 0;
 }
 
 // qk: [rows·P][2C] (q | k), vt: [C][rows·P] (Vᵀ), O: [rows·P][C]
-void attention_tc(const bf16* qk, const bf16* vt, bf16* O, int rows, int heads, int d, int C, int P,
-                  cudaStream_t st) {
+static void attention_tc16(const TcSrc& sr, bf16* O, int ldo, int rows, int heads, int d, int P, cudaStream_t st,
+                           bool f16) {
+  if (sr.Lk % 128 && attn_emu() != 8) throw CudaError("attention_tc: ragged keys need the default (OP 4) variant");
   switch (d) {
     case 40:
       switch (attn_nb() * 100 + attn_split() * 10 + attn_emu()) {
-        case 110: launch_tc<40, 1, 1, 0>(qk, vt, O, rows, heads, C, P, st); break;
-        case 114: launch_tc<40, 1, 1, 4>(qk, vt, O, rows, heads, C, P, st); break;
-        case 124: launch_tc<40, 1, 2, 4>(qk, vt, O, rows, heads, C, P, st); break;
-        case 210: launch_tc<40, 2, 1, 0>(qk, vt, O, rows, heads, C, P, st); break;
-        case 220: launch_tc<40, 2, 2, 0>(qk, vt, O, rows, heads, C, P, st); break;
-        case 224: launch_tc<40, 2, 2, 4>(qk, vt, O, rows, heads, C, P, st); break;
-        case 125: launch_tc<40, 1, 2, 0, 1>(qk, vt, O, rows, heads, C, P, st); break;  // SD_ATTN_EMU=5: one-pass
-        case 225: launch_tc<40, 2, 2, 0, 1>(qk, vt, O, rows, heads, C, P, st); break;
-        case 126: launch_tc<40, 1, 2, 0, 2>(qk, vt, O, rows, heads, C, P, st); break;
-        case 127: launch_tc<40, 1, 2, 0, 3>(qk, vt, O, rows, heads, C, P, st); break;
-        case 128: launch_tc<40, 1, 2, 0, 4>(qk, vt, O, rows, heads, C, P, st); break;  // SD_ATTN_EMU=8: P in TMEM
-        default: launch_tc<40, 1, 2, 0>(qk, vt, O, rows, heads, C, P, st); break;
+        case 110: launch_tc<40, 1, 1, 0>(sr, O, ldo, rows, heads, P, st, f16); break;
+        case 114: launch_tc<40, 1, 1, 4>(sr, O, ldo, rows, heads, P, st, f16); break;
+        case 124: launch_tc<40, 1, 2, 4>(sr, O, ldo, rows, heads, P, st, f16); break;
+        case 210: launch_tc<40, 2, 1, 0>(sr, O, ldo, rows, heads, P, st, f16); break;
+        case 220: launch_tc<40, 2, 2, 0>(sr, O, ldo, rows, heads, P, st, f16); break;
+        case 224: launch_tc<40, 2, 2, 4>(sr, O, ldo, rows, heads, P, st, f16); break;
+        case 125: launch_tc<40, 1, 2, 0, 1>(sr, O, ldo, rows, heads, P, st, f16); break;  // SD_ATTN_EMU=5: one-pass
+        case 225: launch_tc<40, 2, 2, 0, 1>(sr, O, ldo, rows, heads, P, st, f16); break;
+        case 126: launch_tc<40, 1, 2, 0, 2>(sr, O, ldo, rows, heads, P, st, f16); break;
+        case 127: launch_tc<40, 1, 2, 0, 3>(sr, O, ldo, rows, heads, P, st, f16); break;
+        case 128: launch_tc<40, 1, 2, 0, 4>(sr, O, ldo, rows, heads, P, st, f16); break;  // SD_ATTN_EMU=8: P in TMEM
+        default: launch_tc<40, 1, 2, 0>(sr, O, ldo, rows, heads, P, st, f16); break;
       }
       break;
     case 64:  // SD_ATTN_EMU=8 (default): the d = 40 structure — two CTAs per SM, two softmax threads per
               // row, one TMEM pass, P in TMEM (S 128 | O 64 | P 64 columns): SDXL [16,10,64,4096] 1.27 → 1.16
               // ms vs NB = 2 / one thread per row (which was 1.18× faster than NB = 1 with P in smem)
       if (attn_emu() == 8)
-        launch_tc<64, 1, 2, 0, 4>(qk, vt, O, rows, heads, C, P, st);
+        launch_tc<64, 1, 2, 0, 4>(sr, O, ldo, rows, heads, P, st, f16);
       else if (attn_emu() == 5)
-        launch_tc<64, 2, 1, 0, 5>(qk, vt, O, rows, heads, C, P, st);
+        launch_tc<64, 2, 1, 0, 5>(sr, O, ldo, rows, heads, P, st, f16);
       else if (attn_emu() != 4)
-        launch_tc<64, 2, 1, 0>(qk, vt, O, rows, heads, C, P, st);
+        launch_tc<64, 2, 1, 0>(sr, O, ldo, rows, heads, P, st, f16);
       else
-        launch_tc<64, 2, 1, 4>(qk, vt, O, rows, heads, C, P, st);
+        launch_tc<64, 2, 1, 4>(sr, O, ldo, rows, heads, P, st, f16);
       break;
     case 80:  // SD_ATTN_EMU=8 (default): two softmax threads per row, one TMEM pass, P in TMEM; S | O | P
               // need 272 columns, so one CTA per SM (512 allocated): [16,8,80,1024] 87.9 → 83.1 µs
       if (attn_emu() == 8)
-        launch_tc<80, 1, 2, 0, 4>(qk, vt, O, rows, heads, C, P, st);
+        launch_tc<80, 1, 2, 0, 4>(sr, O, ldo, rows, heads, P, st, f16);
       else if (attn_emu() == 5)
-        launch_tc<80, 2, 1, 0, 5>(qk, vt, O, rows, heads, C, P, st);
+        launch_tc<80, 2, 1, 0, 5>(sr, O, ldo, rows, heads, P, st, f16);
       else if (attn_emu() != 4)
-        launch_tc<80, 2, 1, 0>(qk, vt, O, rows, heads, C, P, st);
+        launch_tc<80, 2, 1, 0>(sr, O, ldo, rows, heads, P, st, f16);
       else
-        launch_tc<80, 2, 1, 4>(qk, vt, O, rows, heads, C, P, st);
+        launch_tc<80, 2, 1, 4>(sr, O, ldo, rows, heads, P, st, f16);
+      break;
+    case 160:  // SD-1.5 16×16 and the 8×8 mid block: S | O (160) | P in 512 columns, one K/V stage
+      launch_tc<160, 1, 2, 0, 4>(sr, O, ldo, rows, heads, P, st, f16);
       break;
     default: throw CudaError("attention_tc: unsupported head dim");
   }
+}
+
+static TcSrc self_src(const void* qk, const void* vt, int rows, int C, int P) {
+  const long T = (long)rows * P;
+  TcSrc sr{};
+  sr.q = sr.k = qk;
+  sr.q_rows = sr.k_rows = T;
+  sr.ldq = sr.ldk = 2 * C;
+  sr.vt = vt;
+  sr.vt_rows = C;
+  sr.ld_keys = T;
+  sr.qcol0 = 0;
+  sr.kcol0 = C;
+  sr.vrow0 = 0;
+  sr.Lk = P;
+  sr.kv_index = nullptr;
+  return sr;
+}
+void attention_tc(const bf16* qk, const bf16* vt, bf16* O, int rows, int heads, int d, int C, int P, cudaStream_t st) {
+  attention_tc16(self_src(qk, vt, rows, C, P), O, C, rows, heads, d, P, st, false);
+}
+void attention_tc(const f16* qk, const f16* vt, f16* O, int rows, int heads, int d, int C, int P, cudaStream_t st) {
+  attention_tc16(self_src(qk, vt, rows, C, P), reinterpret_cast<bf16*>(O), C, rows, heads, d, P, st, true);
+}
+
+// cross-attention over the cached text tokens (K7): Q [rows·P][C]; kcache [n_slots·Lk][ldk] with this
+// layer's K at column kcol; vtcache [vt_rows][ld_keys] with this layer's Vᵀ at row vrow (key j of slot s
+// at column s·⌈Lk⌉₈ + j); kv_index [rows] = slot per batch row (device)
+template <class T>
+static void xattn_tc_impl(const T* q, const T* kcache, int ldk, long n_slots, int kcol, const T* vtcache,
+                          long vt_rows, long ld_keys, int vrow, const int* kv_index, int Lk, T* O, int rows, int heads,
+                          int d, int C, int P, cudaStream_t st) {
+  TcSrc sr{};
+  sr.q = q;
+  sr.q_rows = (long)rows * P;
+  sr.ldq = C;
+  sr.k = kcache;
+  sr.k_rows = n_slots * Lk;
+  sr.ldk = ldk;
+  sr.vt = vtcache;
+  sr.vt_rows = vt_rows;
+  sr.ld_keys = ld_keys;
+  sr.qcol0 = 0;
+  sr.kcol0 = kcol;
+  sr.vrow0 = vrow;
+  sr.Lk = Lk;
+  sr.kv_index = kv_index;
+  attention_tc16(sr, reinterpret_cast<bf16*>(O), C, rows, heads, d, P, st, std::is_same<T, f16>::value);
+}
+void xattention_tc(const bf16* q, const bf16* kc, int ldk, long n_slots, int kcol, const bf16* vtc, long vt_rows,
+                   long ld_keys, int vrow, const int* kv_index, int Lk, bf16* O, int rows, int heads, int d, int C, int P,
+                   cudaStream_t st) {
+  xattn_tc_impl(q, kc, ldk, n_slots, kcol, vtc, vt_rows, ld_keys, vrow, kv_index, Lk, O, rows, heads, d, C, P, st);
+}
+void xattention_tc(const f16* q, const f16* kc, int ldk, long n_slots, int kcol, const f16* vtc, long vt_rows,
+                   long ld_keys, int vrow, const int* kv_index, int Lk, f16* O, int rows, int heads, int d, int C, int P,
+                   cudaStream_t st) {
+  xattn_tc_impl(q, kc, ldk, n_slots, kcol, vtc, vt_rows, ld_keys, vrow, kv_index, Lk, O, rows, heads, d, C, P, st);
 }
 
 }  // namespace sd

@@ -4,14 +4,17 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <stdint.h>
 #include <stdio.h>
 
 #include <atomic>
+#include <utility>
 #include <stdexcept>
 #include <string>
 
 typedef __nv_bfloat16 bf16;
+typedef __half f16;  // SD_PREC_FP16: the same kernels with fp16 operands / storage (R19a)
 
 namespace sd {
 
@@ -37,6 +40,27 @@ extern std::atomic<long long> g_launches;
   } while (0)
 
 static inline int cdiv(long a, long b) { return (int)((a + b - 1) / b); }
+
+// Programmatic dependent launch (PDL): every kernel of the library is launched with programmatic stream
+// serialization and starts with pdl_wait() (griddepcontrol.wait) before touching global memory, so the
+// next grid is scheduled — and runs its prologue (barrier init, TMEM alloc, tensor-map prefetch) — while
+// the previous grid drains, instead of after it; memory semantics are those of plain stream order.
+// SD_PDL=0 launches without the attribute (pdl_wait is then a no-op).
+extern int g_pdl;
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = g_pdl ? 1 : 0;
+  SD_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
 
 #if defined(__CUDACC__)
 
@@ -146,6 +170,10 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 __host__ __device__ constexpr uint32_t make_idesc_bf16(int M, int N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
+// the same with A = B = fp16 (format code 0) when is_f16
+__host__ __device__ constexpr uint32_t make_idesc16(int M, int N, bool is_f16) {
+  return make_idesc_bf16(M, N) & ~(is_f16 ? ((7u << 7) | (7u << 10)) : 0u);
+}
 
 // Shared-memory matrix descriptor (sm_100 "version 1"), K-major, SWIZZLE_128B:
 // start>>4 [0,14), LBO>>4 [16,30) (unused for swizzled K-major: 1), SBO>>4 [32,46) = 1024 B
@@ -153,6 +181,12 @@ __host__ __device__ constexpr uint32_t make_idesc_bf16(int M, int N) {
 __device__ __forceinline__ uint64_t make_sdesc_sw128(uint32_t smem_addr) {
   return (uint64_t)((smem_addr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+// The same for SWIZZLE_64B tiles (64-byte rows, 8-row groups 512 B apart; layout type 4)
+__device__ __forceinline__ uint64_t make_sdesc_sw64(uint32_t smem_addr) {
+  return (uint64_t)((smem_addr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(512 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
 }
 
 // 32 lanes x 32 consecutive 32-bit columns → 32 registers per thread (thread i ↔ lane base+i).
@@ -193,6 +227,9 @@ __device__ __forceinline__ void tmem_wait_ld_tied(uint32_t (&r)[32]) {
                : "memory");
 }
 
+// PDL: wait until the preceding grid in the stream has completed and its writes are visible
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // make generic-proxy shared-memory writes visible to the async proxy (TMA / tensor core)
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -226,10 +263,28 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-// activation element type T ∈ {bf16 (product path), float (fp32 parity mode, R19)}: scalar and
-// 8-element (16 / 32-byte) vector conversions
+__device__ __forceinline__ uint32_t pack_f16(float a, float b) {
+  __half2 v = __floats2half2_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+// 16-bit storage chosen at run time (kernels shared by the bf16 and fp16 paths; is_f16 is uniform)
+__device__ __forceinline__ uint32_t pack16(float a, float b, bool is_f16) {
+  return is_f16 ? pack_f16(a, b) : pack_bf16(a, b);
+}
+__device__ __forceinline__ float cvt16(bf16 v, bool is_f16) {
+  const unsigned short u = __bfloat16_as_ushort(v);
+  return is_f16 ? __half2float(__ushort_as_half(u)) : __bfloat162float(v);
+}
+__device__ __forceinline__ bf16 to16(float v, bool is_f16) {
+  return is_f16 ? __ushort_as_bfloat16(__half_as_ushort(__float2half_rn(v))) : __float2bfloat16(v);
+}
+
+// activation element type T ∈ {bf16 (product path), f16 (SD_PREC_FP16), float (fp32 parity mode,
+// R19)}: scalar and 8-element (16 / 32-byte) vector conversions
 __device__ __forceinline__ float act_ld(const bf16* p) { return __bfloat162float(*p); }
 __device__ __forceinline__ float act_ld(const float* p) { return *p; }
+__device__ __forceinline__ float act_ld(const f16* p) { return __half2float(*p); }
+__device__ __forceinline__ void act_st(f16* p, float v) { *p = __float2half_rn(v); }
 __device__ __forceinline__ void act_st(bf16* p, float v) { *p = __float2bfloat16(v); }
 __device__ __forceinline__ void act_st(float* p, float v) { *p = v; }
 __device__ __forceinline__ void load8(const bf16* p, float (&f)[8]) {
@@ -237,6 +292,16 @@ __device__ __forceinline__ void load8(const bf16* p, float (&f)[8]) {
   const bf16* e = reinterpret_cast<const bf16*>(&u);
 #pragma unroll
   for (int i = 0; i < 8; ++i) f[i] = __bfloat162float(e[i]);
+}
+__device__ __forceinline__ void load8(const f16* p, float (&f)[8]) {
+  const uint4 u = *reinterpret_cast<const uint4*>(p);
+  const f16* e = reinterpret_cast<const f16*>(&u);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) f[i] = __half2float(e[i]);
+}
+__device__ __forceinline__ void store8(f16* p, const float (&o)[8]) {
+  *reinterpret_cast<uint4*>(p) =
+      make_uint4(pack_f16(o[0], o[1]), pack_f16(o[2], o[3]), pack_f16(o[4], o[5]), pack_f16(o[6], o[7]));
 }
 __device__ __forceinline__ void load8(const float* p, float (&f)[8]) {
   const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];

@@ -13,6 +13,7 @@ namespace sd {
 // cpad-channel row is zero; 16/32-byte stores
 template <class T>
 __global__ void gather_rows_kernel(RowMap m, int rows, int hw, int nv, T* __restrict__ out) {
+  pdl_wait();
   const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;  // (pixel of a row, vector)
   if (i >= (long)rows * hw * nv) return;
   const long px = i / nv;
@@ -33,7 +34,7 @@ template <class T>
 void gather_rows(const RowMap& m, int rows, int hw, int cpad, T* out, cudaStream_t st) {
   if (cpad % 8) throw CudaError("gather_rows: cpad must be a multiple of 8");
   const long n = (long)rows * hw * (cpad / 8);
-  gather_rows_kernel<T><<<cdiv(n, 256), 256, 0, st>>>(m, rows, hw, cpad / 8, out);
+  launch_k(gather_rows_kernel<T>, cdiv(n, 256), 256, 0, st, m, rows, hw, cpad / 8, out);
   SD_CHECK_LAUNCH();
 }
 
@@ -43,6 +44,7 @@ void gather_rows(const RowMap& m, int rows, int hw, int cpad, T* out, cudaStream
 // the cond row of request r is row r (R26).
 __global__ void combine_update_kernel(RowMap m, int n_req, int hw, const float* __restrict__ eps, int ld,
                                       float* const* lat) {
+  pdl_wait();
   const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (long)n_req * hw) return;
   const int r = (int)(i / hw), p = (int)(i % hw);
@@ -63,13 +65,14 @@ __global__ void combine_update_kernel(RowMap m, int n_req, int hw, const float* 
 void combine_update(const RowMap& m, int n_req, int hw, const float* eps, int ld_eps, float* const* lat,
                     cudaStream_t st) {
   const long n = (long)n_req * hw;
-  combine_update_kernel<<<cdiv(n, 256), 256, 0, st>>>(m, n_req, hw, eps, ld_eps, lat);
+  launch_k(combine_update_kernel, cdiv(n, 256), 256, 0, st, m, n_req, hw, eps, ld_eps, lat);
   SD_CHECK_LAUNCH();
 }
 
 // K10 front: [cos(t·f_k) ‖ sin(t·f_k)], f_k = exp(−ln(10⁴)·k/half) (flip_sin_to_cos, R27).
 template <class T>
 __global__ void sinusoid_kernel(const float* __restrict__ t, int rows, int dim, T* __restrict__ out) {
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int half = dim / 2;
   if (i >= rows * half) return;
@@ -82,12 +85,13 @@ __global__ void sinusoid_kernel(const float* __restrict__ t, int rows, int dim, 
 
 template <class T>
 void timestep_sinusoid(const float* t_row, int rows, int dim, T* out, cudaStream_t st) {
-  sinusoid_kernel<T><<<cdiv(rows * dim / 2, 256), 256, 0, st>>>(t_row, rows, dim, out);
+  launch_k(sinusoid_kernel<T>, cdiv(rows * dim / 2, 256), 256, 0, st, t_row, rows, dim, out);
   SD_CHECK_LAUNCH();
 }
 
 // nearest 2× upsample, NHWC, 16-byte vectors
 __global__ void upsample2x_kernel(const uint4* __restrict__ x, uint4* __restrict__ y, int B, int H, int W, int V) {
+  pdl_wait();
   const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
   const long n = (long)B * 2 * H * 2 * W * V;
   if (i >= n) return;
@@ -104,13 +108,14 @@ template <class T>
 void upsample2x(const T* x, T* y, int B, int H, int W, int C, cudaStream_t st) {
   const int V = C * (int)sizeof(T) / 16;
   const long n = (long)B * 4 * H * W * V;
-  upsample2x_kernel<<<cdiv(n, 256), 256, 0, st>>>(reinterpret_cast<const uint4*>(x), reinterpret_cast<uint4*>(y), B,
+  launch_k(upsample2x_kernel, cdiv(n, 256), 256, 0, st, reinterpret_cast<const uint4*>(x), reinterpret_cast<uint4*>(y), B,
                                                   H, W, V);
   SD_CHECK_LAUNCH();
 }
 
 // im2col for 3×3 / stride 2 / pad 1: y[(b,yo,xo)][tap·C + c] (tap-major, matches weights [N][9][C])
 __global__ void im2col_s2_kernel(const uint4* __restrict__ x, uint4* __restrict__ y, int B, int H, int W, int V) {
+  pdl_wait();
   const int Ho = (H + 1) / 2, Wo = (W + 1) / 2;
   const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
   const long n = (long)B * Ho * Wo * 9 * V;
@@ -133,13 +138,14 @@ template <class T>
 void im2col_s2(const T* x, T* y, int B, int H, int W, int C, cudaStream_t st) {
   const int V = C * (int)sizeof(T) / 16;
   const long n = (long)B * ((H + 1) / 2) * ((W + 1) / 2) * 9 * V;
-  im2col_s2_kernel<<<cdiv(n, 256), 256, 0, st>>>(reinterpret_cast<const uint4*>(x), reinterpret_cast<uint4*>(y), B,
+  launch_k(im2col_s2_kernel, cdiv(n, 256), 256, 0, st, reinterpret_cast<const uint4*>(x), reinterpret_cast<uint4*>(y), B,
                                                  H, W, V);
   SD_CHECK_LAUNCH();
 }
 
 __global__ void concat_kernel(const uint4* __restrict__ a, int va, const uint4* __restrict__ b, int vb,
                               uint4* __restrict__ y, long P) {
+  pdl_wait();
   const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
   const int V = va + vb;
   if (i >= P * V) return;
@@ -152,19 +158,31 @@ template <class T>
 void concat_channels(const T* a, int ca, const T* b, int cb, T* y, long P, cudaStream_t st) {
   const int per = 16 / (int)sizeof(T);  // elements per 16-byte vector
   const long n = P * (ca + cb) / per;
-  concat_kernel<<<cdiv(n, 256), 256, 0, st>>>(reinterpret_cast<const uint4*>(a), ca / per,
+  launch_k(concat_kernel, cdiv(n, 256), 256, 0, st, reinterpret_cast<const uint4*>(a), ca / per,
                                               reinterpret_cast<const uint4*>(b), cb / per, reinterpret_cast<uint4*>(y),
                                               P);
   SD_CHECK_LAUNCH();
 }
 
 __global__ void f32_to_bf16_kernel(const float* __restrict__ x, bf16* __restrict__ y, long n) {
+  pdl_wait();
   const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) y[i] = __float2bfloat16(x[i]);
 }
 
 void f32_to_bf16(const float* x, bf16* y, long n, cudaStream_t st) {
-  f32_to_bf16_kernel<<<cdiv(n, 256), 256, 0, st>>>(x, y, n);
+  launch_k(f32_to_bf16_kernel, cdiv(n, 256), 256, 0, st, x, y, n);
+  SD_CHECK_LAUNCH();
+}
+
+__global__ void f32_to_f16_kernel(const float* __restrict__ x, f16* __restrict__ y, long n) {
+  pdl_wait();
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = __float2half_rn(x[i]);
+}
+
+void f32_to_act(const float* x, f16* y, long n, cudaStream_t st) {
+  launch_k(f32_to_f16_kernel, cdiv(n, 256), 256, 0, st, x, y, n);
   SD_CHECK_LAUNCH();
 }
 
@@ -175,18 +193,20 @@ void f32_to_act(const float* x, float* y, long n, cudaStream_t st) {
 // dst[r][0..n) = src[idx[r]][0..n) (fp32): the SDXL added embedding of each row's prompt slot
 __global__ void gather_rows_f32_kernel(const float* __restrict__ src, const int* __restrict__ idx, int n,
                                        float* __restrict__ dst) {
+  pdl_wait();
   const int r = blockIdx.y;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) dst[(long)r * n + i] = src[(long)idx[r] * n + i];
 }
 
 void gather_rows_f32(const float* src, const int* idx, int rows, int n, float* dst, cudaStream_t st) {
-  gather_rows_f32_kernel<<<dim3(cdiv(n, 256), rows), 256, 0, st>>>(src, idx, n, dst);
+  launch_k(gather_rows_f32_kernel, dim3(cdiv(n, 256), rows), 256, 0, st, src, idx, n, dst);
   SD_CHECK_LAUNCH();
 }
 
 template <class T>
 __global__ void latent_to_nhwc_kernel(const float* __restrict__ z, int hw, float scale, int cpad, T* __restrict__ out) {
+  pdl_wait();
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= hw) return;
   T* o = out + (long)p * cpad;
@@ -195,11 +215,12 @@ __global__ void latent_to_nhwc_kernel(const float* __restrict__ z, int hw, float
 
 template <class T>
 void latent_to_nhwc(const float* z, int hw, float scale, int cpad, T* out, cudaStream_t st) {
-  latent_to_nhwc_kernel<T><<<cdiv(hw, 256), 256, 0, st>>>(z, hw, scale, cpad, out);
+  launch_k(latent_to_nhwc_kernel<T>, cdiv(hw, 256), 256, 0, st, z, hw, scale, cpad, out);
   SD_CHECK_LAUNCH();
 }
 
 __global__ void nhwc_to_nchw3_kernel(const float* __restrict__ x, int ld, long P, float* __restrict__ y) {
+  pdl_wait();
   const long p = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= P) return;
 #pragma unroll
@@ -207,7 +228,7 @@ __global__ void nhwc_to_nchw3_kernel(const float* __restrict__ x, int ld, long P
 }
 
 void nhwc_to_nchw3(const float* x, int ld, long P, float* y, cudaStream_t st) {
-  nhwc_to_nchw3_kernel<<<cdiv(P, 256), 256, 0, st>>>(x, ld, P, y);
+  launch_k(nhwc_to_nchw3_kernel, cdiv(P, 256), 256, 0, st, x, ld, P, y);
   SD_CHECK_LAUNCH();
 }
 
@@ -219,6 +240,7 @@ void nhwc_to_nchw3(const float* x, int ld, long P, float* y, cudaStream_t st) {
   template void concat_channels<T>(const T*, int, const T*, int, T*, long, cudaStream_t);         \
   template void latent_to_nhwc<T>(const float*, int, float, int, T*, cudaStream_t);
 SD_EW_INST(bf16)
+SD_EW_INST(f16)
 SD_EW_INST(float)
 
 }  // namespace sd

@@ -142,7 +142,7 @@ struct Builder {
     w.F = F;
     w.dst0 = d0;
     w.dst1 = d1;
-    w.out_bf16 = bf ? 1 : 0;
+    w.out_bf16 = bf ? (e->f16 ? 2 : 1) : 0;
     w.src = nullptr;
     init_weight(w, st);
     e->wreg[name] = w;
@@ -379,6 +379,7 @@ Engine::~Engine() {
   warena.release();
   ws.release();
   if (kv_cache) cudaFree(kv_cache);
+  if (vt_cache) cudaFree(vt_cache);
   if (aug_cache) cudaFree(aug_cache);
   if (reg_scratch) cudaFree(reg_scratch);
   if (gn_ws) cudaFree(gn_ws);
@@ -440,6 +441,7 @@ void build_engine(Engine* e) {
   e->vc = vae_cfg(e->cfg.model);
   e->max_rows = 2 * e->cfg.b_max;
   e->f32 = e->cfg.precision == SD_PREC_FP32;
+  e->f16 = e->cfg.precision == SD_PREC_FP16;
   e->esize = e->f32 ? 4 : 2;
   const size_t wbytes = (e->cfg.model == SD_MODEL_SD15   ? ((size_t)2200 << 20)
                          : e->cfg.model == SD_MODEL_SDXL ? ((size_t)5600 << 20)
@@ -463,6 +465,11 @@ void build_engine(Engine* e) {
   e->slot_elems = (long)e->uc.ctx_len * e->U.kv_width;
   SD_CUDA(cudaMalloc(&e->kv_cache, (size_t)e->max_slots * e->slot_elems * e->esize));
   SD_CUDA(cudaMemset(e->kv_cache, 0, (size_t)e->max_slots * e->slot_elems * e->esize));
+  if (!e->f32) {  // finite everywhere: the cross-attention reads (and masks) keys beyond a slot's 77
+    e->vt_ld = (long)e->max_slots * ((e->uc.ctx_len + 7) / 8 * 8);  // slot stride ⌈77⌉₈ = 80 keys
+    SD_CUDA(cudaMalloc(&e->vt_cache, (size_t)e->U.kv_width * e->vt_ld * e->esize));
+    SD_CUDA(cudaMemset(e->vt_cache, 0, (size_t)e->U.kv_width * e->vt_ld * e->esize));
+  }
   if (e->uc.add_time_dim) {
     SD_CUDA(cudaMalloc(&e->aug_cache, (size_t)e->max_slots * e->uc.temb_dim() * sizeof(float)));
     SD_CUDA(cudaMemset(e->aug_cache, 0, (size_t)e->max_slots * e->uc.temb_dim() * sizeof(float)));
@@ -490,6 +497,8 @@ void build_engine(Engine* e) {
   e->use_graphs = !(ng && ng[0] == '1');
   const char* at = getenv("SD_ATTN_TC");
   e->use_attn_tc = !(at && at[0] == '0') && !e->f32;
+  const char* xt = getenv("SD_XATTN_TC");  // SD_XATTN_TC=0: cross-attention on the mma.sync kernel
+  e->use_xattn_tc = e->use_attn_tc && !(xt && xt[0] == '0');
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -551,6 +560,22 @@ static void ctx_kv(Engine* e, const float* emb, int len, int dim, const float* p
   d.out = static_cast<AT*>(e->kv_cache) + (long)slot * e->slot_elems;
   d.ldo = e->U.kv_width;
   gemm(d, st);
+  if (e->vt_cache) {
+    // the same projections transposed, [kv_width][len] at key column slot·⌈len⌉₈ of the Vᵀ cache (the B
+    // operand of the cross-attention PV MMA is K-major over keys)
+    GemmDescT<AT> v;
+    v.A = wt<AT>(e->U.kv_all_w);
+    v.M = e->U.kv_width;
+    v.K = dim;
+    v.lda = dim;
+    v.Bw[0] = tmp;
+    v.N = len;
+    v.ldb = dim;
+    v.out = static_cast<AT*>(e->vt_cache);
+    v.ldo = (int)e->vt_ld;
+    v.col_off = slot * ((len + 7) / 8 * 8);
+    gemm(v, st);
+  }
   if (e->uc.add_time_dim) added_embedding<AT>(e, pooled, slot, st);
   SD_CUDA(cudaEventRecord(e->reg_ev, st));
   e->reg_ev_valid = true;
@@ -573,6 +598,8 @@ int ctx_register(Engine* e, const float* emb, int len, int dim, const float* poo
   }
   if (e->f32)
     ctx_kv<float>(e, emb, len, dim, pooled, slot, st);
+  else if (e->f16)
+    ctx_kv<f16>(e, emb, len, dim, pooled, slot, st);
   else
     ctx_kv<bf16>(e, emb, len, dim, pooled, slot, st);
   return slot;
@@ -608,7 +635,7 @@ struct Fwd {
     e->prof.end(pi, st);
   }
   void linear(const AT* A, long M, int K, const AT* W, int N, const float* bias, void* out, int ldo,
-              const AT* res = nullptr, int act = ACT_NONE, int out_f32 = 0) {
+              const AT* res = nullptr, int act = ACT_NONE, int out_f32 = 0, int cls = PC_GEMM) {
     GemmDescT<AT> d;
     d.A = A;
     d.M = (int)M;
@@ -624,7 +651,7 @@ struct Fwd {
     d.ldr = ldo;
     d.act = act;
     d.out_f32 = out_f32;
-    const int pi = e->prof.begin(PC_GEMM, st, 2.0 * M * N * K);
+    const int pi = e->prof.begin(cls, st, 2.0 * M * N * K);
     gemm(d, st);
     e->prof.end(pi, st);
   }
@@ -699,13 +726,13 @@ struct Fwd {
       d.out = s;
       d.ldo = r.cout;
       d.bias = r.bsc;
-      const int pi = e->prof.begin(PC_GEMM, st, 2.0 * R * P * r.cout * r.cin);
+      const int pi = e->prof.begin(PC_CONV1, st, 2.0 * R * P * r.cout * r.cin);
       gemm(d, st);
       e->prof.end(pi, st);
       sc = s;
     } else if (r.wsc) {
       AT* s = buf((long)R * P * r.cout);
-      linear(x, (long)R * P, r.cin, wt<AT>(r.wsc), r.cout, r.bsc, s, r.cout);
+      linear(x, (long)R * P, r.cin, wt<AT>(r.wsc), r.cout, r.bsc, s, r.cout, nullptr, ACT_NONE, 0, PC_CONV1);
       sc = s;
     }
     conv(a2, H, W, r.cout, wt<AT>(r.w2), r.cout, r.b2, out, nullptr, sc);
@@ -722,7 +749,7 @@ struct Fwd {
     AT* a = buf(T * C);
     gn(x, a, P, C, t.gng, t.gnb, e->uc.eps_tf, false);
     AT* h = buf(T * C);
-    linear(a, T, C, wt<AT>(t.wpin), C, t.bpin, h, C);
+    linear(a, T, C, wt<AT>(t.wpin), C, t.bpin, h, C, nullptr, ACT_NONE, 0, PC_CONV1);
     AT* hb = buf(T * C);  // ping-pong hidden state across blocks
     for (const BlkW& k : t.blk) {
       const size_t mb = e->ws.mark();
@@ -730,7 +757,7 @@ struct Fwd {
       ln(h, n, T, C, k.l1g, k.l1b);
       AT* o = buf(T * C);
       bool tc = false;
-      if constexpr (std::is_same<AT, bf16>::value) tc = e->use_attn_tc && attention_tc_supported(dh, P, C);
+      if constexpr (!std::is_same<AT, float>::value) tc = e->use_attn_tc && attention_tc_supported(dh, P, C);
       if (tc) {
         // tcgen05 flash attention: q|k token-major from one GEMM, Vᵀ channel-major from another
         AT* qk = buf(T * 2 * C);
@@ -738,7 +765,7 @@ struct Fwd {
         AT* vt = buf(T * C);
         linear(wt<AT>(k.wqkv) + 2L * C * C, C, C, n, (int)T, nullptr, vt, (int)T);
         const int pi = e->prof.begin(PC_ATTN, st, 4.0 * R * heads * (double)P * P * dh);
-        if constexpr (std::is_same<AT, bf16>::value) attention_tc(qk, vt, o, R, heads, dh, C, P, st);
+        if constexpr (!std::is_same<AT, float>::value) attention_tc(qk, vt, o, R, heads, dh, C, P, st);
         e->prof.end(pi, st);
       } else {
         AT* qkv = buf(T * 3 * C);
@@ -767,6 +794,18 @@ struct Fwd {
       ln(h2, n, T, C, k.l2g, k.l2b);
       AT* q2 = buf(T * C);
       linear(n, T, C, wt<AT>(k.wq2), C, nullptr, q2, C);
+      bool xtc = false;
+      if constexpr (!std::is_same<AT, float>::value)
+        xtc = e->use_xattn_tc && e->vt_cache && attention_tc_supported(dh, 128, C);
+      if (xtc) {
+        if constexpr (!std::is_same<AT, float>::value) {
+          const int pi = e->prof.begin(PC_ATTN, st, 4.0 * R * heads * (double)P * e->uc.ctx_len * dh);
+          xattention_tc(q2, static_cast<const AT*>(e->kv_cache), e->U.kv_width, e->max_slots, k.koff,
+                        static_cast<const AT*>(e->vt_cache), e->U.kv_width, e->vt_ld, k.voff, kv_index,
+                        e->uc.ctx_len, o, R, heads, dh, C, P, st);
+          e->prof.end(pi, st);
+        }
+      } else {
       AttnDescT<AT> cd{};
       cd.Q = q2;
       cd.ldq = C;
@@ -785,6 +824,7 @@ struct Fwd {
       cd.Lq = P;
       cd.Lk = e->uc.ctx_len;
       attn(cd);
+      }
       AT* h3 = buf(T * C);
       linear(o, T, C, wt<AT>(k.wo2), C, k.bo2, h3, C, h2);
       ln(h3, n, T, C, k.l3g, k.l3b);
@@ -794,7 +834,7 @@ struct Fwd {
       e->ws.reset(mb);
       std::swap(h, hb);
     }
-    linear(h, T, C, wt<AT>(t.wpout), C, t.bpout, out, C, x);  // proj_out + the transformer's input
+    linear(h, T, C, wt<AT>(t.wpout), C, t.bpout, out, C, x, ACT_NONE, 0, PC_CONV1);  // proj_out + the input
     e->ws.reset(mk);
     return out;
   }
@@ -865,7 +905,7 @@ static void unet_forward(Engine* e, cudaStream_t st, int R, int H, int W, const 
       const size_t mk = e->ws.mark();
       AT* out = f.buf((long)R * ho * wo * C);
       const size_t mk2 = e->ws.mark();
-      if constexpr (std::is_same<AT, bf16>::value) {
+      if constexpr (!std::is_same<AT, float>::value) {
         // 3×3 / stride 2 / pad 1 as an implicit GEMM whose TMA boxes step 2 input pixels per output
         // pixel (element strides), so the taps are never materialised
         if (h % 2 || w % 2) throw std::invalid_argument("downsampler: odd spatial size");
@@ -890,7 +930,7 @@ static void unet_forward(Engine* e, cudaStream_t st, int R, int H, int W, const 
     for (size_t j = 0; j < u.res.size(); ++j) {
       Skip s = skips.back();
       skips.pop_back();
-      if constexpr (std::is_same<AT, bf16>::value) {
+      if constexpr (!std::is_same<AT, float>::value) {
         x = f.resblock(u.res[j], x, h, w, s.p, s.C);  // concat [x | skip] read as two sources
       } else {  // fp32 parity mode: its SIMT GEMM takes one source
         const int Ccat = C + s.C;
@@ -1049,6 +1089,11 @@ void step_batch(Engine* e, const sd_batch* b, cudaStream_t st, float* eps_dump, 
       gather_rows(m, R, hw, 64, x_in, s);
       eps = e->ws.get<float>((size_t)R * hw * 4);
       unet_forward<float>(e, s, R, h, w, x_in, m.t_row, kv_dev, eps);
+    } else if (e->f16) {
+      f16* x_in = e->ws.get<f16>((size_t)R * hw * 64);
+      gather_rows(m, R, hw, 64, x_in, s);
+      eps = e->ws.get<float>((size_t)R * hw * 4);
+      unet_forward<f16>(e, s, R, h, w, x_in, m.t_row, kv_dev, eps);
     } else {
       bf16* x_in = e->ws.get<bf16>((size_t)R * hw * 64);
       gather_rows(m, R, hw, 64, x_in, s);

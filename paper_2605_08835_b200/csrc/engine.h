@@ -136,7 +136,9 @@ struct VItem {
 struct DecodeState;
 
 // Per-kernel-class device timing with CUDA events on the launching stream (bench roofline).
-enum { PC_CONV = 0, PC_GEMM = 1, PC_ATTN = 2, PC_GN = 3, PC_LN = 4, PC_OTHER = 5, PC_VAE = 6, PC_N = 7 };
+// PC_CONV1: the UNet's 1×1 convolutions (ResBlock shortcuts, transformer proj_in / proj_out) — dense
+// GEMMs counted in SURVEY §8(d)'s UNet conv fraction together with PC_CONV
+enum { PC_CONV = 0, PC_GEMM = 1, PC_ATTN = 2, PC_GN = 3, PC_LN = 4, PC_OTHER = 5, PC_VAE = 6, PC_CONV1 = 7, PC_N = 8 };
 struct Prof {
   bool on = false;
   struct Rec {
@@ -147,8 +149,8 @@ struct Prof {
   std::vector<Rec> recs;            // eager launches since the last read
   std::vector<Rec>* sink = nullptr; // while capturing a profiled graph: that graph's records
   std::vector<cudaEvent_t> pool;
-  double tot_ms[8] = {0}, tot_work[8] = {0};
-  long long tot_n[8] = {0};
+  double tot_ms[PC_N] = {0}, tot_work[PC_N] = {0};
+  long long tot_n[PC_N] = {0};
   cudaEvent_t ev();
   int begin(int cls, cudaStream_t st, double work);
   void end(int idx, cudaStream_t st);
@@ -172,9 +174,14 @@ struct Engine {
   UNetW U{};
   VAEW V{};
   bool f32 = false;       // SD_PREC_FP32: fp32 weights / activations, SIMT kernels (fp32.cu)
+  bool f16 = false;       // SD_PREC_FP16: fp16 weights / activations on the same tcgen05 kernels
   size_t esize = 2;       // bytes per weight / activation element
   // text K/V cache (activation precision)
   void* kv_cache = nullptr;
+  // text Vᵀ cache for the tcgen05 cross-attention: [kv_width][vt_ld], key j of slot s at column s·ctx_len + j
+  // (rows of every layer's K and V projections; the kernel reads the V rows)
+  void* vt_cache = nullptr;
+  long vt_ld = 0;
   float* aug_cache = nullptr;  // SDXL: [max_slots][T] added embedding per prompt slot (fp32)
   // admission scratch (the activation-precision copy of a prompt embedding, the added-embedding
   // rows, the constant time ids): reused by every sd_ctx_register; the event orders reuse across
@@ -205,7 +212,8 @@ struct Engine {
   };
   std::map<std::tuple<int, int, int, int, int>, GraphEntry> graphs;
   bool use_graphs = true;
-  bool use_attn_tc = true;  // tcgen05 flash attention where supported (SD_ATTN_TC=0 disables)
+  bool use_attn_tc = true;
+  bool use_xattn_tc = true;  // tcgen05 cross-attention over the text K / Vᵀ caches  // tcgen05 flash attention where supported (SD_ATTN_TC=0 disables)
   int graphs_built = 0;
   cudaStream_t cap_stream = nullptr;
   int max_rows = 0;

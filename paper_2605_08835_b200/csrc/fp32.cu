@@ -61,6 +61,7 @@ __device__ __forceinline__ int geglu_value_col(int j) { return (j / 64) * 128 + 
 
 template <bool GEGLU>
 __global__ void __launch_bounds__(256) gemm_f32_kernel(const F32GemmArgs g) {
+  pdl_wait();
   constexpr int NB = GEGLU ? 2 : 1;  // B row sets per tile: value (+ gate)
   __shared__ float As[FBK][FBM + 4];
   __shared__ float Bs[NB][FBK][FBN + 4];
@@ -141,6 +142,7 @@ __global__ void __launch_bounds__(256) gemm_f32_kernel(const F32GemmArgs g) {
 // O = softmax(Q·Kᵀ/√d)·V for one query per warp; lane l holds head channels l, l+32, … (NPL each)
 template <int NPL>
 __global__ void __launch_bounds__(128) attn_f32_kernel(const AttnDescT<float> a, float scale) {
+  pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = blockIdx.x * 4 + warp, head = blockIdx.y, row = blockIdx.z;
   if (q >= a.Lq) return;
@@ -231,9 +233,9 @@ void gemm(const GemmDescF& d, cudaStream_t st) {
   const int n_out = d.act == ACT_GEGLU ? d.N / 2 : d.N;
   const dim3 grid(cdiv(g.m_end - g.m0, FBM), cdiv(n_out, FBN));
   if (d.act == ACT_GEGLU)
-    gemm_f32_kernel<true><<<grid, 256, 0, st>>>(g);
+    launch_k(gemm_f32_kernel<true>, grid, 256, 0, st, g);
   else
-    gemm_f32_kernel<false><<<grid, 256, 0, st>>>(g);
+    launch_k(gemm_f32_kernel<false>, grid, 256, 0, st, g);
   SD_CHECK_LAUNCH();
 }
 
@@ -243,15 +245,15 @@ void attention(const AttnDescT<float>& a, cudaStream_t st) {
   const float scale = 1.f / sqrtf((float)a.d);
   const int npl = cdiv(a.d, 32);
   if (npl <= 1)
-    attn_f32_kernel<1><<<grid, 128, 0, st>>>(a, scale);
+    launch_k(attn_f32_kernel<1>, grid, 128, 0, st, a, scale);
   else if (npl <= 2)
-    attn_f32_kernel<2><<<grid, 128, 0, st>>>(a, scale);
+    launch_k(attn_f32_kernel<2>, grid, 128, 0, st, a, scale);
   else if (npl <= 4)
-    attn_f32_kernel<4><<<grid, 128, 0, st>>>(a, scale);
+    launch_k(attn_f32_kernel<4>, grid, 128, 0, st, a, scale);
   else if (npl <= 8)
-    attn_f32_kernel<8><<<grid, 128, 0, st>>>(a, scale);
+    launch_k(attn_f32_kernel<8>, grid, 128, 0, st, a, scale);
   else
-    attn_f32_kernel<16><<<grid, 128, 0, st>>>(a, scale);
+    launch_k(attn_f32_kernel<16>, grid, 128, 0, st, a, scale);
   SD_CHECK_LAUNCH();
 }
 

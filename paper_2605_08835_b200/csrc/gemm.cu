@@ -45,6 +45,7 @@ struct GemmArgs {
   int tma_store;      // bf16 output through the per-warp smem slab + TMA store
   int res_tma;        // dense: the residual sub-tile arrives by TMA in the staging slab (coalesced)
   int gelu_tanh;      // GEGLU: tanh form of GELU on MUFU tanh.approx (default; SD_GELU_TANH=0 = erf form)
+  int f16;            // 16-bit operands / outputs are fp16 (SD_PREC_FP16) instead of bf16
   int dbg;            // experiment switch (SD_EPI_DBG): 1 = no store, 2 = no bias, 3 = no TMEM load
   int splits, kps;    // split-K: K blocks [s·kps, (s+1)·kps) of split s
   float* part;        // split-K fp32 partials [splits][M][N] (raw accumulators)
@@ -206,7 +207,7 @@ struct EpiCtx {
 };
 
 // write 32 fp32 values (this lane's row, columns [col, col+32)) to the staging slab and TMA-store it
-template <int MODE>
+template <int MODE, bool F16>
 __device__ __forceinline__ void stage_store(const GemmArgs& g, const CUtensorMap* om, EpiCtx& ec, const float* o,
                                             int col, int lane, bool slab_ready = false) {
   uint8_t* buf = ec.stage + ec.slot * 2048;
@@ -217,8 +218,8 @@ __device__ __forceinline__ void stage_store(const GemmArgs& g, const CUtensorMap
   const int sw = (lane >> 1) & 3;
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
-    const uint4 v = make_uint4(pack_bf16(o[8 * c], o[8 * c + 1]), pack_bf16(o[8 * c + 2], o[8 * c + 3]),
-                               pack_bf16(o[8 * c + 4], o[8 * c + 5]), pack_bf16(o[8 * c + 6], o[8 * c + 7]));
+    const uint4 v = make_uint4(pack16(o[8 * c], o[8 * c + 1], F16), pack16(o[8 * c + 2], o[8 * c + 3], F16),
+                               pack16(o[8 * c + 4], o[8 * c + 5], F16), pack16(o[8 * c + 6], o[8 * c + 7], F16));
     *reinterpret_cast<uint4*>(buf + lane * 64 + ((c ^ sw) << 4)) = v;
   }
   fence_async_smem();
@@ -253,7 +254,7 @@ __device__ __forceinline__ void res_load32(uint4 (&r)[4], const bf16* rp) {
 }
 
 // `tfull` / `tphase`: the accumulator-ready barrier of this tile
-template <int BN, int MODE>
+template <int BN, int MODE, bool F16>
 __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorMap* om, const CUtensorMap* res_map,
                                               EpiCtx& ec, uint32_t tbase,
                                               int mbox, int n0, int q, int lane, int half, int split, uint64_t* tfull,
@@ -328,9 +329,9 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
         if (g.res && valid) {
           const bf16* rp = g.res + prow * g.ldr + ocol;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] += __bfloat162float(rp[i]);
+          for (int i = 0; i < 32; ++i) o[i] += cvt16(rp[i], F16);
         }
-        stage_store<MODE>(g, om, ec, o, ocol, lane);
+        stage_store<MODE, F16>(g, om, ec, o, ocol, lane);
       }
     }
     return;
@@ -410,7 +411,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
         const uint4 u = *reinterpret_cast<const uint4*>(buf + lane * 64 + ((i ^ sw) << 4));
         const bf16* e = reinterpret_cast<const bf16*>(&u);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) o[8 * i + k] += __bfloat162float(e[k]);
+        for (int k = 0; k < 8; ++k) o[8 * i + k] += cvt16(e[k], F16);
       }
     } else if (g.res && valid) {
       const bf16* rp = g.res + prow * g.ldr + col;
@@ -421,16 +422,16 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
         for (int i = 0; i < 4; ++i) {
           const bf16* e = reinterpret_cast<const bf16*>(&u4[i]);
 #pragma unroll
-          for (int k = 0; k < 8; ++k) o[8 * i + k] += __bfloat162float(e[k]);
+          for (int k = 0; k < 8; ++k) o[8 * i + k] += cvt16(e[k], F16);
         }
       } else {
-        for (int i = 0; i < 32 && col + i < g.N; ++i) o[i] += __bfloat162float(rp[i]);
+        for (int i = 0; i < 32 && col + i < g.N; ++i) o[i] += cvt16(rp[i], F16);
       }
     }
     if (g.dbg == 1) {
       if (o[0] == 12345.f) g.res ? (void)0 : __trap();
     } else if (g.tma_store) {
-      stage_store<MODE>(g, om, ec, o, col, lane, rt);
+      stage_store<MODE, F16>(g, om, ec, o, col, lane, rt);
     } else if (valid) {
       if (g.out_f32) {
         float* op = reinterpret_cast<float*>(g.out) + prow * g.ldo + g.col_off + col;
@@ -447,17 +448,17 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
           uint4* o4 = reinterpret_cast<uint4*>(op);
 #pragma unroll
           for (int i = 0; i < 4; ++i)
-            o4[i] = make_uint4(pack_bf16(o[8 * i], o[8 * i + 1]), pack_bf16(o[8 * i + 2], o[8 * i + 3]),
-                               pack_bf16(o[8 * i + 4], o[8 * i + 5]), pack_bf16(o[8 * i + 6], o[8 * i + 7]));
+            o4[i] = make_uint4(pack16(o[8 * i], o[8 * i + 1], F16), pack16(o[8 * i + 2], o[8 * i + 3], F16),
+                               pack16(o[8 * i + 4], o[8 * i + 5], F16), pack16(o[8 * i + 6], o[8 * i + 7], F16));
         } else {
-          for (int i = 0; i < 32 && col + i < g.N; ++i) op[i] = __float2bfloat16(o[i]);
+          for (int i = 0; i < 32 && col + i < g.N; ++i) op[i] = to16(o[i], F16);
         }
       }
     }
   }
 }
 
-template <int BN, int CG, int MODE>
+template <int BN, int CG, int MODE, bool F16>
 __global__ void __launch_bounds__(320, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ CUtensorMap ta1,
                 const __grid_constant__ CUtensorMap tb0, const __grid_constant__ CUtensorMap tb1,
@@ -507,6 +508,7 @@ __global__ void __launch_bounds__(320, 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // barrier init, TMEM alloc and descriptor prefetch above overlapped the previous grid (PDL)
 
   const int total = g.m_tiles * g.n_tiles * g.splits;
   const int worker = blockIdx.x / CG, nworkers = gridDim.x / CG;
@@ -572,7 +574,7 @@ __global__ void __launch_bounds__(320, 1)
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
       // ================= MMA issuer (leader CTA) =================
-      constexpr uint32_t idesc = make_idesc_bf16(128 * CG, BN);
+      const uint32_t idesc = make_idesc16(128 * CG, BN, F16);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -615,7 +617,7 @@ __global__ void __launch_bounds__(320, 1)
       int mt, nt, sp, kb0, kb1;
       decode_tile(g, t, mt, nt, sp, kb0, kb1);
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * C::TMEM_STRIDE;
-      epilogue_tile<BN, MODE>(g, &tout, &tres, ec, tbase, mt * CG + (int)rank, nt * BN, q, lane, (warp - 2) >> 2, sp,
+      epilogue_tile<BN, MODE, F16>(g, &tout, &tres, ec, tbase, mt * CG + (int)rank, nt * BN, q, lane, (warp - 2) >> 2, sp,
                               &tfull[acc], acc_phase);
       tc_fence_before();
       __syncwarp();
@@ -659,6 +661,9 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
+// 16-bit element type of the maps built by this thread's current gemm() call (bf16, or fp16)
+static thread_local CUtensorMapDataType t_map_dtype = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+
 static void make_map(CUtensorMap* m, const void* ptr, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
                      const uint32_t* box, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B,
                      const uint32_t* elem_strides = nullptr) {
@@ -670,17 +675,19 @@ static void make_map(CUtensorMap* m, const void* ptr, int rank, const uint64_t* 
     es[i] = elem_strides ? elem_strides[i] : 1;
     if (i + 1 < rank) gs[i] = strides_bytes[i];
   }
-  CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), gd, gs, bx, es,
+  CUresult r = encode_fn()(m, t_map_dtype, rank, const_cast<void*>(ptr), gd, gs, bx, es,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
 }
 
 void make_tmap_2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_bytes, uint32_t box_in,
-                  uint32_t box_out) {
+                  uint32_t box_out, bool is_f16, bool swz64) {
   uint64_t d[2] = {inner, outer}, s[1] = {row_bytes};
   uint32_t b[2] = {box_in, box_out};
-  make_map(m, ptr, 2, d, s, b);
+  t_map_dtype = is_f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  make_map(m, ptr, 2, d, s, b, swz64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B);
+  t_map_dtype = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
 }
 
 int num_sms() {
@@ -711,7 +718,8 @@ void conv3_tile_geometry(int B, int H, int W, int* wt, int* ht, int* bt) {
 __global__ void splitk_reduce_kernel(const float* __restrict__ part, int S, long M, int N, const float* __restrict__ bias,
                                      const float* __restrict__ temb, int ld_temb, int rows_per_img,
                                      const bf16* __restrict__ res, int ldr, int act, float alpha, bf16* __restrict__ out,
-                                     int ldo, int col_off) {
+                                     int ldo, int col_off, int is_f16) {
+  pdl_wait();
   const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;  // one group of 4 columns
   const int nq = N / 4;
   if (i >= M * nq) return;
@@ -730,9 +738,9 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ part, int S, long
     if (bias) o[k] += bias[n + k];
     if (temb) o[k] += temb[(m / rows_per_img) * ld_temb + n + k];
     if (act == ACT_SILU) o[k] = silu_f(o[k]);
-    if (res) o[k] += __bfloat162float(res[m * ldr + n + k]);
+    if (res) o[k] += cvt16(res[m * ldr + n + k], is_f16);
   }
-  uint2 pk = make_uint2(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]));
+  uint2 pk = make_uint2(pack16(o[0], o[1], is_f16), pack16(o[2], o[3], is_f16));
   *reinterpret_cast<uint2*>(out + m * ldo + col_off + n) = pk;
 }
 
@@ -741,7 +749,8 @@ static void launch(const CUtensorMap* m, const GemmArgs& a, cudaStream_t st) {
   using C = Cfg<BN, CG>;
   static bool attr_set = false;
   if (!attr_set) {
-    SD_CUDA(cudaFuncSetAttribute(gemm_kernel<BN, CG, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    SD_CUDA(cudaFuncSetAttribute(gemm_kernel<BN, CG, MODE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    SD_CUDA(cudaFuncSetAttribute(gemm_kernel<BN, CG, MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr_set = true;
   }
   const int total = a.m_tiles * a.n_tiles * a.splits;
@@ -753,14 +762,19 @@ static void launch(const CUtensorMap* m, const GemmArgs& a, cudaStream_t st) {
   cfg.blockDim = dim3(320);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  SD_CUDA(cudaLaunchKernelEx(&cfg, gemm_kernel<BN, CG, MODE>, m[0], m[1], m[2], m[3], m[4], m[5], a));
+  cfg.numAttrs = g_pdl ? 2 : 1;
+  if (a.f16)
+    SD_CUDA(cudaLaunchKernelEx(&cfg, gemm_kernel<BN, CG, MODE, true>, m[0], m[1], m[2], m[3], m[4], m[5], a));
+  else
+    SD_CUDA(cudaLaunchKernelEx(&cfg, gemm_kernel<BN, CG, MODE, false>, m[0], m[1], m[2], m[3], m[4], m[5], a));
   SD_CHECK_LAUNCH();
 }
 
@@ -795,7 +809,11 @@ static int pick_bn(int N, int act) {
   return 256;
 }
 
-int g_cg_override = -1;  // 0 = heuristic, 1 / 2 = force (tests, SD_GEMM_CG)
+int g_cg_override = -1;
+int g_pdl = [] {  // SD_PDL=0: plain stream-ordered launches
+  const char* e = getenv("SD_PDL");
+  return e && e[0] == '0' ? 0 : 1;
+}();  // 0 = heuristic, 1 / 2 = force (tests, SD_GEMM_CG)
 
 static int conv_num_kb(const GemmDesc& d) {
   int kb = 0;
@@ -839,6 +857,8 @@ void gemm(const GemmDesc& d, cudaStream_t st) {
   CUtensorMap maps[6];
   memset(maps, 0, sizeof(maps));
   a.mode = d.mode;
+  a.f16 = d.f16;
+  t_map_dtype = d.f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   a.N = d.N;
   static int bn_env = -1;  // SD_GEMM_BN: force the N tile of dense GEMMs (experiments)
   if (bn_env < 0) {
@@ -1016,17 +1036,30 @@ void gemm(const GemmDesc& d, cudaStream_t st) {
     make_map(&maps[5], d.res, 2, dR, sR, bR, CU_TENSOR_MAP_SWIZZLE_64B);
     a.res_tma = 1;
   }
+  t_map_dtype = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   if (d.mode == GEMM_DENSE)
     dispatch<GEMM_DENSE>(bn, cg, maps, a, st);
   else
     dispatch<GEMM_CONV3>(bn, cg, maps, a, st);
   if (a.splits > 1) {
     const long n4 = (long)a.M * (d.N / 4);
-    splitk_reduce_kernel<<<(unsigned)cdiv(n4, 256), 256, 0, st>>>(
+    launch_k(splitk_reduce_kernel, (unsigned)cdiv(n4, 256), 256, 0, st, 
         a.part, a.splits, a.M, d.N, d.bias, d.temb, d.ld_temb, d.H * d.W, d.res, d.ldr, d.act, d.alpha,
-        reinterpret_cast<bf16*>(d.out), d.ldo, d.col_off);
+        reinterpret_cast<bf16*>(d.out), d.ldo, d.col_off, d.f16);
     SD_CHECK_LAUNCH();
   }
 }
+
+// SD_PREC_FP16: the same kernels; the descriptor differs only in its pointer types
+static GemmDesc as16(const GemmDescT<f16>& d) {
+  static_assert(sizeof(GemmDescT<f16>) == sizeof(GemmDesc), "GemmDescT layouts must match");
+  GemmDesc b;
+  memcpy(static_cast<void*>(&b), static_cast<const void*>(&d), sizeof(b));
+  b.f16 = 1;
+  return b;
+}
+void gemm(const GemmDescT<f16>& d, cudaStream_t st) { gemm(as16(d), st); }
+int gemm_splits(const GemmDescT<f16>& d) { return gemm_splits(as16(d)); }
+size_t gemm_split_ws_bytes(const GemmDescT<f16>& d) { return gemm_split_ws_bytes(as16(d)); }
 
 }  // namespace sd

@@ -2,9 +2,11 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <stdint.h>
 
 typedef __nv_bfloat16 bf16;
+typedef __half f16;
 
 namespace sd {
 
@@ -56,6 +58,7 @@ struct GemmDescT {
   int splits = 0;
   float* split_ws = nullptr;
   size_t split_ws_bytes = 0;
+  int f16 = 0;                // fp16 instead of bf16 (set by the GemmDescT<f16> overloads)
 };
 
 using GemmDesc = GemmDescT<bf16>;
@@ -66,6 +69,9 @@ void gemm(const GemmDescF& d, cudaStream_t st);  // fp32 parity mode (fp32.cu)
 inline size_t gemm_split_ws_bytes(const GemmDescF&) { return 0; }
 int gemm_splits(const GemmDesc& d);              // the split count gemm() will use given a workspace
 size_t gemm_split_ws_bytes(const GemmDesc& d);   // workspace bytes (0 when not split)
+void gemm(const GemmDescT<f16>& d, cudaStream_t st);  // SD_PREC_FP16: fp16 operands / outputs
+int gemm_splits(const GemmDescT<f16>& d);
+size_t gemm_split_ws_bytes(const GemmDescT<f16>& d);
 // M tiles of a conv3 launch whose output rows lie in [y0, y1) of image 0 (used for bands).
 void conv3_tile_geometry(int B, int H, int W, int* wt, int* ht, int* bt);
 int num_sms();

@@ -2,10 +2,12 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <stddef.h>
 #include <stdint.h>
 
 typedef __nv_bfloat16 bf16;
+typedef __half f16;
 
 namespace sd {
 
@@ -51,13 +53,25 @@ using AttnDesc = AttnDescT<bf16>;
 void attention(const AttnDesc& a, cudaStream_t st);
 // fp32 parity mode (fp32.cu): one warp per query, fp32 online softmax; any d ≤ 512
 void attention(const AttnDescT<float>& a, cudaStream_t st);
+void attention(const AttnDescT<f16>& a, cudaStream_t st);  // SD_PREC_FP16 (mma.sync .f16)
 
 // tcgen05 flash attention (attention_tc.cu): qk [rows·P][2C] (q | k), vt [C][rows·P], O [rows·P][C]
 bool attention_tc_supported(int d, int P, int C);
 void attention_tc(const bf16* qk, const bf16* vt, bf16* O, int rows, int heads, int d, int C, int P, cudaStream_t st);
+void attention_tc(const f16* qk, const f16* vt, f16* O, int rows, int heads, int d, int C, int P, cudaStream_t st);
+// tcgen05 cross-attention over cached text tokens (K7): q [rows·P][C]; kc [n_slots·Lk][ldk] (this layer's K at
+// column kcol); vtc [vt_rows][ld_keys] (this layer's Vᵀ at row vrow; key j of slot s at column s·⌈Lk⌉₈ + j);
+// kv_index [rows] slot per batch row (device); O [rows·P][C]. d ∈ {40, 64, 80, 160}.
+void xattention_tc(const bf16* q, const bf16* kc, int ldk, long n_slots, int kcol, const bf16* vtc, long vt_rows,
+                   long ld_keys, int vrow, const int* kv_index, int Lk, bf16* O, int rows, int heads, int d, int C, int P,
+                   cudaStream_t st);
+void xattention_tc(const f16* q, const f16* kc, int ldk, long n_slots, int kcol, const f16* vtc, long vt_rows,
+                   long ld_keys, int vrow, const int* kv_index, int Lk, f16* O, int rows, int heads, int d, int C, int P,
+                   cudaStream_t st);
 
 // row softmax for the VAE attention path: P[r][:] = softmax(S[r][:]) (S fp32, P bf16)
 void softmax_rows(const float* S, bf16* P, int rows, int cols, cudaStream_t st);
+void softmax_rows(const float* S, f16* P, int rows, int cols, cudaStream_t st);
 
 // ---- elementwise (elementwise.cu) ----
 struct RowMap {                 // device-side per-step metadata (uploaded once per call)
@@ -85,6 +99,7 @@ void concat_channels(const T* a, int ca, const T* b, int cb, T* y, long P, cudaS
 void f32_to_bf16(const float* x, bf16* y, long n, cudaStream_t st);
 inline void f32_to_act(const float* x, bf16* y, long n, cudaStream_t st) { f32_to_bf16(x, y, n, st); }
 void f32_to_act(const float* x, float* y, long n, cudaStream_t st);  // device copy
+void f32_to_act(const float* x, f16* y, long n, cudaStream_t st);
 void gather_rows_f32(const float* src, const int* idx, int rows, int n, float* dst, cudaStream_t st);
 // VAE head input: z fp32 [4][h][w] → NHWC [h][w][cpad] of z·scale (zeros in channels ≥ 4)
 template <class T>
@@ -106,7 +121,7 @@ struct WeightInit {
   int F;               // GEGLU: half width (rows are [value F | gate F])
   void* dst0;
   void* dst1;
-  int out_bf16;
+  int out_bf16;        // 0 fp32, 1 bf16, 2 fp16 (SD_PREC_FP16)
   const float* src;    // nullptr: generate; else canonical fp32 values (sd_engine_set_weight)
 };
 void init_weight(const WeightInit& w, cudaStream_t st);

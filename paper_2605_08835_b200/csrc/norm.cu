@@ -50,6 +50,16 @@ struct Raw8<bf16> {
   }
 };
 template <>
+struct Raw8<f16> {
+  uint4 u;
+  __device__ __forceinline__ void ld(const f16* p) { u = __ldg(reinterpret_cast<const uint4*>(p)); }
+  __device__ __forceinline__ void get(float (&f)[8]) const {
+    const f16* e = reinterpret_cast<const f16*>(&u);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) f[i] = __half2float(e[i]);
+  }
+};
+template <>
 struct Raw8<float> {
   float4 a, b;
   __device__ __forceinline__ void ld(const float* p) {
@@ -133,6 +143,7 @@ template <class T>
 __global__ void __launch_bounds__(512) gn_stats_kernel(const T* __restrict__ x, const T* __restrict__ x1, int V0, int P,
                                                        int C, int G, int chunk_px, int c_base, int nch_total,
                                                        GNPart* __restrict__ part) {
+  pdl_wait();
   extern __shared__ float sh[];  // [R][C] sums, then [R][C] sums of squares
   const int V = blockDim.x, R = blockDim.y;
   const int v = threadIdx.x, ry = threadIdx.y;
@@ -202,6 +213,7 @@ __global__ void __launch_bounds__(512) gn_stats_kernel(const T* __restrict__ x, 
 __global__ void gn_finalize_kernel(int P, int C, int G, int chunk_px, int nchunks, const GNPart* __restrict__ part,
                                    float eps, const float* __restrict__ gamma, const float* __restrict__ beta,
                                    float2* __restrict__ tab) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int b = blockIdx.y;
@@ -229,6 +241,7 @@ template <class T>
 __global__ void __launch_bounds__(512) gn_apply_kernel(const T* __restrict__ x, const T* __restrict__ x1, int V0,
                                                        long p_begin, long p_end, int P, int V,
                                                        const float2* __restrict__ tab, int silu, T* __restrict__ y) {
+  pdl_wait();
   constexpr int U = 4;
   const int v = threadIdx.x, R = blockDim.y;
   // source of this thread's channel vector; pixel p of the flat [B·P] range sits at row p of it
@@ -283,7 +296,7 @@ static float2* gn_tab(void* ws, int B, int P, int G) {
 static void gn_finalize(int B, int P, int C, int G, int cp, void* ws, float eps, const float* gamma, const float* beta,
                         cudaStream_t st) {
   const int wpb = 4;  // warps per block
-  gn_finalize_kernel<<<dim3(cdiv(G, wpb), B), 32 * wpb, 0, st>>>(P, C, G, cp, cdiv(P, cp), gn_parts(ws), eps, gamma,
+  launch_k(gn_finalize_kernel, dim3(cdiv(G, wpb), B), 32 * wpb, 0, st, P, C, G, cp, cdiv(P, cp), gn_parts(ws), eps, gamma,
                                                                   beta, gn_tab(ws, B, P, G));
   SD_CHECK_LAUNCH();
 }
@@ -308,7 +321,7 @@ static void gn_apply(const T* x, const T* x1, int C0, T* y, long p0, long p1, in
     st_env = e ? atoi(e) : 1;
   }
   const int sm = !silu ? 0 : (std::is_same<T, bf16>::value && st_env) ? 2 : 1;
-  gn_apply_kernel<T><<<grid, blk, 0, st>>>(x, x1, C0 / 8, p0, p1, P, C / 8, tab, sm, y);
+  launch_k(gn_apply_kernel<T>, grid, blk, 0, st, x, x1, C0 / 8, p0, p1, P, C / 8, tab, sm, y);
   SD_CHECK_LAUNCH();
   (void)B;
 }
@@ -323,7 +336,7 @@ static void gn_stats(const T* x, const T* x1, int C0, int B, int P, int C, int G
   const int cp = gn_chunk_px(C);
   const dim3 blk = gn_stats_block(C);
   const size_t sh = (size_t)blk.x * blk.y * 8 * 2 * sizeof(float);
-  gn_stats_kernel<<<dim3(c1 - c0, B), blk, sh, st>>>(x, x1, C0 / 8, P, C, G, cp, c0, cdiv(P, cp), gn_parts(ws));
+  launch_k(gn_stats_kernel<T>, dim3(c1 - c0, B), blk, sh, st, x, x1, C0 / 8, P, C, G, cp, c0, cdiv(P, cp), gn_parts(ws));
   SD_CHECK_LAUNCH();
 }
 
@@ -369,6 +382,7 @@ void group_norm2(const T* x0, int C0, const T* x1, int C1, T* y, int B, int P, i
 template <int NV, int LANES, class E>
 __global__ void layer_norm_kernel(const E* __restrict__ x, int T, int C, const float* __restrict__ gamma,
                                   const float* __restrict__ beta, float eps, E* __restrict__ y) {
+  pdl_wait();
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
   const int tok = gtid / LANES, l = gtid % LANES;
   if (tok >= T) return;  // LANES divides 32, so whole lane groups exit together
@@ -429,7 +443,7 @@ static void ln_launch(const E* x, E* y, int T, int C, const float* g, const floa
                       cudaStream_t st) {
   const int threads = 256;
   const long total = (long)T * LANES;
-  layer_norm_kernel<NV, LANES, E><<<cdiv(total, threads), threads, 0, st>>>(x, T, C, g, b, eps, y);
+  launch_k(layer_norm_kernel<NV, LANES, E>, cdiv(total, threads), threads, 0, st, x, T, C, g, b, eps, y);
   SD_CHECK_LAUNCH();
 }
 
@@ -461,6 +475,7 @@ void layer_norm(const E* x, E* y, int T, int C, const float* gamma, const float*
   template void group_norm2<T>(const T*, int, const T*, int, T*, int, int, int, const float*, const float*, float, \
                                bool, void*, cudaStream_t);
 SD_NORM_INST(bf16)
+SD_NORM_INST(f16)
 SD_NORM_INST(float)
 
 }  // namespace sd

@@ -16,6 +16,12 @@
 
 namespace sd {
 
+// query rows per chunk of the VAE mid-block attention: fp32 scores ≤ 2^24 elements (64 MB)
+static size_t vae_attn_rows(size_t P) {
+  size_t r = ((size_t)1 << 24) / P / 128 * 128;
+  return std::max<size_t>(128, std::min(P, r));
+}
+
 enum { VOP_HEAD = 0, VOP_GN_STATS, VOP_GN_APPLY, VOP_CONV, VOP_SHORTCUT, VOP_UPSAMPLE, VOP_FINAL };
 enum { NBUF = 6 };
 
@@ -76,7 +82,8 @@ static void conv_desc(GemmDescT<AT>& d, const AT* x, int H, int W, int C, const 
 
 // restrict a conv launch to output rows [y0, y1) of image 0: 128-pixel boxes of the tcgen05 kernel,
 // output pixels of the fp32 kernel (kernels.h)
-static void set_band(GemmDesc& d, int H, int W, int y0, int y1) {
+template <class T>
+static void set_band(GemmDescT<T>& d, int H, int W, int y0, int y1) {
   int wt, ht, bt;
   conv3_tile_geometry(1, H, W, &wt, &ht, &bt);
   const int tx = cdiv(W, wt);
@@ -166,15 +173,21 @@ static void run_head(Engine* e, DecodeState* s, const float* z, cudaStream_t st)
   AT* o = sb<AT>(s, 4);
   lin(a, P, cm, wt<AT>(V.wq), cm, V.bq, q, cm, nullptr, 0, 1.f, 0);
   lin(a, P, cm, wt<AT>(V.wk), cm, V.bk, k, cm, nullptr, 0, 1.f, 0);
-  if constexpr (std::is_same<AT, bf16>::value) {
+  if constexpr (!std::is_same<AT, float>::value) {
     // via tcgen05 GEMMs: S = QKᵀ/√d (fp32), P = softmax(S), O = P·Vᵀᵀ
+    // in query chunks of Pq rows, so the fp32 scores stay ≤ 64 MB (1024² = 16384 tokens: 16 chunks of
+    // 1024 rows instead of one 1 GiB S and a 512 MiB P)
+    const int Pq = (int)vae_attn_rows((size_t)P);
     AT* vt = s->ar.get<AT>((size_t)P * cm);
-    float* S = s->ar.get<float>((size_t)P * P);
-    AT* Pm = s->ar.get<AT>((size_t)P * P);
+    float* S = s->ar.get<float>((size_t)Pq * P);
+    AT* Pm = s->ar.get<AT>((size_t)Pq * P);
     lin(wt<AT>(V.wv), cm, cm, a, P, V.bv, vt, P, nullptr, 1, 1.f, 0);  // Vᵀ = Wv·aᵀ (+bv per row)
-    lin(q, P, cm, k, P, nullptr, S, P, nullptr, 0, 1.f / sqrtf((float)cm), 1);
-    softmax_rows(S, Pm, P, P, st);
-    lin(Pm, P, P, vt, cm, nullptr, o, cm, nullptr, 0, 1.f, 0);
+    for (int r0 = 0; r0 < P; r0 += Pq) {
+      const int rq = std::min(Pq, P - r0);
+      lin(q + (long)r0 * cm, rq, cm, k, P, nullptr, S, P, nullptr, 0, 1.f / sqrtf((float)cm), 1);
+      softmax_rows(S, Pm, rq, P, st);
+      lin(Pm, rq, P, vt, cm, nullptr, o + (long)r0 * cm, cm, nullptr, 0, 1.f, 0);
+    }
   } else {
     // fp32 parity mode: V token-major and the fp32 attention kernel
     AT* v = s->ar.get<AT>((size_t)P * cm);
@@ -405,7 +418,7 @@ static DecodeState* new_decode(Engine* e, int h, int w) {
   s->buf_elems = decode_buf_elems(e, h, w);
   const size_t P = (size_t)h * w;
   const int cm = e->vc.block_out.back();
-  const size_t head = P * 64 * 2 * 2 + P * cm * 2 * 3 + P * P * 6 + ((size_t)8 << 20);
+  const size_t head = P * 64 * 2 * 2 + P * cm * 2 * 3 + vae_attn_rows(P) * P * 6 + ((size_t)8 << 20);
   const size_t img = (size_t)64 * P * 3 * 4;
   const size_t gnb = gn_workspace_bytes(1, (int)(64 * P), 64, 1024);
   s->ar.init(NBUF * (s->buf_elems * e->esize + 4096) + head * (e->esize / 2) + img + gnb + ((size_t)16 << 20));
@@ -458,6 +471,8 @@ void vae_decode_chunk(Engine* e, const float* z, int h, int w, int n_chunks, int
     for (int i = s->bounds[chunk]; i < s->bounds[chunk + 1]; ++i) {
       if (e->f32)
         run_item<float>(e, s, s->items[i], z, image, st);
+      else if (e->f16)
+        run_item<f16>(e, s, s->items[i], z, image, st);
       else
         run_item<bf16>(e, s, s->items[i], z, image, st);
     }

@@ -23,6 +23,7 @@ __device__ __forceinline__ float gen(const WeightInit& w, long i) {
 }
 
 __global__ void init_weight_kernel(const WeightInit w) {
+  pdl_wait();
   const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= w.n) return;
   const float v = w.src ? w.src[i] : gen(w, i);
@@ -50,7 +51,9 @@ __global__ void init_weight_kernel(const WeightInit w) {
   } else if (w.layout == WL_ROWS) {
     off = (i / w.I) * w.Ipad + (i % w.I);
   }
-  if (w.out_bf16)
+  if (w.out_bf16 == 2)  // SD_PREC_FP16: the generated bf16 value (R20), held in fp16; loaded values round once
+    reinterpret_cast<f16*>(dst)[off] = __float2half_rn(w.src ? v : __bfloat162float(__float2bfloat16_rn(v)));
+  else if (w.out_bf16)
     reinterpret_cast<bf16*>(dst)[off] = __float2bfloat16_rn(v);
   else
     reinterpret_cast<float*>(dst)[off] = v;
@@ -58,7 +61,7 @@ __global__ void init_weight_kernel(const WeightInit w) {
 
 void init_weight(const WeightInit& w, cudaStream_t st) {
   if (w.n <= 0) return;
-  init_weight_kernel<<<cdiv(w.n, 256), 256, 0, st>>>(w);
+  launch_k(init_weight_kernel, cdiv(w.n, 256), 256, 0, st, w);
   SD_CHECK_LAUNCH();
 }
 

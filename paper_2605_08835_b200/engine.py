@@ -19,15 +19,17 @@ def _stream(s):
 
 class Engine:
     def __init__(self, model="tiny", sampler="ddim", max_latent_hw=None, b_max=8, c_max=16, weight_seed=0,
-                 device=0, precision="bf16"):
-        """precision: "bf16" (the product path) or "fp32" (the parity mode, SD_PREC_FP32)."""
+                 device=0, precision="fp16"):
+        """precision: "fp16" (the product default, SD_PREC_FP16: fp16 operands / activations, the bf16-valued
+        weights held exactly), "bf16" (SD_PREC_BF16: the same kernels with bf16 operands / activations) or
+        "fp32" (the parity mode, SD_PREC_FP32)."""
         m = {"tiny": B.SD_MODEL_TINY, "sd15": B.SD_MODEL_SD15, "sdxl": B.SD_MODEL_SDXL,
              "tinyxl": B.SD_MODEL_TINY_XL}[model]
         sm = {"ddim": B.SD_SAMPLER_DDIM, "euler": B.SD_SAMPLER_EULER}[sampler]
         tiny = model in ("tiny", "tinyxl")
         if max_latent_hw is None:
             max_latent_hw = 8 if tiny else (128 if model == "sdxl" else 64)
-        prec = {"bf16": B.SD_PREC_BF16, "fp32": B.SD_PREC_FP32}[precision]
+        prec = {"bf16": B.SD_PREC_BF16, "fp16": B.SD_PREC_FP16, "fp32": B.SD_PREC_FP32}[precision]
         cfg = B.EngineConfig(m, prec, sm, max_latent_hw, b_max, c_max, weight_seed)
         h = C.c_void_p()
         B.call("sd_engine_create", C.byref(cfg), device, C.byref(h))

@@ -203,7 +203,8 @@ def test_attention_mma(R, heads, d, L, S):
     assert rel(o.cpu(), _attn_ref(q.float(), k.float(), v.float(), heads)) < 1e-2
 
 
-@pytest.mark.parametrize("R,heads,d,P", [(2, 8, 40, 256), (1, 8, 80, 384), (2, 10, 64, 128), (1, 8, 40, 4096)])
+@pytest.mark.parametrize("R,heads,d,P", [(2, 8, 40, 256), (1, 8, 80, 384), (2, 10, 64, 128), (1, 8, 40, 4096),
+                                         (2, 8, 160, 256), (3, 8, 160, 64), (2, 8, 40, 200), (2, 8, 80, 8)])
 def test_attention_tcgen05(R, heads, d, P):
     g = torch.Generator().manual_seed(P + d)
     C = heads * d
@@ -214,6 +215,39 @@ def test_attention_tcgen05(R, heads, d, P):
     B.call("sd_debug_attention_tc", B._p(qk), B._p(vt), B._p(o), R, heads, d, P, None)
     torch.cuda.synchronize()
     assert rel(o.cpu().reshape(R, P, C), _attn_ref(q.float(), k.float(), v.float(), heads)) < 1e-2
+
+
+@pytest.mark.parametrize("f16", [0, 1])
+@pytest.mark.parametrize("R,heads,d,P,n_slots,Lk", [(3, 8, 40, 256, 5, 77), (2, 8, 80, 200, 4, 77), (2, 8, 160, 64, 3, 77), (2, 8, 160, 256, 4, 77),
+                                                   (2, 10, 64, 128, 3, 77), (1, 2, 40, 128, 2, 128), (2, 4, 40, 64, 4, 8)])
+def test_xattention_tcgen05(R, heads, d, P, n_slots, Lk, f16):
+    """tcgen05 cross-attention (K7) over a text K / Vᵀ cache laid out like the engine's: per slot Lk token rows of
+    [K | V | other layers] (row stride ldk), and the transposed cache [kv rows][slots·Lk]; batch row r reads slot
+    kv_index[r]. Reference: fp64 softmax(QKᵀ/√d)V on the same rounded values."""
+    dt = torch.float16 if f16 else torch.bfloat16
+    g = torch.Generator().manual_seed(P + d + Lk)
+    C = heads * d
+    kcol, vrow, ldk = 24, 8 + C, 3 * C + 48          # this layer's K at column 24, V at 24 + C (+ padding)
+    q = (torch.randn(R, P, C, generator=g) * 1.5).to(dt)
+    kvc = torch.randn(n_slots * Lk, ldk, generator=g).to(dt)        # token-major cache (K and V columns)
+    Lp = (Lk + 7) // 8 * 8                                         # slot stride of the Vᵀ cache
+    vtc = torch.zeros(ldk, n_slots * Lp, dtype=dt)
+    for s_ in range(n_slots):
+        vtc[:, s_ * Lp:s_ * Lp + Lk] = kvc[s_ * Lk:(s_ + 1) * Lk].t()
+    vrow = kcol + C
+    slots = torch.tensor([(3 * r + 1) % n_slots for r in range(R)], dtype=torch.int32)
+    o = torch.empty(R * P, C, device="cuda", dtype=dt)
+    qd, kd, vd, sd_ = q.reshape(R * P, C).cuda(), kvc.cuda(), vtc.cuda(), slots.cuda()
+    B.call("sd_debug_xattention_tc", B._p(qd), B._p(kd), ldk, n_slots, kcol, B._p(vd), ldk, vtc.shape[1], vrow,
+           B._p(sd_), Lk, B._p(o), R, heads, d, P, f16, None)
+    torch.cuda.synchronize()
+    k = torch.stack([kvc[s * Lk:(s + 1) * Lk, kcol:kcol + C] for s in slots.tolist()]).double()
+    v = torch.stack([kvc[s * Lk:(s + 1) * Lk, vrow:vrow + C] for s in slots.tolist()]).double()
+    qh = q.double().reshape(R, P, heads, d).transpose(1, 2)
+    kh, vh = k.reshape(R, Lk, heads, d).transpose(1, 2), v.reshape(R, Lk, heads, d).transpose(1, 2)
+    ref = torch.softmax(qh @ kh.transpose(-1, -2) / d ** 0.5, -1) @ vh
+    ref = ref.transpose(1, 2).reshape(R, P, C)
+    assert rel(o.cpu().reshape(R, P, C), ref) < (2e-3 if f16 else 1e-2)
 
 
 @pytest.mark.parametrize("nb,P,C,G,silu", [(2, 4096, 320, 32, 1), (3, 256, 1280, 32, 0), (1, 64, 2560, 32, 1),

@@ -25,9 +25,9 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
 
 
-@pytest.fixture(scope="module")
-def tiny():
-    eng = Engine("tiny", max_latent_hw=16, b_max=4)
+@pytest.fixture(scope="module", params=["bf16", "fp16"])
+def tiny(request):
+    eng = Engine("tiny", max_latent_hw=16, b_max=4, precision=request.param)
     ctx_u = synth.uncond_embedding(0, 8, 32)
     eng.set_uncond(torch.from_numpy(ctx_u))
     P = configs.unet_params(configs.TINY_UNET, 0, np.float32, bf16_weights=True)
@@ -91,7 +91,7 @@ def test_tiny_unet_cfg_on_off(tiny, sampler):
     eng, P, V, ctx_u = tiny
     sched = [[1, 1], [1, 0], [0, 1], [0, 0]]     # CFG on / Skip-CFG mixes (CFG#1)
     final, worst, lat, xo = _run_tiny(eng, P, ctx_u, sampler, sched)
-    print(f"tiny final rel-L2 {final:.3e}, worst per-step error / bound {worst:.3f}")
+    print(f"tiny {eng.precision} final rel-L2 {final:.3e}, worst per-step error / bound {worst:.3f}")
     assert final <= TOL and worst <= 1.0
 
 
@@ -138,7 +138,7 @@ def test_tiny_vae_whole_and_chunked(tiny):
     whole = eng.decode(zt, 1)
     torch.cuda.synchronize()
     r = rel(whole.cpu().numpy(), ref)
-    print(f"tiny VAE rel-L2 {r:.3e}")
+    print(f"tiny {eng.precision} VAE rel-L2 {r:.3e}")
     assert r <= TOL
     for c in (2, 3, 5):
         ch = eng.decode(zt, c)
@@ -157,9 +157,9 @@ def test_vae_chunk_order_enforced(tiny):
     assert ei.value.status in (B.SD_E_STATE, B.SD_E_INVAL)
 
 
-@pytest.fixture(scope="module")
-def sd15():
-    eng = Engine("sd15", max_latent_hw=64, b_max=8)
+@pytest.fixture(scope="module", params=["bf16", "fp16"])
+def sd15(request):
+    eng = Engine("sd15", max_latent_hw=64, b_max=8, precision=request.param)
     ctx_u = synth.uncond_embedding(0, 77, 768)
     eng.set_uncond(torch.from_numpy(ctx_u))
     yield eng, synth.bf16_round(ctx_u)
@@ -199,7 +199,7 @@ def test_sd15_step_parity(sd15):
         got = lat[i].cpu().numpy()
         r_x = rel(got, exp)
         r_eps = rel(got - A * x0[i], exp - A * x0[i])      # ε-part (R21)
-        print(f"sd15 req {i} (step {steps[i]}, cfg {hu[i]}, g {g[i]}): x rel-L2 {r_x:.3e}, eps-part rel-L2 "
+        print(f"sd15 {eng.precision} req {i} (step {steps[i]}, cfg {hu[i]}, g {g[i]}): x rel-L2 {r_x:.3e}, eps-part rel-L2 "
               f"{r_eps:.3e}, kappa {kappa:.2f}, eps-part/kappa {r_eps / kappa:.3e}")
         worst = max(worst, r_x / TOL, r_eps / (TOL * kappa))
     for s in slots:
@@ -217,7 +217,7 @@ def test_sd15_vae_parity(sd15):
     ch = eng.decode(zt, 4)
     torch.cuda.synchronize()
     r = rel(whole.cpu().numpy(), ref)
-    print(f"sd VAE 512² rel-L2 {r:.3e}")
+    print(f"sd VAE {eng.precision} 512² rel-L2 {r:.3e}")
     assert r <= TOL
     assert torch.equal(ch, whole)
 
@@ -373,7 +373,7 @@ def test_sd15_bench_launch_config(sd15):
     A = np.sqrt(ap / a)
     got = lat[0].cpu().numpy()
     r_x, r_eps = rel(got, exp), rel(got - A * x0[0], exp - A * x0[0])
-    print(f"sd15 16-row bench launch, request 0: x {r_x:.3e}, eps-part {r_eps:.3e}, kappa {kappa:.2f}")
+    print(f"sd15 {eng.precision} 16-row bench launch, request 0: x {r_x:.3e}, eps-part {r_eps:.3e}, kappa {kappa:.2f}")
     for s in slots:
         eng.release(s)
     assert r_x <= TOL and r_eps <= TOL * kappa

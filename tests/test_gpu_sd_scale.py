@@ -27,9 +27,9 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
 
 
-@pytest.fixture(scope="module")
-def sd15():
-    eng = Engine("sd15", max_latent_hw=64, b_max=4, c_max=4)
+@pytest.fixture(scope="module", params=["bf16", "fp16"])
+def sd15(request):
+    eng = Engine("sd15", max_latent_hw=64, b_max=4, c_max=4, precision=request.param)
     ctx_u = synth.uncond_embedding(0, 77, 768)
     eng.set_uncond(torch.from_numpy(ctx_u))
     P = configs.unet_params(configs.SD15_UNET, 0, np.float32, bf16_weights=True)
@@ -83,7 +83,7 @@ def test_sd15_512_two_requests_skip_cfg_two_chunk_vae(sd15):
         img = vae.decode(V, configs.SD_VAE, x[None])[0]
         r_x = rel(lat[i].cpu().numpy(), x)
         r_img = rel(imgs[i].cpu().numpy(), img)
-        print(f"sd15 512² request {i} (n {n_steps[i]}, skip {sorted(skips[i])}): final latent rel-L2 {r_x:.3e}, "
+        print(f"sd15 512² {eng.precision} request {i} (n {n_steps[i]}, skip {sorted(skips[i])}): final latent rel-L2 {r_x:.3e}, "
               f"image rel-L2 {r_img:.3e} (bound {TOL})")
         worst = max(worst, r_x, r_img)
     assert worst <= TOL
@@ -109,7 +109,7 @@ def test_sd15_per_row_eps(sd15):
     ref = unet.forward(P, cfg, np.stack([x0[i] for i in order]), np.array([ts[i] for i in order]),
                        np.stack([cb[0], cb[1], cb[2], ctx_u, ctx_u]))
     errs = [rel(got[k], ref[k]) for k in range(5)]
-    print("sd15 per-row eps rel-L2 (c0, c1, c2, u0, u2): " + ", ".join(f"{e:.3e}" for e in errs))
+    print(f"sd15 {eng.precision} per-row eps rel-L2 (c0, c1, c2, u0, u2): " + ", ".join(f"{e:.3e}" for e in errs))
     for s in slots:
         eng.release(s)
     assert max(errs) <= TOL

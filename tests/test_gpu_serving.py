@@ -62,9 +62,10 @@ def _replay(plans, rows):
             assert all(got_d[x] == t for x in d_ids), w
 
 
+@pytest.mark.parametrize("precision", ["bf16", "fp16"])
 @pytest.mark.parametrize("cstar", [1, 2])
-def test_serving_tiny_matches_oracle_alone(cstar):
-    eng = Engine("tiny", max_latent_hw=8, b_max=4, c_max=3)
+def test_serving_tiny_matches_oracle_alone(cstar, precision):
+    eng = Engine("tiny", max_latent_hw=8, b_max=4, c_max=3, precision=precision)
     ctx_u = synth.uncond_embedding(0, 8, 32)
     eng.set_uncond(torch.from_numpy(ctx_u))
     tab = _table()
@@ -121,11 +122,13 @@ def test_serving_tiny_matches_oracle_alone(cstar):
     P = configs.unet_params(configs.TINY_UNET, 0, np.float32, bf16_weights=True)
     V = configs.vae_params(configs.TINY_VAE, 0, np.float32, bf16_weights=True)
     cu = synth.bf16_round(ctx_u)
-    # (2) oracle, end to end (noise → denoise → decode): this compounds the latent error through the
-    # decoder, so the bound is the north-star latent budget plus the VAE budget, 2e-2 + 1e-2
-    # (the north-star 2e-2 itself is asserted on latents and on images from identical
-    # latents in test_gpu_parity.py). Requests with > 4 steps are reported only.
-    worst = worst_long = 0.0
+    # (2) oracle, end to end (noise → denoise → decode), every request, north-star bound 2e-2 on images
+    # (fp16, the product precision). The bf16 mode sits at its own rounding floor on this 4-6-step g = 7.5
+    # tiny workload: the oracle with bf16 operand / storage rounding emulated reaches 2.0e-2 itself
+    # (tests/experiments/bf16_sites.py, reading R19a), so bf16 is held to the floor bound
+    # below — and, above, bitwise to its standalone path, which meets 2e-2 at SD scale (test_gpu_sd_scale).
+    bound = 2e-2 if precision == "fp16" else 2.5e-2
+    worst = 0.0
     total_skips = 0
     for i in range(n):
         A, U, Vt, skips, img = got[i]
@@ -136,13 +139,9 @@ def test_serving_tiny_matches_oracle_alone(cstar):
         x = pipeline.denoise(P, configs.TINY_UNET, xT, synth.bf16_round(embs[i]), cu, steps[i], 7.5 - 0.5 * (i % 3),
                              "ddim", skip=set(skips))
         ref = vae.decode(V, configs.TINY_VAE, x[None])[0]
-        r = np.linalg.norm(img - ref) / np.linalg.norm(ref)
-        if steps[i] <= 4:
-            worst = max(worst, r)
-        else:
-            worst_long = max(worst_long, r)
-    print(f"serving: worst image rel-L2 {worst:.3e} (4 steps), {worst_long:.3e} (5-6 steps); skips {total_skips}")
-    assert worst <= 3e-2
+        worst = max(worst, np.linalg.norm(img - ref) / np.linalg.norm(ref))
+    print(f"serving {precision}: worst image rel-L2 over all {n} requests (4-6 steps) {worst:.3e}; skips {total_skips}")
+    assert worst <= bound
     B.lib().sd_table_free(tab)
 
 
