@@ -358,10 +358,10 @@ sd_status sd_debug_conv3x3(const void* x, int32_t cin, const void* x2, int32_t c
  * (mma.sync flash kernel, any d <= 160, d % 8 == 0). */
 sd_status sd_debug_attention(const void* q, const void* k, const void* v, void* o, int32_t rows, int32_t heads,
                              int32_t d, int32_t Lq, int32_t Lk, void* stream);
-/* tcgen05 flash attention: qk bf16 [rows*P][2*heads*d] (q | k), vt bf16 [heads*d][rows*P] (V^T),
- * o bf16 [rows*P][heads*d]; d in {40, 64, 80}, P % 128 == 0. */
+/* tcgen05 flash attention: qk [rows*P][2*heads*d] (q | k), vt [heads*d][rows*P] (V^T), o [rows*P][heads*d];
+ * d in {40, 64, 80, 160}, P % 8 == 0 (ragged key blocks masked); use_f16 != 0: fp16 operands, else bf16. */
 sd_status sd_debug_attention_tc(const void* qk, const void* vt, void* o, int32_t rows, int32_t heads, int32_t d,
-                                int32_t P, void* stream);
+                                int32_t P, int32_t use_f16, void* stream);
 /* tcgen05 cross-attention over a text K / Vᵀ cache: q [rows*P][heads*d]; kc [n_slots*Lk][ldk]
  * with the K of head h at columns kcol + h*d; vtc [vt_rows][ld_keys] with Vᵀ of head h at rows vrow + h*d and
  * key j of slot s at column s*ceil8(Lk) + j (slot stride rounded up to 8 keys: 16-byte aligned TMA boxes); kv_index (device int32 [rows]) = slot per batch row; o [rows*P][heads*d].

@@ -147,7 +147,7 @@ SIGNATURES = {
     "sd_debug_set_gemm_cg": [I32],
     "sd_debug_set_conv_splits": [I32],
     "sd_debug_attention": [P, P, P, P, I32, I32, I32, I32, I32, P],
-    "sd_debug_attention_tc": [P, P, P, I32, I32, I32, I32, P],
+    "sd_debug_attention_tc": [P, P, P, I32, I32, I32, I32, I32, P],
     "sd_debug_xattention_tc": [P, P, I32, I32, I32, P, I32, I32, I32, P, I32, P, I32, I32, I32, I32, I32, P],
     "sd_debug_groupnorm": [P, P, I32, I32, I32, I32, P, P, C.c_float, I32, P],
     "sd_debug_layernorm": [P, P, I32, I32, P, P, C.c_float, P],

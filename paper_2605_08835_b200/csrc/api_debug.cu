@@ -170,12 +170,16 @@ extern "C" sd_status sd_debug_attention(const void* q, const void* k, const void
 }
 
 extern "C" sd_status sd_debug_attention_tc(const void* qk, const void* vt, void* o, int32_t rows, int32_t heads,
-                                           int32_t d, int32_t P, void* stream) {
+                                           int32_t d, int32_t P, int32_t use_f16, void* stream) {
   SD_REQUIRE(qk && vt && o && rows > 0 && heads > 0, "sd_debug_attention_tc: bad arguments");
   SD_REQUIRE(sd::attention_tc_supported(d, P, heads * d), "sd_debug_attention_tc: d in {40,64,80,160}, P % 8 == 0");
   SD_API_BEGIN
-  sd::attention_tc(static_cast<const bf16*>(qk), static_cast<const bf16*>(vt), static_cast<bf16*>(o), rows, heads, d,
-                   heads * d, P, static_cast<cudaStream_t>(stream));
+  if (use_f16)
+    sd::attention_tc(static_cast<const f16*>(qk), static_cast<const f16*>(vt), static_cast<f16*>(o), rows, heads, d,
+                     heads * d, P, static_cast<cudaStream_t>(stream));
+  else
+    sd::attention_tc(static_cast<const bf16*>(qk), static_cast<const bf16*>(vt), static_cast<bf16*>(o), rows, heads,
+                     d, heads * d, P, static_cast<cudaStream_t>(stream));
   SD_API_END
 }
 

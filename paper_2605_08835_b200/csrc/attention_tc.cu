@@ -81,6 +81,12 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, u
       : "memory");
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// two fp16 exponentials in one MUFU op (inputs / outputs packed half2)
+__device__ __forceinline__ uint32_t ex2_h2(uint32_t x) {
+  uint32_t y;
+  asm("ex2.approx.f16x2 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -112,6 +118,7 @@ struct AttnTcArgs {
   float scale_log2;
   int qcol0, kcol0, vrow0;  // column of head 0 in tq / tk; row of head 0's channels in tvt
   const int* kv_index;      // nullptr: self-attention
+  int ex2h;                 // fp16: packed f16x2 exponentials (SD_ATTN_EX2H, default on)
   int vt_slot;              // cross-attention: key columns per slot in tvt (Lk rounded up to 8: TMA needs the
                             // inner box start 16-byte aligned)
 };
@@ -123,6 +130,7 @@ __global__ void __launch_bounds__(64 + 128 * SPLIT, 3 - NB)
                    const __grid_constant__ CUtensorMap tk_t, const AttnTcArgs a) {
   const int P = a.P, Lk = a.Lk, ldo = a.ldo;
   constexpr bool is_f16 = F16;
+  const bool ex2h = a.ex2h != 0;
   const float scale_log2 = a.scale_log2;
   bf16* __restrict__ O = a.O;
   using A = TcAttn<D, NB, SPLIT, EMU, (OP == 4 || OP == 5) ? 1 : 0>;
@@ -320,6 +328,23 @@ __global__ void __launch_bounds__(64 + 128 * SPLIT, 3 - NB)
         const float alpha = upd ? ex2((m - mnew) * scale_log2) : 1.f;
         const float ms = mnew * scale_log2;
         float sum8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        if (F16 && ex2h) {
+          // fp16 P: the exponent pair goes through ONE packed MUFU op (ex2.approx.f16x2) — half the MUFU
+          // issue of the fp32 path, the bound of this softmax; x is rounded to fp16 first (|Δx| ≤ 2⁻¹¹·|x|),
+          // P comes out as the fp16 pair the PV MMA consumes (no pack)
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const uint32_t pa = ex2_h2(pack_f16(fmaf(__uint_as_float(ta[2 * i]), scale_log2, -ms),
+                                                fmaf(__uint_as_float(ta[2 * i + 1]), scale_log2, -ms)));
+            const uint32_t pb = ex2_h2(pack_f16(fmaf(__uint_as_float(tb[2 * i]), scale_log2, -ms),
+                                                fmaf(__uint_as_float(tb[2 * i + 1]), scale_log2, -ms)));
+            const float2 fa = __half22float2(*reinterpret_cast<const __half2*>(&pa));
+            const float2 fb = __half22float2(*reinterpret_cast<const __half2*>(&pb));
+            sum8[i & 7] += (fa.x + fa.y) + (fb.x + fb.y);
+            ta[i] = pa;
+            tb[i] = pb;
+          }
+        } else {
 #pragma unroll
         for (int i = 0; i < 16; ++i) {  // P packed in place: ta[i] ← bf16x2(p(ta[2i]), p(ta[2i+1]))
           const float x0 = fmaf(__uint_as_float(ta[2 * i]), scale_log2, -ms);
@@ -339,6 +364,7 @@ __global__ void __launch_bounds__(64 + 128 * SPLIT, 3 - NB)
           const float p1 = emu ? ex2_poly(x1) : ex2(x1);
           sum8[i & 7] += p0 + p1;
           tb[i] = pack16(p0, p1, is_f16);
+        }
         }
         const float sum = ((sum8[0] + sum8[1]) + (sum8[2] + sum8[3])) + ((sum8[4] + sum8[5]) + (sum8[6] + sum8[7]));
         l = l * alpha + sum;
@@ -531,6 +557,11 @@ __global__ void __launch_bounds__(64 + 128 * SPLIT, 3 - NB)
 }
 
 // host ------------------------------------------------------------------------------------------
+static bool env_on(const char* name) {
+  const char* e = getenv(name);
+  return !(e && e[0] == '0');
+}
+
 void make_tmap_2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_bytes, uint32_t box_in,
                   uint32_t box_out, bool is_f16, bool swz64 = false);
 
@@ -583,6 +614,8 @@ static void launch_tc(const TcSrc& sr, bf16* O, int ldo, int rows, int heads, in
   a.vrow0 = sr.vrow0;
   a.kv_index = sr.kv_index;
   a.vt_slot = (sr.Lk + 7) / 8 * 8;
+  static const int ex2h_env = env_on("SD_ATTN_EX2H") ? 1 : 0;
+  a.ex2h = ex2h_env;
   if (f16)
     launch_k(attn_tc_kernel<D, NB, SPLIT, EMU, OP, true>, grid, A::THREADS, A::SMEM, st, mq, mk, mvt, mq_t, mk_t, a);
   else
@@ -627,11 +660,6 @@ static int attn_nb() {
     if (v != 2) v = 1;
   }
   return v;
-}
-
-static bool env_on(const char* name) {
-  const char* e = getenv(name);
-  return !(e && e[0] == '0');
 }
 
 bool attention_tc_supported(int d, int P, int C) {

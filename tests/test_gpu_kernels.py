@@ -205,16 +205,18 @@ def test_attention_mma(R, heads, d, L, S):
 
 @pytest.mark.parametrize("R,heads,d,P", [(2, 8, 40, 256), (1, 8, 80, 384), (2, 10, 64, 128), (1, 8, 40, 4096),
                                          (2, 8, 160, 256), (3, 8, 160, 64), (2, 8, 40, 200), (2, 8, 80, 8)])
-def test_attention_tcgen05(R, heads, d, P):
+@pytest.mark.parametrize("f16", [0, 1])
+def test_attention_tcgen05(R, heads, d, P, f16):
     g = torch.Generator().manual_seed(P + d)
     C = heads * d
-    q, k, v = (bf(torch.randn(R, P, C, generator=g) * (1.5 if i == 0 else 1.0)) for i in range(3))
+    dt = torch.float16 if f16 else torch.bfloat16
+    q, k, v = ((torch.randn(R, P, C, generator=g) * (1.5 if i == 0 else 1.0)).to(dt) for i in range(3))
     qk = torch.cat([q, k], -1).reshape(R * P, 2 * C).contiguous().cuda()
     vt = v.reshape(R * P, C).t().contiguous().cuda()
-    o = torch.empty(R * P, C, device="cuda", dtype=torch.bfloat16)
-    B.call("sd_debug_attention_tc", B._p(qk), B._p(vt), B._p(o), R, heads, d, P, None)
+    o = torch.empty(R * P, C, device="cuda", dtype=dt)
+    B.call("sd_debug_attention_tc", B._p(qk), B._p(vt), B._p(o), R, heads, d, P, f16, None)
     torch.cuda.synchronize()
-    assert rel(o.cpu().reshape(R, P, C), _attn_ref(q.float(), k.float(), v.float(), heads)) < 1e-2
+    assert rel(o.cpu().reshape(R, P, C), _attn_ref(q.double(), k.double(), v.double(), heads)) < (2e-3 if f16 else 1e-2)
 
 
 @pytest.mark.parametrize("f16", [0, 1])

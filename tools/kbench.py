@@ -150,7 +150,22 @@ def main():
             ms = timeit(lambda: B.call("sd_debug_attention", B._p(q), B._p(k), B._p(v), B._p(o), R, heads, d, P, 77,
                                        B._p(cur())), args.reps)
             by = 2.0 * q.numel() * 2
-            print(json.dumps(dict(kind="xattn", shape=[R, heads, d, P, 77], ms=ms, gbs=by / ms / 1e6)), flush=True)
+            print(json.dumps(dict(kind="xattn_mma", shape=[R, heads, d, P, 77], ms=ms, gbs=by / ms / 1e6)), flush=True)
+            # the tcgen05 path: one slot per row, the engine's cache layout (K token-major, Vᵀ with 80-key slots)
+            for f16 in (0, 1):
+                dt = torch.float16 if f16 else torch.bfloat16
+                q_ = q.to(dt).reshape(R * P, C)
+                kc = torch.cat([k, v], -1).reshape(R * 77, 2 * C).to(dt).contiguous()
+                vtc = torch.zeros(2 * C, R * 80, device="cuda", dtype=dt)
+                for r in range(R):
+                    vtc[:, r * 80:r * 80 + 77] = kc[r * 77:(r + 1) * 77].t()
+                idx = torch.arange(R, device="cuda", dtype=torch.int32)
+                o_ = torch.empty(R * P, C, device="cuda", dtype=dt)
+                ms = timeit(lambda: B.call("sd_debug_xattention_tc", B._p(q_), B._p(kc), 2 * C, R, 0, B._p(vtc), 2 * C,
+                                           R * 80, C, B._p(idx), 77, B._p(o_), R, heads, d, P, f16, B._p(cur())),
+                            args.reps)
+                print(json.dumps(dict(kind="xattn_tc", dtype=str(dt), shape=[R, heads, d, P, 77], ms=ms,
+                                      gbs=by / ms / 1e6)), flush=True)
     if args.only in ("", "attn"):
         for i_, (R, heads, d, P) in enumerate([(16, 8, 40, 4096), (16, 8, 80, 1024), (16, 10, 64, 4096)]):
             if args.pick >= 0 and i_ != args.pick:
@@ -160,10 +175,14 @@ def main():
             vt = torch.randn(C, R * P, device="cuda").to(torch.bfloat16)
             o = torch.empty(R * P, C, device="cuda", dtype=torch.bfloat16)
             fl = 4.0 * R * heads * P * P * d
-            ms = timeit(lambda: B.call("sd_debug_attention_tc", B._p(qk), B._p(vt), B._p(o), R, heads, d, P,
-                                       B._p(cur())), args.reps)
-            print(json.dumps(dict(kind="attn_tc", shape=[R, heads, d, P], ms=ms, tflops=fl / ms / 1e9,
-                                  exp_per_s=R * heads * P * P / ms / 1e3)), flush=True)
+            for f16 in (0, 1):
+                dt = torch.float16 if f16 else torch.bfloat16
+                qk_, vt_ = qk.to(dt), vt.to(dt)
+                o_ = torch.empty(R * P, C, device="cuda", dtype=dt)
+                ms = timeit(lambda: B.call("sd_debug_attention_tc", B._p(qk_), B._p(vt_), B._p(o_), R, heads, d, P,
+                                           f16, B._p(cur())), args.reps)
+                print(json.dumps(dict(kind="attn_tc", dtype=str(dt), shape=[R, heads, d, P], ms=ms,
+                                      tflops=fl / ms / 1e9, exp_per_s=R * heads * P * P / ms / 1e3)), flush=True)
             q, k, v = (torch.randn(R, P, C, device="cuda").to(torch.bfloat16) for _ in range(3))
             ms = timeit(lambda: B.call("sd_debug_attention", B._p(q), B._p(k), B._p(v), B._p(o), R, heads, d, P, P,
                                        B._p(cur())), args.reps)

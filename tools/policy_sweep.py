@@ -60,6 +60,12 @@ def main():
                     help="also a burst trace: half the requests inside a window at 2·C₁ on a 0.5·C₁ background "
                          "(PAPER.md:315 burst traffic)")
     ap.add_argument("--arms", nargs="+", default=list(ARMS))
+    ap.add_argument("--c1-requests", type=int, default=16,
+                    help="requests of the saturation trace (all arriving at t = 0) that defines C1; CFG#3 of "
+                         "SURVEY 8(d) uses the full trace size")
+    ap.add_argument("--burst-span-s", type=float, default=0.0,
+                    help="burst window in seconds (CFG#3 / S:499: 10); 0 = half the requests at 2*C1")
+    ap.add_argument("--no-sim", action="store_true", help="skip the virtual-clock replay")
     ap.add_argument("--out", default="profiles/r01/policy_sweep.json")
     args = ap.parse_args()
     eng = Engine("sd15", max_latent_hw=64, b_max=8, c_max=2)
@@ -77,26 +83,31 @@ def main():
     print(f"profiled {len(tab)} table entries in {time.time() - t0:.1f} s; c* = {c_star}, C_max = {c_max}", flush=True)
     cal = [(i, 0, n) for (i, _, n) in serving.poisson_trace(16, 0.0, seed=11)]
     serving.run_trace(eng, h, cal, 64, 8, c_star, c_max, n_max=3)          # captures the CUDA graphs
-    _, m = serving.run_trace(eng, h, cal, 64, 8, c_star, c_max, n_max=3)
+    if args.c1_requests != 16:
+        cal = [(i, 0, n) for (i, _, n) in serving.poisson_trace(args.c1_requests, 0.0, seed=11)]
+    _, m = serving.run_trace(eng, h, cal, 64, 8, c_star, c_max, n_max=3, timeout_s=3600)
     c1 = m["images_per_s"]
     print(f"C1 = {c1:.3f} images/s", flush=True)
     res = dict(workload="SD-1.5-shaped 512² (latent 64×64), B_max 8, steps U{20..50}, g 7.5, DDIM, "
-                        f"{args.requests} Poisson requests per load, λ = ρ·C₁",
+                        f"{args.requests} Poisson requests per load, λ = ρ·C₁ (C₁ from {args.c1_requests} requests "
+                        f"at t = 0), precision {eng.precision}",
                c1_images_per_s=c1, c_star=c_star, c_max=c_max,
                table={f"{k}": v for k, v in sorted(tab.items())}, loads={})
     loads = [(str(rho), serving.poisson_trace(args.requests, rho * c1, seed=7)) for rho in args.rho]
     if args.burst:
         nb = args.requests // 2
-        loads.append(("burst", serving.burst_trace(args.requests, 0.5 * c1, frac=0.5,
-                                                   span_us=int(nb / (2.0 * c1) * 1e6), seed=7)))
+        span = args.burst_span_s * 1e6 if args.burst_span_s > 0 else nb / (2.0 * c1) * 1e6
+        loads.append(("burst", serving.burst_trace(args.requests, 0.5 * c1, frac=0.5, span_us=int(span), seed=7)))
     for rho, trace in loads:
         row = {}
         for name in args.arms:
             pol, abl, chunk = ARMS[name]
             cs, cm = (c_star, c_max) if chunk else (1, 1)
             t1 = time.time()
-            _, g = serving.run_trace(eng, h, trace, 64, 8, cs, cm, n_max=3, policy=pol, ablation=abl)
-            sim = simulate(h, trace, pol, abl, cs, cm)
+            _, g = serving.run_trace(eng, h, trace, 64, 8, cs, cm, n_max=3, policy=pol, ablation=abl,
+                                     timeout_s=3600)
+            sim = simulate(h, trace, pol, abl, cs, cm) if not args.no_sim else \
+                dict(images_per_s=0.0, mean_e2e_ms=0.0, p99_e2e_ms=0.0)
             row[name] = dict(gpu=g, virtual_clock=sim)
             print(f"rho {rho}: {name:26s} {g['images_per_s']:.3f} img/s, mean {g['mean_e2e_ms']:.0f} ms, "
                   f"P99 {g['p99_e2e_ms']:.0f} ms, skips {g['skipped_steps']} | sim {sim['images_per_s']:.3f} img/s, "
