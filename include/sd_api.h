@@ -213,6 +213,12 @@ sd_status sd_map_tasks(const int32_t* stages, int32_t n_stages, int32_t n_unet, 
 sd_status sd_chunk_choice(const sd_table* t, int32_t m, int32_t n, const int32_t* c_values, int32_t n_c,
                           int32_t lam_num, int32_t lam_den, int32_t* c_max_out, int32_t* c_star_out, double* cost_out);
 
+/* Saturation batch B_max ("identify the saturation batch size B_max based on the sub-linear
+ * scaling of throughput"; SPEC find_b_max): throughput(m) = m / tau^1(m, 0, 0) from the profiled table;
+ * B_max = the smallest m in [1, m_max) with throughput(m+1)/throughput(m) - 1 < eps (eps = eps_num /
+ * eps_den, SPEC: 0.05), else m_max. Exact (128-bit integers). SD_E_INVAL if a (1, m, 0, 0) row is missing. */
+sd_status sd_find_b_max(const sd_table* t, int32_t m_max, int32_t eps_num, int32_t eps_den, int32_t* b_max_out);
+
 /* Min-max partition of the ordered VAE work list into c chunks (R7): boundaries[0..c]. */
 sd_status sd_chunk_ranges(const int64_t* costs, int32_t n_items, int32_t c, int32_t* boundaries_out);
 

@@ -44,6 +44,20 @@ def select_c(costs_by_c):
     return min(sorted(costs_by_c), key=lambda c: (costs_by_c[c], c))
 
 
+def find_b_max(tau_solo_us_by_m, eps=Fraction(1, 20)):
+    """Saturation batch B_max ("the saturation batch size B_max based on the sub-linear
+    scaling of throughput"; SPEC find_b_max S:202-210): throughput(m) = m / τ(m, 0, 0); B_max = the
+    smallest m with throughput(m+1)/throughput(m) − 1 < ε; the largest profiled m if none (never
+    saturates). Exact in Fractions. tau_solo_us_by_m: {m: τ(m, 0, 0) µs} for m = 1 … m_max."""
+    ms = sorted(tau_solo_us_by_m)
+    assert ms == list(range(1, len(ms) + 1)), "profile m = 1 .. m_max"
+    thr = {m: Fraction(m, tau_solo_us_by_m[m]) for m in ms}
+    for m in ms[:-1]:
+        if thr[m + 1] / thr[m] - 1 < eps:
+            return m
+    return ms[-1]
+
+
 def find_c_max(concurrent_unet_us_by_c, solo_unet_us, num=5, den=100):
     """C_max = largest c whose concurrent UNet round ≤ (1 + 5 %)·solo; ≥ 1."""
     ok = [c for c, t in concurrent_unet_us_by_c.items() if t * den <= solo_unet_us * (den + num)]

@@ -115,6 +115,7 @@ SIGNATURES = {
     "sd_controller_decide": [P, I64, I32, C.POINTER(Directive)],
     "sd_controller_free": [P],
     "sd_chunk_ranges": [PI64, I32, I32, PI32],
+    "sd_find_b_max": [P, I32, I32, I32, PI32],
     "sd_chunk_choice": [P, I32, I32, PI32, I32, I32, I32, PI32, PI32, C.POINTER(C.c_double)],
     "sd_engine_warmup": [P, I32, I32, I32, I32, P],
     "sd_vae_decode_tiled": [P, P, I32, I32, I32, I32, P, P],

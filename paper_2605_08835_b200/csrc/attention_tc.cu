@@ -81,6 +81,23 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, u
       : "memory");
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// two 2^x on the FMA pipe with packed fp32 pairs (ex2_poly's method, FADD2 / FFMA2 for the float parts)
+__device__ __forceinline__ void ex2_poly2(float x0, float x1, float& y0, float& y1) {
+  x0 = fmaxf(x0, -120.f);
+  x1 = fmaxf(x1, -120.f);
+  float t0 = x0, t1 = x1;
+  fadd2(t0, t1, 12582912.f, 12582912.f);  // rint by the 1.5·2²³ magic add
+  float r0 = t0, r1 = t1;
+  fadd2(r0, r1, -12582912.f, -12582912.f);
+  float f0 = x0, f1 = x1;
+  fadd2(f0, f1, -r0, -r1);
+  float p0, p1;
+  ffma2(p0, p1, 0.05520857f, 0.05520857f, f0, f1, 0.24226530f, 0.24226530f);
+  ffma2(p0, p1, p0, p1, f0, f1, 0.69324851f, 0.69324851f);
+  ffma2(p0, p1, p0, p1, f0, f1, 1.0f, 1.0f);
+  y0 = __int_as_float(__float_as_int(p0) + ((__float_as_int(t0) - 0x4B400000) << 23));
+  y1 = __int_as_float(__float_as_int(p1) + ((__float_as_int(t1) - 0x4B400000) << 23));
+}
 // two fp16 exponentials in one MUFU op (inputs / outputs packed half2)
 __device__ __forceinline__ uint32_t ex2_h2(uint32_t x) {
   uint32_t y;
@@ -344,6 +361,30 @@ __global__ void __launch_bounds__(64 + 128 * SPLIT, 3 - NB)
             ta[i] = pa;
             tb[i] = pb;
           }
+        } else if (OP == 4) {
+          // packed fp32 pairs (FFMA2 / FADD2) and one pair in PER on the FMA pipe (ex2_poly2); the other
+          // pairs on MUFU. P packed in place: ta[i] ← 16-bit pair (p(ta[2i]), p(ta[2i+1]))
+          constexpr int PER = EMU > 0 ? EMU : 8;
+          float sp0[4] = {0.f, 0.f, 0.f, 0.f}, sp1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {  // i < 16: ta pairs, i ≥ 16: tb pairs
+            uint32_t (&src)[32] = i < 16 ? ta : tb;
+            const int ii = i & 15;
+            float x0, x1;
+            ffma2(x0, x1, __uint_as_float(src[2 * ii]), __uint_as_float(src[2 * ii + 1]), scale_log2, scale_log2,
+                  -ms, -ms);
+            float p0, p1;
+            if (i % PER == PER - 1) {
+              ex2_poly2(x0, x1, p0, p1);
+            } else {
+              p0 = ex2(x0);
+              p1 = ex2(x1);
+            }
+            fadd2(sp0[i & 3], sp1[i & 3], p0, p1);
+            src[ii] = pack16(p0, p1, is_f16);
+          }
+          sum8[0] = (sp0[0] + sp1[0]) + (sp0[1] + sp1[1]);
+          sum8[1] = (sp0[2] + sp1[2]) + (sp0[3] + sp1[3]);
         } else {
 #pragma unroll
         for (int i = 0; i < 16; ++i) {  // P packed in place: ta[i] ← bf16x2(p(ta[2i]), p(ta[2i+1]))
@@ -651,6 +692,16 @@ static int attn_emu() {
   }
   return v;
 }
+// SD_ATTN_EF=8|4|3: one softmax pair in EF computes its exponentials on the FMA pipe (d = 40, OP 4)
+static int attn_ef() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SD_ATTN_EF");
+    v = e ? atoi(e) : 8;
+    if (v != 4 && v != 3) v = 8;
+  }
+  return v;
+}
 // SD_ATTN_NB=1|2: S / P buffers at d = 40 (default 1: two CTAs per SM)
 static int attn_nb() {
   static int v = -1;
@@ -688,7 +739,14 @@ static void attention_tc16(const TcSrc& sr, bf16* O, int ldo, int rows, int head
         case 225: launch_tc<40, 2, 2, 0, 1>(sr, O, ldo, rows, heads, P, st, f16); break;
         case 126: launch_tc<40, 1, 2, 0, 2>(sr, O, ldo, rows, heads, P, st, f16); break;
         case 127: launch_tc<40, 1, 2, 0, 3>(sr, O, ldo, rows, heads, P, st, f16); break;
-        case 128: launch_tc<40, 1, 2, 0, 4>(sr, O, ldo, rows, heads, P, st, f16); break;  // SD_ATTN_EMU=8: P in TMEM
+        case 128:  // SD_ATTN_EMU=8 (default): P in TMEM; SD_ATTN_EF = pairs per FMA-pipe exp pair (8 / 4 / 3)
+          if (attn_ef() == 4)
+            launch_tc<40, 1, 2, 4, 4>(sr, O, ldo, rows, heads, P, st, f16);
+          else if (attn_ef() == 3)
+            launch_tc<40, 1, 2, 3, 4>(sr, O, ldo, rows, heads, P, st, f16);
+          else
+            launch_tc<40, 1, 2, 0, 4>(sr, O, ldo, rows, heads, P, st, f16);
+          break;
         default: launch_tc<40, 1, 2, 0>(sr, O, ldo, rows, heads, P, st, f16); break;
       }
       break;

@@ -473,6 +473,31 @@ extern "C" sd_status sd_chunk_choice(const sd_table* t, int32_t m, int32_t n, co
   SD_API_END
 }
 
+// Saturation batch (SPEC find_b_max): smallest m with thr(m+1)/thr(m) − 1 < ε, thr(m) = m/τ(m,0,0)
+extern "C" sd_status sd_find_b_max(const sd_table* t, int32_t m_max, int32_t eps_num, int32_t eps_den,
+                                   int32_t* b_max_out) {
+  SD_REQUIRE(t && b_max_out && m_max >= 1 && eps_den > 0 && eps_num > 0 && eps_num < eps_den,
+             "sd_find_b_max: bad args (need 0 < eps < 1, m_max >= 1)");
+  SD_API_BEGIN
+  std::vector<int64_t> tau(m_max + 1, 0);
+  for (int m = 1; m <= m_max; ++m) {
+    int64_t d;
+    if (!t->t.get(1, m, 0, 0, &tau[m], &d) || tau[m] <= 0)
+      throw std::invalid_argument("sd_find_b_max: table lacks (1, m, 0, 0) for m = " + std::to_string(m));
+  }
+  int best = m_max;
+  for (int m = 1; m < m_max; ++m) {
+    // thr(m+1)/thr(m) − 1 < ε  ⇔  (m+1)·τ(m)·den < m·τ(m+1)·(den + num)   (all positive)
+    typedef __int128 i128;
+    if ((i128)(m + 1) * tau[m] * eps_den < (i128)m * tau[m + 1] * (eps_den + eps_num)) {
+      best = m;
+      break;
+    }
+  }
+  *b_max_out = best;
+  SD_API_END
+}
+
 extern "C" sd_status sd_controller_create(const sd_controller_config* cfg, sd_controller** out) {
   SD_REQUIRE(cfg && out && cfg->c_star >= 1 && cfg->c_max >= cfg->c_star && cfg->window >= 2 &&
                  cfg->hysteresis >= 1 && cfg->up_den > 0 && cfg->down_den > 0,

@@ -237,13 +237,13 @@ __device__ __forceinline__ void stage_store(const GemmArgs& g, const CUtensorMap
 // o[0..32) += p[0..32) with 16-byte read-only loads (p 16-byte aligned: bias / temb rows are)
 __device__ __forceinline__ void add32(float* o, const float* p) {
   const float4* p4 = reinterpret_cast<const float4*>(p);
+  float4 v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __ldg(p4 + i);  // all loads in flight before the adds
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    const float4 v = __ldg(p4 + i);
-    o[4 * i] += v.x;
-    o[4 * i + 1] += v.y;
-    o[4 * i + 2] += v.z;
-    o[4 * i + 3] += v.w;
+    fadd2(o[4 * i], o[4 * i + 1], v[i].x, v[i].y);
+    fadd2(o[4 * i + 2], o[4 * i + 3], v[i].z, v[i].w);
   }
 }
 
@@ -376,7 +376,11 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
     }
     float o[32];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(rv[i]) * g.alpha;
+    for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(rv[i]);
+    if (g.alpha != 1.f) {  // warp-uniform; most GEMMs have α = 1
+#pragma unroll
+      for (int i = 0; i < 32; i += 2) fmul2(o[i], o[i + 1], g.alpha, g.alpha);
+    }
     const bool full32 = col + 32 <= g.N;
     if (g.bias && g.dbg != 2) {
       if (g.bias_per_row) {
@@ -411,7 +415,8 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
         const uint4 u = *reinterpret_cast<const uint4*>(buf + lane * 64 + ((i ^ sw) << 4));
         const bf16* e = reinterpret_cast<const bf16*>(&u);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) o[8 * i + k] += cvt16(e[k], F16);
+        for (int k = 0; k < 8; k += 2)
+          fadd2(o[8 * i + k], o[8 * i + k + 1], cvt16(e[k], F16), cvt16(e[k + 1], F16));
       }
     } else if (g.res && valid) {
       const bf16* rp = g.res + prow * g.ldr + col;

@@ -14,8 +14,12 @@
 // The reduction order depends only on (P, C, G) — never on the batch (I5) or on banding (I6).
 // Chunk size adapts to C (≈ 40 K elements per chunk).
 #include <algorithm>
+#include <mutex>
+#include <map>
 #include <cstdlib>
 #include <type_traits>
+
+#include <cooperative_groups.h>
 
 #include "common.cuh"
 #include "kernels_ew.h"
@@ -139,15 +143,13 @@ __device__ __forceinline__ const T* gn_src(const T* x, const T* x1, int V0, int 
   return x1 + (long)b * P * ld + (v - V0) * 8;
 }
 
+// partials of one (image b, pixel chunk ch) by one block (V, R); sh = [R][C] sums then [R][C] squares
 template <class T>
-__global__ void __launch_bounds__(512) gn_stats_kernel(const T* __restrict__ x, const T* __restrict__ x1, int V0, int P,
-                                                       int C, int G, int chunk_px, int c_base, int nch_total,
-                                                       GNPart* __restrict__ part) {
-  pdl_wait();
-  extern __shared__ float sh[];  // [R][C] sums, then [R][C] sums of squares
+__device__ __forceinline__ void gn_stats_item(const T* __restrict__ x, const T* __restrict__ x1, int V0, int P, int C,
+                                              int G, int chunk_px, int b, int ch, int nch_total,
+                                              GNPart* __restrict__ part, float* sh) {
   const int V = blockDim.x, R = blockDim.y;
   const int v = threadIdx.x, ry = threadIdx.y;
-  const int b = blockIdx.y, ch = blockIdx.x + c_base;
   const int p0 = ch * chunk_px, p1 = min(P, p0 + chunk_px);
   float s[8], q[8];
 #pragma unroll
@@ -209,6 +211,15 @@ __global__ void __launch_bounds__(512) gn_stats_kernel(const T* __restrict__ x, 
   }
 }
 
+template <class T>
+__global__ void __launch_bounds__(512) gn_stats_kernel(const T* __restrict__ x, const T* __restrict__ x1, int V0, int P,
+                                                       int C, int G, int chunk_px, int c_base, int nch_total,
+                                                       GNPart* __restrict__ part) {
+  pdl_wait();
+  extern __shared__ float sh[];  // [R][C] sums, then [R][C] sums of squares
+  gn_stats_item(x, x1, V0, P, C, G, chunk_px, blockIdx.y, blockIdx.x + c_base, nch_total, part, sh);
+}
+
 // finalize: one warp per (image, group)
 __global__ void gn_finalize_kernel(int P, int C, int G, int chunk_px, int nchunks, const GNPart* __restrict__ part,
                                    float eps, const float* __restrict__ gamma, const float* __restrict__ beta,
@@ -238,10 +249,9 @@ __device__ __forceinline__ float silu_tanh(float x) {
 // only when its pixel crosses into the next image); U pixel rows per thread per iteration, all
 // loads issued before any math; grid-stride over blocks of R·U pixels.
 template <class T>
-__global__ void __launch_bounds__(512) gn_apply_kernel(const T* __restrict__ x, const T* __restrict__ x1, int V0,
-                                                       long p_begin, long p_end, int P, int V,
-                                                       const float2* __restrict__ tab, int silu, T* __restrict__ y) {
-  pdl_wait();
+__device__ __forceinline__ void gn_apply_dev(const T* __restrict__ x, const T* __restrict__ x1, int V0, long p_begin,
+                                             long p_end, int P, int V, const float2* __restrict__ tab, int silu,
+                                             T* __restrict__ y) {
   constexpr int U = 4;
   const int v = threadIdx.x, R = blockDim.y;
   // source of this thread's channel vector; pixel p of the flat [B·P] range sits at row p of it
@@ -281,6 +291,57 @@ __global__ void __launch_bounds__(512) gn_apply_kernel(const T* __restrict__ x, 
   }
 }
 
+template <class T>
+__global__ void __launch_bounds__(512) gn_apply_kernel(const T* __restrict__ x, const T* __restrict__ x1, int V0,
+                                                       long p_begin, long p_end, int P, int V,
+                                                       const float2* __restrict__ tab, int silu, T* __restrict__ y) {
+  pdl_wait();
+  gn_apply_dev(x, x1, V0, p_begin, p_end, P, V, tab, silu, y);
+}
+
+// GroupNorm in ONE cooperative launch (the whole-tensor path, group_norm / group_norm2): the three
+// phases of the three-kernel path, separated by grid-wide barriers instead of kernel boundaries —
+//   1. partials of every (image, chunk) item, block-strided (gn_stats_item),
+//   2. one warp per (image, group): gn_merge_group → the affine table,
+//   3. the apply, grid-stride (gn_apply_dev; x is re-read, mostly from L2).
+// Identical arithmetic and reduction order to the three-kernel path (bitwise equal results); 2 launch
+// boundaries fewer per GroupNorm. Needs every block co-resident (cooperative launch, grid ≤ occupancy).
+template <class T>
+__global__ void __launch_bounds__(512) gn_fused_kernel(const T* __restrict__ x, const T* __restrict__ x1, int V0,
+                                                       int B, int P, int C, int G, int chunk_px, int nchunks,
+                                                       GNPart* __restrict__ part, float2* __restrict__ tab,
+                                                       const float* __restrict__ gamma, const float* __restrict__ beta,
+                                                       float eps, int silu, T* __restrict__ y) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ float sh[];
+  pdl_wait();
+  const int items = nchunks * B;
+  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+    gn_stats_item(x, x1, V0, P, C, G, chunk_px, it / nchunks, it % nchunks, nchunks, part, sh);
+    __syncthreads();  // the shared partial sums are rewritten by the next item
+  }
+  __threadfence();
+  grid.sync();
+  {
+    const int tid = threadIdx.y * blockDim.x + threadIdx.x, lane = tid & 31;
+    const int nwf = (blockDim.x * blockDim.y) >> 5;  // full warps of the block
+    if ((tid >> 5) < nwf) {
+      for (int pr = blockIdx.x * nwf + (tid >> 5); pr < B * G; pr += gridDim.x * nwf) {
+        const int b = pr / G, g = pr % G;
+        const GNPart* pb = part + (long)b * nchunks * G + g;
+        gn_merge_group(
+            P, C, G, chunk_px, nchunks,
+            [&](int k) { return __ldcg(reinterpret_cast<const float2*>(pb + (long)k * G)); }, eps, gamma, beta,
+            tab + (long)b * C, g, lane);
+      }
+    }
+  }
+  __threadfence();
+  grid.sync();
+  gn_apply_dev(x, x1, V0, 0L, (long)B * P, P, C / 8, tab, silu, y);
+}
+
 // workspace: [partials] [affine table]
 static size_t gn_part_bytes(int B, int P, int G) {
   return ((size_t)B * cdiv(P, 16) * G * sizeof(GNPart) + 255) & ~size_t(255);
@@ -301,6 +362,67 @@ static void gn_finalize(int B, int P, int C, int G, int cp, void* ws, float eps,
   SD_CHECK_LAUNCH();
 }
 
+// SiLU form of the apply: 0 none, 1 ex2 + rcp, 2 one MUFU tanh (bf16 only; SD_SILU_TANH=0 disables)
+template <class T>
+static int gn_silu_mode(bool silu) {
+  static int st_env = -1;
+  if (st_env < 0) {
+    const char* e = getenv("SD_SILU_TANH");
+    st_env = e ? atoi(e) : 1;
+  }
+  return !silu ? 0 : (std::is_same<T, bf16>::value && st_env) ? 2 : 1;
+}
+
+// SD_GN_FUSED=0: the three-launch path (stats → finalize → apply) for whole tensors too
+static bool gn_fused_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SD_GN_FUSED");
+    v = !(e && e[0] == '0');
+  }
+  return v != 0;
+}
+
+template <class T>
+static void gn_fused(const T* x, const T* x1, int C0, T* y, int B, int P, int C, int G, int cp, void* ws,
+                     const float* gamma, const float* beta, float eps, bool silu, cudaStream_t st) {
+  const dim3 blk = gn_stats_block(C);
+  const size_t sh = (size_t)blk.x * blk.y * 8 * 2 * sizeof(float);
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, int> occ;  // (block threads, smem) → co-resident blocks per SM
+  int per_sm;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto key = std::make_pair((int)(blk.x * blk.y), (int)sh);
+    auto it = occ.find(key);
+    if (it == occ.end()) {
+      int n = 0;
+      SD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, gn_fused_kernel<T>, blk.x * blk.y, sh));
+      it = occ.emplace(key, std::max(n, 1)).first;
+    }
+    per_sm = it->second;
+  }
+  static int sms = 0;
+  if (!sms) SD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  const int nchunks = cdiv(P, cp);
+  const long rows = (long)blk.y * 4;
+  const long want = std::max<long>((long)nchunks * B, ((long)B * P + rows - 1) / rows);
+  const int grid = (int)std::min<long>(want, (long)sms * per_sm);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = blk;
+  cfg.dynamicSmemBytes = sh;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  SD_CUDA(cudaLaunchKernelEx(&cfg, gn_fused_kernel<T>, x, x1, C0 / 8, B, P, C, G, cp, nchunks, gn_parts(ws),
+                             gn_tab(ws, B, P, G), gamma, beta, eps, gn_silu_mode<T>(silu), y));
+  SD_CHECK_LAUNCH();
+}
+
 template <class T>
 static void gn_apply(const T* x, const T* x1, int C0, T* y, long p0, long p1, int B, int P, int C, const float2* tab,
                      bool silu, cudaStream_t st) {
@@ -313,14 +435,8 @@ static void gn_apply(const T* x, const T* x1, int C0, T* y, long p0, long p1, in
   const long want = (p1 - p0 + rows - 1) / rows;
   const int grid = (int)std::min<long>(want, (long)sms * (2048 / (blk.x * blk.y)));
   // bf16 outputs: SiLU through one MUFU tanh instead of ex2 + rcp (the apply pass was partly
-  // MUFU-bound: 2 MUFU ops per element); fp32 outputs (the 1e-4 parity mode) keep the exact form.
-  // SD_SILU_TANH=0 restores ex2 + rcp for bf16 too.
-  static int st_env = -1;
-  if (st_env < 0) {
-    const char* e = getenv("SD_SILU_TANH");
-    st_env = e ? atoi(e) : 1;
-  }
-  const int sm = !silu ? 0 : (std::is_same<T, bf16>::value && st_env) ? 2 : 1;
+  // MUFU-bound: 2 MUFU ops per element); fp16 / fp32 outputs keep the exact form.
+  const int sm = gn_silu_mode<T>(silu);
   launch_k(gn_apply_kernel<T>, grid, blk, 0, st, x, x1, C0 / 8, p0, p1, P, C / 8, tab, sm, y);
   SD_CHECK_LAUNCH();
   (void)B;
@@ -371,6 +487,10 @@ void group_norm2(const T* x0, int C0, const T* x1, int C1, T* y, int B, int P, i
   check_gn(C, G);
   if (x1 && (C0 % 8 || C1 % 8)) throw CudaError("group_norm2: source channels must be multiples of 8");
   const int cp = gn_chunk_px(C);
+  if (gn_fused_on() && (long)B * P < (1L << 31)) {
+    gn_fused(x0, x1, C0, y, B, P, C, G, cp, ws, gamma, beta, eps, silu, st);
+    return;
+  }
   gn_stats(x0, x1, C0, B, P, C, G, 0, cdiv(P, cp), ws, st);
   gn_finalize(B, P, C, G, cp, ws, eps, gamma, beta, st);
   gn_apply(x0, x1, C0, y, 0, (long)B * P, B, P, C, gn_tab(ws, B, P, G), silu, st);

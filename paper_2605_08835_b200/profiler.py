@@ -132,3 +132,24 @@ def chunk_choice(tab, c_values, m, n=1, lam=(1, 2)):
     finally:
         B.lib().sd_table_free(h)
     return cmax.value, cstar.value, {c: cost[i] for i, c in enumerate(c_values)}
+
+
+def solo_unet_table(prof, m_max, reps=3):
+    """τ^1(m, 0, 0) for m = 1 … m_max (one UNet step of m requests with CFG, no decode), µs: the input of
+    the B_max saturation rule."""
+    tab = {}
+    for m in range(1, m_max + 1):
+        vals = sorted(prof._stage(1, m, 0, 0)[0] for _ in range(reps))
+        tab[(1, m, 0, 0)] = (vals[len(vals) // 2], 0)
+    return tab
+
+
+def find_b_max(tab, m_max, eps=(1, 20)):
+    """B_max by sd_find_b_max on a table holding (1, m, 0, 0) for m = 1 … m_max."""
+    h = to_table_handle(tab)
+    try:
+        out = C.c_int32()
+        B.call("sd_find_b_max", h, m_max, eps[0], eps[1], C.byref(out))
+    finally:
+        B.lib().sd_table_free(h)
+    return out.value

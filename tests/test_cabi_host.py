@@ -427,3 +427,17 @@ def test_chunk_choice_bitexact_vs_oracle():
         assert cmax == sched.find_c_max({c: F(tab[(c, m, n, 0)][0], c) for c in cs}, tu1), trial
         for c in cs:
             assert cost[c] == pytest.approx(float(L[c]), rel=1e-12, abs=1e-15)
+
+
+def test_find_b_max_bitexact_vs_oracle():
+    """sd_find_b_max equals oracle.sched.find_b_max on random sub-linear profiles."""
+    from fractions import Fraction
+    from paper_2605_08835_b200 import profiler
+    rng = np.random.default_rng(9)
+    for trial in range(300):
+        mm = int(rng.integers(2, 17))
+        h, a = int(rng.integers(0, 60_000)), int(rng.integers(1_000, 20_000))
+        tau = {m: h + a * m + int(rng.integers(0, 3_000)) for m in range(1, mm + 1)}
+        tab = {(1, m, 0, 0): (t, 0) for m, t in tau.items()}
+        for eps in ((1, 20), (1, 10), (3, 100)):
+            assert profiler.find_b_max(tab, mm, eps) == sched.find_b_max(tau, Fraction(*eps)), (trial, eps)

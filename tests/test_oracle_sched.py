@@ -206,3 +206,17 @@ def test_alg1_hand_trace():
     assert sched.solve_exact(tab, w["M"], w["N"], w["K"], lim) == (e["cost"], e["time"],
                                                                     tuple(tuple(s) for s in e["stages"]))
     assert sched.plan_window(tab, w["M"], w["N"], w["K"], mode="alg1") == tuple(tuple(s) for s in r["stages"])
+
+
+def test_find_b_max_closed_forms():
+    """B_max rule pinned by closed forms: with τ(m) = h + a·m the throughput
+    ratio is (m+1)(h + a·m) / (m(h + a·m + a)); the first m where it drops below 1 + ε is found by hand for
+    h = 40, a = 10, ε = 1/20: m = 2 gives 3·60/(2·70) = 9/7 > 1.05, …, m = 6: 7·100/(6·110) = 70/66 =
+    1.0606 > 1.05, m = 7: 8·110/(7·120) = 88/84 = 1.0476 < 1.05 → B_max = 7. A linear τ = a·m (no fixed cost)
+    saturates immediately (ratio 1) → 1; a constant τ has ratio (m+1)/m, which first drops below 1.05 at
+    m = 21 (22/21; 21/20 = 1.05 is not below) → 21, or the scan ceiling when that is smaller."""
+    aff = {m: 40 + 10 * m for m in range(1, 17)}
+    assert sched.find_b_max(aff) == 7
+    assert sched.find_b_max({m: 7 * m for m in range(1, 9)}) == 1
+    assert sched.find_b_max({m: 100 for m in range(1, 13)}) == 12
+    assert sched.find_b_max({m: 100 for m in range(1, 31)}) == 21      # 21/20 = 1.05 is not < 1.05
