@@ -245,6 +245,10 @@ typedef struct {
   int32_t n_res;
   const int32_t* res_hw;
   const sd_table* const* res_tables;
+  /* SM partitioning of UNet ∥ VAE: 0 = the two streams differ only in priority
+   * (UNet high, VAE low); > 0 = the VAE chunks run in a green context of vae_sms SMs (rounded up by the
+   * driver, multiples of 8) and the UNet rounds in one of the remaining SMs (sd_sm_partition_create). */
+  int32_t vae_sms;
 } sd_serve_config;
 /* Serving policies (§IV Baselines; semantics in oracle/serving.py):
  *  SYNERDIFF  the method: threshold-aware plan, Skip-CFG, VAE chunking, feedback controller;
@@ -285,6 +289,15 @@ sd_status sd_poll(sd_engine* e, sd_completion* out, int32_t max, int32_t* n_out,
  * image_host / skipped_steps of that completion are invalid afterwards. */
 sd_status sd_release(sd_engine* e, uint64_t id);
 sd_status sd_serve_stop(sd_engine* e);                     /* drains nothing; stops the thread    */
+/* Two streams on disjoint SM partitions (CUDA green contexts): vae_stream on vae_sms SMs (rounded up by
+ * the driver to its granularity, 8 on sm_90+), unet_stream on the rest; the counts actually provisioned are
+ * returned. Every kernel of the library sizes its persistent / cooperative grid by the SM count of the
+ * stream it is launched on. The streams belong to the partition object (destroyed with it).
+ * SD_E_INVAL / SD_E_CUDA if the driver has no green contexts or the split fails. */
+typedef struct sd_partition sd_partition;
+sd_status sd_sm_partition_create(int32_t cuda_device, int32_t vae_sms, sd_partition** out, void** unet_stream,
+                                 void** vae_stream, int32_t* unet_sms, int32_t* vae_sms_out);
+sd_status sd_sm_partition_destroy(sd_partition* p);
 /* Controller trajectory (one record per planned window, in order): start / end µs, M, N, K, the level
  * and chunk count the window ran with, the waiting queue the controller then observed, its new level
  * and chunk count. Any output array may be NULL. Call before sd_serve_stop. */

@@ -49,7 +49,7 @@ class ServeConfig(C.Structure):
                 ("c_star", C.c_int32), ("ctl", ControllerConfig), ("table", C.c_void_p), ("latent_hw", C.c_int32),
                 ("trace_seed", C.c_uint64), ("n_max", C.c_int32), ("policy", C.c_int32), ("ablation", C.c_int32),
                 ("dyn_window_us", C.c_int64), ("n_res", C.c_int32), ("res_hw", C.POINTER(C.c_int32)),
-                ("res_tables", C.POINTER(C.c_void_p))]
+                ("res_tables", C.POINTER(C.c_void_p)), ("vae_sms", C.c_int32)]
 
 
 SD_POLICY_SYNERDIFF, SD_POLICY_NAIVE, SD_POLICY_DYNAMIC, SD_POLICY_SERIAL = 0, 1, 2, 3
@@ -137,6 +137,8 @@ SIGNATURES = {
     "sd_vserve_results": [P, PI64, PI64, PI32, PI64, PI32],
     "sd_vserve_trajectory": [P, I32, PI32, PI32, PI32, PI32],
     "sd_vserve_free": [P],
+    "sd_sm_partition_create": [I32, I32, C.POINTER(P), C.POINTER(P), C.POINTER(P), PI32, PI32],
+    "sd_sm_partition_destroy": [P],
     "sd_map_tasks": [PI32, I32, I32, C.POINTER(C.c_uint64), PI32, PI32, C.POINTER(C.c_uint8), I32,
                      C.POINTER(C.c_uint64), PI64, PI32, C.POINTER(C.c_uint8), PI32],
     "sd_serve_window_plan": [P, I32, PI32, I32, PI32, C.POINTER(LoggedUnet), I32, PI32, C.POINTER(LoggedDecode), I32,

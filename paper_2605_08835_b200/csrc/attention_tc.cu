@@ -135,7 +135,7 @@ struct AttnTcArgs {
   float scale_log2;
   int qcol0, kcol0, vrow0;  // column of head 0 in tq / tk; row of head 0's channels in tvt
   const int* kv_index;      // nullptr: self-attention
-  int ex2h;                 // fp16: packed f16x2 exponentials (SD_ATTN_EX2H, default on)
+  int ex2h;                 // fp16: packed f16x2 exponentials (SD_ATTN_EX2H=1; default off)
   int vt_slot;              // cross-attention: key columns per slot in tvt (Lk rounded up to 8: TMA needs the
                             // inner box start 16-byte aligned)
 };
@@ -655,7 +655,9 @@ static void launch_tc(const TcSrc& sr, bf16* O, int ldo, int rows, int heads, in
   a.vrow0 = sr.vrow0;
   a.kv_index = sr.kv_index;
   a.vt_slot = (sr.Lk + 7) / 8 * 8;
-  static const int ex2h_env = env_on("SD_ATTN_EX2H") ? 1 : 0;
+  // SD_ATTN_EX2H=1: fp16 exponentials in ex2.approx.f16x2 — it lowers to two MUFU.EX2.F16 (no issue saving)
+  // and measured slower (d = 40: 0.755 vs 0.728 ms), so off by default
+  static const int ex2h_env = getenv("SD_ATTN_EX2H") && getenv("SD_ATTN_EX2H")[0] == '1' ? 1 : 0;
   a.ex2h = ex2h_env;
   if (f16)
     launch_k(attn_tc_kernel<D, NB, SPLIT, EMU, OP, true>, grid, A::THREADS, A::SMEM, st, mq, mk, mvt, mq_t, mk_t, a);

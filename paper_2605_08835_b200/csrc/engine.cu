@@ -497,8 +497,11 @@ void build_engine(Engine* e) {
   e->use_graphs = !(ng && ng[0] == '1');
   const char* at = getenv("SD_ATTN_TC");
   e->use_attn_tc = !(at && at[0] == '0') && !e->f32;
-  const char* xt = getenv("SD_XATTN_TC");  // SD_XATTN_TC=0: cross-attention on the mma.sync kernel
-  e->use_xattn_tc = e->use_attn_tc && !(xt && xt[0] == '0');
+  // SD_XATTN_TC=1: cross-attention on the tcgen05 kernel. Off by default: with 77 keys one CTA does a
+  // single 128×128 score tile, and the per-CTA setup (TMEM alloc, barriers, K/V load) outweighs it — the
+  // mma.sync kernel that keeps K/V resident across query tiles measured faster (64²: 55 vs 71 µs)
+  const char* xt = getenv("SD_XATTN_TC");
+  e->use_xattn_tc = e->use_attn_tc && (xt && xt[0] == '1');
 }
 
 // ---------------------------------------------------------------------------------------------

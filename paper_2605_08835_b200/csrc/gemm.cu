@@ -759,7 +759,7 @@ static void launch(const CUtensorMap* m, const GemmArgs& a, cudaStream_t st) {
     attr_set = true;
   }
   const int total = a.m_tiles * a.n_tiles * a.splits;
-  int workers = num_sms() / CG;
+  int workers = stream_sms(st) / CG;
   if (total < workers) workers = total;
   if (workers <= 0) return;
   cudaLaunchConfig_t cfg{};

@@ -75,6 +75,13 @@ size_t gemm_split_ws_bytes(const GemmDescT<f16>& d);
 // M tiles of a conv3 launch whose output rows lie in [y0, y1) of image 0 (used for bands).
 void conv3_tile_geometry(int B, int H, int W, int* wt, int* ht, int* bt);
 int num_sms();
+// SMs a kernel launched on `st` can use: the partition's count for an SM-partition stream (smpart.cpp,
+// green contexts), else num_sms(). Persistent and cooperative grids are sized by it.
+int stream_sms(cudaStream_t st);
+struct Partition;
+Partition* partition_create(int device, int vae_sms);
+void partition_destroy(Partition* p);
+cudaStream_t partition_stream(Partition* p, int i);  // 0 = the vae_sms group, 1 = the rest
 extern int g_cg_override;
 
 }  // namespace sd

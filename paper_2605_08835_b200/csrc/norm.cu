@@ -22,6 +22,7 @@
 #include <cooperative_groups.h>
 
 #include "common.cuh"
+#include "kernels.h"
 #include "kernels_ew.h"
 
 namespace sd {
@@ -402,8 +403,7 @@ static void gn_fused(const T* x, const T* x1, int C0, T* y, int B, int P, int C,
     }
     per_sm = it->second;
   }
-  static int sms = 0;
-  if (!sms) SD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  const int sms = stream_sms(st);  // cooperative: every block co-resident on the stream's SMs
   const int nchunks = cdiv(P, cp);
   const long rows = (long)blk.y * 4;
   const long want = std::max<long>((long)nchunks * B, ((long)B * P + rows - 1) / rows);

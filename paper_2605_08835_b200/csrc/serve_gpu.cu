@@ -72,6 +72,7 @@ struct Server {
   std::map<uint64_t, STask*> owned;
   std::chrono::steady_clock::time_point t0;
   cudaStream_t hi = nullptr, lo = nullptr;
+  Partition* part = nullptr;  // cfg.vae_sms > 0: hi / lo are green-context streams on disjoint SMs
   cudaEvent_t ev_hi = nullptr, ev_lo = nullptr;
   int32_t counters[4] = {0, 0, 0, 0};  // waiting, decode-pending, active, completed
   std::vector<int32_t> global;
@@ -264,10 +265,16 @@ extern "C" sd_status sd_serve_start(sd_engine* e, const sd_serve_config* cfg) {
   S->loop.ctl.cfg.c_star = cfg->c_star;
   S->loop.ctl.c = cfg->c_star;
   SD_CUDA(cudaSetDevice(e->e.device));
-  int lo_p, hi_p;
-  SD_CUDA(cudaDeviceGetStreamPriorityRange(&lo_p, &hi_p));
-  SD_CUDA(cudaStreamCreateWithPriority(&S->hi, cudaStreamNonBlocking, hi_p));
-  SD_CUDA(cudaStreamCreateWithPriority(&S->lo, cudaStreamNonBlocking, lo_p));
+  if (cfg->vae_sms > 0) {
+    S->part = partition_create(e->e.device, cfg->vae_sms);
+    S->lo = partition_stream(S->part, 0);
+    S->hi = partition_stream(S->part, 1);
+  } else {
+    int lo_p, hi_p;
+    SD_CUDA(cudaDeviceGetStreamPriorityRange(&lo_p, &hi_p));
+    SD_CUDA(cudaStreamCreateWithPriority(&S->hi, cudaStreamNonBlocking, hi_p));
+    SD_CUDA(cudaStreamCreateWithPriority(&S->lo, cudaStreamNonBlocking, lo_p));
+  }
   SD_CUDA(cudaEventCreateWithFlags(&S->ev_hi, cudaEventDisableTiming));
   SD_CUDA(cudaEventCreateWithFlags(&S->ev_lo, cudaEventDisableTiming));
   const size_t hw = (size_t)e->e.cfg.max_latent_hw * e->e.cfg.max_latent_hw;  // any request resolution
@@ -400,8 +407,12 @@ extern "C" sd_status sd_serve_stop(sd_engine* e) {
   cudaFree(S->emb_dev);
   cudaEventDestroy(S->ev_hi);
   cudaEventDestroy(S->ev_lo);
-  cudaStreamDestroy(S->hi);
-  cudaStreamDestroy(S->lo);
+  if (S->part) {
+    partition_destroy(S->part);  // owns hi / lo
+  } else {
+    cudaStreamDestroy(S->hi);
+    cudaStreamDestroy(S->lo);
+  }
   const std::string err = S->error;
   delete S;
   e->e.server = nullptr;

@@ -23,12 +23,23 @@ def _rows_of(m, k):
 
 
 class Profiler:
-    def __init__(self, eng, h=64, w=64, b_max=8, reps=2):
+    def __init__(self, eng, h=64, w=64, b_max=8, reps=2, vae_sms=0):
+        """vae_sms > 0: profile on the green-context SM partition the server uses with the same setting
+        (sd_sm_partition_create: VAE stream on vae_sms SMs, UNet stream on the rest)."""
         self.eng, self.h, self.w, self.b_max, self.reps = eng, h, w, b_max, reps
         dev = torch.device(f"cuda:{eng.device}")
-        lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, -1)
-        self.hi = torch.cuda.Stream(device=dev, priority=-1)
-        self.lo = torch.cuda.Stream(device=dev, priority=0)
+        self.part = None
+        if vae_sms > 0:
+            part, us, vs = C.c_void_p(), C.c_void_p(), C.c_void_p()
+            nu, nv = C.c_int32(), C.c_int32()
+            B.call("sd_sm_partition_create", eng.device, vae_sms, C.byref(part), C.byref(us), C.byref(vs),
+                   C.byref(nu), C.byref(nv))
+            self.part, self.partition_sms = part, (nu.value, nv.value)
+            self.hi = torch.cuda.ExternalStream(us.value, device=dev)
+            self.lo = torch.cuda.ExternalStream(vs.value, device=dev)
+        else:
+            self.hi = torch.cuda.Stream(device=dev, priority=-1)
+            self.lo = torch.cuda.Stream(device=dev, priority=0)
         g = torch.Generator(device="cpu").manual_seed(0)
         self.lat = [torch.randn(4, h, w, generator=g).to(dev) for _ in range(b_max)]
         self.lat_save = [t.clone() for t in self.lat]
@@ -41,6 +52,10 @@ class Profiler:
     def close(self):
         for s in self.slots:
             self.eng.release(s)
+        if self.part is not None:
+            torch.cuda.synchronize()
+            B.call("sd_sm_partition_destroy", self.part)
+            self.part = None
 
     def _stage(self, c, m, n, k):
         """One stage (m, n, k) at granularity c; returns (τ µs, δ µs)."""

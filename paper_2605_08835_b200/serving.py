@@ -46,16 +46,18 @@ def p99(values):
 
 def run_trace(eng, table_h, trace, latent_hw=64, b_max=8, c_star=1, c_max=2, dp_mode=0, guidance=7.5,
               trace_seed=7, ctl=None, timeout_s=600, n_max=None, policy="synerdiff", ablation=0,
-              dyn_window_us=500_000, res_tables=None, trajectory=None):
+              dyn_window_us=500_000, res_tables=None, trajectory=None, vae_sms=0):
     """Serve `trace` [(id, arrival_us, n_steps[, latent_hw])] on `eng`; returns per-request records and
     metrics. `res_tables` {latent_hw: table handle} makes the server mixed-resolution. A list passed as
     `trajectory` receives the controller trajectory (one dict per planned window, sd_serve_window_log).
     Arrival times are relative to sd_serve_start; all requests are submitted up front and admitted
     by the server when their arrival time has passed. `policy` selects SynerDiff or one of the
-    paper's baselines, `ablation` the SD_ABL_* bits."""
+    paper's baselines, `ablation` the SD_ABL_* bits. `vae_sms` > 0
+    runs the VAE chunks and the UNet rounds on disjoint green-context SM partitions (sd_serve_config)."""
     ctl = ctl or B.ControllerConfig(c_star, c_max, 10, 3, 1, 2, -1, 5)
     cfg = B.ServeConfig(b_max, 1, 10, dp_mode, c_star, ctl, table_h, latent_hw, trace_seed, n_max or 0,
                         B.POLICIES[policy], ablation, dyn_window_us)
+    cfg.vae_sms = vae_sms
     if res_tables:
         keys = sorted(res_tables)
         hw_arr = (C.c_int32 * len(keys))(*keys)

@@ -247,3 +247,57 @@ def test_serving_mixed_resolutions_tiny():
     eng.close()
     B.lib().sd_table_free(t8)
     B.lib().sd_table_free(t16)
+
+
+def test_serving_sm_partition_tiny():
+    """UNet ∥ VAE on disjoint green-context SM partitions (sd_serve_config.vae_sms):
+    every request completes with A ≤ U ≤ V, and each served image equals the request run alone on the
+    whole chip (the kernels size their grids by the partition, the per-tile arithmetic is unchanged)."""
+    import ctypes as C_
+    part, us, vs = C_.c_void_p(), C_.c_void_p(), C_.c_void_p()
+    nu, nv = C_.c_int32(), C_.c_int32()
+    B.call("sd_sm_partition_create", 0, 16, C_.byref(part), C_.byref(us), C_.byref(vs), C_.byref(nu), C_.byref(nv))
+    assert nv.value >= 16 and nu.value >= 100 and nu.value + nv.value <= 148, (nu.value, nv.value)
+    B.call("sd_sm_partition_destroy", part)
+    eng = Engine("tiny", max_latent_hw=8, b_max=4, c_max=3)
+    ctx_u = synth.uncond_embedding(0, 8, 32)
+    eng.set_uncond(torch.from_numpy(ctx_u))
+    tab = _table()
+    ctl = B.ControllerConfig(2, 3, 4, 1, 1, 1_000_000, -1, 5)
+    cfg = B.ServeConfig(4, 1, 10, 0, 2, ctl, tab, 8, 5)
+    cfg.vae_sms = 16
+    B.call("sd_serve_start", eng.h, C.byref(cfg))
+    n = 6
+    embs = [synth.text_embedding(5, i, 8, 32) for i in range(n)]
+    steps = [4, 5, 4, 6, 4, 5]
+    for i in range(n):
+        r = B.Request(i, 1000 * i, steps[i], 7.5, embs[i].ctypes.data, 8, 32)
+        B.call("sd_submit", eng.h, C.byref(r))
+    got = {}
+    out = (B.Completion * 16)()
+    cnt = C.c_int32()
+    for _ in range(400):
+        B.call("sd_poll", eng.h, out, 16, C.byref(cnt), 50)
+        for j in range(cnt.value):
+            c_ = out[j]
+            img = np.ctypeslib.as_array(C.cast(c_.image_host, C.POINTER(C.c_float)), shape=(3, c_.h, c_.w)).copy()
+            got[c_.id] = (c_.arrival_us, c_.denoise_done_us, c_.decode_done_us,
+                          [c_.skipped_steps[q] for q in range(c_.n_skipped)], img)
+            B.call("sd_release", eng.h, c_.id)
+        if len(got) == n:
+            break
+    B.call("sd_serve_stop", eng.h)
+    assert len(got) == n
+    for i in range(n):
+        A, U, Vt, skips, img = got[i]
+        assert A <= U <= Vt
+        slot = eng.register(torch.from_numpy(embs[i]))
+        lat = [torch.from_numpy(synth.initial_noise(5, i, 8, 8) * np.float32(eng.init_sigma(steps[i]))).cuda()]
+        for s in range(steps[i]):
+            eng.step(lat, [s], [steps[i]], [0 if s in skips else 1], [7.5], [slot])
+        alone = eng.decode(lat[0], 1)
+        torch.cuda.synchronize()
+        eng.release(slot)
+        assert np.array_equal(alone.cpu().numpy(), img), i
+    eng.close()
+    B.lib().sd_table_free(tab)

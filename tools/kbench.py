@@ -167,7 +167,8 @@ def main():
                 print(json.dumps(dict(kind="xattn_tc", dtype=str(dt), shape=[R, heads, d, P, 77], ms=ms,
                                       gbs=by / ms / 1e6)), flush=True)
     if args.only in ("", "attn"):
-        for i_, (R, heads, d, P) in enumerate([(16, 8, 40, 4096), (16, 8, 80, 1024), (16, 10, 64, 4096)]):
+        for i_, (R, heads, d, P) in enumerate([(16, 8, 40, 4096), (16, 8, 80, 1024), (16, 10, 64, 4096),
+                                                (16, 8, 160, 256), (16, 8, 160, 64)]):
             if args.pick >= 0 and i_ != args.pick:
                 continue
             C = heads * d

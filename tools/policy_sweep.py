@@ -66,6 +66,8 @@ def main():
     ap.add_argument("--burst-span-s", type=float, default=0.0,
                     help="burst window in seconds (CFG#3 / S:499: 10); 0 = half the requests at 2*C1")
     ap.add_argument("--no-sim", action="store_true", help="skip the virtual-clock replay")
+    ap.add_argument("--vae-sms", type=int, nargs="+", default=[0],
+                    help="SM partition sizes for the VAE (0 = stream priority only); each arm runs once per value")
     ap.add_argument("--out", default="profiles/r01/policy_sweep.json")
     args = ap.parse_args()
     eng = Engine("sd15", max_latent_hw=64, b_max=8, c_max=2)
@@ -78,6 +80,13 @@ def main():
     tab = prof.measure([1, 2], b_max=8, n_max=3)
     prof.close()
     h = profiler.to_table_handle(tab)
+    part_tables = {}  # vae_sms → table profiled on that SM partition (the planner must see its own timings)
+    for vs in args.vae_sms:
+        if vs > 0:
+            pp = profiler.Profiler(eng, 64, 64, 8, reps=1, vae_sms=vs)
+            part_tables[vs] = (profiler.to_table_handle(pp.measure([1, 2], b_max=8, n_max=3)), pp.partition_sms)
+            pp.close()
+            print(f"profiled the {pp.partition_sms} SM partition", flush=True)
     c_max, c_star, _ = profiler.chunk_choice(tab, [1, 2], m=8, n=1)
     c_max = max(c_max, c_star)
     print(f"profiled {len(tab)} table entries in {time.time() - t0:.1f} s; c* = {c_star}, C_max = {c_max}", flush=True)
@@ -100,13 +109,18 @@ def main():
         loads.append(("burst", serving.burst_trace(args.requests, 0.5 * c1, frac=0.5, span_us=int(span), seed=7)))
     for rho, trace in loads:
         row = {}
-        for name in args.arms:
-            pol, abl, chunk = ARMS[name]
+        for name0 in args.arms:
+          for vs in args.vae_sms:
+            name = name0 if vs == 0 else f"{name0} | VAE on {vs} SMs"
+            pol, abl, chunk = ARMS[name0]
             cs, cm = (c_star, c_max) if chunk else (1, 1)
             t1 = time.time()
-            _, g = serving.run_trace(eng, h, trace, 64, 8, cs, cm, n_max=3, policy=pol, ablation=abl,
-                                     timeout_s=3600)
-            sim = simulate(h, trace, pol, abl, cs, cm) if not args.no_sim else \
+            hv = part_tables[vs][0] if vs > 0 else h
+            _, g = serving.run_trace(eng, hv, trace, 64, 8, cs, cm, n_max=3, policy=pol, ablation=abl,
+                                     timeout_s=3600, vae_sms=vs)
+            if vs > 0:
+                g["partition_sms_unet_vae"] = part_tables[vs][1]
+            sim = simulate(hv, trace, pol, abl, cs, cm) if not args.no_sim else \
                 dict(images_per_s=0.0, mean_e2e_ms=0.0, p99_e2e_ms=0.0)
             row[name] = dict(gpu=g, virtual_clock=sim)
             print(f"rho {rho}: {name:26s} {g['images_per_s']:.3f} img/s, mean {g['mean_e2e_ms']:.0f} ms, "
