@@ -1,3 +1,4 @@
+#include <stdlib.h>
 // Test-only C-ABI exports: single kernels on caller-owned device buffers (sd_api.h, last section).
 #include "api_common.h"
 #include "common.cuh"
@@ -193,7 +194,17 @@ extern "C" sd_status sd_debug_xattention_tc(const void* q, const void* kc, int32
              "sd_debug_xattention_tc: d in {40,64,80,160}, ldk and ld_keys multiples of 8");
   SD_API_BEGIN
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (use_f16)
+  const char* v2 = getenv("SD_XATTN_TC2");  // SD_XATTN_TC2=0: the general tcgen05 kernel
+  if (!(v2 && v2[0] == '0') && sd::xattention_tc2_supported(d, Lk)) {
+    if (use_f16)
+      sd::xattention_tc2(static_cast<const f16*>(q), static_cast<const f16*>(kc), ldk, n_slots, kcol,
+                         static_cast<const f16*>(vtc), vt_rows, ld_keys, vrow, kv_index, Lk, static_cast<f16*>(o),
+                         rows, heads, d, heads * d, P, st);
+    else
+      sd::xattention_tc2(static_cast<const bf16*>(q), static_cast<const bf16*>(kc), ldk, n_slots, kcol,
+                         static_cast<const bf16*>(vtc), vt_rows, ld_keys, vrow, kv_index, Lk, static_cast<bf16*>(o),
+                         rows, heads, d, heads * d, P, st);
+  } else if (use_f16)
     sd::xattention_tc(static_cast<const f16*>(q), static_cast<const f16*>(kc), ldk, n_slots, kcol,
                       static_cast<const f16*>(vtc), vt_rows, ld_keys, vrow, kv_index, Lk, static_cast<f16*>(o), rows,
                       heads, d, heads * d, P, st);

@@ -502,6 +502,9 @@ void build_engine(Engine* e) {
   // mma.sync kernel that keeps K/V resident across query tiles measured faster (64²: 55 vs 71 µs)
   const char* xt = getenv("SD_XATTN_TC");
   e->use_xattn_tc = e->use_attn_tc && (xt && xt[0] == '1');
+  // the persistent tcgen05 cross-attention (K / Vᵀ resident across query tiles): SD_XATTN_TC2=1 enables it
+  const char* x2 = getenv("SD_XATTN_TC2");
+  e->use_xattn_tc2 = e->use_attn_tc && (x2 && x2[0] == '1');
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -797,10 +800,20 @@ struct Fwd {
       ln(h2, n, T, C, k.l2g, k.l2b);
       AT* q2 = buf(T * C);
       linear(n, T, C, wt<AT>(k.wq2), C, nullptr, q2, C);
-      bool xtc = false;
-      if constexpr (!std::is_same<AT, float>::value)
-        xtc = e->use_xattn_tc && e->vt_cache && attention_tc_supported(dh, 128, C);
-      if (xtc) {
+      bool xtc = false, xtc2 = false;
+      if constexpr (!std::is_same<AT, float>::value) {
+        xtc2 = e->use_xattn_tc2 && e->vt_cache && xattention_tc2_supported(dh, e->uc.ctx_len);
+        xtc = !xtc2 && e->use_xattn_tc && e->vt_cache && attention_tc_supported(dh, 128, C);
+      }
+      if (xtc2) {
+        if constexpr (!std::is_same<AT, float>::value) {
+          const int pi = e->prof.begin(PC_ATTN, st, 4.0 * R * heads * (double)P * e->uc.ctx_len * dh);
+          xattention_tc2(q2, static_cast<const AT*>(e->kv_cache), e->U.kv_width, e->max_slots, k.koff,
+                         static_cast<const AT*>(e->vt_cache), e->U.kv_width, e->vt_ld, k.voff, kv_index,
+                         e->uc.ctx_len, o, R, heads, dh, C, P, st);
+          e->prof.end(pi, st);
+        }
+      } else if (xtc) {
         if constexpr (!std::is_same<AT, float>::value) {
           const int pi = e->prof.begin(PC_ATTN, st, 4.0 * R * heads * (double)P * e->uc.ctx_len * dh);
           xattention_tc(q2, static_cast<const AT*>(e->kv_cache), e->U.kv_width, e->max_slots, k.koff,

@@ -213,7 +213,8 @@ struct Engine {
   std::map<std::tuple<int, int, int, int, int>, GraphEntry> graphs;
   bool use_graphs = true;
   bool use_attn_tc = true;
-  bool use_xattn_tc = true;  // tcgen05 cross-attention over the text K / Vᵀ caches  // tcgen05 flash attention where supported (SD_ATTN_TC=0 disables)
+  bool use_xattn_tc = true;   // tcgen05 cross-attention over the text K / Vᵀ caches (general kernel)
+  bool use_xattn_tc2 = false; // the persistent tcgen05 cross-attention (xattention_tc.cu)  // tcgen05 flash attention where supported (SD_ATTN_TC=0 disables)
   int graphs_built = 0;
   cudaStream_t cap_stream = nullptr;
   int max_rows = 0;

@@ -68,6 +68,15 @@ void xattention_tc(const bf16* q, const bf16* kc, int ldk, long n_slots, int kco
 void xattention_tc(const f16* q, const f16* kc, int ldk, long n_slots, int kcol, const f16* vtc, long vt_rows,
                    long ld_keys, int vrow, const int* kv_index, int Lk, f16* O, int rows, int heads, int d, int C, int P,
                    cudaStream_t st);
+// the same layouts on the persistent variant (xattention_tc.cu): one CTA per (row, head) run of query tiles
+// with K / Vᵀ resident; d ∈ {40, 64, 80}, Lk ≤ 128
+bool xattention_tc2_supported(int d, int Lk);
+void xattention_tc2(const bf16* q, const bf16* kc, int ldk, long n_slots, int kcol, const bf16* vtc, long vt_rows,
+                    long ld_keys, int vrow, const int* kv_index, int Lk, bf16* O, int rows, int heads, int d, int C,
+                    int P, cudaStream_t st);
+void xattention_tc2(const f16* q, const f16* kc, int ldk, long n_slots, int kcol, const f16* vtc, long vt_rows,
+                    long ld_keys, int vrow, const int* kv_index, int Lk, f16* O, int rows, int heads, int d, int C,
+                    int P, cudaStream_t st);
 
 // row softmax for the VAE attention path: P[r][:] = softmax(S[r][:]) (S fp32, P bf16)
 void softmax_rows(const float* S, bf16* P, int rows, int cols, cudaStream_t st);
