@@ -694,15 +694,17 @@ static int attn_emu() {
   }
   return v;
 }
-// SD_ATTN_EF=8|4|3: one softmax pair in EF computes its exponentials on the FMA pipe (d = 40, OP 4)
-static int attn_ef() {
+// SD_ATTN_EF=8|4|3: one softmax pair in EF computes its exponentials on the FMA pipe (d = 40, OP 4).
+// Default by precision (kbench [16, 8, 40, 4096], B200): bf16 EF 8 675 µs (EF 3: 682); fp16 EF 3 690 µs
+// (EF 8: 709) — the fp16 P conversion competes with the exponentials, so fp16 moves more of them off MUFU
+static int attn_ef(bool f16) {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("SD_ATTN_EF");
-    v = e ? atoi(e) : 8;
-    if (v != 4 && v != 3) v = 8;
+    v = e ? atoi(e) : 0;
+    if (v != 4 && v != 3 && v != 8) v = 0;
   }
-  return v;
+  return v ? v : (f16 ? 3 : 8);
 }
 // SD_ATTN_NB=1|2: S / P buffers at d = 40 (default 1: two CTAs per SM)
 static int attn_nb() {
@@ -742,9 +744,9 @@ static void attention_tc16(const TcSrc& sr, bf16* O, int ldo, int rows, int head
         case 126: launch_tc<40, 1, 2, 0, 2>(sr, O, ldo, rows, heads, P, st, f16); break;
         case 127: launch_tc<40, 1, 2, 0, 3>(sr, O, ldo, rows, heads, P, st, f16); break;
         case 128:  // SD_ATTN_EMU=8 (default): P in TMEM; SD_ATTN_EF = pairs per FMA-pipe exp pair (8 / 4 / 3)
-          if (attn_ef() == 4)
+          if (attn_ef(f16) == 4)
             launch_tc<40, 1, 2, 4, 4>(sr, O, ldo, rows, heads, P, st, f16);
-          else if (attn_ef() == 3)
+          else if (attn_ef(f16) == 3)
             launch_tc<40, 1, 2, 3, 4>(sr, O, ldo, rows, heads, P, st, f16);
           else
             launch_tc<40, 1, 2, 0, 4>(sr, O, ldo, rows, heads, P, st, f16);
