@@ -757,7 +757,9 @@ static void attention_tc16(const TcSrc& sr, bf16* O, int ldo, int rows, int head
     case 64:  // SD_ATTN_EMU=8 (default): the d = 40 structure — two CTAs per SM, two softmax threads per
               // row, one TMEM pass, P in TMEM (S 128 | O 64 | P 64 columns): SDXL [16,10,64,4096] 1.27 → 1.16
               // ms vs NB = 2 / one thread per row (which was 1.18× faster than NB = 1 with P in smem)
-      if (attn_emu() == 8)
+      if (attn_emu() == 8 && attn_ef(f16) == 3)
+        launch_tc<64, 1, 2, 3, 4>(sr, O, ldo, rows, heads, P, st, f16);
+      else if (attn_emu() == 8)
         launch_tc<64, 1, 2, 0, 4>(sr, O, ldo, rows, heads, P, st, f16);
       else if (attn_emu() == 5)
         launch_tc<64, 2, 1, 0, 5>(sr, O, ldo, rows, heads, P, st, f16);
@@ -768,7 +770,9 @@ static void attention_tc16(const TcSrc& sr, bf16* O, int ldo, int rows, int head
       break;
     case 80:  // SD_ATTN_EMU=8 (default): two softmax threads per row, one TMEM pass, P in TMEM; S | O | P
               // need 272 columns, so one CTA per SM (512 allocated): [16,8,80,1024] 87.9 → 83.1 µs
-      if (attn_emu() == 8)
+      if (attn_emu() == 8 && attn_ef(f16) == 3)
+        launch_tc<80, 1, 2, 3, 4>(sr, O, ldo, rows, heads, P, st, f16);
+      else if (attn_emu() == 8)
         launch_tc<80, 1, 2, 0, 4>(sr, O, ldo, rows, heads, P, st, f16);
       else if (attn_emu() == 5)
         launch_tc<80, 2, 1, 0, 5>(sr, O, ldo, rows, heads, P, st, f16);

@@ -14,9 +14,16 @@ Cold caches (ncu's default cache control), serialised launches.
 import csv
 import io
 import json
+import re
 import subprocess
 import sys
 
+
+
+def gemm_mode(name):
+    """MODE template argument (0 dense, 1 conv3) of a gemm_kernel<BN, CG, MODE[, F16]> name, else None."""
+    m = re.search(r"gemm_kernel<\s*(\d+)\s*,\s*(\d+)\s*,\s*(\d+)", name)
+    return int(m.group(3)) if m else None
 
 def main():
     if sys.argv[1].endswith(".ncu-rep"):
@@ -40,7 +47,7 @@ def main():
         us = val(r, "gpu__time_duration.sum")
         tens = val(r, "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed")
         base = name.split("(")[0]
-        if "gemm_kernel" in base and base.rstrip(">").endswith("1"):
+        if gemm_mode(base) == 1:
             cur = dict(bytes=by, us=us, tensor_w=tens * us, launches=1)
             ops.append(cur)
         elif "splitk_reduce" in base and cur is not None:

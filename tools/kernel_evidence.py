@@ -12,6 +12,7 @@ Warm caches (--cache-control none): the kernels run as in the step, producer out
 import collections
 import csv
 import json
+import re
 import os
 import sys
 
@@ -20,16 +21,24 @@ METRICS = ("gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,"
            "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active,launch__grid_size")
 
 
+
+def gemm_mode(name):
+    """MODE template argument (0 dense, 1 conv3) of a gemm_kernel<BN, CG, MODE[, F16]> name, else None."""
+    m = re.search(r"gemm_kernel<\s*(\d+)\s*,\s*(\d+)\s*,\s*(\d+)", name)
+    return int(m.group(3)) if m else None
+
 def classify(name):
     n = name.split("(")[0]
     if "gemm_kernel" in n:
-        return "conv3x3 implicit GEMM (tcgen05)" if n.rstrip(">").endswith("1") else "dense GEMM (tcgen05)"
+        return "conv3x3 implicit GEMM (tcgen05)" if gemm_mode(name) == 1 else "dense GEMM (tcgen05)"
     if "attn_tc" in n:
         return "self-attention (tcgen05 flash)"
+    if "xattn_tc_kernel" in n:
+        return "cross-attention (tcgen05, K/V resident)"
     if "xattn" in n:
         return "cross-attention (short-context mma.sync)"
     if "attn_kernel" in n:
-        return "self-attention (mma.sync flash, d=160)"
+        return "self-attention (mma.sync flash)"
     if "gn_" in n:
         return "GroupNorm (stats/finalize/apply)"
     if "layer_norm" in n:
