@@ -803,7 +803,10 @@ struct Fwd {
       bool xtc = false, xtc2 = false;
       if constexpr (!std::is_same<AT, float>::value) {
         xtc2 = e->use_xattn_tc2 && e->vt_cache && xattention_tc2_supported(dh, e->uc.ctx_len);
-        xtc = !xtc2 && e->use_xattn_tc && e->vt_cache && attention_tc_supported(dh, 128, C);
+        // d = 160 at P ≥ 128 (the 16×16 level): the general tcgen05 kernel beats mma.sync (13.5 vs 14.3 µs);
+        // at d ≤ 80 and at the 8×8 mid block mma.sync is faster for 77 keys
+        const bool pick = e->use_xattn_tc || (e->use_attn_tc && dh == 160 && P >= 128);
+        xtc = !xtc2 && pick && e->vt_cache && attention_tc_supported(dh, 128, C);
       }
       if (xtc2) {
         if constexpr (!std::is_same<AT, float>::value) {

@@ -234,12 +234,22 @@ __global__ void __launch_bounds__(320, 1)
         const float ms = mx * a.scale_log2;
         float sum = 0.f;
         uint32_t pk[32];
+        // exponentials only for the 16-key chunks that hold valid keys (77 keys: h = 1 needs one of its
+        // four chunks); masked chunks are zero without touching MUFU (valid is warp-uniform)
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float p0 = ex2f(fmaf(__uint_as_float(s[2 * i]), a.scale_log2, -ms));
-          const float p1 = ex2f(fmaf(__uint_as_float(s[2 * i + 1]), a.scale_log2, -ms));
-          sum += p0 + p1;
-          pk[i] = pack16(p0, p1, F16);
+        for (int c = 0; c < 4; ++c) {
+          if (c * 16 < valid) {
+#pragma unroll
+            for (int i = c * 8; i < c * 8 + 8; ++i) {
+              const float p0 = ex2f(fmaf(__uint_as_float(s[2 * i]), a.scale_log2, -ms));
+              const float p1 = ex2f(fmaf(__uint_as_float(s[2 * i + 1]), a.scale_log2, -ms));
+              sum += p0 + p1;
+              pk[i] = pack16(p0, p1, F16);
+            }
+          } else {
+#pragma unroll
+            for (int i = c * 8; i < c * 8 + 8; ++i) pk[i] = 0u;
+          }
         }
         // P of tile t into TMEM buffer b: PV of tile t − 2 (same buffer) finished before the epilogue of
         // tile t − 2, which this thread waited for in iteration t − 1
