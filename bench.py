@@ -144,9 +144,10 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def config(n):
-    return {"workload": "CFG#2: SD-1.5-shaped UNet bf16, 512x512 (latent 64x64), 8 requests/GPU lockstep x 50 "
-                        "DDIM steps, CFG every step (16 UNet rows/step), then 8 whole VAE decodes",
+def config(n, precision="fp16"):
+    return {"workload": "CFG#2: SD-1.5-shaped UNet (bf16-valued weights), 512x512 (latent 64x64), 8 requests/GPU "
+                        "lockstep x 50 DDIM steps, CFG every step (16 UNet rows/step), then 8 whole VAE decodes",
+            "precision": f"{precision} tensor-core operands / activations, fp32 accumulation (DESIGN R19a)",
             "model": "sd15-shaped UNet (859.5M params) + SD VAE decoder, random init", "global_batch": N_REQ * n,
             "seq_len": LAT * LAT, "parallelism": f"dp{n} (request sharding, weak scaling)",
             "l2": "inputs larger than L2: 1.7 GB of UNet weights and >40 MB per activation stream through HBM"}
@@ -409,7 +410,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": args.precision, "data": "synthetic (seeded; random-init weights)",
-            "config": config(world),
+            "config": config(world, args.precision),
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": sus, "unit": "TFLOP/s",
                          "frac": achieved / sus, "traffic": traffic,
                          "kernel": "conv3x3 implicit GEMM (tcgen05/TMEM/TMA), all UNet conv3x3 launches",
