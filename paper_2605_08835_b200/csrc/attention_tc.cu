@@ -98,12 +98,6 @@ __device__ __forceinline__ void ex2_poly2(float x0, float x1, float& y0, float& 
   y0 = __int_as_float(__float_as_int(p0) + ((__float_as_int(t0) - 0x4B400000) << 23));
   y1 = __int_as_float(__float_as_int(p1) + ((__float_as_int(t1) - 0x4B400000) << 23));
 }
-// two fp16 exponentials in one MUFU op (inputs / outputs packed half2)
-__device__ __forceinline__ uint32_t ex2_h2(uint32_t x) {
-  uint32_t y;
-  asm("ex2.approx.f16x2 %0, %1;" : "=r"(y) : "r"(x));
-  return y;
-}
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -135,7 +129,6 @@ struct AttnTcArgs {
   float scale_log2;
   int qcol0, kcol0, vrow0;  // column of head 0 in tq / tk; row of head 0's channels in tvt
   const int* kv_index;      // nullptr: self-attention
-  int ex2h;                 // fp16: packed f16x2 exponentials (SD_ATTN_EX2H=1; default off)
   int vt_slot;              // cross-attention: key columns per slot in tvt (Lk rounded up to 8: TMA needs the
                             // inner box start 16-byte aligned)
 };
@@ -147,7 +140,6 @@ __global__ void __launch_bounds__(64 + 128 * SPLIT, 3 - NB)
                    const __grid_constant__ CUtensorMap tk_t, const AttnTcArgs a) {
   const int P = a.P, Lk = a.Lk, ldo = a.ldo;
   constexpr bool is_f16 = F16;
-  const bool ex2h = a.ex2h != 0;
   const float scale_log2 = a.scale_log2;
   bf16* __restrict__ O = a.O;
   using A = TcAttn<D, NB, SPLIT, EMU, (OP == 4 || OP == 5) ? 1 : 0>;
@@ -345,23 +337,7 @@ __global__ void __launch_bounds__(64 + 128 * SPLIT, 3 - NB)
         const float alpha = upd ? ex2((m - mnew) * scale_log2) : 1.f;
         const float ms = mnew * scale_log2;
         float sum8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        if (F16 && ex2h) {
-          // fp16 P: the exponent pair goes through ONE packed MUFU op (ex2.approx.f16x2) — half the MUFU
-          // issue of the fp32 path, the bound of this softmax; x is rounded to fp16 first (|Δx| ≤ 2⁻¹¹·|x|),
-          // P comes out as the fp16 pair the PV MMA consumes (no pack)
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const uint32_t pa = ex2_h2(pack_f16(fmaf(__uint_as_float(ta[2 * i]), scale_log2, -ms),
-                                                fmaf(__uint_as_float(ta[2 * i + 1]), scale_log2, -ms)));
-            const uint32_t pb = ex2_h2(pack_f16(fmaf(__uint_as_float(tb[2 * i]), scale_log2, -ms),
-                                                fmaf(__uint_as_float(tb[2 * i + 1]), scale_log2, -ms)));
-            const float2 fa = __half22float2(*reinterpret_cast<const __half2*>(&pa));
-            const float2 fb = __half22float2(*reinterpret_cast<const __half2*>(&pb));
-            sum8[i & 7] += (fa.x + fa.y) + (fb.x + fb.y);
-            ta[i] = pa;
-            tb[i] = pb;
-          }
-        } else if (OP == 4) {
+        if (OP == 4) {
           // packed fp32 pairs (FFMA2 / FADD2) and one pair in PER on the FMA pipe (ex2_poly2); the other
           // pairs on MUFU. P packed in place: ta[i] ← 16-bit pair (p(ta[2i]), p(ta[2i+1]))
           constexpr int PER = EMU > 0 ? EMU : 8;
@@ -655,10 +631,6 @@ static void launch_tc(const TcSrc& sr, bf16* O, int ldo, int rows, int heads, in
   a.vrow0 = sr.vrow0;
   a.kv_index = sr.kv_index;
   a.vt_slot = (sr.Lk + 7) / 8 * 8;
-  // SD_ATTN_EX2H=1: fp16 exponentials in ex2.approx.f16x2 — it lowers to two MUFU.EX2.F16 (no issue saving)
-  // and measured slower (d = 40: 0.755 vs 0.728 ms), so off by default
-  static const int ex2h_env = getenv("SD_ATTN_EX2H") && getenv("SD_ATTN_EX2H")[0] == '1' ? 1 : 0;
-  a.ex2h = ex2h_env;
   if (f16)
     launch_k(attn_tc_kernel<D, NB, SPLIT, EMU, OP, true>, grid, A::THREADS, A::SMEM, st, mq, mk, mvt, mq_t, mk_t, a);
   else

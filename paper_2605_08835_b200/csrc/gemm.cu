@@ -65,13 +65,19 @@ __device__ __forceinline__ void decode_tile(const GemmArgs& g, int t, int& mt, i
 template <int BN, int CG>
 struct Cfg {
   static constexpr int BM = 128, BK = 64;
+  // BN = 320 (conv3, CTA pairs): two N = 160 MMAs per k-step share the A operand — A is read from smem
+  // once per 320 output columns instead of once per 160 (the N = 160 tiles were operand-bandwidth bound:
+  // tensor pipe ~51 %, with the MMA warp never waiting on data or the epilogue)
+  static constexpr int NH = BN > 256 ? 2 : 1;                    // MMA N-halves per k-step
+  static constexpr int MMA_N = BN / NH;
   static constexpr int A_BYTES = BM * BK * 2;                    // 16 KB (this CTA's rows)
   static constexpr int B_ROWS = BN / CG;                         // B rows loaded by this CTA
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int STAGES = (192 * 1024) / STAGE > 8 ? 8 : (192 * 1024) / STAGE;
-  static constexpr int TMEM_STRIDE = BN <= 64 ? 64 : (BN <= 128 ? 128 : 256);
-  static constexpr int TMEM_COLS = 2 * TMEM_STRIDE;
+  static constexpr int TMEM_STRIDE = BN <= 64 ? 64 : (BN <= 128 ? 128 : (BN <= 256 ? 256 : BN));
+  static constexpr int NACC = 2 * TMEM_STRIDE <= 512 ? 2 : 1;    // double-buffered accumulator if it fits
+  static constexpr int TMEM_COLS = NACC == 2 ? 2 * TMEM_STRIDE : 512;
   static constexpr int STAGING = 8 * 2 * 2048;                   // 8 epilogue warps × 2 slabs
   static constexpr int SMEM = 1024 + STAGES * STAGE + STAGING + 512;
   static_assert(B_BYTES % 1024 == 0, "B tile must be a whole number of 8-row swizzle groups");
@@ -567,7 +573,14 @@ __global__ void __launch_bounds__(320, 1)
             const CUtensorMap* ma = src ? &ta1 : &ta0;
             const CUtensorMap* mb = src ? &tb1 : &tb0;
             tma4<CG>(dA, ma, &full[stage], bar_l, cb * C::BK, g.stride * x0 + dx, g.stride * y0 + dy, b0);
-            tma3<CG>(dB, mb, &full[stage], bar_l, cb * C::BK, tap, n0);
+            if (C::NH == 1) {
+              tma3<CG>(dB, mb, &full[stage], bar_l, cb * C::BK, tap, n0);
+            } else {  // this CTA's slice of each N-half: rows nt·BN + h·MMA_N + rank·MMA_N/CG
+#pragma unroll
+              for (int h = 0; h < C::NH; ++h)
+                tma3<CG>(static_cast<uint8_t*>(dB) + h * (C::B_ROWS / C::NH) * 128, mb, &full[stage], bar_l,
+                         cb * C::BK, tap, nt * BN + h * C::MMA_N + (int)rank * (C::MMA_N / CG));
+            }
           }
           if (++stage == C::STAGES) {
             stage = 0;
@@ -579,13 +592,13 @@ __global__ void __launch_bounds__(320, 1)
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
       // ================= MMA issuer (leader CTA) =================
-      const uint32_t idesc = make_idesc16(128 * CG, BN, F16);
+      const uint32_t idesc = make_idesc16(128 * CG, C::MMA_N, F16);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
       for (int t = worker; t < total; t += nworkers, ++it) {
-        const int acc = it & 1;
-        const uint32_t acc_phase = (it >> 1) & 1;
+        const int acc = C::NACC == 2 ? (it & 1) : 0;
+        const uint32_t acc_phase = C::NACC == 2 ? ((it >> 1) & 1) : (it & 1);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * C::TMEM_STRIDE;
@@ -598,8 +611,11 @@ __global__ void __launch_bounds__(320, 1)
           const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
 #pragma unroll
           for (int k = 0; k < C::BK / 16; ++k)
-            mma<CG>(d, make_sdesc_sw128(a0 + k * 32), make_sdesc_sw128(b0 + k * 32), idesc,
-                    (kb != kb0 || k != 0) ? 1u : 0u);
+#pragma unroll
+            for (int h = 0; h < C::NH; ++h)  // N-half h: B rows [h·B_ROWS/NH, …) of every CTA, TMEM cols h·MMA_N
+              mma<CG>(d + h * C::MMA_N, make_sdesc_sw128(a0 + k * 32),
+                      make_sdesc_sw128(b0 + h * (C::B_ROWS / C::NH) * 128 + k * 32), idesc,
+                      (kb != kb0 || k != 0) ? 1u : 0u);
           commit<CG>(&empty[stage]);
           if (++stage == C::STAGES) {
             stage = 0;
@@ -617,8 +633,8 @@ __global__ void __launch_bounds__(320, 1)
     EpiCtx ec{sStage + (warp - 2) * 4096, 0, 0, 0, 0, rbar + (warp - 2) * 2, 0u};
     int it = 0;
     for (int t = worker; t < total; t += nworkers, ++it) {
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
+      const int acc = C::NACC == 2 ? (it & 1) : 0;
+      const uint32_t acc_phase = C::NACC == 2 ? ((it >> 1) & 1) : (it & 1);
       int mt, nt, sp, kb0, kb1;
       decode_tile(g, t, mt, nt, sp, kb0, kb1);
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * C::TMEM_STRIDE;
@@ -794,6 +810,7 @@ static void dispatch(int bn, int cg, const CUtensorMap* maps, const GemmArgs& a,
     case 128 * 4 + 2: launch<128, 2, MODE>(maps, a, st); break;
     case 160 * 4 + 2: launch<160, 2, MODE>(maps, a, st); break;
     case 256 * 4 + 2: launch<256, 2, MODE>(maps, a, st); break;
+    case 320 * 4 + 2: launch<320, 2, MODE>(maps, a, st); break;
     default: throw CudaError("unsupported BN/CG");
   }
 }
@@ -839,8 +856,18 @@ int gemm_splits(const GemmDesc& d) {
   if (s == 0) {
     // the 8×8 level of SD-1.5 (1280 / 2560 channels): 40 output tiles at 8 requests × CFG leave
     // most of the 148 SMs idle over 180–360 K blocks; 3 splits make one full wave
-    if ((long)d.H * d.W > 64 || kb < 90) return 1;
-    s = env >= 0 ? env : 3;
+    // SD_SPLIT16=s: also split the 16×16 level (80 pair tiles = 1.08 waves of 74 pairs at 16 rows)
+    static int s16 = -2;
+    if (s16 == -2) {
+      const char* e = getenv("SD_SPLIT16");
+      s16 = e ? atoi(e) : 0;
+    }
+    if ((long)d.H * d.W == 256 && kb >= 90 && s16 > 1) {
+      s = s16;
+    } else {
+      if ((long)d.H * d.W > 64 || kb < 90) return 1;
+      s = env >= 0 ? env : 3;
+    }
   }
   s = std::max(1, std::min(s, std::min(8, kb)));
   const int kps = cdiv(kb, s);
@@ -934,7 +961,18 @@ void gemm(const GemmDesc& d, cudaStream_t st) {
   int cg = (pair_ok && (((long)box_count * 128 <= 16L * d.N) || conv_pair)) ? 2 : 1;
   if (g_cg_override == 1 || g_cg_override == 2) cg = g_cg_override;
   if (cg == 2 && (box_begin % 2 || bn < 128)) cg = 1;
-  const uint32_t brows = (uint32_t)(bn / cg);
+  // paired conv tiles with N a multiple of 320 (the 64×64 / 32×32 levels): BN = 320 = two N = 160 MMAs
+  // sharing A (SD_CONV_BN320=0: BN = 160)
+  static int bn320 = -1;
+  if (bn320 < 0) {
+    const char* e = getenv("SD_CONV_BN320");
+    bn320 = !(e && e[0] == '0');
+  }
+  if (bn320 && d.mode == GEMM_CONV3 && cg == 2 && bn == 160 && d.N % 320 == 0 && !d.bn) {
+    bn = 320;
+    a.n_tiles = cdiv(d.N, bn);
+  }
+  const uint32_t brows = (uint32_t)(bn / cg / (bn > 256 ? 2 : 1));
   if (d.mode == GEMM_DENSE && d.nsrc == 2) {
     for (int s = 0; s < 2; ++s) {  // source s: its own activation tensor [M][cs] and weight columns
       uint64_t dA[2] = {(uint64_t)d.cs[s], (uint64_t)d.M}, sA[1] = {(uint64_t)d.cs[s] * 2};

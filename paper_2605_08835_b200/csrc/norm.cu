@@ -371,7 +371,8 @@ static int gn_silu_mode(bool silu) {
     const char* e = getenv("SD_SILU_TANH");
     st_env = e ? atoi(e) : 1;
   }
-  return !silu ? 0 : (std::is_same<T, bf16>::value && st_env) ? 2 : 1;
+  // SD_SILU_TANH=2 also for fp16 (experiments)
+  return !silu ? 0 : ((std::is_same<T, bf16>::value && st_env) || (std::is_same<T, f16>::value && st_env == 2)) ? 2 : 1;
 }
 
 // SD_GN_FUSED=1: the single cooperative launch for whole tensors. Off by default — measured slower than the

@@ -64,7 +64,7 @@ def main():
         "dram_bytes_per_launch": sum(o["bytes"] for o in ops) / max(n, 1),
         "ncu_ms_per_unet_step": sum(o["us"] for o in ops) / 1e3,
         "mean_tensor_pipe_active_pct": sum(o["tensor_w"] for o in ops) / max(sum(o["us"] for o in ops), 1e-9),
-        "round": "r01",
+        "round": "r02",
     }
     print(json.dumps(res, indent=1))
 
