@@ -404,6 +404,9 @@ sd_status sd_debug_layernorm(const void* x, void* y, int32_t T, int32_t C, const
  * §8(c) I7 (DDIM ε ≡ 0 telescoping; Euler constant ε) run through the GPU kernel. */
 sd_status sd_debug_step_eps(sd_engine* e, const sd_batch* b, float* eps_dev, void* stream);
 sd_status sd_debug_combine_update(sd_engine* e, const sd_batch* b, const float* eps_dev, void* stream);
+/* fp16 (on != 0) instead of bf16 element type for sd_debug_gemm / _gemm_res / _conv3x3 / _conv3x3_s2 /
+ * _groupnorm / _layernorm (the SD_PREC_FP16 instantiations of the same kernels); process-wide, tests only. */
+sd_status sd_debug_set_f16(int32_t on);
 /* GEMM tile mode for the tests: 0 = heuristic, 1 = 128-row CTA tiles, 2 = 256-row CTA-pair tiles. */
 sd_status sd_debug_set_gemm_cg(int32_t cg);
 /* 3x3 / stride 2 / pad 1 conv (the UNet downsamplers) by TMA boxes with element stride 2: x bf16

@@ -148,6 +148,7 @@ SIGNATURES = {
     "sd_debug_gemm": [P, P, P, P, I32, I32, I32, I32, I32, P],
     "sd_debug_gemm_res": [P, P, P, P, I32, P, I32, I32, I32, P],
     "sd_debug_set_gemm_cg": [I32],
+    "sd_debug_set_f16": [I32],
     "sd_debug_set_conv_splits": [I32],
     "sd_debug_attention": [P, P, P, P, I32, I32, I32, I32, I32, P],
     "sd_debug_attention_tc": [P, P, P, I32, I32, I32, I32, I32, P],

@@ -12,6 +12,12 @@ void set_error(const std::string& s) { g_err = s; }
 }  // namespace sd
 
 static int g_dbg_splits = 0;  // split-K of sd_debug_conv3x3 (0 = the production rule)
+static int g_dbg_f16 = 0;     // sd_debug_set_f16: fp16 instead of bf16 operands in the GEMM / conv / norm exports
+
+extern "C" sd_status sd_debug_set_f16(int32_t on) {
+  g_dbg_f16 = on ? 1 : 0;
+  return SD_OK;
+}
 
 extern "C" const char* sd_last_error(void) { return sd::g_err.c_str(); }
 
@@ -47,6 +53,7 @@ extern "C" sd_status sd_debug_gemm(const void* A, const void* B, const float* bi
   d.out_f32 = out_f32;
   d.bias = bias;
   d.act = act;
+  d.f16 = g_dbg_f16;
   sd::gemm(d, static_cast<cudaStream_t>(stream));
   SD_API_END
 }
@@ -70,6 +77,7 @@ extern "C" sd_status sd_debug_gemm_res(const void* A, const void* B, const float
   d.bias = bias;
   d.res = static_cast<const bf16*>(res);
   d.ldr = ldr;
+  d.f16 = g_dbg_f16;
   sd::gemm(d, static_cast<cudaStream_t>(stream));
   SD_API_END
 }
@@ -101,6 +109,7 @@ extern "C" sd_status sd_debug_conv3x3(const void* x, int32_t cin, const void* x2
   d.res = static_cast<const bf16*>(res);
   d.ldr = cout;
   d.splits = g_dbg_splits;
+  d.f16 = g_dbg_f16;
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
   d.split_ws_bytes = sd::gemm_split_ws_bytes(d);
   if (d.split_ws_bytes) SD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d.split_ws), d.split_ws_bytes, st));
@@ -128,6 +137,7 @@ extern "C" sd_status sd_debug_conv3x3_s2(const void* x, int32_t cin, const void*
   d.ldo = cout;
   d.bias = bias;
   d.splits = 1;
+  d.f16 = g_dbg_f16;
   sd::gemm(d, static_cast<cudaStream_t>(stream));
   SD_API_END
 }
@@ -223,7 +233,11 @@ extern "C" sd_status sd_debug_groupnorm(const void* x, void* y, int32_t nb, int3
   void* ws = nullptr;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   SD_CUDA(cudaMallocAsync(&ws, sd::gn_workspace_bytes(nb, P, G, C), st));
-  sd::group_norm(static_cast<const bf16*>(x), static_cast<bf16*>(y), nb, P, C, G, gamma, beta, eps, silu != 0, ws, st);
+  if (g_dbg_f16)
+    sd::group_norm(static_cast<const f16*>(x), static_cast<f16*>(y), nb, P, C, G, gamma, beta, eps, silu != 0, ws, st);
+  else
+    sd::group_norm(static_cast<const bf16*>(x), static_cast<bf16*>(y), nb, P, C, G, gamma, beta, eps, silu != 0, ws,
+                   st);
   SD_CUDA(cudaFreeAsync(ws, st));
   SD_API_END
 }
@@ -232,7 +246,11 @@ extern "C" sd_status sd_debug_layernorm(const void* x, void* y, int32_t T, int32
                                         const float* beta, float eps, void* stream) {
   SD_REQUIRE(x && y && gamma && beta && T > 0 && C > 0 && C % 8 == 0, "sd_debug_layernorm: bad arguments");
   SD_API_BEGIN
-  sd::layer_norm(static_cast<const bf16*>(x), static_cast<bf16*>(y), T, C, gamma, beta, eps,
-                 static_cast<cudaStream_t>(stream));
+  if (g_dbg_f16)
+    sd::layer_norm(static_cast<const f16*>(x), static_cast<f16*>(y), T, C, gamma, beta, eps,
+                   static_cast<cudaStream_t>(stream));
+  else
+    sd::layer_norm(static_cast<const bf16*>(x), static_cast<bf16*>(y), T, C, gamma, beta, eps,
+                   static_cast<cudaStream_t>(stream));
   SD_API_END
 }

@@ -856,11 +856,12 @@ int gemm_splits(const GemmDesc& d) {
   if (s == 0) {
     // the 8×8 level of SD-1.5 (1280 / 2560 channels): 40 output tiles at 8 requests × CFG leave
     // most of the 148 SMs idle over 180–360 K blocks; 3 splits make one full wave
-    // SD_SPLIT16=s: also split the 16×16 level (80 pair tiles = 1.08 waves of 74 pairs at 16 rows)
+    // the 16×16 level too: 80 pair tiles are 1.08 waves of 74 pairs at 16 rows; 3 splits measured
+    // [16, 16, 16, 1280, 1280] 116.7 → 105.1 µs (2 splits: 109.7). SD_SPLIT16=1 turns it off.
     static int s16 = -2;
     if (s16 == -2) {
       const char* e = getenv("SD_SPLIT16");
-      s16 = e ? atoi(e) : 0;
+      s16 = e ? atoi(e) : 3;
     }
     if ((long)d.H * d.W == 256 && kb >= 90 && s16 > 1) {
       s = s16;

@@ -22,8 +22,22 @@ def rel(a, b):
     return float((a.double() - b.double()).norm() / b.double().norm().clamp_min(1e-30))
 
 
+DT = torch.bfloat16  # element type of the GEMM / conv / norm exports under test (fixture `elem`)
+
+
+@pytest.fixture(params=["bf16", "fp16"], autouse=True)
+def elem(request):
+    """Run the GEMM / conv / norm kernel tests on the bf16 and the fp16 (SD_PREC_FP16) instantiations."""
+    global DT
+    DT = torch.float16 if request.param == "fp16" else torch.bfloat16
+    B.call("sd_debug_set_f16", 1 if request.param == "fp16" else 0)
+    yield request.param
+    B.call("sd_debug_set_f16", 0)
+    DT = torch.bfloat16
+
+
 def bf(x):
-    return x.to(torch.bfloat16)
+    return x.to(DT)
 
 
 @pytest.mark.parametrize("M,N,K", [(128, 64, 64), (300, 320, 320), (1000, 1280, 640), (77, 256, 768),
@@ -38,7 +52,7 @@ def test_gemm_dense(M, N, K, out_f32):
     bias = torch.randn(N, generator=g)
     ref = bf(A).double() @ bf(Wt).double().T + bias.double()
     Ad, Wd = bf(A).cuda(), bf(Wt).cuda()
-    D = torch.empty(M, N, device="cuda", dtype=torch.float32 if out_f32 else torch.bfloat16)
+    D = torch.empty(M, N, device="cuda", dtype=torch.float32 if out_f32 else DT)
     B.debug_gemm(Ad, Wd, bias.cuda(), D, M, N, K, out_f32=out_f32)
     torch.cuda.synchronize()
     assert rel(D.cpu(), ref) < (1e-5 if out_f32 else 6e-3)
@@ -54,7 +68,7 @@ def test_gemm_residual(M, N, K, ldr, inplace):
     bias, res = torch.randn(N, generator=g), bf(torch.randn(M, ldr, generator=g))
     ref = bf(A).double() @ bf(Wt).double().T + bias.double() + res[:, :N].double()
     Ad, Wd, bd, resd = bf(A).cuda(), bf(Wt).cuda(), bias.cuda(), res.cuda()  # kept alive across the call
-    D = resd if inplace else torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    D = resd if inplace else torch.empty(M, N, device="cuda", dtype=DT)
     B.call("sd_debug_gemm_res", B._p(Ad), B._p(Wd), B._p(bd), B._p(resd), ldr, B._p(D), M, N, K, None)
     torch.cuda.synchronize()
     out = D.cpu()[:, :N] if inplace else D.cpu()
@@ -70,7 +84,7 @@ def test_gemm_geglu_and_silu():
     v = torch.cat([full[:, 128 * j:128 * j + 64] for j in range(N // 128)], 1)
     gt = torch.cat([full[:, 128 * j + 64:128 * j + 128] for j in range(N // 128)], 1)
     ref = v * F.gelu(gt)
-    D = torch.empty(M, N // 2, device="cuda", dtype=torch.bfloat16)
+    D = torch.empty(M, N // 2, device="cuda", dtype=DT)
     B.debug_gemm(bf(A).cuda(), bf(Wt).cuda(), bias.cuda(), D, M, N, K, act=B.ACT_GEGLU)
     S = torch.empty(M, N, device="cuda", dtype=torch.float32)
     B.debug_gemm(bf(A).cuda(), bf(Wt).cuda(), bias.cuda(), S, M, N, K, out_f32=1, act=B.ACT_SILU)
@@ -104,7 +118,7 @@ def test_conv3x3(nb, h, w, cin, cout):
     temb = torch.randn(nb, cout, generator=g)
     res = bf(torch.randn(nb, h, w, cout, generator=g))
     ref = _conv_ref(x.float(), wt.float(), b, temb, res.float())
-    y = torch.empty(nb, h, w, cout, device="cuda", dtype=torch.bfloat16)
+    y = torch.empty(nb, h, w, cout, device="cuda", dtype=DT)
     B.debug_conv3x3(x.cuda(), cin, None, 0, _to_dev_w(wt), None, b.cuda(), temb.cuda(), res.cuda(), y, nb, h, w, cout)
     torch.cuda.synchronize()
     assert rel(y.cpu(), ref) < 6e-3
@@ -120,7 +134,7 @@ def test_conv3x3_stride2(nb, h, w, cin, cout):
     wt = bf(torch.randn(cout, cin, 3, 3, generator=g) / (9 * cin) ** 0.5)
     b = torch.randn(cout, generator=g)
     ref = F.conv2d(x.double().permute(0, 3, 1, 2), wt.double(), b.double(), stride=2, padding=1).permute(0, 2, 3, 1)
-    y = torch.empty(nb, h // 2, w // 2, cout, device="cuda", dtype=torch.bfloat16)
+    y = torch.empty(nb, h // 2, w // 2, cout, device="cuda", dtype=DT)
     xd, wd, bd = x.cuda(), _to_dev_w(wt), b.cuda()
     B.call("sd_debug_conv3x3_s2", B._p(xd), cin, B._p(wd), B._p(bd), B._p(y), nb, h, w, cout, None)
     torch.cuda.synchronize()
@@ -146,7 +160,7 @@ def test_conv3x3_splitk(splits, nb, h, w, c1, c2, cout):
                w2=_to_dev_w(wt[:, c1:]) if c2 else None, b=b.cuda(), temb=temb.cuda(), res=res.cuda())
 
     def run(n):
-        y = torch.empty(n, h, w, cout, device="cuda", dtype=torch.bfloat16)
+        y = torch.empty(n, h, w, cout, device="cuda", dtype=DT)
         B.debug_conv3x3(dev["x1"][:n], c1, None if x2 is None else dev["x2"][:n], c2, dev["w1"], dev["w2"], dev["b"],
                         dev["temb"][:n], dev["res"][:n], y, n, h, w, cout)
         torch.cuda.synchronize()
@@ -169,7 +183,7 @@ def test_conv3x3_concat():
     wt = bf(torch.randn(cout, c1 + c2, 3, 3, generator=g) / (9 * (c1 + c2)) ** 0.5)
     b = torch.randn(cout, generator=g)
     ref = _conv_ref(torch.cat([x1, x2], -1).float(), wt.float(), b, None, None)
-    y = torch.empty(nb, h, w, cout, device="cuda", dtype=torch.bfloat16)
+    y = torch.empty(nb, h, w, cout, device="cuda", dtype=DT)
     B.debug_conv3x3(x1.cuda(), c1, x2.cuda(), c2, _to_dev_w(wt[:, :c1]), _to_dev_w(wt[:, c1:]), b.cuda(), None, None,
                     y, nb, h, w, cout)
     torch.cuda.synchronize()
@@ -195,7 +209,7 @@ def _attn_ref(q, k, v, heads):
 def test_attention_mma(R, heads, d, L, S):
     g = torch.Generator().manual_seed(L + S + d)
     C = heads * d
-    q, k, v = (bf(torch.randn(R, n, C, generator=g)) for n in (L, S, S))
+    q, k, v = (torch.randn(R, n, C, generator=g).to(torch.bfloat16) for n in (L, S, S))  # bf16-only kernel
     o = torch.empty(R, L, C, device="cuda", dtype=torch.bfloat16)
     qd, kd, vd = q.cuda(), k.cuda(), v.cuda()       # keep the device copies alive across the call
     B.call("sd_debug_attention", B._p(qd), B._p(kd), B._p(vd), B._p(o), R, heads, d, L, S, None)
@@ -262,7 +276,7 @@ def test_groupnorm(nb, P, C, G, silu):
     ref = F.group_norm(x.double().permute(0, 2, 1), G, gam.double(), bet.double(), 1e-5).permute(0, 2, 1)
     if silu:
         ref = F.silu(ref)
-    y = torch.empty(nb, P, C, device="cuda", dtype=torch.bfloat16)
+    y = torch.empty(nb, P, C, device="cuda", dtype=DT)
     xd, gd, bd = x.cuda(), gam.cuda(), bet.cuda()
     B.call("sd_debug_groupnorm", B._p(xd), B._p(y), nb, P, C, G, B._p(gd), B._p(bd), 1e-5, silu, None)
     torch.cuda.synchronize()
@@ -275,7 +289,7 @@ def test_layernorm(T, C):
     x = bf(torch.randn(T, C, generator=g) * 3 - 1)
     gam, bet = 1 + 0.1 * torch.randn(C, generator=g), 0.1 * torch.randn(C, generator=g)
     ref = F.layer_norm(x.double(), (C,), gam.double(), bet.double(), 1e-5)
-    y = torch.empty(T, C, device="cuda", dtype=torch.bfloat16)
+    y = torch.empty(T, C, device="cuda", dtype=DT)
     xd, gd, bd = x.cuda(), gam.cuda(), bet.cuda()
     B.call("sd_debug_layernorm", B._p(xd), B._p(y), T, C, B._p(gd), B._p(bd), 1e-5, None)
     torch.cuda.synchronize()
