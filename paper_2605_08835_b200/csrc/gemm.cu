@@ -316,7 +316,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
         }
         if (g.gelu_tanh) {
           // GELU(x) ≈ ½x(1 + tanh(√(2/π)(x + 0.044715x³))): |Δ| ≤ 4.7e-4 from the erf form, plus the
-          // tanh.approx error (≤ ½|x|·2^-10.9) — below one bf16 ulp of the output; 6 instructions instead
+          // tanh.approx error (≤ ½|x|·2^-10.9 absolute; not below an ulp for negative x, DESIGN R33); 6 instructions instead
           // of the 15 of the erf polynomial (the FF1 epilogue was issue-bound: 64 % issue, 36 % tensor
           // pipe) → FF1 at 64×64: 135 → 109 µs
 #pragma unroll
