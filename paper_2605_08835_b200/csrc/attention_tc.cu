@@ -729,7 +729,7 @@ static void attention_tc16(const TcSrc& sr, bf16* O, int ldo, int rows, int head
     case 64:  // SD_ATTN_EMU=8 (default): the d = 40 structure — two CTAs per SM, two softmax threads per
               // row, one TMEM pass, P in TMEM (S 128 | O 64 | P 64 columns): SDXL [16,10,64,4096] 1.27 → 1.16
               // ms vs NB = 2 / one thread per row (which was 1.18× faster than NB = 1 with P in smem)
-      if (attn_emu() == 8 && attn_ef(f16) == 3)
+      if (attn_emu() == 8 && getenv("SD_ATTN_EF") && attn_ef(f16) == 3)  // measured: EF 8 faster at d = 64
         launch_tc<64, 1, 2, 3, 4>(sr, O, ldo, rows, heads, P, st, f16);
       else if (attn_emu() == 8)
         launch_tc<64, 1, 2, 0, 4>(sr, O, ldo, rows, heads, P, st, f16);
@@ -742,7 +742,7 @@ static void attention_tc16(const TcSrc& sr, bf16* O, int ldo, int rows, int head
       break;
     case 80:  // SD_ATTN_EMU=8 (default): two softmax threads per row, one TMEM pass, P in TMEM; S | O | P
               // need 272 columns, so one CTA per SM (512 allocated): [16,8,80,1024] 87.9 → 83.1 µs
-      if (attn_emu() == 8 && attn_ef(f16) == 3)
+      if (attn_emu() == 8 && getenv("SD_ATTN_EF") && attn_ef(f16) == 3)  // measured: EF 8 faster at d = 80
         launch_tc<80, 1, 2, 3, 4>(sr, O, ldo, rows, heads, P, st, f16);
       else if (attn_emu() == 8)
         launch_tc<80, 1, 2, 0, 4>(sr, O, ldo, rows, heads, P, st, f16);
