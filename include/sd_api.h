@@ -392,6 +392,23 @@ sd_status sd_debug_xattention_tc(const void* q, const void* kc, int32_t ldk, int
 /* GroupNorm(+SiLU) over x bf16 [nb][P][C] (NHWC), G groups, fp32 gamma/beta; LayerNorm over x [T][C]. */
 sd_status sd_debug_groupnorm(const void* x, void* y, int32_t nb, int32_t P, int32_t C, int32_t G, const float* gamma,
                              const float* beta, float eps, int32_t silu, void* stream);
+/* GroupNorm statistics from the producer's epilogue (fusions; the GroupNorm
+ * definition PAPER.md:146-148 / SURVEY §2.4 K8 is unchanged — only where its sums are taken moves).
+ * sd_debug_conv3x3_gn / sd_debug_gemm_gn: the conv (one source, optional residual) / dense GEMM of
+ * sd_debug_conv3x3 / sd_debug_gemm_res, which also writes gn_part = device fp32 [nb][P/32][cout][2]:
+ * (sum, sum of squares) of each channel over each 32-pixel slot of the STORED 16-bit output (conv: the
+ * slot is a box of min(wt, 32) x 32/min(wt, 32) pixels of the conv tile geometry; dense: 32 consecutive
+ * rows of one image of P rows). SD_E_INVAL if the launch cannot emit them (output channels % 32, a
+ * slot straddling two images, split-K). sd_debug_groupnorm_parts: GroupNorm(+SiLU) of the channel concat
+ * [x0 (C0) | x1 (C1), optional] from those statistics (one finalize launch + the apply; no statistics
+ * pass), same output as sd_debug_groupnorm up to summation order. All buffers device, caller-owned. */
+sd_status sd_debug_conv3x3_gn(const void* x, int32_t cin, const void* w, const float* bias, const void* res, void* y,
+                              int32_t nb, int32_t h, int32_t wd, int32_t cout, float* gn_part, void* stream);
+sd_status sd_debug_gemm_gn(const void* A, const void* B, const float* bias, const void* res, void* D, int32_t M,
+                           int32_t N, int32_t K, int32_t P, float* gn_part, void* stream);
+sd_status sd_debug_groupnorm_parts(const void* x0, int32_t C0, const float* part0, const void* x1, int32_t C1,
+                                   const float* part1, void* y, int32_t nb, int32_t P, int32_t G, const float* gamma,
+                                   const float* beta, float eps, int32_t silu, void* stream);
 sd_status sd_debug_layernorm(const void* x, void* y, int32_t T, int32_t C, const float* gamma, const float* beta,
                              float eps, void* stream);
 /* sd_debug_step_eps: the UNet part of sd_step_batch only (K11 gather → UNet), with the same rows as

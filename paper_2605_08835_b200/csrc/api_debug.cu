@@ -242,6 +242,84 @@ extern "C" sd_status sd_debug_groupnorm(const void* x, void* y, int32_t nb, int3
   SD_API_END
 }
 
+extern "C" sd_status sd_debug_conv3x3_gn(const void* x, int32_t cin, const void* w, const float* bias, const void* res,
+                                         void* y, int32_t nb, int32_t h, int32_t wd, int32_t cout, float* gn_part,
+                                         void* stream) {
+  SD_REQUIRE(x && w && y && gn_part && cin > 0 && cout > 0 && nb > 0 && h > 0 && wd > 0,
+             "sd_debug_conv3x3_gn: bad arguments");
+  SD_API_BEGIN
+  sd::GemmDesc d;
+  d.mode = sd::GEMM_CONV3;
+  d.xs[0] = static_cast<const bf16*>(x);
+  d.cs[0] = cin;
+  d.Bw[0] = static_cast<const bf16*>(w);
+  d.B = nb;
+  d.H = h;
+  d.W = wd;
+  d.N = cout;
+  d.out = y;
+  d.ldo = cout;
+  d.bias = bias;
+  d.res = static_cast<const bf16*>(res);
+  d.ldr = cout;
+  d.splits = 1;
+  d.f16 = g_dbg_f16;
+  d.gn_part = reinterpret_cast<float2*>(gn_part);
+  if (!sd::gemm_gn_ok(d)) throw std::invalid_argument("sd_debug_conv3x3_gn: launch cannot emit GroupNorm statistics");
+  sd::gemm(d, static_cast<cudaStream_t>(stream));
+  SD_API_END
+}
+
+extern "C" sd_status sd_debug_gemm_gn(const void* A, const void* B, const float* bias, const void* res, void* D,
+                                      int32_t M, int32_t N, int32_t K, int32_t P, float* gn_part, void* stream) {
+  SD_REQUIRE(A && B && D && gn_part && M > 0 && N > 0 && K > 0 && K % 8 == 0 && P > 0,
+             "sd_debug_gemm_gn: bad arguments");
+  SD_API_BEGIN
+  sd::GemmDesc d;
+  d.A = static_cast<const bf16*>(A);
+  d.M = M;
+  d.K = K;
+  d.lda = K;
+  d.Bw[0] = static_cast<const bf16*>(B);
+  d.N = N;
+  d.ldb = K;
+  d.out = D;
+  d.ldo = N;
+  d.bias = bias;
+  d.res = static_cast<const bf16*>(res);
+  d.ldr = N;
+  d.f16 = g_dbg_f16;
+  d.gn_part = reinterpret_cast<float2*>(gn_part);
+  d.gn_P = P;
+  if (!sd::gemm_gn_ok(d)) throw std::invalid_argument("sd_debug_gemm_gn: launch cannot emit GroupNorm statistics");
+  sd::gemm(d, static_cast<cudaStream_t>(stream));
+  SD_API_END
+}
+
+extern "C" sd_status sd_debug_groupnorm_parts(const void* x0, int32_t C0, const float* part0, const void* x1,
+                                              int32_t C1, const float* part1, void* y, int32_t nb, int32_t P,
+                                              int32_t G, const float* gamma, const float* beta, float eps,
+                                              int32_t silu, void* stream) {
+  SD_REQUIRE(x0 && part0 && y && gamma && beta && nb > 0 && P > 0 && P % 32 == 0 && C0 > 0 && G > 0,
+             "sd_debug_groupnorm_parts: bad arguments");
+  SD_REQUIRE(!x1 || (part1 && C1 > 0), "sd_debug_groupnorm_parts: second source needs its statistics");
+  SD_API_BEGIN
+  const int C = C0 + (x1 ? C1 : 0);
+  void* ws = nullptr;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  SD_CUDA(cudaMallocAsync(&ws, sd::gn_workspace_bytes(nb, P, G, C), st));
+  const float2* p0 = reinterpret_cast<const float2*>(part0);
+  const float2* p1 = reinterpret_cast<const float2*>(part1);
+  if (g_dbg_f16)
+    sd::group_norm_parts(static_cast<const f16*>(x0), C0, p0, static_cast<const f16*>(x1), C1, p1,
+                         static_cast<f16*>(y), nb, P, G, gamma, beta, eps, silu != 0, ws, st);
+  else
+    sd::group_norm_parts(static_cast<const bf16*>(x0), C0, p0, static_cast<const bf16*>(x1), C1, p1,
+                         static_cast<bf16*>(y), nb, P, G, gamma, beta, eps, silu != 0, ws, st);
+  SD_CUDA(cudaFreeAsync(ws, st));
+  SD_API_END
+}
+
 extern "C" sd_status sd_debug_layernorm(const void* x, void* y, int32_t T, int32_t C, const float* gamma,
                                         const float* beta, float eps, void* stream) {
   SD_REQUIRE(x && y && gamma && beta && T > 0 && C > 0 && C % 8 == 0, "sd_debug_layernorm: bad arguments");

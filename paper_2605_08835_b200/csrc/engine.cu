@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <stdlib.h>
 #include <type_traits>
+#include <unordered_map>
 
 #include <nvtx3/nvToolsExt.h>
 #include "engine.h"
@@ -497,14 +498,15 @@ void build_engine(Engine* e) {
   e->use_graphs = !(ng && ng[0] == '1');
   const char* at = getenv("SD_ATTN_TC");
   e->use_attn_tc = !(at && at[0] == '0') && !e->f32;
-  // SD_XATTN_TC=1: cross-attention on the tcgen05 kernel. Off by default: with 77 keys one CTA does a
-  // single 128×128 score tile, and the per-CTA setup (TMEM alloc, barriers, K/V load) outweighs it — the
-  // mma.sync kernel that keeps K/V resident across query tiles measured faster (64²: 55 vs 71 µs)
+  // SD_XATTN_TC=1: cross-attention at d ≤ 80 on the general tcgen05 flash kernel (one CTA per 128-query
+  // tile; with 77 keys its per-CTA setup dominates: 64² 71 µs) instead of the persistent one below
   const char* xt = getenv("SD_XATTN_TC");
   e->use_xattn_tc = e->use_attn_tc && (xt && xt[0] == '1');
-  // the persistent tcgen05 cross-attention (K / Vᵀ resident across query tiles): SD_XATTN_TC2=1 enables it
+  // the persistent tcgen05 cross-attention (xattention_tc.cu: K / Vᵀ resident across a run of query
+  // tiles, P in place of S in TMEM, two CTAs per SM) for d = 40 / 64 / 80; SD_XATTN_TC2=0 falls back to
+  // the mma.sync kernel of attention.cu
   const char* x2 = getenv("SD_XATTN_TC2");
-  e->use_xattn_tc2 = e->use_attn_tc && (x2 && x2[0] == '1');
+  e->use_xattn_tc2 = e->use_attn_tc && !(x2 && x2[0] == '0');
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -625,9 +627,41 @@ struct Fwd {
 
   AT* buf(long elems) { return e->ws.get<AT>((size_t)elems); }
 
+  // GroupNorm statistics emitted by the producing conv / GEMM epilogue (GemmDescT::gn_part), keyed by
+  // the output tensor. Every GroupNorm input of the UNet is written by conv() / linear() / gemm_out(),
+  // and each of those updates its output's entry (set, or erased when the launch cannot emit them),
+  // so a lookup never sees statistics of an older tensor at a reused address. Whether a launch emits
+  // them depends only on the layer (gemm_gn_ok), never on the batch: batch invariance holds (I5).
+  std::unordered_map<const void*, const float2*> gnp;
+  bool gn_epi = false;  // SD_GN_EPI (default on for 16-bit activations)
+  // statistics buffer for an output of `pixels` rows × C channels; allocate it next to the output so it
+  // lives exactly as long
+  float2* gn_buf(long pixels, int C) {
+    if (!gn_epi) return nullptr;
+    return e->ws.get<float2>((size_t)((pixels + 31) / 32) * C);
+  }
+  template <class D>
+  void gn_note(D& d, const void* out, float2* gp) {
+    if (gp && gemm_gn_ok(d)) {
+      d.gn_part = gp;
+      gnp[out] = gp;
+    } else {
+      gnp.erase(out);
+    }
+  }
+  const float2* gn_of(const void* x) const {
+    auto it = gnp.find(x);
+    return it == gnp.end() ? nullptr : it->second;
+  }
+
   void gn(const AT* x, AT* y, int P, int C, const float* g, const float* b, float eps, bool silu) {
-    const int pi = e->prof.begin(PC_GN, st, 3.0 * R * P * C * 2);
-    group_norm(x, y, R, P, C, e->uc.groups, g, b, eps, silu, gn_ws, st);
+    const float2* gp = gn_of(x);
+    const int pi = e->prof.begin(PC_GN, st, (gp ? 2.0 : 3.0) * R * P * C * 2);
+    if (gp)
+      group_norm_parts(x, C, gp, (const AT*)nullptr, 0, (const float2*)nullptr, y, R, P, e->uc.groups, g, b, eps, silu,
+                       gn_ws, st);
+    else
+      group_norm(x, y, R, P, C, e->uc.groups, g, b, eps, silu, gn_ws, st);
     e->prof.end(pi, st);
   }
   void ln(const AT* x, AT* y, long T, int C, const float* g, const float* b) {
@@ -641,7 +675,8 @@ struct Fwd {
     e->prof.end(pi, st);
   }
   void linear(const AT* A, long M, int K, const AT* W, int N, const float* bias, void* out, int ldo,
-              const AT* res = nullptr, int act = ACT_NONE, int out_f32 = 0, int cls = PC_GEMM) {
+              const AT* res = nullptr, int act = ACT_NONE, int out_f32 = 0, int cls = PC_GEMM, float2* gp = nullptr,
+              int gn_P = 0) {
     GemmDescT<AT> d;
     d.A = A;
     d.M = (int)M;
@@ -657,6 +692,8 @@ struct Fwd {
     d.ldr = ldo;
     d.act = act;
     d.out_f32 = out_f32;
+    d.gn_P = gn_P;
+    gn_note(d, out, gp);
     const int pi = e->prof.begin(cls, st, 2.0 * M * N * K);
     gemm(d, st);
     e->prof.end(pi, st);
@@ -664,7 +701,7 @@ struct Fwd {
   // 3×3 conv, pad 1; H × W is the OUTPUT size (the input is stride·H × stride·W)
   void conv(const AT* x, int H, int W, int C, const AT* w, int N, const float* bias, void* out,
             const float* temb = nullptr, const AT* res = nullptr, int out_f32 = 0, int ldo = 0, int c_real = 0,
-            int stride = 1) {
+            int stride = 1, float2* gp = nullptr) {
     GemmDescT<AT> d;
     d.mode = GEMM_CONV3;
     d.stride = stride;
@@ -686,6 +723,7 @@ struct Fwd {
     const size_t mk = e->ws.mark();
     d.split_ws_bytes = gemm_split_ws_bytes(d);
     if (d.split_ws_bytes) d.split_ws = e->ws.get<float>(d.split_ws_bytes / sizeof(float));
+    gn_note(d, out, gp);
     const int pi = e->prof.begin(PC_CONV, st, 2.0 * R * H * W * N * 9.0 * (c_real ? c_real : C));
     gemm(d, st);
     e->prof.end(pi, st);
@@ -698,19 +736,26 @@ struct Fwd {
     const int P = H * W;
     const size_t mk = e->ws.mark();
     AT* out = buf((long)R * P * r.cout);  // allocated below the scratch mark
+    float2* out_gp = gn_buf((long)R * P, r.cout);
     const size_t mk2 = e->ws.mark();
     (void)mk;
     AT* a = buf((long)R * P * r.cin);
     if (x1) {
       if (!r.wsc) throw std::logic_error("two-source resblock needs the 1x1 shortcut");
-      const int pi = e->prof.begin(PC_GN, st, 3.0 * R * P * r.cin * 2);
-      group_norm2(x, r.cin - C1, x1, C1, a, R, P, e->uc.groups, r.n1g, r.n1b, e->uc.eps_res, true, gn_ws, st);
+      const float2 *g0 = gn_of(x), *g1 = gn_of(x1);
+      const int pi = e->prof.begin(PC_GN, st, (g0 && g1 ? 2.0 : 3.0) * R * P * r.cin * 2);
+      if (g0 && g1)
+        group_norm_parts(x, r.cin - C1, g0, x1, C1, g1, a, R, P, e->uc.groups, r.n1g, r.n1b, e->uc.eps_res, true,
+                         gn_ws, st);
+      else
+        group_norm2(x, r.cin - C1, x1, C1, a, R, P, e->uc.groups, r.n1g, r.n1b, e->uc.eps_res, true, gn_ws, st);
       e->prof.end(pi, st);
     } else {
       gn(x, a, P, r.cin, r.n1g, r.n1b, e->uc.eps_res, true);
     }
     AT* h1 = buf((long)R * P * r.cout);
-    conv(a, H, W, r.cin, wt<AT>(r.w1), r.cout, r.b1, h1, temb_all + r.temb_off);
+    conv(a, H, W, r.cin, wt<AT>(r.w1), r.cout, r.b1, h1, temb_all + r.temb_off, nullptr, 0, 0, 0, 1,
+         gn_buf((long)R * P, r.cout));
     AT* a2 = buf((long)R * P * r.cout);
     gn(h1, a2, P, r.cout, r.n2g, r.n2b, e->uc.eps_res, true);
     const AT* sc = x;
@@ -732,6 +777,7 @@ struct Fwd {
       d.out = s;
       d.ldo = r.cout;
       d.bias = r.bsc;
+      gn_note(d, s, nullptr);
       const int pi = e->prof.begin(PC_CONV1, st, 2.0 * R * P * r.cout * r.cin);
       gemm(d, st);
       e->prof.end(pi, st);
@@ -741,7 +787,7 @@ struct Fwd {
       linear(x, (long)R * P, r.cin, wt<AT>(r.wsc), r.cout, r.bsc, s, r.cout, nullptr, ACT_NONE, 0, PC_CONV1);
       sc = s;
     }
-    conv(a2, H, W, r.cout, wt<AT>(r.w2), r.cout, r.b2, out, nullptr, sc);
+    conv(a2, H, W, r.cout, wt<AT>(r.w2), r.cout, r.b2, out, nullptr, sc, 0, 0, 0, 1, out_gp);
     e->ws.reset(mk2);
     return out;
   }
@@ -751,6 +797,7 @@ struct Fwd {
     const long T = (long)R * P;
     const int heads = e->uc.heads_at(C), dh = C / heads;
     AT* out = buf(T * C);
+    float2* out_gp = gn_buf(T, C);
     const size_t mk = e->ws.mark();
     AT* a = buf(T * C);
     gn(x, a, P, C, t.gng, t.gnb, e->uc.eps_tf, false);
@@ -803,9 +850,9 @@ struct Fwd {
       bool xtc = false, xtc2 = false;
       if constexpr (!std::is_same<AT, float>::value) {
         xtc2 = e->use_xattn_tc2 && e->vt_cache && xattention_tc2_supported(dh, e->uc.ctx_len);
-        // d = 160 at P ≥ 128 (the 16×16 level): the general tcgen05 kernel beats mma.sync (13.5 vs 14.3 µs);
-        // at d ≤ 80 and at the 8×8 mid block mma.sync is faster for 77 keys
-        const bool pick = e->use_xattn_tc || (e->use_attn_tc && dh == 160 && P >= 128);
+        // d = 160 (the 16×16 level and the 8×8 mid block): the general tcgen05 kernel (16×16: 13.5 vs
+        // 14.3 µs on mma.sync)
+        const bool pick = e->use_xattn_tc || (e->use_attn_tc && dh == 160);
         xtc = !xtc2 && pick && e->vt_cache && attention_tc_supported(dh, 128, C);
       }
       if (xtc2) {
@@ -853,7 +900,7 @@ struct Fwd {
       e->ws.reset(mb);
       std::swap(h, hb);
     }
-    linear(h, T, C, wt<AT>(t.wpout), C, t.bpout, out, C, x, ACT_NONE, 0, PC_CONV1);  // proj_out + the input
+    linear(h, T, C, wt<AT>(t.wpout), C, t.bpout, out, C, x, ACT_NONE, 0, PC_CONV1, out_gp, P);  // proj_out + the input
     e->ws.reset(mk);
     return out;
   }
@@ -866,6 +913,7 @@ static void unet_forward(Engine* e, cudaStream_t st, int R, int H, int W, const 
   UNetW& U = e->U;
   Fwd<AT> f{e, st, R, nullptr, kv_index, nullptr};
   f.gn_ws = e->gn_ws;
+  f.gn_epi = !std::is_same<AT, float>::value && gn_epilogue_on();
   const int T = c.temb_dim(), C0 = c.block_out[0];
   // time embedding: sinusoid → linear_1 → SiLU → linear_2 → SiLU (the ResBlocks consume SiLU(temb))
   AT* sinus = f.buf((long)R * C0);
@@ -904,7 +952,8 @@ static void unet_forward(Engine* e, cudaStream_t st, int R, int H, int W, const 
 
   int h = H, w = W;
   AT* x = f.buf((long)R * h * w * C0);
-  f.conv(x_in, h, w, 64, wt<AT>(U.conv_in_w), C0, U.conv_in_b, x, nullptr, nullptr, 0, 0, c.in_ch);
+  float2* x_gp = f.gn_buf((long)R * h * w, C0);
+  f.conv(x_in, h, w, 64, wt<AT>(U.conv_in_w), C0, U.conv_in_b, x, nullptr, nullptr, 0, 0, c.in_ch, 1, x_gp);
   struct Skip {
     AT* p;
     int C;
@@ -923,12 +972,13 @@ static void unet_forward(Engine* e, cudaStream_t st, int R, int H, int W, const 
       const int ho = (h + 1) / 2, wo = (w + 1) / 2;
       const size_t mk = e->ws.mark();
       AT* out = f.buf((long)R * ho * wo * C);
+      float2* out_gp = f.gn_buf((long)R * ho * wo, C);
       const size_t mk2 = e->ws.mark();
       if constexpr (!std::is_same<AT, float>::value) {
         // 3×3 / stride 2 / pad 1 as an implicit GEMM whose TMA boxes step 2 input pixels per output
         // pixel (element strides), so the taps are never materialised
         if (h % 2 || w % 2) throw std::invalid_argument("downsampler: odd spatial size");
-        f.conv(x, ho, wo, C, wt<AT>(d.wdown), C, d.bdown, out, nullptr, nullptr, 0, 0, 0, 2);
+        f.conv(x, ho, wo, C, wt<AT>(d.wdown), C, d.bdown, out, nullptr, nullptr, 0, 0, 0, 2, out_gp);
       } else {
         AT* cols = f.buf((long)R * ho * wo * 9 * C);
         im2col_s2(x, cols, R, h, w, C, st);
@@ -966,7 +1016,7 @@ static void unet_forward(Engine* e, cudaStream_t st, int R, int H, int W, const 
       h *= 2;
       w *= 2;
       AT* out = f.buf((long)R * h * w * C);
-      f.conv(upx, h, w, C, wt<AT>(u.wup), C, u.bup, out);
+      f.conv(upx, h, w, C, wt<AT>(u.wup), C, u.bup, out, nullptr, nullptr, 0, 0, 0, 1, f.gn_buf((long)R * h * w, C));
       x = out;
     }
   }

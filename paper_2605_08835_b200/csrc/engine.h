@@ -122,6 +122,17 @@ struct VAEW {
 };
 
 // one VAE work item: op over a band of output rows [y0, y1) (R7 V1)
+// SD_GN_EPI=0: GroupNorm statistics by the separate statistics pass instead of the producers' conv /
+// GEMM epilogues (gemm.cu gn_colstats)
+inline bool gn_epilogue_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("SD_GN_EPI");
+    v = !(s && s[0] == '0');
+  }
+  return v != 0;
+}
+
 struct VItem {
   int op;          // VOP_*
   int a, b, c;     // buffer ids (src, dst, extra)
@@ -131,6 +142,9 @@ struct VItem {
   int gn;          // GN layer index (partials slot)
   int silu;
   const void* p1 = nullptr;
+  // GN_STATS / GN_APPLY: the statistics come from the producer's epilogue (DecodeState::gn_part; the
+  // stats item is a no-op); CONV: this launch writes them for the next GroupNorm
+  int gnf = 0;
 };
 
 struct DecodeState;

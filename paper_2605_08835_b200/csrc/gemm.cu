@@ -49,6 +49,12 @@ struct GemmArgs {
   int dbg;            // experiment switch (SD_EPI_DBG): 1 = no store, 2 = no bias, 3 = no TMEM load
   int splits, kps;    // split-K: K blocks [s·kps, (s+1)·kps) of split s
   float* part;        // split-K fp32 partials [splits][M][N] (raw accumulators)
+  // GroupNorm statistics of the stored output (the consumer's GN skips its statistics pass): per
+  // 32-pixel output quarter ("slot", wholly inside one image) and channel, (Σy, Σy²) over the quarter's
+  // 32 stored 16-bit values → gn_part[(img · gn_slots + slot) · N + n] (float2). Slot of a conv quarter
+  // box sw × sh at (x, y): (y / sh) · (W / sw) + x / sw; of a dense quarter: (row mod gn_P) / 32.
+  float2* gn_part;
+  int gn_P, gn_slots, gn_sw, gn_sh;
 };
 
 // tile t → (M tile, N tile, K-block range); tiles of split s follow those of split s-1
@@ -204,6 +210,38 @@ __device__ __forceinline__ void bulk_wait_read() {
 }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// (Σy, Σy²) per column of a staged 32×32 16-bit sub-tile (64-byte rows, 64B swizzle as written by
+// stage_store): lane (h, w) reads the column pair w (channels 2w, 2w+1) of rows 2k + h, k = 0..15 — the
+// two rows of one LDS are the two halves of one 128-byte line, so every load is bank-conflict free — then
+// one xor-16 exchange; lanes 0..15 store (S_2w, Q_2w, S_2w+1, Q_2w+1). Fixed order: deterministic.
+template <bool F16>
+__device__ __forceinline__ void gn_colstats(const uint8_t* buf, int lane, float2* dst) {
+  const int h = lane >> 4, w = lane & 15;
+  float s0 = 0.f, s1 = 0.f, q0 = 0.f, q1 = 0.f;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const int r = 2 * k + h;
+    const uint32_t u = *reinterpret_cast<const uint32_t*>(buf + r * 64 + (((w >> 2) ^ (k & 3)) << 4) + (w & 3) * 4);
+    float a, b;
+    if (F16) {
+      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&u));
+      a = f.x, b = f.y;
+    } else {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u));
+      a = f.x, b = f.y;
+    }
+    s0 += a;
+    s1 += b;
+    q0 = fmaf(a, a, q0);
+    q1 = fmaf(b, b, q1);
+  }
+  s0 += __shfl_xor_sync(0xffffffff, s0, 16);
+  s1 += __shfl_xor_sync(0xffffffff, s1, 16);
+  q0 += __shfl_xor_sync(0xffffffff, q0, 16);
+  q1 += __shfl_xor_sync(0xffffffff, q1, 16);
+  if (lane < 16) reinterpret_cast<float4*>(dst)[w] = make_float4(s0, q0, s1, q1);
+}
+
 struct EpiCtx {
   uint8_t* stage;   // this warp's 2 × 2 KB staging slabs
   int slot;         // alternating slab
@@ -215,7 +253,7 @@ struct EpiCtx {
 // write 32 fp32 values (this lane's row, columns [col, col+32)) to the staging slab and TMA-store it
 template <int MODE, bool F16>
 __device__ __forceinline__ void stage_store(const GemmArgs& g, const CUtensorMap* om, EpiCtx& ec, const float* o,
-                                            int col, int lane, bool slab_ready = false) {
+                                            int col, int lane, bool slab_ready = false, float2* gn_dst = nullptr) {
   uint8_t* buf = ec.stage + ec.slot * 2048;
   if (!slab_ready) {
     if (lane == 0) bulk_wait_read<1>();    // the store issued two chunks ago has finished reading
@@ -237,6 +275,7 @@ __device__ __forceinline__ void stage_store(const GemmArgs& g, const CUtensorMap
       tma_store_4d(om, buf, col, ec.sx, ec.sy, ec.sb);
     bulk_commit();
   }
+  if (gn_dst) gn_colstats<F16>(buf, lane, gn_dst);  // the slab is only read: concurrent with the TMA store
   ec.slot ^= 1;
 }
 
@@ -288,6 +327,22 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
     ec.sx = tx * g.wt + r0 % g.wt;
     ec.sy = ty * g.ht + (r0 / g.wt) % g.ht;
     ec.sb = tb * g.bt + r0 / (g.wt * g.ht);
+  }
+  // GN statistics slot of this warp's 32-row quarter (warp-uniform; the host checked that a quarter
+  // never straddles two images and that whole quarters are in or out of range)
+  int gq_img = 0, gq_slot = 0;
+  bool gq_valid = false;
+  if (g.gn_part) {
+    if (MODE == GEMM_DENSE) {
+      const long r0 = (long)mbox * 128 + q * 32;
+      gq_valid = r0 < g.M;
+      gq_img = (int)(r0 / g.gn_P);
+      gq_slot = (int)(r0 - (long)gq_img * g.gn_P) >> 5;
+    } else {
+      gq_valid = ec.sb < g.B;
+      gq_img = ec.sb;
+      gq_slot = (ec.sy / g.gn_sh) * (g.W / g.gn_sw) + ec.sx / g.gn_sw;
+    }
   }
   mbar_wait(tfull, tphase);
   tc_fence_after();
@@ -442,7 +497,9 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
     if (g.dbg == 1) {
       if (o[0] == 12345.f) g.res ? (void)0 : __trap();
     } else if (g.tma_store) {
-      stage_store<MODE, F16>(g, om, ec, o, col, lane, rt);
+      float2* gd = nullptr;
+      if (g.gn_part && gq_valid) gd = g.gn_part + ((long)gq_img * g.gn_slots + gq_slot) * g.N + col;
+      stage_store<MODE, F16>(g, om, ec, o, col, lane, rt, gd);
     } else if (valid) {
       if (g.out_f32) {
         float* op = reinterpret_cast<float*>(g.out) + prow * g.ldo + g.col_off + col;
@@ -881,7 +938,17 @@ size_t gemm_split_ws_bytes(const GemmDesc& d) {
   return (size_t)s * d.B * d.H * d.W * d.N * sizeof(float);
 }
 
+bool gemm_gn_ok(const GemmDesc& d) {
+  if (d.out_f32 || d.act == ACT_GEGLU || d.col_off || d.ldo != d.N || d.N % 32 || d.bias_per_row) return false;
+  if (gemm_splits(d) > 1) return false;
+  if (d.mode == GEMM_DENSE) return d.gn_P > 0 && d.gn_P % 32 == 0 && d.M % d.gn_P == 0;
+  int wt, ht, bt;
+  conv3_tile_geometry(d.B, d.H, d.W, &wt, &ht, &bt);
+  return wt * ht >= 32 && d.W % wt == 0 && d.H % ht == 0;
+}
+
 void gemm(const GemmDesc& d, cudaStream_t st) {
+  if (d.gn_part && !gemm_gn_ok(d)) throw CudaError("gemm: GroupNorm statistics requested for an ineligible launch");
   if (g_cg_override < 0) {
     const char* s = getenv("SD_GEMM_CG");
     g_cg_override = s ? atoi(s) : 0;
@@ -933,6 +1000,14 @@ void gemm(const GemmDesc& d, cudaStream_t st) {
       a.kb_src[s] = cdiv(d.cs[s], 64);
       a.num_kb += 9 * a.kb_src[s];
     }
+  }
+  a.gn_part = d.gn_part;
+  if (d.gn_part) {
+    const int P = d.mode == GEMM_DENSE ? d.gn_P : d.H * d.W;
+    a.gn_P = P;
+    a.gn_slots = P / 32;
+    a.gn_sw = d.mode == GEMM_DENSE ? 32 : (a.wt < 32 ? a.wt : 32);
+    a.gn_sh = 32 / a.gn_sw;
   }
   a.splits = 1;
   a.kps = a.num_kb;
@@ -1046,6 +1121,7 @@ void gemm(const GemmDesc& d, cudaStream_t st) {
     a.dbg = dbg;
     if (dbg == 4) a.tma_store = 0;  // direct stores
   }
+  if (d.gn_part && !a.tma_store) throw CudaError("gemm: GroupNorm statistics need the TMA-store epilogue");
   if (a.tma_store) {
     const bf16* ob = reinterpret_cast<const bf16*>(d.out) + d.col_off;
     if (d.mode == GEMM_DENSE) {
@@ -1104,6 +1180,7 @@ static GemmDesc as16(const GemmDescT<f16>& d) {
 }
 void gemm(const GemmDescT<f16>& d, cudaStream_t st) { gemm(as16(d), st); }
 int gemm_splits(const GemmDescT<f16>& d) { return gemm_splits(as16(d)); }
+bool gemm_gn_ok(const GemmDescT<f16>& d) { return gemm_gn_ok(as16(d)); }
 size_t gemm_split_ws_bytes(const GemmDescT<f16>& d) { return gemm_split_ws_bytes(as16(d)); }
 
 }  // namespace sd

@@ -59,6 +59,11 @@ struct GemmDescT {
   float* split_ws = nullptr;
   size_t split_ws_bytes = 0;
   int f16 = 0;                // fp16 instead of bf16 (set by the GemmDescT<f16> overloads)
+  // GroupNorm statistics of the stored output for a consumer GroupNorm (gemm.cu gn_colstats): per
+  // 32-pixel quarter slot and channel, (Σy, Σy²) → gn_part[(img·(P/32) + slot)·N + n]. Needs
+  // gemm_gn_ok(d); gn_P = pixels per image (dense mode; conv3 uses H·W).
+  float2* gn_part = nullptr;
+  int gn_P = 0;
 };
 
 using GemmDesc = GemmDescT<bf16>;
@@ -71,6 +76,11 @@ int gemm_splits(const GemmDesc& d);              // the split count gemm() will 
 size_t gemm_split_ws_bytes(const GemmDesc& d);   // workspace bytes (0 when not split)
 void gemm(const GemmDescT<f16>& d, cudaStream_t st);  // SD_PREC_FP16: fp16 operands / outputs
 int gemm_splits(const GemmDescT<f16>& d);
+// whether gemm() can emit the GroupNorm statistics of this launch's output (16-bit TMA-stored output,
+// N % 32 == 0, whole 32-pixel quarters inside one image, no split-K)
+bool gemm_gn_ok(const GemmDesc& d);
+bool gemm_gn_ok(const GemmDescT<f16>& d);
+inline bool gemm_gn_ok(const GemmDescF&) { return false; }
 size_t gemm_split_ws_bytes(const GemmDescT<f16>& d);
 // M tiles of a conv3 launch whose output rows lie in [y0, y1) of image 0 (used for bands).
 void conv3_tile_geometry(int B, int H, int W, int* wt, int* ht, int* bt);

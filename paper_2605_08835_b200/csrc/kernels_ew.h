@@ -30,6 +30,17 @@ void gn_stats_range(const T* x, int P, int C, int G, int p0, int p1, void* ws, c
 template <class T>
 void gn_apply_range(const T* x, T* y, int P, int C, int G, int p0, int p1, const float* gamma, const float* beta,
                     float eps, bool silu, void* ws, cudaStream_t st);
+// GroupNorm whose statistics came from the producers' GEMM / conv epilogues (GemmDescT::gn_part):
+// part0 / part1 = [B][P/32][C0] / [B][P/32][C1] (Σy, Σy²) per 32-pixel slot and channel (P % 32 == 0).
+// One finalize launch + the apply: no statistics pass over x.
+template <class T>
+void group_norm_parts(const T* x0, int C0, const float2* part0, const T* x1, int C1, const float2* part1, T* y, int B,
+                      int P, int G, const float* gamma, const float* beta, float eps, bool silu, void* ws,
+                      cudaStream_t st);
+// banded apply (B = 1) from producer statistics; the finalize runs with the first band (p0 == 0)
+template <class T>
+void gn_apply_range_parts(const T* x, T* y, int P, int C, int G, int p0, int p1, const float2* part, const float* gamma,
+                          const float* beta, float eps, bool silu, void* ws, cudaStream_t st);
 template <class T>
 void layer_norm(const T* x, T* y, int T_, int C, const float* gamma, const float* beta, float eps, cudaStream_t st);
 

@@ -236,6 +236,103 @@ __global__ void gn_finalize_kernel(int P, int C, int G, int chunk_px, int nchunk
       eps, gamma, beta, tab + (long)b * C, g, lane);
 }
 
+// ---- finalize from the producer's epilogue statistics (gemm.cu gn_colstats) --------------------
+// part[(b·ns + s)·C_src + c] = (Σy, Σy²) of channel c over the 32 pixels of slot s of image b (ns = P/32
+// slots per image). One block of NT threads per (group, image); the group's ns·cg (slot, channel) items
+// (cg = C/G) are each the (Σ, Σ²) of 32 values: thread t merges items t, t+NT, … sequentially (Chan et
+// al.), then a fixed xor butterfly per warp and one across the warps' results. The order depends only on
+// (P, C, G) — NT is a function of them — never on the batch or on banding (I5, I6). Two sources:
+// channels [0, C0) from part0 (stride C0), [C0, C) from part1 (stride C − C0) — a group may straddle the
+// concat boundary, and the two producers' slots need not cover the same pixels: (Σy, Σy²) are additive
+// over any partition of the group's values.
+__device__ __forceinline__ void chan_butterfly(float& n, float& mean, float& m2, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const float n2 = __shfl_xor_sync(0xffffffff, n, o);
+    const float mu2 = __shfl_xor_sync(0xffffffff, mean, o);
+    const float q2 = __shfl_xor_sync(0xffffffff, m2, o);
+    const bool lo = (lane & o) == 0;  // lower lane first: both partners compute the identical value
+    const float na = lo ? n : n2, ma = lo ? mean : mu2, qa = lo ? m2 : q2;
+    const float nb = lo ? n2 : n, mb = lo ? mu2 : mean, qb = lo ? q2 : m2;
+    const float tot = na + nb;
+    if (tot > 0.f) {
+      const float d = mb - ma;
+      const float w = __fdividef(nb, tot);
+      mean = ma + d * w;
+      m2 = qa + qb + d * d * (na * w);
+    } else {
+      mean = 0.f;
+      m2 = 0.f;
+    }
+    n = tot;
+  }
+}
+
+__global__ void __launch_bounds__(1024) gn_finalize_cols_kernel(int ns, int C, int C0, int G,
+                                                                const float2* __restrict__ part0,
+                                                                const float2* __restrict__ part1, float eps,
+                                                                const float* __restrict__ gamma,
+                                                                const float* __restrict__ beta,
+                                                                float2* __restrict__ tab) {
+  pdl_wait();
+  __shared__ float sh[32][3];
+  const int g = blockIdx.x, b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int nt = blockDim.x, nw = nt >> 5;
+  const int cg = C / G, c0 = g * cg, C1 = C - C0;
+  // items i = (slot i / cg, channel c0 + i mod cg): consecutive threads read consecutive channels of a
+  // slot; each item is the (Σ, Σ²) of 32 values — its (mean, M2) merged sequentially per thread (Chan
+  // et al.), 4 items' loads in flight at a time
+  const int items = ns * cg;
+  float n = 0.f, mean = 0.f, m2 = 0.f;
+  auto ld = [&](int i) {
+    const int s = i / cg, c = c0 + (i - s * cg);
+    const long row = (long)b * ns + s;
+    return c < C0 ? __ldcg(part0 + row * C0 + c) : __ldcg(part1 + row * C1 + (c - C0));
+  };
+  auto merge = [&](float2 p) {
+    const float ms = p.x * (1.f / 32.f);
+    const float qs = fmaxf(p.y - p.x * ms, 0.f);
+    const float tot = n + 32.f;
+    const float d = ms - mean;
+    const float w = __fdividef(32.f, tot);
+    mean += d * w;
+    m2 += qs + d * d * (n * w);
+    n = tot;
+  };
+  int i = tid;
+  for (; i + 3 * nt < items; i += 4 * nt) {
+    const float2 p0 = ld(i), p1 = ld(i + nt), p2 = ld(i + 2 * nt), p3 = ld(i + 3 * nt);
+    merge(p0);
+    merge(p1);
+    merge(p2);
+    merge(p3);
+  }
+  for (; i < items; i += nt) merge(ld(i));
+  chan_butterfly(n, mean, m2, lane);
+  if (nw > 1) {
+    if (lane == 0) {
+      sh[wid][0] = n;
+      sh[wid][1] = mean;
+      sh[wid][2] = m2;
+    }
+    __syncthreads();
+    if (wid) return;
+    n = lane < nw ? sh[lane][0] : 0.f;
+    mean = lane < nw ? sh[lane][1] : 0.f;
+    m2 = lane < nw ? sh[lane][2] : 0.f;
+    chan_butterfly(n, mean, m2, lane);
+  }
+  const float rstd = rsqrtf(m2 / n + eps);
+  float2* tb = tab + (long)b * C;
+  for (int c = c0 + lane; c < c0 + cg; c += 32) {
+    const float sc = gamma[c] * rstd;
+    tb[c] = make_float2(sc, beta[c] - mean * sc);
+  }
+}
+
+// threads per (group, image) block: ~8 items each, 32 … 1024 (a function of the layer only)
+static int gn_cols_threads(int items) { return std::min(1024, std::max(32, (items / 8 + 31) / 32 * 32)); }
+
 // SiLU(x) = x·σ(x) = ½x + ½x·tanh(x/2) on MUFU tanh.approx: absolute error ≤ ½|x|·2^-10.9 — about one
 // bf16 ulp for x > 0, but up to ~10 % relative for x ≈ −6 where SiLU is near 0 (bf16 path only; measured
 // effect on the SD-1.5 parity tests: none, DESIGN R33; 16-bit outputs only)
@@ -503,6 +600,33 @@ void group_norm2(const T* x0, int C0, const T* x1, int C1, T* y, int B, int P, i
   gn_apply(x0, x1, C0, y, 0, (long)B * P, B, P, C, gn_tab(ws, B, P, G), silu, st);
 }
 
+static void gn_finalize_cols(int B, int P, int C0, const float2* part0, int C1, const float2* part1, int G, void* ws,
+                             float eps, const float* gamma, const float* beta, cudaStream_t st) {
+  const int C = C0 + C1;
+  check_gn(C, G);
+  if (P % 32) throw CudaError("group_norm_parts: P must be a multiple of 32");
+  const int ns = P / 32;
+  launch_k(gn_finalize_cols_kernel, dim3(G, B), gn_cols_threads(ns * (C / G)), 0, st, ns, C, C0, G, part0, part1, eps, gamma,
+           beta, gn_tab(ws, B, P, G));
+  SD_CHECK_LAUNCH();
+}
+
+template <class T>
+void group_norm_parts(const T* x0, int C0, const float2* part0, const T* x1, int C1, const float2* part1, T* y, int B,
+                      int P, int G, const float* gamma, const float* beta, float eps, bool silu, void* ws,
+                      cudaStream_t st) {
+  if (x1 && (C0 % 8 || C1 % 8)) throw CudaError("group_norm_parts: source channels must be multiples of 8");
+  gn_finalize_cols(B, P, C0, part0, x1 ? C1 : 0, part1, G, ws, eps, gamma, beta, st);
+  gn_apply(x0, x1, C0, y, 0, (long)B * P, B, P, C0 + (x1 ? C1 : 0), gn_tab(ws, B, P, G), silu, st);
+}
+
+template <class T>
+void gn_apply_range_parts(const T* x, T* y, int P, int C, int G, int p0, int p1, const float2* part, const float* gamma,
+                          const float* beta, float eps, bool silu, void* ws, cudaStream_t st) {
+  if (p0 == 0) gn_finalize_cols(1, P, C, part, 0, nullptr, G, ws, eps, gamma, beta, st);  // bands run in order
+  gn_apply(x, (const T*)nullptr, C, y, p0, p1, 1, P, C, gn_tab(ws, 1, P, G), silu, st);
+}
+
 // ---- LayerNorm: LANES lanes per token (NV 16-byte vectors each), two-pass in registers ----------
 // C = 320/640/1280 → 8/16/32 lanes × 5 vectors: every lane issues all its loads up front and a warp
 // serves 4/2/1 tokens, so the per-token reduction is short and the loads are balanced.
@@ -600,7 +724,11 @@ void layer_norm(const E* x, E* y, int T, int C, const float* gamma, const float*
                                   void*, cudaStream_t);                                                      \
   template void layer_norm<T>(const T*, T*, int, int, const float*, const float*, float, cudaStream_t);   \
   template void group_norm2<T>(const T*, int, const T*, int, T*, int, int, int, const float*, const float*, float, \
-                               bool, void*, cudaStream_t);
+                               bool, void*, cudaStream_t);                                                   \
+  template void group_norm_parts<T>(const T*, int, const float2*, const T*, int, const float2*, T*, int, int, int, \
+                                    const float*, const float*, float, bool, void*, cudaStream_t);           \
+  template void gn_apply_range_parts<T>(const T*, T*, int, int, int, int, int, const float2*, const float*,     \
+                                        const float*, float, bool, void*, cudaStream_t);
 SD_NORM_INST(bf16)
 SD_NORM_INST(f16)
 SD_NORM_INST(float)

@@ -33,6 +33,11 @@ struct DecodeState {
   void* buf[NBUF];  // activation precision of the engine (bf16, or fp32 in the parity mode)
   float* img_nhwc = nullptr;
   void* gn_ws = nullptr;
+  // GroupNorm statistics from the producing conv's epilogue (GemmDescT::gn_part), [P/32][C] per layer:
+  // one buffer serves every layer — each GroupNorm's finalize (with its first band) is stream-ordered
+  // before the next producer overwrites it
+  float2* gn_part = nullptr;
+  int head_gnf = 0;  // the head's last conv writes the statistics of the first tail GroupNorm
   std::vector<VItem> items;
   std::vector<int64_t> cost;
   std::vector<int> bounds;
@@ -99,24 +104,40 @@ static void set_band(GemmDescF& d, int H, int W, int y0, int y1) {
 
 template <class AT>
 static void run_conv_band(Engine* e, const AT* x, int H, int W, int C, const AT* w, int N, const float* b, void* out,
-                          const AT* res, int y0, int y1, int out_f32, cudaStream_t st) {
+                          const AT* res, int y0, int y1, int out_f32, cudaStream_t st, float2* gp = nullptr) {
   (void)e;
   GemmDescT<AT> d;
   conv_desc(d, x, H, W, C, w, N, b, out, res);
   d.out_f32 = out_f32;
+  d.gn_part = gp;
   set_band(d, H, W, y0, y1);
   gemm(d, st);
+}
+
+// whether a conv layer of the tail (B = 1, output H × W × N, 16-bit) can write the GroupNorm statistics
+// of its output (a function of the layer only: banding does not change it)
+static bool vae_conv_gn_ok(const Engine* e, int H, int W, int C, int N) {
+  if (e->f32 || !gn_epilogue_on()) return false;
+  GemmDesc d;
+  d.mode = GEMM_CONV3;
+  d.cs[0] = C;
+  d.B = 1;
+  d.H = H;
+  d.W = W;
+  d.N = N;
+  d.ldo = N;
+  return gemm_gn_ok(d);
 }
 
 // whole-tensor resblock at the latent resolution (head)
 template <class AT>
 static void head_res(Engine* e, DecodeState* s, const ResW& r, AT* x, AT* out, AT* t1, AT* t2, int H, int W,
-                     cudaStream_t st) {
+                     cudaStream_t st, float2* gp = nullptr) {
   const int P = H * W, G = e->vc.groups;
   group_norm(x, t1, 1, P, r.cin, G, r.n1g, r.n1b, e->vc.eps, true, s->gn_ws, st);
   run_conv_band(e, t1, H, W, r.cin, wt<AT>(r.w1), r.cout, r.b1, t2, (const AT*)nullptr, 0, H, 0, st);
   group_norm(t2, t1, 1, P, r.cout, G, r.n2g, r.n2b, e->vc.eps, true, s->gn_ws, st);
-  run_conv_band(e, t1, H, W, r.cout, wt<AT>(r.w2), r.cout, r.b2, out, (const AT*)x, 0, H, 0, st);
+  run_conv_band(e, t1, H, W, r.cout, wt<AT>(r.w2), r.cout, r.b2, out, (const AT*)x, 0, H, 0, st, gp);
 }
 
 template <class AT>
@@ -213,7 +234,7 @@ static void run_head(Engine* e, DecodeState* s, const float* z, cudaStream_t st)
   }
   AT* x2 = sb<AT>(s, 1);
   lin(o, P, cm, wt<AT>(V.wo), cm, V.bo, x2, cm, x1, 0, 1.f, 0);
-  head_res(e, s, V.mid1, x2, sb<AT>(s, 0), sb<AT>(s, 3), sb<AT>(s, 4), H, W, st);
+  head_res(e, s, V.mid1, x2, sb<AT>(s, 0), sb<AT>(s, 3), sb<AT>(s, 4), H, W, st, s->head_gnf ? s->gn_part : nullptr);
   s->ar.reset(mk);
 }
 
@@ -228,6 +249,8 @@ static void build_items(Engine* e, DecodeState* s) {
   int H = s->h, W = s->w;
   it.push_back(VItem{VOP_HEAD});
   const int cm = c.block_out.back();
+  s->head_gnf = vae_conv_gn_ok(e, H, W, cm, cm);
+  int cur_gnf = s->head_gnf;  // statistics of `cur` were written by its producer
   cost.push_back(conv_cost((long)H * W, cm, cm) * 5 + (int64_t)H * W * H * W * cm * 4 / 1000000);
   int cur = 0;
   auto other = [&](std::initializer_list<int> used) {
@@ -243,27 +266,31 @@ static void build_items(Engine* e, DecodeState* s) {
       const int t3 = other({cur, t1, t2});
       const int y = other({cur, t1, t2, t3});
       const int br = band_rows(H, s->nbands);
-      auto push_gn = [&](int src, int dst, const float* gam, const float* bet, int C) {
-        for (int yy = 0; yy < H; yy += br) {
-          VItem v{VOP_GN_STATS, src, dst, 0, gam, C, 0, H, W, yy, std::min(H, yy + br), gn_id, 1};
-          it.push_back(v);
-          cost.push_back(std::max<int64_t>(1, (int64_t)(v.y1 - v.y0) * W * C * 2 / 6000));
-        }
+      auto push_gn = [&](int src, int dst, const float* gam, const float* bet, int C, int gnf) {
+        if (!gnf)
+          for (int yy = 0; yy < H; yy += br) {
+            VItem v{VOP_GN_STATS, src, dst, 0, gam, C, 0, H, W, yy, std::min(H, yy + br), gn_id, 1};
+            it.push_back(v);
+            cost.push_back(std::max<int64_t>(1, (int64_t)(v.y1 - v.y0) * W * C * 2 / 6000));
+          }
         for (int yy = 0; yy < H; yy += br) {
           VItem v{VOP_GN_APPLY, src, dst, 0, gam, C, 0, H, W, yy, std::min(H, yy + br), gn_id, 1};
           v.p1 = bet;
+          v.gnf = gnf;
           it.push_back(v);
           cost.push_back(std::max<int64_t>(1, (int64_t)(v.y1 - v.y0) * W * C * 4 / 6000));
         }
         ++gn_id;
       };
-      push_gn(cur, t1, r.n1g, r.n1b, r.cin);
+      push_gn(cur, t1, r.n1g, r.n1b, r.cin, cur_gnf);
+      const int c1_gnf = vae_conv_gn_ok(e, H, W, r.cin, r.cout);
       for (int yy = 0; yy < H; yy += br) {
         VItem v{VOP_CONV, t1, t2, -1, &r, r.cin, r.cout, H, W, yy, std::min(H, yy + br), 1, 0};
+        v.gnf = c1_gnf;
         it.push_back(v);
         cost.push_back(conv_cost((long)(v.y1 - v.y0) * W, r.cin, r.cout));
       }
-      push_gn(t2, t1, r.n2g, r.n2b, r.cout);
+      push_gn(t2, t1, r.n2g, r.n2b, r.cout, c1_gnf);
       int resb = cur;
       if (r.wsc) {
         for (int yy = 0; yy < H; yy += br) {
@@ -273,8 +300,10 @@ static void build_items(Engine* e, DecodeState* s) {
         }
         resb = t3;
       }
+      cur_gnf = vae_conv_gn_ok(e, H, W, r.cout, r.cout);
       for (int yy = 0; yy < H; yy += br) {
         VItem v{VOP_CONV, t1, y, resb, &r, r.cout, r.cout, H, W, yy, std::min(H, yy + br), 2, 0};
+        v.gnf = cur_gnf;
         it.push_back(v);
         cost.push_back(conv_cost((long)(v.y1 - v.y0) * W, r.cout, r.cout));
       }
@@ -291,8 +320,10 @@ static void build_items(Engine* e, DecodeState* s) {
         cost.push_back(std::max<int64_t>(1, (int64_t)(v.y1 - v.y0) * W * C * 3 / 6000));
       }
       const int y = other({cur});
+      cur_gnf = vae_conv_gn_ok(e, H, W, C, C);
       for (int yy = 0; yy < H; yy += br) {
         VItem v{VOP_CONV, 5, y, -1, &u, C, C, H, W, yy, std::min(H, yy + br), 3, 0};
+        v.gnf = cur_gnf;
         it.push_back(v);
         cost.push_back(conv_cost((long)(v.y1 - v.y0) * W, C, C));
       }
@@ -303,14 +334,16 @@ static void build_items(Engine* e, DecodeState* s) {
   const int t1 = other({cur});
   {
     const int br = band_rows(H, s->nbands);
-    for (int yy = 0; yy < H; yy += br) {
-      VItem v{VOP_GN_STATS, cur, t1, 0, e->V.nout_g, C0, 0, H, W, yy, std::min(H, yy + br), gn_id, 1};
-      it.push_back(v);
-      cost.push_back(std::max<int64_t>(1, (int64_t)(v.y1 - v.y0) * W * C0 * 2 / 6000));
-    }
+    if (!cur_gnf)
+      for (int yy = 0; yy < H; yy += br) {
+        VItem v{VOP_GN_STATS, cur, t1, 0, e->V.nout_g, C0, 0, H, W, yy, std::min(H, yy + br), gn_id, 1};
+        it.push_back(v);
+        cost.push_back(std::max<int64_t>(1, (int64_t)(v.y1 - v.y0) * W * C0 * 2 / 6000));
+      }
     for (int yy = 0; yy < H; yy += br) {
       VItem v{VOP_GN_APPLY, cur, t1, 0, e->V.nout_g, C0, 0, H, W, yy, std::min(H, yy + br), gn_id, 1};
       v.p1 = e->V.nout_b;
+      v.gnf = cur_gnf;
       it.push_back(v);
       cost.push_back(std::max<int64_t>(1, (int64_t)(v.y1 - v.y0) * W * C0 * 4 / 6000));
     }
@@ -338,22 +371,27 @@ static void run_item(Engine* e, DecodeState* s, const VItem& v, const float* z, 
     case VOP_GN_APPLY: {
       const int P = v.H * v.W;
       const float* gam = static_cast<const float*>(v.p0);
-      gn_apply_range(sb<AT>(s, v.a), sb<AT>(s, v.b), P, v.C, G, v.y0 * v.W, v.y1 * v.W, gam,
-                     static_cast<const float*>(v.p1), e->vc.eps, v.silu != 0, s->gn_ws, st);
+      if (v.gnf)
+        gn_apply_range_parts(sb<AT>(s, v.a), sb<AT>(s, v.b), P, v.C, G, v.y0 * v.W, v.y1 * v.W, s->gn_part, gam,
+                             static_cast<const float*>(v.p1), e->vc.eps, v.silu != 0, s->gn_ws, st);
+      else
+        gn_apply_range(sb<AT>(s, v.a), sb<AT>(s, v.b), P, v.C, G, v.y0 * v.W, v.y1 * v.W, gam,
+                       static_cast<const float*>(v.p1), e->vc.eps, v.silu != 0, s->gn_ws, st);
       break;
     }
     case VOP_CONV: {
       const AT* res = v.c >= 0 ? sb<AT>(s, v.c) : nullptr;
       const AT* x = sb<AT>(s, v.a);
+      float2* gp = v.gnf ? s->gn_part : nullptr;
       if (v.gn == 1) {
         const ResW* r = static_cast<const ResW*>(v.p0);
-        run_conv_band(e, x, v.H, v.W, v.C, wt<AT>(r->w1), v.C2, r->b1, sb<AT>(s, v.b), res, v.y0, v.y1, 0, st);
+        run_conv_band(e, x, v.H, v.W, v.C, wt<AT>(r->w1), v.C2, r->b1, sb<AT>(s, v.b), res, v.y0, v.y1, 0, st, gp);
       } else if (v.gn == 2) {
         const ResW* r = static_cast<const ResW*>(v.p0);
-        run_conv_band(e, x, v.H, v.W, v.C, wt<AT>(r->w2), v.C2, r->b2, sb<AT>(s, v.b), res, v.y0, v.y1, 0, st);
+        run_conv_band(e, x, v.H, v.W, v.C, wt<AT>(r->w2), v.C2, r->b2, sb<AT>(s, v.b), res, v.y0, v.y1, 0, st, gp);
       } else if (v.gn == 3) {
         const UpW* u = static_cast<const UpW*>(v.p0);
-        run_conv_band(e, x, v.H, v.W, v.C, wt<AT>(u->wup), v.C2, u->bup, sb<AT>(s, v.b), res, v.y0, v.y1, 0, st);
+        run_conv_band(e, x, v.H, v.W, v.C, wt<AT>(u->wup), v.C2, u->bup, sb<AT>(s, v.b), res, v.y0, v.y1, 0, st, gp);
       } else {
         GemmDescT<AT> d;
         conv_desc(d, x, v.H, v.W, v.C, wt<AT>(e->V.cout_w), 3, e->V.cout_b, s->img_nhwc, (const AT*)nullptr);
@@ -421,10 +459,12 @@ static DecodeState* new_decode(Engine* e, int h, int w) {
   const size_t head = P * 64 * 2 * 2 + P * cm * 2 * 3 + vae_attn_rows(P) * P * 6 + ((size_t)8 << 20);
   const size_t img = (size_t)64 * P * 3 * 4;
   const size_t gnb = gn_workspace_bytes(1, (int)(64 * P), 64, 1024);
-  s->ar.init(NBUF * (s->buf_elems * e->esize + 4096) + head * (e->esize / 2) + img + gnb + ((size_t)16 << 20));
+  const size_t gpb = (s->buf_elems / 32 + 64) * sizeof(float2);
+  s->ar.init(NBUF * (s->buf_elems * e->esize + 4096) + head * (e->esize / 2) + img + gnb + gpb + ((size_t)16 << 20));
   for (int i = 0; i < NBUF; ++i) s->buf[i] = s->ar.alloc(s->buf_elems * e->esize);
   s->img_nhwc = s->ar.get<float>(64 * P * 3);
   s->gn_ws = s->ar.alloc(gnb);
+  s->gn_part = s->ar.get<float2>(s->buf_elems / 32 + 64);
 
   build_items(e, s);
   return s;

@@ -294,3 +294,118 @@ def test_layernorm(T, C):
     B.call("sd_debug_layernorm", B._p(xd), B._p(y), T, C, B._p(gd), B._p(bd), 1e-5, None)
     torch.cuda.synchronize()
     assert rel(y.cpu(), ref) < 6e-3
+
+
+# ---- GroupNorm statistics from the producer's epilogue (gemm.cu gn_colstats) ----------------------------
+def _pow2_div(n, cap):
+    p = 1
+    while p * 2 <= cap and n % (p * 2) == 0:
+        p *= 2
+    return p
+
+
+def _slot_sums(y, h, w):
+    """Expected (Σy, Σy²) per (image, 32-pixel slot, channel) of a conv output [nb][h][w][C] under the conv
+    tile geometry (wt = largest power of two dividing w, ≤ 128; slot box sw = min(wt, 32) × 32/sw)."""
+    wt = _pow2_div(w, 128)
+    sw = min(wt, 32)
+    sh = 32 // sw
+    nb, C = y.shape[0], y.shape[-1]
+    yy = y.double().reshape(nb, h // sh, sh, w // sw, sw, C).permute(0, 1, 3, 2, 4, 5).reshape(nb, -1, 32, C)
+    return torch.stack([yy.sum(2), (yy * yy).sum(2)], -1)
+
+
+def _gn_ref(y, G, gam, bet, silu):
+    ref = F.group_norm(y.double().permute(0, 2, 1), G, gam.double(), bet.double(), 1e-5).permute(0, 2, 1)
+    return F.silu(ref) if silu else ref
+
+
+@pytest.mark.parametrize("nb,h,w,cin,cout,silu", [(2, 64, 64, 320, 320, 1), (3, 32, 32, 640, 640, 1),
+                                                  (2, 16, 16, 640, 1280, 0), (3, 8, 8, 1280, 640, 1),
+                                                  (1, 32, 64, 128, 256, 1), (1, 128, 128, 64, 128, 1)])
+def test_conv_gn_epilogue_stats(nb, h, w, cin, cout, silu):
+    """The conv epilogue's per-slot column sums equal the sums of the stored output (fp64 over the same
+    16-bit values), are bitwise deterministic and batch-invariant; GroupNorm from them matches GroupNorm
+    of the conv output (fp64) and the statistics-pass kernel."""
+    g = torch.Generator().manual_seed(nb + h + cin + cout)
+    x = bf(torch.randn(nb, h, w, cin, generator=g))
+    wt = bf(torch.randn(cout, cin, 3, 3, generator=g) / (9 * cin) ** 0.5)
+    b = torch.randn(cout, generator=g) + 0.3
+    res = bf(torch.randn(nb, h, w, cout, generator=g))
+    gam, bet = 1 + 0.1 * torch.randn(cout, generator=g), 0.1 * torch.randn(cout, generator=g)
+    xd, wd, bd, rd, gd, btd = x.cuda(), _to_dev_w(wt), b.cuda(), res.cuda(), gam.cuda(), bet.cuda()
+    P = h * w
+
+    def run(n):
+        y = torch.empty(n, h, w, cout, device="cuda", dtype=DT)
+        part = torch.full((n, P // 32, cout, 2), float("nan"), device="cuda")
+        B.call("sd_debug_conv3x3_gn", B._p(xd[:n]), cin, B._p(wd), B._p(bd), B._p(rd[:n]), B._p(y), n, h, w, cout,
+               B._p(part), None)
+        torch.cuda.synchronize()
+        return y, part
+
+    y, part = run(nb)
+    _, part2 = run(nb)
+    _, part1 = run(1)
+    assert torch.equal(part, part2), "epilogue statistics not deterministic"
+    assert torch.equal(part[:1], part1), "epilogue statistics depend on the batch"
+    exp = _slot_sums(y.cpu(), h, w)
+    assert float((part.cpu().double() - exp).abs().max() / exp.abs().max()) < 1e-5
+    gn = torch.empty_like(y)
+    B.call("sd_debug_groupnorm_parts", B._p(y), cout, B._p(part), None, 0, None, B._p(gn), nb, P, 32, B._p(gd),
+           B._p(btd), 1e-5, silu, None)
+    gn_pass = torch.empty_like(y)
+    B.call("sd_debug_groupnorm", B._p(y), B._p(gn_pass), nb, P, cout, 32, B._p(gd), B._p(btd), 1e-5, silu, None)
+    torch.cuda.synchronize()
+    ref = _gn_ref(y.cpu().reshape(nb, P, cout), 32, gam, bet, silu)
+    assert rel(gn.cpu().reshape(nb, P, cout), ref) < 6e-3
+    assert rel(gn.cpu(), gn_pass.cpu()) < 2e-3
+
+
+def test_conv_gn_epilogue_ineligible():
+    """4×4 images: a 32-pixel slot would straddle two images — the export refuses (no silent fallback)."""
+    x = torch.zeros(2, 4, 4, 64, device="cuda", dtype=DT)
+    wd = torch.zeros(64, 9, 64, device="cuda", dtype=DT)
+    y = torch.empty(2, 4, 4, 64, device="cuda", dtype=DT)
+    part = torch.empty(2, 1, 64, 2, device="cuda")
+    with pytest.raises(B.SDError):
+        B.call("sd_debug_conv3x3_gn", B._p(x), 64, B._p(wd), None, None, B._p(y), 2, 4, 4, 64, B._p(part), None)
+
+
+@pytest.mark.parametrize("nb,P,N,K", [(2, 4096, 320, 320), (3, 1024, 640, 640), (4, 64, 1280, 1280), (2, 96, 256, 512)])
+def test_gemm_gn_epilogue_stats_and_concat(nb, P, N, K):
+    """Dense producer (rows = pixels of nb images of P): slot s = rows 32s..32s+31 of an image, exact sums;
+    then GroupNorm over the concat [dense output | conv output] whose groups straddle the boundary
+    (C = N + 320, G = 32), from the two producers' statistics, vs fp64."""
+    g = torch.Generator().manual_seed(nb * P + N)
+    M = nb * P
+    A = bf(torch.randn(M, K, generator=g))
+    Wt = bf(torch.randn(N, K, generator=g) / K ** 0.5)
+    b = torch.randn(N, generator=g)
+    res = bf(torch.randn(M, N, generator=g))
+    Ad, Wd, bd, rd = A.cuda(), Wt.cuda(), b.cuda(), res.cuda()
+    y = torch.empty(M, N, device="cuda", dtype=DT)
+    part = torch.full((nb, P // 32, N, 2), float("nan"), device="cuda")
+    B.call("sd_debug_gemm_gn", B._p(Ad), B._p(Wd), B._p(bd), B._p(rd), B._p(y), M, N, K, P, B._p(part), None)
+    torch.cuda.synchronize()
+    yy = y.cpu().double().reshape(nb, P // 32, 32, N)
+    exp = torch.stack([yy.sum(2), (yy * yy).sum(2)], -1)
+    assert float((part.cpu().double() - exp).abs().max() / exp.abs().max()) < 1e-5
+    # second source: a conv output over the same pixels viewed as an image of P = h·w
+    h, w = {4096: (64, 64), 1024: (32, 32), 64: (8, 8), 96: (3, 32)}[P]
+    C1 = 320
+    x = bf(torch.randn(nb, h, w, 64, generator=g))
+    wc = bf(torch.randn(C1, 64, 3, 3, generator=g) / 24.0)
+    y1 = torch.empty(nb, h, w, C1, device="cuda", dtype=DT)
+    part1 = torch.full((nb, P // 32, C1, 2), float("nan"), device="cuda")
+    xd, wcd = x.cuda(), _to_dev_w(wc)
+    B.call("sd_debug_conv3x3_gn", B._p(xd), 64, B._p(wcd), None, None, B._p(y1), nb, h, w, C1, B._p(part1), None)
+    C = N + C1
+    gam, bet = 1 + 0.1 * torch.randn(C, generator=g), 0.1 * torch.randn(C, generator=g)
+    gd, btd = gam.cuda(), bet.cuda()
+    gn = torch.empty(nb, P, C, device="cuda", dtype=DT)
+    B.call("sd_debug_groupnorm_parts", B._p(y), N, B._p(part), B._p(y1), C1, B._p(part1), B._p(gn), nb, P, 32,
+           B._p(gd), B._p(btd), 1e-5, 1, None)
+    torch.cuda.synchronize()
+    cat = torch.cat([y.cpu().reshape(nb, P, N), y1.cpu().reshape(nb, P, C1)], -1)
+    assert rel(gn.cpu(), _gn_ref(cat, 32, gam, bet, 1)) < 6e-3

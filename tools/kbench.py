@@ -138,9 +138,27 @@ def main():
             by = 2.0 * x.numel() * 2
             print(json.dumps(dict(kind="layernorm", shape=[nb * P, C], ms=ms, gbs=by / ms / 1e6,
                                   frac=by / ms / 1e6 / hbm)), flush=True)
+    if args.only in ("", "gnparts"):  # GroupNorm from the producers' epilogue statistics vs the 3-kernel form
+        hbm = 6446.9
+        for i_, (nb, P, C) in enumerate([(16, 4096, 320), (16, 1024, 640), (16, 256, 1280), (16, 4096, 640),
+                                          (16, 4096, 960), (1, 262144, 128), (1, 65536, 256), (1, 16384, 512)]):
+            if args.pick >= 0 and i_ != args.pick:
+                continue
+            x = torch.randn(nb, P, C, device="cuda").to(torch.bfloat16)
+            y = torch.empty_like(x)
+            gam, bet = torch.ones(C, device="cuda"), torch.zeros(C, device="cuda")
+            xs = x.double().reshape(nb, P // 32, 32, C)
+            part = torch.stack([xs.sum(2), (xs * xs).sum(2)], -1).float().contiguous()
+            ms3 = timeit(lambda: B.call("sd_debug_groupnorm", B._p(x), B._p(y), nb, P, C, 32, B._p(gam), B._p(bet),
+                                        1e-5, 1, B._p(cur())), args.reps)
+            msp = timeit(lambda: B.call("sd_debug_groupnorm_parts", B._p(x), C, B._p(part), None, 0, None, B._p(y),
+                                        nb, P, 32, B._p(gam), B._p(bet), 1e-5, 1, B._p(cur())), args.reps)
+            by = 2.0 * x.numel() * 2
+            print(json.dumps(dict(kind="gn_parts", shape=[nb, P, C], ms_3kernel=ms3, ms_parts=msp,
+                                  gbs_parts=by / msp / 1e6, frac=by / msp / 1e6 / hbm)), flush=True)
     if args.only in ("", "xattn"):  # cross-attention to 77 cached text tokens (SD-1.5 levels)
         for i_, (R, heads, d, P) in enumerate([(16, 8, 40, 4096), (16, 8, 80, 1024), (16, 8, 160, 256),
-                                                (16, 8, 160, 64)]):
+                                                (16, 8, 160, 64), (16, 10, 64, 4096), (16, 20, 64, 1024)]):
             if args.pick >= 0 and i_ != args.pick:
                 continue
             C = heads * d
