@@ -411,13 +411,23 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
       }
       __syncwarp();
     }
+    const int col = n0 + c * 32;
+    // the chunk's bias (one 128-byte row, the same for every lane: L1 broadcast) is requested before the
+    // accumulator read, so its latency overlaps the TMEM load instead of following it (measured on
+    // [65536, 320, 320]: skipping the bias entirely saved 13 % of the kernel — the serial LDG chain)
+    const bool pre_b = g.bias && !g.bias_per_row && g.dbg != 2 && col + 32 <= g.N && g.splits == 1;
+    float4 bv[8];
+    if (pre_b) {
+      const float4* b4 = reinterpret_cast<const float4*>(g.bias + col);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) bv[i] = __ldg(b4 + i);
+    }
     if (g.dbg != 3) {
       tmem_ld32(tbase + c * 32, rv);
     } else {
 #pragma unroll
       for (int i = 0; i < 32; ++i) rv[i] = 0;
     }
-    const int col = n0 + c * 32;
     if (col >= g.N) continue;  // warp-uniform
     if (g.splits > 1) {
       // split-K: raw fp32 partial sums; bias / temb / act / residual are applied by splitk_reduce
@@ -443,7 +453,13 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
       for (int i = 0; i < 32; i += 2) fmul2(o[i], o[i + 1], g.alpha, g.alpha);
     }
     const bool full32 = col + 32 <= g.N;
-    if (g.bias && g.dbg != 2) {
+    if (pre_b) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        fadd2(o[4 * i], o[4 * i + 1], bv[i].x, bv[i].y);
+        fadd2(o[4 * i + 2], o[4 * i + 3], bv[i].z, bv[i].w);
+      }
+    } else if (g.bias && g.dbg != 2) {
       if (g.bias_per_row) {
         const float bv = valid ? g.bias[prow] : 0.f;
 #pragma unroll
@@ -605,11 +621,15 @@ __global__ void __launch_bounds__(320, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint32_t bar_l = 0;
+          // experiment switches (SD_EPI_DBG; results are garbage): 5 = B loaded only for a tile's first K
+          // block, 6 = A only for the first — how much of the time the operand feed of each costs
+          const bool skipB = g.dbg == 5 && kb != kb0, skipA = g.dbg == 6 && kb != kb0;
+          const int bytes = C::STAGE - (skipB ? C::B_BYTES : 0) - (skipA ? C::A_BYTES : 0);
           if (CG == 1) {
-            mbar_expect_tx(&full[stage], C::STAGE);
+            mbar_expect_tx(&full[stage], bytes);
           } else {
             bar_l = leader_addr(&full[stage]);
-            if (rank == 0) mbar_expect_tx(&full[stage], 2 * C::STAGE);
+            if (rank == 0) mbar_expect_tx(&full[stage], 2 * bytes);
           }
           void* dA = sA + stage * C::A_BYTES;
           void* dB = sB + stage * C::B_BYTES;
@@ -617,8 +637,8 @@ __global__ void __launch_bounds__(320, 1)
             // two sources (a channel concat never materialised): K blocks [0, kb_src0) from source 0
             const bool s1 = g.nsrc > 1 && kb >= g.kb_src[0];
             const int kk = s1 ? kb - g.kb_src[0] : kb;
-            tma2<CG>(dA, s1 ? &ta1 : &ta0, &full[stage], bar_l, kk * C::BK, m0);
-            tma2<CG>(dB, s1 ? &tb1 : &tb0, &full[stage], bar_l, kk * C::BK, n0);
+            if (!skipA) tma2<CG>(dA, s1 ? &ta1 : &ta0, &full[stage], bar_l, kk * C::BK, m0);
+            if (!skipB) tma2<CG>(dB, s1 ? &tb1 : &tb0, &full[stage], bar_l, kk * C::BK, n0);
           } else {
             int r = kb, src = 0;
             if (r >= 9 * g.kb_src[0]) {
@@ -629,8 +649,9 @@ __global__ void __launch_bounds__(320, 1)
             const int dy = tap / 3 - 1, dx = tap % 3 - 1;
             const CUtensorMap* ma = src ? &ta1 : &ta0;
             const CUtensorMap* mb = src ? &tb1 : &tb0;
-            tma4<CG>(dA, ma, &full[stage], bar_l, cb * C::BK, g.stride * x0 + dx, g.stride * y0 + dy, b0);
-            if (C::NH == 1) {
+            if (!skipA) tma4<CG>(dA, ma, &full[stage], bar_l, cb * C::BK, g.stride * x0 + dx, g.stride * y0 + dy, b0);
+            if (skipB) {
+            } else if (C::NH == 1) {
               tma3<CG>(dB, mb, &full[stage], bar_l, cb * C::BK, tap, n0);
             } else {  // this CTA's slice of each N-half: rows nt·BN + h·MMA_N + rank·MMA_N/CG
 #pragma unroll

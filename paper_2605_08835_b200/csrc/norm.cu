@@ -391,7 +391,7 @@ __device__ __forceinline__ void gn_apply_dev(const T* __restrict__ x, const T* _
 }
 
 template <class T>
-__global__ void __launch_bounds__(512) gn_apply_kernel(const T* __restrict__ x, const T* __restrict__ x1, int V0,
+__global__ void __launch_bounds__(512, 2) gn_apply_kernel(const T* __restrict__ x, const T* __restrict__ x1, int V0,
                                                        long p_begin, long p_end, int P, int V,
                                                        const float2* __restrict__ tab, int silu, T* __restrict__ y) {
   pdl_wait();
@@ -536,8 +536,24 @@ static void gn_apply(const T* x, const T* x1, int C0, T* y, long p0, long p1, in
   const long rows = (long)blk.y * 4;
   static int sms = 0;
   if (!sms) SD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  // resident blocks per SM of this block shape (registers bound it: ncu showed 2 of the assumed 8 blocks
+  // of 240 threads at 85 registers — 16 warps per SM; ≤ 64 registers now)
+  static std::mutex mu;
+  static std::map<int, int> occ;
+  int per_sm;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    const int nt = (int)(blk.x * blk.y);
+    auto it = occ.find(nt);
+    if (it == occ.end()) {
+      int n = 0;
+      SD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, gn_apply_kernel<T>, nt, 0));
+      it = occ.emplace(nt, std::max(n, 1)).first;
+    }
+    per_sm = it->second;
+  }
   const long want = (p1 - p0 + rows - 1) / rows;
-  const int grid = (int)std::min<long>(want, (long)sms * (2048 / (blk.x * blk.y)));
+  const int grid = (int)std::min<long>(want, (long)sms * per_sm);
   // 16-bit outputs: SiLU through one MUFU tanh instead of ex2 + rcp (the apply pass was partly
   // MUFU-bound: 2 MUFU ops per element); fp32 outputs keep the exact form.
   const int sm = gn_silu_mode<T>(silu);
