@@ -431,7 +431,9 @@ sd_status sd_debug_set_gemm_cg(int32_t cg);
 sd_status sd_debug_conv3x3_s2(const void* x, int32_t cin, const void* w, const float* bias, void* y, int32_t nb,
                               int32_t h_in, int32_t w_in, int32_t cout, void* stream);
 /* split-K of sd_debug_conv3x3: 0 = the production rule (conv layers of <= 64 pixels with >= 90 K
- * blocks of 64 channels take 3 splits), 1 = off, 2..8 = forced; partials summed in split order. */
+ * blocks of 64 channels take 3 splits), 1 = off, 2..8 = forced; partials summed in split order. A forced
+ * count (2..8) also splits sd_debug_gemm_res (dense split-K: the engine's rule is 3 splits for the
+ * transformer projections of <= 64-pixel levels with K >= 1280). */
 sd_status sd_debug_set_conv_splits(int32_t splits);
 
 #ifdef __cplusplus

@@ -78,7 +78,12 @@ extern "C" sd_status sd_debug_gemm_res(const void* A, const void* B, const float
   d.res = static_cast<const bf16*>(res);
   d.ldr = ldr;
   d.f16 = g_dbg_f16;
-  sd::gemm(d, static_cast<cudaStream_t>(stream));
+  d.splits = g_dbg_splits > 1 ? g_dbg_splits : 0;  // dense split-K only when forced (sd_debug_set_conv_splits)
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  d.split_ws_bytes = sd::gemm_split_ws_bytes(d);
+  if (d.split_ws_bytes) SD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d.split_ws), d.split_ws_bytes, st));
+  sd::gemm(d, st);
+  if (d.split_ws) SD_CUDA(cudaFreeAsync(d.split_ws, st));
   SD_API_END
 }
 

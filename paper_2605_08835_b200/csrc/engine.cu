@@ -693,10 +693,30 @@ struct Fwd {
     d.act = act;
     d.out_f32 = out_f32;
     d.gn_P = gn_P;
+    // split-K for the transformer projections of the ≤ 64-pixel levels (8×8: [1024, 1280, 1280] at 16
+    // rows is 40 output tiles on 148 SMs): 3 splits, a function of the layer (pixels per image, K), not
+    // of the batch — fp32 partials summed in split order, batch-invariant. SD_DENSE_SPLIT=1 disables.
+    const size_t mk = e->ws.mark();
+    if (!std::is_same<AT, float>::value && split_P > 0 && split_P <= 64 && K >= 1280 && act != ACT_GEGLU &&
+        !out_f32 && dense_split() > 1) {
+      d.splits = dense_split();
+      d.split_ws_bytes = gemm_split_ws_bytes(d);
+      if (d.split_ws_bytes) d.split_ws = e->ws.get<float>(d.split_ws_bytes / sizeof(float));
+    }
     gn_note(d, out, gp);
     const int pi = e->prof.begin(cls, st, 2.0 * M * N * K);
     gemm(d, st);
     e->prof.end(pi, st);
+    e->ws.reset(mk);
+  }
+  int split_P = 0;  // pixels per image of the transformer being run (split-K rule of linear())
+  static int dense_split() {
+    static int v = -1;
+    if (v < 0) {
+      const char* s = getenv("SD_DENSE_SPLIT");
+      v = s ? atoi(s) : 3;
+    }
+    return v;
   }
   // 3×3 conv, pad 1; H × W is the OUTPUT size (the input is stride·H × stride·W)
   void conv(const AT* x, int H, int W, int C, const AT* w, int N, const float* bias, void* out,
@@ -796,6 +816,7 @@ struct Fwd {
     const int C = t.C, P = H * W;
     const long T = (long)R * P;
     const int heads = e->uc.heads_at(C), dh = C / heads;
+    split_P = P;
     AT* out = buf(T * C);
     float2* out_gp = gn_buf(T, C);
     const size_t mk = e->ws.mark();
@@ -901,6 +922,7 @@ struct Fwd {
       std::swap(h, hb);
     }
     linear(h, T, C, wt<AT>(t.wpout), C, t.bpout, out, C, x, ACT_NONE, 0, PC_CONV1, out_gp, P);  // proj_out + the input
+    split_P = 0;
     e->ws.reset(mk);
     return out;
   }

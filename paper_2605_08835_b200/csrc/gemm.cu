@@ -4,7 +4,8 @@
 //   warp 0      TMA producer   (one elected lane): A and B tiles into a STAGES-deep smem ring
 //   warp 1      MMA issuer     (one elected lane of the leader CTA): tcgen05.mma into a
 //                              double-buffered TMEM accumulator; also owns TMEM alloc/dealloc
-//   warps 2..9  epilogue       tcgen05.ld → bias / temb / act / residual → bf16|fp32 stores
+//   warps 2..   epilogue       tcgen05.ld → bias / temb / act / residual → bf16|fp32 stores (8 warps for
+//                              conv3, 16 for dense: 2 or 4 per TMEM lane quarter)
 // CG = 1: one CTA computes a 128×BN tile.
 // CG = 2: a CTA pair (cluster of 2, cta_group::2) computes a 256×BN tile: each CTA loads its 128
 //         rows of A and half of B, the leader issues 256×BN×16 MMAs reading both CTAs' smem, and
@@ -68,7 +69,7 @@ __device__ __forceinline__ void decode_tile(const GemmArgs& g, int t, int& mt, i
   kb1 = min(g.num_kb, kb0 + g.kps);
 }
 
-template <int BN, int CG>
+template <int BN, int CG, int EPW = 8>
 struct Cfg {
   static constexpr int BM = 128, BK = 64;
   // BN = 320 (conv3, CTA pairs): two N = 160 MMAs per k-step share the A operand — A is read from smem
@@ -80,12 +81,15 @@ struct Cfg {
   static constexpr int B_ROWS = BN / CG;                         // B rows loaded by this CTA
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (192 * 1024) / STAGE > 8 ? 8 : (192 * 1024) / STAGE;
+  // EPW epilogue warps (8, or 16 for the short-K dense GEMMs whose epilogue is the critical path), each
+  // with 2 × 2 KB staging slabs; the operand ring gets the rest of 224 KB
+  static constexpr int STAGING = EPW * 2 * 2048;
+  static constexpr int RING = 224 * 1024 - STAGING;
+  static constexpr int STAGES = RING / STAGE > 8 ? 8 : RING / STAGE;
   static constexpr int TMEM_STRIDE = BN <= 64 ? 64 : (BN <= 128 ? 128 : (BN <= 256 ? 256 : BN));
   static constexpr int NACC = 2 * TMEM_STRIDE <= 512 ? 2 : 1;    // double-buffered accumulator if it fits
   static constexpr int TMEM_COLS = NACC == 2 ? 2 * TMEM_STRIDE : 512;
-  static constexpr int STAGING = 8 * 2 * 2048;                   // 8 epilogue warps × 2 slabs
-  static constexpr int SMEM = 1024 + STAGES * STAGE + STAGING + 512;
+  static constexpr int SMEM = 1024 + STAGES * STAGE + STAGING + 1024;
   static_assert(B_BYTES % 1024 == 0, "B tile must be a whole number of 8-row swizzle groups");
 };
 
@@ -299,7 +303,9 @@ __device__ __forceinline__ void res_load32(uint4 (&r)[4], const bf16* rp) {
 }
 
 // `tfull` / `tphase`: the accumulator-ready barrier of this tile
-template <int BN, int MODE, bool F16>
+// NW epilogue warps share each TMEM lane quarter; warp `half` (0 … NW−1) takes the 32-column chunks
+// c ≡ half (mod NW)
+template <int BN, int MODE, bool F16, int NW>
 __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorMap* om, const CUtensorMap* res_map,
                                               EpiCtx& ec, uint32_t tbase,
                                               int mbox, int n0, int q, int lane, int half, int split, uint64_t* tfull,
@@ -349,9 +355,9 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
   if (g.act == ACT_GEGLU) {
     // columns [128j, 128j+64) = value, [128j+64, 128j+128) = gate; output width BN/2
 #pragma unroll 1
-    for (int j = 0; j < BN / 128; ++j) {
-#pragma unroll 1
-      for (int h = half; h < 2; h += 2) {  // the two epilogue warps of a lane quarter split the halves
+    for (int ci = half; ci < 2 * (BN / 128); ci += NW) {  // (128-column group j, 32-column half h) items
+      const int j = ci >> 1, h = ci & 1;
+      {
         uint32_t rv[32], rg[32];
         const int cv = j * 128 + h * 32, cgc = cv + 64;
         tmem_ld32(tbase + cv, rv);
@@ -398,7 +404,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
     return;
   }
 #pragma unroll 1
-  for (int c = half; c < BN / 32; c += 2) {  // two epilogue warps per lane quarter: alternate chunks
+  for (int c = half; c < BN / 32; c += NW) {  // NW epilogue warps per lane quarter: interleaved chunks
     uint32_t rv[32];
     const bool rt = g.res_tma && n0 + c * 32 < g.N;  // warp-uniform
     if (rt) {
@@ -542,13 +548,13 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
   }
 }
 
-template <int BN, int CG, int MODE, bool F16>
-__global__ void __launch_bounds__(320, 1)
+template <int BN, int CG, int MODE, bool F16, int EPW>
+__global__ void __launch_bounds__(64 + 32 * EPW, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ CUtensorMap ta1,
                 const __grid_constant__ CUtensorMap tb0, const __grid_constant__ CUtensorMap tb1,
                 const __grid_constant__ CUtensorMap tout, const __grid_constant__ CUtensorMap tres,
                 const GemmArgs g) {
-  using C = Cfg<BN, CG>;
+  using C = Cfg<BN, CG, EPW>;
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned (SWIZZLE_128B atoms); offsetting the shared array itself keeps the pointer in the
   // shared state space, so the compiler emits STS / LDS rather than generic ST / LD
@@ -560,8 +566,8 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* rbar = tempty + 2;  // [8 epilogue warps][2 slabs]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 16);
+  uint64_t* rbar = tempty + 2;  // [EPW epilogue warps][2 slabs]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 2 * EPW);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = CG == 2 ? cluster_rank() : 0;
@@ -572,9 +578,9 @@ __global__ void __launch_bounds__(320, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 8 * CG);
+      mbar_init(&tempty[s], EPW * CG);
     }
-    for (int s = 0; s < 16; ++s) mbar_init(&rbar[s], 1);
+    for (int s = 0; s < 2 * EPW; ++s) mbar_init(&rbar[s], 1);
     fence_mbar_init();
     tma_prefetch(&ta0);
     tma_prefetch(&tb0);
@@ -716,8 +722,8 @@ __global__ void __launch_bounds__(320, 1)
       int mt, nt, sp, kb0, kb1;
       decode_tile(g, t, mt, nt, sp, kb0, kb1);
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * C::TMEM_STRIDE;
-      epilogue_tile<BN, MODE, F16>(g, &tout, &tres, ec, tbase, mt * CG + (int)rank, nt * BN, q, lane, (warp - 2) >> 2, sp,
-                              &tfull[acc], acc_phase);
+      epilogue_tile<BN, MODE, F16, EPW / 4>(g, &tout, &tres, ec, tbase, mt * CG + (int)rank, nt * BN, q, lane,
+                                            (warp - 2) >> 2, sp, &tfull[acc], acc_phase);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -843,13 +849,15 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ part, int S, long
   *reinterpret_cast<uint2*>(out + m * ldo + col_off + n) = pk;
 }
 
-template <int BN, int CG, int MODE>
+template <int BN, int CG, int MODE, int EPW>
 static void launch(const CUtensorMap* m, const GemmArgs& a, cudaStream_t st) {
-  using C = Cfg<BN, CG>;
+  using C = Cfg<BN, CG, EPW>;
   static bool attr_set = false;
   if (!attr_set) {
-    SD_CUDA(cudaFuncSetAttribute(gemm_kernel<BN, CG, MODE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    SD_CUDA(cudaFuncSetAttribute(gemm_kernel<BN, CG, MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    SD_CUDA(cudaFuncSetAttribute(gemm_kernel<BN, CG, MODE, false, EPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 C::SMEM));
+    SD_CUDA(cudaFuncSetAttribute(gemm_kernel<BN, CG, MODE, true, EPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 C::SMEM));
     attr_set = true;
   }
   const int total = a.m_tiles * a.n_tiles * a.splits;
@@ -858,7 +866,7 @@ static void launch(const CUtensorMap* m, const GemmArgs& a, cudaStream_t st) {
   if (workers <= 0) return;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(workers * CG);
-  cfg.blockDim = dim3(320);
+  cfg.blockDim = dim3(64 + 32 * EPW);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
@@ -871,26 +879,52 @@ static void launch(const CUtensorMap* m, const GemmArgs& a, cudaStream_t st) {
   cfg.attrs = attr;
   cfg.numAttrs = g_pdl ? 2 : 1;
   if (a.f16)
-    SD_CUDA(cudaLaunchKernelEx(&cfg, gemm_kernel<BN, CG, MODE, true>, m[0], m[1], m[2], m[3], m[4], m[5], a));
+    SD_CUDA(cudaLaunchKernelEx(&cfg, gemm_kernel<BN, CG, MODE, true, EPW>, m[0], m[1], m[2], m[3], m[4], m[5], a));
   else
-    SD_CUDA(cudaLaunchKernelEx(&cfg, gemm_kernel<BN, CG, MODE, false>, m[0], m[1], m[2], m[3], m[4], m[5], a));
+    SD_CUDA(cudaLaunchKernelEx(&cfg, gemm_kernel<BN, CG, MODE, false, EPW>, m[0], m[1], m[2], m[3], m[4], m[5], a));
   SD_CHECK_LAUNCH();
 }
 
 // conv3 and dense launches are separate instantiations (distinct kernel names in launch lists)
-template <int MODE>
-static void dispatch(int bn, int cg, const CUtensorMap* maps, const GemmArgs& a, cudaStream_t st) {
+template <int MODE, int EPW>
+static void dispatch_w(int bn, int cg, const CUtensorMap* maps, const GemmArgs& a, cudaStream_t st) {
   switch (bn * 4 + cg) {
-    case 64 * 4 + 1: launch<64, 1, MODE>(maps, a, st); break;
-    case 128 * 4 + 1: launch<128, 1, MODE>(maps, a, st); break;
-    case 160 * 4 + 1: launch<160, 1, MODE>(maps, a, st); break;
-    case 256 * 4 + 1: launch<256, 1, MODE>(maps, a, st); break;
-    case 128 * 4 + 2: launch<128, 2, MODE>(maps, a, st); break;
-    case 160 * 4 + 2: launch<160, 2, MODE>(maps, a, st); break;
-    case 256 * 4 + 2: launch<256, 2, MODE>(maps, a, st); break;
-    case 320 * 4 + 2: launch<320, 2, MODE>(maps, a, st); break;
+    case 64 * 4 + 1: launch<64, 1, MODE, EPW>(maps, a, st); break;
+    case 128 * 4 + 1: launch<128, 1, MODE, EPW>(maps, a, st); break;
+    case 160 * 4 + 1: launch<160, 1, MODE, EPW>(maps, a, st); break;
+    case 256 * 4 + 1: launch<256, 1, MODE, EPW>(maps, a, st); break;
+    case 128 * 4 + 2: launch<128, 2, MODE, EPW>(maps, a, st); break;
+    case 160 * 4 + 2: launch<160, 2, MODE, EPW>(maps, a, st); break;
+    case 256 * 4 + 2: launch<256, 2, MODE, EPW>(maps, a, st); break;
+    case 320 * 4 + 2: launch<320, 2, MODE, EPW>(maps, a, st); break;
     default: throw CudaError("unsupported BN/CG");
   }
+}
+// epilogue warps: 12 (3 per TMEM lane quarter) for dense launches with K ≤ 320 (5 K blocks) that are not
+// GEGLU, else 8. With such short K the epilogue's serial chunk chain per warp (TMEM load → math →
+// staging → TMA store) is the critical path — [65536, 320, 320]: 25.0 µs with stores, 19.0 µs without,
+// and removing either operand's loads changed nothing — and 3 warps per quarter cut the longest chain
+// of a BN = 160 tile from 3 chunks to 2: 25.3 → 22.9 µs, [65536, 960, 320] 64.0 → 60.0 µs, with the
+// residual 32.2 → 30.3 µs. Longer K and GEGLU lose 2-4 % (fewer ring stages in the smaller smem share,
+// 128 registers). 16 warps would cap registers at 96 (18 warps, 5 per SMSP: 200-byte spills).
+// SD_EPI_WARPS=8 turns the 12-warp form off.
+static int epi_warps(int mode, const GemmArgs& a) {
+  static int e = -1;
+  if (e < 0) {
+    const char* s = getenv("SD_EPI_WARPS");
+    e = s ? atoi(s) : 12;
+  }
+  return mode == GEMM_DENSE && e == 12 && a.num_kb <= 5 && a.act != ACT_GEGLU ? 12 : 8;
+}
+template <int MODE>
+static void dispatch(int bn, int cg, const CUtensorMap* maps, const GemmArgs& a, cudaStream_t st) {
+  if constexpr (MODE == GEMM_DENSE) {
+    if (epi_warps(MODE, a) == 12) {
+      dispatch_w<MODE, 12>(bn, cg, maps, a, st);
+      return;
+    }
+  }
+  dispatch_w<MODE, 8>(bn, cg, maps, a, st);
 }
 
 static int pick_bn(int N, int act) {
@@ -927,8 +961,16 @@ int gemm_splits(const GemmDesc& d) {
     const char* s = getenv("SD_SPLITK");
     env = s ? atoi(s) : -1;
   }
-  if (d.splits == 1 || d.mode != GEMM_CONV3) return 1;
+  if (d.splits == 1) return 1;
   if (d.act == ACT_GEGLU || d.out_f32 || d.bias_per_row || d.N % 4 || d.ldo % 4 || d.col_off % 4) return 1;
+  if (d.mode == GEMM_DENSE) {
+    // dense: only an explicit split count (the caller picks it from the layer, never from the batch, so
+    // results stay batch-invariant); K blocks of 64 split evenly, ≥ 4 per split
+    if (d.splits <= 1) return 1;
+    const int kbd = cdiv(d.K, 64);
+    const int sd = std::max(1, std::min(d.splits, std::min(8, kbd / 4)));
+    return cdiv(kbd, cdiv(kbd, sd));
+  }
   const int kb = conv_num_kb(d);
   int s = d.splits;
   if (s == 0) {
@@ -956,7 +998,8 @@ int gemm_splits(const GemmDesc& d) {
 size_t gemm_split_ws_bytes(const GemmDesc& d) {
   const int s = gemm_splits(d);
   if (s <= 1) return 0;
-  return (size_t)s * d.B * d.H * d.W * d.N * sizeof(float);
+  const long M = d.mode == GEMM_DENSE ? (long)d.M : (long)d.B * d.H * d.W;
+  return (size_t)s * M * d.N * sizeof(float);
 }
 
 bool gemm_gn_ok(const GemmDesc& d) {
@@ -1185,7 +1228,8 @@ void gemm(const GemmDesc& d, cudaStream_t st) {
   if (a.splits > 1) {
     const long n4 = (long)a.M * (d.N / 4);
     launch_k(splitk_reduce_kernel, (unsigned)cdiv(n4, 256), 256, 0, st, 
-        a.part, a.splits, a.M, d.N, d.bias, d.temb, d.ld_temb, d.H * d.W, d.res, d.ldr, d.act, d.alpha,
+        a.part, a.splits, a.M, d.N, d.bias, d.temb, d.ld_temb,
+        d.mode == GEMM_DENSE ? (d.rows_per_img > 0 ? d.rows_per_img : 1) : d.H * d.W, d.res, d.ldr, d.act, d.alpha,
         reinterpret_cast<bf16*>(d.out), d.ldo, d.col_off, d.f16);
     SD_CHECK_LAUNCH();
   }

@@ -75,6 +75,34 @@ def test_gemm_residual(M, N, K, ldr, inplace):
     assert rel(out, ref) < 6e-3
 
 
+@pytest.mark.parametrize("splits", [2, 3])
+@pytest.mark.parametrize("M,N,K", [(1024, 1280, 1280), (640, 1280, 5120), (300, 320, 1280)])
+def test_gemm_splitk_dense(splits, M, N, K):
+    """Dense split-K (fp32 partials per K range, summed in split order by the reduce kernel, which applies
+    bias + residual) vs fp64; bitwise deterministic, and the first rows equal those of a smaller-M call
+    (the split rule never depends on M)."""
+    g = torch.Generator().manual_seed(splits + M + K)
+    A, Wt = torch.randn(M, K, generator=g), torch.randn(N, K, generator=g) / K ** 0.5
+    bias, res = torch.randn(N, generator=g), bf(torch.randn(M, N, generator=g))
+    ref = bf(A).double() @ bf(Wt).double().T + bias.double() + res.double()
+    Ad, Wd, bd, resd = bf(A).cuda(), bf(Wt).cuda(), bias.cuda(), res.cuda()
+
+    def run(m):
+        D = torch.empty(m, N, device="cuda", dtype=DT)
+        B.call("sd_debug_gemm_res", B._p(Ad), B._p(Wd), B._p(bd), B._p(resd), N, B._p(D), m, N, K, None)
+        torch.cuda.synchronize()
+        return D.cpu()
+
+    B.call("sd_debug_set_conv_splits", splits)
+    try:
+        y, y2, y_small = run(M), run(M), run(128)
+    finally:
+        B.call("sd_debug_set_conv_splits", 0)
+    assert rel(y, ref) < 6e-3
+    assert torch.equal(y, y2)
+    assert torch.equal(y[:128], y_small)
+
+
 def test_gemm_geglu_and_silu():
     M, N, K = 260, 512, 128
     g = torch.Generator().manual_seed(5)

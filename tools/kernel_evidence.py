@@ -31,10 +31,10 @@ def classify(name):
     n = name.split("(")[0]
     if "gemm_kernel" in n:
         return "conv3x3 implicit GEMM (tcgen05)" if gemm_mode(name) == 1 else "dense GEMM (tcgen05)"
-    if "attn_tc" in n:
-        return "self-attention (tcgen05 flash)"
     if "xattn_tc_kernel" in n:
         return "cross-attention (tcgen05, K/V resident)"
+    if "attn_tc" in n:
+        return "self-attention (tcgen05 flash)"
     if "xattn" in n:
         return "cross-attention (short-context mma.sync)"
     if "attn_kernel" in n:
