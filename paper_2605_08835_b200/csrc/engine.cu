@@ -694,8 +694,10 @@ struct Fwd {
     d.out_f32 = out_f32;
     d.gn_P = gn_P;
     // split-K for the transformer projections of the ≤ 64-pixel levels (8×8: [1024, 1280, 1280] at 16
-    // rows is 40 output tiles on 148 SMs): 3 splits, a function of the layer (pixels per image, K), not
-    // of the batch — fp32 partials summed in split order, batch-invariant. SD_DENSE_SPLIT=1 disables.
+    // rows is 40 output tiles on 148 SMs): a function of the layer (pixels per image, K), not of the
+    // batch — fp32 partials summed in split order, batch-invariant. Off by default (SD_DENSE_SPLIT=3
+    // enables 3 splits): measured neutral-to-negative — the split GEMM keeps most of its fixed cost
+    // (ncu: 17.8 µs per third of K vs 25.7 µs whole) and the reduce adds 7-8 µs
     const size_t mk = e->ws.mark();
     if (!std::is_same<AT, float>::value && split_P > 0 && split_P <= 64 && K >= 1280 && act != ACT_GEGLU &&
         !out_f32 && dense_split() > 1) {
@@ -714,7 +716,7 @@ struct Fwd {
     static int v = -1;
     if (v < 0) {
       const char* s = getenv("SD_DENSE_SPLIT");
-      v = s ? atoi(s) : 3;
+      v = s ? atoi(s) : 1;
     }
     return v;
   }

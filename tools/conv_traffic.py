@@ -50,6 +50,8 @@ def main():
         if gemm_mode(base) == 1:
             cur = dict(bytes=by, us=us, tensor_w=tens * us, launches=1)
             ops.append(cur)
+        elif gemm_mode(base) == 0:
+            cur = None  # a reduce after a dense GEMM (dense split-K) belongs to that GEMM, not to a conv
         elif "splitk_reduce" in base and cur is not None:
             cur["bytes"] += by
             cur["us"] += us
