@@ -309,7 +309,8 @@ template <int BN, int MODE, bool F16, int NW>
 __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorMap* om, const CUtensorMap* res_map,
                                               EpiCtx& ec, uint32_t tbase,
                                               int mbox, int n0, int q, int lane, int half, int split, uint64_t* tfull,
-                                              uint32_t tphase) {
+                                              uint32_t tphase, int c_lo = 0, int c_hi = BN / 32) {
+  // chunks [c_lo, c_hi) of the tile; chunk c's accumulator columns start at tbase + (c − c_lo)·32
   const int r = q * 32 + lane;
   long prow;
   int img;
@@ -404,7 +405,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
     return;
   }
 #pragma unroll 1
-  for (int c = half; c < BN / 32; c += NW) {  // NW epilogue warps per lane quarter: interleaved chunks
+  for (int c = c_lo + (half - c_lo % NW + NW) % NW; c < c_hi; c += NW) {  // NW warps per lane quarter: c ≡ half
     uint32_t rv[32];
     const bool rt = g.res_tma && n0 + c * 32 < g.N;  // warp-uniform
     if (rt) {
@@ -429,7 +430,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
       for (int i = 0; i < 8; ++i) bv[i] = __ldg(b4 + i);
     }
     if (g.dbg != 3) {
-      tmem_ld32(tbase + c * 32, rv);
+      tmem_ld32(tbase + (c - c_lo) * 32, rv);
     } else {
 #pragma unroll
       for (int i = 0; i < 32; ++i) rv[i] = 0;
@@ -565,8 +566,8 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(sStage + C::STAGING);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* rbar = tempty + 2;  // [EPW epilogue warps][2 slabs]
+  uint64_t* tempty = tfull + 3;  // 2 accumulators, or 3 rotating 160-column halves (NH = 2)
+  uint64_t* rbar = tempty + 3;  // [EPW epilogue warps][2 slabs]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 2 * EPW);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -576,7 +577,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < 3; ++s) {
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], EPW * CG);
     }
@@ -683,9 +684,23 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
       for (int t = worker; t < total; t += nworkers, ++it) {
         const int acc = C::NACC == 2 ? (it & 1) : 0;
         const uint32_t acc_phase = C::NACC == 2 ? ((it >> 1) & 1) : (it & 1);
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        // NH = 2 (BN = 320): the two 160-column halves of tile `it` are global halves j = 2·it + h, in
+        // rotating buffers j mod 3 of 160 TMEM columns (480 of 512): the next tile's MMAs start as soon as
+        // this tile's first half is drained, instead of after its whole epilogue
+        uint32_t dh[2];
+        if constexpr (C::NH == 2) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int j = 2 * it + h, b = j % 3;
+            mbar_wait(&tempty[b], ((j / 3) & 1) ^ 1);
+            dh[h] = tmem_base + b * C::MMA_N;
+          }
+        } else {
+          mbar_wait(&tempty[acc], acc_phase ^ 1);
+          dh[0] = tmem_base + acc * C::TMEM_STRIDE;
+          dh[1] = dh[0] + C::MMA_N;
+        }
         tc_fence_after();
-        const uint32_t d = tmem_base + acc * C::TMEM_STRIDE;
         int mt, nt, sp, kb0, kb1;
         decode_tile(g, t, mt, nt, sp, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -697,7 +712,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
           for (int k = 0; k < C::BK / 16; ++k)
 #pragma unroll
             for (int h = 0; h < C::NH; ++h)  // N-half h: B rows [h·B_ROWS/NH, …) of every CTA, TMEM cols h·MMA_N
-              mma<CG>(d + h * C::MMA_N, make_sdesc_sw128(a0 + k * 32),
+              mma<CG>(dh[h], make_sdesc_sw128(a0 + k * 32),
                       make_sdesc_sw128(b0 + h * (C::B_ROWS / C::NH) * 128 + k * 32), idesc,
                       (kb != kb0 || k != 0) ? 1u : 0u);
           commit<CG>(&empty[stage]);
@@ -706,7 +721,12 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             phase ^= 1;
           }
         }
-        commit<CG>(&tfull[acc]);
+        if constexpr (C::NH == 2) {
+          commit<CG>(&tfull[(2 * it) % 3]);
+          commit<CG>(&tfull[(2 * it + 1) % 3]);
+        } else {
+          commit<CG>(&tfull[acc]);
+        }
       }
     }
     __syncwarp();
@@ -721,18 +741,35 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
       const uint32_t acc_phase = C::NACC == 2 ? ((it >> 1) & 1) : (it & 1);
       int mt, nt, sp, kb0, kb1;
       decode_tile(g, t, mt, nt, sp, kb0, kb1);
-      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * C::TMEM_STRIDE;
-      epilogue_tile<BN, MODE, F16, EPW / 4>(g, &tout, &tres, ec, tbase, mt * CG + (int)rank, nt * BN, q, lane,
-                                            (warp - 2) >> 2, sp, &tfull[acc], acc_phase);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if (CG == 1) {
-          mbar_arrive(&tempty[acc]);
-        } else {
-          const uint32_t a = leader_addr(&tempty[acc]);
-          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
+      auto release = [&](int b) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (CG == 1) {
+            mbar_arrive(&tempty[b]);
+          } else {
+            const uint32_t a = leader_addr(&tempty[b]);
+            asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
+          }
         }
+      };
+      const uint32_t lq = (uint32_t)(q * 32) << 16;
+      if constexpr (C::NH == 2) {
+        // the tile's two 160-column halves from their rotating buffers, first half first (its release lets
+        // the next tile's MMAs start)
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+          const int j = 2 * it + h, b = j % 3;
+          epilogue_tile<BN, MODE, F16, EPW / 4>(g, &tout, &tres, ec, tmem_base + lq + b * C::MMA_N, mt * CG + (int)rank,
+                                                nt * BN, q, lane, (warp - 2) >> 2, sp, &tfull[b], (j / 3) & 1,
+                                                h * (BN / 64), (h + 1) * (BN / 64));
+          release(b);
+        }
+      } else {
+        const uint32_t tbase = tmem_base + lq + acc * C::TMEM_STRIDE;
+        epilogue_tile<BN, MODE, F16, EPW / 4>(g, &tout, &tres, ec, tbase, mt * CG + (int)rank, nt * BN, q, lane,
+                                              (warp - 2) >> 2, sp, &tfull[acc], acc_phase);
+        release(acc);
       }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -847,6 +884,52 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ part, int S, long
   }
   uint2 pk = make_uint2(pack16(o[0], o[1], is_f16), pack16(o[2], o[3], is_f16));
   *reinterpret_cast<uint2*>(out + m * ldo + col_off + n) = pk;
+}
+
+// the same reduction, 8 columns per thread with every split's loads issued before the first add (the
+// 4-column loop above kept one 16-byte load in flight per thread: latency-bound, ~3 TB/s); identical
+// summation order ((p0 + p1) + p2) …, so the results are bitwise those of the 4-column kernel
+__global__ void splitk_reduce8_kernel(const float* __restrict__ part, int S, long M, int N, const float* __restrict__ bias,
+                                      const float* __restrict__ temb, int ld_temb, int rows_per_img,
+                                      const bf16* __restrict__ res, int ldr, int act, float alpha,
+                                      bf16* __restrict__ out, int ldo, int col_off, int is_f16) {
+  pdl_wait();
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;  // one group of 8 columns
+  const int nq = N / 8;
+  if (i >= M * nq) return;
+  const long m = i / nq;
+  const int n = (int)(i % nq) * 8;
+  float4 v[8][2];
+#pragma unroll
+  for (int s = 0; s < 8; ++s)
+    if (s < S) {
+      const float4* p = reinterpret_cast<const float4*>(part + ((long)s * M + m) * N + n);
+      v[s][0] = __ldcs(p);
+      v[s][1] = __ldcs(p + 1);
+    }
+  float o[8] = {v[0][0].x, v[0][0].y, v[0][0].z, v[0][0].w, v[0][1].x, v[0][1].y, v[0][1].z, v[0][1].w};
+#pragma unroll
+  for (int s = 1; s < 8; ++s)
+    if (s < S) {
+      o[0] += v[s][0].x, o[1] += v[s][0].y, o[2] += v[s][0].z, o[3] += v[s][0].w;
+      o[4] += v[s][1].x, o[5] += v[s][1].y, o[6] += v[s][1].z, o[7] += v[s][1].w;
+    }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    o[k] *= alpha;
+    if (bias) o[k] += bias[n + k];
+    if (temb) o[k] += temb[(m / rows_per_img) * ld_temb + n + k];
+    if (act == ACT_SILU) o[k] = silu_f(o[k]);
+  }
+  if (res) {
+    const uint4 r = *reinterpret_cast<const uint4*>(res + m * ldr + n);
+    const bf16* e = reinterpret_cast<const bf16*>(&r);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o[k] += cvt16(e[k], is_f16);
+  }
+  *reinterpret_cast<uint4*>(out + m * ldo + col_off + n) =
+      make_uint4(pack16(o[0], o[1], is_f16), pack16(o[2], o[3], is_f16), pack16(o[4], o[5], is_f16),
+                 pack16(o[6], o[7], is_f16));
 }
 
 template <int BN, int CG, int MODE, int EPW>
@@ -1225,7 +1308,14 @@ void gemm(const GemmDesc& d, cudaStream_t st) {
     dispatch<GEMM_DENSE>(bn, cg, maps, a, st);
   else
     dispatch<GEMM_CONV3>(bn, cg, maps, a, st);
-  if (a.splits > 1) {
+  if (a.splits > 1 && a.splits <= 8 && d.N % 8 == 0 && d.ldo % 8 == 0 && d.col_off % 8 == 0 &&
+      (!d.res || d.ldr % 8 == 0)) {
+    const long n8 = (long)a.M * (d.N / 8);
+    launch_k(splitk_reduce8_kernel, (unsigned)cdiv(n8, 256), 256, 0, st, a.part, a.splits, a.M, d.N, d.bias, d.temb,
+             d.ld_temb, d.mode == GEMM_DENSE ? (d.rows_per_img > 0 ? d.rows_per_img : 1) : d.H * d.W, d.res, d.ldr,
+             d.act, d.alpha, reinterpret_cast<bf16*>(d.out), d.ldo, d.col_off, d.f16);
+    SD_CHECK_LAUNCH();
+  } else if (a.splits > 1) {
     const long n4 = (long)a.M * (d.N / 4);
     launch_k(splitk_reduce_kernel, (unsigned)cdiv(n4, 256), 256, 0, st, 
         a.part, a.splits, a.M, d.N, d.bias, d.temb, d.ld_temb,
