@@ -409,6 +409,16 @@ sd_status sd_debug_gemm_gn(const void* A, const void* B, const float* bias, cons
 sd_status sd_debug_groupnorm_parts(const void* x0, int32_t C0, const float* part0, const void* x1, int32_t C1,
                                    const float* part1, void* y, int32_t nb, int32_t P, int32_t G, const float* gamma,
                                    const float* beta, float eps, int32_t silu, void* stream);
+/* LayerNorm folded into the consumer GEMM ("LN into the GEMM"; the LayerNorm and
+ * linear definitions of PAPER.md's UNet / SURVEY §2.4 K9 are unchanged — only where the normalisation is
+ * applied moves): x 16-bit [T][K] (the raw hidden state), W 16-bit [N][K], gamma / beta / bias fp32 (bias
+ * optional). cols = 0: D [T][N] (or [T][N/2] with act = 2, GEGLU over 128-column groups) = LN(x)·Wᵀ + b;
+ * cols = 1: D [N][T] = W·LN(x)ᵀ + b (the Vᵀ projection: LN output as the B operand, bias per row). Computed
+ * as W′ = W·diag(gamma) (16-bit), w̄ = row sums of W′, b′ = b + W·beta, per-token (μ, rstd), and the GEMM
+ * epilogue v = rstd·(acc − μ·w̄) + b′. Device buffers, caller-owned; scratch is stream-ordered. */
+sd_status sd_debug_gemm_ln(const void* x, int32_t T, const void* W, int32_t N, int32_t K, const float* gamma,
+                           const float* beta, const float* bias, void* D, float eps, int32_t cols, int32_t act,
+                           void* stream);
 sd_status sd_debug_layernorm(const void* x, void* y, int32_t T, int32_t C, const float* gamma, const float* beta,
                              float eps, void* stream);
 /* sd_debug_step_eps: the UNet part of sd_step_batch only (K11 gather → UNet), with the same rows as

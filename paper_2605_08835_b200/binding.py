@@ -159,6 +159,7 @@ SIGNATURES = {
     "sd_debug_conv3x3_s2": [P, I32, P, P, P, I32, I32, I32, I32, P],
     "sd_debug_conv3x3_gn": [P, I32, P, P, P, P, I32, I32, I32, I32, P, P],
     "sd_debug_gemm_gn": [P, P, P, P, P, I32, I32, I32, I32, P, P],
+    "sd_debug_gemm_ln": [P, I32, P, I32, I32, P, P, P, P, C.c_float, I32, I32, P],
     "sd_debug_groupnorm_parts": [P, I32, P, P, I32, P, P, I32, I32, I32, P, P, C.c_float, I32, P],
     "sd_debug_step_eps": [P, C.POINTER(Batch), P, P],
     "sd_debug_combine_update": [P, C.POINTER(Batch), P, P],

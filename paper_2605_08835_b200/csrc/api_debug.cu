@@ -325,6 +325,68 @@ extern "C" sd_status sd_debug_groupnorm_parts(const void* x0, int32_t C0, const 
   SD_API_END
 }
 
+namespace {
+template <class T>
+void gemm_ln_impl(const void* x, int32_t T_, const void* W, int32_t Nw, int32_t K, const float* gamma,
+                  const float* beta, const float* bias, void* D, float eps, int32_t cols, int32_t act,
+                  cudaStream_t st) {
+  float2* stat = nullptr;
+  T* Wf = nullptr;
+  float *wbar = nullptr, *bf = nullptr;
+  SD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&stat), (size_t)T_ * sizeof(float2), st));
+  SD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&Wf), (size_t)Nw * K * sizeof(T), st));
+  SD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&wbar), (size_t)Nw * sizeof(float), st));
+  SD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bf), (size_t)Nw * sizeof(float), st));
+  sd::ln_stats(static_cast<const T*>(x), T_, K, eps, stat, st);
+  sd::ln_fold(static_cast<const T*>(W), Nw, K, gamma, beta, bias, Wf, wbar, bf, st);
+  sd::GemmDescT<T> d;
+  d.mode = sd::GEMM_DENSE;
+  d.K = K;
+  d.lda = K;
+  d.ldb = K;
+  d.ln_stat = stat;
+  d.ln_wbar = wbar;
+  d.ln_cols = cols;
+  d.bias = bf;
+  d.out = D;
+  if (!cols) {  // D[T][Nw] = LN(x)·Wᵀ + b
+    d.A = static_cast<const T*>(x);
+    d.M = T_;
+    d.Bw[0] = Wf;
+    d.N = Nw;
+    d.act = act;
+    d.ldo = act == sd::ACT_GEGLU ? Nw / 2 : Nw;
+  } else {  // D[Nw][T] = W·LN(x)ᵀ + b (bias per row)
+    d.A = Wf;
+    d.M = Nw;
+    d.Bw[0] = static_cast<const T*>(x);
+    d.N = T_;
+    d.bias_per_row = 1;
+    d.ldo = T_;
+  }
+  sd::gemm(d, st);
+  SD_CUDA(cudaFreeAsync(stat, st));
+  SD_CUDA(cudaFreeAsync(Wf, st));
+  SD_CUDA(cudaFreeAsync(wbar, st));
+  SD_CUDA(cudaFreeAsync(bf, st));
+}
+}  // namespace
+
+extern "C" sd_status sd_debug_gemm_ln(const void* x, int32_t T, const void* W, int32_t N, int32_t K, const float* gamma,
+                                      const float* beta, const float* bias, void* D, float eps, int32_t cols,
+                                      int32_t act, void* stream) {
+  SD_REQUIRE(x && W && gamma && beta && D && T > 0 && N > 0 && K > 0 && K % 8 == 0 && (act == 0 || act == 2) &&
+                 (!cols || act == 0),
+             "sd_debug_gemm_ln: bad arguments");
+  SD_API_BEGIN
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (g_dbg_f16)
+    gemm_ln_impl<f16>(x, T, W, N, K, gamma, beta, bias, D, eps, cols, act, st);
+  else
+    gemm_ln_impl<bf16>(x, T, W, N, K, gamma, beta, bias, D, eps, cols, act, st);
+  SD_API_END
+}
+
 extern "C" sd_status sd_debug_layernorm(const void* x, void* y, int32_t T, int32_t C, const float* gamma,
                                         const float* beta, float eps, void* stream) {
   SD_REQUIRE(x && y && gamma && beta && T > 0 && C > 0 && C % 8 == 0, "sd_debug_layernorm: bad arguments");

@@ -384,6 +384,7 @@ Engine::~Engine() {
   if (aug_cache) cudaFree(aug_cache);
   if (reg_scratch) cudaFree(reg_scratch);
   if (gn_ws) cudaFree(gn_ws);
+  if (fold_mem) cudaFree(fold_mem);
   if (tile_scratch) cudaFree(tile_scratch);
   if (tile_ev) cudaEventDestroy(tile_ev);
   if (time_ids) cudaFree(time_ids);
@@ -431,6 +432,7 @@ void set_weight(Engine* e, const std::string& name, const float* host, size_t by
   SD_CUDA(cudaMemcpyAsync(d, host, bytes, cudaMemcpyHostToDevice, st));
   w.src = d;
   init_weight(w, st);
+  e->fold_dirty = true;  // folded LayerNorm weights are recomputed before the next step
   SD_CUDA(cudaStreamSynchronize(st));
   SD_CUDA(cudaStreamDestroy(st));
   SD_CUDA(cudaFree(d));
@@ -456,6 +458,48 @@ void build_engine(Engine* e) {
   SD_CUDA(cudaStreamSynchronize(st));
   SD_CUDA(cudaStreamDestroy(st));
   e->ws.init(unet_ws_bytes(e));
+  {
+    // off by default: measured slower on the bench step (LayerNorm 42.0 → 23.6 ms but dense GEMMs
+    // 262.7 → 298.9 ms per bench step — the short-K consumer GEMMs are epilogue-bound, and the per-element
+    // correction with its w̄ / per-column (μ, rstd) loads lands on that critical path); SD_LN_FOLD=1 enables
+    const char* lf = getenv("SD_LN_FOLD");
+    e->ln_fold = !e->f32 && (lf && lf[0] == '1');
+  }
+  if (e->ln_fold) {
+    // folded copies of every transformer block's LN-consumer weights (3C + C + 8C rows of C) + 2 vectors each
+    std::vector<TfW*> tfs;
+    for (auto& d : e->U.down)
+      for (auto& t : d.tf) tfs.push_back(&t);
+    tfs.push_back(&e->U.midtf);
+    for (auto& u : e->U.up)
+      for (auto& t : u.tf) tfs.push_back(&t);
+    size_t bytes = 0;
+    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+    for (TfW* t : tfs)
+      for (size_t j = 0; j < t->blk.size(); ++j)
+        bytes += al(12L * t->C * t->C * e->esize) + 2 * al(12L * t->C * sizeof(float)) + 1024;
+    if (bytes) {
+      SD_CUDA(cudaMalloc(&e->fold_mem, bytes));
+      char* p = static_cast<char*>(e->fold_mem);
+      auto take = [&](size_t b) {
+        char* r = p;
+        p += al(b);
+        return r;
+      };
+      for (TfW* t : tfs)
+        for (BlkW& k : t->blk) {
+          const long C = t->C;
+          k.wqkv_f = take(3 * C * C * e->esize);
+          k.wq2_f = take(C * C * e->esize);
+          k.wff1_f = take(8 * C * C * e->esize);
+          float* v = reinterpret_cast<float*>(take(12 * C * sizeof(float)));
+          k.wb_qkv = v, k.wb_q2 = v + 3 * C, k.wb_ff1 = v + 4 * C;
+          v = reinterpret_cast<float*>(take(12 * C * sizeof(float)));
+          k.bf_qkv = v, k.bf_q2 = v + 3 * C, k.bf_ff1 = v + 4 * C;
+        }
+    }
+    e->fold_dirty = true;
+  }
   {
     const size_t gb = gn_workspace_bytes(e->max_rows, e->cfg.max_latent_hw * e->cfg.max_latent_hw * 4, 64, 4096);
     SD_CUDA(cudaMalloc(&e->gn_ws, gb));
@@ -664,6 +708,14 @@ struct Fwd {
       group_norm(x, y, R, P, C, e->uc.groups, g, b, eps, silu, gn_ws, st);
     e->prof.end(pi, st);
   }
+  // folded LayerNorm: per-token (μ, rstd) only (8 bytes per token); the consumer GEMMs normalise
+  const float2* ln_st(const AT* x, long T, int C) {
+    float2* st_ = e->ws.get<float2>((size_t)T);
+    const int pi = e->prof.begin(PC_LN, st, 1.0 * T * C * 2);
+    if constexpr (!std::is_same<AT, float>::value) ln_stats(x, (int)T, C, e->uc.eps_ln, st_, st);
+    e->prof.end(pi, st);
+    return st_;
+  }
   void ln(const AT* x, AT* y, long T, int C, const float* g, const float* b) {
     const int pi = e->prof.begin(PC_LN, st, 2.0 * T * C * 2);
     layer_norm(x, y, (int)T, C, g, b, e->uc.eps_ln, st);
@@ -676,7 +728,7 @@ struct Fwd {
   }
   void linear(const AT* A, long M, int K, const AT* W, int N, const float* bias, void* out, int ldo,
               const AT* res = nullptr, int act = ACT_NONE, int out_f32 = 0, int cls = PC_GEMM, float2* gp = nullptr,
-              int gn_P = 0) {
+              int gn_P = 0, const float2* ln_st = nullptr, const float* ln_wb = nullptr, int ln_cols = 0) {
     GemmDescT<AT> d;
     d.A = A;
     d.M = (int)M;
@@ -693,6 +745,10 @@ struct Fwd {
     d.act = act;
     d.out_f32 = out_f32;
     d.gn_P = gn_P;
+    d.ln_stat = ln_st;  // folded LayerNorm (the weights / bias passed in are W′ / b′)
+    d.ln_wbar = ln_wb;
+    d.ln_cols = ln_cols;
+    d.bias_per_row = ln_cols;  // the Vᵀ projection: b′ per output row
     // split-K for the transformer projections of the ≤ 64-pixel levels (8×8: [1024, 1280, 1280] at 16
     // rows is 40 output tiles on 148 SMs): a function of the layer (pixels per image, K), not of the
     // batch — fp32 partials summed in split order, batch-invariant. Off by default (SD_DENSE_SPLIT=3
@@ -830,22 +886,38 @@ struct Fwd {
     for (const BlkW& k : t.blk) {
       const size_t mb = e->ws.mark();
       AT* n = buf(T * C);
-      ln(h, n, T, C, k.l1g, k.l1b);
+      const bool fold = e->ln_fold;  // LayerNorm folded into the q|k|v, q2 and FF1 GEMMs (no normalised copy)
+      const float2* s1 = nullptr;
+      if (fold)
+        s1 = ln_st(h, T, C);
+      else
+        ln(h, n, T, C, k.l1g, k.l1b);
       AT* o = buf(T * C);
       bool tc = false;
       if constexpr (!std::is_same<AT, float>::value) tc = e->use_attn_tc && attention_tc_supported(dh, P, C);
       if (tc) {
         // tcgen05 flash attention: q|k token-major from one GEMM, Vᵀ channel-major from another
         AT* qk = buf(T * 2 * C);
-        linear(n, T, C, wt<AT>(k.wqkv), 2 * C, nullptr, qk, 2 * C);
         AT* vt = buf(T * C);
-        linear(wt<AT>(k.wqkv) + 2L * C * C, C, C, n, (int)T, nullptr, vt, (int)T);
+        if (fold) {
+          linear(h, T, C, wt<AT>(k.wqkv_f), 2 * C, k.bf_qkv, qk, 2 * C, nullptr, ACT_NONE, 0, PC_GEMM, nullptr, 0, s1,
+                 k.wb_qkv, 0);
+          linear(wt<AT>(k.wqkv_f) + 2L * C * C, C, C, h, (int)T, k.bf_qkv + 2 * C, vt, (int)T, nullptr, ACT_NONE, 0,
+                 PC_GEMM, nullptr, 0, s1, k.wb_qkv + 2 * C, 1);
+        } else {
+          linear(n, T, C, wt<AT>(k.wqkv), 2 * C, nullptr, qk, 2 * C);
+          linear(wt<AT>(k.wqkv) + 2L * C * C, C, C, n, (int)T, nullptr, vt, (int)T);
+        }
         const int pi = e->prof.begin(PC_ATTN, st, 4.0 * R * heads * (double)P * P * dh);
         if constexpr (!std::is_same<AT, float>::value) attention_tc(qk, vt, o, R, heads, dh, C, P, st);
         e->prof.end(pi, st);
       } else {
         AT* qkv = buf(T * 3 * C);
-        linear(n, T, C, wt<AT>(k.wqkv), 3 * C, nullptr, qkv, 3 * C);
+        if (fold)
+          linear(h, T, C, wt<AT>(k.wqkv_f), 3 * C, k.bf_qkv, qkv, 3 * C, nullptr, ACT_NONE, 0, PC_GEMM, nullptr, 0, s1,
+                 k.wb_qkv, 0);
+        else
+          linear(n, T, C, wt<AT>(k.wqkv), 3 * C, nullptr, qkv, 3 * C);
         AttnDescT<AT> ad{};
         ad.Q = qkv;
         ad.ldq = 3 * C;
@@ -867,9 +939,14 @@ struct Fwd {
       }
       AT* h2 = buf(T * C);
       linear(o, T, C, wt<AT>(k.wo), C, k.bo, h2, C, h);
-      ln(h2, n, T, C, k.l2g, k.l2b);
       AT* q2 = buf(T * C);
-      linear(n, T, C, wt<AT>(k.wq2), C, nullptr, q2, C);
+      if (fold) {
+        const float2* s2 = ln_st(h2, T, C);
+        linear(h2, T, C, wt<AT>(k.wq2_f), C, k.bf_q2, q2, C, nullptr, ACT_NONE, 0, PC_GEMM, nullptr, 0, s2, k.wb_q2, 0);
+      } else {
+        ln(h2, n, T, C, k.l2g, k.l2b);
+        linear(n, T, C, wt<AT>(k.wq2), C, nullptr, q2, C);
+      }
       bool xtc = false, xtc2 = false;
       if constexpr (!std::is_same<AT, float>::value) {
         xtc2 = e->use_xattn_tc2 && e->vt_cache && xattention_tc2_supported(dh, e->uc.ctx_len);
@@ -916,9 +993,15 @@ struct Fwd {
       }
       AT* h3 = buf(T * C);
       linear(o, T, C, wt<AT>(k.wo2), C, k.bo2, h3, C, h2);
-      ln(h3, n, T, C, k.l3g, k.l3b);
       AT* gg = buf(T * 4 * C);
-      linear(n, T, C, wt<AT>(k.wff1), 8 * C, k.bff1, gg, 4 * C, nullptr, ACT_GEGLU);
+      if (fold) {
+        const float2* s3 = ln_st(h3, T, C);
+        linear(h3, T, C, wt<AT>(k.wff1_f), 8 * C, k.bf_ff1, gg, 4 * C, nullptr, ACT_GEGLU, 0, PC_GEMM, nullptr, 0, s3,
+               k.wb_ff1, 0);
+      } else {
+        ln(h3, n, T, C, k.l3g, k.l3b);
+        linear(n, T, C, wt<AT>(k.wff1), 8 * C, k.bff1, gg, 4 * C, nullptr, ACT_GEGLU);
+      }
       linear(gg, T, 4 * C, wt<AT>(k.wff2), C, k.bff2, hb, C, h3);  // block output → hb
       e->ws.reset(mb);
       std::swap(h, hb);
@@ -1105,7 +1188,37 @@ float init_sigma(int sampler, int n) {
 // eps_dump (debug): run the gather and the UNet only, copy ε (fp32 NHWC [rows][h][w][4], rows in R26
 // order) to eps_dump and leave the latents alone. eps_inject (debug): skip the UNet and apply the K12
 // combine + sampler to the given ε (same layout). Both run eagerly (no graph).
+// recompute the folded LayerNorm weights (W′ = W·diag(γ), w̄, b′ = b + W·β) of every transformer block, on
+// the step's stream, when a weight changed since the last fold (build, sd_engine_set_weight)
+template <class AT>
+static void refold_t(Engine* e, cudaStream_t st) {
+  auto fold_tf = [&](TfW& t) {
+    const int C = t.C;
+    for (BlkW& k : t.blk) {
+      ln_fold(wt<AT>(k.wqkv), 3 * C, C, k.l1g, k.l1b, (const float*)nullptr, static_cast<AT*>(k.wqkv_f), k.wb_qkv,
+              k.bf_qkv, st);
+      ln_fold(wt<AT>(k.wq2), C, C, k.l2g, k.l2b, (const float*)nullptr, static_cast<AT*>(k.wq2_f), k.wb_q2, k.bf_q2,
+              st);
+      ln_fold(wt<AT>(k.wff1), 8 * C, C, k.l3g, k.l3b, k.bff1, static_cast<AT*>(k.wff1_f), k.wb_ff1, k.bf_ff1, st);
+    }
+  };
+  for (auto& d : e->U.down)
+    for (auto& t : d.tf) fold_tf(t);
+  fold_tf(e->U.midtf);
+  for (auto& u : e->U.up)
+    for (auto& t : u.tf) fold_tf(t);
+}
+static void refold_if_dirty(Engine* e, cudaStream_t st) {
+  if (!e->ln_fold || !e->fold_dirty) return;
+  if (e->f16)
+    refold_t<f16>(e, st);
+  else
+    refold_t<bf16>(e, st);
+  e->fold_dirty = false;
+}
+
 void step_batch(Engine* e, const sd_batch* b, cudaStream_t st, float* eps_dump, const float* eps_inject) {
+  refold_if_dirty(e, st);
   const int n = b->n_req, h = b->latent_h, w = b->latent_w, hw = h * w;
   std::vector<int> row_req, unc_row(n, -1);
   for (int r = 0; r < n; ++r) row_req.push_back(r);

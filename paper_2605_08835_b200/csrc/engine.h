@@ -69,6 +69,11 @@ struct BlkW {  // one BasicTransformerBlock
   float *l1g, *l1b, *bo, *l2g, *l2b, *bo2, *l3g, *l3b, *bff1, *bff2;
   wptr wqkv, wo, wq2, wo2, wff1, wff2;
   int koff, voff;  // column offsets of this block's K / V in the text K/V cache rows
+  // LayerNorm folded into the consumer GEMMs (Engine::ln_fold; norm.cu ln_fold): W′ = W·diag(γ) of the
+  // LN1 → q|k|v, LN2 → q2 and LN3 → FF1 weights, their row sums w̄ and the folded biases b′
+  wptr wqkv_f = nullptr, wq2_f = nullptr, wff1_f = nullptr;
+  float *wb_qkv = nullptr, *bf_qkv = nullptr, *wb_q2 = nullptr, *bf_q2 = nullptr, *wb_ff1 = nullptr,
+        *bf_ff1 = nullptr;
 };
 struct TfW {  // one Transformer2DModel: GN → proj_in → blocks → proj_out (+ x)
   int C;
@@ -202,6 +207,11 @@ struct Engine {
   // streams (no stream-ordered allocation on the admission path)
   char* reg_scratch = nullptr;
   void* gn_ws = nullptr;  // UNet GroupNorm workspace (partials + affine table), persistent
+  // LayerNorm folded into its consumer GEMMs (16-bit modes, SD_LN_FOLD=1; off by default: measured slower):
+  // the folded weights live in fold_mem and are recomputed before the next step whenever a weight changed
+  bool ln_fold = false;
+  bool fold_dirty = true;
+  void* fold_mem = nullptr;
   float* time_ids = nullptr;
   cudaEvent_t reg_ev = nullptr;
   bool reg_ev_valid = false;

@@ -56,7 +56,37 @@ struct GemmArgs {
   // box sw × sh at (x, y): (y / sh) · (W / sw) + x / sw; of a dense quarter: (row mod gn_P) / 32.
   float2* gn_part;
   int gn_P, gn_slots, gn_sw, gn_sh;
+  const float2* ln_stat;  // folded LayerNorm (GemmDescT::ln_stat)
+  const float* ln_wbar;
+  int ln_cols;
 };
+
+// folded LayerNorm: o ← rstd·(o − μ·w̄) for the 32 columns [col, col + 32) of this lane's row (before the bias)
+__device__ __forceinline__ void ln_correct32(const GemmArgs& g, float* o, long prow, bool valid, int col) {
+  if (!g.ln_cols) {
+    const float2 st = valid ? __ldg(g.ln_stat + prow) : make_float2(0.f, 0.f);
+    if (col + 32 <= g.N) {
+      const float4* w4 = reinterpret_cast<const float4*>(g.ln_wbar + col);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float4 w = __ldg(w4 + i);
+        o[4 * i] = st.y * fmaf(-st.x, w.x, o[4 * i]);
+        o[4 * i + 1] = st.y * fmaf(-st.x, w.y, o[4 * i + 1]);
+        o[4 * i + 2] = st.y * fmaf(-st.x, w.z, o[4 * i + 2]);
+        o[4 * i + 3] = st.y * fmaf(-st.x, w.w, o[4 * i + 3]);
+      }
+    } else {
+      for (int i = 0; i < 32 && col + i < g.N; ++i) o[i] = st.y * fmaf(-st.x, __ldg(g.ln_wbar + col + i), o[i]);
+    }
+  } else {
+    const float wb = valid ? __ldg(g.ln_wbar + prow) : 0.f;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const float2 st = col + i < g.N ? __ldg(g.ln_stat + col + i) : make_float2(0.f, 0.f);
+      o[i] = st.y * fmaf(-st.x, wb, o[i]);
+    }
+  }
+}
 
 // tile t → (M tile, N tile, K-block range); tiles of split s follow those of split s-1
 __device__ __forceinline__ void decode_tile(const GemmArgs& g, int t, int& mt, int& nt, int& s, int& kb0, int& kb1) {
@@ -372,6 +402,10 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
           vv[i] = __uint_as_float(rv[i]) * g.alpha;
           gg[i] = __uint_as_float(rg[i]) * g.alpha;
         }
+        if (g.ln_stat) {
+          ln_correct32(g, vv, prow, valid, n0 + cv);
+          ln_correct32(g, gg, prow, valid, n0 + cgc);
+        }
         if (g.bias) {
           add32(vv, g.bias + n0 + cv);
           add32(gg, g.bias + n0 + cgc);
@@ -460,6 +494,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const CUtensorM
       for (int i = 0; i < 32; i += 2) fmul2(o[i], o[i + 1], g.alpha, g.alpha);
     }
     const bool full32 = col + 32 <= g.N;
+    if (g.ln_stat) ln_correct32(g, o, prow, valid, col);
     if (pre_b) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
@@ -1044,7 +1079,7 @@ int gemm_splits(const GemmDesc& d) {
     const char* s = getenv("SD_SPLITK");
     env = s ? atoi(s) : -1;
   }
-  if (d.splits == 1) return 1;
+  if (d.splits == 1 || d.ln_stat) return 1;
   if (d.act == ACT_GEGLU || d.out_f32 || d.bias_per_row || d.N % 4 || d.ldo % 4 || d.col_off % 4) return 1;
   if (d.mode == GEMM_DENSE) {
     // dense: only an explicit split count (the caller picks it from the layer, never from the batch, so
@@ -1148,6 +1183,11 @@ void gemm(const GemmDesc& d, cudaStream_t st) {
       a.num_kb += 9 * a.kb_src[s];
     }
   }
+  a.ln_stat = d.ln_stat;
+  a.ln_wbar = d.ln_wbar;
+  a.ln_cols = d.ln_cols;
+  if (d.ln_stat && (d.mode != GEMM_DENSE || !d.ln_wbar || d.act == ACT_SILU))
+    throw CudaError("gemm: folded LayerNorm needs a dense launch with w-bar (no SiLU)");
   a.gn_part = d.gn_part;
   if (d.gn_part) {
     const int P = d.mode == GEMM_DENSE ? d.gn_P : d.H * d.W;

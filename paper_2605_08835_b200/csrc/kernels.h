@@ -64,6 +64,13 @@ struct GemmDescT {
   // gemm_gn_ok(d); gn_P = pixels per image (dense mode; conv3 uses H·W).
   float2* gn_part = nullptr;
   int gn_P = 0;
+  // LayerNorm folded into this GEMM (dense; norm.cu ln_fold / ln_stats): the weights are W′ = W·diag(γ) and
+  // the bias b′; the epilogue applies v = rstd·(acc − μ·w̄) before the bias, with (μ, rstd) = ln_stat[row]
+  // and w̄ = ln_wbar[column] — or, with ln_cols (the LN output is the B operand: Vᵀ = W·LN(h)ᵀ), (μ, rstd) =
+  // ln_stat[column] and w̄ = ln_wbar[row]. Never split.
+  const float2* ln_stat = nullptr;
+  const float* ln_wbar = nullptr;
+  int ln_cols = 0;
 };
 
 using GemmDesc = GemmDescT<bf16>;

@@ -41,6 +41,13 @@ void group_norm_parts(const T* x0, int C0, const float2* part0, const T* x1, int
 template <class T>
 void gn_apply_range_parts(const T* x, T* y, int P, int C, int G, int p0, int p1, const float2* part, const float* gamma,
                           const float* beta, float eps, bool silu, void* ws, cudaStream_t st);
+// LayerNorm folded into the consumer GEMM (norm.cu; gemm.cu ln_stat epilogue): per-token (μ, rstd), and
+// the folded weights W′ = W·diag(γ) (16-bit), w̄ = row sums of W′, b′ = b + W·β (bias may be null)
+template <class T>
+void ln_stats(const T* x, int T_, int C, float eps, float2* st, cudaStream_t s);
+template <class T>
+void ln_fold(const T* W, int N, int K, const float* gamma, const float* beta, const float* bias, T* Wf, float* wbar,
+             float* bf, cudaStream_t s);
 template <class T>
 void layer_norm(const T* x, T* y, int T_, int C, const float* gamma, const float* beta, float eps, cudaStream_t st);
 

@@ -732,6 +732,114 @@ void layer_norm(const E* x, E* y, int T, int C, const float* gamma, const float*
   throw CudaError("layer_norm: C too large");
 }
 
+// ---- LayerNorm folded into its consumer GEMMs (the algebraic form; gemm.cu ln_stat epilogue) ----------
+// LN(h)·Wᵀ + b = rstd_m·(h·W′ᵀ − μ_m·w̄) + b′ with W′ = W·diag(γ), w̄_n = Σ_k W′_nk, b′ = b + W·β: the GEMM reads
+// the raw hidden state h and its epilogue applies (μ_m, rstd_m) per row (or per column when h is the B
+// operand, the Vᵀ projection). ln_stats: the same two-pass register arithmetic as layer_norm_kernel, only
+// the per-token (μ, rstd) written (8 bytes per token instead of the normalised row).
+template <int NV, int LANES, class E>
+__global__ void ln_stats_kernel(const E* __restrict__ x, int T, int C, float eps, float2* __restrict__ st) {
+  pdl_wait();
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int tok = gtid / LANES, l = gtid % LANES;
+  if (tok >= T) return;
+  const int V = C / 8;
+  const E* xr = x + (long)tok * C;
+  float f[NV][8];
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int vi = l + LANES * k;
+    if (vi < V) {
+      load8(xr + vi * 8, f[k]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) f[k][i] = 0.f;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += f[k][i];
+#pragma unroll
+  for (int o = LANES / 2; o; o >>= 1) s += __shfl_xor_sync(0xffffffff, s, o);
+  const float mean = s / C;
+  float q = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+    if (l + LANES * k < V)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float d = f[k][i] - mean;
+        q += d * d;
+      }
+#pragma unroll
+  for (int o = LANES / 2; o; o >>= 1) q += __shfl_xor_sync(0xffffffff, q, o);
+  if (l == 0) st[tok] = make_float2(mean, rsqrtf(q / C + eps));
+}
+
+template <int NV, int LANES, class E>
+static void lns_launch(const E* x, int T, int C, float eps, float2* st, cudaStream_t s) {
+  const long total = (long)T * LANES;
+  launch_k(ln_stats_kernel<NV, LANES, E>, cdiv(total, 256), 256, 0, s, x, T, C, eps, st);
+  SD_CHECK_LAUNCH();
+}
+
+template <class E>
+void ln_stats(const E* x, int T, int C, float eps, float2* st, cudaStream_t s) {
+  if (C % 8) throw CudaError("ln_stats: C % 8");
+  const int V = C / 8;
+  if (V == 40) return lns_launch<5, 8>(x, T, C, eps, st, s);
+  if (V == 80) return lns_launch<5, 16>(x, T, C, eps, st, s);
+  if (V == 160) return lns_launch<5, 32>(x, T, C, eps, st, s);
+  if (V <= 4) return lns_launch<1, 4>(x, T, C, eps, st, s);
+  if (V <= 8) return lns_launch<1, 8>(x, T, C, eps, st, s);
+  if (V <= 16) return lns_launch<1, 16>(x, T, C, eps, st, s);
+  if (V <= 32) return lns_launch<1, 32>(x, T, C, eps, st, s);
+  if (V <= 64) return lns_launch<2, 32>(x, T, C, eps, st, s);
+  if (V <= 128) return lns_launch<4, 32>(x, T, C, eps, st, s);
+  if (V <= 256) return lns_launch<8, 32>(x, T, C, eps, st, s);
+  throw CudaError("ln_stats: C too large");
+}
+
+// one warp per weight row n: W′[n][k] = 16-bit(W[n][k]·γ[k]); w̄[n] = Σ_k W′[n][k] (of the rounded values the
+// MMA multiplies, so the μ term cancels exactly up to fp32 accumulation); b′[n] = b[n] + Σ_k W[n][k]·β[k].
+// Fixed lane-strided order and xor butterfly: deterministic.
+template <class E>
+__global__ void ln_fold_kernel(const E* __restrict__ W, int N, int K, const float* __restrict__ gamma,
+                               const float* __restrict__ beta, const float* __restrict__ bias, E* __restrict__ Wf,
+                               float* __restrict__ wbar, float* __restrict__ bf) {
+  const int n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (n >= N) return;
+  const E* wr = W + (long)n * K;
+  E* fr = Wf + (long)n * K;
+  float sw = 0.f, sb = 0.f;
+  for (int k = lane; k < K; k += 32) {
+    const float w = act_ld(wr + k);
+    E wf;
+    act_st(&wf, w * gamma[k]);
+    fr[k] = wf;
+    sw += act_ld(&wf);
+    sb = fmaf(w, beta[k], sb);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    sw += __shfl_xor_sync(0xffffffff, sw, o);
+    sb += __shfl_xor_sync(0xffffffff, sb, o);
+  }
+  if (lane == 0) {
+    wbar[n] = sw;
+    bf[n] = (bias ? bias[n] : 0.f) + sb;
+  }
+}
+
+template <class E>
+void ln_fold(const E* W, int N, int K, const float* gamma, const float* beta, const float* bias, E* Wf, float* wbar,
+             float* bf, cudaStream_t s) {
+  launch_k(ln_fold_kernel<E>, cdiv(N, 8), 256, 0, s, W, N, K, gamma, beta, bias, Wf, wbar, bf);
+  SD_CHECK_LAUNCH();
+}
+
 #define SD_NORM_INST(T)                                                                                      \
   template void group_norm<T>(const T*, T*, int, int, int, int, const float*, const float*, float, bool, void*, \
                               cudaStream_t);                                                                 \
@@ -741,6 +849,9 @@ void layer_norm(const E* x, E* y, int T, int C, const float* gamma, const float*
   template void layer_norm<T>(const T*, T*, int, int, const float*, const float*, float, cudaStream_t);   \
   template void group_norm2<T>(const T*, int, const T*, int, T*, int, int, int, const float*, const float*, float, \
                                bool, void*, cudaStream_t);                                                   \
+  template void ln_stats<T>(const T*, int, int, float, float2*, cudaStream_t);                               \
+  template void ln_fold<T>(const T*, int, int, const float*, const float*, const float*, T*, float*, float*,  \
+                           cudaStream_t);                                                                    \
   template void group_norm_parts<T>(const T*, int, const float2*, const T*, int, const float2*, T*, int, int, int, \
                                     const float*, const float*, float, bool, void*, cudaStream_t);           \
   template void gn_apply_range_parts<T>(const T*, T*, int, int, int, int, int, const float2*, const float*,     \

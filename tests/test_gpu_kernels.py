@@ -437,3 +437,30 @@ def test_gemm_gn_epilogue_stats_and_concat(nb, P, N, K):
     torch.cuda.synchronize()
     cat = torch.cat([y.cpu().reshape(nb, P, N), y1.cpu().reshape(nb, P, C1)], -1)
     assert rel(gn.cpu(), _gn_ref(cat, 32, gam, bet, 1)) < 6e-3
+
+
+@pytest.mark.parametrize("T,N,K,cols,act", [(1000, 640, 320, 0, 0), (300, 1280, 1280, 0, 0), (4096, 512, 640, 0, 2),
+                                           (200, 320, 320, 1, 0), (1024, 1280, 1280, 1, 0), (77, 2560, 1280, 0, 2)])
+def test_gemm_layernorm_folded(T, N, K, cols, act):
+    """LayerNorm folded into the GEMM (W' = W diag(gamma), w-bar, b' = b + W beta, per-token (mu, rstd) applied
+    in the epilogue) against fp64 LN then the GEMM on the same 16-bit inputs; the hidden state has a large
+    mean (mean/std ~ 3) so the cancellation of the mu term is exercised. cols = 1: the V^T projection."""
+    g = torch.Generator().manual_seed(T + N + K + cols)
+    x = bf(torch.randn(T, K, generator=g) * 2.0 + 6.0)
+    Wt = bf(torch.randn(N, K, generator=g) / K ** 0.5)
+    gam, bet = 1 + 0.2 * torch.randn(K, generator=g), 0.2 * torch.randn(K, generator=g)
+    bias = torch.randn(N, generator=g)
+    ln = F.layer_norm(x.double(), (K,), gam.double(), bet.double(), 1e-5)
+    full = ln @ Wt.double().T + bias.double()          # [T][N]
+    if act == 2:
+        v = torch.cat([full[:, 128 * j:128 * j + 64] for j in range(N // 128)], 1)
+        gt = torch.cat([full[:, 128 * j + 64:128 * j + 128] for j in range(N // 128)], 1)
+        ref = v * F.gelu(gt)
+    else:
+        ref = full.T if cols else full
+    D = torch.empty(*ref.shape, device="cuda", dtype=DT)
+    xd, Wd, gd, btd, bd = x.cuda(), Wt.cuda(), gam.cuda(), bet.cuda(), bias.cuda()
+    B.call("sd_debug_gemm_ln", B._p(xd), T, B._p(Wd), N, K, B._p(gd), B._p(btd), B._p(bd), B._p(D), 1e-5, cols, act,
+           None)
+    torch.cuda.synchronize()
+    assert rel(D.cpu(), ref) < 8e-3

@@ -95,6 +95,23 @@ def test_tiny_unet_cfg_on_off(tiny, sampler):
     assert final <= TOL and worst <= 1.0
 
 
+@pytest.mark.parametrize("precision", ["bf16", "fp16"])
+def test_tiny_unet_ln_fold(precision, monkeypatch):
+    """The folded-LayerNorm engine path (SD_LN_FOLD=1: LN1/LN2/LN3 applied in the q|k|v, Vt, q2 and FF1 GEMM
+    epilogues) against the oracle on the CFG / Skip-CFG schedule of test_tiny_unet_cfg_on_off."""
+    monkeypatch.setenv("SD_LN_FOLD", "1")
+    eng = Engine("tiny", max_latent_hw=16, b_max=4, precision=precision)
+    try:
+        ctx_u = synth.uncond_embedding(0, 8, 32)
+        eng.set_uncond(torch.from_numpy(ctx_u))
+        P = configs.unet_params(configs.TINY_UNET, 0, np.float32, bf16_weights=True)
+        final, worst, _, _ = _run_tiny(eng, P, synth.bf16_round(ctx_u), "ddim", [[1, 1], [1, 0], [0, 1], [0, 0]])
+        print(f"tiny {precision} LN-fold final rel-L2 {final:.3e}, worst per-step error / bound {worst:.3f}")
+        assert final <= TOL and worst <= 1.0
+    finally:
+        eng.close()
+
+
 def test_tiny_unet_euler():
     """R5 Euler (ε-prediction, σ grid on the same timesteps) through the bf16 path: 4 steps with CFG /
     Skip-CFG mixes vs the oracle (final latents and teacher-forced ε-parts)."""
