@@ -364,11 +364,17 @@ __device__ __forceinline__ void gn_apply_dev(const T* __restrict__ x, const T* _
     Raw8<T> u[U];
 #pragma unroll
     for (int k = 0; k < U; ++k) u[k].ld(xs + (min(pb + (long)k * R, p_end - 1) * ldv + vs) * 8);
+    // image of each row without a division per row: one per iteration, then step across image ends
+    int b = (int)((unsigned)pb / (unsigned)P);  // < 2^31 pixels (checked on the host)
+    long b_end = (long)(b + 1) * P;
 #pragma unroll
     for (int k = 0; k < U; ++k) {
       const long p = pb + (long)k * R;
       if (p >= p_end) break;
-      const int b = (int)((unsigned)p / (unsigned)P);  // < 2^31 pixels (checked on the host)
+      while (p >= b_end) {
+        ++b;
+        b_end += P;
+      }
       if (b != b_cur) {
         const float4* t4 = reinterpret_cast<const float4*>(tab + ((long)b * V + v) * 8);
 #pragma unroll
