@@ -146,7 +146,9 @@ def run_reference(args):
 
 def config(n, precision="fp16"):
     return {"workload": "CFG#2: SD-1.5-shaped UNet (bf16-valued weights), 512x512 (latent 64x64), 8 requests/GPU "
-                        "lockstep x 50 DDIM steps, CFG every step (16 UNet rows/step), then 8 whole VAE decodes",
+                        "lockstep x 50 DDIM steps, CFG every step (16 UNet rows/step), then 8 whole VAE decodes "
+                        "(on a low-priority stream, overlapping the next batch's UNet steps: PAPER.md:146-148; "
+                        "--no-overlap serialises them)",
             "precision": f"{precision} tensor-core operands / activations, fp32 accumulation (DESIGN R19a)",
             "model": "sd15-shaped UNet (859.5M params) + SD VAE decoder, random init", "global_batch": N_REQ * n,
             "seq_len": LAT * LAT, "parallelism": f"dp{n} (request sharding, weak scaling)",
@@ -226,6 +228,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-serving", action="store_true")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="decode each batch on the UNet stream after its last step instead of on the "
+                         "low-priority VAE stream overlapping the next batch's UNet steps")
     ap.add_argument("--serving-requests", type=int, default=200)
     ap.add_argument("--rho", type=float, default=0.8)
     ap.add_argument("--profile-range", action="store_true",
@@ -256,7 +261,10 @@ def main():
 
     eng = Engine("sd15", max_latent_hw=LAT, b_max=N_REQ, device=local, precision=args.precision)
     eng.set_uncond(torch.from_numpy(synth.uncond_embedding(0, 77, 768)))
-    st = torch.cuda.Stream(device=dev)
+    # UNet steps on a high-priority stream; each batch's decodes on a low-priority one, overlapping the
+    # next batch's UNet steps (the paper's UNet ∥ VAE co-execution, at batch granularity)
+    st = torch.cuda.Stream(device=dev, priority=-1)
+    vst = torch.cuda.Stream(device=dev, priority=0)
     ids = [rank * N_REQ + i for i in range(N_REQ)]
     # host inputs (pinned): text embeddings and initial noise per request (R20)
     emb_h = torch.from_numpy(np.stack([synth.text_embedding(1, i, 77, 768) for i in ids])).pin_memory()
@@ -266,17 +274,44 @@ def main():
     emb_d = emb_h.to(dev)
     z_d = z_h.to(dev)
     slots = [eng.register(emb_d[i]) for i in range(N_REQ)]
-    lat = torch.empty_like(z_d)
+    lats = [torch.empty_like(z_d), torch.empty_like(z_d)]  # batch k uses lats[k % 2]
     imgs = torch.empty(N_REQ, 3, 8 * LAT, 8 * LAT, device=dev)
+    pipe = {"k": 0, "dec": [None, None], "last": None}
 
-    def denoise_and_decode(slot_ids):
+    def denoise_and_decode(slot_ids, overlap=not args.no_overlap):
+        """One bench step (8 requests: 50 steps + 8 decodes). With overlap, the decodes go to the
+        low-priority stream after this batch's last UNet step, and the next batch's UNet steps start at
+        once on `st` (the latents buffer is double-buffered; a batch waits for the decodes of the batch two
+        back, which read the same buffer). `drain()` makes `st` wait for the outstanding decodes."""
+        b = pipe["k"] % 2
+        pipe["k"] += 1
+        lat = lats[b]
         with torch.cuda.stream(st):
+            if pipe["dec"][b] is not None:
+                st.wait_event(pipe["dec"][b])
             lat.copy_(z_d)                       # x_T = init_sigma (=1, DDIM) · z
             views = [lat[i] for i in range(N_REQ)]
             for s in range(nsteps):
                 eng.step(views, [s] * N_REQ, [nsteps] * N_REQ, [1] * N_REQ, [G] * N_REQ, slot_ids, stream=st)
+            if not overlap:
+                for i in range(N_REQ):
+                    eng.decode(lat[i], 1, image=imgs[i], stream=st)
+                pipe["dec"][b] = None
+                return
+            done = torch.cuda.Event()
+            done.record(st)
+        with torch.cuda.stream(vst):
+            vst.wait_event(done)
             for i in range(N_REQ):
-                eng.decode(lat[i], 1, image=imgs[i], stream=st)
+                eng.decode(lat[i], 1, image=imgs[i], stream=vst)
+            ev = torch.cuda.Event()
+            ev.record(vst)
+        pipe["dec"][b] = ev
+        pipe["last"] = ev
+
+    def drain():
+        if pipe["last"] is not None:
+            st.wait_event(pipe["last"])
 
     for _ in range(args.warmup):
         denoise_and_decode(slots)
@@ -294,6 +329,7 @@ def main():
         ev0.record(st)
         for _ in range(args.steps):
             denoise_and_decode(slots)
+        drain()  # the last batch's decodes are inside the timed region
         ev1.record(st)
         torch.cuda.synchronize()
         if args.profile_range:
@@ -308,7 +344,7 @@ def main():
     eng.profile(True)
     with torch.cuda.stream(st):
         for _ in range(args.steps):
-            denoise_and_decode(slots)
+            denoise_and_decode(slots, overlap=False)  # per-class times without co-running kernels
     torch.cuda.synchronize()
     prof = {c: eng.profile_read(c) for c in (0, 1, 2, 3, 4, 7)}
     eng.profile(False)
@@ -328,17 +364,29 @@ def main():
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
+        prev = None
         for _ in range(args.steps):
             with torch.cuda.stream(st):
                 emb_d.copy_(emb_h, non_blocking=True)
                 z_d.copy_(z_h, non_blocking=True)
             sl = [eng.register(emb_d[i], stream=st) for i in range(N_REQ)]
             denoise_and_decode(sl)
-            with torch.cuda.stream(st):
+            # the images of this batch leave once its decodes are done (on the decode stream when
+            # overlapped); the host waits for the previous batch only, so batches pipeline
+            dstream = st if args.no_overlap else vst
+            with torch.cuda.stream(dstream):
                 img_h.copy_(imgs, non_blocking=True)
-            st.synchronize()
+                out_ev = torch.cuda.Event()
+                out_ev.record(dstream)
+            st.synchronize()  # this batch's UNet steps (its text K/V slots are then free to reuse)
             for s_ in sl:
                 eng.release(s_)
+            if prev is not None:
+                prev.synchronize()
+            prev = out_ev
+        drain()
+        if prev is not None:
+            st.wait_event(prev)
         e1.record(st)
         torch.cuda.synchronize()
         te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
@@ -378,6 +426,7 @@ def main():
         a0.record(st)
         for _ in range(args.steps):
             denoise_and_decode(slots)
+        drain()
         a1.record(st)
         torch.cuda.synchronize()
         ta = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device=dev)

@@ -902,14 +902,20 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ part, int S, long
   if (i >= M * nq) return;
   const long m = i / nq;
   const int n = (int)(i % nq) * 4;
-  float4 acc = reinterpret_cast<const float4*>(part + m * N + n)[0];
-  for (int s = 1; s < S; ++s) {
-    const float4 v = reinterpret_cast<const float4*>(part + ((long)s * M + m) * N + n)[0];
-    acc.x += v.x;
-    acc.y += v.y;
-    acc.z += v.z;
-    acc.w += v.w;
-  }
+  // every split's 16-byte load issued before the first add (S ≤ 8), summed in split order
+  float4 v[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s)
+    if (s < S) v[s] = reinterpret_cast<const float4*>(part + ((long)s * M + m) * N + n)[0];
+  float4 acc = v[0];
+#pragma unroll
+  for (int s = 1; s < 8; ++s)
+    if (s < S) {
+      acc.x += v[s].x;
+      acc.y += v[s].y;
+      acc.z += v[s].z;
+      acc.w += v[s].w;
+    }
   float o[4] = {acc.x * alpha, acc.y * alpha, acc.z * alpha, acc.w * alpha};
   for (int k = 0; k < 4; ++k) {
     if (bias) o[k] += bias[n + k];
@@ -919,52 +925,6 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ part, int S, long
   }
   uint2 pk = make_uint2(pack16(o[0], o[1], is_f16), pack16(o[2], o[3], is_f16));
   *reinterpret_cast<uint2*>(out + m * ldo + col_off + n) = pk;
-}
-
-// the same reduction, 8 columns per thread with every split's loads issued before the first add (the
-// 4-column loop above kept one 16-byte load in flight per thread: latency-bound, ~3 TB/s); identical
-// summation order ((p0 + p1) + p2) …, so the results are bitwise those of the 4-column kernel
-__global__ void splitk_reduce8_kernel(const float* __restrict__ part, int S, long M, int N, const float* __restrict__ bias,
-                                      const float* __restrict__ temb, int ld_temb, int rows_per_img,
-                                      const bf16* __restrict__ res, int ldr, int act, float alpha,
-                                      bf16* __restrict__ out, int ldo, int col_off, int is_f16) {
-  pdl_wait();
-  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;  // one group of 8 columns
-  const int nq = N / 8;
-  if (i >= M * nq) return;
-  const long m = i / nq;
-  const int n = (int)(i % nq) * 8;
-  float4 v[8][2];
-#pragma unroll
-  for (int s = 0; s < 8; ++s)
-    if (s < S) {
-      const float4* p = reinterpret_cast<const float4*>(part + ((long)s * M + m) * N + n);
-      v[s][0] = __ldcs(p);
-      v[s][1] = __ldcs(p + 1);
-    }
-  float o[8] = {v[0][0].x, v[0][0].y, v[0][0].z, v[0][0].w, v[0][1].x, v[0][1].y, v[0][1].z, v[0][1].w};
-#pragma unroll
-  for (int s = 1; s < 8; ++s)
-    if (s < S) {
-      o[0] += v[s][0].x, o[1] += v[s][0].y, o[2] += v[s][0].z, o[3] += v[s][0].w;
-      o[4] += v[s][1].x, o[5] += v[s][1].y, o[6] += v[s][1].z, o[7] += v[s][1].w;
-    }
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    o[k] *= alpha;
-    if (bias) o[k] += bias[n + k];
-    if (temb) o[k] += temb[(m / rows_per_img) * ld_temb + n + k];
-    if (act == ACT_SILU) o[k] = silu_f(o[k]);
-  }
-  if (res) {
-    const uint4 r = *reinterpret_cast<const uint4*>(res + m * ldr + n);
-    const bf16* e = reinterpret_cast<const bf16*>(&r);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) o[k] += cvt16(e[k], is_f16);
-  }
-  *reinterpret_cast<uint4*>(out + m * ldo + col_off + n) =
-      make_uint4(pack16(o[0], o[1], is_f16), pack16(o[2], o[3], is_f16), pack16(o[4], o[5], is_f16),
-                 pack16(o[6], o[7], is_f16));
 }
 
 template <int BN, int CG, int MODE, int EPW>
@@ -1348,14 +1308,7 @@ void gemm(const GemmDesc& d, cudaStream_t st) {
     dispatch<GEMM_DENSE>(bn, cg, maps, a, st);
   else
     dispatch<GEMM_CONV3>(bn, cg, maps, a, st);
-  if (a.splits > 1 && a.splits <= 8 && d.N % 8 == 0 && d.ldo % 8 == 0 && d.col_off % 8 == 0 &&
-      (!d.res || d.ldr % 8 == 0)) {
-    const long n8 = (long)a.M * (d.N / 8);
-    launch_k(splitk_reduce8_kernel, (unsigned)cdiv(n8, 256), 256, 0, st, a.part, a.splits, a.M, d.N, d.bias, d.temb,
-             d.ld_temb, d.mode == GEMM_DENSE ? (d.rows_per_img > 0 ? d.rows_per_img : 1) : d.H * d.W, d.res, d.ldr,
-             d.act, d.alpha, reinterpret_cast<bf16*>(d.out), d.ldo, d.col_off, d.f16);
-    SD_CHECK_LAUNCH();
-  } else if (a.splits > 1) {
+  if (a.splits > 1) {
     const long n4 = (long)a.M * (d.N / 4);
     launch_k(splitk_reduce_kernel, (unsigned)cdiv(n4, 256), 256, 0, st, 
         a.part, a.splits, a.M, d.N, d.bias, d.temb, d.ld_temb,
