@@ -56,6 +56,10 @@ struct GemmArgs {
   // box sw × sh at (x, y): (y / sh) · (W / sw) + x / sw; of a dense quarter: (row mod gn_P) / 32.
   float2* gn_part;
   int gn_P, gn_slots, gn_sw, gn_sh;
+  // NH = 2 (BN = 320) tail balancing: work units u < full_units are whole tiles; the last tiles (one
+  // partial wave) are split into their two 160-column N-halves, units full_units + 2i + h → tile
+  // full_units + i, half h. The same N = 160 MMAs over the same K blocks either way: bitwise identical.
+  int full_units, total_units;
   const float2* ln_stat;  // folded LayerNorm (GemmDescT::ln_stat)
   const float* ln_wbar;
   int ln_cols;
@@ -86,6 +90,16 @@ __device__ __forceinline__ void ln_correct32(const GemmArgs& g, float* o, long p
       o[i] = st.y * fmaf(-st.x, wb, o[i]);
     }
   }
+}
+
+// work unit u → tile index and N-half selector (−1 = whole tile; 0 / 1 = that 160-column half)
+__device__ __forceinline__ int decode_unit(const GemmArgs& g, int u, int& hsel) {
+  if (u < g.full_units) {
+    hsel = -1;
+    return u;
+  }
+  hsel = (u - g.full_units) & 1;
+  return g.full_units + ((u - g.full_units) >> 1);
 }
 
 // tile t → (M tile, N tile, K-block range); tiles of split s follow those of split s-1
@@ -636,7 +650,7 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
   const uint32_t tmem_base = *tmem_slot;
   pdl_wait();  // barrier init, TMEM alloc and descriptor prefetch above overlapped the previous grid (PDL)
 
-  const int total = g.m_tiles * g.n_tiles * g.splits;
+  const int total = g.total_units;
   const int worker = blockIdx.x / CG, nworkers = gridDim.x / CG;
 
   if (warp == 0) {
@@ -644,7 +658,9 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
       // ================= TMA producer (both CTAs of a pair load their halves) =================
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = worker; t < total; t += nworkers) {
+      for (int u = worker; u < total; u += nworkers) {
+        int hsel;
+        const int t = decode_unit(g, u, hsel);
         int mt, nt, sp, kb0, kb1;
         decode_tile(g, t, mt, nt, sp, kb0, kb1);
         const int mbox = mt * CG + (int)rank;  // this CTA's 128-row box
@@ -666,7 +682,8 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
           // experiment switches (SD_EPI_DBG; results are garbage): 5 = B loaded only for a tile's first K
           // block, 6 = A only for the first — how much of the time the operand feed of each costs
           const bool skipB = g.dbg == 5 && kb != kb0, skipA = g.dbg == 6 && kb != kb0;
-          const int bytes = C::STAGE - (skipB ? C::B_BYTES : 0) - (skipA ? C::A_BYTES : 0);
+          const int bytes = C::STAGE - (skipB ? C::B_BYTES : 0) - (skipA ? C::A_BYTES : 0) -
+                            (hsel >= 0 && !skipB ? C::B_BYTES / 2 : 0);  // a half unit loads one N-half of B
           if (CG == 1) {
             mbar_expect_tx(&full[stage], bytes);
           } else {
@@ -698,7 +715,8 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
             } else {  // this CTA's slice of each N-half: rows nt·BN + h·MMA_N + rank·MMA_N/CG
 #pragma unroll
               for (int h = 0; h < C::NH; ++h)
-                tma3<CG>(static_cast<uint8_t*>(dB) + h * (C::B_ROWS / C::NH) * 128, mb, &full[stage], bar_l,
+                if (hsel < 0 || h == hsel)
+                  tma3<CG>(static_cast<uint8_t*>(dB) + h * (C::B_ROWS / C::NH) * 128, mb, &full[stage], bar_l,
                          cb * C::BK, tap, nt * BN + h * C::MMA_N + (int)rank * (C::MMA_N / CG));
             }
           }
@@ -715,20 +733,26 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
       const uint32_t idesc = make_idesc16(128 * CG, C::MMA_N, F16);
       int stage = 0;
       uint32_t phase = 0;
-      int it = 0;
-      for (int t = worker; t < total; t += nworkers, ++it) {
+      int it = 0, jh = 0;
+      for (int u = worker; u < total; u += nworkers, ++it) {
+        int hsel;
+        const int t = decode_unit(g, u, hsel);
         const int acc = C::NACC == 2 ? (it & 1) : 0;
         const uint32_t acc_phase = C::NACC == 2 ? ((it >> 1) & 1) : (it & 1);
-        // NH = 2 (BN = 320): the two 160-column halves of tile `it` are global halves j = 2·it + h, in
-        // rotating buffers j mod 3 of 160 TMEM columns (480 of 512): the next tile's MMAs start as soon as
-        // this tile's first half is drained, instead of after its whole epilogue
-        uint32_t dh[2];
+        // NH = 2 (BN = 320): each 160-column half computed takes the next global half index j (jh, jh + 1,
+        // …), in rotating buffers j mod 3 of 160 TMEM columns (480 of 512): the next tile's MMAs start as
+        // soon as this tile's first half is drained, instead of after its whole epilogue. A half unit
+        // (tail balancing) computes only its half h = hsel.
+        uint32_t dh[2] = {0u, 0u};
+        int jb[2] = {0, 0};
         if constexpr (C::NH == 2) {
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const int j = 2 * it + h, b = j % 3;
+            if (hsel >= 0 && h != hsel) continue;
+            const int j = jh++, b = j % 3;
             mbar_wait(&tempty[b], ((j / 3) & 1) ^ 1);
             dh[h] = tmem_base + b * C::MMA_N;
+            jb[h] = b;
           }
         } else {
           mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -747,9 +771,10 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
           for (int k = 0; k < C::BK / 16; ++k)
 #pragma unroll
             for (int h = 0; h < C::NH; ++h)  // N-half h: B rows [h·B_ROWS/NH, …) of every CTA, TMEM cols h·MMA_N
-              mma<CG>(dh[h], make_sdesc_sw128(a0 + k * 32),
-                      make_sdesc_sw128(b0 + h * (C::B_ROWS / C::NH) * 128 + k * 32), idesc,
-                      (kb != kb0 || k != 0) ? 1u : 0u);
+              if (hsel < 0 || h == hsel)
+                mma<CG>(dh[h], make_sdesc_sw128(a0 + k * 32),
+                        make_sdesc_sw128(b0 + h * (C::B_ROWS / C::NH) * 128 + k * 32), idesc,
+                        (kb != kb0 || k != 0) ? 1u : 0u);
           commit<CG>(&empty[stage]);
           if (++stage == C::STAGES) {
             stage = 0;
@@ -757,8 +782,9 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
           }
         }
         if constexpr (C::NH == 2) {
-          commit<CG>(&tfull[(2 * it) % 3]);
-          commit<CG>(&tfull[(2 * it + 1) % 3]);
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            if (hsel < 0 || h == hsel) commit<CG>(&tfull[jb[h]]);
         } else {
           commit<CG>(&tfull[acc]);
         }
@@ -770,8 +796,10 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
     // the 32-column chunks, so the epilogue keeps up with short-K tiles) =====
     const int q = warp & 3;
     EpiCtx ec{sStage + (warp - 2) * 4096, 0, 0, 0, 0, rbar + (warp - 2) * 2, 0u};
-    int it = 0;
-    for (int t = worker; t < total; t += nworkers, ++it) {
+    int it = 0, jh = 0;
+    for (int u = worker; u < total; u += nworkers, ++it) {
+      int hsel;
+      const int t = decode_unit(g, u, hsel);
       const int acc = C::NACC == 2 ? (it & 1) : 0;
       const uint32_t acc_phase = C::NACC == 2 ? ((it >> 1) & 1) : (it & 1);
       int mt, nt, sp, kb0, kb1;
@@ -794,7 +822,8 @@ __global__ void __launch_bounds__(64 + 32 * EPW, 1)
         // the next tile's MMAs start)
 #pragma unroll 1
         for (int h = 0; h < 2; ++h) {
-          const int j = 2 * it + h, b = j % 3;
+          if (hsel >= 0 && h != hsel) continue;  // a half unit drains only its half
+          const int j = jh++, b = j % 3;
           epilogue_tile<BN, MODE, F16, EPW / 4>(g, &tout, &tres, ec, tmem_base + lq + b * C::MMA_N, mt * CG + (int)rank,
                                                 nt * BN, q, lane, (warp - 2) >> 2, sp, &tfull[b], (j / 3) & 1,
                                                 h * (BN / 64), (h + 1) * (BN / 64));
@@ -938,10 +967,27 @@ static void launch(const CUtensorMap* m, const GemmArgs& a, cudaStream_t st) {
                                  C::SMEM));
     attr_set = true;
   }
-  const int total = a.m_tiles * a.n_tiles * a.splits;
+  const int tiles = a.m_tiles * a.n_tiles * a.splits;
   int workers = stream_sms(st) / CG;
-  if (total < workers) workers = total;
+  if (tiles < workers) workers = tiles;
   if (workers <= 0) return;
+  // NH = 2 tail balancing: a last partial wave of ≤ workers/2 tiles runs as 2× as many half-tile units
+  // (SD_TAIL_HALVES=0 disables); results are bitwise the same
+  GemmArgs b = a;
+  b.full_units = tiles;
+  b.total_units = tiles;
+  {
+    static int th = -1;
+    if (th < 0) {
+      const char* e = getenv("SD_TAIL_HALVES");
+      th = !(e && e[0] == '0');
+    }
+    const int tail = tiles % workers;
+    if (C::NH == 2 && th && a.splits == 1 && tiles > workers && tail > 0 && 2 * tail <= workers) {
+      b.full_units = tiles - tail;
+      b.total_units = b.full_units + 2 * tail;
+    }
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(workers * CG);
   cfg.blockDim = dim3(64 + 32 * EPW);
@@ -957,9 +1003,9 @@ static void launch(const CUtensorMap* m, const GemmArgs& a, cudaStream_t st) {
   cfg.attrs = attr;
   cfg.numAttrs = g_pdl ? 2 : 1;
   if (a.f16)
-    SD_CUDA(cudaLaunchKernelEx(&cfg, gemm_kernel<BN, CG, MODE, true, EPW>, m[0], m[1], m[2], m[3], m[4], m[5], a));
+    SD_CUDA(cudaLaunchKernelEx(&cfg, gemm_kernel<BN, CG, MODE, true, EPW>, m[0], m[1], m[2], m[3], m[4], m[5], b));
   else
-    SD_CUDA(cudaLaunchKernelEx(&cfg, gemm_kernel<BN, CG, MODE, false, EPW>, m[0], m[1], m[2], m[3], m[4], m[5], a));
+    SD_CUDA(cudaLaunchKernelEx(&cfg, gemm_kernel<BN, CG, MODE, false, EPW>, m[0], m[1], m[2], m[3], m[4], m[5], b));
   SD_CHECK_LAUNCH();
 }
 

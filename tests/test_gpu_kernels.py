@@ -464,3 +464,27 @@ def test_gemm_layernorm_folded(T, N, K, cols, act):
            None)
     torch.cuda.synchronize()
     assert rel(D.cpu(), ref) < 8e-3
+
+
+def test_conv_bn320_tail_halves_bitwise():
+    """BN = 320 pair tiles with tail balancing (the last partial wave split into 160-column half units): 16
+    images at 64×64 → 256 pair tiles on 74 pairs, 34 tail tiles run as 68 halves; 8 images → 128 tiles,
+    no halving. The first 8 images must agree bit for bit (same N = 160 MMAs over the same K blocks), and
+    both must match fp64."""
+    g = torch.Generator().manual_seed(320)
+    nb, h, w, cin, cout = 16, 64, 64, 320, 320
+    x = bf(torch.randn(nb, h, w, cin, generator=g))
+    wt = bf(torch.randn(cout, cin, 3, 3, generator=g) / (9 * cin) ** 0.5)
+    b = torch.randn(cout, generator=g)
+    xd, wd, bd = x.cuda(), _to_dev_w(wt), b.cuda()
+
+    def run(n):
+        y = torch.empty(n, h, w, cout, device="cuda", dtype=DT)
+        B.debug_conv3x3(xd[:n], cin, None, 0, wd, None, bd, None, None, y, n, h, w, cout)
+        torch.cuda.synchronize()
+        return y.cpu()
+
+    y16, y8 = run(16), run(8)
+    assert torch.equal(y16[:8], y8)
+    ref = _conv_ref(x[:2].float(), wt.float(), b, None, None)
+    assert rel(y16[:2], ref) < 6e-3
