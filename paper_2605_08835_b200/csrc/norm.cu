@@ -404,6 +404,108 @@ __global__ void __launch_bounds__(512, 2) gn_apply_kernel(const T* __restrict__ 
   gn_apply_dev(x, x1, V0, p_begin, p_end, P, V, tab, silu, y);
 }
 
+// TMA-staged apply (single source): the pixel rows [p_begin, p_end) of x are contiguous, so a block moves
+// whole chunks of CP rows × C channels with one bulk copy each (cp.async.bulk, mbarrier completion) into a
+// 2-deep shared-memory ring, its threads normalise the chunk in place, and one bulk copy stores it back —
+// the memory pipeline no longer depends on how many loads each thread keeps in flight (the register-bound
+// apply held 4 × 16 B per thread). Thread t keeps channel vector t mod V (its 8 table entries in registers);
+// arithmetic identical to gn_apply_dev, so the results are bitwise the same.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+
+template <class T>
+__global__ void __launch_bounds__(512) gn_apply_bulk_kernel(const T* __restrict__ x, const T* __restrict__ x1, int V0,
+                                                           long p_begin, long p_end, int P, int V, int CP,
+                                                           const float2* __restrict__ tab, int silu,
+                                                           T* __restrict__ y) {
+  // stage layout: [in0: CP × C0][in1: CP × C1 (two sources)][out: CP × C (two sources; else in place)]
+  extern __shared__ __align__(128) uint8_t gsm[];
+  const int nt = blockDim.x, tid = threadIdx.x;
+  const int C = V * 8, C0 = (x1 ? V0 : V) * 8, C1 = C - C0;
+  const long in0_b = (long)CP * C0 * sizeof(T), in1_b = (long)CP * C1 * sizeof(T);
+  const long stage_b = in0_b + in1_b + (x1 ? (long)CP * C * sizeof(T) : 0);
+  uint64_t* full = reinterpret_cast<uint64_t*>(gsm + 2 * stage_b);
+  const long npix = p_end - p_begin;
+  const int nchunks = (int)((npix + CP - 1) / CP);
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  pdl_wait();
+  auto in0 = [&](int st_) { return reinterpret_cast<T*>(gsm + st_ * stage_b); };
+  auto in1 = [&](int st_) { return reinterpret_cast<T*>(gsm + st_ * stage_b + in0_b); };
+  auto outb = [&](int st_) { return x1 ? reinterpret_cast<T*>(gsm + st_ * stage_b + in0_b + in1_b) : in0(st_); };
+  auto issue = [&](int c, int s) {
+    const long q0 = p_begin + (long)c * CP;
+    const int n = (int)min((long)CP, p_end - q0);
+    mbar_expect_tx(&full[s], (uint32_t)(n * C * sizeof(T)));
+    bulk_g2s(in0(s), x + q0 * C0, (uint32_t)(n * C0 * sizeof(T)), &full[s]);
+    if (x1) bulk_g2s(in1(s), x1 + q0 * C1, (uint32_t)(n * C1 * sizeof(T)), &full[s]);
+  };
+  if (tid == 0) {
+    if ((int)blockIdx.x < nchunks) issue(blockIdx.x, 0);
+    if ((int)(blockIdx.x + gridDim.x) < nchunks) issue(blockIdx.x + gridDim.x, 1);
+  }
+  const int v = tid % V, r0 = tid / V, rstep = nt / V;  // nt is a multiple of V
+  const bool second = x1 && v >= V0;
+  int b_cur = -1;
+  float sc[8], sf[8];
+  int it = 0;
+  for (int c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
+    const int s = it & 1;
+    mbar_wait(&full[s], (it >> 1) & 1);
+    const long q0 = p_begin + (long)c * CP;
+    const int n = (int)min((long)CP, p_end - q0);
+    const T* src = second ? in1(s) + (v - V0) * 8 : in0(s) + v * 8;
+    const int lds = second ? C1 : C0;
+    T* dst = outb(s) + v * 8;
+    for (int r = r0; r < n; r += rstep) {
+      const long p = q0 + r;
+      const int b = (int)((unsigned)p / (unsigned)P);
+      if (b != b_cur) {
+        const float4* t4 = reinterpret_cast<const float4*>(tab + ((long)b * V + v) * 8);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float4 t = __ldg(t4 + j);
+          sc[2 * j] = t.x, sf[2 * j] = t.y, sc[2 * j + 1] = t.z, sf[2 * j + 1] = t.w;
+        }
+        b_cur = b;
+      }
+      float f[8], o[8];
+      load8(src + (long)r * lds, f);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float a = f[j] * sc[j] + sf[j];
+        o[j] = silu == 2 ? silu_tanh(a) : silu ? silu_f(a) : a;
+      }
+      store8(dst + (long)r * C, o);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes → the bulk store
+    __syncthreads();
+    if (tid == 0) {
+      bulk_s2g(y + q0 * C, outb(s), (uint32_t)(n * C * sizeof(T)));
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      const int cn = c + 2 * gridDim.x;
+      if (cn < nchunks) {
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // the store has read stage s
+        issue(cn, s);
+      }
+    }
+  }
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // GroupNorm in ONE cooperative launch (the whole-tensor path, group_norm / group_norm2): the three
 // phases of the three-kernel path, separated by grid-wide barriers instead of kernel boundaries —
 //   1. partials of every (image, chunk) item, block-strided (gn_stats_item),
@@ -533,11 +635,55 @@ static void gn_fused(const T* x, const T* x1, int C0, T* y, int B, int P, int C,
   SD_CHECK_LAUNCH();
 }
 
+// SD_GN_BULK=0: the register-pipelined apply for single-source tensors too
+static bool gn_bulk_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SD_GN_BULK");
+    v = !(e && e[0] == '0');
+  }
+  return v != 0;
+}
+
 template <class T>
 static void gn_apply(const T* x, const T* x1, int C0, T* y, long p0, long p1, int B, int P, int C, const float2* tab,
                      bool silu, cudaStream_t st) {
   if (p1 <= p0) return;
   if (p1 >= (1L << 31)) throw CudaError("group_norm: tensor too large");
+  if (gn_bulk_on() && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) |
+                        reinterpret_cast<uintptr_t>(x1)) & 15) == 0) {
+    const int V = C / 8;
+    const int k = std::max(1, 256 / V);        // pixel rows per pass; threads = V·k (≤ 512)
+    const int nt = V * k;
+    const long row_bytes = (long)C * sizeof(T) * (x1 ? 2 : 1);  // two sources: in0 | in1 | out per row
+    int CP = (int)std::max<long>(k, (24L * 1024 / row_bytes) / k * k);  // ~24 KB stages, whole passes
+    const size_t smem = 2 * (size_t)CP * row_bytes + 64;
+    static std::mutex mu;
+    static std::map<std::pair<int, size_t>, int> occ;
+    int per_sm;
+    {
+      std::lock_guard<std::mutex> g(mu);
+      auto key = std::make_pair(nt, smem);
+      auto it = occ.find(key);
+      if (it == occ.end()) {
+        if (smem > 48 * 1024)
+          SD_CUDA(cudaFuncSetAttribute(gn_apply_bulk_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int n = 0;
+        SD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, gn_apply_bulk_kernel<T>, nt, smem));
+        it = occ.emplace(key, std::max(n, 1)).first;
+      }
+      per_sm = it->second;
+    }
+    static int sms = 0;
+    if (!sms) SD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    const long nchunks = (p1 - p0 + CP - 1) / CP;
+    const int grid = (int)std::min<long>(nchunks, (long)sms * per_sm);
+    launch_k(gn_apply_bulk_kernel<T>, grid, nt, smem, st, x, x1, C0 / 8, p0, p1, P, V, CP, tab, gn_silu_mode<T>(silu),
+             y);
+    SD_CHECK_LAUNCH();
+    (void)B;
+    return;
+  }
   const dim3 blk = gn_stats_block(C);
   const long rows = (long)blk.y * 4;
   static int sms = 0;
@@ -711,9 +857,144 @@ __global__ void layer_norm_kernel(const E* __restrict__ x, int T, int C, const f
   }
 }
 
+// TMA-staged LayerNorm (the GroupNorm apply's pattern): ~24 KB chunks of whole tokens arrive by one bulk
+// copy each in a 2-deep shared-memory ring, LANES lanes per token normalise them in place with the same
+// two-pass register arithmetic as layer_norm_kernel (bitwise the same), one bulk copy stores each chunk.
+template <int NV, int LANES, class E>
+__global__ void __launch_bounds__(256) layer_norm_bulk_kernel(const E* __restrict__ x, int T, int C, int TK,
+                                                             const float* __restrict__ gamma,
+                                                             const float* __restrict__ beta, float eps,
+                                                             E* __restrict__ y) {
+  extern __shared__ __align__(128) uint8_t lsm[];
+  const long stage_b = (long)TK * C * sizeof(E);
+  uint64_t* full = reinterpret_cast<uint64_t*>(lsm + 2 * stage_b);
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int nchunks = (T + TK - 1) / TK;
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  pdl_wait();
+  auto sbuf = [&](int st_) { return reinterpret_cast<E*>(lsm + st_ * stage_b); };
+  auto issue = [&](int c, int s) {
+    const int t0 = c * TK, n = min(TK, T - t0);
+    mbar_expect_tx(&full[s], (uint32_t)((long)n * C * sizeof(E)));
+    bulk_g2s(sbuf(s), x + (long)t0 * C, (uint32_t)((long)n * C * sizeof(E)), &full[s]);
+  };
+  if (tid == 0) {
+    if ((int)blockIdx.x < nchunks) issue(blockIdx.x, 0);
+    if ((int)(blockIdx.x + gridDim.x) < nchunks) issue(blockIdx.x + gridDim.x, 1);
+  }
+  const int V = C / 8, l = tid % LANES, tl = tid / LANES, tstep = nt / LANES;
+  int it = 0;
+  for (int c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
+    const int s = it & 1;
+    mbar_wait(&full[s], (it >> 1) & 1);
+    const int t0 = c * TK, n = min(TK, T - t0);
+    E* sb = sbuf(s);
+    for (int tk = tl; tk < n; tk += tstep) {
+      E* xr = sb + (long)tk * C;
+      float f[NV][8];
+      float sum = 0.f;
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        const int vi = l + LANES * k;
+        if (vi < V) {
+          load8(xr + vi * 8, f[k]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) f[k][i] = 0.f;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < NV; ++k)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) sum += f[k][i];
+#pragma unroll
+      for (int o = LANES / 2; o; o >>= 1) sum += __shfl_xor_sync(0xffffffff, sum, o);
+      const float mean = sum / C;
+      float q = 0.f;
+#pragma unroll
+      for (int k = 0; k < NV; ++k)
+        if (l + LANES * k < V)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float d = f[k][i] - mean;
+            q += d * d;
+          }
+#pragma unroll
+      for (int o = LANES / 2; o; o >>= 1) q += __shfl_xor_sync(0xffffffff, q, o);
+      const float rstd = rsqrtf(q / C + eps);
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        const int vi = l + LANES * k;
+        if (vi < V) {
+          const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + vi * 8));
+          const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + vi * 8 + 4));
+          const float4 b0 = __ldg(reinterpret_cast<const float4*>(beta + vi * 8));
+          const float4 b1 = __ldg(reinterpret_cast<const float4*>(beta + vi * 8 + 4));
+          const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+          const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+          float o[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) o[i] = (f[k][i] - mean) * rstd * gg[i] + bb[i];
+          store8(xr + vi * 8, o);
+        }
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      bulk_s2g(y + (long)t0 * C, sb, (uint32_t)((long)n * C * sizeof(E)));
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      const int cn = c + 2 * gridDim.x;
+      if (cn < nchunks) {
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        issue(cn, s);
+      }
+    }
+  }
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// SD_LN_BULK=1: the TMA-staged LayerNorm (off until measured)
+static bool ln_bulk_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SD_LN_BULK");
+    v = e && e[0] == '1';
+  }
+  return v != 0;
+}
+
 template <int NV, int LANES, class E>
 static void ln_launch(const E* x, E* y, int T, int C, const float* g, const float* b, float eps,
                       cudaStream_t st) {
+  if (ln_bulk_on() && NV * LANES * 8 >= C && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0) {
+    const int tpp = 256 / LANES;  // tokens per pass
+    const long row_b = (long)C * sizeof(E);
+    const int TK = (int)std::max<long>(tpp, (24L * 1024 / row_b) / tpp * tpp);
+    const size_t smem = 2 * (size_t)TK * row_b + 64;
+    static int per_sm = 0;
+    static size_t smem_set = 0;
+    if (smem_set != smem) {  // a function of (NV, LANES, E, C): C is fixed per instantiation in practice
+      if (smem > 48 * 1024)
+        SD_CUDA(cudaFuncSetAttribute(layer_norm_bulk_kernel<NV, LANES, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+      SD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, layer_norm_bulk_kernel<NV, LANES, E>, 256, smem));
+      per_sm = std::max(per_sm, 1);
+      smem_set = smem;
+    }
+    static int sms = 0;
+    if (!sms) SD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    const int nch = (T + TK - 1) / TK;
+    const int grid = std::min(nch, sms * per_sm);
+    launch_k(layer_norm_bulk_kernel<NV, LANES, E>, grid, 256, smem, st, x, T, C, TK, g, b, eps, y);
+    SD_CHECK_LAUNCH();
+    return;
+  }
   const int threads = 256;
   const long total = (long)T * LANES;
   launch_k(layer_norm_kernel<NV, LANES, E>, cdiv(total, threads), threads, 0, st, x, T, C, g, b, eps, y);
