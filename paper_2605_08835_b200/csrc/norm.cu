@@ -857,144 +857,9 @@ __global__ void layer_norm_kernel(const E* __restrict__ x, int T, int C, const f
   }
 }
 
-// TMA-staged LayerNorm (the GroupNorm apply's pattern): ~24 KB chunks of whole tokens arrive by one bulk
-// copy each in a 2-deep shared-memory ring, LANES lanes per token normalise them in place with the same
-// two-pass register arithmetic as layer_norm_kernel (bitwise the same), one bulk copy stores each chunk.
-template <int NV, int LANES, class E>
-__global__ void __launch_bounds__(256) layer_norm_bulk_kernel(const E* __restrict__ x, int T, int C, int TK,
-                                                             const float* __restrict__ gamma,
-                                                             const float* __restrict__ beta, float eps,
-                                                             E* __restrict__ y) {
-  extern __shared__ __align__(128) uint8_t lsm[];
-  const long stage_b = (long)TK * C * sizeof(E);
-  uint64_t* full = reinterpret_cast<uint64_t*>(lsm + 2 * stage_b);
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int nchunks = (T + TK - 1) / TK;
-  if (tid == 0) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  pdl_wait();
-  auto sbuf = [&](int st_) { return reinterpret_cast<E*>(lsm + st_ * stage_b); };
-  auto issue = [&](int c, int s) {
-    const int t0 = c * TK, n = min(TK, T - t0);
-    mbar_expect_tx(&full[s], (uint32_t)((long)n * C * sizeof(E)));
-    bulk_g2s(sbuf(s), x + (long)t0 * C, (uint32_t)((long)n * C * sizeof(E)), &full[s]);
-  };
-  if (tid == 0) {
-    if ((int)blockIdx.x < nchunks) issue(blockIdx.x, 0);
-    if ((int)(blockIdx.x + gridDim.x) < nchunks) issue(blockIdx.x + gridDim.x, 1);
-  }
-  const int V = C / 8, l = tid % LANES, tl = tid / LANES, tstep = nt / LANES;
-  int it = 0;
-  for (int c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
-    const int s = it & 1;
-    mbar_wait(&full[s], (it >> 1) & 1);
-    const int t0 = c * TK, n = min(TK, T - t0);
-    E* sb = sbuf(s);
-    for (int tk = tl; tk < n; tk += tstep) {
-      E* xr = sb + (long)tk * C;
-      float f[NV][8];
-      float sum = 0.f;
-#pragma unroll
-      for (int k = 0; k < NV; ++k) {
-        const int vi = l + LANES * k;
-        if (vi < V) {
-          load8(xr + vi * 8, f[k]);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) f[k][i] = 0.f;
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < NV; ++k)
-#pragma unroll
-        for (int i = 0; i < 8; ++i) sum += f[k][i];
-#pragma unroll
-      for (int o = LANES / 2; o; o >>= 1) sum += __shfl_xor_sync(0xffffffff, sum, o);
-      const float mean = sum / C;
-      float q = 0.f;
-#pragma unroll
-      for (int k = 0; k < NV; ++k)
-        if (l + LANES * k < V)
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float d = f[k][i] - mean;
-            q += d * d;
-          }
-#pragma unroll
-      for (int o = LANES / 2; o; o >>= 1) q += __shfl_xor_sync(0xffffffff, q, o);
-      const float rstd = rsqrtf(q / C + eps);
-#pragma unroll
-      for (int k = 0; k < NV; ++k) {
-        const int vi = l + LANES * k;
-        if (vi < V) {
-          const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + vi * 8));
-          const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + vi * 8 + 4));
-          const float4 b0 = __ldg(reinterpret_cast<const float4*>(beta + vi * 8));
-          const float4 b1 = __ldg(reinterpret_cast<const float4*>(beta + vi * 8 + 4));
-          const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-          const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-          float o[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) o[i] = (f[k][i] - mean) * rstd * gg[i] + bb[i];
-          store8(xr + vi * 8, o);
-        }
-      }
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-    if (tid == 0) {
-      bulk_s2g(y + (long)t0 * C, sb, (uint32_t)((long)n * C * sizeof(E)));
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      const int cn = c + 2 * gridDim.x;
-      if (cn < nchunks) {
-        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        issue(cn, s);
-      }
-    }
-  }
-  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-}
-
-// SD_LN_BULK=1: the TMA-staged LayerNorm (off until measured)
-static bool ln_bulk_on() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("SD_LN_BULK");
-    v = e && e[0] == '1';
-  }
-  return v != 0;
-}
-
 template <int NV, int LANES, class E>
 static void ln_launch(const E* x, E* y, int T, int C, const float* g, const float* b, float eps,
                       cudaStream_t st) {
-  if (ln_bulk_on() && NV * LANES * 8 >= C && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0) {
-    const int tpp = 256 / LANES;  // tokens per pass
-    const long row_b = (long)C * sizeof(E);
-    const int TK = (int)std::max<long>(tpp, (24L * 1024 / row_b) / tpp * tpp);
-    const size_t smem = 2 * (size_t)TK * row_b + 64;
-    static int per_sm = 0;
-    static size_t smem_set = 0;
-    if (smem_set != smem) {  // a function of (NV, LANES, E, C): C is fixed per instantiation in practice
-      if (smem > 48 * 1024)
-        SD_CUDA(cudaFuncSetAttribute(layer_norm_bulk_kernel<NV, LANES, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-      SD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, layer_norm_bulk_kernel<NV, LANES, E>, 256, smem));
-      per_sm = std::max(per_sm, 1);
-      smem_set = smem;
-    }
-    static int sms = 0;
-    if (!sms) SD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-    const int nch = (T + TK - 1) / TK;
-    const int grid = std::min(nch, sms * per_sm);
-    launch_k(layer_norm_bulk_kernel<NV, LANES, E>, grid, 256, smem, st, x, T, C, TK, g, b, eps, y);
-    SD_CHECK_LAUNCH();
-    return;
-  }
   const int threads = 256;
   const long total = (long)T * LANES;
   launch_k(layer_norm_kernel<NV, LANES, E>, cdiv(total, threads), threads, 0, st, x, T, C, g, b, eps, y);
