@@ -656,7 +656,12 @@ static void gn_apply(const T* x, const T* x1, int C0, T* y, long p0, long p1, in
     const int k = std::max(1, 256 / V);        // pixel rows per pass; threads = V·k (≤ 512)
     const int nt = V * k;
     const long row_bytes = (long)C * sizeof(T) * (x1 ? 2 : 1);  // two sources: in0 | in1 | out per row
-    int CP = (int)std::max<long>(k, (24L * 1024 / row_bytes) / k * k);  // ~24 KB stages, whole passes
+    static long stage_kb = -1;  // SD_GN_CHUNK_KB: stage size (experiments)
+    if (stage_kb < 0) {
+      const char* e = getenv("SD_GN_CHUNK_KB");
+      stage_kb = e ? std::max(4, atoi(e)) : 24;
+    }
+    int CP = (int)std::max<long>(k, (stage_kb * 1024 / row_bytes) / k * k);  // ~24 KB stages, whole passes
     const size_t smem = 2 * (size_t)CP * row_bytes + 64;
     static std::mutex mu;
     static std::map<std::pair<int, size_t>, int> occ;
